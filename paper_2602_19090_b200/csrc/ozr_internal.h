@@ -1,0 +1,45 @@
+// ozr_internal.h — internal (non-ABI) declarations shared by the ozr CUDA sources.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace ozr {
+
+constexpr int kMaxPairs = 256;   // digit pairs per product
+constexpr int kMaxGroups = 96;   // int32 accumulation groups (output planes) per product
+
+// A product C = Σ_groups Σ_{(s,t) in group} D^A_s · D^B_t is described by a pair table.
+// Group g accumulates pairs [first[g], first[g+1]) into ONE int32 plane out_plane[g].
+// s/t are 0-based digit-plane indices of the A / B operand.
+struct PairTable {
+  int ngroups;
+  int first[kMaxGroups + 1];
+  int out_plane[kMaxGroups];
+  int diag[kMaxGroups];  // s+t (1-based digits) of the group: its weight 256^{-diag}
+  unsigned char s[kMaxPairs];
+  unsigned char t[kMaxPairs];
+};
+
+// Digit-plane operand: planes of int8, "column-major" i.e. plane[p][col][row] with row contiguous.
+// For a GEMM operand the contiguous index is K (K-major); `rows` = K extent, `cols` = M or N extent.
+struct DigitOperand {
+  const int8_t* base;
+  int64_t ld;            // bytes between consecutive columns (>= rows, multiple of 16)
+  int64_t plane_stride;  // bytes between planes (multiple of 16)
+  int nplanes;
+};
+
+// Launch the tcgen05 INT8 slice-product kernel: for each group g, out_planes[out_plane[g]] (M x N int32,
+// column-major, leading dim ldo) = Σ_{pairs} A_s^T-tile products over K.
+//   A: M "columns" of K bytes each (A operand, K-major), B: N columns of K bytes (B operand, K-major).
+cudaError_t launch_gemm_i8(const DigitOperand& A, const DigitOperand& B, int M, int N, int K,
+                           const PairTable& pt, int32_t* out, int64_t out_plane_stride, int64_t ldo,
+                           cudaStream_t stream);
+
+// Reference (SIMT) version of the same contract; used only by the dev harness to cross-check the
+// tensor-core kernel on the GPU. Not on the product path.
+cudaError_t launch_gemm_i8_simt(const DigitOperand& A, const DigitOperand& B, int M, int N, int K,
+                                const PairTable& pt, int32_t* out, int64_t out_plane_stride, int64_t ldo,
+                                cudaStream_t stream);
+
+}  // namespace ozr
