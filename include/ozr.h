@@ -1,0 +1,158 @@
+/* ozr.h — C ABI of libozr: forward-error-oriented Ogita–Aishima eigenvector refinement with an
+ * INT8 Ozaki-scheme accurate product, native to NVIDIA B200 (sm_100a).
+ *
+ * Method: Terao & Ozaki, arXiv 2602.19090 (reference text: PAPER.md). Citations are PAPER.md lines.
+ *   Problem: symmetric A, approximate eigenvectors X̂ (and D̂); return a
+ *             refined X̂ with ‖X − X̂‖₂ ≈ δ and the Rayleigh-quotient eigenvalues D̂.
+ *   Sweep     (Algorithm 1) with the one-sided accurate product (§3.1/§3.3,
+ *             PAPER.md:308-317, 400-421) and the tuned β of §4.1.
+ *   Splitting (§2.3, eq. sigma/tau/a/x) realised as INT8 digit planes
+ *             (readings R4-R7).
+ *
+ * Conventions (all entry points):
+ *   - Matrix pointers are DEVICE pointers to column-major storage with the given leading dimension
+ *     (in elements). Vectors (lambda, exponents) are device pointers unless marked "host".
+ *   - The caller owns every buffer passed in; the library owns only the workspace inside the context
+ *     (allocated lazily and grown on demand, freed by ozr_destroy).
+ *   - Work is issued on the context's stream. ozr_split and ozr_gemm are stream-ordered and do not
+ *     synchronise; ozr_refine_step / ozr_refine_to_tol synchronise a few times per sweep to read
+ *     scalars that choose digit budgets, and return with all work complete.
+ *   - Errors never cross the ABI as exceptions: every call returns an ozr_status; the text of the last
+ *     error is available from ozr_last_error(ctx). On error, outputs are unspecified and inputs are
+ *     untouched, except OZR_ERR_NOT_CONVERGED (see ozr_refine_to_tol).
+ *   - Results are deterministic (fixed reduction orders, integer accumulation, no FP atomics).
+ *   - A context is not thread-safe; use one per host thread and device.
+ */
+#ifndef OZR_H_
+#define OZR_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct ozr_ctx_s* ozr_ctx;
+
+typedef enum {
+  OZR_OK = 0,
+  OZR_ERR_ARG = 1,           /* bad argument: null pointer, bad size/stride/leading dimension, bad mode */
+  OZR_ERR_NONFINITE = 2,     /* NaN or Inf in an input matrix */
+  OZR_ERR_RANGE = 3,         /* δ ≤ u, digit count out of range, or an exponent/int range limit exceeded */
+  OZR_ERR_DEGENERATE = 4,    /* r_j ≥ 1 (zero column), or equal eigenvalue estimates with the cluster
+                                branch disabled (PAPER.md:333 assumes distinct eigenvalues) */
+  OZR_ERR_NOT_CONVERGED = 5, /* stagnation / divergence; X and lambda hold the last accepted sweep */
+  OZR_ERR_CUDA = 6,          /* CUDA runtime error (message in ozr_last_error) */
+  OZR_ERR_NOMEM = 8          /* device allocation failed */
+} ozr_status;
+
+/* Library version string (static storage). */
+const char* ozr_version(void);
+
+/* Create a context on CUDA device `device`, issuing work on `stream` (a cudaStream_t; NULL = the
+ * legacy default stream). n_max is a sizing hint for the workspace (0 = grow on demand). */
+ozr_status ozr_create(ozr_ctx* out, int device, void* stream, int64_t n_max);
+void ozr_destroy(ozr_ctx ctx);
+const char* ozr_last_error(ozr_ctx ctx);
+
+/* ------------------------------------------------------------------------------------------------
+ * ozr_split — error-free splitting into INT8 digit planes (§2.3, eq. tau/x lines 176-193).
+ *
+ * mode OZR_SPLIT_FIXED (k = k_or_beta, 1..15): per-line exponent e = ⌈log2 max|m|⌉ (0 for a zero
+ *   line), LSB exponent ℓ = e − (8(k−1)+6), integer p = RNE(m·2^−ℓ) [+ RNE(m_lo·2^−ℓ) when M_lo is
+ *   given: the double-double M + M_lo], written as k "excess-128" base-256 digits d_1..d_k in
+ *   [−128, 127], p = Σ d_s 256^{k−s} (R5/R6).
+ * mode OZR_SPLIT_X1 (β = k_or_beta, 2..52): the proposed method's truncation X̂ → X̂^(1),
+ *   x^(1) = fl(fl(τ_j + x) − τ_j), τ_j = 0.75·2^{⌈log2 w_j⌉}·2^β (eq. tau/x with s = 1); the digits
+ *   are those of q = x^(1)/2^{g_j}, g_j = ⌈log2 w_j⌉ + β − 53, with k = k_X(β) = smallest k such that
+ *   8(k−1)+6 ≥ 53−β, and ℓ_j = g_j. COLWISE only. If x1_out is non-null it receives X̂^(1) (fp64).
+ *
+ * axis OZR_COLWISE: one exponent per column of M (rows x cols); digit plane p holds element (i,j) at
+ *   digits[p*plane_stride + j*ldd + i] (ldd ≥ rows).
+ * axis OZR_ROWWISE: one exponent per row; plane p holds element (i,j) at digits[p*plane_stride +
+ *   i*ldd + j] (ldd ≥ cols) — the digits of Mᵀ column-wise (FIXED mode only).
+ * ldd and plane_stride are in bytes and must be multiples of 16 (TMA requirement).
+ * lsb_exp (device, int32[cols or rows]) receives ℓ. k_out (host, nullable) receives k.
+ * Errors: OZR_ERR_ARG, OZR_ERR_RANGE (k or β out of range), OZR_ERR_NONFINITE (checked).
+ * ------------------------------------------------------------------------------------------------ */
+enum { OZR_COLWISE = 0, OZR_ROWWISE = 1 };
+enum { OZR_SPLIT_FIXED = 0, OZR_SPLIT_X1 = 1 };
+ozr_status ozr_split(ozr_ctx ctx, const double* M, const double* M_lo, int64_t rows, int64_t cols, int64_t ldm,
+                     int axis, int mode, int k_or_beta, int8_t* digits, int64_t ldd, int64_t plane_stride,
+                     int32_t* lsb_exp, double* x1_out, int64_t ldx1, int* k_out);
+
+/* ------------------------------------------------------------------------------------------------
+ * ozr_gemm — accurate product C = A·B by the Ozaki scheme (§2.3) with INT8
+ * digits: A (m x k) split ROWWISE into kA digits, B (k x n) COLWISE into kB digits, keep digit pairs
+ * with s + t ≤ L (L = 0: all kA·kB pairs), each group of pairs of one diagonal d = s+t accumulated
+ * exactly in int32 on the tcgen05 tensor cores (K·pairs·2^14 < 2^31), then recombined exactly and
+ * rounded once to double-double: C_hi = RN(c), C_lo = RN(c − C_hi) for the exact value c of the kept
+ * pairs when it fits one int128 Horner chunk (otherwise a deterministic chunked sum, error < 2^-104|c|).
+ * C_lo may be NULL (fp64 result C_hi only). planes (nullable, device): the int32 group planes,
+ * element (i,j) of group g at planes[g*plane_stride + j*m + i] (plane_stride in elements ≥ m*n).
+ * ngroups_out (host, nullable). Errors: OZR_ERR_ARG, OZR_ERR_RANGE (kA/kB not in 1..15, k ≥ 2^31/2^14).
+ * ------------------------------------------------------------------------------------------------ */
+ozr_status ozr_gemm(ozr_ctx ctx, int64_t m, int64_t n, int64_t k, const double* A, int64_t lda, const double* B,
+                    int64_t ldb, int kA, int kB, int L, double* C_hi, double* C_lo, int64_t ldc, int32_t* planes,
+                    int64_t plane_stride, int* ngroups_out);
+
+/* Host-only: the group plan ozr_gemm uses for contraction length k (pairs (s,t), 1≤s≤kA, 1≤t≤kB,
+ * s+t ≤ L, by ascending diagonal then s, diagonals cut into chunks of ≤ ⌊(2^31−1)/(k·2^14)⌋ pairs).
+ * group_diag / group_npairs receive up to max_groups entries. */
+ozr_status ozr_gemm_plan(int64_t k, int kA, int kB, int L, int* ngroups, int* group_diag, int* group_npairs,
+                         int max_groups);
+
+/* ------------------------------------------------------------------------------------------------
+ * Refinement (Algorithm 1, one-sided product §3.3, β of §4.1 by default).
+ * ------------------------------------------------------------------------------------------------ */
+typedef struct {
+  double delta;      /* prescribed forward error δ (> u)                                     */
+  double theta;      /* β is chosen for δ' = δ/θ (R11; default 1)                  */
+  int beta_mode;     /* 0: §4.1 tuned β (⌊·⌋, nδ) [default]; 1: §3.3 eq. proposed_beta (⌈·⌉, ξ) */
+  double xi;         /* ξ for beta_mode 1 (0 → n)                                            */
+  int beta_override; /* > 0: use this β instead of the formula                               */
+  int truncate;      /* 1: X̂ → X̂^(1) (the proposed method) [default]; 0: keep all of X̂        */
+  int max_sweeps;    /* ozr_refine_to_tol: sweep limit (default 6)                            */
+  int kA_split;      /* digits of the one-time A split (default 15)                          */
+  double theta_V, theta_W, theta_U; /* accuracy targets of the three products as fractions of δ'·gap (V, W)
+                                       and δ' (X̂Ẽ) (R8; defaults 1/16, 1/16, 1/16)  */
+  int L_V, L_W, L_U; /* > 0: force the pair budgets (s+t ≤ L) instead of the planner          */
+  int cluster_mode;  /* 0: error on equal λ̂; 1: OA threshold branch (R13)      */
+} ozr_params;
+
+void ozr_params_default(ozr_params* p);
+
+typedef struct {
+  int sweep;
+  int beta, beta_raw, alpha;        /* β used (clamped to [2,52]), formula β, reported α (§4.1)       */
+  int kX, kA, kR, kE;               /* digit counts of X̂^(1), A (prefix used), Res, Ẽ'               */
+  int L_V, L_W, L_U;                /* pair budgets                                                    */
+  int pairs_V, pairs_W, pairs_U;    /* INT8 slice products (each an n x n_local x n INT8 GEMM)         */
+  int n_clusters;                   /* pairs |λ̂_i − λ̂_j| ≤ ω treated by the cluster branch              */
+  double gap_min, max_abs_lambda;   /* from the λ̂ that chose β                                         */
+  double normE_fro;                 /* ‖Ẽ‖_F                                                          */
+  double net_update;                /* ν = ‖X̂_new − X̂_old‖_F                                          */
+  double predicted_error;           /* ν² max|λ̂| / (n gap) (eq. assume2 with ξ = n), information       */
+  double ms_total, ms_gemm;         /* device time of the sweep and of its slice-product kernels       */
+  double int8_ops;                  /* 2·m·n·k·pairs summed over the sweep's slice products            */
+} ozr_step_report;
+
+/* One sweep on columns [0, n): A (n x n, symmetric — only its columns are read), X (n x n, in/out:
+ * X̂ → X̂^(1)(I + Ẽ) rounded to fp64), lambda (device, n, in: λ̂ of the previous sweep / the initial
+ * eigensolver, used for β and the digit budgets; out: the new Rayleigh quotients). report: host.
+ * Errors: OZR_ERR_ARG, OZR_ERR_RANGE (δ ≤ u), OZR_ERR_DEGENERATE, OZR_ERR_CUDA, OZR_ERR_NOMEM. */
+ozr_status ozr_refine_step(ozr_ctx ctx, const double* A, int64_t n, int64_t lda, double* X, int64_t ldx,
+                           double* lambda, const ozr_params* params, ozr_step_report* report);
+
+/* Repeat sweeps until the stop rule (R12): after sweep k stop when ν_k ≤ δ or ν_k² max|λ̂| /
+ * (n gap) ≤ δ; report OZR_ERR_NOT_CONVERGED on stagnation (ν_k > ν_{k−1}/2) or when max_sweeps is
+ * reached without converging — X / lambda then hold the last completed sweep. history (host, nullable)
+ * receives up to max_hist reports; sweeps_done (host, nullable). */
+ozr_status ozr_refine_to_tol(ozr_ctx ctx, const double* A, int64_t n, int64_t lda, double* X, int64_t ldx,
+                             double* lambda, const ozr_params* params, ozr_step_report* history, int max_hist,
+                             int* sweeps_done);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* OZR_H_ */

@@ -1,0 +1,210 @@
+"""Algorithm 1 with the one-sided product, its driver, reference eigenvectors and the forward error
+(TEST INFRASTRUCTURE ONLY — see oracle/__init__.py).
+
+The sweep follows PAPER.md Algorithm 1 (lines 261-278) line by line, with
+  * X̂ replaced by its leading slice X̂^(1) (§3.1, eq. E' line 331: X' = X̂^(1)(I+Ẽ)),
+  * β from §4.1 (lines 458-463) or §3.3 eq. (proposed_beta) (lines 400-405),
+  * accmul(A, X̂^(1)) = A·X̂^(1) EXACTLY (the quantity eq. mat_mul, computes with
+    n_A error-free slice products), here as a naive double-double triple loop (ddmm.c),
+  * accsum (line 275, "for example, Section 2.2") = the double-double sum rounded once to fp64.
+The other products of the sweep (W = X̂ᵀ(V − X̂D̂), X̂Ẽ) are also formed in double-double, so this is
+Algorithm 1 evaluated with products accurate to ~2^-100: the GPU path differs from it only by its
+documented digit budgets.
+"""
+import numpy as np
+
+from . import _clib
+from .fp import U, ceil_log2, dd_add, dd_div_dd, fast_two_sum, two_prod, two_sum
+from .split import (alpha_dense, alpha_theoretical, beta_dense, beta_theoretical, gap_min, sum_pow2_2c,
+                    x1_truncate)
+
+BETA_MIN, BETA_MAX = 2, 52  # reading R4: τ + x stays in τ's binade iff β ≥ 2; ≥ 1 bit kept iff β ≤ 52
+
+
+def col_dot_dd(X, Yh, Yl=None):
+    """s_j = Σ_i x_ij (yh_ij + yl_ij) in double-double, summed in row order i = 0..n-1."""
+    n, m = X.shape
+    sh = np.zeros(m)
+    sl = np.zeros(m)
+    for i in range(n):
+        p, e = two_prod(X[i], Yh[i])
+        if Yl is not None:
+            e = e + X[i] * Yl[i]
+        sh, sl = dd_add(sh, sl, p, e)
+    return sh, sl
+
+
+def choose_beta(n, delta_p, lam_prev, c, w, beta_mode="dense", xi=None):
+    """β for this sweep from the PREVIOUS sweep's λ̂ (reading R9; the paper computes λ̂ only after V)."""
+    if beta_mode == "dense":
+        b = beta_dense(n, delta_p, lam_prev, c, w)
+        a = alpha_dense(n, min(max(b, BETA_MIN), BETA_MAX))
+    else:
+        b = beta_theoretical(xi if xi else n, delta_p, lam_prev, c, w)
+        a = alpha_theoretical(n, min(max(b, BETA_MIN), BETA_MAX))
+    return b, a
+
+
+def sweep(A, X, lam_prev, delta, theta=1.0, beta=None, beta_mode="dense", xi=None, truncate=True):
+    """One iteration of Algorithm 1. Returns (X_new fp64, λ̂ fp64, info dict)."""
+    A = np.asarray(A, dtype=np.float64)
+    X = np.asarray(X, dtype=np.float64)
+    n = A.shape[0]
+    info = {}
+    w = np.max(np.abs(X), axis=0)
+    c = ceil_log2(w)
+    if beta is None:
+        beta, alpha = choose_beta(n, delta / theta, lam_prev, c, w, beta_mode, xi)
+    else:
+        alpha = alpha_dense(n, beta)
+    info["beta_raw"] = int(beta)
+    beta = int(min(max(beta, BETA_MIN), BETA_MAX))
+    info["beta"], info["alpha"] = beta, int(alpha)
+    # X̂ <- X̂^(1): eq. (x), s = 1
+    X1 = x1_truncate(X, beta)[0] if truncate else X.copy()
+    # line 1: V = accmul(A, X̂)  — exact product (A symmetric: V = A X̂^(1))
+    Vh, Vl = _clib.dd_gemm_nt(A, np.ascontiguousarray(X1.T))
+    # line 2: r_i = 1 − x̂_iᵀ x̂_i
+    sh, sl = col_dot_dd(X1, X1)
+    rh, rl = dd_add(np.ones(n), np.zeros(n), -sh, -sl)
+    if np.any(rh >= 1.0):
+        raise ValueError("degenerate column: r_i >= 1")
+    # line 3: λ̂_i = x̂_iᵀ v̂_i / (1 − r_i)   (1 − r_i = x̂_iᵀx̂_i)
+    th, tl = col_dot_dd(X1, Vh, Vl)
+    lh, ll = dd_div_dd(th, tl, sh, sl)
+    lam = lh + ll
+    # line 4: W = X̂ᵀ (V − X̂ D̂)
+    ph, pl = two_prod(X1, lam[None, :])
+    Rh, Rl = dd_add(Vh, Vl, -ph, -pl)
+    Wh, Wl = _clib.dd_gemm_nt(np.ascontiguousarray(X1.T), np.ascontiguousarray(Rh.T), None,
+                              np.ascontiguousarray(Rl.T))
+    W = Wh + Wl
+    # line 5: ẽ_ij = w_ij / (λ̃_j − λ̃_i), i ≠ j;  ẽ_ii = r_i / 2
+    dl = lam[None, :] - lam[:, None]
+    off = ~np.eye(n, dtype=bool)
+    if np.any(dl[off] == 0):
+        raise ValueError("clustered eigenvalues: equal λ̂ (PAPER.md:333 assumes none)")
+    E = np.where(off, W / np.where(off, dl, 1.0), 0.0)
+    E[np.arange(n), np.arange(n)] = (rh + rl) / 2
+    # line 6: X̂ <- accsum(X̂, X̂Ẽ)  on X̂^(1) (eq. E')
+    Uh, Ul = _clib.dd_gemm_nt(X1, np.ascontiguousarray(E.T))
+    s, e = two_sum(X1, Uh)
+    Xn, _ = fast_two_sum(s, e + Ul)
+    info["normE_fro"] = float(np.sqrt(np.sum(E * E)))
+    info["net_update"] = float(np.sqrt(np.sum((Xn - X) ** 2)))
+    info["gap_min"] = gap_min(lam_prev)
+    info["X1"] = X1
+    info["V"] = (Vh, Vl)
+    info["W"] = (Wh, Wl)
+    info["r"] = (rh, rl)
+    info["E"] = E
+    return Xn, lam, info
+
+
+def refine_to_tol(A, X0, lam0, delta, theta=1.0, max_sweeps=6, beta_mode="dense", xi=None, callback=None):
+    """Driver (reading R12): repeat sweeps; stop after sweep k when ν_k = ‖X_k − X_{k−1}‖_F ≤ δ, or when
+    the paper's error model predicts ‖X − X_k‖ ≲ ν_k² max|λ̂| / (n gap) ≤ δ (eq. assume2 / gamma,
+    PAPER.md:341-373 with ξ = n as in §4.1), or at stagnation (ν_k > ν_{k−1}/2), or at max_sweeps."""
+    X, lam = np.asarray(X0, dtype=np.float64), np.asarray(lam0, dtype=np.float64)
+    n = X.shape[0]
+    hist = []
+    nu_prev = None
+    for k in range(max_sweeps):
+        Xn, lamn, info = sweep(A, X, lam, delta, theta, beta_mode=beta_mode, xi=xi)
+        nu = info["net_update"]
+        pred = nu * nu * np.max(np.abs(lamn)) / (n * gap_min(lamn))
+        rec = dict(sweep=k + 1, beta=info["beta"], alpha=info["alpha"], net_update=nu, predicted=pred,
+                   normE_fro=info["normE_fro"])
+        X, lam = Xn, lamn
+        if callback:
+            rec.update(callback(X, lam))
+        hist.append(rec)
+        if nu <= delta or pred <= delta:
+            rec["stop"] = "converged"
+            break
+        if nu_prev is not None and nu > nu_prev / 2:
+            rec["stop"] = "stagnation"
+            break
+        nu_prev = nu
+    return X, lam, hist
+
+
+# ----------------------------------------------------------------------------- reference solution
+
+def reference_eigvecs(A, X0, lam0, tol=1e-27, max_sweeps=10):
+    """Reference eigenvectors of the STORED A (PAPER.md:62 uses a pseudo-quadruple reference): the
+    Ogita–Aishima iteration (the R/S form ẽ_ij = (s_ij + λ̃_j r_ij)/(λ̃_j − λ̃_i))
+    with X̂ kept in double-double and every product in double-double, untruncated, from an LAPACK
+    start, until ‖Ẽ‖_F ≤ tol. Returns (Xh, Xl, λh, λl, history). Certified separately by
+    residual_certificate() and pinned against __float128 Jacobi (n ≤ 32) and exact families."""
+    A = np.asarray(A, dtype=np.float64)
+    n = A.shape[0]
+    Xh, Xl = np.array(X0, dtype=np.float64), np.zeros((n, n))
+    hist = []
+    lh = ll = None
+    for k in range(max_sweeps):
+        XhT, XlT = np.ascontiguousarray(Xh.T), np.ascontiguousarray(Xl.T)
+        Vh, Vl = _clib.dd_gemm_nt(A, XhT, None, XlT)               # V = A X
+        Gh, Gl = _clib.dd_gemm_nt(XhT, XhT, XlT, XlT)             # G = XᵀX
+        VT_h, VT_l = np.ascontiguousarray(Vh.T), np.ascontiguousarray(Vl.T)
+        Sh, Sl = _clib.dd_gemm_nt(XhT, VT_h, XlT, VT_l)           # S = XᵀA X
+        dh, dl_ = np.diag(Gh).copy(), np.diag(Gl).copy()
+        th, tl = np.diag(Sh).copy(), np.diag(Sl).copy()
+        lh, ll = dd_div_dd(th, tl, dh, dl_)                        # Rayleigh quotients
+        Rh, Rl = dd_add(np.eye(n), np.zeros((n, n)), -Gh, -Gl)    # R = I − XᵀX
+        lam = lh + ll
+        R = Rh + Rl
+        # s_ij + λ̃_j r_ij in dd, then divided in fp64 (Ẽ needs only relative accuracy ~ ‖Ẽ‖)
+        ph, pl = two_prod(Rh, lh[None, :])
+        Nh, Nl = dd_add(Sh, Sl, ph, pl + Rl * lh[None, :] + Rh * ll[None, :])
+        dlam = (lh[None, :] - lh[:, None]) + (ll[None, :] - ll[:, None])
+        off = ~np.eye(n, dtype=bool)
+        E = np.where(off, (Nh + Nl) / np.where(off, dlam, 1.0), 0.0)
+        E[np.arange(n), np.arange(n)] = np.diag(R) / 2
+        Uh, Ul = _clib.dd_gemm_nt(Xh, np.ascontiguousarray(E.T), Xl, None)  # U = X Ẽ
+        Xh, Xl = dd_add(Xh, Xl, Uh, Ul)
+        nE = float(np.sqrt(np.sum(E * E)))
+        hist.append(nE)
+        if nE <= tol or (len(hist) >= 3 and nE > hist[-2] / 4 and nE < 1e-15):
+            break
+    return Xh, Xl, lh, ll, hist
+
+
+def residual_certificate(A, Xh, Xl, lh, ll):
+    """Pin P8: per-column residual ‖A x_j − λ_j x_j‖₂ in double-double and the
+    orthogonality defect; with the eigenvalue gaps these bound the reference's own forward error
+    (Davis–Kahan sin θ ≤ ‖r_j‖ / gap_j). Returns (res_norms, ortho_max)."""
+    n = A.shape[0]
+    XhT, XlT = np.ascontiguousarray(Xh.T), np.ascontiguousarray(Xl.T)
+    Vh, Vl = _clib.dd_gemm_nt(A, XhT, None, XlT)
+    ph, pl = two_prod(Xh, lh[None, :])
+    pl = pl + Xl * lh[None, :] + Xh * ll[None, :]
+    Rh, Rl = dd_add(Vh, Vl, -ph, -pl)
+    res = np.sqrt(np.sum((Rh + Rl) ** 2, axis=0))
+    Gh, Gl = _clib.dd_gemm_nt(XhT, XhT, XlT, XlT)
+    Dh, Dl = dd_add(Gh, Gl, -np.eye(n), np.zeros((n, n)))
+    return res, float(np.max(np.abs(Dh + Dl)))
+
+
+def forward_error(Xh_ref, Xl_ref, X, lam_ref=None, lam=None, power_iters=None):
+    """‖X − X̂‖₂ (PAPER.md:48-50, 2-norm per PAPER.md:121). Columns are matched by ascending λ (when
+    λ's are given) and signs by sign(x_refᵀ x̂). For n ≤ 2048 the exact 2-norm (SVD); beyond, a
+    power iteration of `power_iters` (default 40) steps on DᵀD."""
+    X = np.asarray(X, dtype=np.float64)
+    if lam_ref is not None and lam is not None:
+        pr, px = np.argsort(lam_ref, kind="stable"), np.argsort(lam, kind="stable")
+        Xh_ref, Xl_ref, X = Xh_ref[:, pr], Xl_ref[:, pr], X[:, px]
+    sgn = np.sign(np.sum(Xh_ref * X, axis=0))
+    sgn[sgn == 0] = 1.0
+    D = (Xh_ref * sgn[None, :] - X) + Xl_ref * sgn[None, :]
+    n = D.shape[0]
+    if power_iters is None and n <= 2048:
+        return float(np.linalg.norm(D, 2))
+    v = np.random.default_rng(0).standard_normal(n)
+    v /= np.linalg.norm(v)
+    s = 0.0
+    for _ in range(power_iters or 40):
+        y = D.T @ (D @ v)
+        s = np.linalg.norm(y)
+        v = y / s
+    return float(np.sqrt(s))

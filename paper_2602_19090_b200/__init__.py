@@ -1,0 +1,12 @@
+"""paper_2602_19090_b200 — B200-native forward-error-oriented eigenvector refinement (arXiv 2602.19090).
+
+The product is the C-ABI library libozr.so (include/ozr.h) built from csrc/ for sm_100a; this package
+is its thin Python binding (argument marshalling only). See DESIGN.md.
+"""
+from ._ozr import (OZR_COLWISE, OZR_ROWWISE, OZR_SPLIT_FIXED, OZR_SPLIT_X1, Context, OzrError, Params, StepReport,
+                   colmajor, default_params, lib, ozr_gemm, ozr_gemm_plan, ozr_refine_step, ozr_refine_to_tol,
+                   ozr_split, ozr_version)
+
+__all__ = ["Context", "OzrError", "Params", "StepReport", "colmajor", "default_params", "lib", "ozr_gemm",
+           "ozr_gemm_plan", "ozr_refine_step", "ozr_refine_to_tol", "ozr_split", "ozr_version", "OZR_COLWISE",
+           "OZR_ROWWISE", "OZR_SPLIT_FIXED", "OZR_SPLIT_X1"]

@@ -1,0 +1,404 @@
+// kernels.cu — the HBM-bound kernels of one ozr sweep. Each is "one CTA per column": the column
+// is re-read from L2 between passes, every reduction has a fixed shape (deterministic; integer
+// reductions are exact), and a column is produced by exactly one CTA (the block-column partition
+// of X̂ across GPUs changes nothing).
+//
+//   k_colmax          w_j = max_i |x_ij|
+//   k_x1_split        X̂ → X̂^(1) by the τ trick (eq. tau/x, s = 1), its INT8
+//                     digits, g_j, and r_j = 1 − x̂_jᵀx̂_j EXACTLY (Alg. 1 line 2)
+//   k_split_fixed     column-wise fixed-point digits of an fp64 or double-double matrix (R5/R6)
+//   k_transpose_i8    digit planes [p][col][row] → [p][row][col] (A operand of X̂^(1)·Ẽ)
+//   k_transpose_f64   fp64 transpose (ROWWISE splits of ozr_split / ozr_gemm)
+//   k_recombine_V     V = Σ slice products (exact) → dd; λ̂_j = x̂_jᵀv_j/(1−r_j); Res = V − X̂D̂;
+//                     column maxima of Res                            (Alg. 1 lines 1,3,4)
+//   k_recombine_E     W → Ẽ (Alg. 1 line 5), scaled Ẽ' = diag(2^g)Ẽ, column maxima, ‖Ẽ‖_F parts
+//   k_final           U = X̂^(1)Ẽ → X̂ ← RN(X̂^(1) + U) (Alg. 1 line 6, accsum), ν, column maxima
+//   k_recombine_dd    generic recombination for ozr_gemm
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "ddmath.cuh"
+#include "kernels.h"
+
+namespace ozr {
+
+namespace {
+
+constexpr int BS = 256;  // threads per CTA of every column kernel
+
+// ---------------------------------------------------------------- deterministic block reductions
+__device__ __forceinline__ double block_max(double v, double* sh) {
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) sh[w] = v;
+  __syncthreads();
+  double r = sh[0];
+  for (int i = 1; i < BS / 32; ++i) r = fmax(r, sh[i]);
+  __syncthreads();
+  return r;
+}
+
+__device__ __forceinline__ double block_sum(double v, double* sh) {  // fixed butterfly + fixed order
+  for (int o = 16; o > 0; o >>= 1) v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, o));
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) sh[w] = v;
+  __syncthreads();
+  double r = sh[0];
+  for (int i = 1; i < BS / 32; ++i) r = __dadd_rn(r, sh[i]);
+  __syncthreads();
+  return r;
+}
+
+__device__ __forceinline__ dd block_sum_dd(dd v, double* sh) {
+  for (int o = 16; o > 0; o >>= 1) {
+    dd u;
+    u.hi = __shfl_xor_sync(0xffffffffu, v.hi, o);
+    u.lo = __shfl_xor_sync(0xffffffffu, v.lo, o);
+    v = dd_add(v, u);
+  }
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) {
+    sh[2 * w] = v.hi;
+    sh[2 * w + 1] = v.lo;
+  }
+  __syncthreads();
+  dd r{sh[0], sh[1]};
+  for (int i = 1; i < BS / 32; ++i) r = dd_add(r, dd{sh[2 * i], sh[2 * i + 1]});
+  __syncthreads();
+  return r;
+}
+
+__device__ __forceinline__ i128 block_sum_i128(i128 v, i128* sh) {  // exact: order irrelevant
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  for (int o = 16; o > 0; o >>= 1) {
+    uint64_t lo = static_cast<uint64_t>(v), hi = static_cast<uint64_t>(static_cast<u128>(v) >> 64);
+    uint64_t lo2 = __shfl_xor_sync(0xffffffffu, lo, o), hi2 = __shfl_xor_sync(0xffffffffu, hi, o);
+    v += static_cast<i128>((static_cast<u128>(hi2) << 64) | lo2);
+  }
+  __syncthreads();
+  if (l == 0) sh[w] = v;
+  __syncthreads();
+  i128 r = 0;
+  for (int i = 0; i < BS / 32; ++i) r += sh[i];
+  __syncthreads();
+  return r;
+}
+
+// ---------------------------------------------------------------- recombination of one element
+// value = Σ_chunks T_c · 2^{8(L − dhi_c) + e}, T_c = Horner over the chunk's groups (exact int128).
+__device__ __forceinline__ dd recombine_elem(const int32_t* __restrict__ planes, long long pstride, long long off,
+                                             const RecombPlan& rp, int e) {
+  dd acc{0.0, 0.0};
+  for (int c = 0; c < rp.nchunks; ++c) {
+    i128 T = 0;
+    int dprev = rp.diag[rp.chunk_first[c]];
+    for (int g = rp.chunk_first[c]; g < rp.chunk_first[c + 1]; ++g) {
+      const int d = rp.diag[g];
+      T = static_cast<i128>(static_cast<u128>(T) << (8 * (d - dprev))) + static_cast<i128>(__ldg(planes + g * pstride + off));
+      dprev = d;
+    }
+    dd v = i128_to_dd(T);
+    const int sc = 8 * (rp.L - dprev) + e;
+    v.hi = scalbn(v.hi, sc);
+    v.lo = scalbn(v.lo, sc);
+    acc = (c == 0) ? v : dd_add(acc, v);
+  }
+  return acc;
+}
+
+// ---------------------------------------------------------------- kernels
+__global__ void __launch_bounds__(BS) k_colmax(const double* __restrict__ X, long long ldx, int rows,
+                                               double* __restrict__ w, int* __restrict__ err) {
+  __shared__ double sh[BS / 32];
+  const double* col = X + blockIdx.x * ldx;
+  double m = 0.0;
+  bool bad = false;
+  for (int i = threadIdx.x; i < rows; i += BS) {
+    const double x = col[i];
+    bad |= !isfinite(x);
+    m = fmax(m, fabs(x));
+  }
+  if (bad) atomicOr(err, ERR_NONFINITE);
+  m = block_max(m, sh);
+  if (threadIdx.x == 0) w[blockIdx.x] = m;
+}
+
+__global__ void __launch_bounds__(BS)
+    k_x1_split(const double* __restrict__ X, long long ldx, int rows, int beta, int kx, const double* __restrict__ w,
+               double* __restrict__ X1, long long ldx1, int8_t* __restrict__ dig, long long ldd, long long pstride,
+               int32_t* __restrict__ g_out, double* __restrict__ s_hi, double* __restrict__ s_lo,
+               double* __restrict__ r_hi, double* __restrict__ r_lo, int* __restrict__ err) {
+  __shared__ i128 shq[BS / 32];
+  const int j = blockIdx.x;
+  const double* col = X + j * ldx;
+  const double wj = w[j];
+  const int c = ceil_log2_d(wj);
+  const int g = c + beta - 53;
+  const double tau = (wj == 0.0) ? 0.0 : scalbn(0.75, c + beta);  // eq. (tau)
+  i128 sq = 0;
+  for (int i = threadIdx.x; i < rows; i += BS) {
+    const double x = col[i];
+    const double x1 = __dsub_rn(__dadd_rn(tau, x), tau);  // eq. (x), s = 1: fl(fl(τ + x) − τ)
+    X1[j * ldx1 + i] = x1;
+    const long long q = static_cast<long long>(scalbn(x1, -g));  // exact integer, |q| <= 2^{53-β}
+    sq += static_cast<i128>(q) * q;
+    int d[8];
+    excess_digits(static_cast<i128>(q), kx, d);
+    for (int p = 0; p < kx; ++p) dig[p * pstride + j * ldd + i] = static_cast<int8_t>(d[p]);
+  }
+  const i128 SQ = block_sum_i128(sq, shq);
+  if (threadIdx.x == 0) {
+    g_out[j] = g;
+    // x̂_jᵀx̂_j = 2^{2g} SQ and r_j = 1 − 2^{2g} SQ = 2^{2g}(2^{−2g} − SQ), both exact integers scaled.
+    if (-2 * g > 125 || -2 * g < 0) {
+      atomicOr(err, ERR_RANGE);
+    } else {
+      const dd s = i128_to_dd(SQ);
+      const dd r = i128_to_dd((static_cast<i128>(1) << (-2 * g)) - SQ);
+      s_hi[j] = scalbn(s.hi, 2 * g);
+      s_lo[j] = scalbn(s.lo, 2 * g);
+      r_hi[j] = scalbn(r.hi, 2 * g);
+      r_lo[j] = scalbn(r.lo, 2 * g);
+      if (SQ == 0) atomicOr(err, ERR_DEGENERATE);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(BS)
+    k_split_fixed(const double* __restrict__ M, const double* __restrict__ Mlo, long long ldm, int rows, int k,
+                  int8_t* __restrict__ dig, long long ldd, long long pstride, int32_t* __restrict__ ell_out,
+                  int* __restrict__ err) {
+  __shared__ double sh[BS / 32];
+  const int j = blockIdx.x;
+  const double* col = M + j * ldm;
+  const double* cl = Mlo ? Mlo + j * ldm : nullptr;
+  double m = 0.0;
+  bool bad = false;
+  for (int i = threadIdx.x; i < rows; i += BS) {
+    const double x = col[i];
+    bad |= !isfinite(x);
+    m = fmax(m, fabs(x));
+  }
+  if (bad) atomicOr(err, ERR_NONFINITE);
+  m = block_max(m, sh);
+  const int e = ceil_log2_d(m);
+  const int S = 8 * (k - 1) + 6;
+  for (int i = threadIdx.x; i < rows; i += BS) {
+    i128 p = rint_to_i128(scalbn(col[i], S - e));
+    if (cl) p += rint_to_i128(scalbn(cl[i], S - e));
+    int d[16];
+    excess_digits(p, k, d);
+    for (int q = 0; q < k; ++q) dig[q * pstride + j * ldd + i] = static_cast<int8_t>(d[q]);
+  }
+  if (threadIdx.x == 0) ell_out[j] = e - S;
+}
+
+__global__ void k_transpose_i8(const int8_t* __restrict__ src, long long lds, long long sps, int8_t* __restrict__ dst,
+                               long long ldt, long long tps, int rows, int cols) {
+  // src element (i,j) at src[p*sps + j*lds + i]; dst element (i,j) at dst[p*tps + i*ldt + j]
+  __shared__ int8_t t[64][65];
+  const int p = blockIdx.z;
+  const int i0 = blockIdx.x * 64, j0 = blockIdx.y * 64;
+  for (int e = threadIdx.x; e < 64 * 64; e += blockDim.x) {
+    const int ii = e & 63, jj = e >> 6;
+    const int i = i0 + ii, j = j0 + jj;
+    t[jj][ii] = (i < rows && j < cols) ? src[p * sps + j * lds + i] : 0;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < 64 * 64; e += blockDim.x) {
+    const int jj = e & 63, ii = e >> 6;
+    const int i = i0 + ii, j = j0 + jj;
+    if (i < rows && j < cols) dst[p * tps + static_cast<long long>(i) * ldt + j] = t[jj][ii];
+  }
+}
+
+__global__ void k_transpose_f64(const double* __restrict__ src, long long lds, double* __restrict__ dst,
+                                long long ldt, int rows, int cols) {
+  // dst (cols x rows) = srcᵀ, column-major both
+  __shared__ double t[32][33];
+  const int i0 = blockIdx.x * 32, j0 = blockIdx.y * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+  for (int jj = ty; jj < 32; jj += 8) {
+    const int i = i0 + tx, j = j0 + jj;
+    t[jj][tx] = (i < rows && j < cols) ? src[static_cast<long long>(j) * lds + i] : 0.0;
+  }
+  __syncthreads();
+  for (int ii = ty; ii < 32; ii += 8) {
+    const int j = j0 + tx, i = i0 + ii;
+    if (i < rows && j < cols) dst[static_cast<long long>(i) * ldt + j] = t[tx][ii];
+  }
+}
+
+__global__ void __launch_bounds__(BS)
+    k_recombine_V(const int32_t* __restrict__ planes, long long pstride, int rows, const __grid_constant__ RecombPlan rp,
+                  const int32_t* __restrict__ ellA, const int32_t* __restrict__ ellB, int scale8,
+                  const double* __restrict__ X1, long long ldx1, const double* __restrict__ s_hi,
+                  const double* __restrict__ s_lo, double* __restrict__ Vh, double* __restrict__ Vl, long long ldv,
+                  double* __restrict__ lam_out, int32_t* __restrict__ eR, int* __restrict__ eR_max) {
+  __shared__ double sh[2 * BS / 32];
+  const int j = blockIdx.x;
+  const int eb = ellB[j] + scale8;
+  const double* x1 = X1 + j * ldx1;
+  dd t{0.0, 0.0};
+  // pass 1: V (Alg. 1 line 1) and x̂_jᵀ v_j (line 3)
+  for (int i = threadIdx.x; i < rows; i += BS) {
+    const dd v = recombine_elem(planes, pstride, static_cast<long long>(j) * rows + i, rp, ellA[i] + eb);
+    Vh[j * ldv + i] = v.hi;
+    Vl[j * ldv + i] = v.lo;
+    t = dd_add(t, dd_mul_d(v, x1[i]));
+  }
+  t = block_sum_dd(t, sh);
+  const dd lam = dd_div(t, dd{s_hi[j], s_lo[j]});  // λ̂_j = x̂_jᵀv̂_j / (1 − r_j)
+  const double l = lam.hi;
+  // pass 2: Res = V − X̂ D̂ (line 4, inner part), in double-double; column max of |Res|
+  double m = 0.0;
+  for (int i = threadIdx.x; i < rows; i += BS) {
+    double ph, pl;
+    two_prod(x1[i], l, ph, pl);
+    const dd r = dd_add(dd{Vh[j * ldv + i], Vl[j * ldv + i]}, dd{-ph, -pl});
+    Vh[j * ldv + i] = r.hi;
+    Vl[j * ldv + i] = r.lo;
+    m = fmax(m, fabs(r.hi));
+  }
+  m = block_max(m, sh);
+  if (threadIdx.x == 0) {
+    lam_out[j] = l;
+    const int e = ceil_log2_d(m);
+    eR[j] = e;
+    if (m > 0.0) atomicMax(eR_max, e);
+  }
+}
+
+__global__ void __launch_bounds__(BS)
+    k_recombine_E(const int32_t* __restrict__ planes, long long pstride, int rows, const __grid_constant__ RecombPlan rp,
+                  const int32_t* __restrict__ ellA, const int32_t* __restrict__ ellB, int scale8,
+                  const double* __restrict__ r_hi, const double* __restrict__ lam, const int32_t* __restrict__ gX,
+                  int col0, double* __restrict__ Ep, long long lde, double* __restrict__ nrm2,
+                  int* __restrict__ eE_max, int* __restrict__ err) {
+  __shared__ double sh[BS / 32];
+  const int j = blockIdx.x;        // local column
+  const int jg = col0 + j;         // global index of column j (its λ̂)
+  const int eb = ellB[j] + scale8;
+  const double lj = lam[jg];
+  double m = 0.0, s2 = 0.0;
+  bool bad = false;
+  for (int i = threadIdx.x; i < rows; i += BS) {
+    double e;
+    if (i == jg) {
+      e = r_hi[j] * 0.5;  // ẽ_jj = r_j / 2
+    } else {
+      const dd wv = recombine_elem(planes, pstride, static_cast<long long>(j) * rows + i, rp, ellA[i] + eb);
+      const double dl = __dsub_rn(lj, lam[i]);  // λ̃_j − λ̃_i
+      if (dl == 0.0) bad = true;
+      e = __ddiv_rn(wv.hi, dl);  // ẽ_ij = w_ij / (λ̃_j − λ̃_i)  (Alg. 1 line 5)
+    }
+    s2 = __fma_rn(e, e, s2);
+    const double ep = scalbn(e, gX[i]);  // Ẽ' = diag(2^g) Ẽ (exact)
+    Ep[j * lde + i] = ep;
+    m = fmax(m, fabs(ep));
+  }
+  if (bad) atomicOr(err, ERR_DEGENERATE);
+  m = block_max(m, sh);
+  s2 = block_sum(s2, sh);
+  if (threadIdx.x == 0) {
+    nrm2[j] = s2;
+    if (m > 0.0) atomicMax(eE_max, ceil_log2_d(m));
+  }
+}
+
+__global__ void __launch_bounds__(BS)
+    k_final(const int32_t* __restrict__ planes, long long pstride, int rows, const __grid_constant__ RecombPlan rp,
+            const int32_t* __restrict__ ellB, int scale8, const double* __restrict__ X1, long long ldx1,
+            double* __restrict__ X, long long ldx, double* __restrict__ nu2, double* __restrict__ wnext) {
+  __shared__ double sh[BS / 32];
+  const int j = blockIdx.x;
+  const int eb = ellB[j] + scale8;  // the Q operand (digits of X̂^(1)/2^g) has ℓ = 0 on every row
+  double s2 = 0.0, m = 0.0;
+  for (int i = threadIdx.x; i < rows; i += BS) {
+    const dd u = recombine_elem(planes, pstride, static_cast<long long>(j) * rows + i, rp, eb);
+    const double x1 = X1[j * ldx1 + i];
+    double s, e;
+    two_sum(x1, u.hi, s, e);
+    const double xn = __dadd_rn(s, __dadd_rn(e, u.lo));  // accsum: RN(x^(1) + U)
+    const double xo = X[j * ldx + i];
+    const double d = __dsub_rn(xn, xo);
+    s2 = __fma_rn(d, d, s2);
+    m = fmax(m, fabs(xn));
+    X[j * ldx + i] = xn;
+  }
+  s2 = block_sum(s2, sh);
+  m = block_max(m, sh);
+  if (threadIdx.x == 0) {
+    nu2[j] = s2;
+    wnext[j] = m;
+  }
+}
+
+__global__ void __launch_bounds__(BS)
+    k_recombine_dd(const int32_t* __restrict__ planes, long long pstride, int rows, const __grid_constant__ RecombPlan rp,
+                   const int32_t* __restrict__ ellA, const int32_t* __restrict__ ellB, int scale8,
+                   double* __restrict__ Ch, double* __restrict__ Cl, long long ldc) {
+  const int j = blockIdx.x;
+  const int eb = ellB[j] + scale8;
+  for (int i = threadIdx.x; i < rows; i += BS) {
+    const dd v = recombine_elem(planes, pstride, static_cast<long long>(j) * rows + i, rp, ellA[i] + eb);
+    Ch[j * ldc + i] = v.hi;
+    if (Cl) Cl[j * ldc + i] = v.lo;
+  }
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------- launchers
+void launch_colmax(const double* X, long long ldx, int rows, int cols, double* w, int* err, cudaStream_t s) {
+  k_colmax<<<cols, BS, 0, s>>>(X, ldx, rows, w, err);
+}
+void launch_x1_split(const double* X, long long ldx, int rows, int cols, int beta, int kx, const double* w, double* X1,
+                     long long ldx1, int8_t* dig, long long ldd, long long pstride, int32_t* g, double* s_hi,
+                     double* s_lo, double* r_hi, double* r_lo, int* err, cudaStream_t s) {
+  k_x1_split<<<cols, BS, 0, s>>>(X, ldx, rows, beta, kx, w, X1, ldx1, dig, ldd, pstride, g, s_hi, s_lo, r_hi, r_lo,
+                                 err);
+}
+void launch_split_fixed(const double* M, const double* Mlo, long long ldm, int rows, int cols, int k, int8_t* dig,
+                        long long ldd, long long pstride, int32_t* ell, int* err, cudaStream_t s) {
+  k_split_fixed<<<cols, BS, 0, s>>>(M, Mlo, ldm, rows, k, dig, ldd, pstride, ell, err);
+}
+void launch_transpose_i8(const int8_t* src, long long lds, long long sps, int8_t* dst, long long ldt, long long tps,
+                         int rows, int cols, int planes, cudaStream_t s) {
+  dim3 grid((rows + 63) / 64, (cols + 63) / 64, planes);
+  k_transpose_i8<<<grid, 256, 0, s>>>(src, lds, sps, dst, ldt, tps, rows, cols);
+}
+void launch_transpose_f64(const double* src, long long lds, double* dst, long long ldt, int rows, int cols,
+                          cudaStream_t s) {
+  dim3 grid((rows + 31) / 32, (cols + 31) / 32);
+  k_transpose_f64<<<grid, 256, 0, s>>>(src, lds, dst, ldt, rows, cols);
+}
+void launch_recombine_V(const int32_t* planes, long long pstride, int rows, int cols, const RecombPlan& rp,
+                        const int32_t* ellA, const int32_t* ellB, int scale8, const double* X1, long long ldx1,
+                        const double* s_hi, const double* s_lo, double* Vh, double* Vl, long long ldv,
+                        double* lam_out, int32_t* eR, int* eR_max, cudaStream_t s) {
+  k_recombine_V<<<cols, BS, 0, s>>>(planes, pstride, rows, rp, ellA, ellB, scale8, X1, ldx1, s_hi, s_lo, Vh, Vl, ldv,
+                                    lam_out, eR, eR_max);
+}
+void launch_recombine_E(const int32_t* planes, long long pstride, int rows, int cols, const RecombPlan& rp,
+                        const int32_t* ellA, const int32_t* ellB, int scale8, const double* r_hi, const double* lam,
+                        const int32_t* gX, int col0, double* Ep, long long lde, double* nrm2, int* eE_max, int* err,
+                        cudaStream_t s) {
+  k_recombine_E<<<cols, BS, 0, s>>>(planes, pstride, rows, rp, ellA, ellB, scale8, r_hi, lam, gX, col0, Ep, lde, nrm2,
+                                    eE_max, err);
+}
+void launch_final(const int32_t* planes, long long pstride, int rows, int cols, const RecombPlan& rp,
+                  const int32_t* ellB, int scale8, const double* X1, long long ldx1, double* X, long long ldx,
+                  double* nu2, double* wnext, cudaStream_t s) {
+  k_final<<<cols, BS, 0, s>>>(planes, pstride, rows, rp, ellB, scale8, X1, ldx1, X, ldx, nu2, wnext);
+}
+void launch_recombine_dd(const int32_t* planes, long long pstride, int rows, int cols, const RecombPlan& rp,
+                         const int32_t* ellA, const int32_t* ellB, int scale8, double* Ch, double* Cl, long long ldc,
+                         cudaStream_t s) {
+  k_recombine_dd<<<cols, BS, 0, s>>>(planes, pstride, rows, rp, ellA, ellB, scale8, Ch, Cl, ldc);
+}
+
+}  // namespace ozr

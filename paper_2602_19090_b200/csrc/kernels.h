@@ -1,0 +1,48 @@
+// kernels.h — launchers of the HBM-bound ozr kernels (kernels.cu). Internal, not ABI.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace ozr {
+
+enum { ERR_NONFINITE = 1, ERR_RANGE = 2, ERR_DEGENERATE = 4 };
+
+constexpr int kMaxChunks = 8;
+constexpr int kPlanGroups = 96;
+
+// How the int32 group planes of one product are recombined:
+// value = Σ_c T_c · 2^{8(L − d_last(c)) + ℓA_i + ℓB_j + scale8}, T_c = Σ_{g∈c} 256^{d_last(c) − d_g} C_g (int128).
+struct RecombPlan {
+  int ngroups;
+  int L;
+  int nchunks;
+  int chunk_first[kMaxChunks + 1];
+  int diag[kPlanGroups];
+};
+
+void launch_colmax(const double* X, long long ldx, int rows, int cols, double* w, int* err, cudaStream_t s);
+void launch_x1_split(const double* X, long long ldx, int rows, int cols, int beta, int kx, const double* w, double* X1,
+                     long long ldx1, int8_t* dig, long long ldd, long long pstride, int32_t* g, double* s_hi,
+                     double* s_lo, double* r_hi, double* r_lo, int* err, cudaStream_t s);
+void launch_split_fixed(const double* M, const double* Mlo, long long ldm, int rows, int cols, int k, int8_t* dig,
+                        long long ldd, long long pstride, int32_t* ell, int* err, cudaStream_t s);
+void launch_transpose_i8(const int8_t* src, long long lds, long long sps, int8_t* dst, long long ldt, long long tps,
+                         int rows, int cols, int planes, cudaStream_t s);
+void launch_transpose_f64(const double* src, long long lds, double* dst, long long ldt, int rows, int cols,
+                          cudaStream_t s);
+void launch_recombine_V(const int32_t* planes, long long pstride, int rows, int cols, const RecombPlan& rp,
+                        const int32_t* ellA, const int32_t* ellB, int scale8, const double* X1, long long ldx1,
+                        const double* s_hi, const double* s_lo, double* Vh, double* Vl, long long ldv,
+                        double* lam_out, int32_t* eR, int* eR_max, cudaStream_t s);
+void launch_recombine_E(const int32_t* planes, long long pstride, int rows, int cols, const RecombPlan& rp,
+                        const int32_t* ellA, const int32_t* ellB, int scale8, const double* r_hi, const double* lam,
+                        const int32_t* gX, int col0, double* Ep, long long lde, double* nrm2, int* eE_max, int* err,
+                        cudaStream_t s);
+void launch_final(const int32_t* planes, long long pstride, int rows, int cols, const RecombPlan& rp,
+                  const int32_t* ellB, int scale8, const double* X1, long long ldx1, double* X, long long ldx,
+                  double* nu2, double* wnext, cudaStream_t s);
+void launch_recombine_dd(const int32_t* planes, long long pstride, int rows, int cols, const RecombPlan& rp,
+                         const int32_t* ellA, const int32_t* ellB, int scale8, double* Ch, double* Cl, long long ldc,
+                         cudaStream_t s);
+
+}  // namespace ozr

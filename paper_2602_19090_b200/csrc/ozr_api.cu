@@ -1,0 +1,797 @@
+// ozr_api.cu — the C ABI (include/ozr.h) and the host orchestration of one refinement sweep:
+// parameter choice (β, digit budgets, pair plans), kernel launches on the context stream, and the
+// few device->host reads of scalars the choices depend on. No math of the method runs on the host
+// except the choice of β (§4.1 lines 458-463 / §3.3) from O(n) statistics.
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "../../include/ozr.h"
+#include "kernels.h"
+#include "ozr_internal.h"
+
+using namespace ozr;
+
+namespace {
+
+constexpr double kU = 0x1p-53;
+constexpr int kBetaMin = 2, kBetaMax = 52;
+constexpr int kMaxDigits = 15;
+
+int64_t round16(int64_t x) { return (x + 15) / 16 * 16; }
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+};
+
+}  // namespace
+
+struct ozr_ctx_s {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  std::string err;
+  std::vector<DevBuf> bufs;
+  cudaEvent_t ev[8];
+  bool events = false;
+
+  // Workspace slot: grow-only device buffer.
+  template <typename T>
+  T* ws(int slot, size_t count) {
+    if (static_cast<int>(bufs.size()) <= slot) bufs.resize(slot + 1);
+    DevBuf& b = bufs[slot];
+    size_t need = count * sizeof(T);
+    if (need == 0) need = 16;
+    if (b.bytes < need) {
+      if (b.p) cudaFree(b.p);
+      b.p = nullptr;
+      b.bytes = 0;
+      if (cudaMalloc(&b.p, need) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+      }
+      b.bytes = need;
+    }
+    return static_cast<T*>(b.p);
+  }
+};
+
+namespace {
+
+enum Slot {
+  S_ADIG, S_AELL, S_W, S_X1, S_XDIG, S_XDIGT, S_G, S_SH, S_SL, S_RH, S_RL, S_PLANES, S_VH, S_VL, S_LAM, S_ER,
+  S_ERR, S_EMAX, S_RDIG, S_RELL, S_EP, S_NRM2, S_NU2, S_WNEXT, S_ZEROELL, S_TMP1, S_TMP2, S_BELL, S_AT, S_ONES
+};
+
+ozr_status fail(ozr_ctx c, ozr_status st, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  if (c) c->err = buf;
+  return st;
+}
+
+ozr_status cuda_check(ozr_ctx c, cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return OZR_OK;
+  cudaGetLastError();
+  return fail(c, e == cudaErrorMemoryAllocation ? OZR_ERR_NOMEM : OZR_ERR_CUDA, "%s: %s", what,
+              cudaGetErrorString(e));
+}
+
+#define OZR_CK(expr, what)                                  \
+  do {                                                      \
+    ozr_status st__ = cuda_check(ctx, (expr), (what));      \
+    if (st__ != OZR_OK) return st__;                        \
+  } while (0)
+#define OZR_ALLOC(ptr)                                                        \
+  do {                                                                        \
+    if (!(ptr)) return fail(ctx, OZR_ERR_NOMEM, "workspace allocation failed"); \
+  } while (0)
+
+// ---------------------------------------------------------------- pair / group planning (R7)
+struct Group {
+  int d;
+  std::vector<std::pair<int, int>> pairs;  // 1-based (s, t)
+};
+
+int64_t pair_cap(int64_t K) {
+  const int64_t c = (int64_t(2147483647)) / (K * 16384);
+  return c < 1 ? 1 : c;
+}
+
+std::vector<Group> plan_groups(int kA, int kB, int L, int64_t K) {
+  std::vector<Group> out;
+  const int64_t cap = pair_cap(K);
+  const int dmax = std::min(L, kA + kB);
+  for (int d = 2; d <= dmax; ++d) {
+    std::vector<std::pair<int, int>> pairs;
+    for (int s = 1; s <= kA; ++s) {
+      const int t = d - s;
+      if (t >= 1 && t <= kB) pairs.push_back({s, t});
+    }
+    for (size_t i = 0; i < pairs.size(); i += cap) {
+      Group g;
+      g.d = d;
+      for (size_t q = i; q < pairs.size() && q < i + cap; ++q) g.pairs.push_back(pairs[q]);
+      out.push_back(g);
+    }
+  }
+  return out;
+}
+
+int count_pairs(const std::vector<Group>& gs) {
+  int n = 0;
+  for (auto& g : gs) n += static_cast<int>(g.pairs.size());
+  return n;
+}
+
+bool make_tables(const std::vector<Group>& gs, int L, int64_t K, PairTable& pt, RecombPlan& rp) {
+  if (gs.empty() || static_cast<int>(gs.size()) > kMaxGroups || static_cast<int>(gs.size()) > kPlanGroups) return false;
+  if (count_pairs(gs) > kMaxPairs) return false;
+  memset(&pt, 0, sizeof pt);
+  memset(&rp, 0, sizeof rp);
+  int np = 0;
+  for (size_t g = 0; g < gs.size(); ++g) {
+    pt.first[g] = np;
+    pt.out_plane[g] = static_cast<int>(g);
+    pt.diag[g] = gs[g].d;
+    for (auto& st : gs[g].pairs) {
+      pt.s[np] = static_cast<unsigned char>(st.first - 1);
+      pt.t[np] = static_cast<unsigned char>(st.second - 1);
+      ++np;
+    }
+    rp.diag[g] = gs[g].d;
+  }
+  pt.first[gs.size()] = np;
+  pt.ngroups = static_cast<int>(gs.size());
+  rp.ngroups = pt.ngroups;
+  rp.L = L;
+  // chunks: T_c must fit an int128: bits(C) + log2(groups in chunk) + 1 + 8(d_last − d_first) ≤ 125
+  double cbits = std::log2(static_cast<double>(K) * 16384.0 * static_cast<double>(pair_cap(K)) + 1.0);
+  cbits = std::min(cbits, 31.0);
+  int nc = 0;
+  size_t g = 0;
+  while (g < gs.size()) {
+    if (nc >= kMaxChunks) return false;
+    rp.chunk_first[nc] = static_cast<int>(g);
+    const int d0 = gs[g].d;
+    size_t h = g + 1;
+    while (h < gs.size()) {
+      const double bits = cbits + std::ceil(std::log2(static_cast<double>(h - g + 1))) + 1.0 + 8.0 * (gs[h].d - d0);
+      if (bits > 125.0) break;
+      ++h;
+    }
+    ++nc;
+    g = h;
+  }
+  rp.chunk_first[nc] = static_cast<int>(gs.size());
+  rp.nchunks = nc;
+  return true;
+}
+
+// Smallest L such that dropping diagonals d > L costs ≤ tau (statistical √K bound, R8):
+// diagonal d contributes ≤ np(d) · 2√K · 2^14 · 2^{eA + eB + 4 − 8d} to every |c_ij|.
+int choose_L(int kA, int kB, int64_t K, int eA, int eB, double tau) {
+  for (int L = 2; L < kA + kB; ++L) {
+    double tail = 0.0;
+    for (int d = L + 1; d <= kA + kB; ++d) {
+      int np = 0;
+      for (int s = 1; s <= kA; ++s)
+        if (d - s >= 1 && d - s <= kB) ++np;
+      tail += np * 2.0 * std::sqrt(static_cast<double>(K)) * std::ldexp(1.0, 14 + eA + eB + 4 - 8 * d);
+    }
+    if (tail <= tau) return L;
+  }
+  return kA + kB;
+}
+
+// Digits needed so that the fixed-point LSB 2^{e − S_k} ≤ 2^{lsb_max} (k clamped to [1, 15]).
+int digits_for(int emax, int lsb_max) {
+  int k = 1;
+  while (k < kMaxDigits && (emax - (8 * (k - 1) + 6)) > lsb_max) ++k;
+  return k;
+}
+
+int kx_for_beta(int beta) {
+  int k = 1;
+  while (8 * (k - 1) + 6 < 53 - beta) ++k;
+  return k;
+}
+
+int ceil_log2_host(double v) {
+  if (v == 0.0) return 0;
+  int e;
+  const double m = std::frexp(v, &e);
+  return (m == 0.5) ? e - 1 : e;
+}
+
+// β of §4.1 (mode 0) / §3.3 (mode 1), evaluated in the operation order of DESIGN.md R3.
+int choose_beta(int64_t n, double delta_p, int mode, double xi, double gap, double maxlam, double ssum) {
+  const double c = (mode == 0) ? static_cast<double>(n) : (xi > 0 ? xi : static_cast<double>(n));
+  const double t = ((c * delta_p) * gap) / (maxlam * ssum);
+  const double Z = std::sqrt(t) / (0.75 * kU);
+  int e;
+  const double m = std::frexp(Z, &e);
+  if (mode == 0) return e - 1;         // ⌊log2 Z⌋
+  return (m == 0.5) ? e - 1 : e;       // ⌈log2 Z⌉
+}
+
+int alpha_dense(int64_t n, int beta) {
+  int c = 0;
+  while ((int64_t(1) << (2 * c)) < n) ++c;
+  return 53 - beta + c;
+}
+
+double gap_min_sorted(std::vector<double> l) {
+  std::sort(l.begin(), l.end());
+  double g = INFINITY;
+  for (size_t i = 1; i < l.size(); ++i) g = std::min(g, l[i] - l[i - 1]);
+  return g;
+}
+
+double sum_pow2_2c(const std::vector<double>& w) {
+  std::vector<int> cs;
+  for (double x : w)
+    if (x != 0.0) cs.push_back(ceil_log2_host(x));
+  std::sort(cs.begin(), cs.end());
+  double s = 0.0;
+  for (int c : cs) s = s + std::ldexp(1.0, 2 * c);
+  return s;
+}
+
+ozr_status run_gemm(ozr_ctx ctx, const DigitOperand& A, const DigitOperand& B, int M, int N, int K,
+                    const PairTable& pt, int32_t* planes, float* ms) {
+  if (ms) cudaEventRecord(ctx->ev[6], ctx->stream);
+  OZR_CK(launch_gemm_i8(A, B, M, N, K, pt, planes, static_cast<int64_t>(M) * N, M, ctx->stream), "slice GEMM");
+  if (ms) {
+    cudaEventRecord(ctx->ev[7], ctx->stream);
+    cudaEventSynchronize(ctx->ev[7]);
+    float t = 0;
+    cudaEventElapsedTime(&t, ctx->ev[6], ctx->ev[7]);
+    *ms += t;
+  }
+  return OZR_OK;
+}
+
+ozr_status read_err(ozr_ctx ctx, int* derr) {
+  int h = 0;
+  OZR_CK(cudaMemcpyAsync(&h, derr, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream), "D2H err");
+  OZR_CK(cudaStreamSynchronize(ctx->stream), "sync");
+  if (h & ERR_NONFINITE) return fail(ctx, OZR_ERR_NONFINITE, "non-finite value in an input matrix");
+  if (h & ERR_RANGE) return fail(ctx, OZR_ERR_RANGE, "exponent range exceeded in the digit split");
+  if (h & ERR_DEGENERATE)
+    return fail(ctx, OZR_ERR_DEGENERATE, "degenerate column or equal eigenvalue estimates (PAPER.md:333)");
+  return OZR_OK;
+}
+
+// ---------------------------------------------------------------- one sweep (internal)
+struct SweepState {
+  // A split (reused across sweeps of one ozr_refine_to_tol call)
+  const double* A = nullptr;
+  int64_t nA = 0;
+  int kA_split = 0;
+  int eA_max = 0;
+  bool have_w = false;  // wnext valid (column maxima of the current X)
+};
+
+ozr_status split_A(ozr_ctx ctx, const double* A, int64_t n, int64_t lda, int kA, SweepState& st) {
+  const int64_t ld = round16(n);
+  int8_t* adig = ctx->ws<int8_t>(S_ADIG, static_cast<size_t>(kA) * ld * n);
+  int32_t* aell = ctx->ws<int32_t>(S_AELL, n);
+  int* derr = ctx->ws<int>(S_ERR, 4);
+  OZR_ALLOC(adig);
+  OZR_ALLOC(aell);
+  OZR_ALLOC(derr);
+  OZR_CK(cudaMemsetAsync(derr, 0, sizeof(int), ctx->stream), "memset");
+  // A symmetric: its columns are its rows, so the COLWISE split of A is the row-wise split of the
+  // A operand of V = A·X̂ (K-major) and ℓ_i is its per-row exponent.
+  launch_split_fixed(A, nullptr, lda, static_cast<int>(n), static_cast<int>(n), kA, adig, ld, ld * n, aell, derr,
+                     ctx->stream);
+  OZR_CK(cudaGetLastError(), "split A");
+  ozr_status s = read_err(ctx, derr);
+  if (s != OZR_OK) return s;
+  std::vector<int32_t> h(n);
+  OZR_CK(cudaMemcpy(h.data(), aell, n * sizeof(int32_t), cudaMemcpyDeviceToHost), "D2H ell");
+  int em = -100000;
+  for (int64_t i = 0; i < n; ++i) em = std::max(em, h[i] + 8 * (kA - 1) + 6);
+  st.A = A;
+  st.nA = n;
+  st.kA_split = kA;
+  st.eA_max = em;
+  return OZR_OK;
+}
+
+ozr_status sweep(ozr_ctx ctx, const double* A, int64_t n, int64_t lda, double* X, int64_t ldx, double* lambda,
+                 const ozr_params& P, ozr_step_report& rep, SweepState& st) {
+  memset(&rep, 0, sizeof rep);
+  cudaStream_t s = ctx->stream;
+  const int N = static_cast<int>(n);
+  const int64_t ld = round16(n);
+  const int64_t nn = n * n;
+  cudaEventRecord(ctx->ev[0], s);
+  float gemm_ms = 0.f;
+  double ops = 0.0;
+
+  int* derr = ctx->ws<int>(S_ERR, 4);
+  int* demax = ctx->ws<int>(S_EMAX, 4);
+  double* w = ctx->ws<double>(S_W, n);
+  double* wnext = ctx->ws<double>(S_WNEXT, n);
+  OZR_ALLOC(derr);
+  OZR_ALLOC(demax);
+  OZR_ALLOC(w);
+  OZR_ALLOC(wnext);
+  OZR_CK(cudaMemsetAsync(derr, 0, sizeof(int), s), "memset");
+
+  // ---- a0: statistics and parameters
+  if (!st.have_w) {
+    launch_colmax(X, ldx, N, N, w, derr, s);
+    OZR_CK(cudaGetLastError(), "colmax");
+  } else {
+    OZR_CK(cudaMemcpyAsync(w, wnext, n * sizeof(double), cudaMemcpyDeviceToDevice, s), "copy w");
+  }
+  std::vector<double> hw(n), hlam(n);
+  OZR_CK(cudaMemcpyAsync(hw.data(), w, n * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H w");
+  OZR_CK(cudaMemcpyAsync(hlam.data(), lambda, n * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H lambda");
+  {
+    ozr_status e = read_err(ctx, derr);
+    if (e != OZR_OK) return e;
+  }
+  for (double x : hlam)
+    if (!std::isfinite(x)) return fail(ctx, OZR_ERR_NONFINITE, "non-finite lambda");
+  const double delta_p = P.delta / (P.theta > 0 ? P.theta : 1.0);
+  const double gap = gap_min_sorted(hlam);
+  double maxlam = 0.0;
+  for (double x : hlam) maxlam = std::max(maxlam, std::fabs(x));
+  if (!(gap > 0.0) && P.cluster_mode == 0)
+    return fail(ctx, OZR_ERR_DEGENERATE, "equal eigenvalue estimates (gap = 0) with the cluster branch off");
+  const double ssum = sum_pow2_2c(hw);
+  if (ssum == 0.0 || maxlam == 0.0) return fail(ctx, OZR_ERR_DEGENERATE, "zero X or zero spectrum");
+  int beta_raw = (P.beta_override > 0) ? P.beta_override
+                                       : choose_beta(n, delta_p, P.beta_mode, P.xi, gap, maxlam, ssum);
+  int beta = std::min(std::max(beta_raw, kBetaMin), kBetaMax);
+  if (!P.truncate) beta = kBetaMin;
+  const int kx = kx_for_beta(beta);
+  int cmax = -100000;
+  for (double x : hw)
+    if (x != 0.0) cmax = std::max(cmax, ceil_log2_host(x));
+  rep.beta = beta;
+  rep.beta_raw = beta_raw;
+  rep.alpha = alpha_dense(n, beta);
+  rep.kX = kx;
+  rep.gap_min = gap;
+  rep.max_abs_lambda = maxlam;
+
+  // ---- A split (once per refine_to_tol call)
+  if (st.A != A || st.nA != n) {
+    ozr_status e = split_A(ctx, A, n, lda, P.kA_split, st);
+    if (e != OZR_OK) return e;
+  }
+  const double tauV = P.theta_V * delta_p * gap;
+  int LV = P.L_V > 0 ? P.L_V : choose_L(st.kA_split, kx, n, st.eA_max, cmax, tauV);
+  LV = std::min(LV, st.kA_split + kx);
+  const int kA = std::min(st.kA_split, LV - 1);
+  rep.kA = kA;
+  rep.L_V = LV;
+
+  // ---- a2: X̂ → X̂^(1) + digits + r (exact)
+  double* X1 = ctx->ws<double>(S_X1, nn);
+  int8_t* xdig = ctx->ws<int8_t>(S_XDIG, static_cast<size_t>(7) * ld * n);
+  int8_t* xdigT = ctx->ws<int8_t>(S_XDIGT, static_cast<size_t>(7) * ld * n);
+  int32_t* g = ctx->ws<int32_t>(S_G, n);
+  double* sh = ctx->ws<double>(S_SH, n);
+  double* sl = ctx->ws<double>(S_SL, n);
+  double* rh = ctx->ws<double>(S_RH, n);
+  double* rl = ctx->ws<double>(S_RL, n);
+  int32_t* zell = ctx->ws<int32_t>(S_ZEROELL, n);
+  OZR_ALLOC(X1); OZR_ALLOC(xdig); OZR_ALLOC(xdigT); OZR_ALLOC(g); OZR_ALLOC(sh); OZR_ALLOC(sl); OZR_ALLOC(rh);
+  OZR_ALLOC(rl); OZR_ALLOC(zell);
+  launch_x1_split(X, ldx, N, N, beta, kx, w, X1, n, xdig, ld, ld * n, g, sh, sl, rh, rl, derr, s);
+  OZR_CK(cudaGetLastError(), "x1 split");
+  launch_transpose_i8(xdig, ld, ld * n, xdigT, ld, ld * n, N, N, kx, s);
+  OZR_CK(cudaGetLastError(), "transpose digits");
+  OZR_CK(cudaMemsetAsync(zell, 0, n * sizeof(int32_t), s), "memset");
+
+  // ---- a3: P1  V = A·X̂^(1)  (Alg. 1 line 1, eq. mat_mul)
+  std::vector<Group> gV = plan_groups(kA, kx, LV, n);
+  PairTable pt;
+  RecombPlan rp;
+  if (!make_tables(gV, LV, n, pt, rp)) return fail(ctx, OZR_ERR_RANGE, "V plan too large");
+  size_t maxG = gV.size();
+  int32_t* planes = ctx->ws<int32_t>(S_PLANES, maxG * nn);
+  OZR_ALLOC(planes);
+  DigitOperand opA{reinterpret_cast<const int8_t*>(ctx->bufs[S_ADIG].p), ld, ld * n, st.kA_split};
+  DigitOperand opX{xdig, ld, ld * n, kx};
+  {
+    ozr_status e = run_gemm(ctx, opA, opX, N, N, N, pt, planes, &gemm_ms);
+    if (e != OZR_OK) return e;
+  }
+  rep.pairs_V = count_pairs(gV);
+  ops += 2.0 * n * n * n * rep.pairs_V;
+
+  // ---- a4-a6: recombine V, λ̂, Res, column maxima
+  double* Vh = ctx->ws<double>(S_VH, nn);
+  double* Vl = ctx->ws<double>(S_VL, nn);
+  double* lam = ctx->ws<double>(S_LAM, n);
+  int32_t* eR = ctx->ws<int32_t>(S_ER, n);
+  OZR_ALLOC(Vh); OZR_ALLOC(Vl); OZR_ALLOC(lam); OZR_ALLOC(eR);
+  const int intmin = -(1 << 30);
+  OZR_CK(cudaMemcpyAsync(demax, &intmin, sizeof(int), cudaMemcpyHostToDevice, s), "H2D");
+  launch_recombine_V(planes, nn, N, N, rp, reinterpret_cast<const int32_t*>(ctx->bufs[S_AELL].p), g,
+                     8 * (st.kA_split + kx - LV), X1, n, sh, sl, Vh, Vl, n, lam, eR, demax, s);
+  OZR_CK(cudaGetLastError(), "recombine V");
+  int eRmax = 0;
+  std::vector<double> hlam_new(n);
+  OZR_CK(cudaMemcpyAsync(&eRmax, demax, sizeof(int), cudaMemcpyDeviceToHost, s), "D2H");
+  OZR_CK(cudaMemcpyAsync(hlam_new.data(), lam, n * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H");
+  {
+    ozr_status e = read_err(ctx, derr);
+    if (e != OZR_OK) return e;
+  }
+  const double gap_new = gap_min_sorted(hlam_new);
+  if (!(gap_new > 0.0) && P.cluster_mode == 0)
+    return fail(ctx, OZR_ERR_DEGENERATE, "equal Rayleigh quotients (gap = 0) with the cluster branch off");
+  if (eRmax == intmin) eRmax = -1074;
+
+  // ---- a6: Res digits (k_R from the accuracy W needs, R8)
+  const double gapW = std::min(gap, gap_new);
+  const double tauW = P.theta_W * delta_p * gapW;
+  const int kR = digits_for(eRmax, static_cast<int>(std::floor(std::log2(tauW / 2.0))));
+  int8_t* rdig = ctx->ws<int8_t>(S_RDIG, static_cast<size_t>(kMaxDigits) * ld * n);
+  int32_t* rell = ctx->ws<int32_t>(S_RELL, n);
+  OZR_ALLOC(rdig); OZR_ALLOC(rell);
+  launch_split_fixed(Vh, Vl, n, N, N, kR, rdig, ld, ld * n, rell, derr, s);
+  OZR_CK(cudaGetLastError(), "split Res");
+
+  // ---- a7: P3  W = X̂^(1)ᵀ Res  (Alg. 1 line 4)
+  int LW = P.L_W > 0 ? P.L_W : choose_L(kx, kR, n, cmax, eRmax, tauW / 2.0);
+  LW = std::min(LW, kx + kR);
+  std::vector<Group> gW = plan_groups(kx, kR, LW, n);
+  if (!make_tables(gW, LW, n, pt, rp)) return fail(ctx, OZR_ERR_RANGE, "W plan too large");
+  if (gW.size() > maxG) {
+    maxG = gW.size();
+    planes = ctx->ws<int32_t>(S_PLANES, maxG * nn);
+    OZR_ALLOC(planes);
+  }
+  DigitOperand opR{rdig, ld, ld * n, kR};
+  {
+    ozr_status e = run_gemm(ctx, opX, opR, N, N, N, pt, planes, &gemm_ms);
+    if (e != OZR_OK) return e;
+  }
+  rep.kR = kR;
+  rep.L_W = LW;
+  rep.pairs_W = count_pairs(gW);
+  ops += 2.0 * n * n * n * rep.pairs_W;
+
+  // ---- a8: Ẽ (Alg. 1 line 5), Ẽ' = diag(2^g) Ẽ
+  double* Ep = ctx->ws<double>(S_EP, nn);
+  double* nrm2 = ctx->ws<double>(S_NRM2, n);
+  OZR_ALLOC(Ep); OZR_ALLOC(nrm2);
+  OZR_CK(cudaMemcpyAsync(demax, &intmin, sizeof(int), cudaMemcpyHostToDevice, s), "H2D");
+  launch_recombine_E(planes, nn, N, N, rp, g, rell, 8 * (kx + kR - LW), rh, lam, g, 0, Ep, n, nrm2, demax, derr, s);
+  OZR_CK(cudaGetLastError(), "recombine E");
+  int eEmax = 0;
+  OZR_CK(cudaMemcpyAsync(&eEmax, demax, sizeof(int), cudaMemcpyDeviceToHost, s), "D2H");
+  {
+    ozr_status e = read_err(ctx, derr);
+    if (e != OZR_OK) return e;
+  }
+  if (eEmax == intmin) eEmax = -1074;
+  int gmin = 100000;
+  {
+    std::vector<int32_t> hg(n);
+    OZR_CK(cudaMemcpy(hg.data(), g, n * sizeof(int32_t), cudaMemcpyDeviceToHost), "D2H g");
+    for (int x : hg) gmin = std::min(gmin, x);
+  }
+
+  // ---- a9: P4  U = X̂^(1) Ẽ = Q Ẽ' ; X̂ ← RN(X̂^(1) + U)  (Alg. 1 line 6)
+  const double tauU = P.theta_U * delta_p;
+  const int kE = digits_for(eEmax, static_cast<int>(std::floor(std::log2(tauU / 2.0))) + gmin);
+  launch_split_fixed(Ep, nullptr, n, N, N, kE, rdig, ld, ld * n, rell, derr, s);
+  OZR_CK(cudaGetLastError(), "split E");
+  const int SX = 8 * (kx - 1) + 6;
+  int LU = P.L_U > 0 ? P.L_U : choose_L(kx, kE, n, SX, eEmax, tauU / 2.0);
+  LU = std::min(LU, kx + kE);
+  std::vector<Group> gU = plan_groups(kx, kE, LU, n);
+  if (!make_tables(gU, LU, n, pt, rp)) return fail(ctx, OZR_ERR_RANGE, "U plan too large");
+  if (gU.size() > maxG) {
+    maxG = gU.size();
+    planes = ctx->ws<int32_t>(S_PLANES, maxG * nn);
+    OZR_ALLOC(planes);
+  }
+  DigitOperand opQ{xdigT, ld, ld * n, kx};
+  DigitOperand opE{rdig, ld, ld * n, kE};
+  {
+    ozr_status e = run_gemm(ctx, opQ, opE, N, N, N, pt, planes, &gemm_ms);
+    if (e != OZR_OK) return e;
+  }
+  rep.kE = kE;
+  rep.L_U = LU;
+  rep.pairs_U = count_pairs(gU);
+  ops += 2.0 * n * n * n * rep.pairs_U;
+  double* nu2 = ctx->ws<double>(S_NU2, n);
+  OZR_ALLOC(nu2);
+  launch_final(planes, nn, N, N, rp, rell, 8 * (kx + kE - LU), X1, n, X, ldx, nu2, wnext, s);
+  OZR_CK(cudaGetLastError(), "final update");
+  OZR_CK(cudaMemcpyAsync(lambda, lam, n * sizeof(double), cudaMemcpyDeviceToDevice, s), "copy lambda");
+  cudaEventRecord(ctx->ev[1], s);
+  std::vector<double> hnu(n), hnrm(n);
+  OZR_CK(cudaMemcpyAsync(hnu.data(), nu2, n * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H");
+  OZR_CK(cudaMemcpyAsync(hnrm.data(), nrm2, n * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H");
+  {
+    ozr_status e = read_err(ctx, derr);
+    if (e != OZR_OK) return e;
+  }
+  double nu = 0.0, ne = 0.0;
+  for (int64_t j = 0; j < n; ++j) {
+    nu += hnu[j];
+    ne += hnrm[j];
+  }
+  float tot = 0.f;
+  cudaEventElapsedTime(&tot, ctx->ev[0], ctx->ev[1]);
+  st.have_w = true;
+  rep.net_update = std::sqrt(nu);
+  rep.normE_fro = std::sqrt(ne);
+  double maxlam_new = 0.0;
+  for (double x : hlam_new) maxlam_new = std::max(maxlam_new, std::fabs(x));
+  rep.predicted_error = rep.net_update * rep.net_update * maxlam_new / (static_cast<double>(n) * gap_new);
+  rep.ms_total = tot;
+  rep.ms_gemm = gemm_ms;
+  rep.int8_ops = ops;
+  return OZR_OK;
+}
+
+ozr_status check_ctx(ozr_ctx ctx) {
+  if (!ctx) return OZR_ERR_ARG;
+  OZR_CK(cudaSetDevice(ctx->device), "cudaSetDevice");
+  return OZR_OK;
+}
+
+}  // namespace
+
+// ================================================================ C ABI
+extern "C" {
+
+const char* ozr_version(void) { return "ozr 0.1 (sm_100a, tcgen05 kind::i8)"; }
+
+ozr_status ozr_create(ozr_ctx* out, int device, void* stream, int64_t n_max) {
+  (void)n_max;
+  if (!out) return OZR_ERR_ARG;
+  *out = nullptr;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) {
+    cudaGetLastError();
+    return OZR_ERR_CUDA;
+  }
+  if (cudaSetDevice(device) != cudaSuccess) return OZR_ERR_CUDA;
+  ozr_ctx c = new ozr_ctx_s();
+  c->device = device;
+  c->stream = static_cast<cudaStream_t>(stream);
+  for (int i = 0; i < 8; ++i) cudaEventCreate(&c->ev[i]);
+  c->events = true;
+  *out = c;
+  return OZR_OK;
+}
+
+void ozr_destroy(ozr_ctx ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  for (auto& b : ctx->bufs)
+    if (b.p) cudaFree(b.p);
+  if (ctx->events)
+    for (int i = 0; i < 8; ++i) cudaEventDestroy(ctx->ev[i]);
+  delete ctx;
+}
+
+const char* ozr_last_error(ozr_ctx ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+void ozr_params_default(ozr_params* p) {
+  if (!p) return;
+  memset(p, 0, sizeof *p);
+  p->delta = 1e-12;
+  p->theta = 1.0;
+  p->beta_mode = 0;
+  p->xi = 0.0;
+  p->beta_override = 0;
+  p->truncate = 1;
+  p->max_sweeps = 6;
+  p->kA_split = 15;
+  p->theta_V = 1.0 / 16;
+  p->theta_W = 1.0 / 16;
+  p->theta_U = 1.0 / 16;
+  p->cluster_mode = 0;
+}
+
+ozr_status ozr_split(ozr_ctx ctx, const double* M, const double* M_lo, int64_t rows, int64_t cols, int64_t ldm,
+                     int axis, int mode, int k_or_beta, int8_t* digits, int64_t ldd, int64_t plane_stride,
+                     int32_t* lsb_exp, double* x1_out, int64_t ldx1, int* k_out) {
+  ozr_status st = check_ctx(ctx);
+  if (st != OZR_OK) return st;
+  if (!M || !digits || !lsb_exp || rows <= 0 || cols <= 0 || ldm < rows || (ldd % 16) || (plane_stride % 16))
+    return fail(ctx, OZR_ERR_ARG, "ozr_split: bad argument");
+  if (rows > (int64_t(1) << 31) || cols > (int64_t(1) << 31)) return fail(ctx, OZR_ERR_ARG, "ozr_split: too large");
+  cudaStream_t s = ctx->stream;
+  int* derr = ctx->ws<int>(S_ERR, 4);
+  OZR_ALLOC(derr);
+  OZR_CK(cudaMemsetAsync(derr, 0, sizeof(int), s), "memset");
+  if (mode == OZR_SPLIT_X1) {
+    if (axis != OZR_COLWISE || M_lo) return fail(ctx, OZR_ERR_ARG, "ozr_split: X1 mode is COLWISE, fp64 only");
+    const int beta = k_or_beta;
+    if (beta < kBetaMin || beta > kBetaMax) return fail(ctx, OZR_ERR_RANGE, "ozr_split: beta must be in [2, 52]");
+    if (ldd < rows || plane_stride < ldd * cols) return fail(ctx, OZR_ERR_ARG, "ozr_split: digit layout too small");
+    const int kx = kx_for_beta(beta);
+    double* w = ctx->ws<double>(S_W, cols);
+    double* X1 = x1_out ? x1_out : ctx->ws<double>(S_TMP1, rows * cols);
+    const int64_t ld1 = x1_out ? ldx1 : rows;
+    double* tmp = ctx->ws<double>(S_TMP2, 4 * cols);
+    OZR_ALLOC(w); OZR_ALLOC(X1); OZR_ALLOC(tmp);
+    if (x1_out && ldx1 < rows) return fail(ctx, OZR_ERR_ARG, "ozr_split: ldx1 < rows");
+    launch_colmax(M, ldm, static_cast<int>(rows), static_cast<int>(cols), w, derr, s);
+    launch_x1_split(M, ldm, static_cast<int>(rows), static_cast<int>(cols), beta, kx, w, X1, ld1, digits, ldd,
+                    plane_stride, lsb_exp, tmp, tmp + cols, tmp + 2 * cols, tmp + 3 * cols, derr, s);
+    OZR_CK(cudaGetLastError(), "ozr_split");
+    if (k_out) *k_out = kx;
+    // a zero column is legal for a split (ERR_DEGENERATE only matters to the refinement)
+    int h = 0;
+    OZR_CK(cudaMemcpyAsync(&h, derr, sizeof(int), cudaMemcpyDeviceToHost, s), "D2H");
+    OZR_CK(cudaStreamSynchronize(s), "sync");
+    if (h & ERR_NONFINITE) return fail(ctx, OZR_ERR_NONFINITE, "non-finite value in M");
+    if (h & ERR_RANGE) return fail(ctx, OZR_ERR_RANGE, "exponent range exceeded");
+    return OZR_OK;
+  }
+  if (mode != OZR_SPLIT_FIXED) return fail(ctx, OZR_ERR_ARG, "ozr_split: bad mode");
+  const int k = k_or_beta;
+  if (k < 1 || k > kMaxDigits) return fail(ctx, OZR_ERR_RANGE, "ozr_split: k must be in [1, 15]");
+  const double* src = M;
+  const double* srcl = M_lo;
+  int64_t r = rows, c = cols, lds = ldm;
+  if (axis == OZR_ROWWISE) {
+    double* T = ctx->ws<double>(S_TMP1, rows * cols);
+    OZR_ALLOC(T);
+    launch_transpose_f64(M, ldm, T, cols, static_cast<int>(rows), static_cast<int>(cols), s);
+    src = T;
+    if (M_lo) {
+      double* Tl = ctx->ws<double>(S_TMP2, rows * cols);
+      OZR_ALLOC(Tl);
+      launch_transpose_f64(M_lo, ldm, Tl, cols, static_cast<int>(rows), static_cast<int>(cols), s);
+      srcl = Tl;
+    }
+    r = cols;
+    c = rows;
+    lds = cols;
+  } else if (axis != OZR_COLWISE) {
+    return fail(ctx, OZR_ERR_ARG, "ozr_split: bad axis");
+  }
+  if (ldd < r || plane_stride < ldd * c) return fail(ctx, OZR_ERR_ARG, "ozr_split: digit layout too small");
+  launch_split_fixed(src, srcl, lds, static_cast<int>(r), static_cast<int>(c), k, digits, ldd, plane_stride, lsb_exp,
+                     derr, s);
+  OZR_CK(cudaGetLastError(), "ozr_split");
+  if (k_out) *k_out = k;
+  return read_err(ctx, derr);
+}
+
+ozr_status ozr_gemm_plan(int64_t k, int kA, int kB, int L, int* ngroups, int* group_diag, int* group_npairs,
+                         int max_groups) {
+  if (k <= 0 || kA < 1 || kB < 1 || kA > kMaxDigits || kB > kMaxDigits) return OZR_ERR_RANGE;
+  if (L <= 0) L = kA + kB;
+  std::vector<Group> gs = plan_groups(kA, kB, L, k);
+  if (ngroups) *ngroups = static_cast<int>(gs.size());
+  for (int i = 0; i < static_cast<int>(gs.size()) && i < max_groups; ++i) {
+    if (group_diag) group_diag[i] = gs[i].d;
+    if (group_npairs) group_npairs[i] = static_cast<int>(gs[i].pairs.size());
+  }
+  return OZR_OK;
+}
+
+ozr_status ozr_gemm(ozr_ctx ctx, int64_t m, int64_t n, int64_t k, const double* A, int64_t lda, const double* B,
+                    int64_t ldb, int kA, int kB, int L, double* C_hi, double* C_lo, int64_t ldc, int32_t* planes_out,
+                    int64_t plane_stride, int* ngroups_out) {
+  ozr_status st = check_ctx(ctx);
+  if (st != OZR_OK) return st;
+  if (!A || !B || !C_hi || m <= 0 || n <= 0 || k <= 0 || lda < m || ldb < k || ldc < m)
+    return fail(ctx, OZR_ERR_ARG, "ozr_gemm: bad argument");
+  if (kA < 1 || kB < 1 || kA > kMaxDigits || kB > kMaxDigits) return fail(ctx, OZR_ERR_RANGE, "ozr_gemm: kA/kB");
+  if (k * 16384 > 2147483647LL) return fail(ctx, OZR_ERR_RANGE, "ozr_gemm: k too large for exact int32 slices");
+  if (L <= 0) L = kA + kB;
+  cudaStream_t s = ctx->stream;
+  const int64_t ldk = round16(k);
+  int8_t* da = ctx->ws<int8_t>(S_RDIG, static_cast<size_t>(kA) * ldk * m);
+  int8_t* db = ctx->ws<int8_t>(S_XDIG, static_cast<size_t>(kB) * ldk * n);
+  int32_t* ea = ctx->ws<int32_t>(S_AELL, m);
+  int32_t* eb = ctx->ws<int32_t>(S_BELL, n);
+  OZR_ALLOC(da); OZR_ALLOC(db); OZR_ALLOC(ea); OZR_ALLOC(eb);
+  st = ozr_split(ctx, A, nullptr, m, k, lda, OZR_ROWWISE, OZR_SPLIT_FIXED, kA, da, ldk, ldk * m, ea, nullptr, 0,
+                 nullptr);
+  if (st != OZR_OK) return st;
+  st = ozr_split(ctx, B, nullptr, k, n, ldb, OZR_COLWISE, OZR_SPLIT_FIXED, kB, db, ldk, ldk * n, eb, nullptr, 0,
+                 nullptr);
+  if (st != OZR_OK) return st;
+  std::vector<Group> gs = plan_groups(kA, kB, L, k);
+  PairTable pt;
+  RecombPlan rp;
+  if (!make_tables(gs, L, k, pt, rp)) return fail(ctx, OZR_ERR_RANGE, "ozr_gemm: plan too large");
+  if (ngroups_out) *ngroups_out = pt.ngroups;
+  const int64_t mn = m * n;
+  int32_t* planes = planes_out;
+  int64_t ps = plane_stride;
+  if (!planes) {
+    planes = ctx->ws<int32_t>(S_PLANES, static_cast<size_t>(pt.ngroups) * mn);
+    OZR_ALLOC(planes);
+    ps = mn;
+  } else if (plane_stride < mn) {
+    return fail(ctx, OZR_ERR_ARG, "ozr_gemm: plane_stride < m*n");
+  }
+  DigitOperand oa{da, ldk, ldk * m, kA}, ob{db, ldk, ldk * n, kB};
+  OZR_CK(launch_gemm_i8(oa, ob, static_cast<int>(m), static_cast<int>(n), static_cast<int>(k), pt, planes, ps, m, s),
+         "slice GEMM");
+  launch_recombine_dd(planes, ps, static_cast<int>(m), static_cast<int>(n), rp, ea, eb, 8 * (kA + kB - L), C_hi, C_lo,
+                      ldc, s);
+  OZR_CK(cudaGetLastError(), "recombine");
+  return OZR_OK;
+}
+
+ozr_status ozr_refine_step(ozr_ctx ctx, const double* A, int64_t n, int64_t lda, double* X, int64_t ldx,
+                           double* lambda, const ozr_params* params, ozr_step_report* report) {
+  ozr_status st = check_ctx(ctx);
+  if (st != OZR_OK) return st;
+  if (!A || !X || !lambda || !params || n < 2 || lda < n || ldx < n)
+    return fail(ctx, OZR_ERR_ARG, "ozr_refine_step: bad argument");
+  if (n > 65536) return fail(ctx, OZR_ERR_ARG, "ozr_refine_step: n too large");
+  if (!(params->delta > kU)) return fail(ctx, OZR_ERR_RANGE, "delta must exceed u = 2^-53");
+  if (params->kA_split < 2 || params->kA_split > kMaxDigits) return fail(ctx, OZR_ERR_RANGE, "kA_split");
+  SweepState ss;
+  ozr_step_report rep;
+  st = sweep(ctx, A, n, lda, X, ldx, lambda, *params, rep, ss);
+  rep.sweep = 1;
+  if (report) *report = rep;
+  return st;
+}
+
+ozr_status ozr_refine_to_tol(ozr_ctx ctx, const double* A, int64_t n, int64_t lda, double* X, int64_t ldx,
+                             double* lambda, const ozr_params* params, ozr_step_report* history, int max_hist,
+                             int* sweeps_done) {
+  ozr_status st = check_ctx(ctx);
+  if (st != OZR_OK) return st;
+  if (!A || !X || !lambda || !params || n < 2 || lda < n || ldx < n)
+    return fail(ctx, OZR_ERR_ARG, "ozr_refine_to_tol: bad argument");
+  if (!(params->delta > kU)) return fail(ctx, OZR_ERR_RANGE, "delta must exceed u = 2^-53");
+  if (params->kA_split < 2 || params->kA_split > kMaxDigits) return fail(ctx, OZR_ERR_RANGE, "kA_split");
+  SweepState ss;
+  double nu_prev = -1.0;
+  int done = 0;
+  ozr_status result = OZR_ERR_NOT_CONVERGED;
+  const int maxs = params->max_sweeps > 0 ? params->max_sweeps : 6;
+  for (int k = 0; k < maxs; ++k) {
+    ozr_step_report rep;
+    st = sweep(ctx, A, n, lda, X, ldx, lambda, *params, rep, ss);
+    rep.sweep = k + 1;
+    if (st != OZR_OK) {
+      if (sweeps_done) *sweeps_done = done;
+      return st;
+    }
+    if (history && k < max_hist) history[k] = rep;
+    done = k + 1;
+    if (rep.net_update <= params->delta || rep.predicted_error <= params->delta) {
+      result = OZR_OK;
+      break;
+    }
+    if (nu_prev >= 0.0 && rep.net_update > nu_prev / 2) {
+      fail(ctx, OZR_ERR_NOT_CONVERGED, "stagnation: net update %.3e > previous %.3e / 2", rep.net_update, nu_prev);
+      break;
+    }
+    nu_prev = rep.net_update;
+  }
+  if (result != OZR_OK && ctx->err.empty()) fail(ctx, OZR_ERR_NOT_CONVERGED, "max_sweeps reached");
+  if (sweeps_done) *sweeps_done = done;
+  return result;
+}
+
+}  // extern "C"

@@ -1,0 +1,81 @@
+"""GPU parity of the refinement sweep (Algorithm 1, one-sided product §3.3, β §4.1)
+against the oracle sweep, and the forward error of ozr_refine_to_tol against the oracle's reference
+eigenvectors. Bars (BASELINE.json north star): X̂ and D̂ within 1e-13 (D̂ relative to ‖A‖), the
+same β as the oracle, forward error at or below the prescribed target."""
+import numpy as np
+import pytest
+
+from gpu_util import to_dev, to_np, vec_dev
+from oracle import refine as orf
+import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+
+def _gpu_sweep(ctx, A, X, lam, delta, **kw):
+    import paper_2602_19090_b200 as ozr
+    Xd, ld = to_dev(X), vec_dev(lam)
+    rep = ozr.ozr_refine_step(ctx, to_dev(A), Xd, ld, ozr.default_params(delta=delta, **kw))
+    return to_np(Xd), to_np(ld), rep
+
+
+CASES = [("c1", 100, 1e-15, "fp64"), ("c1", 100, 1e-10, "fp64"), ("c1", 100, 1e-6, "fp64"),
+         ("c2", 256, 1e-14, "fp64"), ("c2", 1024, 1e-14, "fp64"), ("c3", 512, 1e-12, "fp64")]
+
+
+def _case(cfg, n, start):
+    c = dict(W.CONFIGS[cfg])
+    A, _ = W.make_matrix(n, c["kind"], c["cnd"], c["seed"])
+    lam0, X0 = W.initial_eig(A, start)
+    return A, lam0, X0
+
+
+@pytest.mark.parametrize("cfg,n,delta,start", CASES)
+def test_sweep_matches_oracle(ctx, cfg, n, delta, start):
+    """North-star bar: |ΔX̂| ≤ 1e-13 and |ΔD̂| ≤ 1e-13·‖A‖ against the exact-product oracle sweep. The
+    product budgets are tightened (θ·δ ≤ 1e-15) so the digit truncations sit below the bar for any δ."""
+    A, lam0, X0 = _case(cfg, n, start)
+    th = min(1.0 / 16, 1e-15 / delta)
+    Xg, lg, rep = _gpu_sweep(ctx, A, X0, lam0, delta, theta_V=th, theta_W=th, theta_U=th)
+    Xo, lo, info = orf.sweep(A, X0, lam0, delta)
+    assert rep["beta"] == info["beta"]
+    dX = np.max(np.abs(Xg - Xo))
+    dl = np.max(np.abs(lg - lo)) / np.max(np.abs(lam0))
+    assert dX <= 1e-13, dX
+    assert dl <= 1e-13, dl
+
+
+@pytest.mark.parametrize("cfg,n,delta,start", CASES)
+def test_sweep_default_budgets_within_delta(ctx, cfg, n, delta, start):
+    """With the default budgets (θ = 1/16 of δ'·gap / δ', R8) the sweep stays within δ/4 of
+    the exact-product sweep: the digit truncation is a deliberate, bounded part of the method."""
+    A, lam0, X0 = _case(cfg, n, start)
+    Xg, lg, rep = _gpu_sweep(ctx, A, X0, lam0, delta)
+    Xo, lo, info = orf.sweep(A, X0, lam0, delta)
+    assert rep["beta"] == info["beta"]
+    assert np.max(np.abs(Xg - Xo)) <= delta / 4
+
+
+def test_refine_to_tol_c1_forward_error(ctx):
+    import paper_2602_19090_b200 as ozr
+    A, lam0, X0, cfg = W.make_config("c1")
+    Xh, Xl, lh, ll, _ = orf.reference_eigvecs(A, X0, lam0)
+    for delta in (1e-8, 1e-12, 1e-15):
+        Xd, ld = to_dev(X0), vec_dev(lam0)
+        st, hist = ozr.ozr_refine_to_tol(ctx, to_dev(A), Xd, ld, ozr.default_params(delta=delta))
+        fe = orf.forward_error(Xh, Xl, to_np(Xd))
+        assert st == 0, hist
+        assert fe <= 2 * delta, (delta, fe, hist)
+        assert len(hist) <= 3
+
+
+def test_refine_step_errors(ctx):
+    import paper_2602_19090_b200 as ozr
+    A = np.diag([1.0, 2.0, 3.0, 4.0])
+    X = np.eye(4)
+    with pytest.raises(ozr.OzrError) as e:   # δ ≤ u
+        _gpu_sweep(ctx, A, X, np.array([1.0, 2, 3, 4]), 1e-17)
+    assert e.value.status == 3
+    with pytest.raises(ozr.OzrError) as e:   # equal eigenvalue estimates, cluster branch off
+        _gpu_sweep(ctx, A, X, np.array([1.0, 1.0, 3, 4]), 1e-10)
+    assert e.value.status == 4

@@ -1,0 +1,124 @@
+"""workloads — seeded synthetic inputs shared by the tests, the bench and the oracle.
+
+Holds NONE of the method's arithmetic (no splitting, no products beyond forming the test matrix,
+no refinement): it only builds A = Q·diag(λ)·Qᵀ like the paper's test matrices and the initial
+approximation X̂₀ from an LAPACK eigensolver, exactly as BASELINE.json's configs describe them.
+
+PAPER.md:447 `gallery('randsvd',n,-cnd,3,n-1,n-1,1)`: mode 3 = geometric singular values
+σ_i = cnd^{-(i-1)/(n-1)}, negative cnd = symmetric positive definite, full bandwidth. MATLAB's PRNG
+stream cannot be reproduced, so Q is a Haar orthogonal matrix from numpy's PCG64 (QR of a seeded
+N(0,1) matrix, columns multiplied by sign(diag R)); A is formed in fp64 and symmetrised as
+(A + Aᵀ)/2. The reference solution is always the eigensystem of the STORED A.
+"""
+import numpy as np
+
+# BASELINE.json configs (c1..c5): n, spectrum, start precision, target δ
+CONFIGS = {
+    "c1": dict(n=100, kind="geometric", cnd=1e8, start="fp64", delta=1e-15, seed=1001),
+    "c2": dict(n=1024, kind="geometric", cnd=1e12, start="fp32", delta=1e-14, seed=1002),
+    "c3": dict(n=4096, kind="clustered", cnd=None, start="fp64", delta=1e-12, seed=1003),
+    "c4": dict(n=8192, kind="geometric", cnd=1e14, start="fp32", delta=1e-10, seed=1004),
+    "c5": dict(n=16384, kind="geometric", cnd=1e10, start="fp64", delta=1e-15, seed=1005),
+    # c4': the paper's own Fig. 4(h-j) setting at n = 8192 (cnd 1e10, FP64 eig start, δ = 1e-12)
+    "c4p": dict(n=8192, kind="geometric", cnd=1e10, start="fp64", delta=1e-12, seed=1014),
+}
+
+
+def haar(n, rng):
+    """Haar orthogonal Q: QR of N(0,1)^{n×n}, columns times sign(diag R)."""
+    G = rng.standard_normal((n, n))
+    Q, R = np.linalg.qr(G)
+    return Q * np.sign(np.diag(R))[None, :]
+
+
+def geometric_spectrum(n, cnd):
+    """λ_i = cnd^{-(i-1)/(n-1)}, i = 1..n (randsvd mode 3): λ_max = 1, λ_min = 1/cnd."""
+    i = np.arange(n, dtype=np.float64)
+    return cnd ** (-i / max(n - 1, 1))
+
+
+def clustered_spectrum(n, rng, nclusters=64, csize=8, sep=1e-10):
+    """BASELINE.json c3: λ uniform in [−1, 1] with `nclusters` clusters of `csize` eigenvalues
+    separated by `sep`: n − nclusters·csize singletons plus nclusters anchors c drawn U[−1, 1], each
+    anchor expanded to {c + m·sep, m = 0..csize−1}."""
+    nsingle = n - nclusters * csize
+    draws = rng.uniform(-1.0, 1.0, nsingle + nclusters)
+    anchors = draws[:nclusters]
+    lam = list(draws[nclusters:])
+    for c in anchors:
+        lam.extend(c + sep * np.arange(csize))
+    return np.sort(np.array(lam))
+
+
+def make_matrix(n, kind="geometric", cnd=1e10, seed=0):
+    """A = fl(Q diag(λ) Qᵀ), symmetrised. Returns (A, λ_design)."""
+    rng = np.random.default_rng(seed)
+    if kind == "geometric":
+        lam = geometric_spectrum(n, cnd)
+    elif kind == "clustered":
+        lam = clustered_spectrum(n, rng)
+    else:
+        raise ValueError(kind)
+    Q = haar(n, rng)
+    A = (Q * lam[None, :]) @ Q.T
+    A = (A + A.T) * 0.5
+    return np.ascontiguousarray(A), lam
+
+
+def sign_fix(X):
+    """Make the largest-|entry| of every column positive (lowest index on ties)."""
+    idx = np.argmax(np.abs(X), axis=0)
+    s = np.sign(X[idx, np.arange(X.shape[1])])
+    s[s == 0] = 1.0
+    return X * s[None, :]
+
+
+def initial_eig(A, start="fp64"):
+    """X̂₀, λ̂₀ from LAPACK (numpy.linalg.eigh = syevd): in fp64, or in fp32 on fl32(A) and cast
+    back (BASELINE.json c2/c4 'mixed-precision start'). Ascending λ, sign-fixed columns."""
+    if start == "fp64":
+        lam, X = np.linalg.eigh(A)
+    elif start == "fp32":
+        lam, X = np.linalg.eigh(A.astype(np.float32))
+        lam, X = lam.astype(np.float64), X.astype(np.float64)
+    else:
+        raise ValueError(start)
+    return lam, np.ascontiguousarray(sign_fix(X))
+
+
+def make_config(name, n=None):
+    """(A, λ̂₀, X̂₀, cfg) for a named BASELINE config (optionally at a smaller n, same recipe)."""
+    cfg = dict(CONFIGS[name])
+    if n is not None:
+        cfg["n"] = n
+    A, _ = make_matrix(cfg["n"], cfg["kind"], cfg["cnd"], cfg["seed"])
+    lam0, X0 = initial_eig(A, cfg["start"])
+    return A, lam0, X0, cfg
+
+
+def householder_exact(m, lam_bits=12, seed=0):
+    """Pin family: n = 2^m, v ∈ {±1}^n, H = I − (2/n) v vᵀ (exactly orthogonal,
+    symmetric, dyadic). λ_k = distinct dyadic numbers with `lam_bits`-bit numerators in (0, 1].
+    A = H diag(λ) H is then exactly representable for moderate n and lam_bits, and its exact
+    eigenvectors are the columns of H. Returns (A, λ ascending, X exact (columns of H, sign-fixed,
+    ordered by λ))."""
+    n = 2 ** m
+    rng = np.random.default_rng(seed)
+    v = rng.choice([-1.0, 1.0], size=n)
+    H = np.eye(n) - (2.0 / n) * np.outer(v, v)
+    nums = rng.choice(np.arange(1, 2 ** lam_bits), size=n, replace=False)
+    lam = np.sort(nums.astype(np.float64) / 2 ** lam_bits)
+    order = rng.permutation(n)
+    lam_cols = np.empty(n)
+    lam_cols[order] = lam  # column order[k] of H carries λ_k
+    A = (H * lam_cols[None, :]) @ H
+    X = H[:, order]
+    return A, lam, sign_fix(X), H, lam_cols
+
+
+def pivot_2x2(theta):
+    """A = diag(1, 2) and X̂ = rotation by θ (SPEC-style closed form)."""
+    A = np.diag([1.0, 2.0])
+    c, s = np.cos(theta), np.sin(theta)
+    X = np.array([[c, -s], [s, c]])
+    return A, X
