@@ -1,0 +1,309 @@
+#!/usr/bin/env python
+"""bench.py — ozr on B200: effective FP64 TFLOP/s of the refinement sweep and time-to-target.
+
+One "step" = one refinement sweep (Algorithm 1 with the one-sided INT8 Ozaki product, PAPER.md:261-278,
+every §8(a) row of SURVEY.md) over the n x n workload, through the C ABI (ozr_refine_step), restarted
+from the same X̂₀ each step (the restore copy is inside the timed step). Effective FP64 work per sweep =
+3 products × 2n³ (V = A·X̂, W = X̂ᵀ(V − X̂D̂), U = X̂Ẽ — the n³ products Algorithm 1 performs).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4p] [--n N] [--impl ozr|reference]
+
+N > 1 (torchrun): every rank refines its own seeded problem (weak scaling, no data-path collective;
+DESIGN.md "Multi-GPU"); time = max over ranks (NCCL all-reduce of the device times).
+--impl reference: the CPU oracle (oracle/, dd triple loops) on a bounded column sample of the same
+workload, rank 0 only.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Ozaki-GEMM effective FP64 TFLOP/s; time-to-target forward error at n=8192"
+PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
+
+
+def _peaks():
+    try:
+        with open(PEAKS_FILE) as f:
+            return json.load(f), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.lines = []
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"], stdout=subprocess.PIPE,
+                                      stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.p = None
+
+    def _read(self):
+        for line in self.p.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=5)
+        except Exception:
+            self.p.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = float(f[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def cpu_oracle_sample(name, n, budget_s=15.0, ncols=None, seed_offset=0):
+    """The oracle (oracle/refine.sweep_columns, dd triple loops) on a column sample of the workload."""
+    import workloads as W
+    from oracle import _clib
+    from oracle import refine as orf
+    cfg = dict(W.CONFIGS[name])
+    n_eff = min(n, 2048)  # the CPU generator/eigensolver for the sample matrix is O(n^3) too
+    A, _ = W.make_matrix(n_eff, cfg["kind"], cfg["cnd"], cfg["seed"] + seed_offset)
+    lam0, X0 = W.initial_eig(A, cfg["start"])
+    J = np.arange(ncols or 8)
+    t0 = time.perf_counter()
+    orf.sweep_columns(A, X0, lam0, cfg["delta"], J)
+    dt = time.perf_counter() - t0
+    flops = 3 * 2.0 * n_eff * n_eff * len(J)
+    return {"value": flops / dt / 1e12, "unit": "TFLOP/s", "cores": _clib.num_threads(), "kind": "oracle",
+            "sample": f"oracle sweep restricted to {len(J)} of {n_eff} columns (dd triple loops, O(n^2·|J|) per "
+                      f"product) of the {name} recipe at n={n_eff}; {dt:.2f} s",
+            "seconds": dt}
+
+
+def run_reference(args):
+    ws, rank, _ = _dist()
+    if rank != 0:
+        return 0
+    import workloads as W
+    from oracle import _clib
+    from oracle import refine as orf
+    name = args.config
+    cfg = dict(W.CONFIGS[name])
+    n = args.n or cfg["n"]
+    n_eff = min(n, 2048)
+    A, _ = W.make_matrix(n_eff, cfg["kind"], cfg["cnd"], cfg["seed"])
+    lam0, X0 = W.initial_eig(A, cfg["start"])
+    J = np.arange(args.ref_cols)
+    for _ in range(args.warmup):
+        orf.sweep_columns(A, X0, lam0, cfg["delta"], J)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        orf.sweep_columns(A, X0, lam0, cfg["delta"], J)
+    dt = (time.perf_counter() - t0) / args.steps
+    flops = 3 * 2.0 * n_eff * n_eff * len(J)
+    val = flops / dt / 1e12
+    out = {"impl": "reference", "metric": METRIC, "value": val, "unit": "TFLOP/s", "n_gpus": ws,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "f64 (double-double)", "data": "synthetic",
+           "config": {"workload": f"{name}: " + _describe(cfg, n), "sample_n": n_eff, "sample_cols": len(J)},
+           "cpu_baseline": {"value": val, "unit": "TFLOP/s", "cores": _clib.num_threads(), "kind": "oracle",
+                            "sample": f"each step: oracle sweep on {len(J)} of {n_eff} columns of the {name} "
+                                      f"recipe at n={n_eff}"},
+           "e2e": {"value": val, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out))
+    return 0
+
+
+def _describe(cfg, n):
+    spec = f"geometric cnd={cfg['cnd']:.0e}" if cfg["kind"] == "geometric" else "uniform[-1,1]+64x8 clusters@1e-10"
+    return f"n={n} symmetric A=Q diag(lam) Q^T (Haar Q), {spec}, X0 from {cfg['start']} eigensolver, " \
+           f"delta={cfg['delta']:.0e}"
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c4p")
+    ap.add_argument("--n", type=int, default=0)
+    ap.add_argument("--impl", default="ozr", choices=["ozr", "reference"])
+    ap.add_argument("--ref-cols", type=int, default=8)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+    ws, rank, local = _dist()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    import paper_2602_19090_b200 as ozr
+    import workloads as W
+
+    name = args.config
+    A, lam0, X0, cfg = W.make_config_torch(name, dev, n=args.n or None, seed_offset=rank)
+    n = cfg["n"]
+    delta = cfg["delta"]
+    ctx = ozr.Context(local)
+    params = ozr.default_params(delta=delta)
+    X = X0.clone()
+    X = ozr.colmajor(X)
+    lam = lam0.clone()
+
+    def step():
+        X.copy_(X0)
+        lam.copy_(lam0)
+        return ozr.ozr_refine_step(ctx, A, X, lam, params)
+
+    for _ in range(max(args.warmup, 0)):
+        step()
+    torch.cuda.synchronize()
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.3)
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = []
+    e0.record()
+    for _ in range(args.steps):
+        reps.append(step())
+    e1.record()
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    clocks = sampler.stop()
+    ms = e0.elapsed_time(e1)
+    if ws > 1:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_step = ms / args.steps
+    flops_step = 3 * 2.0 * n ** 3
+    value = ws * flops_step / (ms_step / 1e3) / 1e12
+
+    # dominant kernel: the tcgen05 INT8 slice GEMM (device time from the library's own events)
+    gemm_ms = sum(r["ms_gemm"] for r in reps)
+    gemm_ops = sum(r["int8_ops"] for r in reps)
+    peaks, src = _peaks()
+    int8_peak = 2.0 * peaks["bf16_tflops_sustained"]
+    achieved = gemm_ops / (gemm_ms / 1e3) / 1e12
+    roofline = {"bound": "tensor", "achieved": achieved, "peak": int8_peak, "unit": "TFLOP/s", "frac": achieved / int8_peak,
+                "traffic": None, "dtype": "int8 (TOPS)",
+                "peak_source": f"2 x bf16_tflops_sustained of {src} MEASURED_PEAKS.json (nominal int8:bf16 = 2)",
+                "gemm_share_of_step": gemm_ms / ms}
+
+    # time to target: ozr_refine_to_tol from X̂0 (self-certified stop rule)
+    X.copy_(X0)
+    lam.copy_(lam0)
+    torch.cuda.synchronize()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record()
+    st, hist = ozr.ozr_refine_to_tol(ctx, A, X, lam, ozr.default_params(delta=delta, max_sweeps=6))
+    t1.record()
+    torch.cuda.synchronize()
+    ttt = {"ms": t0.elapsed_time(t1), "sweeps": len(hist), "status": int(st), "delta": delta,
+           "net_update_per_sweep": [h["net_update"] for h in hist],
+           "note": "self-certified stop (DESIGN.md R12); forward error vs oracle reference verified in tests at n<=1024"}
+
+    # e2e: host (pinned) buffers -> device, sweep, device -> host, every step
+    hA = A.cpu().pin_memory()
+    hX0 = X0.cpu().pin_memory()
+    hl0 = lam0.cpu().pin_memory()
+    hX = torch.empty_like(hX0).pin_memory()
+    hl = torch.empty_like(hl0).pin_memory()
+    Ad = torch.empty_like(A)
+    torch.cuda.synchronize()
+    w0 = time.perf_counter()
+    s0 = torch.cuda.Event(enable_timing=True)
+    s1 = torch.cuda.Event(enable_timing=True)
+    s0.record()
+    for _ in range(args.e2e_steps):
+        Ad.copy_(hA, non_blocking=True)
+        X.copy_(hX0, non_blocking=True)
+        lam.copy_(hl0, non_blocking=True)
+        ozr.ozr_refine_step(ctx, Ad, X, lam, params)
+        hX.copy_(X, non_blocking=True)
+        hl.copy_(lam, non_blocking=True)
+    s1.record()
+    torch.cuda.synchronize()
+    e2e_ms = s0.elapsed_time(s1) / args.e2e_steps
+    h2d = (A.numel() + X0.numel() + lam0.numel()) * 8
+    d2h = (X0.numel() + lam0.numel()) * 8
+    e2e = {"value": ws * flops_step / (e2e_ms / 1e3) / 1e12, "unit": "TFLOP/s", "h2d_bytes_per_step": h2d,
+           "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms}
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        try:
+            cpu = cpu_oracle_sample(name, n)
+        except Exception as ex:  # the oracle C library missing on the box is a setup error: report it
+            cpu = {"value": None, "unit": "TFLOP/s", "cores": os.cpu_count(), "kind": "oracle", "sample": f"failed: {ex}"}
+
+    r0 = reps[-1]
+    if rank == 0:
+        out = {"metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": ws, "steps": args.steps,
+               "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+               "vs_baseline": None, "dtype": "int8", "data": "synthetic",
+               "config": {"workload": f"{name}: " + _describe(cfg, n), "n": n, "delta": delta,
+                          "parallelism": f"replicas x{ws}" if ws > 1 else "1 GPU",
+                          "l2": "inputs larger than L2 (A + X = %.1f GiB per rank, L2 126 MB)" % (2 * n * n * 8 / 2 ** 30),
+                          "flops_per_step": "3 x 2n^3 (V=AX, W=X^T Res, U=X E)",
+                          "sweep": {k: r0[k] for k in ("beta", "alpha", "kX", "kA", "kR", "kE", "L_V", "L_W", "L_U",
+                                                       "pairs_V", "pairs_W", "pairs_U")}},
+               "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+               "gpu_launches": int(sum(r["launches"] for r in reps)), "clocks": clocks,
+               "time_to_target": ttt}
+        print(json.dumps(out))
+    ctx.close()
+    if ws > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

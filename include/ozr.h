@@ -129,6 +129,7 @@ typedef struct {
   int L_V, L_W, L_U;                /* pair budgets                                                    */
   int pairs_V, pairs_W, pairs_U;    /* INT8 slice products (each an n x n_local x n INT8 GEMM)         */
   int n_clusters;                   /* pairs |λ̂_i − λ̂_j| ≤ ω treated by the cluster branch              */
+  int launches;                     /* CUDA kernels this sweep launched                                */
   double gap_min, max_abs_lambda;   /* from the λ̂ that chose β                                         */
   double normE_fro;                 /* ‖Ẽ‖_F                                                          */
   double net_update;                /* ν = ‖X̂_new − X̂_old‖_F                                          */

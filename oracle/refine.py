@@ -208,3 +208,39 @@ def forward_error(Xh_ref, Xl_ref, X, lam_ref=None, lam=None, power_iters=None):
         s = np.linalg.norm(y)
         v = y / s
     return float(np.sqrt(s))
+
+
+def sweep_columns(A, X, lam_prev, delta, J, theta=1.0, beta=None):
+    """Algorithm 1 restricted to the output columns J (bench.py's bounded CPU sample; identical formulas
+    to sweep(), only the products' column sets shrink): V_J = A X̂^(1)_J, λ̂_J, Res_J,
+    W_{:,J} = X̂^(1)ᵀ Res_J, Ẽ_{:,J} (needs λ̂ of all columns: λ_prev is used for i ∉ J),
+    U_J = X̂^(1) Ẽ_{:,J}. Returns (X_new[:, J], λ̂_J, β)."""
+    A = np.asarray(A, dtype=np.float64)
+    X = np.asarray(X, dtype=np.float64)
+    n = A.shape[0]
+    J = np.asarray(J)
+    w = np.max(np.abs(X), axis=0)
+    c = ceil_log2(w)
+    if beta is None:
+        beta, _ = choose_beta(n, delta / theta, lam_prev, c, w)
+    beta = int(min(max(beta, BETA_MIN), BETA_MAX))
+    X1 = x1_truncate(X, beta)[0]
+    X1J = X1[:, J]
+    Vh, Vl = _clib.dd_gemm_nt(A, np.ascontiguousarray(X1J.T))
+    sh, sl = col_dot_dd(X1J, X1J)
+    rh, rl = dd_add(np.ones(len(J)), np.zeros(len(J)), -sh, -sl)
+    th, tl = col_dot_dd(X1J, Vh, Vl)
+    lh, ll = dd_div_dd(th, tl, sh, sl)
+    lamJ = lh + ll
+    ph, pl = two_prod(X1J, lamJ[None, :])
+    Rh, Rl = dd_add(Vh, Vl, -ph, -pl)
+    Wh, Wl = _clib.dd_gemm_nt(np.ascontiguousarray(X1.T), np.ascontiguousarray(Rh.T), None,
+                              np.ascontiguousarray(Rl.T))
+    lam = np.array(lam_prev, dtype=np.float64)
+    lam[J] = lamJ
+    dl = lamJ[None, :] - lam[:, None]
+    E = np.where(dl != 0, (Wh + Wl) / np.where(dl != 0, dl, 1.0), 0.0)
+    E[J, np.arange(len(J))] = (rh + rl) / 2
+    Uh, Ul = _clib.dd_gemm_nt(X1, np.ascontiguousarray(E.T))
+    s, e = two_sum(X1J, Uh)
+    return fast_two_sum(s, e + Ul)[0], lamJ, beta

@@ -37,7 +37,7 @@ class Params(ctypes.Structure):
 
 class StepReport(ctypes.Structure):
     _fields_ = ([(f, ctypes.c_int) for f in ["sweep", "beta", "beta_raw", "alpha", "kX", "kA", "kR", "kE", "L_V",
-                                              "L_W", "L_U", "pairs_V", "pairs_W", "pairs_U", "n_clusters"]] +
+                                              "L_W", "L_U", "pairs_V", "pairs_W", "pairs_U", "n_clusters", "launches"]] +
                 [(f, ctypes.c_double) for f in ["gap_min", "max_abs_lambda", "normE_fro", "net_update",
                                                  "predicted_error", "ms_total", "ms_gemm", "int8_ops"]])
 

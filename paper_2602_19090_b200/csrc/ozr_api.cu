@@ -247,17 +247,13 @@ double sum_pow2_2c(const std::vector<double>& w) {
   return s;
 }
 
+// Slice GEMM `idx` (0: V, 1: W, 2: U) of a sweep, bracketed by events ev[2+2idx], ev[3+2idx]
+// (read after the sweep's final synchronisation; no extra host sync here).
 ozr_status run_gemm(ozr_ctx ctx, const DigitOperand& A, const DigitOperand& B, int M, int N, int K,
-                    const PairTable& pt, int32_t* planes, float* ms) {
-  if (ms) cudaEventRecord(ctx->ev[6], ctx->stream);
+                    const PairTable& pt, int32_t* planes, int idx) {
+  cudaEventRecord(ctx->ev[2 + 2 * idx], ctx->stream);
   OZR_CK(launch_gemm_i8(A, B, M, N, K, pt, planes, static_cast<int64_t>(M) * N, M, ctx->stream), "slice GEMM");
-  if (ms) {
-    cudaEventRecord(ctx->ev[7], ctx->stream);
-    cudaEventSynchronize(ctx->ev[7]);
-    float t = 0;
-    cudaEventElapsedTime(&t, ctx->ev[6], ctx->ev[7]);
-    *ms += t;
-  }
+  cudaEventRecord(ctx->ev[3 + 2 * idx], ctx->stream);
   return OZR_OK;
 }
 
@@ -331,6 +327,7 @@ ozr_status sweep(ozr_ctx ctx, const double* A, int64_t n, int64_t lda, double* X
   OZR_CK(cudaMemsetAsync(derr, 0, sizeof(int), s), "memset");
 
   // ---- a0: statistics and parameters
+  const bool fresh_w = !st.have_w;
   if (!st.have_w) {
     launch_colmax(X, ldx, N, N, w, derr, s);
     OZR_CK(cudaGetLastError(), "colmax");
@@ -410,7 +407,7 @@ ozr_status sweep(ozr_ctx ctx, const double* A, int64_t n, int64_t lda, double* X
   DigitOperand opA{reinterpret_cast<const int8_t*>(ctx->bufs[S_ADIG].p), ld, ld * n, st.kA_split};
   DigitOperand opX{xdig, ld, ld * n, kx};
   {
-    ozr_status e = run_gemm(ctx, opA, opX, N, N, N, pt, planes, &gemm_ms);
+    ozr_status e = run_gemm(ctx, opA, opX, N, N, N, pt, planes, 0);
     if (e != OZR_OK) return e;
   }
   rep.pairs_V = count_pairs(gV);
@@ -462,7 +459,7 @@ ozr_status sweep(ozr_ctx ctx, const double* A, int64_t n, int64_t lda, double* X
   }
   DigitOperand opR{rdig, ld, ld * n, kR};
   {
-    ozr_status e = run_gemm(ctx, opX, opR, N, N, N, pt, planes, &gemm_ms);
+    ozr_status e = run_gemm(ctx, opX, opR, N, N, N, pt, planes, 1);
     if (e != OZR_OK) return e;
   }
   rep.kR = kR;
@@ -509,7 +506,7 @@ ozr_status sweep(ozr_ctx ctx, const double* A, int64_t n, int64_t lda, double* X
   DigitOperand opQ{xdigT, ld, ld * n, kx};
   DigitOperand opE{rdig, ld, ld * n, kE};
   {
-    ozr_status e = run_gemm(ctx, opQ, opE, N, N, N, pt, planes, &gemm_ms);
+    ozr_status e = run_gemm(ctx, opQ, opE, N, N, N, pt, planes, 2);
     if (e != OZR_OK) return e;
   }
   rep.kE = kE;
@@ -536,6 +533,11 @@ ozr_status sweep(ozr_ctx ctx, const double* A, int64_t n, int64_t lda, double* X
   }
   float tot = 0.f;
   cudaEventElapsedTime(&tot, ctx->ev[0], ctx->ev[1]);
+  for (int q = 0; q < 3; ++q) {
+    float t = 0.f;
+    cudaEventElapsedTime(&t, ctx->ev[2 + 2 * q], ctx->ev[3 + 2 * q]);
+    gemm_ms += t;
+  }
   st.have_w = true;
   rep.net_update = std::sqrt(nu);
   rep.normE_fro = std::sqrt(ne);
@@ -545,6 +547,8 @@ ozr_status sweep(ozr_ctx ctx, const double* A, int64_t n, int64_t lda, double* X
   rep.ms_total = tot;
   rep.ms_gemm = gemm_ms;
   rep.int8_ops = ops;
+  // kernels of this sweep: [colmax] x1_split transpose GEMM recombine_V split GEMM recombine_E split GEMM final
+  rep.launches = (fresh_w ? 1 : 0) + 10;
   return OZR_OK;
 }
 

@@ -96,6 +96,45 @@ def make_config(name, n=None):
     return A, lam0, X0, cfg
 
 
+def make_config_torch(name, device, n=None, seed_offset=0):
+    """Same recipe as make_config, built on the GPU with torch (fp64 QR / GEMM / syevd via cuSOLVER)
+    so that n = 8192..16384 inputs take seconds. Returns column-major CUDA tensors
+    (A, λ̂₀, X̂₀) and cfg. The N(0,1) matrix comes from numpy's PCG64 with the config seed."""
+    import torch
+    cfg = dict(CONFIGS[name])
+    if n is not None:
+        cfg["n"] = n
+    n = cfg["n"]
+    rng = np.random.default_rng(cfg["seed"] + seed_offset)
+    if cfg["kind"] == "geometric":
+        lam = geometric_spectrum(n, cfg["cnd"])
+        G = rng.standard_normal((n, n))
+    else:
+        lam = clustered_spectrum(n, rng)
+        G = rng.standard_normal((n, n))
+    Gt = torch.from_numpy(G).to(device)
+    del G
+    Q, R = torch.linalg.qr(Gt)
+    del Gt
+    Q = Q * torch.sign(torch.diagonal(R))[None, :]
+    del R
+    lt = torch.from_numpy(lam).to(device)
+    A = (Q * lt[None, :]) @ Q.T
+    del Q
+    A = (A + A.T) * 0.5
+    if cfg["start"] == "fp64":
+        lam0, X0 = torch.linalg.eigh(A)
+    else:
+        lam0, X0 = torch.linalg.eigh(A.float())
+        lam0, X0 = lam0.double(), X0.double()
+    idx = torch.argmax(X0.abs(), dim=0)
+    s = torch.sign(X0[idx, torch.arange(n, device=device)])
+    s[s == 0] = 1.0
+    X0 = X0 * s[None, :]
+    colmajor = lambda t: t.t().contiguous().t()  # noqa: E731
+    return colmajor(A), lam0.contiguous(), colmajor(X0), cfg
+
+
 def householder_exact(m, lam_bits=12, seed=0):
     """Pin family: n = 2^m, v ∈ {±1}^n, H = I − (2/n) v vᵀ (exactly orthogonal,
     symmetric, dyadic). λ_k = distinct dyadic numbers with `lam_bits`-bit numerators in (0, 1].
