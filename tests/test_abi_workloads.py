@@ -1,0 +1,116 @@
+"""CPU checks (-m "not gpu"): libozr.so builds, loads without a GPU and exports every symbol that
+include/ozr.h declares; host-only planning agrees with the oracle's plan; the product path refuses to
+run without a GPU (no CPU fallback); the seeded workloads have the paper's structure."""
+import ctypes
+import json
+import os
+import re
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+import workloads as W
+from oracle import products as opr
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def libozr():
+    from paper_2602_19090_b200 import build
+    build.build()
+    import paper_2602_19090_b200 as ozr
+    return ozr.lib()
+
+
+def test_header_symbols_exported(libozr):
+    hdr = open(os.path.join(ROOT, "include", "ozr.h")).read()
+    declared = set(re.findall(r"\b(ozr_[a-z_0-9]+)\s*\(", hdr))
+    assert {"ozr_split", "ozr_gemm", "ozr_refine_step", "ozr_refine_to_tol"} <= declared
+    out = subprocess.check_output(["nm", "-D", "--defined-only", os.path.join(ROOT, "paper_2602_19090_b200",
+                                                                              "libozr.so")]).decode()
+    exported = set(re.findall(r"\bT (ozr_[a-z_0-9]+)", out))
+    assert declared <= exported, declared - exported
+    for s in declared:
+        assert hasattr(libozr, s)
+
+
+def test_no_torch_types_in_abi():
+    hdr = open(os.path.join(ROOT, "include", "ozr.h")).read()
+    assert not re.search(r"\btorch\b|at::|Tensor|c10", hdr)
+
+
+def test_version_and_plan_on_cpu(libozr):
+    import paper_2602_19090_b200 as ozr
+    assert "sm_100a" in ozr.ozr_version()
+    for K, kA, kB, L in [(1024, 12, 6, 13), (16384, 15, 7, 16), (50000, 3, 3, 0), (100, 4, 4, 5)]:
+        plan = ozr.ozr_gemm_plan(K, kA, kB, L)
+        want = [(d, len(p)) for d, p in opr.plan_groups(kA, kB, L if L > 0 else kA + kB, K)]
+        assert plan == want
+
+
+def test_params_default(libozr):
+    import paper_2602_19090_b200 as ozr
+    p = ozr.default_params()
+    assert p.kA_split == 15 and p.truncate == 1 and p.beta_mode == 0 and abs(p.theta_V - 1 / 16) < 1e-18
+
+
+def test_no_cpu_fallback(libozr):
+    """Without a CUDA device the product path fails loudly (status OZR_ERR_CUDA / RuntimeError)."""
+    import torch
+
+    import paper_2602_19090_b200 as ozr
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    h = ctypes.c_void_p()
+    st = libozr.ozr_create(ctypes.byref(h), 0, None, 0)
+    assert st == 6
+    with pytest.raises(RuntimeError):
+        ozr.Context(0)
+
+
+def test_product_package_does_not_import_oracle():
+    pkg = os.path.join(ROOT, "paper_2602_19090_b200")
+    for dp, _, fs in os.walk(pkg):
+        for f in fs:
+            if f.endswith((".py", ".cu", ".cuh", ".h")):
+                txt = open(os.path.join(dp, f)).read()
+                assert "oracle" not in re.sub(r"#.*|//.*", "", txt).replace("no oracle", ""), f
+
+
+def test_workload_spectra_and_symmetry():
+    A, lam = W.make_matrix(200, "geometric", 1e8, 1)
+    assert np.array_equal(A, A.T)
+    assert lam[0] == 1.0 and abs(lam[-1] - 1e-8) < 1e-22
+    assert np.allclose(np.sort(np.linalg.eigvalsh(A))[::-1], lam, rtol=0, atol=1e-14)
+    A2, _ = W.make_matrix(200, "geometric", 1e8, 1)
+    assert np.array_equal(A, A2)  # seeded, deterministic
+    lam3 = W.clustered_spectrum(4096, np.random.default_rng(1003))
+    d = np.diff(lam3)
+    assert lam3.size == 4096 and np.sum(np.abs(d - 1e-10) < 1e-15) >= 64 * 7
+    assert np.all((lam3 >= -1) & (lam3 <= 1 + 1e-9))
+
+
+def test_initial_eig_sign_and_precision():
+    A, _ = W.make_matrix(128, "geometric", 1e6, 4)
+    l64, X64 = W.initial_eig(A, "fp64")
+    l32, X32 = W.initial_eig(A, "fp32")
+    assert np.all(np.diff(l64) >= 0)
+    idx = np.argmax(np.abs(X64), axis=0)
+    assert np.all(X64[idx, np.arange(128)] > 0)
+    assert np.max(np.abs(X32.astype(np.float32).astype(np.float64) - X32)) == 0  # an fp32 start
+
+
+def test_householder_exact_eigensystem():
+    A, lam, X, H, lc = W.householder_exact(5, lam_bits=10, seed=2)
+    assert np.array_equal(A @ X, X * lam[None, :]) or np.max(np.abs(A @ X - X * lam[None, :])) < 1e-15
+
+
+def test_bench_reference_arm_cpu():
+    out = subprocess.check_output([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--n",
+                                   "128", "--steps", "1", "--warmup", "0", "--ref-cols", "4"], cwd=ROOT)
+    line = json.loads(out.decode().strip().splitlines()[-1])
+    assert line["impl"] == "reference" and line["value"] > 0 and line["e2e"]["h2d_bytes_per_step"] == 0
+    assert line["cpu_baseline"]["kind"] == "oracle"

@@ -1,0 +1,178 @@
+"""Pins for oracle/products.py, oracle/_clib (ddmm.c) and oracle/refine.py (CPU, -m "not gpu"):
+brute force in exact integers/rationals, __float128 Jacobi against closed forms, an exactly-known
+eigensystem family, and the paper's qualitative claims (quadratic convergence, O(δ) forward error)."""
+from fractions import Fraction as F
+
+import numpy as np
+import pytest
+
+import workloads as W
+from oracle import _clib
+from oracle import products as opr
+from oracle import refine as orf
+from oracle import split as osp
+
+
+def test_plan_groups_brute_force():
+    for kA, kB, L, K in [(5, 3, 6, 100), (4, 4, 8, 50000), (15, 7, 13, 16384), (2, 6, 3, 1)]:
+        gs = opr.plan_groups(kA, kB, L, K)
+        flat = [p for _, ps in gs for p in ps]
+        want = [(s, d - s) for d in range(2, min(L, kA + kB) + 1) for s in range(1, kA + 1) if 1 <= d - s <= kB]
+        assert flat == want
+        cap = opr.max_pairs_per_group(K)
+        assert all(len(ps) <= cap and all(s + t == d for s, t in ps) for d, ps in gs)
+        assert K * cap * 2 ** 14 <= 2 ** 31 - 1 or cap == 1
+
+
+def test_slice_planes_vs_python_ints():
+    rng = np.random.default_rng(1)
+    DA = rng.integers(-128, 128, (3, 7, 5)).astype(np.int8)
+    DB = rng.integers(-128, 128, (2, 7, 4)).astype(np.int8)
+    gs = opr.plan_groups(3, 2, 5, 7)
+    P = opr.slice_planes(DA, DB, gs)
+    for gi, (d, ps) in enumerate(gs):
+        for i in range(5):
+            for j in range(4):
+                v = sum(int(DA[s - 1, k, i]) * int(DB[t - 1, k, j]) for s, t in ps for k in range(7))
+                assert P[gi, i, j] == v
+
+
+def test_digit_product_all_pairs_is_exact_product_of_split_operands():
+    """With every pair kept the recombined value is the exact product of the digit-represented
+    operands, correctly rounded to double-double (vs Fractions)."""
+    rng = np.random.default_rng(2)
+    m, k, n = 6, 9, 5
+    A = rng.standard_normal((m, k)) * 2.0 ** rng.integers(-10, 10, (m, 1))
+    B = rng.standard_normal((k, n))
+    kA, kB = 4, 3
+    DA, eA = osp.split_digits_cols(A.T, kA)
+    DB, eB = osp.split_digits_cols(B, kB)
+    hi, lo, _, _ = opr.digit_product(DA, eA, kA, DB, eB, kB, kA + kB)
+    a = osp.digits_value(DA)  # (k, m)
+    b = osp.digits_value(DB)
+    for i in range(m):
+        for j in range(n):
+            ex = sum(F(int(a[q, i])) * F(2) ** int(eA[i]) * F(int(b[q, j])) * F(2) ** int(eB[j]) for q in range(k))
+            h = float(ex)
+            assert hi[i, j] == h and lo[i, j] == float(ex - F(h))
+
+
+def test_to_dd_correct_rounding():
+    rng = np.random.default_rng(3)
+    T = np.array([int(x) << int(s) for x, s in zip(rng.integers(-2 ** 62, 2 ** 62, 300), rng.integers(0, 60, 300))],
+                 dtype=object)
+    hi, lo = opr.to_dd(T, 0)
+    for t, h, l_ in zip(T, hi, lo):
+        assert h == float(t) and l_ == float(F(int(t)) - F(h))
+
+
+def test_dd_gemm_vs_rationals():
+    rng = np.random.default_rng(4)
+    P = rng.standard_normal((5, 40)) * 2.0 ** rng.integers(-20, 20, (5, 1))
+    Q = rng.standard_normal((3, 40))
+    Ql = Q * 2.0 ** -55 * rng.uniform(-1, 1, Q.shape)
+    Ch, Cl = _clib.dd_gemm_nt(P, Q, None, Ql)
+    for i in range(5):
+        for j in range(3):
+            ex = sum(F(P[i, k]) * (F(Q[j, k]) + F(Ql[j, k])) for k in range(40))
+            scale = sum(abs(F(P[i, k]) * F(Q[j, k])) for k in range(40))
+            assert abs(F(Ch[i, j]) + F(Cl[i, j]) - ex) <= scale * F(2) ** -100
+
+
+def test_jacobi_q_closed_forms():
+    wh, wl, Vh, Vl, sw = _clib.jacobi_q(np.diag([3.0, 1.0, 2.0]))
+    assert list(wh) == [1.0, 2.0, 3.0] and sw >= 0
+    assert np.array_equal(np.abs(Vh), np.array([[0, 0, 1], [1, 0, 0], [0, 1, 0]], dtype=float))
+    # 2x2 [[0,1],[1,0]]: λ = ∓1, x = (1, ∓1)/√2 (SPEC-style analytic case)
+    wh, wl, Vh, Vl, _ = _clib.jacobi_q(np.array([[0.0, 1.0], [1.0, 0.0]]))
+    assert abs(wh[0] + 1) < 1e-30 and abs(wh[1] - 1) < 1e-30
+    x0, x1 = F(Vh[0, 0]) + F(Vl[0, 0]), F(Vh[1, 0]) + F(Vl[1, 0])
+    assert abs(x0 * x0 - F(1, 2)) < F(1, 10 ** 30) and abs(x0 * x1 + F(1, 2)) < F(1, 10 ** 30)
+
+
+def test_reference_eigvecs_vs_quad_jacobi():
+    """The dd Ogita–Aishima reference (used for every forward error) agrees with __float128 Jacobi."""
+    A, _ = W.make_matrix(24, "geometric", 1e8, 5)
+    lam0, X0 = W.initial_eig(A)
+    Xh, Xl, lh, ll, hist = orf.reference_eigvecs(A, X0, lam0)
+    wh, wl, Vh, Vl, sw = _clib.jacobi_q(A)
+    assert sw > 0
+    assert np.max(np.abs((lh - wh) + (ll - wl))) < 1e-28
+    s = np.sign(np.sum(Xh * Vh, axis=0))
+    assert np.max(np.abs((Xh - Vh * s) + (Xl - Vl * s))) < 1e-24
+
+
+def test_reference_on_exact_householder_family():
+    """Pin P6: A = H diag(λ) H exactly representable, X = H exactly."""
+    A, lam, X, H, lam_cols = W.householder_exact(6, lam_bits=12, seed=3)
+    n = A.shape[0]
+    # exactness of the stored A: integer check (n/2)^2 2^12 A = Hn diag(m) Hn with Hn = (n/2) H
+    Hn = np.rint(H * n / 2).astype(np.int64)
+    m = np.rint(lam_cols * 2 ** 12).astype(np.int64)
+    assert np.array_equal(((Hn * m[None, :]) @ Hn).astype(np.float64), A * (n / 2) ** 2 * 2 ** 12)
+    lam0, X0 = W.initial_eig(A)
+    Xh, Xl, lh, ll, _ = orf.reference_eigvecs(A, X0, lam0)
+    assert orf.forward_error(Xh, Xl, X) < 1e-25
+    assert np.max(np.abs(lh - lam)) < 1e-28
+
+
+def test_sweep_fixed_point_and_diag_rule():
+    """Alg. 1 on an exact eigensystem: X̂ = I for diagonal A is a fixed point; ẽ_ii = r_i/2."""
+    A = np.diag([1.0, 2.0, 3.0, 5.0])
+    Xn, lam, info = orf.sweep(A, np.eye(4), np.array([1.0, 2, 3, 5]), 1e-12)
+    assert np.array_equal(Xn, np.eye(4)) and np.array_equal(lam, [1.0, 2, 3, 5])
+    A, lam0, X0, _ = W.make_config("c1")
+    Xn, lam, info = orf.sweep(A, X0, lam0, 1e-12)
+    assert np.array_equal(np.diag(info["E"]), (info["r"][0] + info["r"][1]) / 2)
+    # ẽ_ij (λ_j − λ_i) reproduces w_ij (Alg. 1 line 5)
+    E, Wm = info["E"], info["W"][0] + info["W"][1]
+    dl = lam[None, :] - lam[:, None]
+    off = ~np.eye(100, dtype=bool)
+    assert np.max(np.abs(E[off] * dl[off] - Wm[off]) / np.abs(Wm[off])) < 1e-15
+
+
+def test_sweep_2x2_rotation():
+    """A = diag(1,2), X̂ = rotation by θ: one untruncated sweep leaves an O(θ²) error (Theorem 1)."""
+    A, X = W.pivot_2x2(1e-4)
+    Xn, lam, info = orf.sweep(A, X, np.array([1.0, 2.0]), 1e-15, truncate=False)
+    err = np.max(np.abs(np.abs(Xn) - np.eye(2)))
+    assert err < 1e-8
+    # X = X̂(I + E) with X = I  =>  E ≈ X̂ᵀ − I: e_10 ≈ −θ, e_01 ≈ +θ
+    assert abs(info["E"][1, 0] + 1e-4) < 1e-7 and abs(info["E"][0, 1] - 1e-4) < 1e-7
+
+
+def test_quadratic_convergence_untruncated():
+    """Theorem 1: ε_{k+1} = O(ε_k²) — regression slope ≥ 1.7."""
+    A, _ = W.make_matrix(64, "geometric", 1e2, 9)  # gap_min ≈ 7.6e-4: ε ~ 1e-6 is inside Theorem 1's region
+    lam0, X0 = W.initial_eig(A)
+    Xh, Xl, lh, ll, _ = orf.reference_eigvecs(A, X0, lam0)
+    rng = np.random.default_rng(0)
+    X = X0 + rng.standard_normal(X0.shape) * 1e-7
+    lam = lam0.copy()
+    errs = [orf.forward_error(Xh, Xl, X)]
+    for _ in range(2):
+        X, lam, _ = orf.sweep(A, X, lam, 1e-15, truncate=False)
+        errs.append(orf.forward_error(Xh, Xl, X))
+    slope = np.log(errs[1]) / np.log(errs[0])
+    assert slope >= 1.7 or errs[1] < 1e-13, errs
+
+
+@pytest.mark.parametrize("delta", [1e-6, 1e-10, 1e-13])
+def test_forward_error_targets_delta(delta):
+    """‖X − X̂‖ = O(δ): within [δ/10³, 2δ] after the driver stops (c1 recipe)."""
+    A, lam0, X0, _ = W.make_config("c1")
+    Xh, Xl, lh, ll, _ = orf.reference_eigvecs(A, X0, lam0)
+    X, lam, hist = orf.refine_to_tol(A, X0, lam0, delta)
+    fe = orf.forward_error(Xh, Xl, X)
+    assert delta / 1e3 <= fe <= 2 * delta or (fe <= 2 * delta and delta < 1e-12), (fe, hist)
+    assert len(hist) <= 3
+
+
+def test_sweep_columns_matches_sweep():
+    A, lam0, X0, _ = W.make_config("c1")
+    Xn, lam, info = orf.sweep(A, X0, lam0, 1e-12)
+    J = np.array([0, 7, 50, 99])
+    XJ, lamJ, beta = orf.sweep_columns(A, X0, lam0, 1e-12, J)
+    assert beta == info["beta"]
+    assert np.max(np.abs(XJ - Xn[:, J])) < 1e-15
+    assert np.max(np.abs(lamJ - lam[J])) < 1e-15
