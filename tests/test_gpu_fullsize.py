@@ -1,0 +1,95 @@
+"""GPU parity at BASELINE.json's full size (n = 8192, the bench's launch configuration) on outputs the
+oracle can compute one column at a time, plus properties that hold at any size.
+
+ - ozr_gemm (n = 8192, the V-product digit budget of the bench): int32 group planes of sampled
+   columns bit-exact vs the oracle's digit products; the dd result of those columns vs the oracle's
+   exact recombination and vs the exact dd product.
+ - ozr_refine_step at n = 8192: λ̂ of sampled columns vs the oracle's Rayleigh quotients of the same
+   X̂^(1) (column-local: x̂_jᵀ A x̂_j / x̂_jᵀ x̂_j in double-double); β identical.
+ - ozr_refine_to_tol at n = 8192: residuals ‖A x̂_j − λ̂_j x̂_j‖ (dd) and orthogonality of sampled columns,
+   and the Davis–Kahan forward-error bound ‖r_j‖/gap_j ≤ δ for well-separated columns."""
+import numpy as np
+import pytest
+
+from gpu_util import to_np
+from oracle import _clib
+from oracle import products as opr
+from oracle import refine as orf
+from oracle import split as osp
+from oracle.fp import dd_add, dd_div_dd, two_prod
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+N = 8192
+
+
+@pytest.fixture(scope="module")
+def big():
+    import torch
+
+    import workloads as W
+    A, lam0, X0, cfg = W.make_config_torch("c4p", torch.device("cuda", 0))
+    return A, lam0, X0, cfg, to_np(A), to_np(lam0), to_np(X0)
+
+
+def test_gemm_fullsize_sampled_columns(ctx, big):
+    import paper_2602_19090_b200 as ozr
+    A, lam0, X0, cfg, An, ln, Xn = big
+    kA, kB, L = 12, 5, 13
+    Ch, Cl, planes = ozr.ozr_gemm(ctx, A, X0, kA, kB, L, want_planes=True)
+    J = np.array([0, 1, 4095, 8191])
+    DA, eA = osp.split_digits_cols(An.T, kA)           # row-wise split of A (contraction first)
+    DB, eB = osp.split_digits_cols(Xn[:, J], kB)
+    hi, lo, P, groups = opr.digit_product(DA, eA, kA, DB, eB, kB, L)
+    got = to_np(planes[:, J, :]).transpose(0, 2, 1)
+    assert np.array_equal(got, P)
+    assert np.array_equal(to_np(Ch)[:, J], hi)
+    assert np.max(np.abs(to_np(Cl)[:, J] - lo) / np.maximum(np.abs(hi), 1e-300)) <= 2.0 ** -104
+    # vs the exact product of A with the 5-digit B (exact in fp64: 38-bit integers times 2^ℓ)
+    Bt = np.array(osp.digits_value(DB), dtype=np.float64) * np.ldexp(1.0, eB)[None, :]
+    Eh, El = _clib.dd_gemm_nt(An, np.ascontiguousarray(Bt.T))
+    err = np.max(np.abs((to_np(Ch)[:, J] - Eh) + (to_np(Cl)[:, J] - El)))
+    assert err < 1e-25, err   # 12 A digits ≈ 94 bits below the row maxima
+
+
+def test_refine_step_fullsize_sampled_lambda(ctx, big):
+    import paper_2602_19090_b200 as ozr
+    A, lam0, X0, cfg, An, ln, Xn = big
+    X = ozr.colmajor(X0.clone())
+    lam = lam0.clone()
+    rep = ozr.ozr_refine_step(ctx, A, X, lam, ozr.default_params(delta=cfg["delta"]))
+    w = np.max(np.abs(Xn), axis=0)
+    beta, _ = orf.choose_beta(N, cfg["delta"], ln, osp.ceil_log2(w), w)
+    assert rep["beta"] == min(max(beta, 2), 52)
+    J = np.array([0, 17, 4096, 8190, 8191])
+    X1J = osp.x1_truncate(Xn, rep["beta"])[0][:, J]
+    Vh, Vl = _clib.dd_gemm_nt(An, np.ascontiguousarray(X1J.T))
+    sh, sl = orf.col_dot_dd(X1J, X1J)
+    th, tl = orf.col_dot_dd(X1J, Vh, Vl)
+    lh, ll = dd_div_dd(th, tl, sh, sl)
+    dl = np.abs(to_np(lam)[J] - (lh + ll)) / np.max(np.abs(ln))
+    assert np.max(dl) <= 1e-13, dl
+    assert rep["net_update"] > 0 and np.all(np.isfinite(to_np(X)[:, J]))
+
+
+def test_refine_to_tol_fullsize_residual_properties(ctx, big):
+    import paper_2602_19090_b200 as ozr
+    A, lam0, X0, cfg, An, ln, Xn = big
+    X = ozr.colmajor(X0.clone())
+    lam = lam0.clone()
+    st, hist = ozr.ozr_refine_to_tol(ctx, A, X, lam, ozr.default_params(delta=cfg["delta"]))
+    assert st == 0, hist
+    Xr, lr = to_np(X), to_np(lam)
+    J = np.array([8191, 8190, 8000, 6000, 0])      # top of the spectrum ... bottom
+    XJ = np.ascontiguousarray(Xr[:, J])
+    Vh, Vl = _clib.dd_gemm_nt(An, np.ascontiguousarray(XJ.T))
+    ph, pl = two_prod(XJ, lr[J][None, :])
+    Rh, Rl = dd_add(Vh, Vl, -ph, -pl)
+    res = np.sqrt(np.sum((Rh + Rl) ** 2, axis=0))
+    ls = np.sort(lr)
+    gaps = np.array([np.min(np.abs(np.delete(ls, np.searchsorted(ls, lr[j])) - lr[j])) for j in J])
+    assert np.all(res <= 1e-14), res                  # backward error: ~10 u·‖A‖, the fp64 storage level
+    G = XJ.T @ XJ
+    assert np.max(np.abs(G - np.eye(len(J)))) <= 1e-14
+    dk = res / gaps                                    # Davis–Kahan: sin θ_j ≤ ‖r_j‖ / gap_j
+    assert np.all(dk[:3] <= cfg["delta"]), dk          # well-separated top columns certify ≤ δ
