@@ -89,22 +89,50 @@ __device__ __forceinline__ i128 block_sum_i128(i128 v, i128* sh) {  // exact: or
 
 // ---------------------------------------------------------------- recombination of one element
 // value = Σ_chunks T_c · 2^{8(L − dhi_c) + e}, T_c = Horner over the chunk's groups (exact int128).
+__device__ __forceinline__ void flush_chunk(dd& acc, bool& first, i128 T, int dlast, int L, int e) {
+  dd v = i128_to_dd(T);
+  const int sc = 8 * (L - dlast) + e;
+  v.hi = scalbn(v.hi, sc);
+  v.lo = scalbn(v.lo, sc);
+  acc = first ? v : dd_add(acc, v);
+  first = false;
+}
+
+constexpr int kRegGroups = 24;  // plans up to this many groups keep every plane value in registers
+
 __device__ __forceinline__ dd recombine_elem(const int32_t* __restrict__ planes, long long pstride, long long off,
                                              const RecombPlan& rp, int e) {
   dd acc{0.0, 0.0};
+  bool first = true;
+  if (rp.nchunks == 1 && rp.ngroups <= kRegGroups) {
+    // one int128 chunk (the common case): issue every plane load first (memory-level parallelism),
+    // then an unrolled Horner
+    int32_t c[kRegGroups];
+#pragma unroll
+    for (int g = 0; g < kRegGroups; ++g) c[g] = (g < rp.ngroups) ? __ldg(planes + g * pstride + off) : 0;
+    i128 T = 0;
+    int dprev = rp.diag[0];
+#pragma unroll
+    for (int g = 0; g < kRegGroups; ++g) {
+      if (g < rp.ngroups) {
+        const int d = rp.diag[g];
+        T = static_cast<i128>(static_cast<u128>(T) << (8 * (d - dprev))) + static_cast<i128>(c[g]);
+        dprev = d;
+      }
+    }
+    flush_chunk(acc, first, T, dprev, rp.L, e);
+    return acc;
+  }
   for (int c = 0; c < rp.nchunks; ++c) {
     i128 T = 0;
     int dprev = rp.diag[rp.chunk_first[c]];
     for (int g = rp.chunk_first[c]; g < rp.chunk_first[c + 1]; ++g) {
       const int d = rp.diag[g];
-      T = static_cast<i128>(static_cast<u128>(T) << (8 * (d - dprev))) + static_cast<i128>(__ldg(planes + g * pstride + off));
+      T = static_cast<i128>(static_cast<u128>(T) << (8 * (d - dprev))) +
+          static_cast<i128>(__ldg(planes + g * pstride + off));
       dprev = d;
     }
-    dd v = i128_to_dd(T);
-    const int sc = 8 * (rp.L - dprev) + e;
-    v.hi = scalbn(v.hi, sc);
-    v.lo = scalbn(v.lo, sc);
-    acc = (c == 0) ? v : dd_add(acc, v);
+    flush_chunk(acc, first, T, dprev, rp.L, e);
   }
   return acc;
 }
@@ -126,6 +154,29 @@ __global__ void __launch_bounds__(BS) k_colmax(const double* __restrict__ X, lon
   if (threadIdx.x == 0) w[blockIdx.x] = m;
 }
 
+// Digits of four consecutive rows, packed per plane into one 32-bit store (byte r = row i0 + r).
+// Integer type T: long long when |p| < 2^62 (k <= 7), i128 otherwise.
+template <typename T>
+__device__ __forceinline__ void store_digits4(const T (&p)[4], int k, int8_t* __restrict__ base, long long pstride) {
+  T off = 0;
+  for (int s = 1; s < k; ++s) off = (off << 8) | 128;
+  T w[4];
+#pragma unroll
+  for (int r = 0; r < 4; ++r) w[r] = p[r] + off;
+  for (int q = 0; q < k; ++q) {
+    const int sh = 8 * (k - 1 - q);
+    uint32_t packed = 0;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      int d;
+      if (q == 0) d = static_cast<int>(static_cast<long long>(w[r] >> sh));
+      else d = static_cast<int>(static_cast<uint32_t>(w[r] >> sh) & 0xFFu) - 128;
+      packed |= (static_cast<uint32_t>(d) & 0xFFu) << (8 * r);
+    }
+    *reinterpret_cast<uint32_t*>(base + q * pstride) = packed;
+  }
+}
+
 __global__ void __launch_bounds__(BS)
     k_x1_split(const double* __restrict__ X, long long ldx, int rows, int beta, int kx, const double* __restrict__ w,
                double* __restrict__ X1, long long ldx1, int8_t* __restrict__ dig, long long ldd, long long pstride,
@@ -134,36 +185,66 @@ __global__ void __launch_bounds__(BS)
   __shared__ i128 shq[BS / 32];
   const int j = blockIdx.x;
   const double* col = X + j * ldx;
+  double* x1c = X1 + j * ldx1;
   const double wj = w[j];
   const int c = ceil_log2_d(wj);
   const int g = c + beta - 53;
   const double tau = (wj == 0.0) ? 0.0 : scalbn(0.75, c + beta);  // eq. (tau)
   i128 sq = 0;
-  for (int i = threadIdx.x; i < rows; i += BS) {
-    const double x = col[i];
-    const double x1 = __dsub_rn(__dadd_rn(tau, x), tau);  // eq. (x), s = 1: fl(fl(τ + x) − τ)
-    X1[j * ldx1 + i] = x1;
-    const long long q = static_cast<long long>(scalbn(x1, -g));  // exact integer, |q| <= 2^{53-β}
-    sq += static_cast<i128>(q) * q;
-    int d[8];
-    excess_digits(static_cast<i128>(q), kx, d);
-    for (int p = 0; p < kx; ++p) dig[p * pstride + j * ldd + i] = static_cast<int8_t>(d[p]);
+  // 4 consecutive rows per thread: the digit planes get one 32-bit store per plane (ldd % 16 == 0,
+  // so rounding `rows` up to 4 stays inside the column's padding).
+  for (int i0 = 4 * threadIdx.x; i0 < rows; i0 += 4 * BS) {
+    long long q[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int i = i0 + r;
+      const double x = (i < rows) ? col[i] : 0.0;
+      const double x1 = __dsub_rn(__dadd_rn(tau, x), tau);  // eq. (x), s = 1: fl(fl(τ + x) − τ)
+      if (i < rows) x1c[i] = x1;
+      q[r] = __double2ll_rn(scalbn(x1, -g));  // exact integer, |q| <= 2^{53-β}
+      sq += static_cast<i128>(q[r]) * q[r];
+    }
+    store_digits4<long long>(q, kx, dig + j * ldd + i0, pstride);
   }
   const i128 SQ = block_sum_i128(sq, shq);
   if (threadIdx.x == 0) {
     g_out[j] = g;
     // x̂_jᵀx̂_j = 2^{2g} SQ and r_j = 1 − 2^{2g} SQ = 2^{2g}(2^{−2g} − SQ), both exact integers scaled.
-    if (-2 * g > 125 || -2 * g < 0) {
-      atomicOr(err, ERR_RANGE);
-    } else {
-      const dd s = i128_to_dd(SQ);
+    const dd s = i128_to_dd(SQ);
+    s_hi[j] = scalbn(s.hi, 2 * g);
+    s_lo[j] = scalbn(s.lo, 2 * g);
+    if (-2 * g <= 125 && -2 * g >= 0) {
       const dd r = i128_to_dd((static_cast<i128>(1) << (-2 * g)) - SQ);
-      s_hi[j] = scalbn(s.hi, 2 * g);
-      s_lo[j] = scalbn(s.lo, 2 * g);
       r_hi[j] = scalbn(r.hi, 2 * g);
       r_lo[j] = scalbn(r.lo, 2 * g);
-      if (SQ == 0) atomicOr(err, ERR_DEGENERATE);
+    } else {  // a column far from unit norm (never an eigenvector estimate): r in double-double
+      const dd r = dd_add(dd{1.0, 0.0}, dd{-s_hi[j], -s_lo[j]});
+      r_hi[j] = r.hi;
+      r_lo[j] = r.lo;
     }
+    if (SQ == 0) atomicOr(err, ERR_DEGENERATE);
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ T rint_to(double x);
+template <>
+__device__ __forceinline__ long long rint_to<long long>(double x) { return __double2ll_rn(x); }
+template <>
+__device__ __forceinline__ i128 rint_to<i128>(double x) { return rint_to_i128(x); }
+
+template <typename T>
+__device__ __forceinline__ void split_fixed_body(const double* __restrict__ col, const double* __restrict__ cl, int rows,
+                                                 int k, int S, int e, int8_t* __restrict__ base, long long pstride) {
+  for (int i0 = 4 * threadIdx.x; i0 < rows; i0 += 4 * BS) {
+    T p[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int i = i0 + r;
+      p[r] = (i < rows) ? rint_to<T>(scalbn(col[i], S - e)) : T(0);
+      if (cl && i < rows) p[r] += rint_to<T>(scalbn(cl[i], S - e));
+    }
+    store_digits4<T>(p, k, base + i0, pstride);
   }
 }
 
@@ -186,13 +267,9 @@ __global__ void __launch_bounds__(BS)
   m = block_max(m, sh);
   const int e = ceil_log2_d(m);
   const int S = 8 * (k - 1) + 6;
-  for (int i = threadIdx.x; i < rows; i += BS) {
-    i128 p = rint_to_i128(scalbn(col[i], S - e));
-    if (cl) p += rint_to_i128(scalbn(cl[i], S - e));
-    int d[16];
-    excess_digits(p, k, d);
-    for (int q = 0; q < k; ++q) dig[q * pstride + j * ldd + i] = static_cast<int8_t>(d[q]);
-  }
+  // |p| <= 2^S (+1 for a double-double): 64-bit arithmetic while S <= 54 (k <= 7)
+  if (k <= 7) split_fixed_body<long long>(col, cl, rows, k, S, e, dig + j * ldd, pstride);
+  else split_fixed_body<i128>(col, cl, rows, k, S, e, dig + j * ldd, pstride);
   if (threadIdx.x == 0) ell_out[j] = e - S;
 }
 
