@@ -118,6 +118,7 @@ typedef struct {
                                        and δ' (X̂Ẽ) (R8; defaults 1/16, 1/16, 1/16)  */
   int L_V, L_W, L_U; /* > 0: force the pair budgets (s+t ≤ L) instead of the planner          */
   int cluster_mode;  /* 0: error on equal λ̂; 1: OA threshold branch (R13)      */
+  int tile_budgets;  /* 1: per-256-column pair budgets from the local gaps gap_j (R8b) [default]  */
 } ozr_params;
 
 void ozr_params_default(ozr_params* p);

@@ -32,7 +32,8 @@ class Params(ctypes.Structure):
                 ("xi", ctypes.c_double), ("beta_override", ctypes.c_int), ("truncate", ctypes.c_int),
                 ("max_sweeps", ctypes.c_int), ("kA_split", ctypes.c_int), ("theta_V", ctypes.c_double),
                 ("theta_W", ctypes.c_double), ("theta_U", ctypes.c_double), ("L_V", ctypes.c_int),
-                ("L_W", ctypes.c_int), ("L_U", ctypes.c_int), ("cluster_mode", ctypes.c_int)]
+                ("L_W", ctypes.c_int), ("L_U", ctypes.c_int), ("cluster_mode", ctypes.c_int),
+                ("tile_budgets", ctypes.c_int)]
 
 
 class StepReport(ctypes.Structure):

@@ -21,7 +21,7 @@ namespace ozr {
 namespace {
 
 constexpr int BM = 128;
-constexpr int BN = 256;
+constexpr int BN = kTileN;
 constexpr int BK = 128;  // bytes of K per stage (= one 128 B swizzle row)
 constexpr int STAGES = 4;
 constexpr int UMMA_K = 32;  // K per tcgen05.mma for 8-bit inputs
@@ -51,6 +51,7 @@ __global__ void __launch_bounds__(128, 1)
   const int n0 = (tile / tiles_m) * BN;
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  if (pt.tile_budgets && pt.diag[g] > pt.tileL[n0 / BN]) return;  // beyond this column tile's budget
 
   if (threadIdx.x == 0) {
     tma_prefetch(&tmA);
@@ -147,6 +148,7 @@ __global__ void k_gemm_i8_simt(DigitOperand A, DigitOperand B, PairTable pt, int
   const int col = blockIdx.y;
   const int g = blockIdx.z;
   if (row >= M || col >= N) return;
+  if (pt.tile_budgets && pt.diag[g] > pt.tileL[col / kTileN]) return;
   int32_t acc = 0;
   for (int p = pt.first[g]; p < pt.first[g + 1]; ++p) {
     const int8_t* a = A.base + pt.s[p] * A.plane_stride + static_cast<long long>(row) * A.ld;

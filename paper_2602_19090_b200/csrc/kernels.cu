@@ -101,7 +101,7 @@ __device__ __forceinline__ void flush_chunk(dd& acc, bool& first, i128 T, int dl
 constexpr int kRegGroups = 24;  // plans up to this many groups keep every plane value in registers
 
 __device__ __forceinline__ dd recombine_elem(const int32_t* __restrict__ planes, long long pstride, long long off,
-                                             const RecombPlan& rp, int e) {
+                                             const RecombPlan& rp, int e, int Lj) {
   dd acc{0.0, 0.0};
   bool first = true;
   if (rp.nchunks == 1 && rp.ngroups <= kRegGroups) {
@@ -109,7 +109,8 @@ __device__ __forceinline__ dd recombine_elem(const int32_t* __restrict__ planes,
     // then an unrolled Horner
     int32_t c[kRegGroups];
 #pragma unroll
-    for (int g = 0; g < kRegGroups; ++g) c[g] = (g < rp.ngroups) ? __ldg(planes + g * pstride + off) : 0;
+    for (int g = 0; g < kRegGroups; ++g)
+      c[g] = (g < rp.ngroups && rp.diag[g] <= Lj) ? __ldg(planes + g * pstride + off) : 0;
     i128 T = 0;
     int dprev = rp.diag[0];
 #pragma unroll
@@ -128,8 +129,8 @@ __device__ __forceinline__ dd recombine_elem(const int32_t* __restrict__ planes,
     int dprev = rp.diag[rp.chunk_first[c]];
     for (int g = rp.chunk_first[c]; g < rp.chunk_first[c + 1]; ++g) {
       const int d = rp.diag[g];
-      T = static_cast<i128>(static_cast<u128>(T) << (8 * (d - dprev))) +
-          static_cast<i128>(__ldg(planes + g * pstride + off));
+      const int32_t cv = (d <= Lj) ? __ldg(planes + g * pstride + off) : 0;
+      T = static_cast<i128>(static_cast<u128>(T) << (8 * (d - dprev))) + static_cast<i128>(cv);
       dprev = d;
     }
     flush_chunk(acc, first, T, dprev, rp.L, e);
@@ -317,12 +318,13 @@ __global__ void __launch_bounds__(BS)
                   double* __restrict__ lam_out, int32_t* __restrict__ eR, int* __restrict__ eR_max) {
   __shared__ double sh[2 * BS / 32];
   const int j = blockIdx.x;
+  const int Lj = rp.tile_budgets ? rp.tileL[j / 256] : rp.L;
   const int eb = ellB[j] + scale8;
   const double* x1 = X1 + j * ldx1;
   dd t{0.0, 0.0};
   // pass 1: V (Alg. 1 line 1) and x̂_jᵀ v_j (line 3)
   for (int i = threadIdx.x; i < rows; i += BS) {
-    const dd v = recombine_elem(planes, pstride, static_cast<long long>(j) * rows + i, rp, ellA[i] + eb);
+    const dd v = recombine_elem(planes, pstride, static_cast<long long>(j) * rows + i, rp, ellA[i] + eb, Lj);
     Vh[j * ldv + i] = v.hi;
     Vl[j * ldv + i] = v.lo;
     t = dd_add(t, dd_mul_d(v, x1[i]));
@@ -357,6 +359,7 @@ __global__ void __launch_bounds__(BS)
                   int* __restrict__ eE_max, int* __restrict__ err) {
   __shared__ double sh[BS / 32];
   const int j = blockIdx.x;        // local column
+  const int Lj = rp.tile_budgets ? rp.tileL[j / 256] : rp.L;
   const int jg = col0 + j;         // global index of column j (its λ̂)
   const int eb = ellB[j] + scale8;
   const double lj = lam[jg];
@@ -367,7 +370,7 @@ __global__ void __launch_bounds__(BS)
     if (i == jg) {
       e = r_hi[j] * 0.5;  // ẽ_jj = r_j / 2
     } else {
-      const dd wv = recombine_elem(planes, pstride, static_cast<long long>(j) * rows + i, rp, ellA[i] + eb);
+      const dd wv = recombine_elem(planes, pstride, static_cast<long long>(j) * rows + i, rp, ellA[i] + eb, Lj);
       const double dl = __dsub_rn(lj, lam[i]);  // λ̃_j − λ̃_i
       if (dl == 0.0) bad = true;
       e = __ddiv_rn(wv.hi, dl);  // ẽ_ij = w_ij / (λ̃_j − λ̃_i)  (Alg. 1 line 5)
@@ -392,10 +395,11 @@ __global__ void __launch_bounds__(BS)
             double* __restrict__ X, long long ldx, double* __restrict__ nu2, double* __restrict__ wnext) {
   __shared__ double sh[BS / 32];
   const int j = blockIdx.x;
+  const int Lj = rp.tile_budgets ? rp.tileL[j / 256] : rp.L;
   const int eb = ellB[j] + scale8;  // the Q operand (digits of X̂^(1)/2^g) has ℓ = 0 on every row
   double s2 = 0.0, m = 0.0;
   for (int i = threadIdx.x; i < rows; i += BS) {
-    const dd u = recombine_elem(planes, pstride, static_cast<long long>(j) * rows + i, rp, eb);
+    const dd u = recombine_elem(planes, pstride, static_cast<long long>(j) * rows + i, rp, eb, Lj);
     const double x1 = X1[j * ldx1 + i];
     double s, e;
     two_sum(x1, u.hi, s, e);
@@ -419,9 +423,10 @@ __global__ void __launch_bounds__(BS)
                    const int32_t* __restrict__ ellA, const int32_t* __restrict__ ellB, int scale8,
                    double* __restrict__ Ch, double* __restrict__ Cl, long long ldc) {
   const int j = blockIdx.x;
+  const int Lj = rp.tile_budgets ? rp.tileL[j / 256] : rp.L;
   const int eb = ellB[j] + scale8;
   for (int i = threadIdx.x; i < rows; i += BS) {
-    const dd v = recombine_elem(planes, pstride, static_cast<long long>(j) * rows + i, rp, ellA[i] + eb);
+    const dd v = recombine_elem(planes, pstride, static_cast<long long>(j) * rows + i, rp, ellA[i] + eb, Lj);
     Ch[j * ldc + i] = v.hi;
     if (Cl) Cl[j * ldc + i] = v.lo;
   }

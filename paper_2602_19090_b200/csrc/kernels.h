@@ -18,6 +18,9 @@ struct RecombPlan {
   int nchunks;
   int chunk_first[kMaxChunks + 1];
   int diag[kPlanGroups];
+  // per-N-tile budgets (matches PairTable::tileL): column j only sums groups with diag <= tileL[j / 256]
+  int tile_budgets;
+  unsigned char tileL[256];
 };
 
 void launch_colmax(const double* X, long long ldx, int rows, int cols, double* w, int* err, cudaStream_t s);

@@ -193,6 +193,64 @@ int choose_L(int kA, int kB, int64_t K, int eA, int eB, double tau) {
   return kA + kB;
 }
 
+// Local gaps gap_j = min_{i≠j} |λ̂_i − λ̂_j| from the sorted λ̂ (fl-differences of neighbours).
+std::vector<double> col_gaps(const std::vector<double>& lam) {
+  const size_t n = lam.size();
+  std::vector<size_t> idx(n);
+  for (size_t i = 0; i < n; ++i) idx[i] = i;
+  std::stable_sort(idx.begin(), idx.end(), [&](size_t a, size_t b) { return lam[a] < lam[b]; });
+  std::vector<double> g(n, INFINITY);
+  for (size_t p = 0; p < n; ++p) {
+    double a = p > 0 ? lam[idx[p]] - lam[idx[p - 1]] : INFINITY;
+    double b = p + 1 < n ? lam[idx[p + 1]] - lam[idx[p]] : INFINITY;
+    g[idx[p]] = std::min(a, b);
+  }
+  return g;
+}
+
+int pairs_upto(int kA, int kB, int L) {
+  int np = 0;
+  for (int s = 1; s <= kA; ++s)
+    for (int t = 1; t <= kB; ++t)
+      if (s + t <= L) ++np;
+  return np;
+}
+
+// R8b: per-N-tile pair budgets. Column j of V = A·X̂ and of W = X̂ᵀRes only has to be accurate to
+// θ·δ'·gap_j (an error η in w_ij moves ẽ_ij by η/|λ_j − λ_i| ≤ η/gap_j), so each 256-column tile gets
+// the smallest L that meets the tightest column of the tile. Returns the max L over tiles and fills
+// tileL; *int8_pairs receives Σ_tiles pairs(L_t)·(tile width) / n (the average pairs per column).
+int tile_budgets(int kA, int kB, int64_t K, int eA, const std::vector<int>& eB_col, const std::vector<double>& tau_col,
+                 unsigned char* tileL, double* avg_pairs) {
+  const int64_t n = static_cast<int64_t>(tau_col.size());
+  const int64_t nt = (n + kTileN - 1) / kTileN;
+  int Lmax = 2;
+  double pw = 0.0;
+  for (int64_t t = 0; t < nt; ++t) {
+    double tau = INFINITY;
+    int eB = -100000;
+    const int64_t j1 = std::min<int64_t>(n, (t + 1) * kTileN);
+    for (int64_t j = t * kTileN; j < j1; ++j) {
+      tau = std::min(tau, tau_col[j]);
+      eB = std::max(eB, eB_col[j]);
+    }
+    int L = (eB == -100000) ? 2 : choose_L(kA, kB, K, eA, eB, tau);
+    L = std::max(2, std::min(L, kA + kB));
+    tileL[t] = static_cast<unsigned char>(L);
+    Lmax = std::max(Lmax, L);
+    pw += static_cast<double>(pairs_upto(kA, kB, L)) * static_cast<double>(j1 - t * kTileN);
+  }
+  *avg_pairs = pw / static_cast<double>(n);
+  return Lmax;
+}
+
+void apply_tiles(PairTable& pt, RecombPlan& rp, const unsigned char* tileL, int64_t n) {
+  const int64_t nt = (n + kTileN - 1) / kTileN;
+  pt.tile_budgets = 1;
+  rp.tile_budgets = 1;
+  for (int64_t t = 0; t < nt; ++t) pt.tileL[t] = rp.tileL[t] = tileL[t];
+}
+
 // Digits needed so that the fixed-point LSB 2^{e − S_k} ≤ 2^{lsb_max} (k clamped to [1, 15]).
 int digits_for(int emax, int lsb_max) {
   int k = 1;
@@ -371,8 +429,18 @@ ozr_status sweep(ozr_ctx ctx, const double* A, int64_t n, int64_t lda, double* X
     ozr_status e = split_A(ctx, A, n, lda, P.kA_split, st);
     if (e != OZR_OK) return e;
   }
-  const double tauV = P.theta_V * delta_p * gap;
-  int LV = P.L_V > 0 ? P.L_V : choose_L(st.kA_split, kx, n, st.eA_max, cmax, tauV);
+  // per-column accuracy of V (R8, R8b): θ_V·δ'·gap_j with the previous λ̂
+  const std::vector<double> gaps_prev = col_gaps(hlam);
+  std::vector<double> tau_col(n);
+  std::vector<int> c_col(n);
+  for (int64_t j = 0; j < n; ++j) {
+    tau_col[j] = P.theta_V * delta_p * (P.tile_budgets ? gaps_prev[j] : gap);
+    c_col[j] = hw[j] != 0.0 ? ceil_log2_host(hw[j]) : -100000;
+  }
+  unsigned char tileLV[kMaxNTiles];
+  double avg_pairs_V = 0.0;
+  int LV = tile_budgets(st.kA_split, kx, n, st.eA_max, c_col, tau_col, tileLV, &avg_pairs_V);
+  if (P.L_V > 0) LV = P.L_V;
   LV = std::min(LV, st.kA_split + kx);
   const int kA = std::min(st.kA_split, LV - 1);
   rep.kA = kA;
@@ -401,6 +469,8 @@ ozr_status sweep(ozr_ctx ctx, const double* A, int64_t n, int64_t lda, double* X
   PairTable pt;
   RecombPlan rp;
   if (!make_tables(gV, LV, n, pt, rp)) return fail(ctx, OZR_ERR_RANGE, "V plan too large");
+  const bool tilesV = P.tile_budgets && P.L_V <= 0;
+  if (tilesV) apply_tiles(pt, rp, tileLV, n);
   size_t maxG = gV.size();
   int32_t* planes = ctx->ws<int32_t>(S_PLANES, maxG * nn);
   OZR_ALLOC(planes);
@@ -410,8 +480,9 @@ ozr_status sweep(ozr_ctx ctx, const double* A, int64_t n, int64_t lda, double* X
     ozr_status e = run_gemm(ctx, opA, opX, N, N, N, pt, planes, 0);
     if (e != OZR_OK) return e;
   }
-  rep.pairs_V = count_pairs(gV);
-  ops += 2.0 * n * n * n * rep.pairs_V;
+  const double pV = tilesV ? avg_pairs_V : static_cast<double>(count_pairs(gV));
+  rep.pairs_V = static_cast<int>(std::lround(pV));
+  ops += 2.0 * n * n * n * pV;
 
   // ---- a4-a6: recombine V, λ̂, Res, column maxima
   double* Vh = ctx->ws<double>(S_VH, nn);
@@ -448,10 +519,23 @@ ozr_status sweep(ozr_ctx ctx, const double* A, int64_t n, int64_t lda, double* X
   OZR_CK(cudaGetLastError(), "split Res");
 
   // ---- a7: P3  W = X̂^(1)ᵀ Res  (Alg. 1 line 4)
-  int LW = P.L_W > 0 ? P.L_W : choose_L(kx, kR, n, cmax, eRmax, tauW / 2.0);
+  std::vector<int> eR_col(n);
+  OZR_CK(cudaMemcpyAsync(eR_col.data(), eR, n * sizeof(int32_t), cudaMemcpyDeviceToHost, s), "D2H eR");
+  OZR_CK(cudaStreamSynchronize(s), "sync");
+  const std::vector<double> gaps_new = col_gaps(hlam_new);
+  for (int64_t j = 0; j < n; ++j) {
+    tau_col[j] = 0.5 * P.theta_W * delta_p * (P.tile_budgets ? std::min(gaps_prev[j], gaps_new[j]) : gapW);
+    if (eR_col[j] < -1000) eR_col[j] = -100000;
+  }
+  unsigned char tileLW[kMaxNTiles];
+  double avg_pairs_W = 0.0;
+  int LW = tile_budgets(kx, kR, n, cmax, eR_col, tau_col, tileLW, &avg_pairs_W);
+  if (P.L_W > 0) LW = P.L_W;
   LW = std::min(LW, kx + kR);
   std::vector<Group> gW = plan_groups(kx, kR, LW, n);
   if (!make_tables(gW, LW, n, pt, rp)) return fail(ctx, OZR_ERR_RANGE, "W plan too large");
+  const bool tilesW = P.tile_budgets && P.L_W <= 0;
+  if (tilesW) apply_tiles(pt, rp, tileLW, n);
   if (gW.size() > maxG) {
     maxG = gW.size();
     planes = ctx->ws<int32_t>(S_PLANES, maxG * nn);
@@ -464,8 +548,9 @@ ozr_status sweep(ozr_ctx ctx, const double* A, int64_t n, int64_t lda, double* X
   }
   rep.kR = kR;
   rep.L_W = LW;
-  rep.pairs_W = count_pairs(gW);
-  ops += 2.0 * n * n * n * rep.pairs_W;
+  const double pW = tilesW ? avg_pairs_W : static_cast<double>(count_pairs(gW));
+  rep.pairs_W = static_cast<int>(std::lround(pW));
+  ops += 2.0 * n * n * n * pW;
 
   // ---- a8: Ẽ (Alg. 1 line 5), Ẽ' = diag(2^g) Ẽ
   double* Ep = ctx->ws<double>(S_EP, nn);
@@ -612,6 +697,7 @@ void ozr_params_default(ozr_params* p) {
   p->theta_W = 1.0 / 16;
   p->theta_U = 1.0 / 16;
   p->cluster_mode = 0;
+  p->tile_budgets = 1;
 }
 
 ozr_status ozr_split(ozr_ctx ctx, const double* M, const double* M_lo, int64_t rows, int64_t cols, int64_t ldm,

@@ -7,6 +7,8 @@ namespace ozr {
 
 constexpr int kMaxPairs = 256;   // digit pairs per product
 constexpr int kMaxGroups = 96;   // int32 accumulation groups (output planes) per product
+constexpr int kTileN = 256;      // N extent of one slice-GEMM tile
+constexpr int kMaxNTiles = 256;  // per-N-tile pair budgets: N <= 65536
 
 // A product C = Σ_groups Σ_{(s,t) in group} D^A_s · D^B_t is described by a pair table.
 // Group g accumulates pairs [first[g], first[g+1]) into ONE int32 plane out_plane[g].
@@ -18,6 +20,10 @@ struct PairTable {
   int diag[kMaxGroups];  // s+t (1-based digits) of the group: its weight 256^{-diag}
   unsigned char s[kMaxPairs];
   unsigned char t[kMaxPairs];
+  // Per-N-tile budgets (R8b): when tile_budgets != 0, tile `nt` (columns [256 nt, 256 nt + 256))
+  // only accumulates groups with diag <= tileL[nt]; the other CTAs exit without writing.
+  int tile_budgets;
+  unsigned char tileL[kMaxNTiles];
 };
 
 // Digit-plane operand: planes of int8, "column-major" i.e. plane[p][col][row] with row contiguous.
