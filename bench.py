@@ -234,7 +234,8 @@ def main():
     roofline = {"bound": "tensor", "achieved": achieved, "peak": int8_peak, "unit": "TFLOP/s", "frac": achieved / int8_peak,
                 "traffic": None, "dtype": "int8 (TOPS)",
                 "peak_source": f"2 x bf16_tflops_sustained of {src} MEASURED_PEAKS.json (nominal int8:bf16 = 2)",
-                "gemm_share_of_step": gemm_ms / ms}
+                "gemm_share_of_step": gemm_ms / ms,
+                "library_sweep_ms": sum(r["ms_total"] for r in reps) / len(reps)}
 
     # time to target: ozr_refine_to_tol from X̂0 (self-certified stop rule)
     X.copy_(X0)

@@ -59,11 +59,20 @@ __device__ __forceinline__ dd dd_div(dd a, dd b) {
   return o;
 }
 
+// 2^k as an fp64 built from its bit pattern (exact; valid for -1022 <= k <= 1023).
+__device__ __forceinline__ double pow2i(int k) {
+  return __longlong_as_double(static_cast<long long>(1023 + k) << 52);
+}
+// x · 2^k, exact for normal results: one multiply in the common range, scalbn otherwise.
+__device__ __forceinline__ double ldexp_fast(double x, int k) {
+  if (k >= -1022 && k <= 1023) return x * pow2i(k);
+  return scalbn(x, k);
+}
+
 // Correctly rounded (RNE) conversion of a signed 128-bit integer to fp64.
 __device__ __forceinline__ double i128_to_f64(i128 x) {
-  if (x == 0) return 0.0;
   const bool neg = x < 0;
-  u128 a = neg ? static_cast<u128>(-x) : static_cast<u128>(x);
+  const u128 a = neg ? static_cast<u128>(-x) : static_cast<u128>(x);
   const uint64_t hi = static_cast<uint64_t>(a >> 64);
   double r;
   if (hi == 0) {
@@ -73,17 +82,18 @@ __device__ __forceinline__ double i128_to_f64(i128 x) {
     const u128 b = a << lz;  // leading one at bit 127
     uint64_t top = static_cast<uint64_t>(b >> 64);
     top |= (static_cast<uint64_t>(b) != 0) ? 1ull : 0ull;  // sticky bit below the 11 guard bits
-    r = scalbn(__ull2double_rn(top), 64 - lz);
+    r = __ull2double_rn(top) * pow2i(64 - lz);
   }
   return neg ? -r : r;
 }
-// Exact conversion of an integer-valued fp64 to int128.
+// Exact conversion of an integer-valued fp64 to int128 (bit-level: mantissa << exponent).
 __device__ __forceinline__ i128 f64int_to_i128(double h) {
-  if (fabs(h) < 9007199254740992.0) return static_cast<i128>(static_cast<long long>(h));
-  int e;
-  const double m = frexp(h, &e);  // h = m 2^e, 0.5 <= |m| < 1, e > 53
-  const long long mi = static_cast<long long>(scalbn(m, 53));
-  return static_cast<i128>(mi) << (e - 53);
+  if (fabs(h) < 9007199254740992.0) return static_cast<i128>(__double2ll_rz(h));
+  const long long bits = __double_as_longlong(h);
+  const int ex = static_cast<int>((bits >> 52) & 0x7FF) - 1075;  // h = ±m 2^ex, m in [2^52, 2^53)
+  const long long m = (bits & 0xFFFFFFFFFFFFFLL) | 0x10000000000000LL;
+  const i128 v = static_cast<i128>(static_cast<u128>(m) << ex);
+  return (bits < 0) ? -v : v;
 }
 // Correctly rounded double-double of an exact int128: hi = RN(x), lo = RN(x - hi).
 __device__ __forceinline__ dd i128_to_dd(i128 x) {
@@ -95,12 +105,18 @@ __device__ __forceinline__ dd i128_to_dd(i128 x) {
 // Integer nearest to an fp64 (RNE), exactly, as int128 (|x| < 2^126).
 __device__ __forceinline__ i128 rint_to_i128(double x) { return f64int_to_i128(rint(x)); }
 
-// ⌈log2 v⌉ for v > 0 from the exponent field (R2); 0 for v == 0.
+// ⌈log2 v⌉ for v > 0 from the exponent field (R2); 0 for v == 0 (v normal).
 __device__ __forceinline__ int ceil_log2_d(double v) {
   if (v == 0.0) return 0;
-  int e;
-  const double m = frexp(v, &e);
-  return (m == 0.5) ? e - 1 : e;
+  const long long bits = __double_as_longlong(v);
+  const int be = static_cast<int>((bits >> 52) & 0x7FF);
+  if (be == 0) {  // subnormal: fall back
+    int e;
+    const double m = frexp(v, &e);
+    return (m == 0.5) ? e - 1 : e;
+  }
+  const bool pow2 = (bits & 0xFFFFFFFFFFFFFLL) == 0;
+  return be - 1023 + (pow2 ? 0 : 1);
 }
 
 // R5: k excess-128 base-256 digits of p, most significant first: p = Σ d_s 256^{k-s}, d_s ∈ [-128,127].

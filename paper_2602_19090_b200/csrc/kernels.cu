@@ -92,8 +92,8 @@ __device__ __forceinline__ i128 block_sum_i128(i128 v, i128* sh) {  // exact: or
 __device__ __forceinline__ void flush_chunk(dd& acc, bool& first, i128 T, int dlast, int L, int e) {
   dd v = i128_to_dd(T);
   const int sc = 8 * (L - dlast) + e;
-  v.hi = scalbn(v.hi, sc);
-  v.lo = scalbn(v.lo, sc);
+  v.hi = ldexp_fast(v.hi, sc);
+  v.lo = ldexp_fast(v.lo, sc);
   acc = first ? v : dd_add(acc, v);
   first = false;
 }
@@ -202,7 +202,7 @@ __global__ void __launch_bounds__(BS)
       const double x = (i < rows) ? col[i] : 0.0;
       const double x1 = __dsub_rn(__dadd_rn(tau, x), tau);  // eq. (x), s = 1: fl(fl(τ + x) − τ)
       if (i < rows) x1c[i] = x1;
-      q[r] = __double2ll_rn(scalbn(x1, -g));  // exact integer, |q| <= 2^{53-β}
+      q[r] = __double2ll_rn(ldexp_fast(x1, -g));  // exact integer, |q| <= 2^{53-β}
       sq += static_cast<i128>(q[r]) * q[r];
     }
     store_digits4<long long>(q, kx, dig + j * ldd + i0, pstride);
@@ -242,8 +242,8 @@ __device__ __forceinline__ void split_fixed_body(const double* __restrict__ col,
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
       const int i = i0 + r;
-      p[r] = (i < rows) ? rint_to<T>(scalbn(col[i], S - e)) : T(0);
-      if (cl && i < rows) p[r] += rint_to<T>(scalbn(cl[i], S - e));
+      p[r] = (i < rows) ? rint_to<T>(ldexp_fast(col[i], S - e)) : T(0);
+      if (cl && i < rows) p[r] += rint_to<T>(ldexp_fast(cl[i], S - e));
     }
     store_digits4<T>(p, k, base + i0, pstride);
   }
@@ -277,19 +277,27 @@ __global__ void __launch_bounds__(BS)
 __global__ void k_transpose_i8(const int8_t* __restrict__ src, long long lds, long long sps, int8_t* __restrict__ dst,
                                long long ldt, long long tps, int rows, int cols) {
   // src element (i,j) at src[p*sps + j*lds + i]; dst element (i,j) at dst[p*tps + i*ldt + j]
-  __shared__ int8_t t[64][65];
+  // 64 x 64 byte tile, 32-bit global loads and stores (lds, ldt are multiples of 16, so the 4-byte
+  // groups that straddle `rows` / `cols` stay inside each line's padding).
+  __shared__ uint8_t t[64][68];
   const int p = blockIdx.z;
   const int i0 = blockIdx.x * 64, j0 = blockIdx.y * 64;
-  for (int e = threadIdx.x; e < 64 * 64; e += blockDim.x) {
-    const int ii = e & 63, jj = e >> 6;
-    const int i = i0 + ii, j = j0 + jj;
-    t[jj][ii] = (i < rows && j < cols) ? src[p * sps + j * lds + i] : 0;
+  for (int e = threadIdx.x; e < 64 * 16; e += blockDim.x) {
+    const int i4 = (e & 15) * 4, jj = e >> 4;
+    const int i = i0 + i4, j = j0 + jj;
+    uint32_t v = 0;
+    if (i < rows && j < cols) v = *reinterpret_cast<const uint32_t*>(src + p * sps + j * lds + i);
+    *reinterpret_cast<uint32_t*>(&t[jj][i4]) = v;
   }
   __syncthreads();
-  for (int e = threadIdx.x; e < 64 * 64; e += blockDim.x) {
-    const int jj = e & 63, ii = e >> 6;
-    const int i = i0 + ii, j = j0 + jj;
-    if (i < rows && j < cols) dst[p * tps + static_cast<long long>(i) * ldt + j] = t[jj][ii];
+  for (int e = threadIdx.x; e < 64 * 16; e += blockDim.x) {
+    const int j4 = (e & 15) * 4, ii = e >> 4;
+    const int i = i0 + ii, j = j0 + j4;
+    if (i < rows && j < cols) {
+      const uint32_t v = static_cast<uint32_t>(t[j4][ii]) | (static_cast<uint32_t>(t[j4 + 1][ii]) << 8) |
+                         (static_cast<uint32_t>(t[j4 + 2][ii]) << 16) | (static_cast<uint32_t>(t[j4 + 3][ii]) << 24);
+      *reinterpret_cast<uint32_t*>(dst + p * tps + static_cast<long long>(i) * ldt + j) = v;
+    }
   }
 }
 
@@ -356,7 +364,7 @@ __global__ void __launch_bounds__(BS)
                   const int32_t* __restrict__ ellA, const int32_t* __restrict__ ellB, int scale8,
                   const double* __restrict__ r_hi, const double* __restrict__ lam, const int32_t* __restrict__ gX,
                   int col0, double* __restrict__ Ep, long long lde, double* __restrict__ nrm2,
-                  int* __restrict__ eE_max, int* __restrict__ err) {
+                  int* __restrict__ eE_max, int32_t* __restrict__ eE_col, int* __restrict__ err) {
   __shared__ double sh[BS / 32];
   const int j = blockIdx.x;        // local column
   const int Lj = rp.tile_budgets ? rp.tileL[j / 256] : rp.L;
@@ -376,7 +384,7 @@ __global__ void __launch_bounds__(BS)
       e = __ddiv_rn(wv.hi, dl);  // ẽ_ij = w_ij / (λ̃_j − λ̃_i)  (Alg. 1 line 5)
     }
     s2 = __fma_rn(e, e, s2);
-    const double ep = scalbn(e, gX[i]);  // Ẽ' = diag(2^g) Ẽ (exact)
+    const double ep = ldexp_fast(e, gX[i]);  // Ẽ' = diag(2^g) Ẽ (exact)
     Ep[j * lde + i] = ep;
     m = fmax(m, fabs(ep));
   }
@@ -385,6 +393,7 @@ __global__ void __launch_bounds__(BS)
   s2 = block_sum(s2, sh);
   if (threadIdx.x == 0) {
     nrm2[j] = s2;
+    eE_col[j] = (m > 0.0) ? ceil_log2_d(m) : -100000;
     if (m > 0.0) atomicMax(eE_max, ceil_log2_d(m));
   }
 }
@@ -467,10 +476,11 @@ void launch_recombine_V(const int32_t* planes, long long pstride, int rows, int 
 }
 void launch_recombine_E(const int32_t* planes, long long pstride, int rows, int cols, const RecombPlan& rp,
                         const int32_t* ellA, const int32_t* ellB, int scale8, const double* r_hi, const double* lam,
-                        const int32_t* gX, int col0, double* Ep, long long lde, double* nrm2, int* eE_max, int* err,
+                        const int32_t* gX, int col0, double* Ep, long long lde, double* nrm2, int* eE_max,
+                        int32_t* eE_col, int* err,
                         cudaStream_t s) {
   k_recombine_E<<<cols, BS, 0, s>>>(planes, pstride, rows, rp, ellA, ellB, scale8, r_hi, lam, gX, col0, Ep, lde, nrm2,
-                                    eE_max, err);
+                                    eE_max, eE_col, err);
 }
 void launch_final(const int32_t* planes, long long pstride, int rows, int cols, const RecombPlan& rp,
                   const int32_t* ellB, int scale8, const double* X1, long long ldx1, double* X, long long ldx,

@@ -39,7 +39,8 @@ void launch_recombine_V(const int32_t* planes, long long pstride, int rows, int 
                         double* lam_out, int32_t* eR, int* eR_max, cudaStream_t s);
 void launch_recombine_E(const int32_t* planes, long long pstride, int rows, int cols, const RecombPlan& rp,
                         const int32_t* ellA, const int32_t* ellB, int scale8, const double* r_hi, const double* lam,
-                        const int32_t* gX, int col0, double* Ep, long long lde, double* nrm2, int* eE_max, int* err,
+                        const int32_t* gX, int col0, double* Ep, long long lde, double* nrm2, int* eE_max,
+                        int32_t* eE_col, int* err,
                         cudaStream_t s);
 void launch_final(const int32_t* planes, long long pstride, int rows, int cols, const RecombPlan& rp,
                   const int32_t* ellB, int scale8, const double* X1, long long ldx1, double* X, long long ldx,

@@ -6,6 +6,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -40,6 +41,37 @@ struct ozr_ctx_s {
   std::vector<DevBuf> bufs;
   cudaEvent_t ev[8];
   bool events = false;
+  // tracing (OZR_TRACE=1): named events between the kernels of a sweep, printed to stderr per sweep
+  bool trace = false;
+  std::vector<cudaEvent_t> tev;
+  std::vector<const char*> tname;
+  int tn = 0;
+  void mark(const char* name) {
+    if (!trace) return;
+    if (tn >= static_cast<int>(tev.size())) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      tev.push_back(e);
+      tname.push_back(name);
+    }
+    tname[tn] = name;
+    cudaEventRecord(tev[tn++], stream);
+  }
+  void dump() {
+    if (!trace || tn < 2) {
+      tn = 0;
+      return;
+    }
+    cudaEventSynchronize(tev[tn - 1]);
+    fprintf(stderr, "[ozr trace]");
+    for (int i = 1; i < tn; ++i) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, tev[i - 1], tev[i]);
+      fprintf(stderr, " %s=%.3f", tname[i], ms);
+    }
+    fprintf(stderr, "\n");
+    tn = 0;
+  }
 
   // Workspace slot: grow-only device buffer.
   template <typename T>
@@ -371,6 +403,7 @@ ozr_status sweep(ozr_ctx ctx, const double* A, int64_t n, int64_t lda, double* X
   const int64_t ld = round16(n);
   const int64_t nn = n * n;
   cudaEventRecord(ctx->ev[0], s);
+  ctx->mark("start");
   float gemm_ms = 0.f;
   double ops = 0.0;
 
@@ -429,6 +462,7 @@ ozr_status sweep(ozr_ctx ctx, const double* A, int64_t n, int64_t lda, double* X
     ozr_status e = split_A(ctx, A, n, lda, P.kA_split, st);
     if (e != OZR_OK) return e;
   }
+  ctx->mark("stats+splitA");
   // per-column accuracy of V (R8, R8b): θ_V·δ'·gap_j with the previous λ̂
   const std::vector<double> gaps_prev = col_gaps(hlam);
   std::vector<double> tau_col(n);
@@ -461,6 +495,7 @@ ozr_status sweep(ozr_ctx ctx, const double* A, int64_t n, int64_t lda, double* X
   launch_x1_split(X, ldx, N, N, beta, kx, w, X1, n, xdig, ld, ld * n, g, sh, sl, rh, rl, derr, s);
   OZR_CK(cudaGetLastError(), "x1 split");
   launch_transpose_i8(xdig, ld, ld * n, xdigT, ld, ld * n, N, N, kx, s);
+  ctx->mark("x1split+transpose");
   OZR_CK(cudaGetLastError(), "transpose digits");
   OZR_CK(cudaMemsetAsync(zell, 0, n * sizeof(int32_t), s), "memset");
 
@@ -480,6 +515,7 @@ ozr_status sweep(ozr_ctx ctx, const double* A, int64_t n, int64_t lda, double* X
     ozr_status e = run_gemm(ctx, opA, opX, N, N, N, pt, planes, 0);
     if (e != OZR_OK) return e;
   }
+  ctx->mark("gemmV");
   const double pV = tilesV ? avg_pairs_V : static_cast<double>(count_pairs(gV));
   rep.pairs_V = static_cast<int>(std::lround(pV));
   ops += 2.0 * n * n * n * pV;
@@ -495,6 +531,7 @@ ozr_status sweep(ozr_ctx ctx, const double* A, int64_t n, int64_t lda, double* X
   launch_recombine_V(planes, nn, N, N, rp, reinterpret_cast<const int32_t*>(ctx->bufs[S_AELL].p), g,
                      8 * (st.kA_split + kx - LV), X1, n, sh, sl, Vh, Vl, n, lam, eR, demax, s);
   OZR_CK(cudaGetLastError(), "recombine V");
+  ctx->mark("recombV");
   int eRmax = 0;
   std::vector<double> hlam_new(n);
   OZR_CK(cudaMemcpyAsync(&eRmax, demax, sizeof(int), cudaMemcpyDeviceToHost, s), "D2H");
@@ -517,6 +554,7 @@ ozr_status sweep(ozr_ctx ctx, const double* A, int64_t n, int64_t lda, double* X
   OZR_ALLOC(rdig); OZR_ALLOC(rell);
   launch_split_fixed(Vh, Vl, n, N, N, kR, rdig, ld, ld * n, rell, derr, s);
   OZR_CK(cudaGetLastError(), "split Res");
+  ctx->mark("host+splitRes");
 
   // ---- a7: P3  W = X̂^(1)ᵀ Res  (Alg. 1 line 4)
   std::vector<int> eR_col(n);
@@ -546,6 +584,7 @@ ozr_status sweep(ozr_ctx ctx, const double* A, int64_t n, int64_t lda, double* X
     ozr_status e = run_gemm(ctx, opX, opR, N, N, N, pt, planes, 1);
     if (e != OZR_OK) return e;
   }
+  ctx->mark("host+gemmW");
   rep.kR = kR;
   rep.L_W = LW;
   const double pW = tilesW ? avg_pairs_W : static_cast<double>(count_pairs(gW));
@@ -557,8 +596,10 @@ ozr_status sweep(ozr_ctx ctx, const double* A, int64_t n, int64_t lda, double* X
   double* nrm2 = ctx->ws<double>(S_NRM2, n);
   OZR_ALLOC(Ep); OZR_ALLOC(nrm2);
   OZR_CK(cudaMemcpyAsync(demax, &intmin, sizeof(int), cudaMemcpyHostToDevice, s), "H2D");
-  launch_recombine_E(planes, nn, N, N, rp, g, rell, 8 * (kx + kR - LW), rh, lam, g, 0, Ep, n, nrm2, demax, derr, s);
+  launch_recombine_E(planes, nn, N, N, rp, g, rell, 8 * (kx + kR - LW), rh, lam, g, 0, Ep, n, nrm2, demax, eR, derr,
+                     s);
   OZR_CK(cudaGetLastError(), "recombine E");
+  ctx->mark("recombE");
   int eEmax = 0;
   OZR_CK(cudaMemcpyAsync(&eEmax, demax, sizeof(int), cudaMemcpyDeviceToHost, s), "D2H");
   {
@@ -578,11 +619,22 @@ ozr_status sweep(ozr_ctx ctx, const double* A, int64_t n, int64_t lda, double* X
   const int kE = digits_for(eEmax, static_cast<int>(std::floor(std::log2(tauU / 2.0))) + gmin);
   launch_split_fixed(Ep, nullptr, n, N, N, kE, rdig, ld, ld * n, rell, derr, s);
   OZR_CK(cudaGetLastError(), "split E");
+  ctx->mark("host+splitE");
   const int SX = 8 * (kx - 1) + 6;
-  int LU = P.L_U > 0 ? P.L_U : choose_L(kx, kE, n, SX, eEmax, tauU / 2.0);
+  // R8b for X̂Ẽ: uniform accuracy θ_U·δ', but columns with small corrections need fewer pairs
+  std::vector<int> eE_col(n);
+  OZR_CK(cudaMemcpyAsync(eE_col.data(), eR, n * sizeof(int32_t), cudaMemcpyDeviceToHost, s), "D2H eE");
+  OZR_CK(cudaStreamSynchronize(s), "sync");
+  for (int64_t j = 0; j < n; ++j) tau_col[j] = tauU / 2.0;
+  unsigned char tileLU[kMaxNTiles];
+  double avg_pairs_U = 0.0;
+  int LU = tile_budgets(kx, kE, n, SX, eE_col, tau_col, tileLU, &avg_pairs_U);
+  if (P.L_U > 0) LU = P.L_U;
   LU = std::min(LU, kx + kE);
   std::vector<Group> gU = plan_groups(kx, kE, LU, n);
   if (!make_tables(gU, LU, n, pt, rp)) return fail(ctx, OZR_ERR_RANGE, "U plan too large");
+  const bool tilesU = P.tile_budgets && P.L_U <= 0;
+  if (tilesU) apply_tiles(pt, rp, tileLU, n);
   if (gU.size() > maxG) {
     maxG = gU.size();
     planes = ctx->ws<int32_t>(S_PLANES, maxG * nn);
@@ -594,14 +646,17 @@ ozr_status sweep(ozr_ctx ctx, const double* A, int64_t n, int64_t lda, double* X
     ozr_status e = run_gemm(ctx, opQ, opE, N, N, N, pt, planes, 2);
     if (e != OZR_OK) return e;
   }
+  ctx->mark("gemmU");
   rep.kE = kE;
   rep.L_U = LU;
-  rep.pairs_U = count_pairs(gU);
-  ops += 2.0 * n * n * n * rep.pairs_U;
+  const double pU = tilesU ? avg_pairs_U : static_cast<double>(count_pairs(gU));
+  rep.pairs_U = static_cast<int>(std::lround(pU));
+  ops += 2.0 * n * n * n * pU;
   double* nu2 = ctx->ws<double>(S_NU2, n);
   OZR_ALLOC(nu2);
   launch_final(planes, nn, N, N, rp, rell, 8 * (kx + kE - LU), X1, n, X, ldx, nu2, wnext, s);
   OZR_CK(cudaGetLastError(), "final update");
+  ctx->mark("final");
   OZR_CK(cudaMemcpyAsync(lambda, lam, n * sizeof(double), cudaMemcpyDeviceToDevice, s), "copy lambda");
   cudaEventRecord(ctx->ev[1], s);
   std::vector<double> hnu(n), hnrm(n);
@@ -632,6 +687,7 @@ ozr_status sweep(ozr_ctx ctx, const double* A, int64_t n, int64_t lda, double* X
   rep.ms_total = tot;
   rep.ms_gemm = gemm_ms;
   rep.int8_ops = ops;
+  ctx->dump();
   // kernels of this sweep: [colmax] x1_split transpose GEMM recombine_V split GEMM recombine_E split GEMM final
   rep.launches = (fresh_w ? 1 : 0) + 10;
   return OZR_OK;
@@ -665,6 +721,8 @@ ozr_status ozr_create(ozr_ctx* out, int device, void* stream, int64_t n_max) {
   c->stream = static_cast<cudaStream_t>(stream);
   for (int i = 0; i < 8; ++i) cudaEventCreate(&c->ev[i]);
   c->events = true;
+  const char* tr = getenv("OZR_TRACE");
+  c->trace = tr && tr[0] == '1';
   *out = c;
   return OZR_OK;
 }
