@@ -117,8 +117,12 @@ typedef struct {
   double theta_V, theta_W, theta_U; /* accuracy targets of the three products as fractions of δ'·gap (V, W)
                                        and δ' (X̂Ẽ) (R8; defaults 1/16, 1/16, 1/16)  */
   int L_V, L_W, L_U; /* > 0: force the pair budgets (s+t ≤ L) instead of the planner          */
-  int cluster_mode;  /* 0: error on equal λ̂; 1: OA threshold branch (R13)      */
+  int cluster_mode;  /* 0: the paper's Algorithm 1 — equal λ̂ are an error;
+                        1: unresolved groups (|ẽ_ij| > κ or λ̂_i = λ̂_j) get a Rayleigh–Ritz sub-solve
+                           in span(X̂^(1)_J) (R13) [default]                          */
   int tile_budgets;  /* 1: per-256-column pair budgets from the local gaps gap_j (R8b) [default]  */
+  double kappa;      /* cluster_mode 1: linearisation threshold κ on |ẽ_ij| (default 2^-10)     */
+  int max_cluster;   /* cluster_mode 1: largest group solved (default 4096; larger → OZR_ERR_RANGE) */
 } ozr_params;
 
 void ozr_params_default(ozr_params* p);
@@ -129,7 +133,8 @@ typedef struct {
   int kX, kA, kR, kE;               /* digit counts of X̂^(1), A (prefix used), Res, Ẽ'               */
   int L_V, L_W, L_U;                /* pair budgets                                                    */
   int pairs_V, pairs_W, pairs_U;    /* INT8 slice products (each an n x n_local x n INT8 GEMM)         */
-  int n_clusters;                   /* pairs |λ̂_i − λ̂_j| ≤ ω treated by the cluster branch              */
+  int n_clusters;                   /* unresolved groups given the Rayleigh–Ritz sub-solve (R13)       */
+  int max_cluster;                  /* size of the largest such group                                  */
   int launches;                     /* CUDA kernels this sweep launched                                */
   double gap_min, max_abs_lambda;   /* from the λ̂ that chose β                                         */
   double normE_fro;                 /* ‖Ẽ‖_F                                                          */
@@ -145,6 +150,12 @@ typedef struct {
  * Errors: OZR_ERR_ARG, OZR_ERR_RANGE (δ ≤ u), OZR_ERR_DEGENERATE, OZR_ERR_CUDA, OZR_ERR_NOMEM. */
 ozr_status ozr_refine_step(ozr_ctx ctx, const double* A, int64_t n, int64_t lda, double* X, int64_t ldx,
                            double* lambda, const ozr_params* params, ozr_step_report* report);
+
+/* Host: the unresolved groups of the context's last sweep (cluster_mode 1). members receives the global
+ * column indices of every group, concatenated, each group in ascending (λ̂, index) order; offsets[g] is
+ * the start of group g (offsets has ngroups + 1 entries). Returns OZR_ERR_RANGE if a buffer is too small
+ * (*ngroups / offsets still tell the sizes needed when offsets has room). */
+ozr_status ozr_last_clusters(ozr_ctx ctx, int* members, int max_members, int* offsets, int max_groups, int* ngroups);
 
 /* Repeat sweeps until the stop rule (R12): after sweep k stop when ν_k ≤ δ or ν_k² max|λ̂| /
  * (n gap) ≤ δ; report OZR_ERR_NOT_CONVERGED on stagnation (ν_k > ν_{k−1}/2) or when max_sweeps is

@@ -15,7 +15,7 @@ import numpy as np
 
 from . import _clib
 from .fp import U, ceil_log2, dd_add, dd_div_dd, fast_two_sum, two_prod, two_sum
-from .split import (alpha_dense, alpha_theoretical, beta_dense, beta_theoretical, gap_min, sum_pow2_2c,
+from .split import (alpha_dense, alpha_theoretical, beta_dense, beta_theoretical, gap_min, gap_pos, sum_pow2_2c,
                     x1_truncate)
 
 BETA_MIN, BETA_MAX = 2, 52  # reading R4: τ + x stays in τ's binade iff β ≥ 2; ≥ 1 bit kept iff β ≤ 52
@@ -34,19 +34,110 @@ def col_dot_dd(X, Yh, Yl=None):
     return sh, sl
 
 
-def choose_beta(n, delta_p, lam_prev, c, w, beta_mode="dense", xi=None):
-    """β for this sweep from the PREVIOUS sweep's λ̂ (reading R9; the paper computes λ̂ only after V)."""
+def choose_beta(n, delta_p, lam_prev, c, w, beta_mode="dense", xi=None, cluster_mode=1):
+    """β for this sweep from the PREVIOUS sweep's λ̂ (reading R9; the paper computes λ̂ only after V).
+    With the cluster branch, equal estimates are tolerated and the smallest positive gap is used (R13)."""
+    gap = gap_min(lam_prev)
+    if cluster_mode and not gap > 0:
+        gap = gap_pos(lam_prev)
     if beta_mode == "dense":
-        b = beta_dense(n, delta_p, lam_prev, c, w)
+        b = beta_dense(n, delta_p, lam_prev, c, w, gap)
         a = alpha_dense(n, min(max(b, BETA_MIN), BETA_MAX))
     else:
-        b = beta_theoretical(xi if xi else n, delta_p, lam_prev, c, w)
+        b = beta_theoretical(xi if xi else n, delta_p, lam_prev, c, w, gap)
         a = alpha_theoretical(n, min(max(b, BETA_MIN), BETA_MAX))
     return b, a
 
 
-def sweep(A, X, lam_prev, delta, theta=1.0, beta=None, beta_mode="dense", xi=None, truncate=True):
-    """One iteration of Algorithm 1. Returns (X_new fp64, λ̂ fp64, info dict)."""
+KAPPA_DEFAULT = 2.0 ** -10
+
+
+def unresolved_groups(E, lam, kappa=KAPPA_DEFAULT):
+    """Reading R13 (builder-defined; PAPER.md:333 and 730 leave clusters open): the first-order
+    correction ẽ_ij = w_ij / (λ̂_j − λ̂_i) of Algorithm 1 line 5 linearises (I + E)^{-1}
+    and is only trustworthy while |ẽ_ij| ≪ 1. Pairs (i, j), i ≠ j, with λ̂_i = λ̂_j or |ẽ_ij| > κ are
+    "unresolved"; the groups are the connected components of that graph with ≥ 2 members, each listed
+    in ascending (λ̂, index) order, the groups ordered by their first member. E: n x n with the
+    first-order values off the diagonal (0 where λ̂_i = λ̂_j)."""
+    n = E.shape[0]
+    parent = list(range(n))
+
+    def find(a):
+        while parent[a] != a:
+            parent[a] = parent[parent[a]]
+            a = parent[a]
+        return a
+
+    dl = lam[None, :] - lam[:, None]
+    mask = (np.abs(E) > kappa) | (dl == 0)
+    np.fill_diagonal(mask, False)
+    for i, j in zip(*np.nonzero(mask)):
+        a, b = find(int(i)), find(int(j))
+        if a != b:
+            parent[max(a, b)] = min(a, b)
+    groups = {}
+    for i in range(n):
+        groups.setdefault(find(i), []).append(i)
+    out = []
+    for g in groups.values():
+        if len(g) >= 2:
+            out.append(sorted(g, key=lambda k: (lam[k], k)))
+    out.sort(key=lambda J: J[0])
+    return out
+
+
+def cluster_subsolve(E, lam, J, X1, Wh, Wl, rh, rl):
+    """Rayleigh–Ritz in span(X̂^(1)_J) for one unresolved group J (reading R13; the construction follows
+    the cited Ogita–Aishima cluster refinement, restated here — parity unpinned).
+    With G = X̂ᵀX̂ = I − R and S = X̂ᵀAX̂ = W + (I − R)D̂ (Alg. 1 line 4):
+      μ = mean λ̂_J,  M = S_JJ − μ G_JJ = W_JJ + (I − R_JJ)(D̂_J − μI),  K₀ = (M + Mᵀ)/2,
+      C = I + R_JJ/2  (= G_JJ^{-1/2} to first order),  K = C K₀ C = Y Θ Yᵀ  (Θ ascending),
+      Z = C Y:  Ẽ_JJ ← Z − I,  Ẽ_{i,J} ← Ẽ_{i,J} Z for i ∉ J,  λ̂_J ← μ + Θ.
+    Y's column k is signed so that y_kk ≥ 0 (the largest-|y| entry positive if y_kk = 0).
+    R_JJ: r_jj = r_j exact; r_ij = −x̂_iᵀx̂_j (i ≠ j) in double-double. Modifies E and lam in place."""
+    J = np.asarray(J)
+    m = len(J)
+    XJ = np.ascontiguousarray(X1[:, J].T)
+    Gh, Gl = _clib.dd_gemm_nt(XJ, XJ)
+    R = -(Gh + Gl)
+    R[np.arange(m), np.arange(m)] = rh[J] + rl[J]
+    mu = 0.0
+    for j in J:
+        mu = mu + lam[j]
+    mu = mu / m
+    WJ = Wh[np.ix_(J, J)] + Wl[np.ix_(J, J)]
+    M = WJ + (np.eye(m) - R) * (lam[J] - mu)[None, :]
+    K0 = (M + M.T) * 0.5
+    C = np.eye(m) + R * 0.5
+    K = C @ K0 @ C
+    K = (K + K.T) * 0.5
+    th, tl, Yh, Yl, _ = _clib.jacobi_q(K)
+    Y = Yh + Yl
+    for k in range(m):
+        piv = Y[k, k] if Y[k, k] != 0 else Y[np.argmax(np.abs(Y[:, k])), k]
+        if piv < 0:
+            Y[:, k] = -Y[:, k]
+    Z = C @ Y
+    notJ = np.setdiff1d(np.arange(E.shape[0]), J)
+    E[np.ix_(notJ, J)] = E[np.ix_(notJ, J)] @ Z
+    E[np.ix_(J, J)] = Z - np.eye(m)
+    lam[J] = mu + (th + tl)
+    # conditioning of the sub-solve: ‖K‖ / min eigenvalue gap of K (an fp64 eigensolver's eigenvectors
+    # are accurate to ~u·this; the tests derive their tolerance for clustered sweeps from it)
+    gK = np.min(np.diff(th)) if m > 1 else np.inf
+    return float(np.max(np.abs(th)) / gK) if gK > 0 else np.inf
+
+
+def sweep(A, X, lam_prev, delta, theta=1.0, beta=None, beta_mode="dense", xi=None, truncate=True,
+          cluster_mode=1, kappa=KAPPA_DEFAULT, max_cluster=None, groups=None):
+    """One iteration of Algorithm 1. Returns (X_new fp64, λ̂ fp64, info dict).
+
+    cluster_mode 0: the paper's Algorithm 1 (distinct eigenvalues assumed); equal
+    λ̂ raise. cluster_mode 1: unresolved groups get a Rayleigh–Ritz sub-solve (cluster_subsolve,
+    DESIGN.md reading R13; not in the paper — parity unpinned beyond the tests listed there).
+    groups: use these unresolved groups instead of finding them (parity runs: a pair whose |ẽ_ij| sits
+    at κ may be classified differently by the GPU's digit-budget W; the tests check that is the only
+    difference, then evaluate the same groups)."""
     A = np.asarray(A, dtype=np.float64)
     X = np.asarray(X, dtype=np.float64)
     n = A.shape[0]
@@ -54,7 +145,7 @@ def sweep(A, X, lam_prev, delta, theta=1.0, beta=None, beta_mode="dense", xi=Non
     w = np.max(np.abs(X), axis=0)
     c = ceil_log2(w)
     if beta is None:
-        beta, alpha = choose_beta(n, delta / theta, lam_prev, c, w, beta_mode, xi)
+        beta, alpha = choose_beta(n, delta / theta, lam_prev, c, w, beta_mode, xi, cluster_mode)
     else:
         alpha = alpha_dense(n, beta)
     info["beta_raw"] = int(beta)
@@ -82,10 +173,23 @@ def sweep(A, X, lam_prev, delta, theta=1.0, beta=None, beta_mode="dense", xi=Non
     # line 5: ẽ_ij = w_ij / (λ̃_j − λ̃_i), i ≠ j;  ẽ_ii = r_i / 2
     dl = lam[None, :] - lam[:, None]
     off = ~np.eye(n, dtype=bool)
-    if np.any(dl[off] == 0):
+    if cluster_mode == 0 and np.any(dl[off] == 0):
         raise ValueError("clustered eigenvalues: equal λ̂ (PAPER.md:333 assumes none)")
-    E = np.where(off, W / np.where(off, dl, 1.0), 0.0)
+    with np.errstate(divide="ignore", invalid="ignore"):
+        E = np.where(off & (dl != 0), Wh / np.where(dl != 0, dl, 1.0), 0.0)
     E[np.arange(n), np.arange(n)] = (rh + rl) / 2
+    info["clusters"] = []
+    info["E_first_order"] = E.copy() if cluster_mode else None
+    info["lam_rq"] = lam.copy()
+    if cluster_mode:
+        comps = unresolved_groups(E, lam, kappa) if groups is None else [list(J) for J in groups]
+        if max_cluster and any(len(J) > max_cluster for J in comps):
+            raise ValueError("cluster larger than max_cluster")
+        conds = []
+        for J in comps:
+            conds.append(cluster_subsolve(E, lam, J, X1, Wh, Wl, rh, rl))
+        info["clusters"] = comps
+        info["cluster_cond"] = max(conds, default=0.0)
     # line 6: X̂ <- accsum(X̂, X̂Ẽ)  on X̂^(1) (eq. E')
     Uh, Ul = _clib.dd_gemm_nt(X1, np.ascontiguousarray(E.T))
     s, e = two_sum(X1, Uh)
@@ -101,7 +205,8 @@ def sweep(A, X, lam_prev, delta, theta=1.0, beta=None, beta_mode="dense", xi=Non
     return Xn, lam, info
 
 
-def refine_to_tol(A, X0, lam0, delta, theta=1.0, max_sweeps=6, beta_mode="dense", xi=None, callback=None):
+def refine_to_tol(A, X0, lam0, delta, theta=1.0, max_sweeps=6, beta_mode="dense", xi=None, callback=None,
+                  cluster_mode=1, kappa=KAPPA_DEFAULT):
     """Driver (reading R12): repeat sweeps; stop after sweep k when ν_k = ‖X_k − X_{k−1}‖_F ≤ δ, or when
     the paper's error model predicts ‖X − X_k‖ ≲ ν_k² max|λ̂| / (n gap) ≤ δ (eq. assume2 / gamma,
     PAPER.md:341-373 with ξ = n as in §4.1), or at stagnation (ν_k > ν_{k−1}/2), or at max_sweeps."""
@@ -110,9 +215,13 @@ def refine_to_tol(A, X0, lam0, delta, theta=1.0, max_sweeps=6, beta_mode="dense"
     hist = []
     nu_prev = None
     for k in range(max_sweeps):
-        Xn, lamn, info = sweep(A, X, lam, delta, theta, beta_mode=beta_mode, xi=xi)
+        Xn, lamn, info = sweep(A, X, lam, delta, theta, beta_mode=beta_mode, xi=xi, cluster_mode=cluster_mode,
+                               kappa=kappa)
         nu = info["net_update"]
-        pred = nu * nu * np.max(np.abs(lamn)) / (n * gap_min(lamn))
+        ls = np.sort(lamn)
+        d = np.diff(ls)
+        gpos = np.min(d[d > 0]) if np.any(d > 0) else max(np.max(np.abs(lamn)) * U, 1e-300)
+        pred = nu * nu * np.max(np.abs(lamn)) / (n * gpos)
         rec = dict(sweep=k + 1, beta=info["beta"], alpha=info["alpha"], net_update=nu, predicted=pred,
                    normE_fro=info["normE_fro"])
         X, lam = Xn, lamn

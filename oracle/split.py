@@ -97,17 +97,28 @@ def _z_value(n_or_xi, delta, gap, maxlam, ssum):
     return np.sqrt(t) / (0.75 * U)
 
 
-def beta_dense(n, delta, lam, c, w):
+def gap_pos(lam):
+    """Smallest POSITIVE neighbour gap of the sorted λ̂ (reading R13: with the cluster branch, equal
+    estimates are allowed and the smallest nonzero gap sets β and the digit budgets); u·max|λ̂| when
+    every gap is zero."""
+    ls = np.sort(np.asarray(lam, dtype=np.float64))
+    d = ls[1:] - ls[:-1]
+    if np.any(d > 0):
+        return float(np.min(d[d > 0]))
+    return max(float(np.max(np.abs(ls))) * U, 1e-300)
+
+
+def beta_dense(n, delta, lam, c, w, gap=None):
     """§4.1: β = ⌊log2((1/(0.75u)) · sqrt(nδ·gap / (max|λ̂| Σ_j 2^{2⌈log2 w_j⌉})))⌋.
     ⌊log2 Z⌋ is exact from the exponent of the fp64 Z. Returns the unclamped integer β."""
-    Z = _z_value(n, delta, gap_min(lam), np.max(np.abs(lam)), sum_pow2_2c(c, w))
+    Z = _z_value(n, delta, gap_min(lam) if gap is None else gap, np.max(np.abs(lam)), sum_pow2_2c(c, w))
     m, e = np.frexp(Z)
     return int(e) - 1
 
 
-def beta_theoretical(xi, delta, lam, c, w):
+def beta_theoretical(xi, delta, lam, c, w, gap=None):
     """§3.3 eq. (proposed_beta): β = ⌈log2((1/(0.75u)) · sqrt(δξ·gap/(max|λ̂| Σ)))⌉."""
-    Z = _z_value(xi, delta, gap_min(lam), np.max(np.abs(lam)), sum_pow2_2c(c, w))
+    Z = _z_value(xi, delta, gap_min(lam) if gap is None else gap, np.max(np.abs(lam)), sum_pow2_2c(c, w))
     m, e = np.frexp(Z)
     return int(e) - 1 if m == 0.5 else int(e)
 

@@ -4,9 +4,9 @@ The product is the C-ABI library libozr.so (include/ozr.h) built from csrc/ for 
 is its thin Python binding (argument marshalling only). See DESIGN.md.
 """
 from ._ozr import (OZR_COLWISE, OZR_ROWWISE, OZR_SPLIT_FIXED, OZR_SPLIT_X1, Context, OzrError, Params, StepReport,
-                   colmajor, default_params, lib, ozr_gemm, ozr_gemm_plan, ozr_refine_step, ozr_refine_to_tol,
-                   ozr_split, ozr_version)
+                   colmajor, default_params, lib, ozr_gemm, ozr_gemm_plan, ozr_last_clusters, ozr_refine_step,
+                   ozr_refine_to_tol, ozr_split, ozr_version)
 
 __all__ = ["Context", "OzrError", "Params", "StepReport", "colmajor", "default_params", "lib", "ozr_gemm",
-           "ozr_gemm_plan", "ozr_refine_step", "ozr_refine_to_tol", "ozr_split", "ozr_version", "OZR_COLWISE",
+           "ozr_gemm_plan", "ozr_last_clusters", "ozr_refine_step", "ozr_refine_to_tol", "ozr_split", "ozr_version", "OZR_COLWISE",
            "OZR_ROWWISE", "OZR_SPLIT_FIXED", "OZR_SPLIT_X1"]

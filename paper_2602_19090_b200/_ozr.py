@@ -18,7 +18,7 @@ OZR_SPLIT_FIXED, OZR_SPLIT_X1 = 0, 1
 STATUS = {0: "OZR_OK", 1: "OZR_ERR_ARG", 2: "OZR_ERR_NONFINITE", 3: "OZR_ERR_RANGE", 4: "OZR_ERR_DEGENERATE",
           5: "OZR_ERR_NOT_CONVERGED", 6: "OZR_ERR_CUDA", 8: "OZR_ERR_NOMEM"}
 EXPORTS = ["ozr_version", "ozr_create", "ozr_destroy", "ozr_last_error", "ozr_split", "ozr_gemm", "ozr_gemm_plan",
-           "ozr_params_default", "ozr_refine_step", "ozr_refine_to_tol"]
+           "ozr_params_default", "ozr_refine_step", "ozr_refine_to_tol", "ozr_last_clusters"]
 
 
 class OzrError(RuntimeError):
@@ -33,12 +33,13 @@ class Params(ctypes.Structure):
                 ("max_sweeps", ctypes.c_int), ("kA_split", ctypes.c_int), ("theta_V", ctypes.c_double),
                 ("theta_W", ctypes.c_double), ("theta_U", ctypes.c_double), ("L_V", ctypes.c_int),
                 ("L_W", ctypes.c_int), ("L_U", ctypes.c_int), ("cluster_mode", ctypes.c_int),
-                ("tile_budgets", ctypes.c_int)]
+                ("tile_budgets", ctypes.c_int), ("kappa", ctypes.c_double), ("max_cluster", ctypes.c_int)]
 
 
 class StepReport(ctypes.Structure):
     _fields_ = ([(f, ctypes.c_int) for f in ["sweep", "beta", "beta_raw", "alpha", "kX", "kA", "kR", "kE", "L_V",
-                                              "L_W", "L_U", "pairs_V", "pairs_W", "pairs_U", "n_clusters", "launches"]] +
+                                              "L_W", "L_U", "pairs_V", "pairs_W", "pairs_U", "n_clusters", "max_cluster",
+                                              "launches"]] +
                 [(f, ctypes.c_double) for f in ["gap_min", "max_abs_lambda", "normE_fro", "net_update",
                                                  "predicted_error", "ms_total", "ms_gemm", "int8_ops"]])
 
@@ -79,6 +80,8 @@ def lib():
         L.ozr_refine_to_tol.argtypes = [vp, vp, i64, i64, vp, i64, vp, ctypes.POINTER(Params),
                                         ctypes.POINTER(StepReport), i32, ip]
         L.ozr_refine_to_tol.restype = i32
+        L.ozr_last_clusters.argtypes = [vp, ip, i32, ip, i32, ip]
+        L.ozr_last_clusters.restype = i32
         _lib = L
     return _lib
 
@@ -207,3 +210,12 @@ def ozr_refine_to_tol(ctx, A, X, lam, params, raise_on_nonconvergence=False):
     if st != 0 and (st != 5 or raise_on_nonconvergence):
         ctx.check(st)
     return st, [H[i].as_dict() for i in range(done.value)]
+
+
+def ozr_last_clusters(ctx, max_members=1 << 20, max_groups=1 << 16):
+    """The unresolved groups of the context's last sweep: a list of lists of global column indices."""
+    mem = (ctypes.c_int * max_members)()
+    off = (ctypes.c_int * (max_groups + 1))()
+    ng = ctypes.c_int(0)
+    ctx.check(lib().ozr_last_clusters(ctx.h, mem, max_members, off, max_groups, ctypes.byref(ng)))
+    return [list(mem[off[g]:off[g + 1]]) for g in range(ng.value)]

@@ -1,0 +1,396 @@
+// cluster.cu — the clustered-eigenvalue branch of the Ẽ correction (reading R13; the paper
+// assumes distinct eigenvalues, and leaves clusters open).
+//
+// Unresolved groups J (connected components of the pairs with |ẽ_ij| > κ or λ̂_i = λ̂_j, found on the
+// host from the edge list k_recombine_E emits) get a Rayleigh–Ritz sub-solve in span(X̂^(1)_J), restated
+// from the Ogita–Aishima cluster refinement cited at PAPER.md:233-235:
+//   G_JJ = X̂_JᵀX̂_J (exact, from the integer digits), R_JJ = I − G_JJ (diagonal: the exact r_j),
+//   M = W_JJ + (I − R_JJ)(D̂_J − μI)      (= S_JJ − μG_JJ since S = W + (I − R)D̂, Alg. 1 line 4)
+//   K = C·(M + Mᵀ)/2·C,  C = I + R_JJ/2   (C ≈ G_JJ^{-1/2})
+//   K = YΘYᵀ (cyclic parallel Jacobi, Θ ascending, y_kk ≥ 0),  Z = C·Y
+//   Ẽ_JJ ← Z − I,  Ẽ_{i,J} ← Ẽ_{i,J}·Z (i ∉ J),  λ̂_J ← μ + Θ.
+// All on Ẽ' = diag(2^g)Ẽ, the scaled matrix the X̂Ẽ product consumes (rows scale, Z acts on columns).
+//
+//   k_cluster_build   (group, 16x16 tile of (a,b)): exact g_ab from the digits (int128), w_ab from the
+//                     W slice-product planes, M_ab and R_ab into the group's workspace
+//   k_cluster_jacobi  one CTA per group: K, Jacobi, sort, sign, Z = C·Y, λ̂_J
+//   k_cluster_gather  T = Ẽ'[:, J] (compact copy, the apply reads old values)
+//   k_cluster_apply   Ẽ'[:, J] ← T·Z off the group rows, (Z − I)·2^{g_i} on them
+//   k_cluster_colstats column maxima exponents and ‖ẽ_j‖² of the rewritten columns
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "ddmath.cuh"
+#include "kernels.h"
+
+namespace ozr {
+
+namespace {
+
+// Horner recombination of one element of a slice-product (same contract as kernels.cu; kept local so
+// the cluster kernels do not depend on that translation unit's internals).
+__device__ __forceinline__ dd recomb_one(const int32_t* __restrict__ planes, long long pstride, long long off,
+                                         const RecombPlan& rp, int e, int Lj) {
+  dd acc{0.0, 0.0};
+  bool first = true;
+  for (int c = 0; c < rp.nchunks; ++c) {
+    i128 T = 0;
+    int dprev = rp.diag[rp.chunk_first[c]];
+    for (int g = rp.chunk_first[c]; g < rp.chunk_first[c + 1]; ++g) {
+      const int d = rp.diag[g];
+      const int32_t cv = (d <= Lj) ? planes[g * pstride + off] : 0;
+      T = static_cast<i128>(static_cast<u128>(T) << (8 * (d - dprev))) + static_cast<i128>(cv);
+      dprev = d;
+    }
+    dd v = i128_to_dd(T);
+    const int sc = 8 * (rp.L - dprev) + e;
+    v.hi = ldexp_fast(v.hi, sc);
+    v.lo = ldexp_fast(v.lo, sc);
+    acc = first ? v : dd_add(acc, v);
+    first = false;
+  }
+  return acc;
+}
+
+// q = Σ_s d_s 256^{k−s} from the k digit planes of column `col`, row `row`.
+__device__ __forceinline__ long long digits_q(const int8_t* __restrict__ dig, long long ldd, long long pstride, int kx,
+                                              int col, int row) {
+  long long q = 0;
+  const int8_t* p = dig + static_cast<long long>(col) * ldd + row;
+  for (int s = 0; s < kx; ++s) q = q * 256 + static_cast<long long>(p[s * pstride]);
+  return q;
+}
+
+constexpr int TB = 16;   // (a,b) tile edge of k_cluster_build
+constexpr int KC = 64;   // rows per staged chunk
+
+__global__ void __launch_bounds__(TB* TB)
+    k_cluster_build(const int4* __restrict__ tiles, const int* __restrict__ goff, const int* __restrict__ gsq,
+                    const int* __restrict__ mem, const double* __restrict__ mu, const int8_t* __restrict__ xdig,
+                    long long ldd, long long pstride, int kx, int rows, const int32_t* __restrict__ gexp,
+                    const double* __restrict__ r_hi, const double* __restrict__ r_lo, const int32_t* __restrict__ wplanes,
+                    long long wpstride, const __grid_constant__ RecombPlan rpW, const int32_t* __restrict__ ellR,
+                    int scale8, const double* __restrict__ lam, double* __restrict__ Mbuf, double* __restrict__ Rbuf) {
+  __shared__ long long qa[KC][TB + 1];
+  __shared__ long long qb[KC][TB + 1];
+  const int4 t = tiles[blockIdx.x];  // (group, a0, b0, m)
+  const int grp = t.x, a0 = t.y, b0 = t.z, m = t.w;
+  const int tx = threadIdx.x % TB, ty = threadIdx.x / TB;
+  const int a = a0 + ty, b = b0 + tx;
+  const int* J = mem + goff[grp];
+  // exact Σ_k q_ki q_kj in int128 (|q| < 2^52, rows < 2^16)
+  unsigned long long lo = 0;
+  long long hi = 0;
+  for (int k0 = 0; k0 < rows; k0 += KC) {
+    for (int e = threadIdx.x; e < KC * TB; e += TB * TB) {
+      const int kk = e % KC, c = e / KC;  // consecutive threads: consecutive rows of one column
+      const int k = k0 + kk;
+      qa[kk][c] = (k < rows && a0 + c < m) ? digits_q(xdig, ldd, pstride, kx, J[a0 + c], k) : 0;
+      qb[kk][c] = (k < rows && b0 + c < m) ? digits_q(xdig, ldd, pstride, kx, J[b0 + c], k) : 0;
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int kk = 0; kk < KC; ++kk) {
+      const long long x = qa[kk][ty], y = qb[kk][tx];
+      const unsigned long long pl = static_cast<unsigned long long>(x) * static_cast<unsigned long long>(y);
+      const long long ph = __mul64hi(x, y);
+      const unsigned long long s = lo + pl;
+      hi += ph + (s < lo ? 1 : 0);
+      lo = s;
+    }
+    __syncthreads();
+  }
+  if (a >= m || b >= m) return;
+  const int i = J[a], j = J[b];
+  const i128 SQ = static_cast<i128>((static_cast<u128>(static_cast<unsigned long long>(hi)) << 64) | lo);
+  const dd gdd = i128_to_dd(SQ);
+  const double g = ldexp_fast(gdd.hi, gexp[i] + gexp[j]);
+  const double r = (a == b) ? (r_hi[i] + r_lo[i]) : -g;
+  // w_ij from the W = X̂ᵀRes slice-product planes (row i: ℓ = g_i, column j: ℓ = ℓ_Res,j + scale)
+  const int Lj = rpW.tile_budgets ? rpW.tileL[j / 256] : rpW.L;
+  const dd w = recomb_one(wplanes, wpstride, static_cast<long long>(j) * rows + i, rpW, gexp[i] + ellR[j] + scale8, Lj);
+  const double mug = mu[grp];
+  const double Mab = (w.hi + w.lo) + ((a == b ? 1.0 : 0.0) - r) * (lam[j] - mug);
+  const long long o = static_cast<long long>(gsq[grp]) + static_cast<long long>(b) * m + a;
+  Mbuf[o] = Mab;
+  Rbuf[o] = r;
+}
+
+constexpr int JT = 512;  // threads of the Jacobi CTA
+
+__global__ void __launch_bounds__(JT)
+    k_cluster_jacobi(const int* __restrict__ goff, const int* __restrict__ gsq, const int* __restrict__ gm,
+                     const int* __restrict__ mem, const double* __restrict__ mu, const double* __restrict__ Mbuf,
+                     const double* __restrict__ Rbuf, double* __restrict__ Kbuf, double* __restrict__ Vbuf,
+                     double* __restrict__ Zbuf, double* __restrict__ lam, int* __restrict__ sweeps_out) {
+  extern __shared__ double jsm[];  // c[mm/2], s[mm/2], diag/θ[m], perm[m] (as double slots), red[JT/32]
+  const int grp = blockIdx.x;
+  const int m = gm[grp];
+  const long long o = gsq[grp];
+  const double* M = Mbuf + o;
+  const double* R = Rbuf + o;
+  double* K = Kbuf + o;
+  double* V = Vbuf + o;
+  double* Z = Zbuf + o;
+  const int mm = m + (m & 1);
+  const int np = mm / 2;
+  double* cs = jsm;
+  double* sn = jsm + np;
+  double* th = sn + np;
+  int* perm = reinterpret_cast<int*>(th + m);
+  double* red = reinterpret_cast<double*>(perm + m + (m & 1));
+  const int tid = threadIdx.x;
+  const long long mm2 = static_cast<long long>(m) * m;
+  // K0 = (M + Mᵀ)/2 into V (scratch), T = C·K0 into K, K = T·C into V ... then swap roles
+  for (long long e = tid; e < mm2; e += JT) {
+    const int a = static_cast<int>(e % m), b = static_cast<int>(e / m);
+    V[e] = 0.5 * (M[e] + M[static_cast<long long>(a) * m + b]);
+  }
+  __syncthreads();
+  for (long long e = tid; e < mm2; e += JT) {  // K = C K0, C = I + R/2
+    const int a = static_cast<int>(e % m), b = static_cast<int>(e / m);
+    double s = V[e];
+    for (int l = 0; l < m; ++l) s = fma(0.5 * R[static_cast<long long>(l) * m + a], V[static_cast<long long>(b) * m + l], s);
+    K[e] = s;
+  }
+  __syncthreads();
+  for (long long e = tid; e < mm2; e += JT) {  // V = K C
+    const int a = static_cast<int>(e % m), b = static_cast<int>(e / m);
+    double s = K[e];
+    for (int l = 0; l < m; ++l) s = fma(K[static_cast<long long>(l) * m + a], 0.5 * R[static_cast<long long>(b) * m + l], s);
+    V[e] = s;
+  }
+  __syncthreads();
+  double fro2 = 0.0;
+  for (long long e = tid; e < mm2; e += JT) {  // symmetrise into K, V = I
+    const int a = static_cast<int>(e % m), b = static_cast<int>(e / m);
+    const double x = 0.5 * (V[e] + V[static_cast<long long>(a) * m + b]);
+    K[e] = x;
+    fro2 = fma(x, x, fro2);
+  }
+  __syncthreads();
+  for (long long e = tid; e < mm2; e += JT) V[e] = ((e % m) == (e / m)) ? 1.0 : 0.0;
+  // ‖K‖_F (fixed-shape reduction)
+  for (int off = 16; off > 0; off >>= 1) fro2 += __shfl_xor_sync(0xffffffffu, fro2, off);
+  if ((tid & 31) == 0) red[tid >> 5] = fro2;
+  __syncthreads();
+  double f2 = 0.0;
+  for (int w = 0; w < JT / 32; ++w) f2 += red[w];
+  const double tiny = 1e-18 * sqrt(f2);
+  __syncthreads();
+  int sweeps = 0;
+  for (int sw = 0; sw < 40; ++sw) {
+    int rotated = 0;
+    for (int r = 0; r < mm - 1; ++r) {
+      // round-robin: position 0 fixed, the others rotate; pair k = (pos k, pos mm−1−k)
+      for (int k = tid; k < np; k += JT) {
+        auto pos = [&](int x) { return x == 0 ? 0 : 1 + ((x - 1 + r) % (mm - 1)); };
+        int p = pos(k), q = pos(mm - 1 - k);
+        if (p > q) { const int tmp = p; p = q; q = tmp; }
+        double c = 1.0, s = 0.0;
+        if (q < m) {
+          const double apq = K[static_cast<long long>(q) * m + p];
+          if (fabs(apq) > tiny) {
+            const double app = K[static_cast<long long>(p) * m + p], aqq = K[static_cast<long long>(q) * m + q];
+            const double theta = (aqq - app) / (2.0 * apq);
+            const double t = (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(fma(theta, theta, 1.0)));
+            c = 1.0 / sqrt(fma(t, t, 1.0));
+            s = t * c;
+            rotated = 1;
+          }
+        }
+        cs[k] = c;
+        sn[k] = s;
+      }
+      __syncthreads();
+      // rows p,q of K  (K ← JᵀK)
+      for (long long e = tid; e < static_cast<long long>(np) * m; e += JT) {
+        const int k = static_cast<int>(e / m), col = static_cast<int>(e % m);
+        const double s = sn[k];
+        if (s == 0.0) continue;
+        auto pos = [&](int x) { return x == 0 ? 0 : 1 + ((x - 1 + r) % (mm - 1)); };
+        int p = pos(k), q = pos(mm - 1 - k);
+        if (p > q) { const int tmp = p; p = q; q = tmp; }
+        const double c = cs[k];
+        double* kp = K + static_cast<long long>(col) * m;
+        const double x = kp[p], y = kp[q];
+        kp[p] = c * x - s * y;
+        kp[q] = s * x + c * y;
+      }
+      __syncthreads();
+      // columns p,q of K and V  (K ← K J, V ← V J)
+      for (long long e = tid; e < 2LL * np * m; e += JT) {
+        const int which = static_cast<int>(e / (static_cast<long long>(np) * m));
+        const long long e2 = e % (static_cast<long long>(np) * m);
+        const int k = static_cast<int>(e2 / m), row = static_cast<int>(e2 % m);
+        const double s = sn[k];
+        if (s == 0.0) continue;
+        auto pos = [&](int x) { return x == 0 ? 0 : 1 + ((x - 1 + r) % (mm - 1)); };
+        int p = pos(k), q = pos(mm - 1 - k);
+        if (p > q) { const int tmp = p; p = q; q = tmp; }
+        const double c = cs[k];
+        double* B = which ? V : K;
+        const double x = B[static_cast<long long>(p) * m + row], y = B[static_cast<long long>(q) * m + row];
+        B[static_cast<long long>(p) * m + row] = c * x - s * y;
+        B[static_cast<long long>(q) * m + row] = s * x + c * y;
+      }
+      __syncthreads();
+    }
+    sweeps = sw + 1;
+    if (!__syncthreads_or(rotated)) break;
+  }
+  // ascending order (ties by index), y_kk ≥ 0, Z = C·Y, λ̂_J = μ + Θ
+  for (int k = tid; k < m; k += JT) th[k] = K[static_cast<long long>(k) * m + k];
+  __syncthreads();
+  for (int k = tid; k < m; k += JT) {
+    int rk = 0;
+    const double x = th[k];
+    for (int l = 0; l < m; ++l) rk += (th[l] < x || (th[l] == x && l < k)) ? 1 : 0;
+    perm[rk] = k;
+  }
+  __syncthreads();
+  const int* J = mem + goff[grp];
+  for (int k = tid; k < m; k += JT) {
+    const int src = perm[k];
+    double piv = V[static_cast<long long>(src) * m + k];
+    if (piv == 0.0) {
+      double best = -1.0;
+      for (int l = 0; l < m; ++l) {
+        const double v = V[static_cast<long long>(src) * m + l];
+        if (fabs(v) > best) { best = fabs(v); piv = v; }
+      }
+    }
+    const double sg = piv < 0 ? -1.0 : 1.0;
+    for (int a = 0; a < m; ++a) {  // Z[:,k] = C · (sg · V[:,src])
+      double s = sg * V[static_cast<long long>(src) * m + a];
+      for (int l = 0; l < m; ++l) s = fma(0.5 * R[static_cast<long long>(l) * m + a], sg * V[static_cast<long long>(src) * m + l], s);
+      Z[static_cast<long long>(k) * m + a] = s;
+    }
+    lam[J[k]] = mu[grp] + th[src];
+  }
+  if (tid == 0) sweeps_out[grp] = sweeps;
+}
+
+__global__ void k_cluster_gather(const int* __restrict__ mem, int nmembers, const double* __restrict__ Ep, long long lde,
+                                 int rows, double* __restrict__ T) {
+  const int c = blockIdx.x;  // member index over all groups
+  if (c >= nmembers) return;
+  const int j = mem[c];
+  for (int i = blockIdx.y * blockDim.x + threadIdx.x; i < rows; i += gridDim.y * blockDim.x)
+    T[static_cast<long long>(c) * rows + i] = Ep[static_cast<long long>(j) * lde + i];
+}
+
+constexpr int AK = 32;  // output columns per apply CTA
+
+__global__ void __launch_bounds__(256)
+    k_cluster_apply(const int* __restrict__ goff, const int* __restrict__ gsq, const int* __restrict__ gm,
+                    const int* __restrict__ mem, const int* __restrict__ grp_of, const int* __restrict__ pos_of,
+                    const double* __restrict__ T, const double* __restrict__ Zbuf, const int32_t* __restrict__ gexp,
+                    int rows, double* __restrict__ Ep, long long lde) {
+  const int grp = blockIdx.z;
+  const int m = gm[grp];
+  const int k0 = blockIdx.y * AK;
+  if (k0 >= m) return;
+  const int kn = min(AK, m - k0);
+  const double* Z = Zbuf + gsq[grp];
+  const int* J = mem + goff[grp];
+  const double* Tg = T + static_cast<long long>(goff[grp]) * rows;
+  __shared__ double zs[64][AK];
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  double acc[AK];
+#pragma unroll
+  for (int q = 0; q < AK; ++q) acc[q] = 0.0;
+  for (int l0 = 0; l0 < m; l0 += 64) {
+    __syncthreads();
+    for (int e = threadIdx.x; e < 64 * AK; e += blockDim.x) {
+      const int l = l0 + e / AK, q = e % AK;
+      zs[e / AK][q] = (l < m && q < kn) ? Z[static_cast<long long>(k0 + q) * m + l] : 0.0;
+    }
+    __syncthreads();
+    if (i < rows) {
+      const int lmax = min(64, m - l0);
+      for (int l = 0; l < lmax; ++l) {
+        const double t = Tg[static_cast<long long>(l0 + l) * rows + i];
+#pragma unroll
+        for (int q = 0; q < AK; ++q) acc[q] = fma(t, zs[l][q], acc[q]);
+      }
+    }
+  }
+  if (i >= rows) return;
+  const bool in = grp_of[i] == grp;
+  const int a = in ? pos_of[i] : 0;
+#pragma unroll
+  for (int q = 0; q < AK; ++q) {
+    if (q >= kn) break;
+    const int k = k0 + q;
+    double v = acc[q];
+    if (in) v = ldexp_fast(Z[static_cast<long long>(k) * m + a] - (a == k ? 1.0 : 0.0), gexp[i]);
+    Ep[static_cast<long long>(J[k]) * lde + i] = v;
+  }
+}
+
+__global__ void __launch_bounds__(256)
+    k_cluster_colstats(const int* __restrict__ mem, const double* __restrict__ Ep, long long lde, int rows,
+                       const int32_t* __restrict__ gexp, double* __restrict__ nrm2, int32_t* __restrict__ eE_col,
+                       int* __restrict__ eE_max) {
+  __shared__ double sh[2][8];
+  const int j = mem[blockIdx.x];
+  double m = 0.0, s2 = 0.0;
+  for (int i = threadIdx.x; i < rows; i += 256) {
+    const double ep = Ep[static_cast<long long>(j) * lde + i];
+    const double e = ldexp_fast(ep, -gexp[i]);
+    s2 = fma(e, e, s2);
+    m = fmax(m, fabs(ep));
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    s2 = __dadd_rn(s2, __shfl_xor_sync(0xffffffffu, s2, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    sh[0][threadIdx.x >> 5] = m;
+    sh[1][threadIdx.x >> 5] = s2;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double mx = sh[0][0], ss = sh[1][0];
+    for (int w = 1; w < 8; ++w) {
+      mx = fmax(mx, sh[0][w]);
+      ss = __dadd_rn(ss, sh[1][w]);
+    }
+    nrm2[j] = ss;
+    const int e = (mx > 0.0) ? ceil_log2_d(mx) : -100000;
+    eE_col[j] = e;
+    if (mx > 0.0) atomicMax(eE_max, e);
+  }
+}
+
+}  // namespace
+
+size_t cluster_jacobi_smem(int mmax) {
+  const int mm = mmax + (mmax & 1);
+  return sizeof(double) * (mm + mmax) + sizeof(int) * (mmax + 2) + sizeof(double) * (JT / 32) + 64;
+}
+
+cudaError_t launch_cluster(const ClusterLaunch& L, cudaStream_t s) {
+  if (L.ntiles > 0)
+    k_cluster_build<<<L.ntiles, TB * TB, 0, s>>>(L.tiles, L.goff, L.gsq, L.mem, L.mu, L.xdig, L.ldd, L.pstride, L.kx,
+                                                 L.rows, L.gexp, L.r_hi, L.r_lo, L.wplanes, L.wpstride, *L.rpW, L.ellR,
+                                                 L.scale8, L.lam, L.Mbuf, L.Rbuf);
+  const size_t sm = cluster_jacobi_smem(L.mmax);
+  if (sm > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(k_cluster_jacobi, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(sm));
+    if (e != cudaSuccess) return e;
+  }
+  k_cluster_jacobi<<<L.ngroups, JT, sm, s>>>(L.goff, L.gsq, L.gm, L.mem, L.mu, L.Mbuf, L.Rbuf, L.Kbuf, L.Vbuf, L.Zbuf,
+                                              L.lam, L.sweeps);
+  dim3 gg(L.nmembers, (L.rows + 255) / 256 < 64 ? (L.rows + 255) / 256 : 64);
+  k_cluster_gather<<<gg, 256, 0, s>>>(L.mem, L.nmembers, L.Ep, L.lde, L.rows, L.T);
+  dim3 ga((L.rows + 255) / 256, (L.mmax + AK - 1) / AK, L.ngroups);
+  k_cluster_apply<<<ga, 256, 0, s>>>(L.goff, L.gsq, L.gm, L.mem, L.grp_of, L.pos_of, L.T, L.Zbuf, L.gexp, L.rows,
+                                     L.Ep, L.lde);
+  k_cluster_colstats<<<L.nmembers, 256, 0, s>>>(L.mem, L.Ep, L.lde, L.rows, L.gexp, L.nrm2, L.eE_col, L.eE_max);
+  return cudaGetLastError();
+}
+
+}  // namespace ozr

@@ -138,6 +138,45 @@ __device__ __forceinline__ dd recombine_elem(const int32_t* __restrict__ planes,
   return acc;
 }
 
+// ---------------------------------------------------------------- device union-find (cluster branch)
+__device__ __forceinline__ int uf_find(int* parent, int a) {
+  int p = parent[a];
+  while (p != a) {
+    const int gp = parent[p];
+    parent[a] = gp;  // path halving (a benign race: any ancestor is a valid parent)
+    a = p;
+    p = gp;
+  }
+  return a;
+}
+// link the larger root under the smaller one; retried until both are in one set
+__device__ __forceinline__ void uf_unite(int* parent, int a, int b) {
+  while (true) {
+    a = uf_find(parent, a);
+    b = uf_find(parent, b);
+    if (a == b) return;
+    if (a > b) {
+      const int t = a;
+      a = b;
+      b = t;
+    }
+    if (atomicCAS(parent + b, b, a) == b) return;
+  }
+}
+
+__global__ void k_iota(int* p, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) p[i] = i;
+}
+__global__ void k_uf_flatten(int* parent, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) {
+    int a = i;
+    while (parent[a] != a) a = parent[a];
+    parent[i] = a;
+  }
+}
+
 // ---------------------------------------------------------------- kernels
 __global__ void __launch_bounds__(BS) k_colmax(const double* __restrict__ X, long long ldx, int rows,
                                                double* __restrict__ w, int* __restrict__ err) {
@@ -364,7 +403,8 @@ __global__ void __launch_bounds__(BS)
                   const int32_t* __restrict__ ellA, const int32_t* __restrict__ ellB, int scale8,
                   const double* __restrict__ r_hi, const double* __restrict__ lam, const int32_t* __restrict__ gX,
                   int col0, double* __restrict__ Ep, long long lde, double* __restrict__ nrm2,
-                  int* __restrict__ eE_max, int32_t* __restrict__ eE_col, int* __restrict__ err) {
+                  int* __restrict__ eE_max, int32_t* __restrict__ eE_col, int* __restrict__ err,
+                  const EdgeOut eo) {
   __shared__ double sh[BS / 32];
   const int j = blockIdx.x;        // local column
   const int Lj = rp.tile_budgets ? rp.tileL[j / 256] : rp.L;
@@ -372,7 +412,7 @@ __global__ void __launch_bounds__(BS)
   const int eb = ellB[j] + scale8;
   const double lj = lam[jg];
   double m = 0.0, s2 = 0.0;
-  bool bad = false;
+  bool bad = false, unresolved = false;
   for (int i = threadIdx.x; i < rows; i += BS) {
     double e;
     if (i == jg) {
@@ -380,8 +420,18 @@ __global__ void __launch_bounds__(BS)
     } else {
       const dd wv = recombine_elem(planes, pstride, static_cast<long long>(j) * rows + i, rp, ellA[i] + eb, Lj);
       const double dl = __dsub_rn(lj, lam[i]);  // λ̃_j − λ̃_i
-      if (dl == 0.0) bad = true;
-      e = __ddiv_rn(wv.hi, dl);  // ẽ_ij = w_ij / (λ̃_j − λ̃_i)  (Alg. 1 line 5)
+      if (eo.mode == 0) {
+        if (dl == 0.0) bad = true;
+        e = __ddiv_rn(wv.hi, dl);  // ẽ_ij = w_ij / (λ̃_j − λ̃_i)  (Alg. 1 line 5)
+      } else {
+        // cluster branch (R13): equal λ̂ or |ẽ_ij| > κ marks an unresolved pair; the group sub-solve
+        // (cluster.cu) rewrites its columns
+        e = (dl == 0.0) ? 0.0 : __ddiv_rn(wv.hi, dl);
+        if (dl == 0.0 || fabs(e) > eo.kappa) {
+          uf_unite(eo.parent, i, jg);
+          unresolved = true;
+        }
+      }
     }
     s2 = __fma_rn(e, e, s2);
     const double ep = ldexp_fast(e, gX[i]);  // Ẽ' = diag(2^g) Ẽ (exact)
@@ -389,6 +439,7 @@ __global__ void __launch_bounds__(BS)
     m = fmax(m, fabs(ep));
   }
   if (bad) atomicOr(err, ERR_DEGENERATE);
+  if (__syncthreads_or(unresolved) && threadIdx.x == 0) atomicOr(eo.any, 1);
   m = block_max(m, sh);
   s2 = block_sum(s2, sh);
   if (threadIdx.x == 0) {
@@ -477,16 +528,17 @@ void launch_recombine_V(const int32_t* planes, long long pstride, int rows, int 
 void launch_recombine_E(const int32_t* planes, long long pstride, int rows, int cols, const RecombPlan& rp,
                         const int32_t* ellA, const int32_t* ellB, int scale8, const double* r_hi, const double* lam,
                         const int32_t* gX, int col0, double* Ep, long long lde, double* nrm2, int* eE_max,
-                        int32_t* eE_col, int* err,
-                        cudaStream_t s) {
+                        int32_t* eE_col, int* err, const EdgeOut& eo, cudaStream_t s) {
   k_recombine_E<<<cols, BS, 0, s>>>(planes, pstride, rows, rp, ellA, ellB, scale8, r_hi, lam, gX, col0, Ep, lde, nrm2,
-                                    eE_max, eE_col, err);
+                                    eE_max, eE_col, err, eo);
 }
 void launch_final(const int32_t* planes, long long pstride, int rows, int cols, const RecombPlan& rp,
                   const int32_t* ellB, int scale8, const double* X1, long long ldx1, double* X, long long ldx,
                   double* nu2, double* wnext, cudaStream_t s) {
   k_final<<<cols, BS, 0, s>>>(planes, pstride, rows, rp, ellB, scale8, X1, ldx1, X, ldx, nu2, wnext);
 }
+void launch_iota(int* p, int n, cudaStream_t s) { k_iota<<<(n + 255) / 256, 256, 0, s>>>(p, n); }
+void launch_uf_flatten(int* parent, int n, cudaStream_t s) { k_uf_flatten<<<(n + 255) / 256, 256, 0, s>>>(parent, n); }
 void launch_recombine_dd(const int32_t* planes, long long pstride, int rows, int cols, const RecombPlan& rp,
                          const int32_t* ellA, const int32_t* ellB, int scale8, double* Ch, double* Cl, long long ldc,
                          cudaStream_t s) {

@@ -37,11 +37,50 @@ void launch_recombine_V(const int32_t* planes, long long pstride, int rows, int 
                         const int32_t* ellA, const int32_t* ellB, int scale8, const double* X1, long long ldx1,
                         const double* s_hi, const double* s_lo, double* Vh, double* Vl, long long ldv,
                         double* lam_out, int32_t* eR, int* eR_max, cudaStream_t s);
+// Unresolved pairs of k_recombine_E (cluster branch, R13): every pair (i, j), i ≠ j, with
+// λ̂_i = λ̂_j or |ẽ_ij| > κ is united in the device union-find `parent` (O(n) memory, any number of
+// pairs; the resulting partition is independent of the order of the unions), and *any is set.
+struct EdgeOut {
+  int mode;      // 0: the paper's Alg. 1 (equal λ̂ → ERR_DEGENERATE); 1: union unresolved pairs
+  double kappa;
+  int* parent;   // n entries, parent[i] = i on entry (launch_iota)
+  int* any;
+};
+void launch_iota(int* p, int n, cudaStream_t s);
+void launch_uf_flatten(int* parent, int n, cudaStream_t s);  // parent[i] ← root of i
 void launch_recombine_E(const int32_t* planes, long long pstride, int rows, int cols, const RecombPlan& rp,
                         const int32_t* ellA, const int32_t* ellB, int scale8, const double* r_hi, const double* lam,
                         const int32_t* gX, int col0, double* Ep, long long lde, double* nrm2, int* eE_max,
-                        int32_t* eE_col, int* err,
-                        cudaStream_t s);
+                        int32_t* eE_col, int* err, const EdgeOut& eo, cudaStream_t s);
+
+// Cluster sub-solve (cluster.cu). Groups g = 0..ngroups-1 with members mem[goff[g] .. goff[g]+gm[g]) (global
+// column indices, ascending (λ̂, index)); per-group m x m workspaces at offset gsq[g] (Σ m²) in M/R/K/V/Z.
+struct ClusterLaunch {
+  int ngroups, nmembers, mmax, ntiles, rows;
+  const int4* tiles;  // (group, a0, b0, m) 16 x 16 tiles of k_cluster_build
+  const int *goff, *gsq, *gm, *mem, *grp_of, *pos_of;
+  const double* mu;
+  const int8_t* xdig;  // X̂^(1) digit planes (column-major, kx planes)
+  long long ldd, pstride;
+  int kx;
+  const int32_t* gexp;  // g_j (LSB exponent of column j of X̂^(1))
+  const double *r_hi, *r_lo;
+  const int32_t* wplanes;  // W = X̂ᵀRes slice-product planes
+  long long wpstride;
+  const RecombPlan* rpW;
+  const int32_t* ellR;
+  int scale8;
+  double* lam;  // in: λ̂ (Rayleigh quotients), out: λ̂_J = μ + Θ
+  double *Mbuf, *Rbuf, *Kbuf, *Vbuf, *Zbuf, *T;
+  int* sweeps;
+  double* Ep;
+  long long lde;
+  double* nrm2;
+  int32_t* eE_col;
+  int* eE_max;
+};
+size_t cluster_jacobi_smem(int mmax);
+cudaError_t launch_cluster(const ClusterLaunch& L, cudaStream_t s);
 void launch_final(const int32_t* planes, long long pstride, int rows, int cols, const RecombPlan& rp,
                   const int32_t* ellB, int scale8, const double* X1, long long ldx1, double* X, long long ldx,
                   double* nu2, double* wnext, cudaStream_t s);

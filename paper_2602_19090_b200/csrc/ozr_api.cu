@@ -39,6 +39,7 @@ struct ozr_ctx_s {
   cudaStream_t stream = nullptr;
   std::string err;
   std::vector<DevBuf> bufs;
+  std::vector<int> last_members, last_offsets{0};  // unresolved groups of the last sweep (R13)
   cudaEvent_t ev[8];
   bool events = false;
   // tracing (OZR_TRACE=1): named events between the kernels of a sweep, printed to stderr per sweep
@@ -98,7 +99,8 @@ namespace {
 
 enum Slot {
   S_ADIG, S_AELL, S_W, S_X1, S_XDIG, S_XDIGT, S_G, S_SH, S_SL, S_RH, S_RL, S_PLANES, S_VH, S_VL, S_LAM, S_ER,
-  S_ERR, S_EMAX, S_RDIG, S_RELL, S_EP, S_NRM2, S_NU2, S_WNEXT, S_ZEROELL, S_TMP1, S_TMP2, S_BELL, S_AT, S_ONES
+  S_ERR, S_EMAX, S_RDIG, S_RELL, S_EP, S_NRM2, S_NU2, S_WNEXT, S_ZEROELL, S_TMP1, S_TMP2, S_BELL, S_AT, S_ONES,
+  S_EDGES, S_ECOUNT, S_CINT, S_CDBL, S_CM, S_CR, S_CK, S_CV, S_CZ, S_CT
 };
 
 ozr_status fail(ozr_ctx c, ozr_status st, const char* fmt, ...) {
@@ -327,6 +329,40 @@ double gap_min_sorted(std::vector<double> l) {
   return g;
 }
 
+// Smallest POSITIVE neighbour gap (digit budgets need a finite accuracy target when the cluster branch
+// tolerates equal λ̂); falls back to u·max|λ̂| when every gap is zero.
+double gap_pos_sorted(std::vector<double> l) {
+  std::sort(l.begin(), l.end());
+  double g = INFINITY, mx = 0.0;
+  for (size_t i = 0; i < l.size(); ++i) mx = std::max(mx, std::fabs(l[i]));
+  for (size_t i = 1; i < l.size(); ++i)
+    if (l[i] - l[i - 1] > 0.0) g = std::min(g, l[i] - l[i - 1]);
+  return std::isfinite(g) ? g : std::max(mx * kU, 1e-300);
+}
+
+// ---------------------------------------------------------------- cluster branch (R13): host grouping
+// Connected components of the unresolved-pair graph; members sorted by (λ̂, index), groups by first member.
+// root[i]: the (flattened) device union-find label of column i.
+void unresolved_groups(int64_t n, const std::vector<int>& root, const std::vector<double>& lam,
+                       std::vector<int>& members, std::vector<int>& offsets) {
+  std::vector<std::vector<int>> comp(n);
+  for (int64_t i = 0; i < n; ++i) comp[root[i]].push_back(static_cast<int>(i));
+  std::vector<std::vector<int>> groups;
+  for (int64_t r = 0; r < n; ++r)
+    if (comp[r].size() >= 2) {
+      std::vector<int> g = comp[r];
+      std::sort(g.begin(), g.end(), [&](int a, int b) { return lam[a] < lam[b] || (lam[a] == lam[b] && a < b); });
+      groups.push_back(g);
+    }
+  std::sort(groups.begin(), groups.end(), [](const std::vector<int>& a, const std::vector<int>& b) { return a[0] < b[0]; });
+  members.clear();
+  offsets.assign(1, 0);
+  for (auto& g : groups) {
+    members.insert(members.end(), g.begin(), g.end());
+    offsets.push_back(static_cast<int>(members.size()));
+  }
+}
+
 double sum_pow2_2c(const std::vector<double>& w) {
   std::vector<int> cs;
   for (double x : w)
@@ -435,10 +471,11 @@ ozr_status sweep(ozr_ctx ctx, const double* A, int64_t n, int64_t lda, double* X
   for (double x : hlam)
     if (!std::isfinite(x)) return fail(ctx, OZR_ERR_NONFINITE, "non-finite lambda");
   const double delta_p = P.delta / (P.theta > 0 ? P.theta : 1.0);
-  const double gap = gap_min_sorted(hlam);
+  const double gap0 = gap_min_sorted(hlam);
+  const double gap = (P.cluster_mode && !(gap0 > 0.0)) ? gap_pos_sorted(hlam) : gap0;
   double maxlam = 0.0;
   for (double x : hlam) maxlam = std::max(maxlam, std::fabs(x));
-  if (!(gap > 0.0) && P.cluster_mode == 0)
+  if (!(gap0 > 0.0) && P.cluster_mode == 0)
     return fail(ctx, OZR_ERR_DEGENERATE, "equal eigenvalue estimates (gap = 0) with the cluster branch off");
   const double ssum = sum_pow2_2c(hw);
   if (ssum == 0.0 || maxlam == 0.0) return fail(ctx, OZR_ERR_DEGENERATE, "zero X or zero spectrum");
@@ -454,7 +491,7 @@ ozr_status sweep(ozr_ctx ctx, const double* A, int64_t n, int64_t lda, double* X
   rep.beta_raw = beta_raw;
   rep.alpha = alpha_dense(n, beta);
   rep.kX = kx;
-  rep.gap_min = gap;
+  rep.gap_min = gap0;
   rep.max_abs_lambda = maxlam;
 
   // ---- A split (once per refine_to_tol call)
@@ -464,7 +501,9 @@ ozr_status sweep(ozr_ctx ctx, const double* A, int64_t n, int64_t lda, double* X
   }
   ctx->mark("stats+splitA");
   // per-column accuracy of V (R8, R8b): θ_V·δ'·gap_j with the previous λ̂
-  const std::vector<double> gaps_prev = col_gaps(hlam);
+  std::vector<double> gaps_prev = col_gaps(hlam);
+  for (double& x : gaps_prev)
+    if (!(x > 0.0)) x = gap;  // equal λ̂ (cluster branch): the smallest positive gap sets the budget
   std::vector<double> tau_col(n);
   std::vector<int> c_col(n);
   for (int64_t j = 0; j < n; ++j) {
@@ -540,9 +579,10 @@ ozr_status sweep(ozr_ctx ctx, const double* A, int64_t n, int64_t lda, double* X
     ozr_status e = read_err(ctx, derr);
     if (e != OZR_OK) return e;
   }
-  const double gap_new = gap_min_sorted(hlam_new);
-  if (!(gap_new > 0.0) && P.cluster_mode == 0)
+  const double gap_new0 = gap_min_sorted(hlam_new);
+  if (!(gap_new0 > 0.0) && P.cluster_mode == 0)
     return fail(ctx, OZR_ERR_DEGENERATE, "equal Rayleigh quotients (gap = 0) with the cluster branch off");
+  const double gap_new = (gap_new0 > 0.0) ? gap_new0 : gap_pos_sorted(hlam_new);
   if (eRmax == intmin) eRmax = -1074;
 
   // ---- a6: Res digits (k_R from the accuracy W needs, R8)
@@ -560,7 +600,9 @@ ozr_status sweep(ozr_ctx ctx, const double* A, int64_t n, int64_t lda, double* X
   std::vector<int> eR_col(n);
   OZR_CK(cudaMemcpyAsync(eR_col.data(), eR, n * sizeof(int32_t), cudaMemcpyDeviceToHost, s), "D2H eR");
   OZR_CK(cudaStreamSynchronize(s), "sync");
-  const std::vector<double> gaps_new = col_gaps(hlam_new);
+  std::vector<double> gaps_new = col_gaps(hlam_new);
+  for (double& x : gaps_new)
+    if (!(x > 0.0)) x = gap_new;
   for (int64_t j = 0; j < n; ++j) {
     tau_col[j] = 0.5 * P.theta_W * delta_p * (P.tile_budgets ? std::min(gaps_prev[j], gaps_new[j]) : gapW);
     if (eR_col[j] < -1000) eR_col[j] = -100000;
@@ -596,15 +638,128 @@ ozr_status sweep(ozr_ctx ctx, const double* A, int64_t n, int64_t lda, double* X
   double* nrm2 = ctx->ws<double>(S_NRM2, n);
   OZR_ALLOC(Ep); OZR_ALLOC(nrm2);
   OZR_CK(cudaMemcpyAsync(demax, &intmin, sizeof(int), cudaMemcpyHostToDevice, s), "H2D");
+  int* uf = ctx->ws<int>(S_EDGES, n);
+  int* ecount = ctx->ws<int>(S_ECOUNT, 4);
+  OZR_ALLOC(uf); OZR_ALLOC(ecount);
+  OZR_CK(cudaMemsetAsync(ecount, 0, sizeof(int), s), "memset");
+  if (P.cluster_mode) launch_iota(uf, N, s);
+  const EdgeOut eo{P.cluster_mode, P.kappa, uf, ecount};
   launch_recombine_E(planes, nn, N, N, rp, g, rell, 8 * (kx + kR - LW), rh, lam, g, 0, Ep, n, nrm2, demax, eR, derr,
-                     s);
+                     eo, s);
   OZR_CK(cudaGetLastError(), "recombine E");
   ctx->mark("recombE");
-  int eEmax = 0;
+  int eEmax = 0, nedges = 0;
   OZR_CK(cudaMemcpyAsync(&eEmax, demax, sizeof(int), cudaMemcpyDeviceToHost, s), "D2H");
+  OZR_CK(cudaMemcpyAsync(&nedges, ecount, sizeof(int), cudaMemcpyDeviceToHost, s), "D2H");
   {
     ozr_status e = read_err(ctx, derr);
     if (e != OZR_OK) return e;
+  }
+  ctx->last_members.clear();
+  ctx->last_offsets.assign(1, 0);
+  int cluster_launches = P.cluster_mode ? 1 : 0;  // k_iota
+  if (P.cluster_mode && nedges > 0) {
+    cluster_launches += 1;  // k_uf_flatten
+    // ---- a8 cluster branch (R13): unresolved groups → Rayleigh–Ritz sub-solve (cluster.cu)
+    launch_uf_flatten(uf, N, s);
+    std::vector<int> root(n);
+    OZR_CK(cudaMemcpyAsync(root.data(), uf, n * sizeof(int), cudaMemcpyDeviceToHost, s), "D2H labels");
+    OZR_CK(cudaStreamSynchronize(s), "sync");
+    std::vector<int>& mem = ctx->last_members;
+    std::vector<int>& off = ctx->last_offsets;
+    unresolved_groups(n, root, hlam_new, mem, off);
+    const int ng = static_cast<int>(off.size()) - 1;
+    if (ng > 0) {
+      int mmax = 0;
+      std::vector<int> gm(ng), gsq(ng + 1, 0), grp_of(n, -1), pos_of(n, 0);
+      std::vector<double> mu(ng);
+      std::vector<int4> tiles;
+      for (int q = 0; q < ng; ++q) {
+        const int m = off[q + 1] - off[q];
+        gm[q] = m;
+        mmax = std::max(mmax, m);
+        gsq[q + 1] = gsq[q] + m * m;
+        double sm = 0.0;
+        for (int a = 0; a < m; ++a) {
+          const int j = mem[off[q] + a];
+          sm = sm + hlam_new[j];
+          grp_of[j] = q;
+          pos_of[j] = a;
+        }
+        mu[q] = sm / m;
+        for (int a0 = 0; a0 < m; a0 += 16)
+          for (int b0 = 0; b0 < m; b0 += 16) tiles.push_back(make_int4(q, a0, b0, m));
+      }
+      if (mmax > P.max_cluster)
+        return fail(ctx, OZR_ERR_RANGE, "unresolved group of %d columns exceeds max_cluster = %d", mmax, P.max_cluster);
+      const int nmem = off[ng];
+      // one packed int upload: tiles | off | gsq | gm | mem | grp_of | pos_of | sweeps
+      std::vector<int> pk;
+      pk.reserve(tiles.size() * 4 + 3 * ng + 2 + nmem + 2 * n + ng + 8);
+      for (const int4& t : tiles) { pk.push_back(t.x); pk.push_back(t.y); pk.push_back(t.z); pk.push_back(t.w); }
+      const size_t o_off = pk.size(); pk.insert(pk.end(), off.begin(), off.end());
+      const size_t o_gsq = pk.size(); pk.insert(pk.end(), gsq.begin(), gsq.end());
+      const size_t o_gm = pk.size(); pk.insert(pk.end(), gm.begin(), gm.end());
+      const size_t o_mem = pk.size(); pk.insert(pk.end(), mem.begin(), mem.end());
+      const size_t o_grp = pk.size(); pk.insert(pk.end(), grp_of.begin(), grp_of.end());
+      const size_t o_pos = pk.size(); pk.insert(pk.end(), pos_of.begin(), pos_of.end());
+      const size_t o_sw = pk.size(); pk.resize(pk.size() + ng);
+      int* dpk = ctx->ws<int>(S_CINT, pk.size());
+      double* dmu = ctx->ws<double>(S_CDBL, ng);
+      const size_t sq = static_cast<size_t>(gsq[ng]);
+      double* cM = ctx->ws<double>(S_CM, sq);
+      double* cR = ctx->ws<double>(S_CR, sq);
+      double* cK = ctx->ws<double>(S_CK, sq);
+      double* cV = ctx->ws<double>(S_CV, sq);
+      double* cZ = ctx->ws<double>(S_CZ, sq);
+      double* cT = ctx->ws<double>(S_CT, static_cast<size_t>(nmem) * n);
+      OZR_ALLOC(dpk); OZR_ALLOC(dmu); OZR_ALLOC(cM); OZR_ALLOC(cR); OZR_ALLOC(cK); OZR_ALLOC(cV); OZR_ALLOC(cZ);
+      OZR_ALLOC(cT);
+      OZR_CK(cudaMemcpyAsync(dpk, pk.data(), pk.size() * sizeof(int), cudaMemcpyHostToDevice, s), "H2D");
+      OZR_CK(cudaMemcpyAsync(dmu, mu.data(), ng * sizeof(double), cudaMemcpyHostToDevice, s), "H2D");
+      ClusterLaunch L{};
+      L.ngroups = ng;
+      L.nmembers = nmem;
+      L.mmax = mmax;
+      L.ntiles = static_cast<int>(tiles.size());
+      L.rows = N;
+      L.tiles = reinterpret_cast<const int4*>(dpk);
+      L.goff = dpk + o_off;
+      L.gsq = dpk + o_gsq;
+      L.gm = dpk + o_gm;
+      L.mem = dpk + o_mem;
+      L.grp_of = dpk + o_grp;
+      L.pos_of = dpk + o_pos;
+      L.mu = dmu;
+      L.xdig = xdig;
+      L.ldd = ld;
+      L.pstride = ld * n;
+      L.kx = kx;
+      L.gexp = g;
+      L.r_hi = rh;
+      L.r_lo = rl;
+      L.wplanes = planes;
+      L.wpstride = nn;
+      L.rpW = &rp;
+      L.ellR = rell;
+      L.scale8 = 8 * (kx + kR - LW);
+      L.lam = lam;
+      L.Mbuf = cM; L.Rbuf = cR; L.Kbuf = cK; L.Vbuf = cV; L.Zbuf = cZ; L.T = cT;
+      L.sweeps = dpk + o_sw;
+      L.Ep = Ep;
+      L.lde = n;
+      L.nrm2 = nrm2;
+      L.eE_col = eR;
+      L.eE_max = demax;
+      OZR_CK(launch_cluster(L, s), "cluster sub-solve");
+      ctx->mark("cluster");
+      cluster_launches += 5;
+      OZR_CK(cudaMemcpyAsync(&eEmax, demax, sizeof(int), cudaMemcpyDeviceToHost, s), "D2H");
+      OZR_CK(cudaMemcpyAsync(hlam_new.data(), lam, n * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H");
+      OZR_CK(cudaStreamSynchronize(s), "sync");
+      rep.n_clusters = ng;
+      rep.max_cluster = mmax;
+    }
   }
   if (eEmax == intmin) eEmax = -1074;
   int gmin = 100000;
@@ -683,13 +838,14 @@ ozr_status sweep(ozr_ctx ctx, const double* A, int64_t n, int64_t lda, double* X
   rep.normE_fro = std::sqrt(ne);
   double maxlam_new = 0.0;
   for (double x : hlam_new) maxlam_new = std::max(maxlam_new, std::fabs(x));
-  rep.predicted_error = rep.net_update * rep.net_update * maxlam_new / (static_cast<double>(n) * gap_new);
+  const double gap_out = gap_pos_sorted(hlam_new);
+  rep.predicted_error = rep.net_update * rep.net_update * maxlam_new / (static_cast<double>(n) * gap_out);
   rep.ms_total = tot;
   rep.ms_gemm = gemm_ms;
   rep.int8_ops = ops;
   ctx->dump();
   // kernels of this sweep: [colmax] x1_split transpose GEMM recombine_V split GEMM recombine_E split GEMM final
-  rep.launches = (fresh_w ? 1 : 0) + 10;
+  rep.launches = (fresh_w ? 1 : 0) + 10 + cluster_launches;
   return OZR_OK;
 }
 
@@ -754,8 +910,10 @@ void ozr_params_default(ozr_params* p) {
   p->theta_V = 1.0 / 16;
   p->theta_W = 1.0 / 16;
   p->theta_U = 1.0 / 16;
-  p->cluster_mode = 0;
+  p->cluster_mode = 1;
   p->tile_budgets = 1;
+  p->kappa = 0x1p-10;
+  p->max_cluster = 4096;
 }
 
 ozr_status ozr_split(ozr_ctx ctx, const double* M, const double* M_lo, int64_t rows, int64_t cols, int64_t ldm,
@@ -824,6 +982,18 @@ ozr_status ozr_split(ozr_ctx ctx, const double* M, const double* M_lo, int64_t r
   OZR_CK(cudaGetLastError(), "ozr_split");
   if (k_out) *k_out = k;
   return read_err(ctx, derr);
+}
+
+ozr_status ozr_last_clusters(ozr_ctx ctx, int* members, int max_members, int* offsets, int max_groups, int* ngroups) {
+  if (!ctx) return OZR_ERR_ARG;
+  const int ng = static_cast<int>(ctx->last_offsets.size()) - 1;
+  if (ngroups) *ngroups = ng;
+  if (offsets && max_groups >= ng)
+    for (int q = 0; q <= ng; ++q) offsets[q] = ctx->last_offsets[q];
+  const int nm = ctx->last_offsets[ng];
+  if (max_groups < ng || max_members < nm || (nm > 0 && (!members || !offsets))) return OZR_ERR_RANGE;
+  for (int q = 0; q < nm; ++q) members[q] = ctx->last_members[q];
+  return OZR_OK;
 }
 
 ozr_status ozr_gemm_plan(int64_t k, int kA, int kB, int L, int* ngroups, int* group_diag, int* group_npairs,

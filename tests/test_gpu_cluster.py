@@ -1,0 +1,97 @@
+"""GPU parity and convergence of the clustered-eigenvalue branch (reading R13; the paper assumes
+distinct eigenvalues, and leaves clusters open).
+
+ - FP32-eigensolver starts (BASELINE.json c2 recipe): the paper's Algorithm 1 alone diverges; with the
+   Rayleigh–Ritz sub-solve of the unresolved groups the GPU sweep matches the oracle sweep (columns
+   outside the groups to 1e-13; group columns to the accuracy of an fp64 eigensolver of the sub-problem)
+   and ozr_refine_to_tol reaches the prescribed forward error against the oracle's reference.
+ - Exactly repeated eigenvalue estimates: handled by the branch (cluster_mode 1), an error without it.
+ - The c3 recipe (64 clusters of 8 at 1e-10) from an FP64 start stays in the linear regime (no groups)."""
+import numpy as np
+import pytest
+
+from gpu_util import parity_sweep, to_dev, to_np, vec_dev
+from oracle import refine as orf
+import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+U = 2.0 ** -53
+
+
+def _case(cfg, n, start):
+    c = dict(W.CONFIGS[cfg])
+    A, _ = W.make_matrix(n, c["kind"], c["cnd"], c["seed"])
+    lam0, X0 = W.initial_eig(A, start)
+    return A, lam0, X0
+
+
+@pytest.mark.parametrize("n", [128, 256])
+def test_fp32_start_sweep_parity(ctx, n):
+    A, lam0, X0 = _case("c2", n, "fp32")
+    Xg, lg, rep, Xo, lo, info, groups = parity_sweep(ctx, A, X0, lam0, 1e-14)
+    assert rep["beta"] == info["beta"]
+    assert len(groups) >= 1 and rep["n_clusters"] == len(groups)
+    assert rep["max_cluster"] == max(len(J) for J in groups)
+    inJ = np.zeros(n, dtype=bool)
+    for J in groups:
+        inJ[J] = True
+    # columns outside every group: first-order Ẽ only (north-star bar)
+    assert np.max(np.abs(Xg[:, ~inJ] - Xo[:, ~inJ])) <= 1e-13
+    assert np.max(np.abs(lg[~inJ] - lo[~inJ])) <= 1e-13 * np.max(np.abs(lam0))
+    # group columns: fp64 Jacobi (GPU) vs __float128 Jacobi (oracle) of the same K
+    tol = 1e-13 + 10 * np.sqrt(rep["max_cluster"]) * U * info["cluster_cond"]
+    assert np.max(np.abs(Xg[:, inJ] - Xo[:, inJ])) <= tol
+    assert np.max(np.abs(lg[inJ] - lo[inJ])) <= 1e-13 + U * info["cluster_cond"] * np.max(np.abs(lam0))
+
+
+@pytest.mark.parametrize("n,delta", [(256, 1e-14), pytest.param(1024, 1e-14, marks=pytest.mark.slow)])
+def test_fp32_start_converges(ctx, n, delta):
+    """BASELINE.json c2 (n = 1024, cnd 1e12, FP32 start, δ = 1e-14): the forward error against the oracle's
+    reference eigenvectors of the stored A reaches δ."""
+    import paper_2602_19090_b200 as ozr
+    A, lam0, X0 = _case("c2", n, "fp32")
+    lr, Xr = W.initial_eig(A, "fp64")
+    Xh, Xl, lh, ll, _ = orf.reference_eigvecs(A, Xr, lr)
+    Xd, ld = to_dev(X0), vec_dev(lam0)
+    st, hist = ozr.ozr_refine_to_tol(ctx, to_dev(A), Xd, ld, ozr.default_params(delta=delta, max_sweeps=12))
+    fe = orf.forward_error(Xh, Xl, to_np(Xd), lh, to_np(ld))
+    assert st == 0, hist
+    assert hist[0]["n_clusters"] >= 1
+    assert fe <= delta, (fe, [(h["net_update"], h["n_clusters"], h["max_cluster"]) for h in hist])
+
+
+def _double_eigenvalue_case():
+    """Householder-exact family with λ_10 = λ_11: A = X diag(λ) Xᵀ is exact in fp64 and has
+    an exactly double eigenvalue, so its eigenvectors 10, 11 are only defined up to a rotation."""
+    A0, lam, X_exact, H, lam_cols = W.householder_exact(6, lam_bits=12, seed=3)
+    lam = lam.copy()
+    lam[11] = lam[10]
+    A = (X_exact * lam[None, :]) @ X_exact.T
+    rng = np.random.default_rng(7)
+    X0 = X_exact + 1e-9 * rng.standard_normal(X_exact.shape)
+    return A, lam, X_exact, X0
+
+
+def test_double_eigenvalue(ctx):
+    """A double eigenvalue: the Rayleigh quotients of the pair agree to ~1e-18, w_ij/(λ̂_j − λ̂_i) is O(1),
+    so the pair forms a group; after one sweep its columns are an orthonormal eigenbasis of the double
+    eigenvalue and every other column is the exact eigenvector. Equal λ̂ estimates with the branch off
+    are an error (test_gpu_refine.test_refine_step_errors)."""
+    A, lam, X_exact, X0 = _double_eigenvalue_case()
+    Xg, lg, rep, Xo, lo, info, groups = parity_sweep(ctx, A, X0, lam, 1e-12)
+    assert [10, 11] in [sorted(J) for J in groups] and rep["max_cluster"] == 2
+    other = np.setdiff1d(np.arange(A.shape[0]), [10, 11])
+    assert np.max(np.abs(Xg[:, other] - Xo[:, other])) <= 1e-13
+    assert np.max(np.abs(Xg[:, other] - X_exact[:, other])) <= 1e-12
+    P = Xg[:, [10, 11]]
+    assert np.max(np.abs(A @ P - P * lam[10])) <= 1e-13
+    assert np.max(np.abs(P.T @ P - np.eye(2))) <= 1e-13
+    assert np.max(np.abs(lg[[10, 11]] - lam[10])) <= 1e-13
+
+
+def test_c3_fp64_start_stays_linear(ctx):
+    A, lam0, X0 = _case("c3", 1024, "fp64")
+    Xg, lg, rep, Xo, lo, info, groups = parity_sweep(ctx, A, X0, lam0, 1e-12)
+    assert rep["n_clusters"] == 0 and groups == []
+    assert np.max(np.abs(Xg - Xo)) <= 1e-13

@@ -37,10 +37,13 @@ def geometric_spectrum(n, cnd):
     return cnd ** (-i / max(n - 1, 1))
 
 
-def clustered_spectrum(n, rng, nclusters=64, csize=8, sep=1e-10):
+def clustered_spectrum(n, rng, nclusters=None, csize=8, sep=1e-10):
     """BASELINE.json c3: λ uniform in [−1, 1] with `nclusters` clusters of `csize` eigenvalues
     separated by `sep`: n − nclusters·csize singletons plus nclusters anchors c drawn U[−1, 1], each
-    anchor expanded to {c + m·sep, m = 0..csize−1}."""
+    anchor expanded to {c + m·sep, m = 0..csize−1}. nclusters defaults to 64 at n = 4096 (the
+    config) and n/64 at other sizes (so 1/8 of the spectrum is clustered at every n)."""
+    if nclusters is None:
+        nclusters = max(1, n // 64)
     nsingle = n - nclusters * csize
     draws = rng.uniform(-1.0, 1.0, nsingle + nclusters)
     anchors = draws[:nclusters]
