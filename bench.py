@@ -295,7 +295,7 @@ def main():
                           "l2": "inputs larger than L2 (A + X = %.1f GiB per rank, L2 126 MB)" % (2 * n * n * 8 / 2 ** 30),
                           "flops_per_step": "3 x 2n^3 (V=AX, W=X^T Res, U=X E)",
                           "sweep": {k: r0[k] for k in ("beta", "alpha", "kX", "kA", "kR", "kE", "L_V", "L_W", "L_U",
-                                                       "pairs_V", "pairs_W", "pairs_U")}},
+                                                       "pairs_V", "pairs_W", "pairs_U", "n_clusters", "max_cluster")}},
                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                "gpu_launches": int(sum(r["launches"] for r in reps)), "clocks": clocks,
                "time_to_target": ttt}

@@ -17,13 +17,18 @@
 //   k_cluster_gather  T = Ẽ'[:, J] (compact copy, the apply reads old values)
 //   k_cluster_apply   Ẽ'[:, J] ← T·Z off the group rows, (Z − I)·2^{g_i} on them
 //   k_cluster_colstats column maxima exponents and ‖ẽ_j‖² of the rewritten columns
+#include <cooperative_groups.h>
 #include <cstdint>
 #include <cuda_runtime.h>
 
 #include "ddmath.cuh"
 #include "kernels.h"
 
+#include <algorithm>
+
 namespace ozr {
+
+namespace cg = cooperative_groups;
 
 namespace {
 
@@ -116,77 +121,89 @@ __global__ void __launch_bounds__(TB* TB)
   Rbuf[o] = r;
 }
 
-constexpr int JT = 512;  // threads of the Jacobi CTA
+constexpr int JT = 512;        // threads of a Jacobi CTA
+constexpr int kCoopMin = 192;  // groups at least this large use the whole-GPU cooperative kernel
 
-__global__ void __launch_bounds__(JT)
-    k_cluster_jacobi(const int* __restrict__ goff, const int* __restrict__ gsq, const int* __restrict__ gm,
-                     const int* __restrict__ mem, const double* __restrict__ mu, const double* __restrict__ Mbuf,
-                     const double* __restrict__ Rbuf, double* __restrict__ Kbuf, double* __restrict__ Vbuf,
-                     double* __restrict__ Zbuf, double* __restrict__ lam, int* __restrict__ sweeps_out) {
-  extern __shared__ double jsm[];  // c[mm/2], s[mm/2], diag/θ[m], perm[m] (as double slots), red[JT/32]
-  const int grp = blockIdx.x;
-  const int m = gm[grp];
-  const long long o = gsq[grp];
-  const double* M = Mbuf + o;
-  const double* R = Rbuf + o;
-  double* K = Kbuf + o;
-  double* V = Vbuf + o;
-  double* Z = Zbuf + o;
-  const int mm = m + (m & 1);
-  const int np = mm / 2;
-  double* cs = jsm;
-  double* sn = jsm + np;
-  double* th = sn + np;
-  int* perm = reinterpret_cast<int*>(th + m);
-  double* red = reinterpret_cast<double*>(perm + m + (m & 1));
-  const int tid = threadIdx.x;
-  const long long mm2 = static_cast<long long>(m) * m;
-  // K0 = (M + Mᵀ)/2 into V (scratch), T = C·K0 into K, K = T·C into V ... then swap roles
-  for (long long e = tid; e < mm2; e += JT) {
+// Execution policies of the Jacobi core: one CTA per group, or the whole (cooperative) grid on one group.
+struct CtaExec {
+  __device__ int tid() const { return threadIdx.x; }
+  __device__ int nth() const { return blockDim.x; }
+  __device__ void sync() const { __syncthreads(); }
+  __device__ int any(int v, int* /*flag*/) const { return __syncthreads_or(v); }
+};
+struct GridExec {
+  __device__ int tid() const { return blockIdx.x * blockDim.x + threadIdx.x; }
+  __device__ int nth() const { return gridDim.x * blockDim.x; }
+  __device__ void sync() const { cg::this_grid().sync(); }
+  __device__ int any(int v, int* flag) const {  // flag: a fresh zeroed global int per call
+    if (v) atomicOr(flag, 1);
+    cg::this_grid().sync();
+    return *reinterpret_cast<volatile int*>(flag);
+  }
+};
+
+// tournament (round-robin) schedule: round r pairs position k with position mm−1−k; position 0 is fixed
+__device__ __forceinline__ void rr_pair(int k, int r, int mm, int& p, int& q) {
+  auto pos = [&](int x) { return x == 0 ? 0 : 1 + ((x - 1 + r) % (mm - 1)); };
+  p = pos(k);
+  q = pos(mm - 1 - k);
+  if (p > q) {
+    const int t = p;
+    p = q;
+    q = t;
+  }
+}
+
+// Rayleigh–Ritz sub-solve of one group (see the header): K = C·(M+Mᵀ)/2·C, cyclic parallel Jacobi
+// (tournament ordering, the K update of a round applied as independent 2x2 blocks J_aᵀ K_ab J_b),
+// eigenvalues ascending (ties by index), y_kk ≥ 0, Z = C·Y, λ̂_J = μ + Θ. Deterministic: every phase is
+// element-parallel with fixed arithmetic per element; the only reduction is an exact max.
+// scratch: cs[np], sn[np], th[m], sg[m], perm[m], flags[>= 48], amax (1 u64).
+template <class X>
+__device__ void jacobi_group(const X& ex, int m, const double* __restrict__ M, const double* __restrict__ R,
+                             double* __restrict__ K, double* __restrict__ V, double* __restrict__ Z, double* cs,
+                             double* sn, double* th, double* sg, int* perm, int* flags, unsigned long long* amax, double mu,
+                             const int* __restrict__ J, double* __restrict__ lam, int* sweeps_out) {
+  const int tid = ex.tid(), nth = ex.nth();
+  const long long m2 = static_cast<long long>(m) * m;
+  const int mm = m + (m & 1), np = mm / 2;
+  for (long long e = tid; e < m2; e += nth) {  // V ← K0 = (M + Mᵀ)/2
     const int a = static_cast<int>(e % m), b = static_cast<int>(e / m);
     V[e] = 0.5 * (M[e] + M[static_cast<long long>(a) * m + b]);
   }
-  __syncthreads();
-  for (long long e = tid; e < mm2; e += JT) {  // K = C K0, C = I + R/2
+  ex.sync();
+  for (long long e = tid; e < m2; e += nth) {  // K ← C·K0, C = I + R/2
     const int a = static_cast<int>(e % m), b = static_cast<int>(e / m);
     double s = V[e];
     for (int l = 0; l < m; ++l) s = fma(0.5 * R[static_cast<long long>(l) * m + a], V[static_cast<long long>(b) * m + l], s);
     K[e] = s;
   }
-  __syncthreads();
-  for (long long e = tid; e < mm2; e += JT) {  // V = K C
+  ex.sync();
+  for (long long e = tid; e < m2; e += nth) {  // V ← K·C
     const int a = static_cast<int>(e % m), b = static_cast<int>(e / m);
     double s = K[e];
     for (int l = 0; l < m; ++l) s = fma(K[static_cast<long long>(l) * m + a], 0.5 * R[static_cast<long long>(b) * m + l], s);
     V[e] = s;
   }
-  __syncthreads();
-  double fro2 = 0.0;
-  for (long long e = tid; e < mm2; e += JT) {  // symmetrise into K, V = I
+  ex.sync();
+  unsigned long long mx = 0;
+  for (long long e = tid; e < m2; e += nth) {  // K ← sym(V); max |K| (exact, order-free)
     const int a = static_cast<int>(e % m), b = static_cast<int>(e / m);
     const double x = 0.5 * (V[e] + V[static_cast<long long>(a) * m + b]);
     K[e] = x;
-    fro2 = fma(x, x, fro2);
+    mx = max(mx, static_cast<unsigned long long>(__double_as_longlong(fabs(x))));
   }
-  __syncthreads();
-  for (long long e = tid; e < mm2; e += JT) V[e] = ((e % m) == (e / m)) ? 1.0 : 0.0;
-  // ‖K‖_F (fixed-shape reduction)
-  for (int off = 16; off > 0; off >>= 1) fro2 += __shfl_xor_sync(0xffffffffu, fro2, off);
-  if ((tid & 31) == 0) red[tid >> 5] = fro2;
-  __syncthreads();
-  double f2 = 0.0;
-  for (int w = 0; w < JT / 32; ++w) f2 += red[w];
-  const double tiny = 1e-18 * sqrt(f2);
-  __syncthreads();
+  if (mx) atomicMax(amax, mx);
+  ex.sync();
+  for (long long e = tid; e < m2; e += nth) V[e] = ((e % m) == (e / m)) ? 1.0 : 0.0;
+  const double tiny = 1e-18 * __longlong_as_double(static_cast<long long>(*reinterpret_cast<volatile unsigned long long*>(amax)));
   int sweeps = 0;
   for (int sw = 0; sw < 40; ++sw) {
     int rotated = 0;
     for (int r = 0; r < mm - 1; ++r) {
-      // round-robin: position 0 fixed, the others rotate; pair k = (pos k, pos mm−1−k)
-      for (int k = tid; k < np; k += JT) {
-        auto pos = [&](int x) { return x == 0 ? 0 : 1 + ((x - 1 + r) % (mm - 1)); };
-        int p = pos(k), q = pos(mm - 1 - k);
-        if (p > q) { const int tmp = p; p = q; q = tmp; }
+      for (int k = tid; k < np; k += nth) {  // rotation of pair k
+        int p, q;
+        rr_pair(k, r, mm, p, q);
         double c = 1.0, s = 0.0;
         if (q < m) {
           const double apq = K[static_cast<long long>(q) * m + p];
@@ -202,73 +219,130 @@ __global__ void __launch_bounds__(JT)
         cs[k] = c;
         sn[k] = s;
       }
-      __syncthreads();
-      // rows p,q of K  (K ← JᵀK)
-      for (long long e = tid; e < static_cast<long long>(np) * m; e += JT) {
-        const int k = static_cast<int>(e / m), col = static_cast<int>(e % m);
-        const double s = sn[k];
-        if (s == 0.0) continue;
-        auto pos = [&](int x) { return x == 0 ? 0 : 1 + ((x - 1 + r) % (mm - 1)); };
-        int p = pos(k), q = pos(mm - 1 - k);
-        if (p > q) { const int tmp = p; p = q; q = tmp; }
-        const double c = cs[k];
-        double* kp = K + static_cast<long long>(col) * m;
-        const double x = kp[p], y = kp[q];
-        kp[p] = c * x - s * y;
-        kp[q] = s * x + c * y;
+      ex.sync();
+      // K ← JᵀKJ as 2x2 blocks (rows of pair ka, columns of pair kb); V ← V·J (columns of pair kb)
+      const long long nb = static_cast<long long>(np) * np, nv = static_cast<long long>(np) * m;
+      for (long long e = tid; e < nb + nv; e += nth) {
+        if (e < nb) {
+          const int ka = static_cast<int>(e % np), kb = static_cast<int>(e / np);
+          const double ca = cs[ka], sa = sn[ka], cb = cs[kb], sb = sn[kb];
+          if (sa == 0.0 && sb == 0.0) continue;
+          int p1, q1, p2, q2;
+          rr_pair(ka, r, mm, p1, q1);
+          rr_pair(kb, r, mm, p2, q2);
+          const bool q1v = q1 < m, q2v = q2 < m;
+          double* cp = K + static_cast<long long>(p2) * m;
+          double* cq = K + static_cast<long long>(q2) * m;
+          double x11 = cp[p1], x21 = q1v ? cp[q1] : 0.0;
+          double x12 = q2v ? cq[p1] : 0.0, x22 = (q1v && q2v) ? cq[q1] : 0.0;
+          // columns: [x·1, x·2] ← [c x·1 − s x·2, s x·1 + c x·2]
+          double y11 = cb * x11 - sb * x12, y12 = sb * x11 + cb * x12;
+          double y21 = cb * x21 - sb * x22, y22 = sb * x21 + cb * x22;
+          // rows: [y1·; y2·] ← [c y1· − s y2·; s y1· + c y2·]
+          cp[p1] = ca * y11 - sa * y21;
+          if (q1v) cp[q1] = sa * y11 + ca * y21;
+          if (q2v) {
+            cq[p1] = ca * y12 - sa * y22;
+            if (q1v) cq[q1] = sa * y12 + ca * y22;
+          }
+        } else {
+          const long long e2 = e - nb;
+          const int kb = static_cast<int>(e2 / m), row = static_cast<int>(e2 % m);
+          const double sb = sn[kb];
+          if (sb == 0.0) continue;
+          const double cb = cs[kb];
+          int p2, q2;
+          rr_pair(kb, r, mm, p2, q2);
+          double* vp = V + static_cast<long long>(p2) * m + row;
+          double* vq = V + static_cast<long long>(q2) * m + row;
+          const double x = *vp, y = *vq;
+          *vp = cb * x - sb * y;
+          *vq = sb * x + cb * y;
+        }
       }
-      __syncthreads();
-      // columns p,q of K and V  (K ← K J, V ← V J)
-      for (long long e = tid; e < 2LL * np * m; e += JT) {
-        const int which = static_cast<int>(e / (static_cast<long long>(np) * m));
-        const long long e2 = e % (static_cast<long long>(np) * m);
-        const int k = static_cast<int>(e2 / m), row = static_cast<int>(e2 % m);
-        const double s = sn[k];
-        if (s == 0.0) continue;
-        auto pos = [&](int x) { return x == 0 ? 0 : 1 + ((x - 1 + r) % (mm - 1)); };
-        int p = pos(k), q = pos(mm - 1 - k);
-        if (p > q) { const int tmp = p; p = q; q = tmp; }
-        const double c = cs[k];
-        double* B = which ? V : K;
-        const double x = B[static_cast<long long>(p) * m + row], y = B[static_cast<long long>(q) * m + row];
-        B[static_cast<long long>(p) * m + row] = c * x - s * y;
-        B[static_cast<long long>(q) * m + row] = s * x + c * y;
-      }
-      __syncthreads();
+      ex.sync();
     }
     sweeps = sw + 1;
-    if (!__syncthreads_or(rotated)) break;
+    if (!ex.any(rotated, flags + sw)) break;
   }
-  // ascending order (ties by index), y_kk ≥ 0, Z = C·Y, λ̂_J = μ + Θ
-  for (int k = tid; k < m; k += JT) th[k] = K[static_cast<long long>(k) * m + k];
-  __syncthreads();
-  for (int k = tid; k < m; k += JT) {
+  // ascending Θ (ties by index), y_kk ≥ 0, Z = C·Y, λ̂_J = μ + Θ
+  for (int k = tid; k < m; k += nth) th[k] = K[static_cast<long long>(k) * m + k];
+  ex.sync();
+  for (int k = tid; k < m; k += nth) {
     int rk = 0;
     const double x = th[k];
     for (int l = 0; l < m; ++l) rk += (th[l] < x || (th[l] == x && l < k)) ? 1 : 0;
     perm[rk] = k;
   }
-  __syncthreads();
-  const int* J = mem + goff[grp];
-  for (int k = tid; k < m; k += JT) {
+  ex.sync();
+  for (int k = tid; k < m; k += nth) {  // sign of sorted column k
     const int src = perm[k];
     double piv = V[static_cast<long long>(src) * m + k];
     if (piv == 0.0) {
       double best = -1.0;
       for (int l = 0; l < m; ++l) {
         const double v = V[static_cast<long long>(src) * m + l];
-        if (fabs(v) > best) { best = fabs(v); piv = v; }
+        if (fabs(v) > best) {
+          best = fabs(v);
+          piv = v;
+        }
       }
     }
-    const double sg = piv < 0 ? -1.0 : 1.0;
-    for (int a = 0; a < m; ++a) {  // Z[:,k] = C · (sg · V[:,src])
-      double s = sg * V[static_cast<long long>(src) * m + a];
-      for (int l = 0; l < m; ++l) s = fma(0.5 * R[static_cast<long long>(l) * m + a], sg * V[static_cast<long long>(src) * m + l], s);
-      Z[static_cast<long long>(k) * m + a] = s;
-    }
-    lam[J[k]] = mu[grp] + th[src];
+    sg[k] = piv < 0 ? -1.0 : 1.0;
   }
-  if (tid == 0) sweeps_out[grp] = sweeps;
+  ex.sync();
+  for (long long e = tid; e < m2; e += nth) {  // Z[a,k] = Σ_l C[a,l] y_lk
+    const int a = static_cast<int>(e % m), k = static_cast<int>(e / m);
+    const double* y = V + static_cast<long long>(perm[k]) * m;
+    double s = y[a];
+    for (int l = 0; l < m; ++l) s = fma(0.5 * R[static_cast<long long>(l) * m + a], y[l], s);
+    Z[e] = sg[k] * s;
+  }
+  for (int k = tid; k < m; k += nth) lam[J[k]] = mu + th[perm[k]];
+  if (tid == 0) *sweeps_out = sweeps;
+}
+
+__global__ void __launch_bounds__(JT)
+    k_cluster_jacobi(const int* __restrict__ goff, const int* __restrict__ gsq, const int* __restrict__ gm,
+                     const int* __restrict__ mem, const double* __restrict__ mu, const double* __restrict__ Mbuf,
+                     const double* __restrict__ Rbuf, double* __restrict__ Kbuf, double* __restrict__ Vbuf,
+                     double* __restrict__ Zbuf, double* __restrict__ lam, int* __restrict__ sweeps_out) {
+  extern __shared__ double jsm[];  // cs[np] sn[np] th[m] sg[m] perm[m] | amax
+  const int grp = blockIdx.x;
+  const int m = gm[grp];
+  if (m >= kCoopMin) return;  // solved by the cooperative kernel
+  const int mm = m + (m & 1), np = mm / 2;
+  double* cs = jsm;
+  double* sn = cs + np;
+  double* th = sn + np;
+  double* sg = th + m;
+  int* perm = reinterpret_cast<int*>(sg + m);
+  unsigned long long* amax = reinterpret_cast<unsigned long long*>(jsm + 2 * np + 2 * m + (m + 1) / 2 + 1);
+  if (threadIdx.x == 0) *amax = 0;
+  __syncthreads();
+  const long long o = gsq[grp];
+  jacobi_group(CtaExec{}, m, Mbuf + o, Rbuf + o, Kbuf + o, Vbuf + o, Zbuf + o, cs, sn, th, sg, perm, nullptr, amax,
+               mu[grp], mem + goff[grp], lam, sweeps_out + grp);
+}
+
+// One large group on the whole GPU (cooperative launch; grid-wide syncs between the phases).
+__global__ void __launch_bounds__(JT)
+    k_cluster_jacobi_coop(int grp, const int* __restrict__ goff, const int* __restrict__ gsq, const int* __restrict__ gm,
+                          const int* __restrict__ mem, const double* __restrict__ mu, const double* __restrict__ Mbuf,
+                          const double* __restrict__ Rbuf, double* __restrict__ Kbuf, double* __restrict__ Vbuf,
+                          double* __restrict__ Zbuf, double* __restrict__ lam, int* __restrict__ sweeps_out,
+                          double* __restrict__ scratch, int* __restrict__ flags) {
+  const int m = gm[grp];
+  const int mm = m + (m & 1), np = mm / 2;
+  double* cs = scratch;
+  double* sn = cs + np;
+  double* th = sn + np;
+  double* sg = th + m;
+  int* perm = reinterpret_cast<int*>(sg + m);
+  unsigned long long* amax = reinterpret_cast<unsigned long long*>(flags + 64);
+  const long long o = gsq[grp];
+  jacobi_group(GridExec{}, m, Mbuf + o, Rbuf + o, Kbuf + o, Vbuf + o, Zbuf + o, cs, sn, th, sg, perm, flags, amax, mu[grp],
+               mem + goff[grp], lam, sweeps_out + grp);
 }
 
 __global__ void k_cluster_gather(const int* __restrict__ mem, int nmembers, const double* __restrict__ Ep, long long lde,
@@ -367,8 +441,8 @@ __global__ void __launch_bounds__(256)
 }  // namespace
 
 size_t cluster_jacobi_smem(int mmax) {
-  const int mm = mmax + (mmax & 1);
-  return sizeof(double) * (mm + mmax) + sizeof(int) * (mmax + 2) + sizeof(double) * (JT / 32) + 64;
+  const int m = std::min(mmax, kCoopMin);
+  return sizeof(double) * (2 * (m + 1) + 2 * m + (m + 1) / 2 + 2) + 64;
 }
 
 cudaError_t launch_cluster(const ClusterLaunch& L, cudaStream_t s) {
@@ -377,13 +451,29 @@ cudaError_t launch_cluster(const ClusterLaunch& L, cudaStream_t s) {
                                                  L.rows, L.gexp, L.r_hi, L.r_lo, L.wplanes, L.wpstride, *L.rpW, L.ellR,
                                                  L.scale8, L.lam, L.Mbuf, L.Rbuf);
   const size_t sm = cluster_jacobi_smem(L.mmax);
-  if (sm > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(k_cluster_jacobi, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(sm));
-    if (e != cudaSuccess) return e;
-  }
   k_cluster_jacobi<<<L.ngroups, JT, sm, s>>>(L.goff, L.gsq, L.gm, L.mem, L.mu, L.Mbuf, L.Rbuf, L.Kbuf, L.Vbuf, L.Zbuf,
                                               L.lam, L.sweeps);
+  // large groups: one cooperative whole-GPU launch each
+  static int coop_grid = 0;
+  if (coop_grid == 0) {
+    int dev = 0, nsm = 0, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_cluster_jacobi_coop, JT, 0);
+    coop_grid = nsm * std::max(1, std::min(per, 2));
+  }
+  for (int q = 0; q < L.ngroups; ++q) {
+    if (L.hgm[q] < kCoopMin) continue;
+    cudaError_t e = cudaMemsetAsync(L.coop_flags, 0, 128 * sizeof(int), s);
+    if (e != cudaSuccess) return e;
+    int grp = q;
+    void* args[] = {&grp, (void*)&L.goff, (void*)&L.gsq, (void*)&L.gm, (void*)&L.mem, (void*)&L.mu, (void*)&L.Mbuf,
+                    (void*)&L.Rbuf, (void*)&L.Kbuf, (void*)&L.Vbuf, (void*)&L.Zbuf, (void*)&L.lam, (void*)&L.sweeps,
+                    (void*)&L.coop_scratch, (void*)&L.coop_flags};
+    e = cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_cluster_jacobi_coop), dim3(coop_grid), dim3(JT), args, 0,
+                                    s);
+    if (e != cudaSuccess) return e;
+  }
   dim3 gg(L.nmembers, (L.rows + 255) / 256 < 64 ? (L.rows + 255) / 256 : 64);
   k_cluster_gather<<<gg, 256, 0, s>>>(L.mem, L.nmembers, L.Ep, L.lde, L.rows, L.T);
   dim3 ga((L.rows + 255) / 256, (L.mmax + AK - 1) / AK, L.ngroups);

@@ -78,6 +78,9 @@ struct ClusterLaunch {
   double* nrm2;
   int32_t* eE_col;
   int* eE_max;
+  const int* hgm;          // host copy of gm (which groups take the cooperative whole-GPU Jacobi)
+  double* coop_scratch;    // >= 5·mmax + 8 doubles
+  int* coop_flags;         // >= 128 ints
 };
 size_t cluster_jacobi_smem(int mmax);
 cudaError_t launch_cluster(const ClusterLaunch& L, cudaStream_t s);

@@ -100,7 +100,7 @@ namespace {
 enum Slot {
   S_ADIG, S_AELL, S_W, S_X1, S_XDIG, S_XDIGT, S_G, S_SH, S_SL, S_RH, S_RL, S_PLANES, S_VH, S_VL, S_LAM, S_ER,
   S_ERR, S_EMAX, S_RDIG, S_RELL, S_EP, S_NRM2, S_NU2, S_WNEXT, S_ZEROELL, S_TMP1, S_TMP2, S_BELL, S_AT, S_ONES,
-  S_EDGES, S_ECOUNT, S_CINT, S_CDBL, S_CM, S_CR, S_CK, S_CV, S_CZ, S_CT
+  S_EDGES, S_ECOUNT, S_CINT, S_CDBL, S_CM, S_CR, S_CK, S_CV, S_CZ, S_CT, S_CSCR, S_CFLAG
 };
 
 ozr_status fail(ozr_ctx c, ozr_status st, const char* fmt, ...) {
@@ -751,6 +751,10 @@ ozr_status sweep(ozr_ctx ctx, const double* A, int64_t n, int64_t lda, double* X
       L.nrm2 = nrm2;
       L.eE_col = eR;
       L.eE_max = demax;
+      L.hgm = gm.data();
+      L.coop_scratch = ctx->ws<double>(S_CSCR, 5 * static_cast<size_t>(mmax) + 8);
+      L.coop_flags = ctx->ws<int>(S_CFLAG, 128);
+      OZR_ALLOC(L.coop_scratch); OZR_ALLOC(L.coop_flags);
       OZR_CK(launch_cluster(L, s), "cluster sub-solve");
       ctx->mark("cluster");
       cluster_launches += 5;
