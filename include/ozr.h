@@ -43,6 +43,7 @@ typedef enum {
                                 branch disabled (PAPER.md:333 assumes distinct eigenvalues) */
   OZR_ERR_NOT_CONVERGED = 5, /* stagnation / divergence; X and lambda hold the last accepted sweep */
   OZR_ERR_CUDA = 6,          /* CUDA runtime error (message in ozr_last_error) */
+  OZR_ERR_COMM = 7,          /* collective (NCCL / host group) failure, or NCCL not loadable */
   OZR_ERR_NOMEM = 8          /* device allocation failed */
 } ozr_status;
 
@@ -136,6 +137,7 @@ typedef struct {
   int n_clusters;                   /* unresolved groups given the Rayleigh–Ritz sub-solve (R13)       */
   int max_cluster;                  /* size of the largest such group                                  */
   int launches;                     /* CUDA kernels this sweep launched                                */
+  int exchanges;                    /* collectives this rank issued (0 on one GPU)                     */
   double gap_min, max_abs_lambda;   /* from the λ̂ that chose β                                         */
   double normE_fro;                 /* ‖Ẽ‖_F                                                          */
   double net_update;                /* ν = ‖X̂_new − X̂_old‖_F                                          */
@@ -164,6 +166,41 @@ ozr_status ozr_last_clusters(ozr_ctx ctx, int* members, int max_members, int* of
 ozr_status ozr_refine_to_tol(ozr_ctx ctx, const double* A, int64_t n, int64_t lda, double* X, int64_t ldx,
                              double* lambda, const ozr_params* params, ozr_step_report* history, int max_hist,
                              int* sweeps_done);
+
+/* ------------------------------------------------------------------------------------------------
+ * Multi-GPU: block-column partition of X̂. Rank r of P owns the columns
+ * [r·n/P, (r+1)·n/P) of X̂ (n % P == 0; a P-rank result equals the 1-GPU result bit for bit when n/P
+ * is a multiple of 256). A (n x n) and λ̂ (n) are replicated. Per sweep the ranks all-gather the digit
+ * planes of X̂^(1) and the column exponents g (the left operand of W = X̂ᵀRes and of X̂Ẽ), the column
+ * maxima w, λ̂ and a few scalars, plus — only when an unresolved group spans ranks — its W_JJ and
+ * Ẽ_{:,J} blocks. The paper itself is single-node dense (§4); the partition is the build's.
+ *
+ * Communicators:
+ *   ozr_comm_nccl_id        rank 0: a 128-byte NCCL unique id to broadcast to the other ranks
+ *   ozr_comm_create_nccl    every rank, CUDA device `device` (NCCL is dlopen'ed: libnccl.so.2)
+ *   ozr_comm_create_host_group  `nranks` communicators (out[0..nranks-1]) for ranks that are host
+ *                           threads of ONE process sharing memory (device→host→device exchange):
+ *                           the harness that runs the multi-rank protocol on a single GPU
+ * Errors: OZR_ERR_ARG, OZR_ERR_COMM (message in *_last_error is not available: no context; the
+ * status says what failed).
+ * ------------------------------------------------------------------------------------------------ */
+typedef struct ozr_comm_s* ozr_comm;
+ozr_status ozr_comm_nccl_id(void* id128);
+ozr_status ozr_comm_create_nccl(ozr_comm* out, const void* id128, int nranks, int rank, int device);
+ozr_status ozr_comm_create_host_group(ozr_comm* out, int nranks);
+void ozr_comm_destroy(ozr_comm comm);
+int ozr_comm_size(ozr_comm comm);
+int ozr_comm_rank(ozr_comm comm);
+
+/* ozr_refine_step / ozr_refine_to_tol on this rank's column block. X is the full n x n column-major
+ * array (ldx ≥ n) of which only columns [col0, col0 + n/P), col0 = rank·n/P, are read and written;
+ * lambda (n, replicated) is in/out on every rank; reports are identical on every rank. comm = NULL is
+ * the single-GPU call. Every rank must make the same calls with the same parameters. */
+ozr_status ozr_refine_step_dist(ozr_ctx ctx, ozr_comm comm, const double* A, int64_t n, int64_t lda, double* X,
+                                int64_t ldx, double* lambda, const ozr_params* params, ozr_step_report* report);
+ozr_status ozr_refine_to_tol_dist(ozr_ctx ctx, ozr_comm comm, const double* A, int64_t n, int64_t lda, double* X,
+                                  int64_t ldx, double* lambda, const ozr_params* params, ozr_step_report* history,
+                                  int max_hist, int* sweeps_done);
 
 #ifdef __cplusplus
 }

@@ -353,3 +353,37 @@ def sweep_columns(A, X, lam_prev, delta, J, theta=1.0, beta=None):
     Uh, Ul = _clib.dd_gemm_nt(X1, np.ascontiguousarray(E.T))
     s, e = two_sum(X1J, Uh)
     return fast_two_sum(s, e + Ul)[0], lamJ, beta
+
+
+def sweep_block(A, X, lam_prev, delta, col0, nl, allgather, theta=1.0):
+    """Algorithm 1 (cluster branch off) for the column block J = [col0, col0 + nl) of one
+    rank of the block-column partition: X̂^(1) from the full X̂ (column-local truncation,
+    β from the all-gathered column maxima — here the full X̂ is at hand), V_J = A X̂^(1)_J, λ̂_J, then
+    `allgather(λ̂_J)` → λ̂ (n), W_{:,J} = X̂^(1)ᵀ(V_J − X̂^(1)_J D̂_J), Ẽ_{:,J}, X̂_new,J. The same per-element
+    arithmetic as sweep(), so the concatenated blocks equal the full sweep bit for bit.
+    Returns (X_new[:, J], λ̂ (n))."""
+    A = np.asarray(A, dtype=np.float64)
+    X = np.asarray(X, dtype=np.float64)
+    n = A.shape[0]
+    J = np.arange(col0, col0 + nl)
+    w = np.max(np.abs(X), axis=0)
+    beta, _ = choose_beta(n, delta / theta, lam_prev, ceil_log2(w), w, cluster_mode=0)
+    beta = int(min(max(beta, BETA_MIN), BETA_MAX))
+    X1 = x1_truncate(X, beta)[0]
+    X1J = X1[:, J]
+    Vh, Vl = _clib.dd_gemm_nt(A, np.ascontiguousarray(X1J.T))
+    sh, sl = col_dot_dd(X1J, X1J)
+    rh, rl = dd_add(np.ones(nl), np.zeros(nl), -sh, -sl)
+    th, tl = col_dot_dd(X1J, Vh, Vl)
+    lh, ll = dd_div_dd(th, tl, sh, sl)
+    lam = allgather(lh + ll)
+    ph, pl = two_prod(X1J, lam[J][None, :])
+    Rh, Rl = dd_add(Vh, Vl, -ph, -pl)
+    Wh, Wl = _clib.dd_gemm_nt(np.ascontiguousarray(X1.T), np.ascontiguousarray(Rh.T), None,
+                              np.ascontiguousarray(Rl.T))
+    dl = lam[J][None, :] - lam[:, None]
+    E = np.where(dl != 0, Wh / np.where(dl != 0, dl, 1.0), 0.0)
+    E[J, np.arange(nl)] = (rh + rl) / 2
+    Uh, Ul = _clib.dd_gemm_nt(X1, np.ascontiguousarray(E.T))
+    s, e = two_sum(X1J, Uh)
+    return fast_two_sum(s, e + Ul)[0], lam

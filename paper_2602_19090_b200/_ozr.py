@@ -16,9 +16,11 @@ _SO = os.path.join(_HERE, "libozr.so")
 OZR_COLWISE, OZR_ROWWISE = 0, 1
 OZR_SPLIT_FIXED, OZR_SPLIT_X1 = 0, 1
 STATUS = {0: "OZR_OK", 1: "OZR_ERR_ARG", 2: "OZR_ERR_NONFINITE", 3: "OZR_ERR_RANGE", 4: "OZR_ERR_DEGENERATE",
-          5: "OZR_ERR_NOT_CONVERGED", 6: "OZR_ERR_CUDA", 8: "OZR_ERR_NOMEM"}
+          5: "OZR_ERR_NOT_CONVERGED", 6: "OZR_ERR_CUDA", 7: "OZR_ERR_COMM", 8: "OZR_ERR_NOMEM"}
 EXPORTS = ["ozr_version", "ozr_create", "ozr_destroy", "ozr_last_error", "ozr_split", "ozr_gemm", "ozr_gemm_plan",
-           "ozr_params_default", "ozr_refine_step", "ozr_refine_to_tol", "ozr_last_clusters"]
+           "ozr_params_default", "ozr_refine_step", "ozr_refine_to_tol", "ozr_last_clusters", "ozr_comm_nccl_id",
+           "ozr_comm_create_nccl", "ozr_comm_create_host_group", "ozr_comm_destroy", "ozr_comm_size", "ozr_comm_rank",
+           "ozr_refine_step_dist", "ozr_refine_to_tol_dist"]
 
 
 class OzrError(RuntimeError):
@@ -39,7 +41,7 @@ class Params(ctypes.Structure):
 class StepReport(ctypes.Structure):
     _fields_ = ([(f, ctypes.c_int) for f in ["sweep", "beta", "beta_raw", "alpha", "kX", "kA", "kR", "kE", "L_V",
                                               "L_W", "L_U", "pairs_V", "pairs_W", "pairs_U", "n_clusters", "max_cluster",
-                                              "launches"]] +
+                                              "launches", "exchanges"]] +
                 [(f, ctypes.c_double) for f in ["gap_min", "max_abs_lambda", "normE_fro", "net_update",
                                                  "predicted_error", "ms_total", "ms_gemm", "int8_ops"]])
 
@@ -82,6 +84,24 @@ def lib():
         L.ozr_refine_to_tol.restype = i32
         L.ozr_last_clusters.argtypes = [vp, ip, i32, ip, i32, ip]
         L.ozr_last_clusters.restype = i32
+        L.ozr_comm_nccl_id.argtypes = [vp]
+        L.ozr_comm_nccl_id.restype = i32
+        L.ozr_comm_create_nccl.argtypes = [ctypes.POINTER(vp), vp, i32, i32, i32]
+        L.ozr_comm_create_nccl.restype = i32
+        L.ozr_comm_create_host_group.argtypes = [ctypes.POINTER(vp), i32]
+        L.ozr_comm_create_host_group.restype = i32
+        L.ozr_comm_destroy.argtypes = [vp]
+        L.ozr_comm_destroy.restype = None
+        L.ozr_comm_size.argtypes = [vp]
+        L.ozr_comm_size.restype = i32
+        L.ozr_comm_rank.argtypes = [vp]
+        L.ozr_comm_rank.restype = i32
+        L.ozr_refine_step_dist.argtypes = [vp, vp, vp, i64, i64, vp, i64, vp, ctypes.POINTER(Params),
+                                           ctypes.POINTER(StepReport)]
+        L.ozr_refine_step_dist.restype = i32
+        L.ozr_refine_to_tol_dist.argtypes = [vp, vp, vp, i64, i64, vp, i64, vp, ctypes.POINTER(Params),
+                                             ctypes.POINTER(StepReport), i32, ip]
+        L.ozr_refine_to_tol_dist.restype = i32
         _lib = L
     return _lib
 
@@ -219,3 +239,82 @@ def ozr_last_clusters(ctx, max_members=1 << 20, max_groups=1 << 16):
     ng = ctypes.c_int(0)
     ctx.check(lib().ozr_last_clusters(ctx.h, mem, max_members, off, max_groups, ctypes.byref(ng)))
     return [list(mem[off[g]:off[g + 1]]) for g in range(ng.value)]
+
+
+# ------------------------------------------------------------------------------------------ multi-GPU
+class Comm:
+    """A communicator of the block-column partition (include/ozr.h "Multi-GPU")."""
+
+    def __init__(self, handle):
+        self.h = handle
+
+    @property
+    def size(self):
+        return lib().ozr_comm_size(self.h)
+
+    @property
+    def rank(self):
+        return lib().ozr_comm_rank(self.h)
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().ozr_comm_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def ozr_comm_nccl_id():
+    buf = ctypes.create_string_buffer(128)
+    st = lib().ozr_comm_nccl_id(buf)
+    if st != 0:
+        raise OzrError(st, "ozr_comm_nccl_id (is libnccl.so.2 loadable?)")
+    return bytes(buf.raw)
+
+
+def ozr_comm_create_nccl(uid, nranks, rank, device):
+    if len(uid) != 128:
+        raise ValueError("NCCL unique id is 128 bytes")
+    h = ctypes.c_void_p()
+    st = lib().ozr_comm_create_nccl(ctypes.byref(h), ctypes.create_string_buffer(uid, 128), nranks, rank, device)
+    if st != 0:
+        raise OzrError(st, "ozr_comm_create_nccl")
+    return Comm(h)
+
+
+def ozr_comm_create_host_group(nranks):
+    """`nranks` communicators for ranks that are threads of this process (single-GPU protocol harness)."""
+    hs = (ctypes.c_void_p * nranks)()
+    st = lib().ozr_comm_create_host_group(hs, nranks)
+    if st != 0:
+        raise OzrError(st, "ozr_comm_create_host_group")
+    return [Comm(ctypes.c_void_p(hs[r])) for r in range(nranks)]
+
+
+def _comm_h(comm):
+    return comm.h if comm is not None else ctypes.c_void_p(0)
+
+
+def ozr_refine_step_dist(ctx, comm, A, X, lam, params):
+    """One sweep on this rank's column block of X (full n x n column-major array; columns
+    [rank·n/P, (rank+1)·n/P) are read and written); lam (n) replicated. Returns the report dict."""
+    n = A.shape[0]
+    rep = StepReport()
+    ctx.check(lib().ozr_refine_step_dist(ctx.h, _comm_h(comm), _ptr(A), n, _ld(A), _ptr(X), _ld(X), _ptr(lam),
+                                         ctypes.byref(params), ctypes.byref(rep)))
+    return rep.as_dict()
+
+
+def ozr_refine_to_tol_dist(ctx, comm, A, X, lam, params, raise_on_nonconvergence=False):
+    n = A.shape[0]
+    H = (StepReport * 64)()
+    done = ctypes.c_int(0)
+    st = lib().ozr_refine_to_tol_dist(ctx.h, _comm_h(comm), _ptr(A), n, _ld(A), _ptr(X), _ld(X), _ptr(lam),
+                                      ctypes.byref(params), H, 64, ctypes.byref(done))
+    if st != 0 and (st != 5 or raise_on_nonconvergence):
+        ctx.check(st)
+    return st, [H[i].as_dict() for i in range(done.value)]

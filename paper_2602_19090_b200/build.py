@@ -6,8 +6,8 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 SO = os.path.join(HERE, "libozr.so")
-SOURCES = ["ozr_api.cu", "kernels.cu", "gemm_i8.cu", "cluster.cu"]
-HEADERS = ["ptx.cuh", "ddmath.cuh", "kernels.h", "ozr_internal.h"]
+SOURCES = ["ozr_api.cu", "kernels.cu", "gemm_i8.cu", "cluster.cu", "comm.cu"]
+HEADERS = ["ptx.cuh", "ddmath.cuh", "kernels.h", "ozr_internal.h", "comm.h"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
          "-Xcompiler", "-O2"]
@@ -32,7 +32,7 @@ def build(force=False, verbose=False):
             print(" ".join(cmd), file=sys.stderr)
         subprocess.check_call(cmd)
         objs.append(obj)
-    cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", SO] + objs
+    cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", SO] + objs + ["-ldl"]
     subprocess.check_call(cmd)
     for o in objs:
         os.remove(o)

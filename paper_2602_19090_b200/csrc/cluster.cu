@@ -75,7 +75,8 @@ __global__ void __launch_bounds__(TB* TB)
                     long long ldd, long long pstride, int kx, int rows, const int32_t* __restrict__ gexp,
                     const double* __restrict__ r_hi, const double* __restrict__ r_lo, const int32_t* __restrict__ wplanes,
                     long long wpstride, const __grid_constant__ RecombPlan rpW, const int32_t* __restrict__ ellR,
-                    int scale8, const double* __restrict__ lam, double* __restrict__ Mbuf, double* __restrict__ Rbuf) {
+                    int scale8, const double* __restrict__ lam, double* __restrict__ Mbuf, double* __restrict__ Rbuf,
+                    int col0, int ncols) {
   __shared__ long long qa[KC][TB + 1];
   __shared__ long long qb[KC][TB + 1];
   const int4 t = tiles[blockIdx.x];  // (group, a0, b0, m)
@@ -111,14 +112,18 @@ __global__ void __launch_bounds__(TB* TB)
   const dd gdd = i128_to_dd(SQ);
   const double g = ldexp_fast(gdd.hi, gexp[i] + gexp[j]);
   const double r = (a == b) ? (r_hi[i] + r_lo[i]) : -g;
-  // w_ij from the W = X̂ᵀRes slice-product planes (row i: ℓ = g_i, column j: ℓ = ℓ_Res,j + scale)
-  const int Lj = rpW.tile_budgets ? rpW.tileL[j / 256] : rpW.L;
-  const dd w = recomb_one(wplanes, wpstride, static_cast<long long>(j) * rows + i, rpW, gexp[i] + ellR[j] + scale8, Lj);
-  const double mug = mu[grp];
-  const double Mab = (w.hi + w.lo) + ((a == b ? 1.0 : 0.0) - r) * (lam[j] - mug);
   const long long o = static_cast<long long>(gsq[grp]) + static_cast<long long>(b) * m + a;
-  Mbuf[o] = Mab;
-  Rbuf[o] = r;
+  Rbuf[o] = r;  // every rank (from the all-gathered digits)
+  const int jl = j - col0;
+  if (jl < 0 || jl >= ncols) {  // column owned by another rank: its M entries arrive by the all-reduce
+    Mbuf[o] = 0.0;
+    return;
+  }
+  // w_ij from the W = X̂ᵀRes slice-product planes (row i: ℓ = g_i, local column jl: ℓ = ℓ_Res,jl + scale)
+  const int Lj = rpW.tile_budgets ? rpW.tileL[jl / 256] : rpW.L;
+  const dd w = recomb_one(wplanes, wpstride, static_cast<long long>(jl) * rows + i, rpW, gexp[i] + ellR[jl] + scale8, Lj);
+  const double mug = mu[grp];
+  Mbuf[o] = (w.hi + w.lo) + ((a == b ? 1.0 : 0.0) - r) * (lam[j] - mug);
 }
 
 constexpr int JT = 512;        // threads of a Jacobi CTA
@@ -346,12 +351,13 @@ __global__ void __launch_bounds__(JT)
 }
 
 __global__ void k_cluster_gather(const int* __restrict__ mem, int nmembers, const double* __restrict__ Ep, long long lde,
-                                 int rows, double* __restrict__ T) {
+                                 int rows, double* __restrict__ T, int col0, int ncols) {
   const int c = blockIdx.x;  // member index over all groups
   if (c >= nmembers) return;
-  const int j = mem[c];
+  const int jl = mem[c] - col0;
+  const bool own = jl >= 0 && jl < ncols;  // other ranks' columns arrive by the all-reduce
   for (int i = blockIdx.y * blockDim.x + threadIdx.x; i < rows; i += gridDim.y * blockDim.x)
-    T[static_cast<long long>(c) * rows + i] = Ep[static_cast<long long>(j) * lde + i];
+    T[static_cast<long long>(c) * rows + i] = own ? Ep[static_cast<long long>(jl) * lde + i] : 0.0;
 }
 
 constexpr int AK = 32;  // output columns per apply CTA
@@ -360,7 +366,7 @@ __global__ void __launch_bounds__(256)
     k_cluster_apply(const int* __restrict__ goff, const int* __restrict__ gsq, const int* __restrict__ gm,
                     const int* __restrict__ mem, const int* __restrict__ grp_of, const int* __restrict__ pos_of,
                     const double* __restrict__ T, const double* __restrict__ Zbuf, const int32_t* __restrict__ gexp,
-                    int rows, double* __restrict__ Ep, long long lde) {
+                    int rows, double* __restrict__ Ep, long long lde, int col0, int ncols) {
   const int grp = blockIdx.z;
   const int m = gm[grp];
   const int k0 = blockIdx.y * AK;
@@ -397,18 +403,22 @@ __global__ void __launch_bounds__(256)
   for (int q = 0; q < AK; ++q) {
     if (q >= kn) break;
     const int k = k0 + q;
+    const int jl = J[k] - col0;
+    if (jl < 0 || jl >= ncols) continue;  // owned by another rank
     double v = acc[q];
     if (in) v = ldexp_fast(Z[static_cast<long long>(k) * m + a] - (a == k ? 1.0 : 0.0), gexp[i]);
-    Ep[static_cast<long long>(J[k]) * lde + i] = v;
+    Ep[static_cast<long long>(jl) * lde + i] = v;
   }
 }
 
 __global__ void __launch_bounds__(256)
     k_cluster_colstats(const int* __restrict__ mem, const double* __restrict__ Ep, long long lde, int rows,
                        const int32_t* __restrict__ gexp, double* __restrict__ nrm2, int32_t* __restrict__ eE_col,
-                       int* __restrict__ eE_max) {
+                       int* __restrict__ eE_max, int col0, int ncols) {
   __shared__ double sh[2][8];
-  const int j = mem[blockIdx.x];
+  const int jg = mem[blockIdx.x];
+  const int j = jg - col0;  // local column
+  if (j < 0 || j >= ncols) return;
   double m = 0.0, s2 = 0.0;
   for (int i = threadIdx.x; i < rows; i += 256) {
     const double ep = Ep[static_cast<long long>(j) * lde + i];
@@ -431,7 +441,7 @@ __global__ void __launch_bounds__(256)
       mx = fmax(mx, sh[0][w]);
       ss = __dadd_rn(ss, sh[1][w]);
     }
-    nrm2[j] = ss;
+    nrm2[jg] = ss;
     const int e = (mx > 0.0) ? ceil_log2_d(mx) : -100000;
     eE_col[j] = e;
     if (mx > 0.0) atomicMax(eE_max, e);
@@ -445,11 +455,17 @@ size_t cluster_jacobi_smem(int mmax) {
   return sizeof(double) * (2 * (m + 1) + 2 * m + (m + 1) / 2 + 2) + 64;
 }
 
-cudaError_t launch_cluster(const ClusterLaunch& L, cudaStream_t s) {
+cudaError_t launch_cluster_build(const ClusterLaunch& L, cudaStream_t s) {
   if (L.ntiles > 0)
     k_cluster_build<<<L.ntiles, TB * TB, 0, s>>>(L.tiles, L.goff, L.gsq, L.mem, L.mu, L.xdig, L.ldd, L.pstride, L.kx,
                                                  L.rows, L.gexp, L.r_hi, L.r_lo, L.wplanes, L.wpstride, *L.rpW, L.ellR,
-                                                 L.scale8, L.lam, L.Mbuf, L.Rbuf);
+                                                 L.scale8, L.lam, L.Mbuf, L.Rbuf, L.col0, L.ncols);
+  dim3 gg(L.nmembers, (L.rows + 255) / 256 < 64 ? (L.rows + 255) / 256 : 64);
+  k_cluster_gather<<<gg, 256, 0, s>>>(L.mem, L.nmembers, L.Ep, L.lde, L.rows, L.T, L.col0, L.ncols);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_cluster_solve(const ClusterLaunch& L, cudaStream_t s) {
   const size_t sm = cluster_jacobi_smem(L.mmax);
   k_cluster_jacobi<<<L.ngroups, JT, sm, s>>>(L.goff, L.gsq, L.gm, L.mem, L.mu, L.Mbuf, L.Rbuf, L.Kbuf, L.Vbuf, L.Zbuf,
                                               L.lam, L.sweeps);
@@ -474,12 +490,15 @@ cudaError_t launch_cluster(const ClusterLaunch& L, cudaStream_t s) {
                                     s);
     if (e != cudaSuccess) return e;
   }
-  dim3 gg(L.nmembers, (L.rows + 255) / 256 < 64 ? (L.rows + 255) / 256 : 64);
-  k_cluster_gather<<<gg, 256, 0, s>>>(L.mem, L.nmembers, L.Ep, L.lde, L.rows, L.T);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_cluster_apply(const ClusterLaunch& L, cudaStream_t s) {
   dim3 ga((L.rows + 255) / 256, (L.mmax + AK - 1) / AK, L.ngroups);
   k_cluster_apply<<<ga, 256, 0, s>>>(L.goff, L.gsq, L.gm, L.mem, L.grp_of, L.pos_of, L.T, L.Zbuf, L.gexp, L.rows,
-                                     L.Ep, L.lde);
-  k_cluster_colstats<<<L.nmembers, 256, 0, s>>>(L.mem, L.Ep, L.lde, L.rows, L.gexp, L.nrm2, L.eE_col, L.eE_max);
+                                     L.Ep, L.lde, L.col0, L.ncols);
+  k_cluster_colstats<<<L.nmembers, 256, 0, s>>>(L.mem, L.Ep, L.lde, L.rows, L.gexp, L.nrm2, L.eE_col, L.eE_max,
+                                                L.col0, L.ncols);
   return cudaGetLastError();
 }
 

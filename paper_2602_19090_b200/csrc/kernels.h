@@ -57,6 +57,7 @@ void launch_recombine_E(const int32_t* planes, long long pstride, int rows, int 
 // column indices, ascending (λ̂, index)); per-group m x m workspaces at offset gsq[g] (Σ m²) in M/R/K/V/Z.
 struct ClusterLaunch {
   int ngroups, nmembers, mmax, ntiles, rows;
+  int col0, ncols;    // this rank's columns [col0, col0 + ncols) (block-column partition)
   const int4* tiles;  // (group, a0, b0, m) 16 x 16 tiles of k_cluster_build
   const int *goff, *gsq, *gm, *mem, *grp_of, *pos_of;
   const double* mu;
@@ -75,15 +76,20 @@ struct ClusterLaunch {
   int* sweeps;
   double* Ep;
   long long lde;
-  double* nrm2;
-  int32_t* eE_col;
+  double* nrm2;     // n entries, global column index
+  int32_t* eE_col;  // ncols entries, local column index
   int* eE_max;
   const int* hgm;          // host copy of gm (which groups take the cooperative whole-GPU Jacobi)
   double* coop_scratch;    // >= 5·mmax + 8 doubles
   int* coop_flags;         // >= 128 ints
 };
 size_t cluster_jacobi_smem(int mmax);
-cudaError_t launch_cluster(const ClusterLaunch& L, cudaStream_t s);
+// build: R_JJ (all), M_JJ and T = Ẽ'[:, J] on this rank's columns (zero elsewhere; all-reduced between);
+// solve: Jacobi of every group (replicated on every rank); apply: Ẽ'[:, J] and column statistics of the
+// owned columns.
+cudaError_t launch_cluster_build(const ClusterLaunch& L, cudaStream_t s);
+cudaError_t launch_cluster_solve(const ClusterLaunch& L, cudaStream_t s);
+cudaError_t launch_cluster_apply(const ClusterLaunch& L, cudaStream_t s);
 void launch_final(const int32_t* planes, long long pstride, int rows, int cols, const RecombPlan& rp,
                   const int32_t* ellB, int scale8, const double* X1, long long ldx1, double* X, long long ldx,
                   double* nu2, double* wnext, cudaStream_t s);

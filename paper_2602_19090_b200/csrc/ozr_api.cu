@@ -8,12 +8,14 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <memory>
 #include <string>
 #include <vector>
 
 #include <cuda_runtime.h>
 
 #include "../../include/ozr.h"
+#include "comm.h"
 #include "kernels.h"
 #include "ozr_internal.h"
 
@@ -100,7 +102,7 @@ namespace {
 enum Slot {
   S_ADIG, S_AELL, S_W, S_X1, S_XDIG, S_XDIGT, S_G, S_SH, S_SL, S_RH, S_RL, S_PLANES, S_VH, S_VL, S_LAM, S_ER,
   S_ERR, S_EMAX, S_RDIG, S_RELL, S_EP, S_NRM2, S_NU2, S_WNEXT, S_ZEROELL, S_TMP1, S_TMP2, S_BELL, S_AT, S_ONES,
-  S_EDGES, S_ECOUNT, S_CINT, S_CDBL, S_CM, S_CR, S_CK, S_CV, S_CZ, S_CT, S_CSCR, S_CFLAG
+  S_EDGES, S_ECOUNT, S_CINT, S_CDBL, S_CM, S_CR, S_CK, S_CV, S_CZ, S_CT, S_CSCR, S_CFLAG, S_SCAL, S_UFALL
 };
 
 ozr_status fail(ozr_ctx c, ozr_status st, const char* fmt, ...) {
@@ -383,6 +385,14 @@ ozr_status run_gemm(ozr_ctx ctx, const DigitOperand& A, const DigitOperand& B, i
   return OZR_OK;
 }
 
+ozr_status err_bits(ozr_ctx ctx, int h) {
+  if (h & ERR_NONFINITE) return fail(ctx, OZR_ERR_NONFINITE, "non-finite value in an input matrix");
+  if (h & ERR_RANGE) return fail(ctx, OZR_ERR_RANGE, "exponent range exceeded in the digit split");
+  if (h & ERR_DEGENERATE)
+    return fail(ctx, OZR_ERR_DEGENERATE, "degenerate column or equal eigenvalue estimates (PAPER.md:333)");
+  return OZR_OK;
+}
+
 ozr_status read_err(ozr_ctx ctx, int* derr) {
   int h = 0;
   OZR_CK(cudaMemcpyAsync(&h, derr, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream), "D2H err");
@@ -431,43 +441,92 @@ ozr_status split_A(ozr_ctx ctx, const double* A, int64_t n, int64_t lda, int kA,
   return OZR_OK;
 }
 
-ozr_status sweep(ozr_ctx ctx, const double* A, int64_t n, int64_t lda, double* X, int64_t ldx, double* lambda,
-                 const ozr_params& P, ozr_step_report& rep, SweepState& st) {
+// Block-column partition: rank r of P owns columns [col0, col0 + nl), nl = n/P, col0 = r·nl.
+// Every column of V, Res, W, Ẽ and X̂_new depends only on its own column of X̂^(1) plus the full X̂^(1)
+// (left operand of W and U) and the full λ̂, so a rank computes its columns with the slice GEMMs on
+// M = n, N = nl; the exchange per sweep is: the X̂^(1) digit planes and g (all-gather), the column
+// maxima w, λ̂ and a few per-rank scalars (all-gather), and — only when unresolved groups straddle
+// ranks — their W_JJ / Ẽ_{:,J} blocks (all-reduce of zero-padded buffers, exact). Every host decision is
+// taken from all-gathered data in the 1-GPU order, so a P-rank sweep equals the 1-GPU sweep bit for bit
+// when nl is a multiple of the 256-column tile.
+ozr_status sweep(ozr_ctx ctx, Exchange* ex, const double* A, int64_t n, int64_t lda, double* Xfull, int64_t ldx,
+                 double* lambda, const ozr_params& P, ozr_step_report& rep, SweepState& st) {
   memset(&rep, 0, sizeof rep);
   cudaStream_t s = ctx->stream;
-  const int N = static_cast<int>(n);
+  const int NP = ex ? ex->P : 1, RK = ex ? ex->rank : 0;
+  const int64_t nl = n / NP, col0 = RK * nl;
+  const int N = static_cast<int>(n), NL = static_cast<int>(nl);
+  double* X = Xfull + col0 * ldx;  // this rank's column block
   const int64_t ld = round16(n);
-  const int64_t nn = n * n;
+  const int64_t nnl = n * nl;
   cudaEventRecord(ctx->ev[0], s);
   ctx->mark("start");
   float gemm_ms = 0.f;
   double ops = 0.0;
+  int nexch = 0;
 
   int* derr = ctx->ws<int>(S_ERR, 4);
   int* demax = ctx->ws<int>(S_EMAX, 4);
+  int* scal = ctx->ws<int>(S_SCAL, 4 * static_cast<size_t>(NP) + 4);
   double* w = ctx->ws<double>(S_W, n);
   double* wnext = ctx->ws<double>(S_WNEXT, n);
-  OZR_ALLOC(derr);
-  OZR_ALLOC(demax);
-  OZR_ALLOC(w);
-  OZR_ALLOC(wnext);
+  OZR_ALLOC(derr); OZR_ALLOC(demax); OZR_ALLOC(scal); OZR_ALLOC(w); OZR_ALLOC(wnext);
   OZR_CK(cudaMemsetAsync(derr, 0, sizeof(int), s), "memset");
+
+  // exchange helpers (no-ops on one GPU)
+  auto xgather = [&](void* base, size_t bytes) -> ozr_status {
+    if (!ex) return OZR_OK;
+    ++nexch;
+    if (!ex->allgather(base, bytes, s)) return fail(ctx, OZR_ERR_COMM, "all-gather: %s", ex->err.c_str());
+    return OZR_OK;
+  };
+  auto xsum = [&](double* buf, size_t count) -> ozr_status {
+    if (!ex) return OZR_OK;
+    ++nexch;
+    if (!ex->allreduce_sum(buf, count, s)) return fail(ctx, OZR_ERR_COMM, "all-reduce: %s", ex->err.c_str());
+    return OZR_OK;
+  };
+  // Up to 3 device ints combined over the ranks (max) plus the error flags (OR), with ONE host
+  // synchronisation; pending host copies queued on the stream complete with it. Fails on error flags.
+  auto scalars = [&](std::initializer_list<const int*> dvs, int* outs) -> ozr_status {
+    int k = 0;
+    for (const int* dv : dvs) {
+      OZR_CK(cudaMemcpyAsync(scal + 4 * RK + k, dv, sizeof(int), cudaMemcpyDeviceToDevice, s), "D2D");
+      ++k;
+    }
+    OZR_CK(cudaMemcpyAsync(scal + 4 * RK + 3, derr, sizeof(int), cudaMemcpyDeviceToDevice, s), "D2D");
+    ozr_status e = xgather(scal + 0, 4 * sizeof(int));
+    if (e != OZR_OK) return e;
+    std::vector<int> h(4 * NP);
+    OZR_CK(cudaMemcpyAsync(h.data(), scal, h.size() * sizeof(int), cudaMemcpyDeviceToHost, s), "D2H");
+    OZR_CK(cudaStreamSynchronize(s), "sync");
+    int bits = 0;
+    for (int r = 0; r < NP; ++r) bits |= h[4 * r + 3];
+    for (int q = 0; q < k; ++q) {
+      outs[q] = h[q];
+      for (int r = 1; r < NP; ++r) outs[q] = std::max(outs[q], h[4 * r + q]);
+    }
+    return err_bits(ctx, bits);
+  };
+#define OZR_X(expr)                     \
+  do {                                  \
+    ozr_status e__ = (expr);            \
+    if (e__ != OZR_OK) return e__;      \
+  } while (0)
 
   // ---- a0: statistics and parameters
   const bool fresh_w = !st.have_w;
   if (!st.have_w) {
-    launch_colmax(X, ldx, N, N, w, derr, s);
+    launch_colmax(X, ldx, N, NL, w + col0, derr, s);
     OZR_CK(cudaGetLastError(), "colmax");
   } else {
-    OZR_CK(cudaMemcpyAsync(w, wnext, n * sizeof(double), cudaMemcpyDeviceToDevice, s), "copy w");
+    OZR_CK(cudaMemcpyAsync(w + col0, wnext + col0, nl * sizeof(double), cudaMemcpyDeviceToDevice, s), "copy w");
   }
+  OZR_X(xgather(w, nl * sizeof(double)));
   std::vector<double> hw(n), hlam(n);
   OZR_CK(cudaMemcpyAsync(hw.data(), w, n * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H w");
   OZR_CK(cudaMemcpyAsync(hlam.data(), lambda, n * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H lambda");
-  {
-    ozr_status e = read_err(ctx, derr);
-    if (e != OZR_OK) return e;
-  }
+  OZR_X(scalars({}, nullptr));
   for (double x : hlam)
     if (!std::isfinite(x)) return fail(ctx, OZR_ERR_NONFINITE, "non-finite lambda");
   const double delta_p = P.delta / (P.theta > 0 ? P.theta : 1.0);
@@ -494,21 +553,18 @@ ozr_status sweep(ozr_ctx ctx, const double* A, int64_t n, int64_t lda, double* X
   rep.gap_min = gap0;
   rep.max_abs_lambda = maxlam;
 
-  // ---- A split (once per refine_to_tol call)
-  if (st.A != A || st.nA != n) {
-    ozr_status e = split_A(ctx, A, n, lda, P.kA_split, st);
-    if (e != OZR_OK) return e;
-  }
+  // ---- A split (once per refine_to_tol call; A and its digits are replicated on every rank)
+  if (st.A != A || st.nA != n) OZR_X(split_A(ctx, A, n, lda, P.kA_split, st));
   ctx->mark("stats+splitA");
-  // per-column accuracy of V (R8, R8b): θ_V·δ'·gap_j with the previous λ̂
+  // per-column accuracy of V (R8, R8b): θ_V·δ'·gap_j with the previous λ̂ (this rank's columns)
   std::vector<double> gaps_prev = col_gaps(hlam);
   for (double& x : gaps_prev)
     if (!(x > 0.0)) x = gap;  // equal λ̂ (cluster branch): the smallest positive gap sets the budget
-  std::vector<double> tau_col(n);
-  std::vector<int> c_col(n);
-  for (int64_t j = 0; j < n; ++j) {
-    tau_col[j] = P.theta_V * delta_p * (P.tile_budgets ? gaps_prev[j] : gap);
-    c_col[j] = hw[j] != 0.0 ? ceil_log2_host(hw[j]) : -100000;
+  std::vector<double> tau_col(nl);
+  std::vector<int> c_col(nl);
+  for (int64_t j = 0; j < nl; ++j) {
+    tau_col[j] = P.theta_V * delta_p * (P.tile_budgets ? gaps_prev[col0 + j] : gap);
+    c_col[j] = hw[col0 + j] != 0.0 ? ceil_log2_host(hw[col0 + j]) : -100000;
   }
   unsigned char tileLV[kMaxNTiles];
   double avg_pairs_V = 0.0;
@@ -519,66 +575,68 @@ ozr_status sweep(ozr_ctx ctx, const double* A, int64_t n, int64_t lda, double* X
   rep.kA = kA;
   rep.L_V = LV;
 
-  // ---- a2: X̂ → X̂^(1) + digits + r (exact)
-  double* X1 = ctx->ws<double>(S_X1, nn);
+  // ---- a2: X̂ → X̂^(1) + digits + r (exact), local columns; then the digit exchange (a11)
+  double* X1 = ctx->ws<double>(S_X1, nnl);
   int8_t* xdig = ctx->ws<int8_t>(S_XDIG, static_cast<size_t>(7) * ld * n);
   int8_t* xdigT = ctx->ws<int8_t>(S_XDIGT, static_cast<size_t>(7) * ld * n);
   int32_t* g = ctx->ws<int32_t>(S_G, n);
-  double* sh = ctx->ws<double>(S_SH, n);
-  double* sl = ctx->ws<double>(S_SL, n);
-  double* rh = ctx->ws<double>(S_RH, n);
+  double* sh = ctx->ws<double>(S_SH, nl);
+  double* sl = ctx->ws<double>(S_SL, nl);
+  double* rh = ctx->ws<double>(S_RH, n);  // r_j of every column (all-gathered: the cluster branch reads them)
   double* rl = ctx->ws<double>(S_RL, n);
-  int32_t* zell = ctx->ws<int32_t>(S_ZEROELL, n);
   OZR_ALLOC(X1); OZR_ALLOC(xdig); OZR_ALLOC(xdigT); OZR_ALLOC(g); OZR_ALLOC(sh); OZR_ALLOC(sl); OZR_ALLOC(rh);
-  OZR_ALLOC(rl); OZR_ALLOC(zell);
-  launch_x1_split(X, ldx, N, N, beta, kx, w, X1, n, xdig, ld, ld * n, g, sh, sl, rh, rl, derr, s);
+  OZR_ALLOC(rl);
+  launch_x1_split(X, ldx, N, NL, beta, kx, w + col0, X1, n, xdig + col0 * ld, ld, ld * n, g + col0, sh, sl, rh + col0,
+                  rl + col0, derr, s);
   OZR_CK(cudaGetLastError(), "x1 split");
+  if (ex) {
+    if (!ex->group_begin()) return fail(ctx, OZR_ERR_COMM, "%s", ex->err.c_str());
+    for (int p = 0; p < kx; ++p) OZR_X(xgather(xdig + p * ld * n, static_cast<size_t>(nl * ld)));
+    OZR_X(xgather(g, nl * sizeof(int32_t)));
+    OZR_X(xgather(rh, nl * sizeof(double)));
+    OZR_X(xgather(rl, nl * sizeof(double)));
+    if (!ex->group_end(s)) return fail(ctx, OZR_ERR_COMM, "%s", ex->err.c_str());
+  }
   launch_transpose_i8(xdig, ld, ld * n, xdigT, ld, ld * n, N, N, kx, s);
-  ctx->mark("x1split+transpose");
+  ctx->mark("x1split+exchange+transpose");
   OZR_CK(cudaGetLastError(), "transpose digits");
-  OZR_CK(cudaMemsetAsync(zell, 0, n * sizeof(int32_t), s), "memset");
 
-  // ---- a3: P1  V = A·X̂^(1)  (Alg. 1 line 1, eq. mat_mul)
+  // ---- a3: P1  V = A·X̂^(1)_J  (Alg. 1 line 1, eq. mat_mul)
   std::vector<Group> gV = plan_groups(kA, kx, LV, n);
   PairTable pt;
   RecombPlan rp;
   if (!make_tables(gV, LV, n, pt, rp)) return fail(ctx, OZR_ERR_RANGE, "V plan too large");
   const bool tilesV = P.tile_budgets && P.L_V <= 0;
-  if (tilesV) apply_tiles(pt, rp, tileLV, n);
+  if (tilesV) apply_tiles(pt, rp, tileLV, nl);
   size_t maxG = gV.size();
-  int32_t* planes = ctx->ws<int32_t>(S_PLANES, maxG * nn);
+  int32_t* planes = ctx->ws<int32_t>(S_PLANES, maxG * nnl);
   OZR_ALLOC(planes);
   DigitOperand opA{reinterpret_cast<const int8_t*>(ctx->bufs[S_ADIG].p), ld, ld * n, st.kA_split};
-  DigitOperand opX{xdig, ld, ld * n, kx};
-  {
-    ozr_status e = run_gemm(ctx, opA, opX, N, N, N, pt, planes, 0);
-    if (e != OZR_OK) return e;
-  }
+  DigitOperand opXJ{xdig + col0 * ld, ld, ld * n, kx};  // local columns (B operand of V)
+  DigitOperand opX{xdig, ld, ld * n, kx};               // all columns (A operand of W)
+  OZR_X(run_gemm(ctx, opA, opXJ, N, NL, N, pt, planes, 0));
   ctx->mark("gemmV");
   const double pV = tilesV ? avg_pairs_V : static_cast<double>(count_pairs(gV));
   rep.pairs_V = static_cast<int>(std::lround(pV));
-  ops += 2.0 * n * n * n * pV;
+  ops += 2.0 * n * n * nl * pV;
 
   // ---- a4-a6: recombine V, λ̂, Res, column maxima
-  double* Vh = ctx->ws<double>(S_VH, nn);
-  double* Vl = ctx->ws<double>(S_VL, nn);
+  double* Vh = ctx->ws<double>(S_VH, nnl);
+  double* Vl = ctx->ws<double>(S_VL, nnl);
   double* lam = ctx->ws<double>(S_LAM, n);
-  int32_t* eR = ctx->ws<int32_t>(S_ER, n);
+  int32_t* eR = ctx->ws<int32_t>(S_ER, nl);
   OZR_ALLOC(Vh); OZR_ALLOC(Vl); OZR_ALLOC(lam); OZR_ALLOC(eR);
   const int intmin = -(1 << 30);
   OZR_CK(cudaMemcpyAsync(demax, &intmin, sizeof(int), cudaMemcpyHostToDevice, s), "H2D");
-  launch_recombine_V(planes, nn, N, N, rp, reinterpret_cast<const int32_t*>(ctx->bufs[S_AELL].p), g,
-                     8 * (st.kA_split + kx - LV), X1, n, sh, sl, Vh, Vl, n, lam, eR, demax, s);
+  launch_recombine_V(planes, nnl, N, NL, rp, reinterpret_cast<const int32_t*>(ctx->bufs[S_AELL].p), g + col0,
+                     8 * (st.kA_split + kx - LV), X1, n, sh, sl, Vh, Vl, n, lam + col0, eR, demax, s);
   OZR_CK(cudaGetLastError(), "recombine V");
   ctx->mark("recombV");
+  OZR_X(xgather(lam, nl * sizeof(double)));
   int eRmax = 0;
   std::vector<double> hlam_new(n);
-  OZR_CK(cudaMemcpyAsync(&eRmax, demax, sizeof(int), cudaMemcpyDeviceToHost, s), "D2H");
   OZR_CK(cudaMemcpyAsync(hlam_new.data(), lam, n * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H");
-  {
-    ozr_status e = read_err(ctx, derr);
-    if (e != OZR_OK) return e;
-  }
+  OZR_X(scalars({demax}, &eRmax));
   const double gap_new0 = gap_min_sorted(hlam_new);
   if (!(gap_new0 > 0.0) && P.cluster_mode == 0)
     return fail(ctx, OZR_ERR_DEGENERATE, "equal Rayleigh quotients (gap = 0) with the cluster branch off");
@@ -589,22 +647,22 @@ ozr_status sweep(ozr_ctx ctx, const double* A, int64_t n, int64_t lda, double* X
   const double gapW = std::min(gap, gap_new);
   const double tauW = P.theta_W * delta_p * gapW;
   const int kR = digits_for(eRmax, static_cast<int>(std::floor(std::log2(tauW / 2.0))));
-  int8_t* rdig = ctx->ws<int8_t>(S_RDIG, static_cast<size_t>(kMaxDigits) * ld * n);
-  int32_t* rell = ctx->ws<int32_t>(S_RELL, n);
+  int8_t* rdig = ctx->ws<int8_t>(S_RDIG, static_cast<size_t>(kMaxDigits) * ld * nl);
+  int32_t* rell = ctx->ws<int32_t>(S_RELL, nl);
   OZR_ALLOC(rdig); OZR_ALLOC(rell);
-  launch_split_fixed(Vh, Vl, n, N, N, kR, rdig, ld, ld * n, rell, derr, s);
+  launch_split_fixed(Vh, Vl, n, N, NL, kR, rdig, ld, ld * nl, rell, derr, s);
   OZR_CK(cudaGetLastError(), "split Res");
   ctx->mark("host+splitRes");
 
-  // ---- a7: P3  W = X̂^(1)ᵀ Res  (Alg. 1 line 4)
-  std::vector<int> eR_col(n);
-  OZR_CK(cudaMemcpyAsync(eR_col.data(), eR, n * sizeof(int32_t), cudaMemcpyDeviceToHost, s), "D2H eR");
+  // ---- a7: P3  W_{:,J} = X̂^(1)ᵀ Res_J  (Alg. 1 line 4)
+  std::vector<int> eR_col(nl);
+  OZR_CK(cudaMemcpyAsync(eR_col.data(), eR, nl * sizeof(int32_t), cudaMemcpyDeviceToHost, s), "D2H eR");
   OZR_CK(cudaStreamSynchronize(s), "sync");
   std::vector<double> gaps_new = col_gaps(hlam_new);
   for (double& x : gaps_new)
     if (!(x > 0.0)) x = gap_new;
-  for (int64_t j = 0; j < n; ++j) {
-    tau_col[j] = 0.5 * P.theta_W * delta_p * (P.tile_budgets ? std::min(gaps_prev[j], gaps_new[j]) : gapW);
+  for (int64_t j = 0; j < nl; ++j) {
+    tau_col[j] = 0.5 * P.theta_W * delta_p * (P.tile_budgets ? std::min(gaps_prev[col0 + j], gaps_new[col0 + j]) : gapW);
     if (eR_col[j] < -1000) eR_col[j] = -100000;
   }
   unsigned char tileLW[kMaxNTiles];
@@ -615,26 +673,23 @@ ozr_status sweep(ozr_ctx ctx, const double* A, int64_t n, int64_t lda, double* X
   std::vector<Group> gW = plan_groups(kx, kR, LW, n);
   if (!make_tables(gW, LW, n, pt, rp)) return fail(ctx, OZR_ERR_RANGE, "W plan too large");
   const bool tilesW = P.tile_budgets && P.L_W <= 0;
-  if (tilesW) apply_tiles(pt, rp, tileLW, n);
+  if (tilesW) apply_tiles(pt, rp, tileLW, nl);
   if (gW.size() > maxG) {
     maxG = gW.size();
-    planes = ctx->ws<int32_t>(S_PLANES, maxG * nn);
+    planes = ctx->ws<int32_t>(S_PLANES, maxG * nnl);
     OZR_ALLOC(planes);
   }
-  DigitOperand opR{rdig, ld, ld * n, kR};
-  {
-    ozr_status e = run_gemm(ctx, opX, opR, N, N, N, pt, planes, 1);
-    if (e != OZR_OK) return e;
-  }
+  DigitOperand opR{rdig, ld, ld * nl, kR};
+  OZR_X(run_gemm(ctx, opX, opR, N, NL, N, pt, planes, 1));
   ctx->mark("host+gemmW");
   rep.kR = kR;
   rep.L_W = LW;
   const double pW = tilesW ? avg_pairs_W : static_cast<double>(count_pairs(gW));
   rep.pairs_W = static_cast<int>(std::lround(pW));
-  ops += 2.0 * n * n * n * pW;
+  ops += 2.0 * n * n * nl * pW;
 
   // ---- a8: Ẽ (Alg. 1 line 5), Ẽ' = diag(2^g) Ẽ
-  double* Ep = ctx->ws<double>(S_EP, nn);
+  double* Ep = ctx->ws<double>(S_EP, nnl);
   double* nrm2 = ctx->ws<double>(S_NRM2, n);
   OZR_ALLOC(Ep); OZR_ALLOC(nrm2);
   OZR_CK(cudaMemcpyAsync(demax, &intmin, sizeof(int), cudaMemcpyHostToDevice, s), "H2D");
@@ -644,27 +699,51 @@ ozr_status sweep(ozr_ctx ctx, const double* A, int64_t n, int64_t lda, double* X
   OZR_CK(cudaMemsetAsync(ecount, 0, sizeof(int), s), "memset");
   if (P.cluster_mode) launch_iota(uf, N, s);
   const EdgeOut eo{P.cluster_mode, P.kappa, uf, ecount};
-  launch_recombine_E(planes, nn, N, N, rp, g, rell, 8 * (kx + kR - LW), rh, lam, g, 0, Ep, n, nrm2, demax, eR, derr,
-                     eo, s);
+  launch_recombine_E(planes, nnl, N, NL, rp, g, rell, 8 * (kx + kR - LW), rh + col0, lam, g, static_cast<int>(col0), Ep, n,
+                     nrm2 + col0, demax, eR, derr, eo, s);
   OZR_CK(cudaGetLastError(), "recombine E");
   ctx->mark("recombE");
   int eEmax = 0, nedges = 0;
-  OZR_CK(cudaMemcpyAsync(&eEmax, demax, sizeof(int), cudaMemcpyDeviceToHost, s), "D2H");
-  OZR_CK(cudaMemcpyAsync(&nedges, ecount, sizeof(int), cudaMemcpyDeviceToHost, s), "D2H");
   {
-    ozr_status e = read_err(ctx, derr);
-    if (e != OZR_OK) return e;
+    int o2[2];
+    OZR_X(scalars({demax, ecount}, o2));
+    eEmax = o2[0];
+    nedges = o2[1];
   }
   ctx->last_members.clear();
   ctx->last_offsets.assign(1, 0);
   int cluster_launches = P.cluster_mode ? 1 : 0;  // k_iota
   if (P.cluster_mode && nedges > 0) {
-    cluster_launches += 1;  // k_uf_flatten
     // ---- a8 cluster branch (R13): unresolved groups → Rayleigh–Ritz sub-solve (cluster.cu)
+    cluster_launches += 1;  // k_uf_flatten
     launch_uf_flatten(uf, N, s);
     std::vector<int> root(n);
-    OZR_CK(cudaMemcpyAsync(root.data(), uf, n * sizeof(int), cudaMemcpyDeviceToHost, s), "D2H labels");
-    OZR_CK(cudaStreamSynchronize(s), "sync");
+    if (NP == 1) {
+      OZR_CK(cudaMemcpyAsync(root.data(), uf, n * sizeof(int), cudaMemcpyDeviceToHost, s), "D2H labels");
+      OZR_CK(cudaStreamSynchronize(s), "sync");
+    } else {  // every rank's partition of the pairs it saw → one union on the host, in rank order
+      int* ufall = ctx->ws<int>(S_UFALL, static_cast<size_t>(NP) * n);
+      OZR_ALLOC(ufall);
+      OZR_CK(cudaMemcpyAsync(ufall + RK * n, uf, n * sizeof(int), cudaMemcpyDeviceToDevice, s), "D2D");
+      OZR_X(xgather(ufall, n * sizeof(int)));
+      std::vector<int> lab(static_cast<size_t>(NP) * n);
+      OZR_CK(cudaMemcpyAsync(lab.data(), ufall, lab.size() * sizeof(int), cudaMemcpyDeviceToHost, s), "D2H labels");
+      OZR_CK(cudaStreamSynchronize(s), "sync");
+      for (int64_t i = 0; i < n; ++i) root[i] = static_cast<int>(i);
+      auto find = [&](int a) {
+        while (root[a] != a) {
+          root[a] = root[root[a]];
+          a = root[a];
+        }
+        return a;
+      };
+      for (int r = 0; r < NP; ++r)
+        for (int64_t i = 0; i < n; ++i) {
+          const int a = find(static_cast<int>(i)), b = find(lab[r * n + i]);
+          if (a != b) root[std::max(a, b)] = std::min(a, b);
+        }
+      for (int64_t i = 0; i < n; ++i) root[i] = find(static_cast<int>(i));
+    }
     std::vector<int>& mem = ctx->last_members;
     std::vector<int>& off = ctx->last_offsets;
     unresolved_groups(n, root, hlam_new, mem, off);
@@ -723,6 +802,8 @@ ozr_status sweep(ozr_ctx ctx, const double* A, int64_t n, int64_t lda, double* X
       L.mmax = mmax;
       L.ntiles = static_cast<int>(tiles.size());
       L.rows = N;
+      L.col0 = static_cast<int>(col0);
+      L.ncols = NL;
       L.tiles = reinterpret_cast<const int4*>(dpk);
       L.goff = dpk + o_off;
       L.gsq = dpk + o_gsq;
@@ -739,7 +820,7 @@ ozr_status sweep(ozr_ctx ctx, const double* A, int64_t n, int64_t lda, double* X
       L.r_hi = rh;
       L.r_lo = rl;
       L.wplanes = planes;
-      L.wpstride = nn;
+      L.wpstride = nnl;
       L.rpW = &rp;
       L.ellR = rell;
       L.scale8 = 8 * (kx + kR - LW);
@@ -755,12 +836,17 @@ ozr_status sweep(ozr_ctx ctx, const double* A, int64_t n, int64_t lda, double* X
       L.coop_scratch = ctx->ws<double>(S_CSCR, 5 * static_cast<size_t>(mmax) + 8);
       L.coop_flags = ctx->ws<int>(S_CFLAG, 128);
       OZR_ALLOC(L.coop_scratch); OZR_ALLOC(L.coop_flags);
-      OZR_CK(launch_cluster(L, s), "cluster sub-solve");
+      // (1) M_JJ columns owned by this rank, (2) all-reduce → full M on every rank, (3) Jacobi (replicated),
+      // (4) T = Ẽ'[:, J] owned columns, all-reduce, (5) apply + column statistics on owned columns
+      OZR_CK(launch_cluster_build(L, s), "cluster build");
+      OZR_X(xsum(cM, sq));
+      OZR_CK(launch_cluster_solve(L, s), "cluster solve");
+      OZR_X(xsum(cT, static_cast<size_t>(nmem) * n));
+      OZR_CK(launch_cluster_apply(L, s), "cluster apply");
       ctx->mark("cluster");
       cluster_launches += 5;
-      OZR_CK(cudaMemcpyAsync(&eEmax, demax, sizeof(int), cudaMemcpyDeviceToHost, s), "D2H");
       OZR_CK(cudaMemcpyAsync(hlam_new.data(), lam, n * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H");
-      OZR_CK(cudaStreamSynchronize(s), "sync");
+      OZR_X(scalars({demax}, &eEmax));
       rep.n_clusters = ng;
       rep.max_cluster = mmax;
     }
@@ -773,18 +859,18 @@ ozr_status sweep(ozr_ctx ctx, const double* A, int64_t n, int64_t lda, double* X
     for (int x : hg) gmin = std::min(gmin, x);
   }
 
-  // ---- a9: P4  U = X̂^(1) Ẽ = Q Ẽ' ; X̂ ← RN(X̂^(1) + U)  (Alg. 1 line 6)
+  // ---- a9: P4  U_J = X̂^(1) Ẽ_{:,J} = Q Ẽ'_{:,J} ; X̂_J ← RN(X̂^(1)_J + U_J)  (Alg. 1 line 6)
   const double tauU = P.theta_U * delta_p;
   const int kE = digits_for(eEmax, static_cast<int>(std::floor(std::log2(tauU / 2.0))) + gmin);
-  launch_split_fixed(Ep, nullptr, n, N, N, kE, rdig, ld, ld * n, rell, derr, s);
+  launch_split_fixed(Ep, nullptr, n, N, NL, kE, rdig, ld, ld * nl, rell, derr, s);
   OZR_CK(cudaGetLastError(), "split E");
   ctx->mark("host+splitE");
   const int SX = 8 * (kx - 1) + 6;
   // R8b for X̂Ẽ: uniform accuracy θ_U·δ', but columns with small corrections need fewer pairs
-  std::vector<int> eE_col(n);
-  OZR_CK(cudaMemcpyAsync(eE_col.data(), eR, n * sizeof(int32_t), cudaMemcpyDeviceToHost, s), "D2H eE");
+  std::vector<int> eE_col(nl);
+  OZR_CK(cudaMemcpyAsync(eE_col.data(), eR, nl * sizeof(int32_t), cudaMemcpyDeviceToHost, s), "D2H eE");
   OZR_CK(cudaStreamSynchronize(s), "sync");
-  for (int64_t j = 0; j < n; ++j) tau_col[j] = tauU / 2.0;
+  for (int64_t j = 0; j < nl; ++j) tau_col[j] = tauU / 2.0;
   unsigned char tileLU[kMaxNTiles];
   double avg_pairs_U = 0.0;
   int LU = tile_budgets(kx, kE, n, SX, eE_col, tau_col, tileLU, &avg_pairs_U);
@@ -793,38 +879,34 @@ ozr_status sweep(ozr_ctx ctx, const double* A, int64_t n, int64_t lda, double* X
   std::vector<Group> gU = plan_groups(kx, kE, LU, n);
   if (!make_tables(gU, LU, n, pt, rp)) return fail(ctx, OZR_ERR_RANGE, "U plan too large");
   const bool tilesU = P.tile_budgets && P.L_U <= 0;
-  if (tilesU) apply_tiles(pt, rp, tileLU, n);
+  if (tilesU) apply_tiles(pt, rp, tileLU, nl);
   if (gU.size() > maxG) {
     maxG = gU.size();
-    planes = ctx->ws<int32_t>(S_PLANES, maxG * nn);
+    planes = ctx->ws<int32_t>(S_PLANES, maxG * nnl);
     OZR_ALLOC(planes);
   }
   DigitOperand opQ{xdigT, ld, ld * n, kx};
-  DigitOperand opE{rdig, ld, ld * n, kE};
-  {
-    ozr_status e = run_gemm(ctx, opQ, opE, N, N, N, pt, planes, 2);
-    if (e != OZR_OK) return e;
-  }
+  DigitOperand opE{rdig, ld, ld * nl, kE};
+  OZR_X(run_gemm(ctx, opQ, opE, N, NL, N, pt, planes, 2));
   ctx->mark("gemmU");
   rep.kE = kE;
   rep.L_U = LU;
   const double pU = tilesU ? avg_pairs_U : static_cast<double>(count_pairs(gU));
   rep.pairs_U = static_cast<int>(std::lround(pU));
-  ops += 2.0 * n * n * n * pU;
+  ops += 2.0 * n * n * nl * pU;
   double* nu2 = ctx->ws<double>(S_NU2, n);
   OZR_ALLOC(nu2);
-  launch_final(planes, nn, N, N, rp, rell, 8 * (kx + kE - LU), X1, n, X, ldx, nu2, wnext, s);
+  launch_final(planes, nnl, N, NL, rp, rell, 8 * (kx + kE - LU), X1, n, X, ldx, nu2 + col0, wnext + col0, s);
   OZR_CK(cudaGetLastError(), "final update");
   ctx->mark("final");
+  OZR_X(xgather(nu2, nl * sizeof(double)));
+  OZR_X(xgather(nrm2, nl * sizeof(double)));
   OZR_CK(cudaMemcpyAsync(lambda, lam, n * sizeof(double), cudaMemcpyDeviceToDevice, s), "copy lambda");
   cudaEventRecord(ctx->ev[1], s);
   std::vector<double> hnu(n), hnrm(n);
   OZR_CK(cudaMemcpyAsync(hnu.data(), nu2, n * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H");
   OZR_CK(cudaMemcpyAsync(hnrm.data(), nrm2, n * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H");
-  {
-    ozr_status e = read_err(ctx, derr);
-    if (e != OZR_OK) return e;
-  }
+  OZR_X(scalars({}, nullptr));
   double nu = 0.0, ne = 0.0;
   for (int64_t j = 0; j < n; ++j) {
     nu += hnu[j];
@@ -844,12 +926,24 @@ ozr_status sweep(ozr_ctx ctx, const double* A, int64_t n, int64_t lda, double* X
   for (double x : hlam_new) maxlam_new = std::max(maxlam_new, std::fabs(x));
   const double gap_out = gap_pos_sorted(hlam_new);
   rep.predicted_error = rep.net_update * rep.net_update * maxlam_new / (static_cast<double>(n) * gap_out);
+  if (ex) {  // report the global pair budgets (each rank planned its own column tiles)
+    int hv[3] = {rep.L_V, rep.L_W, rep.L_U}, gv[3];
+    OZR_CK(cudaMemcpyAsync(scal + 4 * NP, hv, sizeof hv, cudaMemcpyHostToDevice, s), "H2D");
+    int* d = scal + 4 * NP;
+    OZR_X(scalars({d, d + 1, d + 2}, gv));
+    rep.L_V = gv[0];
+    rep.L_W = gv[1];
+    rep.L_U = gv[2];
+    rep.kA = std::min(st.kA_split, rep.L_V - 1);
+  }
   rep.ms_total = tot;
   rep.ms_gemm = gemm_ms;
   rep.int8_ops = ops;
+  rep.exchanges = nexch;
   ctx->dump();
   // kernels of this sweep: [colmax] x1_split transpose GEMM recombine_V split GEMM recombine_E split GEMM final
   rep.launches = (fresh_w ? 1 : 0) + 10 + cluster_launches;
+#undef OZR_X
   return OZR_OK;
 }
 
@@ -1060,40 +1154,92 @@ ozr_status ozr_gemm(ozr_ctx ctx, int64_t m, int64_t n, int64_t k, const double* 
   return OZR_OK;
 }
 
-ozr_status ozr_refine_step(ozr_ctx ctx, const double* A, int64_t n, int64_t lda, double* X, int64_t ldx,
-                           double* lambda, const ozr_params* params, ozr_step_report* report) {
+struct ozr_comm_s {
+  std::unique_ptr<ozr::Exchange> ex;
+};
+
+ozr_status ozr_comm_nccl_id(void* id128) {
+  if (!id128) return OZR_ERR_ARG;
+  std::string err;
+  return nccl_unique_id(id128, err) ? OZR_OK : OZR_ERR_COMM;
+}
+
+ozr_status ozr_comm_create_nccl(ozr_comm* out, const void* id128, int nranks, int rank, int device) {
+  if (!out || !id128 || nranks < 1 || rank < 0 || rank >= nranks) return OZR_ERR_ARG;
+  *out = nullptr;
+  if (cudaSetDevice(device) != cudaSuccess) return OZR_ERR_CUDA;
+  std::string err;
+  NcclExchange* ex = nccl_create(id128, nranks, rank, err);
+  if (!ex) {
+    fprintf(stderr, "ozr: %s\n", err.c_str());
+    return OZR_ERR_COMM;
+  }
+  ozr_comm c = new ozr_comm_s();
+  c->ex.reset(ex);
+  *out = c;
+  return OZR_OK;
+}
+
+ozr_status ozr_comm_create_host_group(ozr_comm* out, int nranks) {
+  if (!out || nranks < 1) return OZR_ERR_ARG;
+  auto grp = std::make_shared<HostGroup>(nranks);
+  for (int r = 0; r < nranks; ++r) {
+    HostExchange* ex = new HostExchange();
+    ex->P = nranks;
+    ex->rank = r;
+    ex->g = grp;
+    out[r] = new ozr_comm_s();
+    out[r]->ex.reset(ex);
+  }
+  return OZR_OK;
+}
+
+void ozr_comm_destroy(ozr_comm comm) { delete comm; }
+int ozr_comm_size(ozr_comm comm) { return comm ? comm->ex->P : 1; }
+int ozr_comm_rank(ozr_comm comm) { return comm ? comm->ex->rank : 0; }
+
+namespace {
+ozr_status check_refine_args(ozr_ctx ctx, ozr_comm comm, const double* A, int64_t n, int64_t lda, const double* X,
+                             int64_t ldx, const double* lambda, const ozr_params* params) {
   ozr_status st = check_ctx(ctx);
   if (st != OZR_OK) return st;
   if (!A || !X || !lambda || !params || n < 2 || lda < n || ldx < n)
-    return fail(ctx, OZR_ERR_ARG, "ozr_refine_step: bad argument");
-  if (n > 65536) return fail(ctx, OZR_ERR_ARG, "ozr_refine_step: n too large");
+    return fail(ctx, OZR_ERR_ARG, "ozr_refine: bad argument");
+  if (n > 65536) return fail(ctx, OZR_ERR_ARG, "ozr_refine: n too large");
+  if (comm && (n % comm->ex->P != 0 || n / comm->ex->P < 1))
+    return fail(ctx, OZR_ERR_ARG, "ozr_refine: n must be a multiple of the number of ranks");
   if (!(params->delta > kU)) return fail(ctx, OZR_ERR_RANGE, "delta must exceed u = 2^-53");
   if (params->kA_split < 2 || params->kA_split > kMaxDigits) return fail(ctx, OZR_ERR_RANGE, "kA_split");
+  return OZR_OK;
+}
+}  // namespace
+
+ozr_status ozr_refine_step_dist(ozr_ctx ctx, ozr_comm comm, const double* A, int64_t n, int64_t lda, double* X,
+                                int64_t ldx, double* lambda, const ozr_params* params, ozr_step_report* report) {
+  ozr_status st = check_refine_args(ctx, comm, A, n, lda, X, ldx, lambda, params);
+  if (st != OZR_OK) return st;
   SweepState ss;
   ozr_step_report rep;
-  st = sweep(ctx, A, n, lda, X, ldx, lambda, *params, rep, ss);
+  st = sweep(ctx, comm ? comm->ex.get() : nullptr, A, n, lda, X, ldx, lambda, *params, rep, ss);
   rep.sweep = 1;
   if (report) *report = rep;
   return st;
 }
 
-ozr_status ozr_refine_to_tol(ozr_ctx ctx, const double* A, int64_t n, int64_t lda, double* X, int64_t ldx,
-                             double* lambda, const ozr_params* params, ozr_step_report* history, int max_hist,
-                             int* sweeps_done) {
-  ozr_status st = check_ctx(ctx);
+ozr_status ozr_refine_to_tol_dist(ozr_ctx ctx, ozr_comm comm, const double* A, int64_t n, int64_t lda, double* X,
+                                  int64_t ldx, double* lambda, const ozr_params* params, ozr_step_report* history,
+                                  int max_hist, int* sweeps_done) {
+  ozr_status st = check_refine_args(ctx, comm, A, n, lda, X, ldx, lambda, params);
   if (st != OZR_OK) return st;
-  if (!A || !X || !lambda || !params || n < 2 || lda < n || ldx < n)
-    return fail(ctx, OZR_ERR_ARG, "ozr_refine_to_tol: bad argument");
-  if (!(params->delta > kU)) return fail(ctx, OZR_ERR_RANGE, "delta must exceed u = 2^-53");
-  if (params->kA_split < 2 || params->kA_split > kMaxDigits) return fail(ctx, OZR_ERR_RANGE, "kA_split");
   SweepState ss;
   double nu_prev = -1.0;
   int done = 0;
   ozr_status result = OZR_ERR_NOT_CONVERGED;
+  ctx->err.clear();
   const int maxs = params->max_sweeps > 0 ? params->max_sweeps : 6;
   for (int k = 0; k < maxs; ++k) {
     ozr_step_report rep;
-    st = sweep(ctx, A, n, lda, X, ldx, lambda, *params, rep, ss);
+    st = sweep(ctx, comm ? comm->ex.get() : nullptr, A, n, lda, X, ldx, lambda, *params, rep, ss);
     rep.sweep = k + 1;
     if (st != OZR_OK) {
       if (sweeps_done) *sweeps_done = done;
@@ -1114,6 +1260,17 @@ ozr_status ozr_refine_to_tol(ozr_ctx ctx, const double* A, int64_t n, int64_t ld
   if (result != OZR_OK && ctx->err.empty()) fail(ctx, OZR_ERR_NOT_CONVERGED, "max_sweeps reached");
   if (sweeps_done) *sweeps_done = done;
   return result;
+}
+
+ozr_status ozr_refine_step(ozr_ctx ctx, const double* A, int64_t n, int64_t lda, double* X, int64_t ldx,
+                           double* lambda, const ozr_params* params, ozr_step_report* report) {
+  return ozr_refine_step_dist(ctx, nullptr, A, n, lda, X, ldx, lambda, params, report);
+}
+
+ozr_status ozr_refine_to_tol(ozr_ctx ctx, const double* A, int64_t n, int64_t lda, double* X, int64_t ldx,
+                             double* lambda, const ozr_params* params, ozr_step_report* history, int max_hist,
+                             int* sweeps_done) {
+  return ozr_refine_to_tol_dist(ctx, nullptr, A, n, lda, X, ldx, lambda, params, history, max_hist, sweeps_done);
 }
 
 }  // extern "C"

@@ -1,0 +1,124 @@
+"""The block-column partition through libozr's own collectives (include/ozr.h "Multi-GPU").
+
+On the one GPU of the test box the P ranks are host threads of this process, each with its own context
+and stream, exchanging through the library's host-group transport (ozr_comm_create_host_group): no
+kernel ever waits on another rank's kernel. The partitioned sweep must equal the 1-GPU sweep bit for
+bit (X̂ column blocks, λ̂ on every rank, β and digit budgets), including unresolved groups that span
+ranks. The NCCL transport runs as a 1-rank communicator over a torch.distributed group."""
+import threading
+
+import numpy as np
+import pytest
+
+from gpu_util import to_dev, to_np, vec_dev
+import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+
+def _case(cfg, n, start):
+    c = dict(W.CONFIGS[cfg])
+    A, _ = W.make_matrix(n, c["kind"], c["cnd"], c["seed"])
+    lam0, X0 = W.initial_eig(A, start)
+    return A, lam0, X0
+
+
+def _run_ranks(P, A, X0, lam0, params, to_tol=False):
+    import torch
+
+    import paper_2602_19090_b200 as ozr
+    comms = ozr.ozr_comm_create_host_group(P)
+    out, errs = [None] * P, []
+
+    def rank_main(r):
+        try:
+            torch.cuda.set_device(0)
+            stream = torch.cuda.Stream()
+            with torch.cuda.stream(stream):
+                ctx = ozr.Context(0, stream=stream)
+                Ad, Xd, ld = to_dev(A), to_dev(X0), vec_dev(lam0)
+                stream.wait_stream(torch.cuda.default_stream())
+                if to_tol:
+                    st, rep = ozr.ozr_refine_to_tol_dist(ctx, comms[r], Ad, Xd, ld, params)
+                else:
+                    st, rep = 0, ozr.ozr_refine_step_dist(ctx, comms[r], Ad, Xd, ld, params)
+                stream.synchronize()
+                out[r] = (st, to_np(Xd), to_np(ld), rep)
+                ctx.close()
+        except Exception as e:  # pragma: no cover - reported below
+            errs.append((r, repr(e)))
+
+    ts = [threading.Thread(target=rank_main, args=(r,)) for r in range(P)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join(timeout=600)
+    assert not errs, errs
+    return out
+
+
+def _assemble(out, n, P):
+    nl = n // P
+    return np.concatenate([out[r][1][:, r * nl:(r + 1) * nl] for r in range(P)], axis=1)
+
+
+KEYS = ("beta", "kX", "kA", "kR", "kE", "L_V", "L_W", "L_U", "n_clusters", "max_cluster")
+
+
+@pytest.mark.parametrize("cfg,n,start,P", [("c2", 512, "fp64", 2), ("c3", 1024, "fp64", 4),
+                                           ("c2", 512, "fp32", 2)])
+def test_partitioned_sweep_equals_single_gpu(ctx, cfg, n, start, P):
+    import paper_2602_19090_b200 as ozr
+    A, lam0, X0 = _case(cfg, n, start)
+    delta = W.CONFIGS[cfg]["delta"]
+    p = ozr.default_params(delta=delta)
+    Xd, ld = to_dev(X0), vec_dev(lam0)
+    ref = ozr.ozr_refine_step(ctx, to_dev(A), Xd, ld, p)
+    X1, l1 = to_np(Xd), to_np(ld)
+    out = _run_ranks(P, A, X0, lam0, p)
+    Xp = _assemble(out, n, P)
+    assert np.array_equal(Xp, X1)
+    for r in range(P):
+        assert np.array_equal(out[r][2], l1)
+        assert {k: out[r][3][k] for k in KEYS} == {k: ref[k] for k in KEYS}
+        assert out[r][3]["exchanges"] > 0
+    if start == "fp32":  # the unresolved group spans both ranks' columns
+        assert ref["n_clusters"] >= 1 and ref["max_cluster"] > n // P
+
+
+def test_partitioned_refine_to_tol(ctx):
+    import paper_2602_19090_b200 as ozr
+    A, lam0, X0 = _case("c2", 1024, "fp32")
+    p = ozr.default_params(delta=1e-14, max_sweeps=10)
+    Xd, ld = to_dev(X0), vec_dev(lam0)
+    st1, hist1 = ozr.ozr_refine_to_tol(ctx, to_dev(A), Xd, ld, p)
+    out = _run_ranks(4, A, X0, lam0, p, to_tol=True)
+    assert st1 == 0 and all(o[0] == 0 for o in out)
+    assert np.array_equal(_assemble(out, 1024, 4), to_np(Xd))
+    assert len(out[0][3]) == len(hist1)
+
+
+def test_nccl_single_rank(ctx):
+    """The NCCL transport end to end with one rank (libnccl.so.2 dlopen'ed by the library)."""
+    import os
+
+    import torch.distributed as dist
+
+    import paper_2602_19090_b200 as ozr
+    from paper_2602_19090_b200.dist import comm_from_process_group
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29533")
+    dist.init_process_group("gloo", rank=0, world_size=1)
+    try:
+        comm = comm_from_process_group(0)
+        A, lam0, X0 = _case("c3", 512, "fp64")
+        p = ozr.default_params(delta=1e-12)
+        Xd, ld = to_dev(X0), vec_dev(lam0)
+        ref = ozr.ozr_refine_step(ctx, to_dev(A), Xd, ld, p)
+        Xn, ln = to_dev(X0), vec_dev(lam0)
+        rep = ozr.ozr_refine_step_dist(ctx, comm, to_dev(A), Xn, ln, p)
+        assert np.array_equal(to_np(Xn), to_np(Xd)) and np.array_equal(to_np(ln), to_np(ld))
+        assert rep["exchanges"] > 0 and rep["beta"] == ref["beta"]
+        comm.close()
+    finally:
+        dist.destroy_process_group()
