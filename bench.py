@@ -8,8 +8,9 @@ from the same X̂₀ each step (the restore copy is inside the timed step). Effe
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4p] [--n N] [--impl ozr|reference]
 
-N > 1 (torchrun): every rank refines its own seeded problem (weak scaling, no data-path collective;
-DESIGN.md "Multi-GPU"); time = max over ranks (NCCL all-reduce of the device times).
+N > 1 (torchrun): ONE problem partitioned by block columns of X̂ over the ranks (strong scaling; the
+library all-gathers the X̂^(1) digit planes, λ̂ and a few scalars per sweep over NCCL, DESIGN.md §7);
+time = max over ranks (NCCL all-reduce of the device times).
 --impl reference: the CPU oracle (oracle/, dd triple loops) on a bounded column sample of the same
 workload, rank 0 only.
 """
@@ -183,7 +184,27 @@ def main():
     import workloads as W
 
     name = args.config
-    A, lam0, X0, cfg = W.make_config_torch(name, dev, n=args.n or None, seed_offset=rank)
+    comm = None
+    if ws > 1:
+        # one problem, block-column partition: rank 0 builds it, every rank receives A, X̂₀, λ̂₀
+        from paper_2602_19090_b200.dist import comm_from_process_group, partition
+        if rank == 0:
+            A, lam0, X0, cfg = W.make_config_torch(name, dev, n=args.n or None)
+        else:
+            cfg = dict(W.CONFIGS[name])
+            if args.n:
+                cfg["n"] = args.n
+            nn_ = cfg["n"]
+            A = ozr.colmajor(torch.empty((nn_, nn_), dtype=torch.float64, device=dev))
+            X0 = ozr.colmajor(torch.empty((nn_, nn_), dtype=torch.float64, device=dev))
+            lam0 = torch.empty(nn_, dtype=torch.float64, device=dev)
+        for t_ in (A, X0, lam0):
+            dist.broadcast(t_, src=0)
+        comm = comm_from_process_group(local)
+        col0, nl = partition(cfg["n"], ws, rank)
+    else:
+        A, lam0, X0, cfg = W.make_config_torch(name, dev, n=args.n or None)
+        col0, nl = 0, cfg["n"]
     n = cfg["n"]
     delta = cfg["delta"]
     ctx = ozr.Context(local)
@@ -191,11 +212,15 @@ def main():
     X = X0.clone()
     X = ozr.colmajor(X)
     lam = lam0.clone()
+    Xb, X0b = X[:, col0:col0 + nl], X0[:, col0:col0 + nl]  # this rank's column block (contiguous)
+
+    def refine_step(Xt, lt):
+        return ozr.ozr_refine_step_dist(ctx, comm, A, Xt, lt, params)
 
     def step():
-        X.copy_(X0)
+        Xb.copy_(X0b)
         lam.copy_(lam0)
-        return ozr.ozr_refine_step(ctx, A, X, lam, params)
+        return refine_step(X, lam)
 
     for _ in range(max(args.warmup, 0)):
         step()
@@ -222,18 +247,31 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     ms_step = ms / args.steps
-    flops_step = 3 * 2.0 * n ** 3
-    value = ws * flops_step / (ms_step / 1e3) / 1e12
+    flops_step = 3 * 2.0 * n ** 3  # the whole problem (split over the ranks when ws > 1)
+    value = flops_step / (ms_step / 1e3) / 1e12
 
     # dominant kernel: the tcgen05 INT8 slice GEMM (device time from the library's own events)
     gemm_ms = sum(r["ms_gemm"] for r in reps)
     gemm_ops = sum(r["int8_ops"] for r in reps)
     peaks, src = _peaks()
-    int8_peak = 2.0 * peaks["bf16_tflops_sustained"]
+    # the timed region is a fraction of a second at max SM clock (see "clocks"), so the BURST bf16
+    # figure is the denominator; the sustained-clock fraction is reported beside it
+    int8_peak = 2.0 * peaks["bf16_tflops"]
+    int8_sus = 2.0 * peaks["bf16_tflops_sustained"]
     achieved = gemm_ops / (gemm_ms / 1e3) / 1e12
+    traffic, tnote = None, None
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            tj = json.load(f)
+        if tj.get("n") == n and ws == 1:
+            traffic, tnote = tj["dram_bytes"], tj["note"]
+    except Exception:
+        pass
     roofline = {"bound": "tensor", "achieved": achieved, "peak": int8_peak, "unit": "TFLOP/s", "frac": achieved / int8_peak,
-                "traffic": None, "dtype": "int8 (TOPS)",
-                "peak_source": f"2 x bf16_tflops_sustained of {src} MEASURED_PEAKS.json (nominal int8:bf16 = 2)",
+                "traffic": traffic, "traffic_note": tnote, "dtype": "int8 (TOPS)",
+                "peak_source": f"2 x bf16_tflops (burst) of {src} MEASURED_PEAKS.json (nominal int8:bf16 = 4.5:2.25)",
+                "frac_of_sustained_peak": achieved / int8_sus,
+                "kernel": "k_gemm_i8 (tcgen05 kind::i8 slice products; V, W, U launches of the timed sweeps)",
                 "gemm_share_of_step": gemm_ms / ms,
                 "library_sweep_ms": sum(r["ms_total"] for r in reps) / len(reps)}
 
@@ -244,7 +282,7 @@ def main():
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
     t0.record()
-    st, hist = ozr.ozr_refine_to_tol(ctx, A, X, lam, ozr.default_params(delta=delta, max_sweeps=6))
+    st, hist = ozr.ozr_refine_to_tol_dist(ctx, comm, A, X, lam, ozr.default_params(delta=delta, max_sweeps=6))
     t1.record()
     torch.cuda.synchronize()
     ttt = {"ms": t0.elapsed_time(t1), "sweeps": len(hist), "status": int(st), "delta": delta,
@@ -252,30 +290,36 @@ def main():
            "note": "self-certified stop (DESIGN.md R12); forward error vs oracle reference verified in tests at n<=1024"}
 
     # e2e: host (pinned) buffers -> device, sweep, device -> host, every step
+    # (each rank: A and λ̂ replicated, its own column block of X̂ in and out)
     hA = A.cpu().pin_memory()
-    hX0 = X0.cpu().pin_memory()
+    hX0 = X0b.cpu().pin_memory()
     hl0 = lam0.cpu().pin_memory()
     hX = torch.empty_like(hX0).pin_memory()
     hl = torch.empty_like(hl0).pin_memory()
-    Ad = torch.empty_like(A)
+    Ad = ozr.colmajor(torch.empty_like(A))
     torch.cuda.synchronize()
-    w0 = time.perf_counter()
+    if ws > 1:
+        dist.barrier()
     s0 = torch.cuda.Event(enable_timing=True)
     s1 = torch.cuda.Event(enable_timing=True)
     s0.record()
     for _ in range(args.e2e_steps):
         Ad.copy_(hA, non_blocking=True)
-        X.copy_(hX0, non_blocking=True)
+        Xb.copy_(hX0, non_blocking=True)
         lam.copy_(hl0, non_blocking=True)
-        ozr.ozr_refine_step(ctx, Ad, X, lam, params)
-        hX.copy_(X, non_blocking=True)
+        ozr.ozr_refine_step_dist(ctx, comm, Ad, X, lam, params)
+        hX.copy_(Xb, non_blocking=True)
         hl.copy_(lam, non_blocking=True)
     s1.record()
     torch.cuda.synchronize()
     e2e_ms = s0.elapsed_time(s1) / args.e2e_steps
-    h2d = (A.numel() + X0.numel() + lam0.numel()) * 8
-    d2h = (X0.numel() + lam0.numel()) * 8
-    e2e = {"value": ws * flops_step / (e2e_ms / 1e3) / 1e12, "unit": "TFLOP/s", "h2d_bytes_per_step": h2d,
+    if ws > 1:
+        t = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    h2d = ws * (A.numel() + lam0.numel()) * 8 + X0.numel() * 8   # whole job, all ranks
+    d2h = ws * lam0.numel() * 8 + X0.numel() * 8
+    e2e = {"value": flops_step / (e2e_ms / 1e3) / 1e12, "unit": "TFLOP/s", "h2d_bytes_per_step": h2d,
            "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms}
 
     cpu = None
@@ -288,10 +332,11 @@ def main():
     r0 = reps[-1]
     if rank == 0:
         out = {"metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": ws, "steps": args.steps,
-               "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+               "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
                "vs_baseline": None, "dtype": "int8", "data": "synthetic",
                "config": {"workload": f"{name}: " + _describe(cfg, n), "n": n, "delta": delta,
-                          "parallelism": f"replicas x{ws}" if ws > 1 else "1 GPU",
+                          "parallelism": f"block-column partition x{ws} (NCCL all-gather of X^(1) digits per sweep)"
+                          if ws > 1 else "1 GPU",
                           "l2": "inputs larger than L2 (A + X = %.1f GiB per rank, L2 126 MB)" % (2 * n * n * 8 / 2 ** 30),
                           "flops_per_step": "3 x 2n^3 (V=AX, W=X^T Res, U=X E)",
                           "sweep": {k: r0[k] for k in ("beta", "alpha", "kX", "kA", "kR", "kE", "L_V", "L_W", "L_U",

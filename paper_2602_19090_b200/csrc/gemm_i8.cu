@@ -29,6 +29,7 @@ constexpr int A_STAGE_BYTES = BM * BK;
 constexpr int B_STAGE_BYTES = BN * BK;
 constexpr int SMEM_BYTES = STAGES * (A_STAGE_BYTES + B_STAGE_BYTES) + 1024 /*align*/ + 256 /*barriers*/;
 constexpr int TMEM_COLS = 256;
+constexpr int BAND = 4;  // n-tiles per rasterisation band
 
 __global__ void __launch_bounds__(128, 1)
     k_gemm_i8(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -45,10 +46,17 @@ __global__ void __launch_bounds__(128, 1)
 
   const int G = pt.ngroups;
   const int job = blockIdx.x;
-  const int g = job % G;
+  const int g = job % G;  // the groups of one tile run back to back (they share its operand rows)
   const int tile = job / G;
-  const int m0 = (tile % tiles_m) * BM;
-  const int n0 = (tile / tiles_m) * BN;
+  // L2 rasterisation: bands of BAND n-tiles; inside a band, consecutive tiles sweep the band's n-tiles
+  // for one m-tile, then the next m-tile — the band's B columns stay L2-resident while A streams once
+  // per band (instead of once per n-tile)
+  const int tiles_n = (N + BN - 1) / BN;
+  const int band = tile / (BAND * tiles_m);
+  const int r = tile - band * (BAND * tiles_m);
+  const int nb = min(BAND, tiles_n - band * BAND);
+  const int m0 = (r / nb) * BM;
+  const int n0 = (band * BAND + r % nb) * BN;
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   if (pt.tile_budgets && pt.diag[g] > pt.tileL[n0 / BN]) return;  // beyond this column tile's budget

@@ -1,0 +1,98 @@
+#!/usr/bin/env python
+"""Summarise the round's ncu outputs (tools/profile_round.sh) into markdown tables.
+usage: python tools/ncu_summary.py gpurun_out [--hbm-peak 6533.8]"""
+import collections
+import csv
+import io
+import subprocess
+import sys
+
+
+def launch_table(path):
+    rows = list(csv.reader(open(path)))
+    hdr = None
+    agg = collections.OrderedDict()
+    for r in rows:
+        if "Kernel Name" in r:
+            hdr = r
+            continue
+        if hdr and len(r) == len(hdr):
+            d = dict(zip(hdr, r))
+            if d.get("Metric Name") != "gpu__time_duration.sum":
+                continue
+            k = d["Kernel Name"].split("(")[0].replace("ozr::", "").replace("(anonymous namespace)::", "")
+            v = float(d["Metric Value"].replace(",", ""))
+            unit = d.get("Metric Unit", "ns")
+            v = v * {"ns": 1e-6, "us": 1e-3, "usecond": 1e-3, "ms": 1.0, "msecond": 1.0, "nsecond": 1e-6}.get(unit, 1e-6)
+            a = agg.setdefault(k, [0, 0.0])
+            a[0] += 1
+            a[1] += v
+    tot = sum(v[1] for v in agg.values())
+    out = ["| kernel | launches | total ms | share |", "|---|---|---|---|"]
+    for k, (c, t) in sorted(agg.items(), key=lambda x: -x[1][1]):
+        out.append(f"| {k} | {c} | {t:.2f} | {t / tot:.3f} |")
+    return "\n".join(out), agg
+
+
+METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+           "gpu__compute_memory_throughput.avg.pct_of_peak_sustained_elapsed",
+           "dram__throughput.avg.pct_of_peak_sustained_elapsed",
+           "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+           "sm__pipe_tensor_op_imma_cycles_active.avg.pct_of_peak_sustained_elapsed",
+           "sm__inst_executed_pipe_tensor_op_imma.avg.pct_of_peak_sustained_active",
+           "launch__registers_per_thread", "launch__grid_size", "smsp__cycles_active.avg.pct_of_peak_sustained_elapsed",
+           "sm__cycles_elapsed.avg.per_second", "lts__t_sector_hit_rate.pct"]
+
+
+def raw(rep):
+    txt = subprocess.check_output(["ncu", "-i", rep, "--page", "raw", "--csv"], text=True)
+    rows = list(csv.reader(io.StringIO(txt)))
+    hdr, units = rows[0], rows[1]
+    out = []
+    for r in rows[2:]:
+        d = dict(zip(hdr, r))
+        u = dict(zip(hdr, units))
+        out.append((d, u))
+    return out
+
+
+def num(d, u, k):
+    v = d.get(k)
+    if v in (None, "", "n/a"):
+        return None
+    v = float(v.replace(",", ""))
+    unit = u.get(k, "")
+    scale = {"Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "byte": 1.0, "nsecond": 1e-6, "usecond": 1e-3,
+             "msecond": 1.0, "cycle/nsecond": 1e3, "cycle/usecond": 1.0, "Ghz": 1e3, "Mhz": 1.0}.get(unit, 1.0)
+    return v * scale
+
+
+def full_table(rep, hbm_peak):
+    out = ["| kernel | grid | ms | DRAM rd+wr GB | achieved GB/s | % of HBM peak | dram % (ncu) | SM % | imma % | regs |",
+           "|---|---|---|---|---|---|---|---|---|---|"]
+    for d, u in raw(rep):
+        name = d.get("Kernel Name", "?").split("(")[0].replace("ozr::", "").replace("(anonymous namespace)::", "")
+        ms = num(d, u, "gpu__time_duration.sum")
+        rb = num(d, u, "dram__bytes_read.sum") or 0.0
+        wb = num(d, u, "dram__bytes_write.sum") or 0.0
+        gb = (rb + wb) / 1e9
+        gbs = gb / (ms / 1e3) if ms else 0.0
+        f = lambda k: (f"{num(d, u, k):.1f}" if num(d, u, k) is not None else "-")  # noqa: E731
+        out.append(f"| {name} | {d.get('launch__grid_size', '?')} | {ms:.3f} | {gb:.3f} | {gbs:.0f} | "
+                   f"{100 * gbs / hbm_peak:.1f} | {f('dram__throughput.avg.pct_of_peak_sustained_elapsed')} | "
+                   f"{f('sm__throughput.avg.pct_of_peak_sustained_elapsed')} | "
+                   f"{f('sm__pipe_tensor_op_imma_cycles_active.avg.pct_of_peak_sustained_elapsed')} | "
+                   f"{d.get('launch__registers_per_thread', '?')} |")
+    return "\n".join(out)
+
+
+if __name__ == "__main__":
+    d = sys.argv[1] if len(sys.argv) > 1 else "gpurun_out"
+    peak = float(sys.argv[sys.argv.index("--hbm-peak") + 1]) if "--hbm-peak" in sys.argv else 6533.8
+    t, _ = launch_table(f"{d}/launches.csv")
+    print("## Launch list\n\n" + t + "\n")
+    for rep in ("gemm_full", "hbm_full"):
+        try:
+            print(f"## {rep}\n\n" + full_table(f"{d}/{rep}.ncu-rep", peak) + "\n")
+        except Exception as e:
+            print(f"## {rep}: {e}\n")
