@@ -69,30 +69,29 @@ __device__ __forceinline__ long long digits_q(const int8_t* __restrict__ dig, lo
 constexpr int TB = 16;   // (a,b) tile edge of k_cluster_build
 constexpr int KC = 64;   // rows per staged chunk
 
+// Exact partial Gram sums Σ_{k in split} q_ki q_kj (int128 as two u64) of one 16 x 16 tile of (a,b) over
+// one row split: grid (tile, split); partials[(tile·nsplit + split)·256 + thread] (lo, hi).
 __global__ void __launch_bounds__(TB* TB)
-    k_cluster_build(const int4* __restrict__ tiles, const int* __restrict__ goff, const int* __restrict__ gsq,
-                    const int* __restrict__ mem, const double* __restrict__ mu, const int8_t* __restrict__ xdig,
-                    long long ldd, long long pstride, int kx, int rows, const int32_t* __restrict__ gexp,
-                    const double* __restrict__ r_hi, const double* __restrict__ r_lo, const int32_t* __restrict__ wplanes,
-                    long long wpstride, const __grid_constant__ RecombPlan rpW, const int32_t* __restrict__ ellR,
-                    int scale8, const double* __restrict__ lam, double* __restrict__ Mbuf, double* __restrict__ Rbuf,
-                    int col0, int ncols) {
+    k_cluster_dot(const int4* __restrict__ tiles, const int* __restrict__ goff, const int* __restrict__ mem,
+                  const int8_t* __restrict__ xdig, long long ldd, long long pstride, int kx, int rows, int nsplit,
+                  unsigned long long* __restrict__ part) {
   __shared__ long long qa[KC][TB + 1];
   __shared__ long long qb[KC][TB + 1];
   const int4 t = tiles[blockIdx.x];  // (group, a0, b0, m)
   const int grp = t.x, a0 = t.y, b0 = t.z, m = t.w;
   const int tx = threadIdx.x % TB, ty = threadIdx.x / TB;
-  const int a = a0 + ty, b = b0 + tx;
   const int* J = mem + goff[grp];
+  const int span = ((rows + nsplit - 1) / nsplit + KC - 1) / KC * KC;
+  const int r0 = blockIdx.y * span, r1 = min(rows, r0 + span);
   // exact Σ_k q_ki q_kj in int128 (|q| < 2^52, rows < 2^16)
   unsigned long long lo = 0;
   long long hi = 0;
-  for (int k0 = 0; k0 < rows; k0 += KC) {
+  for (int k0 = r0; k0 < r1; k0 += KC) {
     for (int e = threadIdx.x; e < KC * TB; e += TB * TB) {
       const int kk = e % KC, c = e / KC;  // consecutive threads: consecutive rows of one column
       const int k = k0 + kk;
-      qa[kk][c] = (k < rows && a0 + c < m) ? digits_q(xdig, ldd, pstride, kx, J[a0 + c], k) : 0;
-      qb[kk][c] = (k < rows && b0 + c < m) ? digits_q(xdig, ldd, pstride, kx, J[b0 + c], k) : 0;
+      qa[kk][c] = (k < r1 && a0 + c < m) ? digits_q(xdig, ldd, pstride, kx, J[a0 + c], k) : 0;
+      qb[kk][c] = (k < r1 && b0 + c < m) ? digits_q(xdig, ldd, pstride, kx, J[b0 + c], k) : 0;
     }
     __syncthreads();
 #pragma unroll 8
@@ -105,6 +104,32 @@ __global__ void __launch_bounds__(TB* TB)
       lo = s;
     }
     __syncthreads();
+  }
+  unsigned long long* o = part + ((static_cast<long long>(blockIdx.x) * nsplit + blockIdx.y) * (TB * TB) + threadIdx.x) * 2;
+  o[0] = lo;
+  o[1] = static_cast<unsigned long long>(hi);
+}
+
+__global__ void __launch_bounds__(TB* TB)
+    k_cluster_build(const int4* __restrict__ tiles, const int* __restrict__ goff, const int* __restrict__ gsq,
+                    const int* __restrict__ mem, const double* __restrict__ mu, int nsplit,
+                    const unsigned long long* __restrict__ part, int rows, const int32_t* __restrict__ gexp,
+                    const double* __restrict__ r_hi, const double* __restrict__ r_lo, const int32_t* __restrict__ wplanes,
+                    long long wpstride, const __grid_constant__ RecombPlan rpW, const int32_t* __restrict__ ellR,
+                    int scale8, const double* __restrict__ lam, double* __restrict__ Mbuf, double* __restrict__ Rbuf,
+                    int col0, int ncols) {
+  const int4 t = tiles[blockIdx.x];  // (group, a0, b0, m)
+  const int grp = t.x, a0 = t.y, b0 = t.z, m = t.w;
+  const int tx = threadIdx.x % TB, ty = threadIdx.x / TB;
+  const int a = a0 + ty, b = b0 + tx;
+  const int* J = mem + goff[grp];
+  unsigned long long lo = 0;
+  long long hi = 0;
+  for (int q = 0; q < nsplit; ++q) {  // fixed order (exact anyway)
+    const unsigned long long* p = part + ((static_cast<long long>(blockIdx.x) * nsplit + q) * (TB * TB) + threadIdx.x) * 2;
+    const unsigned long long s = lo + p[0];
+    hi += static_cast<long long>(p[1]) + (s < lo ? 1 : 0);
+    lo = s;
   }
   if (a >= m || b >= m) return;
   const int i = J[a], j = J[b];
@@ -455,11 +480,20 @@ size_t cluster_jacobi_smem(int mmax) {
   return sizeof(double) * (2 * (m + 1) + 2 * m + (m + 1) / 2 + 2) + 64;
 }
 
+int cluster_dot_splits(int ntiles, int rows) {
+  const int want = (4 * 148 + ntiles - 1) / ntiles;          // ~4 CTAs per SM in total
+  const int maxs = std::max(1, (rows + KC - 1) / KC);          // at least one row chunk each
+  return std::max(1, std::min(std::min(want, 64), maxs));
+}
+
 cudaError_t launch_cluster_build(const ClusterLaunch& L, cudaStream_t s) {
-  if (L.ntiles > 0)
-    k_cluster_build<<<L.ntiles, TB * TB, 0, s>>>(L.tiles, L.goff, L.gsq, L.mem, L.mu, L.xdig, L.ldd, L.pstride, L.kx,
-                                                 L.rows, L.gexp, L.r_hi, L.r_lo, L.wplanes, L.wpstride, *L.rpW, L.ellR,
+  if (L.ntiles > 0) {
+    k_cluster_dot<<<dim3(L.ntiles, L.nsplit), TB * TB, 0, s>>>(L.tiles, L.goff, L.mem, L.xdig, L.ldd, L.pstride, L.kx,
+                                                               L.rows, L.nsplit, L.part);
+    k_cluster_build<<<L.ntiles, TB * TB, 0, s>>>(L.tiles, L.goff, L.gsq, L.mem, L.mu, L.nsplit, L.part, L.rows,
+                                                 L.gexp, L.r_hi, L.r_lo, L.wplanes, L.wpstride, *L.rpW, L.ellR,
                                                  L.scale8, L.lam, L.Mbuf, L.Rbuf, L.col0, L.ncols);
+  }
   dim3 gg(L.nmembers, (L.rows + 255) / 256 < 64 ? (L.rows + 255) / 256 : 64);
   k_cluster_gather<<<gg, 256, 0, s>>>(L.mem, L.nmembers, L.Ep, L.lde, L.rows, L.T, L.col0, L.ncols);
   return cudaGetLastError();

@@ -66,10 +66,12 @@ static int run_check(int M, int N, int K, int kA, int kB, int L, int maxpairs) {
   PairTable pt = make_table(kA, kB, L, maxpairs);
   int64_t ldo = M, ps = (int64_t)M * N;
   int32_t *o1, *o2;
+  int* counter = nullptr;
+  CK(cudaMalloc(&counter, sizeof(int)));
   CK(cudaMalloc(&o1, ps * pt.ngroups * 4));
   CK(cudaMalloc(&o2, ps * pt.ngroups * 4));
   CK(cudaMemset(o1, 0x55, ps * pt.ngroups * 4));
-  CK(launch_gemm_i8(A, B, M, N, K, pt, o1, ps, ldo, 0));
+  CK(launch_gemm_i8(A, B, M, N, K, pt, o1, ps, ldo, 0, counter));
   CK(launch_gemm_i8_simt(A, B, M, N, K, pt, o2, ps, ldo, 0));
   CK(cudaDeviceSynchronize());
   std::vector<int32_t> h1(ps * pt.ngroups), h2(ps * pt.ngroups);
@@ -101,13 +103,15 @@ static void run_time(int n, int npairs) {
   pt.ngroups = 1; pt.first[0] = 0; pt.first[1] = npairs; pt.out_plane[0] = 0; pt.diag[0] = 2;
   for (int p = 0; p < npairs; ++p) { pt.s[p] = p; pt.t[p] = 0; }
   int32_t* o;
+  int* counter = nullptr;
+  CK(cudaMalloc(&counter, sizeof(int)));
   CK(cudaMalloc(&o, (int64_t)n * n * 4));
-  for (int w = 0; w < 3; ++w) CK(launch_gemm_i8(A, B, n, n, n, pt, o, (int64_t)n * n, n, 0));
+  for (int w = 0; w < 3; ++w) CK(launch_gemm_i8(A, B, n, n, n, pt, o, (int64_t)n * n, n, 0, counter));
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0); cudaEventCreate(&e1);
   const int reps = 10;
   cudaEventRecord(e0);
-  for (int r = 0; r < reps; ++r) CK(launch_gemm_i8(A, B, n, n, n, pt, o, (int64_t)n * n, n, 0));
+  for (int r = 0; r < reps; ++r) CK(launch_gemm_i8(A, B, n, n, n, pt, o, (int64_t)n * n, n, 0, counter));
   cudaEventRecord(e1);
   CK(cudaEventSynchronize(e1));
   float ms; cudaEventElapsedTime(&ms, e0, e1);

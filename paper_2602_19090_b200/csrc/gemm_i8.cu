@@ -9,7 +9,9 @@
 //   warp 0 lane 0 : TMA producer  (A tile 128 x 128 B, B tile 256 x 128 B per stage, SW128)
 //   warp 1 lane 0 : MMA issuer    (4 x tcgen05.mma M128 N256 K32 per stage)
 //   all 4 warps   : epilogue      (tcgen05.ld 32x32b -> int32 column-major plane, coalesced)
+#include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -31,22 +33,25 @@ constexpr int SMEM_BYTES = STAGES * (A_STAGE_BYTES + B_STAGE_BYTES) + 1024 /*ali
 constexpr int TMEM_COLS = 256;
 constexpr int BAND = 4;  // n-tiles per rasterisation band
 
-__global__ void __launch_bounds__(128, 1)
-    k_gemm_i8(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-              const __grid_constant__ PairTable pt, int32_t* __restrict__ out, long long out_plane_stride,
-              long long ldo, int M, int N, int K, int tiles_m) {
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sA = smem;
-  uint8_t* sB = smem + STAGES * A_STAGE_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * B_STAGE_BYTES);
-  uint64_t* empty = full + STAGES;
-  uint64_t* accf = empty + STAGES;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accf + 1);
+// Persistent form: one CTA per SM; its first job is blockIdx.x, the next ones come from a global atomic
+// counter, so the jobs in flight at any moment stay neighbours in the rasterised order (as with the
+// hardware CTA scheduler). The producer fetches the job ids and passes them to the other roles through a
+// small shared-memory queue. Warp roles:
+//   warp 0 lane 0 : job fetch + TMA producer over every job of the CTA (the smem ring never drains)
+//   warp 1 lane 0 : MMA issuer, accumulating job t into TMEM buffer t % 2 (2 x 256 columns)
+//   warps 2..5    : epilogue of job t − 1 (tcgen05.ld → int32 plane) while job t is being multiplied
+constexpr int NWARPS = 6;
+constexpr int TMEM_ALLOC = 2 * TMEM_COLS;
+constexpr int JQ = 4;  // job queue depth (the epilogue trails the MMA issuer by one job)
 
+struct JobInfo {
+  int g, m0, n0, skip;
+};
+
+__device__ __forceinline__ JobInfo job_info(int job, const PairTable& pt, int M, int N, int tiles_m) {
   const int G = pt.ngroups;
-  const int job = blockIdx.x;
-  const int g = job % G;  // the groups of one tile run back to back (they share its operand rows)
+  JobInfo ji;
+  ji.g = job % G;  // the groups of one tile run back to back (they share its operand rows)
   const int tile = job / G;
   // L2 rasterisation: bands of BAND n-tiles; inside a band, consecutive tiles sweep the band's n-tiles
   // for one m-tile, then the next m-tile — the band's B columns stay L2-resident while A streams once
@@ -55,11 +60,32 @@ __global__ void __launch_bounds__(128, 1)
   const int band = tile / (BAND * tiles_m);
   const int r = tile - band * (BAND * tiles_m);
   const int nb = min(BAND, tiles_n - band * BAND);
-  const int m0 = (r / nb) * BM;
-  const int n0 = (band * BAND + r % nb) * BN;
+  ji.m0 = (r / nb) * BM;
+  ji.n0 = (band * BAND + r % nb) * BN;
+  ji.skip = (pt.tile_budgets && pt.diag[ji.g] > pt.tileL[ji.n0 / BN]) ? 1 : 0;  // beyond the tile's budget
+  return ji;
+}
+
+__global__ void __launch_bounds__(NWARPS * 32, 1)
+    k_gemm_i8(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+              const __grid_constant__ PairTable pt, int32_t* __restrict__ out, long long out_plane_stride,
+              long long ldo, int M, int N, int K, int tiles_m, int njobs, int* __restrict__ job_counter) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * A_STAGE_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * B_STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* acc_full = empty + STAGES;    // [2]
+  uint64_t* acc_empty = acc_full + 2;     // [2]
+  uint64_t* jq_full = acc_empty + 2;   // [JQ]
+  uint64_t* jq_empty = jq_full + JQ;   // [JQ]
+  int* jq = reinterpret_cast<int*>(jq_empty + JQ);  // [JQ] job ids (−1 = done)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(jq + JQ);
+
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  if (pt.tile_budgets && pt.diag[g] > pt.tileL[n0 / BN]) return;  // beyond this column tile's budget
+  const int nkb = (K + BK - 1) / BK;
 
   if (threadIdx.x == 0) {
     tma_prefetch(&tmA);
@@ -68,11 +94,18 @@ __global__ void __launch_bounds__(128, 1)
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(accf, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&acc_full[b], 1);
+      mbar_init(&acc_empty[b], 128);  // the 128 epilogue threads
+    }
+    for (int q = 0; q < JQ; ++q) {
+      mbar_init(&jq_full[q], 1);
+      mbar_init(&jq_empty[q], 1 + 128);  // MMA issuer + epilogue threads
+    }
     fence_mbar_init();
   }
   if (warp == 0) {
-    tmem_alloc(tmem_slot, TMEM_COLS);
+    tmem_alloc(tmem_slot, TMEM_ALLOC);
     tmem_relinquish();
   }
   tc_fence_before();
@@ -80,73 +113,320 @@ __global__ void __launch_bounds__(128, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  const int nkb = (K + BK - 1) / BK;
-  const int p0 = pt.first[g];
-  const int npairs = pt.first[g + 1] - p0;
-  const int total = npairs * nkb;
-
   if (warp == 0) {
     if (lane == 0) {
-    // ---------------- TMA producer
-    for (int it = 0; it < total; ++it) {
-      const int stage = it % STAGES;
-      const uint32_t phase = (it / STAGES) & 1;
-      mbar_wait(&empty[stage], phase ^ 1);
-      const int p = p0 + it / nkb;
-      const int kb = it - (it / nkb) * nkb;
-      mbar_arrive_expect_tx(&full[stage], A_STAGE_BYTES + B_STAGE_BYTES);
-      tma_load_3d(sA + stage * A_STAGE_BYTES, &tmA, &full[stage], kb * BK, m0, pt.s[p]);
-      tma_load_3d(sB + stage * B_STAGE_BYTES, &tmB, &full[stage], kb * BK, n0, pt.t[p]);
-    }
+      // ---------------- job fetch + TMA producer
+      int it = 0;  // ring position, continuous across jobs
+      for (int jn = 0;; ++jn) {
+        const int job = (jn == 0) ? static_cast<int>(blockIdx.x) : static_cast<int>(gridDim.x) + atomicAdd(job_counter, 1);
+        const int slot = jn % JQ;
+        mbar_wait(&jq_empty[slot], ((jn / JQ) & 1) ^ 1);
+        jq[slot] = job < njobs ? job : -1;
+        mbar_arrive(&jq_full[slot]);
+        if (job >= njobs) break;
+        const JobInfo ji = job_info(job, pt, M, N, tiles_m);
+        if (ji.skip) continue;
+        const int p0 = pt.first[ji.g];
+        const int total = (pt.first[ji.g + 1] - p0) * nkb;
+        for (int q = 0; q < total; ++q, ++it) {
+          const int stage = it % STAGES;
+          const uint32_t phase = (it / STAGES) & 1;
+          mbar_wait(&empty[stage], phase ^ 1);
+          const int p = p0 + q / nkb;
+          const int kb = q - (q / nkb) * nkb;
+          mbar_arrive_expect_tx(&full[stage], A_STAGE_BYTES + B_STAGE_BYTES);
+          tma_load_3d(sA + stage * A_STAGE_BYTES, &tmA, &full[stage], kb * BK, ji.m0, pt.s[p]);
+          tma_load_3d(sB + stage * B_STAGE_BYTES, &tmB, &full[stage], kb * BK, ji.n0, pt.t[p]);
+        }
+      }
     }
     __syncwarp();
   } else if (warp == 1) {
     if (lane == 0) {
-    // ---------------- MMA issuer (single thread)
-    constexpr uint32_t idesc = idesc_i8(BM, BN);
-    for (int it = 0; it < total; ++it) {
-      const int stage = it % STAGES;
-      const uint32_t phase = (it / STAGES) & 1;
-      mbar_wait(&full[stage], phase);
-      tc_fence_after();
-      const uint32_t a_addr = smem_u32(sA + stage * A_STAGE_BYTES);
-      const uint32_t b_addr = smem_u32(sB + stage * B_STAGE_BYTES);
+      // ---------------- MMA issuer (single thread)
+      constexpr uint32_t idesc = idesc_i8(BM, BN);
+      int it = 0, t = 0;
+      for (int jn = 0;; ++jn) {
+        const int slot = jn % JQ;
+        mbar_wait(&jq_full[slot], (jn / JQ) & 1);
+        const int job = *reinterpret_cast<volatile int*>(&jq[slot]);
+        mbar_arrive(&jq_empty[slot]);
+        if (job < 0) break;
+        const JobInfo ji = job_info(job, pt, M, N, tiles_m);
+        if (ji.skip) continue;
+        const int buf = t & 1;
+        mbar_wait(&acc_empty[buf], ((t >> 1) & 1) ^ 1);  // the epilogue has drained this accumulator
+        tc_fence_after();
+        const uint32_t acc = tmem_base + static_cast<uint32_t>(buf * TMEM_COLS);
+        const int total = (pt.first[ji.g + 1] - pt.first[ji.g]) * nkb;
+        for (int q = 0; q < total; ++q, ++it) {
+          const int stage = it % STAGES;
+          const uint32_t phase = (it / STAGES) & 1;
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a_addr = smem_u32(sA + stage * A_STAGE_BYTES);
+          const uint32_t b_addr = smem_u32(sB + stage * B_STAGE_BYTES);
 #pragma unroll
-      for (int k = 0; k < BK / UMMA_K; ++k) {
-        const uint64_t ad = umma_desc_kmajor_sw128(a_addr + k * UMMA_K);
-        const uint64_t bd = umma_desc_kmajor_sw128(b_addr + k * UMMA_K);
-        mma_i8(tmem_base, ad, bd, idesc, (it > 0 || k > 0) ? 1u : 0u);
+          for (int k = 0; k < BK / UMMA_K; ++k) {
+            const uint64_t ad = umma_desc_kmajor_sw128(a_addr + k * UMMA_K);
+            const uint64_t bd = umma_desc_kmajor_sw128(b_addr + k * UMMA_K);
+            mma_i8(acc, ad, bd, idesc, (q > 0 || k > 0) ? 1u : 0u);
+          }
+          mma_commit(&empty[stage]);  // frees the smem slot when these MMAs complete
+        }
+        mma_commit(&acc_full[buf]);  // accumulator complete (also when total == 0: the epilogue writes 0)
+        ++t;
       }
-      mma_commit(&empty[stage]);  // frees the smem slot when these MMAs complete
-    }
-    mma_commit(accf);  // accumulator complete
     }
     __syncwarp();
-  }
-
-  // ---------------- epilogue: TMEM -> registers -> int32 plane (column-major, coalesced per column)
-  mbar_wait(accf, 0);
-  tc_fence_after();
-  __syncwarp();
-  int32_t* op = out + static_cast<long long>(pt.out_plane[g]) * out_plane_stride;
-  const int row = m0 + warp * 32 + lane;
-  const bool total_zero = (total == 0);
+  } else {
+    // ---------------- epilogue warps 2..5: TMEM lane quarter (warp % 4) → int32 plane, column-major
+    const int quarter = warp & 3;
+    int t = 0;
+    for (int jn = 0;; ++jn) {
+      const int slot = jn % JQ;
+      mbar_wait(&jq_full[slot], (jn / JQ) & 1);
+      const int job = *reinterpret_cast<volatile int*>(&jq[slot]);
+      mbar_arrive(&jq_empty[slot]);
+      if (job < 0) break;
+      const JobInfo ji = job_info(job, pt, M, N, tiles_m);
+      if (ji.skip) continue;
+      const int buf = t & 1;
+      mbar_wait(&acc_full[buf], (t >> 1) & 1);
+      tc_fence_after();
+      __syncwarp();
+      const bool total_zero = (pt.first[ji.g + 1] == pt.first[ji.g]);
+      int32_t* op = out + static_cast<long long>(pt.out_plane[ji.g]) * out_plane_stride;
+      const int row = ji.m0 + quarter * 32 + lane;
+      const uint32_t acc = tmem_base + static_cast<uint32_t>(buf * TMEM_COLS) + (static_cast<uint32_t>(quarter * 32) << 16);
 #pragma unroll 1
-  for (int c0 = 0; c0 < BN; c0 += 32) {
-    uint32_t r[32];
-    tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(warp * 32) << 16) + c0, r);
-    tmem_ld_wait();
-    if (row < M) {
+      for (int c0 = 0; c0 < BN; c0 += 32) {
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(acc + c0, r);
+        tmem_ld_wait();
+        if (row < M) {
 #pragma unroll
-      for (int c = 0; c < 32; ++c) {
-        const int col = n0 + c0 + c;
-        if (col < N) op[static_cast<long long>(col) * ldo + row] = total_zero ? 0 : static_cast<int32_t>(r[c]);
+          for (int c = 0; c < 32; ++c) {
+            const int col = ji.n0 + c0 + c;
+            if (col < N) op[static_cast<long long>(col) * ldo + row] = total_zero ? 0 : static_cast<int32_t>(r[c]);
+          }
+        }
       }
+      tc_fence_before();
+      mbar_arrive(&acc_empty[buf]);
+      ++t;
     }
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 0) tmem_dealloc(tmem_base, TMEM_COLS);
+  if (warp == 0) tmem_dealloc(tmem_base, TMEM_ALLOC);
+}
+
+// ---------------------------------------------------------------- CTA-pair form (cta_group::2)
+// A cluster of 2 CTAs (one TPC) computes a 256 x 256 tile: each CTA stages ITS 128 rows of A and ITS half
+// (128 of 256 rows) of B per K-block, the leader issues tcgen05.mma.cta_group::2 (M = 256) that reads the
+// operands from both CTAs' shared memory and accumulates rows 0-127 in the leader's TMEM, 128-255 in the
+// peer's. Per SM, the shared-memory fill per K-block drops from 48 KB to 32 KB for the same MMA work
+// (the single-CTA form is bound by L2 → SM operand traffic). Roles per CTA as in the single-CTA form; the
+// leader fetches the jobs and mirrors them into the peer's queue (DSMEM), the MMA warp is the leader's.
+constexpr int STAGES2 = 6;
+constexpr int B_HALF_BYTES = (BN / 2) * BK;
+constexpr int SMEM2_BYTES = STAGES2 * (A_STAGE_BYTES + B_HALF_BYTES) + 1024 /*align*/ + 512 /*barriers*/;
+
+__device__ __forceinline__ JobInfo job_info2(int job, const PairTable& pt, int N, int tiles_m2) {
+  const int G = pt.ngroups;
+  JobInfo ji;
+  ji.g = job % G;
+  const int tile = job / G;
+  const int tiles_n = (N + BN - 1) / BN;
+  const int band = tile / (BAND * tiles_m2);
+  const int r = tile - band * (BAND * tiles_m2);
+  const int nb = min(BAND, tiles_n - band * BAND);
+  ji.m0 = (r / nb) * (2 * BM);  // the pair's 256 rows
+  ji.n0 = (band * BAND + r % nb) * BN;
+  ji.skip = (pt.tile_budgets && pt.diag[ji.g] > pt.tileL[ji.n0 / BN]) ? 1 : 0;
+  return ji;
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NWARPS * 32, 1)
+    k_gemm_i8_2sm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                  const __grid_constant__ PairTable pt, int32_t* __restrict__ out, long long out_plane_stride,
+                  long long ldo, int M, int N, int K, int tiles_m2, int njobs, int* __restrict__ job_counter) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES2 * A_STAGE_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES2 * B_HALF_BYTES);
+  uint64_t* empty = full + STAGES2;
+  uint64_t* acc_full = empty + STAGES2;  // [2]
+  uint64_t* acc_empty = acc_full + 2;    // [2] (leader's)
+  uint64_t* jq_full = acc_empty + 2;     // [JQ]
+  uint64_t* jq_empty = jq_full + JQ;     // [JQ] (leader's)
+  int* jq = reinterpret_cast<int*>(jq_empty + JQ);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(jq + JQ);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = (rank == 0);
+  const int nkb = (K + BK - 1) / BK;
+
+  if (threadIdx.x == 0) {
+    tma_prefetch(&tmA);
+    tma_prefetch(&tmB);
+    for (int s = 0; s < STAGES2; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&acc_full[b], 1);
+      mbar_init(&acc_empty[b], 8);  // 4 epilogue warps x 2 CTAs
+    }
+    for (int q = 0; q < JQ; ++q) {
+      mbar_init(&jq_full[q], 1);
+      mbar_init(&jq_empty[q], 10);  // leader: MMA + 4 epilogue warps; peer: producer + 4 epilogue warps
+    }
+    fence_mbar_init();
+  }
+  if (warp == 0) {
+    tmem_alloc_2sm(tmem_slot, TMEM_ALLOC);
+    tmem_relinquish_2sm();
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();  // the peer's barriers are initialised before any remote arrive / multicast
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- job fetch (leader) + TMA producer (both CTAs)
+      int it = 0;
+      for (int jn = 0;; ++jn) {
+        const int slot = jn % JQ;
+        int job;
+        if (leader) {
+          job = (jn == 0) ? static_cast<int>(blockIdx.x >> 1)
+                          : static_cast<int>(gridDim.x >> 1) + atomicAdd(job_counter, 1);
+          if (job >= njobs) job = -1;
+          mbar_wait_cluster(&jq_empty[slot], ((jn / JQ) & 1) ^ 1);
+          jq[slot] = job;
+          st_cluster_u32(mapa_u32(&jq[slot], 1), static_cast<uint32_t>(job));
+          mbar_arrive(&jq_full[slot]);
+          mbar_arrive_remote(mapa_u32(&jq_full[slot], 1));
+        } else {
+          mbar_wait_cluster(&jq_full[slot], (jn / JQ) & 1);
+          job = *reinterpret_cast<volatile int*>(&jq[slot]);
+          mbar_arrive_remote(mapa_u32(&jq_empty[slot], 0));
+        }
+        if (job < 0) break;
+        const JobInfo ji = job_info2(job, pt, N, tiles_m2);
+        if (ji.skip) continue;
+        const int p0 = pt.first[ji.g];
+        const int total = (pt.first[ji.g + 1] - p0) * nkb;
+        for (int q = 0; q < total; ++q, ++it) {
+          const int stage = it % STAGES2;
+          const uint32_t phase = (it / STAGES2) & 1;
+          mbar_wait(&empty[stage], phase ^ 1);
+          if (leader) mbar_arrive_expect_tx(&full[stage], 2 * (A_STAGE_BYTES + B_HALF_BYTES));
+          const int p = p0 + q / nkb;
+          const int kb = q - (q / nkb) * nkb;
+          const uint32_t fb = mapa_u32(&full[stage], 0);  // the leader's barrier counts both CTAs' bytes
+          tma_load_3d_2sm(sA + stage * A_STAGE_BYTES, &tmA, fb, kb * BK, ji.m0 + static_cast<int>(rank) * BM, pt.s[p]);
+          tma_load_3d_2sm(sB + stage * B_HALF_BYTES, &tmB, fb, kb * BK, ji.n0 + static_cast<int>(rank) * (BN / 2),
+                          pt.t[p]);
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (lane == 0 && leader) {
+      // ---------------- MMA issuer (leader CTA, single thread): M = 256 over the pair
+      constexpr uint32_t idesc = idesc_i8(2 * BM, BN);
+      int it = 0, t = 0;
+      for (int jn = 0;; ++jn) {
+        const int slot = jn % JQ;
+        mbar_wait_cluster(&jq_full[slot], (jn / JQ) & 1);
+        const int job = *reinterpret_cast<volatile int*>(&jq[slot]);
+        mbar_arrive(&jq_empty[slot]);
+        if (job < 0) break;
+        const JobInfo ji = job_info2(job, pt, N, tiles_m2);
+        if (ji.skip) continue;
+        const int buf = t & 1;
+        mbar_wait_cluster(&acc_empty[buf], ((t >> 1) & 1) ^ 1);  // both CTAs' epilogues drained it
+        tc_fence_after();
+        const uint32_t acc = tmem_base + static_cast<uint32_t>(buf * TMEM_COLS);
+        const int total = (pt.first[ji.g + 1] - pt.first[ji.g]) * nkb;
+        for (int q = 0; q < total; ++q, ++it) {
+          const int stage = it % STAGES2;
+          const uint32_t phase = (it / STAGES2) & 1;
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a_addr = smem_u32(sA + stage * A_STAGE_BYTES);
+          const uint32_t b_addr = smem_u32(sB + stage * B_HALF_BYTES);
+#pragma unroll
+          for (int k = 0; k < BK / UMMA_K; ++k) {
+            const uint64_t ad = umma_desc_kmajor_sw128(a_addr + k * UMMA_K);
+            const uint64_t bd = umma_desc_kmajor_sw128(b_addr + k * UMMA_K);
+            mma_i8_2sm(acc, ad, bd, idesc, (q > 0 || k > 0) ? 1u : 0u);
+          }
+          mma_commit_2sm(&empty[stage], 0x3);  // frees the stage in both CTAs
+        }
+        mma_commit_2sm(&acc_full[buf], 0x3);
+        ++t;
+      }
+    }
+    __syncwarp();
+  } else {
+    // ---------------- epilogue warps 2..5 of both CTAs: this CTA's 128 rows of the pair tile
+    const int quarter = warp & 3;
+    int t = 0;
+    for (int jn = 0;; ++jn) {
+      const int slot = jn % JQ;
+      mbar_wait_cluster(&jq_full[slot], (jn / JQ) & 1);
+      const int job = *reinterpret_cast<volatile int*>(&jq[slot]);
+      __syncwarp();
+      if (lane == 0) {
+        if (leader) mbar_arrive(&jq_empty[slot]);
+        else mbar_arrive_remote(mapa_u32(&jq_empty[slot], 0));
+      }
+      if (job < 0) break;
+      const JobInfo ji = job_info2(job, pt, N, tiles_m2);
+      if (ji.skip) continue;
+      const int buf = t & 1;
+      mbar_wait(&acc_full[buf], (t >> 1) & 1);
+      tc_fence_after();
+      __syncwarp();
+      const bool total_zero = (pt.first[ji.g + 1] == pt.first[ji.g]);
+      int32_t* op = out + static_cast<long long>(pt.out_plane[ji.g]) * out_plane_stride;
+      const int row = ji.m0 + static_cast<int>(rank) * BM + quarter * 32 + lane;
+      const uint32_t acc = tmem_base + static_cast<uint32_t>(buf * TMEM_COLS) + (static_cast<uint32_t>(quarter * 32) << 16);
+#pragma unroll 1
+      for (int c0 = 0; c0 < BN; c0 += 32) {
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(acc + c0, r);
+        tmem_ld_wait();
+        if (row < M) {
+#pragma unroll
+          for (int c = 0; c < 32; ++c) {
+            const int col = ji.n0 + c0 + c;
+            if (col < N) op[static_cast<long long>(col) * ldo + row] = total_zero ? 0 : static_cast<int32_t>(r[c]);
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        if (leader) mbar_arrive(&acc_empty[buf]);
+        else mbar_arrive_remote(mapa_u32(&acc_empty[buf], 0));
+      }
+      ++t;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();  // no CTA leaves while its peer may still signal its barriers or read its smem
+  if (warp == 0) tmem_dealloc_2sm(tmem_base, TMEM_ALLOC);
 }
 
 // ---------------------------------------------------------------- SIMT cross-check kernel (dev only)
@@ -202,12 +482,17 @@ bool make_tmap(CUtensorMap* tm, const DigitOperand& op, int K, int cols, int box
 
 cudaError_t launch_gemm_i8(const DigitOperand& A, const DigitOperand& B, int M, int N, int K,
                            const PairTable& pt, int32_t* out, int64_t out_plane_stride, int64_t ldo,
-                           cudaStream_t stream) {
+                           cudaStream_t stream, int* job_counter) {
   if (M <= 0 || N <= 0 || pt.ngroups <= 0) return cudaSuccess;
   if (K <= 0 || (A.ld % 16) || (B.ld % 16) || (A.plane_stride % 16) || (B.plane_stride % 16))
     return cudaErrorInvalidValue;
+  static int use2 = -1;
+  if (use2 < 0) {
+    const char* v = getenv("OZR_GEMM");
+    use2 = (v && v[0] == '1') ? 0 : 1;  // OZR_GEMM=1sm: the single-CTA form (A/B measurements)
+  }
   CUtensorMap tmA, tmB;
-  if (!make_tmap(&tmA, A, K, M, BM) || !make_tmap(&tmB, B, K, N, BN)) return cudaErrorInvalidValue;
+  if (!make_tmap(&tmA, A, K, M, BM) || !make_tmap(&tmB, B, K, N, use2 ? BN / 2 : BN)) return cudaErrorInvalidValue;
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(k_gemm_i8, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
@@ -217,8 +502,37 @@ cudaError_t launch_gemm_i8(const DigitOperand& A, const DigitOperand& B, int M, 
   const int tiles_m = (M + BM - 1) / BM;
   const int tiles_n = (N + BN - 1) / BN;
   const long long jobs = static_cast<long long>(tiles_m) * tiles_n * pt.ngroups;
-  k_gemm_i8<<<static_cast<unsigned>(jobs), 128, SMEM_BYTES, stream>>>(tmA, tmB, pt, out, out_plane_stride, ldo, M,
-                                                                      N, K, tiles_m);
+  static int nsm = 0;
+  if (nsm == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  }
+  if (use2) {
+    static bool attr2 = false;
+    if (!attr2) {
+      cudaError_t e2 = cudaFuncSetAttribute(k_gemm_i8_2sm, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2_BYTES);
+      if (e2 != cudaSuccess) return e2;
+      attr2 = true;
+    }
+    const int tiles_m2 = (M + 2 * BM - 1) / (2 * BM);
+    const long long jobs2 = static_cast<long long>(tiles_m2) * tiles_n * pt.ngroups;
+    const int clusters = static_cast<int>(std::min<long long>(jobs2, nsm / 2));
+    if (!job_counter) return cudaErrorInvalidValue;
+    cudaError_t e = cudaMemsetAsync(job_counter, 0, sizeof(int), stream);
+    if (e != cudaSuccess) return e;
+    k_gemm_i8_2sm<<<2 * clusters, NWARPS * 32, SMEM2_BYTES, stream>>>(tmA, tmB, pt, out, out_plane_stride, ldo, M, N,
+                                                                       K, tiles_m2, static_cast<int>(jobs2),
+                                                                       job_counter);
+    return cudaGetLastError();
+  }
+  const int grid = static_cast<int>(std::min<long long>(jobs, nsm));
+  if (!job_counter) return cudaErrorInvalidValue;
+  int* counter = job_counter;  // the caller's (per context): launches on one stream are ordered, reset before each
+  cudaError_t e = cudaMemsetAsync(counter, 0, sizeof(int), stream);
+  if (e != cudaSuccess) return e;
+  k_gemm_i8<<<grid, NWARPS * 32, SMEM_BYTES, stream>>>(tmA, tmB, pt, out, out_plane_stride, ldo, M, N, K, tiles_m,
+                                                        static_cast<int>(jobs), counter);
   return cudaGetLastError();
 }
 

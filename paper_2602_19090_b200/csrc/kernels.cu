@@ -19,6 +19,7 @@
 
 #include "ddmath.cuh"
 #include "kernels.h"
+#include "ptx.cuh"
 
 namespace ozr {
 
@@ -99,11 +100,33 @@ __device__ __forceinline__ void flush_chunk(dd& acc, bool& first, i128 T, int dl
 }
 
 constexpr int kRegGroups = 24;  // plans up to this many groups keep every plane value in registers
+constexpr int kFastGroups = 12;  // consecutive-diagonal plans up to this many groups: 64-bit limb Horner
 
 __device__ __forceinline__ dd recombine_elem(const int32_t* __restrict__ planes, long long pstride, long long off,
                                              const RecombPlan& rp, int e, int Lj) {
   dd acc{0.0, 0.0};
   bool first = true;
+  if (rp.consecutive) {
+    // one group per diagonal d0, d0+1, ...: T = Σ_g c_g·256^{4·nl−1−g} (zero-padded to whole limbs),
+    // four groups per exact int64 limb (|limb| < 2^55), limbs joined with constant 32-bit shifts — the
+    // same exact integer as the general Horner below, without variable 128-bit shifts
+    const int d0 = rp.diag[0];
+    const int nact = min(rp.ngroups, Lj - d0 + 1);
+    int32_t c[kFastGroups];
+#pragma unroll
+    for (int g = 0; g < kFastGroups; ++g) c[g] = (g < nact) ? __ldg(planes + g * pstride + off) : 0;
+    long long Lm[kFastGroups / 4];
+#pragma unroll
+    for (int k = 0; k < kFastGroups / 4; ++k)
+      Lm[k] = ((static_cast<long long>(c[4 * k]) * 256 + c[4 * k + 1]) * 256 + c[4 * k + 2]) * 256 + c[4 * k + 3];
+    const int nl = (rp.ngroups + 3) >> 2;
+    i128 T = Lm[0];
+#pragma unroll
+    for (int k = 1; k < kFastGroups / 4; ++k)
+      if (k < nl) T = static_cast<i128>(static_cast<u128>(T) << 32) + static_cast<i128>(Lm[k]);
+    flush_chunk(acc, first, T, d0 + 4 * nl - 1, rp.L, e);
+    return acc;
+  }
   if (rp.nchunks == 1 && rp.ngroups <= kRegGroups) {
     // one int128 chunk (the common case): issue every plane load first (memory-level parallelism),
     // then an unrolled Horner
@@ -136,6 +159,121 @@ __device__ __forceinline__ dd recombine_elem(const int32_t* __restrict__ planes,
     flush_chunk(acc, first, T, dprev, rp.L, e);
   }
   return acc;
+}
+
+// Column sweep with two rows in flight per thread (the plane loads of row i + BS are issued before row
+// i is combined): f(i, v) for every row i of the column at `coloff`, e(i) its exponent.
+template <class EF, class F>
+__device__ __forceinline__ void for_column(const int32_t* __restrict__ planes, long long pstride, long long coloff,
+                                           int rows, const RecombPlan& rp, int Lj, EF e, F f) {
+  if (!rp.consecutive) {
+    for (int i = threadIdx.x; i < rows; i += BS) f(i, recombine_elem(planes, pstride, coloff + i, rp, e(i), Lj));
+    return;
+  }
+  const int d0 = rp.diag[0];
+  const int nact = min(rp.ngroups, Lj - d0 + 1);
+  const int nl = (rp.ngroups + 3) >> 2;
+  const int dlast = d0 + 4 * nl - 1;
+  auto fetch = [&](int i, int32_t (&c)[kFastGroups]) {
+#pragma unroll
+    for (int g = 0; g < kFastGroups; ++g) c[g] = (g < nact && i < rows) ? __ldg(planes + g * pstride + coloff + i) : 0;
+  };
+  auto combine = [&](const int32_t (&c)[kFastGroups], int ee) {
+    long long Lm[kFastGroups / 4];
+#pragma unroll
+    for (int k = 0; k < kFastGroups / 4; ++k)
+      Lm[k] = ((static_cast<long long>(c[4 * k]) * 256 + c[4 * k + 1]) * 256 + c[4 * k + 2]) * 256 + c[4 * k + 3];
+    i128 T = Lm[0];
+#pragma unroll
+    for (int k = 1; k < kFastGroups / 4; ++k)
+      if (k < nl) T = static_cast<i128>(static_cast<u128>(T) << 32) + static_cast<i128>(Lm[k]);
+    dd acc{0.0, 0.0};
+    bool first = true;
+    flush_chunk(acc, first, T, dlast, rp.L, ee);
+    return acc;
+  };
+  int32_t ca[kFastGroups], cb[kFastGroups];
+  for (int i0 = threadIdx.x; i0 < rows; i0 += 2 * BS) {
+    const int i1 = i0 + BS;
+    fetch(i0, ca);
+    fetch(i1, cb);
+    f(i0, combine(ca, e(i0)));
+    if (i1 < rows) f(i1, combine(cb, e(i1)));
+  }
+}
+
+// TMA-staged column sweep (HBM-bound recombination kernels): the column's plane segments and up to two
+// fp64 side columns stream through a TS-stage shared-memory ring filled by 1-D bulk copies
+// (cp.async.bulk + mbarrier), one stage = TR rows = one row per thread. f(i, v, xv) gets the recombined
+// element and the side-column values of row i. Requires rp.consecutive and 16-byte aligned segments
+// (rows % 4 == 0, even leading dimensions) — checked by the host (`use_tma`); else the register path.
+constexpr int TR = BS;   // rows per stage
+constexpr int TS = 4;    // stages
+constexpr int kStageBytes = kFastGroups * TR * 4 + 2 * TR * 8;
+constexpr int kTmaSmem = TS * kStageBytes + TS * 8;
+
+template <int NX, class EF, class F>
+__device__ __forceinline__ void for_column_x(const int32_t* __restrict__ planes, long long pstride, long long coloff,
+                                             int rows, const RecombPlan& rp, int Lj, const double* const* xcol,
+                                             int use_tma, unsigned char* tsm, EF e, F f) {
+  if (!use_tma) {
+    for_column(planes, pstride, coloff, rows, rp, Lj, e, [&](int i, const dd& v) {
+      double xv[NX > 0 ? NX : 1];
+#pragma unroll
+      for (int x = 0; x < NX; ++x) xv[x] = xcol[x][i];
+      f(i, v, xv);
+    });
+    return;
+  }
+  uint64_t* bar = reinterpret_cast<uint64_t*>(tsm + TS * kStageBytes);
+  const int tid = threadIdx.x;
+  const int d0 = rp.diag[0];
+  const int nact = max(0, min(rp.ngroups, Lj - d0 + 1));
+  const int nl = (rp.ngroups + 3) >> 2;
+  const int dlast = d0 + 4 * nl - 1;
+  const int nch = (rows + TR - 1) / TR;
+  if (tid == 0) {
+    for (int st = 0; st < TS; ++st) mbar_init(&bar[st], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  auto issue = [&](int c) {
+    const int st = c % TS, r0 = c * TR, nr = min(TR, rows - r0);
+    unsigned char* base = tsm + st * kStageBytes;
+    const uint32_t pb = static_cast<uint32_t>(nr) * 4u, xb = static_cast<uint32_t>(nr) * 8u;
+    mbar_arrive_expect_tx(&bar[st], nact * pb + NX * xb);
+    for (int g = 0; g < nact; ++g) bulk_g2s(base + g * TR * 4, planes + g * pstride + coloff + r0, pb, &bar[st]);
+    for (int x = 0; x < NX; ++x) bulk_g2s(base + kFastGroups * TR * 4 + x * TR * 8, xcol[x] + r0, xb, &bar[st]);
+  };
+  if (tid == 0)
+    for (int c = 0; c < TS - 1 && c < nch; ++c) issue(c);
+  for (int c = 0; c < nch; ++c) {
+    if (tid == 0 && c + TS - 1 < nch) issue(c + TS - 1);  // its stage was released by the last barrier
+    mbar_wait(&bar[c % TS], (c / TS) & 1);
+    const int i = c * TR + tid;
+    if (i < rows) {
+      const unsigned char* base = tsm + (c % TS) * kStageBytes;
+      int32_t cv[kFastGroups];
+#pragma unroll
+      for (int g = 0; g < kFastGroups; ++g) cv[g] = (g < nact) ? reinterpret_cast<const int32_t*>(base + g * TR * 4)[tid] : 0;
+      long long Lm[kFastGroups / 4];
+#pragma unroll
+      for (int k = 0; k < kFastGroups / 4; ++k)
+        Lm[k] = ((static_cast<long long>(cv[4 * k]) * 256 + cv[4 * k + 1]) * 256 + cv[4 * k + 2]) * 256 + cv[4 * k + 3];
+      i128 T = Lm[0];
+#pragma unroll
+      for (int k = 1; k < kFastGroups / 4; ++k)
+        if (k < nl) T = static_cast<i128>(static_cast<u128>(T) << 32) + static_cast<i128>(Lm[k]);
+      dd v{0.0, 0.0};
+      bool first = true;
+      flush_chunk(v, first, T, dlast, rp.L, e(i));
+      double xv[NX > 0 ? NX : 1];
+#pragma unroll
+      for (int x = 0; x < NX; ++x) xv[x] = reinterpret_cast<const double*>(base + kFastGroups * TR * 4 + x * TR * 8)[tid];
+      f(i, v, xv);
+    }
+    __syncthreads();
+  }
 }
 
 // ---------------------------------------------------------------- device union-find (cluster branch)
@@ -313,6 +451,45 @@ __global__ void __launch_bounds__(BS)
   if (threadIdx.x == 0) ell_out[j] = e - S;
 }
 
+// Digits of Res = V − X̂^(1)D̂ (Alg. 1 line 4, inner part), formed exactly as k_recombine_V's pass 2:
+// r = dd_add(V, −TwoProd(x̂_ij, λ̂_j)); p = RNE(r_hi·2^{S−e}) + RNE(r_lo·2^{S−e}) (R6 for a double-double).
+template <typename T>
+__device__ __forceinline__ void split_res_body(const double* __restrict__ vh, const double* __restrict__ vl,
+                                               const double* __restrict__ x1, double l, int rows, int k, int S, int e,
+                                               int8_t* __restrict__ base, long long pstride) {
+  for (int i0 = 4 * threadIdx.x; i0 < rows; i0 += 4 * BS) {
+    T p[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int i = i0 + r;
+      p[r] = T(0);
+      if (i < rows) {
+        double ph, pl;
+        two_prod(x1[i], l, ph, pl);
+        const dd rr = dd_add(dd{vh[i], vl[i]}, dd{-ph, -pl});
+        p[r] = rint_to<T>(ldexp_fast(rr.hi, S - e)) + rint_to<T>(ldexp_fast(rr.lo, S - e));
+      }
+    }
+    store_digits4<T>(p, k, base + i0, pstride);
+  }
+}
+
+__global__ void __launch_bounds__(BS)
+    k_split_res(const double* __restrict__ Vh, const double* __restrict__ Vl, long long ldv,
+                const double* __restrict__ X1, long long ldx1, const double* __restrict__ lam, int rows, int k,
+                const int32_t* __restrict__ eR, int8_t* __restrict__ dig, long long ldd, long long pstride,
+                int32_t* __restrict__ ell_out) {
+  const int j = blockIdx.x;
+  const int e = eR[j];  // ⌈log2 max_i |res_ij|⌉ from k_recombine_V (0 for a zero column)
+  const int S = 8 * (k - 1) + 6;
+  const double* vh = Vh + j * ldv;
+  const double* vl = Vl + j * ldv;
+  const double* x1 = X1 + j * ldx1;
+  if (k <= 7) split_res_body<long long>(vh, vl, x1, lam[j], rows, k, S, e, dig + j * ldd, pstride);
+  else split_res_body<i128>(vh, vl, x1, lam[j], rows, k, S, e, dig + j * ldd, pstride);
+  if (threadIdx.x == 0) ell_out[j] = e - S;
+}
+
 __global__ void k_transpose_i8(const int8_t* __restrict__ src, long long lds, long long sps, int8_t* __restrict__ dst,
                                long long ldt, long long tps, int rows, int cols) {
   // src element (i,j) at src[p*sps + j*lds + i]; dst element (i,j) at dst[p*tps + i*ldt + j]
@@ -357,12 +534,13 @@ __global__ void k_transpose_f64(const double* __restrict__ src, long long lds, d
   }
 }
 
-__global__ void __launch_bounds__(BS)
+__global__ void __launch_bounds__(BS, 3)
     k_recombine_V(const int32_t* __restrict__ planes, long long pstride, int rows, const __grid_constant__ RecombPlan rp,
                   const int32_t* __restrict__ ellA, const int32_t* __restrict__ ellB, int scale8,
                   const double* __restrict__ X1, long long ldx1, const double* __restrict__ s_hi,
                   const double* __restrict__ s_lo, double* __restrict__ Vh, double* __restrict__ Vl, long long ldv,
-                  double* __restrict__ lam_out, int32_t* __restrict__ eR, int* __restrict__ eR_max) {
+                  double* __restrict__ lam_out, int32_t* __restrict__ eR, int* __restrict__ eR_max, int use_tma) {
+  extern __shared__ __align__(128) unsigned char tsm[];
   __shared__ double sh[2 * BS / 32];
   const int j = blockIdx.x;
   const int Lj = rp.tile_budgets ? rp.tileL[j / 256] : rp.L;
@@ -370,23 +548,24 @@ __global__ void __launch_bounds__(BS)
   const double* x1 = X1 + j * ldx1;
   dd t{0.0, 0.0};
   // pass 1: V (Alg. 1 line 1) and x̂_jᵀ v_j (line 3)
-  for (int i = threadIdx.x; i < rows; i += BS) {
-    const dd v = recombine_elem(planes, pstride, static_cast<long long>(j) * rows + i, rp, ellA[i] + eb, Lj);
-    Vh[j * ldv + i] = v.hi;
-    Vl[j * ldv + i] = v.lo;
-    t = dd_add(t, dd_mul_d(v, x1[i]));
-  }
+  const double* xc[1] = {x1};
+  for_column_x<1>(planes, pstride, static_cast<long long>(j) * rows, rows, rp, Lj, xc, use_tma, tsm,
+                  [&](int i) { return ellA[i] + eb; },
+                  [&](int i, const dd& v, const double* xv) {
+                    Vh[j * ldv + i] = v.hi;
+                    Vl[j * ldv + i] = v.lo;
+                    t = dd_add(t, dd_mul_d(v, xv[0]));
+                  });
   t = block_sum_dd(t, sh);
   const dd lam = dd_div(t, dd{s_hi[j], s_lo[j]});  // λ̂_j = x̂_jᵀv̂_j / (1 − r_j)
   const double l = lam.hi;
-  // pass 2: Res = V − X̂ D̂ (line 4, inner part), in double-double; column max of |Res|
+  // pass 2: column max of |Res|, Res = V − X̂ D̂ (line 4, inner part) in double-double — Res itself is
+  // formed again, identically, by the digit split (k_split_res), so it is never written here
   double m = 0.0;
   for (int i = threadIdx.x; i < rows; i += BS) {
     double ph, pl;
     two_prod(x1[i], l, ph, pl);
     const dd r = dd_add(dd{Vh[j * ldv + i], Vl[j * ldv + i]}, dd{-ph, -pl});
-    Vh[j * ldv + i] = r.hi;
-    Vl[j * ldv + i] = r.lo;
     m = fmax(m, fabs(r.hi));
   }
   m = block_max(m, sh);
@@ -398,13 +577,14 @@ __global__ void __launch_bounds__(BS)
   }
 }
 
-__global__ void __launch_bounds__(BS)
+__global__ void __launch_bounds__(BS, 3)
     k_recombine_E(const int32_t* __restrict__ planes, long long pstride, int rows, const __grid_constant__ RecombPlan rp,
                   const int32_t* __restrict__ ellA, const int32_t* __restrict__ ellB, int scale8,
                   const double* __restrict__ r_hi, const double* __restrict__ lam, const int32_t* __restrict__ gX,
                   int col0, double* __restrict__ Ep, long long lde, double* __restrict__ nrm2,
                   int* __restrict__ eE_max, int32_t* __restrict__ eE_col, int* __restrict__ err,
-                  const EdgeOut eo) {
+                  const EdgeOut eo, int use_tma) {
+  extern __shared__ __align__(128) unsigned char tsm[];
   __shared__ double sh[BS / 32];
   const int j = blockIdx.x;        // local column
   const int Lj = rp.tile_budgets ? rp.tileL[j / 256] : rp.L;
@@ -413,12 +593,12 @@ __global__ void __launch_bounds__(BS)
   const double lj = lam[jg];
   double m = 0.0, s2 = 0.0;
   bool bad = false, unresolved = false;
-  for (int i = threadIdx.x; i < rows; i += BS) {
+  for_column_x<0>(planes, pstride, static_cast<long long>(j) * rows, rows, rp, Lj, nullptr, use_tma, tsm,
+                  [&](int i) { return ellA[i] + eb; }, [&](int i, const dd& wv, const double*) {
     double e;
     if (i == jg) {
       e = r_hi[j] * 0.5;  // ẽ_jj = r_j / 2
     } else {
-      const dd wv = recombine_elem(planes, pstride, static_cast<long long>(j) * rows + i, rp, ellA[i] + eb, Lj);
       const double dl = __dsub_rn(lj, lam[i]);  // λ̃_j − λ̃_i
       if (eo.mode == 0) {
         if (dl == 0.0) bad = true;
@@ -437,7 +617,7 @@ __global__ void __launch_bounds__(BS)
     const double ep = ldexp_fast(e, gX[i]);  // Ẽ' = diag(2^g) Ẽ (exact)
     Ep[j * lde + i] = ep;
     m = fmax(m, fabs(ep));
-  }
+  });
   if (bad) atomicOr(err, ERR_DEGENERATE);
   if (__syncthreads_or(unresolved) && threadIdx.x == 0) atomicOr(eo.any, 1);
   m = block_max(m, sh);
@@ -449,27 +629,29 @@ __global__ void __launch_bounds__(BS)
   }
 }
 
-__global__ void __launch_bounds__(BS)
+__global__ void __launch_bounds__(BS, 3)
     k_final(const int32_t* __restrict__ planes, long long pstride, int rows, const __grid_constant__ RecombPlan rp,
             const int32_t* __restrict__ ellB, int scale8, const double* __restrict__ X1, long long ldx1,
-            double* __restrict__ X, long long ldx, double* __restrict__ nu2, double* __restrict__ wnext) {
+            double* __restrict__ X, long long ldx, double* __restrict__ nu2, double* __restrict__ wnext, int use_tma) {
+  extern __shared__ __align__(128) unsigned char tsm[];
   __shared__ double sh[BS / 32];
   const int j = blockIdx.x;
   const int Lj = rp.tile_budgets ? rp.tileL[j / 256] : rp.L;
   const int eb = ellB[j] + scale8;  // the Q operand (digits of X̂^(1)/2^g) has ℓ = 0 on every row
   double s2 = 0.0, m = 0.0;
-  for (int i = threadIdx.x; i < rows; i += BS) {
-    const dd u = recombine_elem(planes, pstride, static_cast<long long>(j) * rows + i, rp, eb, Lj);
-    const double x1 = X1[j * ldx1 + i];
+  const double* xc[2] = {X1 + j * ldx1, X + j * ldx};
+  for_column_x<2>(planes, pstride, static_cast<long long>(j) * rows, rows, rp, Lj, xc, use_tma, tsm,
+                  [&](int) { return eb; }, [&](int i, const dd& u, const double* xv) {
+    const double x1 = xv[0];
     double s, e;
     two_sum(x1, u.hi, s, e);
     const double xn = __dadd_rn(s, __dadd_rn(e, u.lo));  // accsum: RN(x^(1) + U)
-    const double xo = X[j * ldx + i];
+    const double xo = xv[1];
     const double d = __dsub_rn(xn, xo);
     s2 = __fma_rn(d, d, s2);
     m = fmax(m, fabs(xn));
     X[j * ldx + i] = xn;
-  }
+  });
   s2 = block_sum(s2, sh);
   m = block_max(m, sh);
   if (threadIdx.x == 0) {
@@ -478,23 +660,46 @@ __global__ void __launch_bounds__(BS)
   }
 }
 
-__global__ void __launch_bounds__(BS)
+__global__ void __launch_bounds__(BS, 3)
     k_recombine_dd(const int32_t* __restrict__ planes, long long pstride, int rows, const __grid_constant__ RecombPlan rp,
                    const int32_t* __restrict__ ellA, const int32_t* __restrict__ ellB, int scale8,
                    double* __restrict__ Ch, double* __restrict__ Cl, long long ldc) {
   const int j = blockIdx.x;
   const int Lj = rp.tile_budgets ? rp.tileL[j / 256] : rp.L;
   const int eb = ellB[j] + scale8;
-  for (int i = threadIdx.x; i < rows; i += BS) {
-    const dd v = recombine_elem(planes, pstride, static_cast<long long>(j) * rows + i, rp, ellA[i] + eb, Lj);
-    Ch[j * ldc + i] = v.hi;
-    if (Cl) Cl[j * ldc + i] = v.lo;
-  }
+  for_column(planes, pstride, static_cast<long long>(j) * rows, rows, rp, Lj, [&](int i) { return ellA[i] + eb; },
+             [&](int i, const dd& v) {
+               Ch[j * ldc + i] = v.hi;
+               if (Cl) Cl[j * ldc + i] = v.lo;
+             });
 }
 
 }  // namespace
 
 // ---------------------------------------------------------------- launchers
+namespace {
+int tma_ok(const RecombPlan& rp, const int32_t* planes, long long pstride, int rows, const double* x0, long long ld0,
+           const double* x1, long long ld1) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_recombine_V, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem);
+    cudaFuncSetAttribute(k_recombine_E, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem);
+    cudaFuncSetAttribute(k_final, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem);
+    attr = true;
+  }
+  auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  if (!rp.consecutive || rows % 4 || pstride % 4 || !al(planes)) return 0;
+  if (x0 && (ld0 % 2 || !al(x0))) return 0;
+  if (x1 && (ld1 % 2 || !al(x1))) return 0;
+  return 1;
+}
+}  // namespace
+
+void launch_split_res(const double* Vh, const double* Vl, long long ldv, const double* X1, long long ldx1,
+                      const double* lam, int rows, int cols, int k, const int32_t* eR, int8_t* dig, long long ldd,
+                      long long pstride, int32_t* ell, cudaStream_t s) {
+  k_split_res<<<cols, BS, 0, s>>>(Vh, Vl, ldv, X1, ldx1, lam, rows, k, eR, dig, ldd, pstride, ell);
+}
 void launch_colmax(const double* X, long long ldx, int rows, int cols, double* w, int* err, cudaStream_t s) {
   k_colmax<<<cols, BS, 0, s>>>(X, ldx, rows, w, err);
 }
@@ -522,20 +727,24 @@ void launch_recombine_V(const int32_t* planes, long long pstride, int rows, int 
                         const int32_t* ellA, const int32_t* ellB, int scale8, const double* X1, long long ldx1,
                         const double* s_hi, const double* s_lo, double* Vh, double* Vl, long long ldv,
                         double* lam_out, int32_t* eR, int* eR_max, cudaStream_t s) {
-  k_recombine_V<<<cols, BS, 0, s>>>(planes, pstride, rows, rp, ellA, ellB, scale8, X1, ldx1, s_hi, s_lo, Vh, Vl, ldv,
-                                    lam_out, eR, eR_max);
+  const int tma = tma_ok(rp, planes, pstride, rows, X1, ldx1, X1, ldx1);
+  k_recombine_V<<<cols, BS, tma ? kTmaSmem : 0, s>>>(planes, pstride, rows, rp, ellA, ellB, scale8, X1, ldx1, s_hi, s_lo,
+                                                     Vh, Vl, ldv, lam_out, eR, eR_max, tma);
 }
 void launch_recombine_E(const int32_t* planes, long long pstride, int rows, int cols, const RecombPlan& rp,
                         const int32_t* ellA, const int32_t* ellB, int scale8, const double* r_hi, const double* lam,
                         const int32_t* gX, int col0, double* Ep, long long lde, double* nrm2, int* eE_max,
                         int32_t* eE_col, int* err, const EdgeOut& eo, cudaStream_t s) {
-  k_recombine_E<<<cols, BS, 0, s>>>(planes, pstride, rows, rp, ellA, ellB, scale8, r_hi, lam, gX, col0, Ep, lde, nrm2,
-                                    eE_max, eE_col, err, eo);
+  const int tma = tma_ok(rp, planes, pstride, rows, nullptr, 0, nullptr, 0);
+  k_recombine_E<<<cols, BS, tma ? kTmaSmem : 0, s>>>(planes, pstride, rows, rp, ellA, ellB, scale8, r_hi, lam, gX, col0,
+                                                     Ep, lde, nrm2, eE_max, eE_col, err, eo, tma);
 }
 void launch_final(const int32_t* planes, long long pstride, int rows, int cols, const RecombPlan& rp,
                   const int32_t* ellB, int scale8, const double* X1, long long ldx1, double* X, long long ldx,
                   double* nu2, double* wnext, cudaStream_t s) {
-  k_final<<<cols, BS, 0, s>>>(planes, pstride, rows, rp, ellB, scale8, X1, ldx1, X, ldx, nu2, wnext);
+  const int tma = tma_ok(rp, planes, pstride, rows, X1, ldx1, X, ldx);
+  k_final<<<cols, BS, tma ? kTmaSmem : 0, s>>>(planes, pstride, rows, rp, ellB, scale8, X1, ldx1, X, ldx, nu2, wnext,
+                                               tma);
 }
 void launch_iota(int* p, int n, cudaStream_t s) { k_iota<<<(n + 255) / 256, 256, 0, s>>>(p, n); }
 void launch_uf_flatten(int* parent, int n, cudaStream_t s) { k_uf_flatten<<<(n + 255) / 256, 256, 0, s>>>(parent, n); }

@@ -15,6 +15,7 @@ constexpr int kPlanGroups = 96;
 struct RecombPlan {
   int ngroups;
   int L;
+  int consecutive;  // 1: group g is the whole diagonal diag[0] + g, ngroups <= 12 — the 64-bit limb path
   int nchunks;
   int chunk_first[kMaxChunks + 1];
   int diag[kPlanGroups];
@@ -29,6 +30,11 @@ void launch_x1_split(const double* X, long long ldx, int rows, int cols, int bet
                      double* s_lo, double* r_hi, double* r_lo, int* err, cudaStream_t s);
 void launch_split_fixed(const double* M, const double* Mlo, long long ldm, int rows, int cols, int k, int8_t* dig,
                         long long ldd, long long pstride, int32_t* ell, int* err, cudaStream_t s);
+// Digits of Res = V − X̂^(1)D̂ formed on the fly from V (dd), X̂^(1) and λ̂ (local column j uses lam[j]),
+// exponent per column from eR (k_recombine_V); same digits as k_split_fixed on the stored Res.
+void launch_split_res(const double* Vh, const double* Vl, long long ldv, const double* X1, long long ldx1,
+                      const double* lam, int rows, int cols, int k, const int32_t* eR, int8_t* dig, long long ldd,
+                      long long pstride, int32_t* ell, cudaStream_t s);
 void launch_transpose_i8(const int8_t* src, long long lds, long long sps, int8_t* dst, long long ldt, long long tps,
                          int rows, int cols, int planes, cudaStream_t s);
 void launch_transpose_f64(const double* src, long long lds, double* dst, long long ldt, int rows, int cols,
@@ -79,11 +85,14 @@ struct ClusterLaunch {
   double* nrm2;     // n entries, global column index
   int32_t* eE_col;  // ncols entries, local column index
   int* eE_max;
+  int nsplit;                 // row splits of the exact Gram partial sums (cluster_dot_splits)
+  unsigned long long* part;   // ntiles·nsplit·256·2 u64
   const int* hgm;          // host copy of gm (which groups take the cooperative whole-GPU Jacobi)
   double* coop_scratch;    // >= 5·mmax + 8 doubles
   int* coop_flags;         // >= 128 ints
 };
 size_t cluster_jacobi_smem(int mmax);
+int cluster_dot_splits(int ntiles, int rows);
 // build: R_JJ (all), M_JJ and T = Ẽ'[:, J] on this rank's columns (zero elsewhere; all-reduced between);
 // solve: Jacobi of every group (replicated on every rank); apply: Ẽ'[:, J] and column statistics of the
 // owned columns.

@@ -102,7 +102,7 @@ namespace {
 enum Slot {
   S_ADIG, S_AELL, S_W, S_X1, S_XDIG, S_XDIGT, S_G, S_SH, S_SL, S_RH, S_RL, S_PLANES, S_VH, S_VL, S_LAM, S_ER,
   S_ERR, S_EMAX, S_RDIG, S_RELL, S_EP, S_NRM2, S_NU2, S_WNEXT, S_ZEROELL, S_TMP1, S_TMP2, S_BELL, S_AT, S_ONES,
-  S_EDGES, S_ECOUNT, S_CINT, S_CDBL, S_CM, S_CR, S_CK, S_CV, S_CZ, S_CT, S_CSCR, S_CFLAG, S_SCAL, S_UFALL
+  S_EDGES, S_ECOUNT, S_CINT, S_CDBL, S_CM, S_CR, S_CK, S_CV, S_CZ, S_CT, S_CSCR, S_CFLAG, S_SCAL, S_UFALL, S_CPART, S_GCNT
 };
 
 ozr_status fail(ozr_ctx c, ozr_status st, const char* fmt, ...) {
@@ -210,6 +210,10 @@ bool make_tables(const std::vector<Group>& gs, int L, int64_t K, PairTable& pt, 
   }
   rp.chunk_first[nc] = static_cast<int>(gs.size());
   rp.nchunks = nc;
+  // fast path: one int128 with the zero-padded limbs: 31 + 8·(4·⌈G/4⌉ − 1) + 2 ≤ 121 bits for G ≤ 12
+  rp.consecutive = (gs.size() <= 12 && nc == 1) ? 1 : 0;
+  for (size_t q = 0; q < gs.size(); ++q)
+    if (gs[q].d != gs[0].d + static_cast<int>(q)) rp.consecutive = 0;
   return true;
 }
 
@@ -380,7 +384,9 @@ double sum_pow2_2c(const std::vector<double>& w) {
 ozr_status run_gemm(ozr_ctx ctx, const DigitOperand& A, const DigitOperand& B, int M, int N, int K,
                     const PairTable& pt, int32_t* planes, int idx) {
   cudaEventRecord(ctx->ev[2 + 2 * idx], ctx->stream);
-  OZR_CK(launch_gemm_i8(A, B, M, N, K, pt, planes, static_cast<int64_t>(M) * N, M, ctx->stream), "slice GEMM");
+  int* cnt = ctx->ws<int>(S_GCNT, 4);
+  OZR_ALLOC(cnt);
+  OZR_CK(launch_gemm_i8(A, B, M, N, K, pt, planes, static_cast<int64_t>(M) * N, M, ctx->stream, cnt), "slice GEMM");
   cudaEventRecord(ctx->ev[3 + 2 * idx], ctx->stream);
   return OZR_OK;
 }
@@ -650,7 +656,7 @@ ozr_status sweep(ozr_ctx ctx, Exchange* ex, const double* A, int64_t n, int64_t 
   int8_t* rdig = ctx->ws<int8_t>(S_RDIG, static_cast<size_t>(kMaxDigits) * ld * nl);
   int32_t* rell = ctx->ws<int32_t>(S_RELL, nl);
   OZR_ALLOC(rdig); OZR_ALLOC(rell);
-  launch_split_fixed(Vh, Vl, n, N, NL, kR, rdig, ld, ld * nl, rell, derr, s);
+  launch_split_res(Vh, Vl, n, X1, n, lam + col0, N, NL, kR, eR, rdig, ld, ld * nl, rell, s);
   OZR_CK(cudaGetLastError(), "split Res");
   ctx->mark("host+splitRes");
 
@@ -832,6 +838,9 @@ ozr_status sweep(ozr_ctx ctx, Exchange* ex, const double* A, int64_t n, int64_t 
       L.nrm2 = nrm2;
       L.eE_col = eR;
       L.eE_max = demax;
+      L.nsplit = cluster_dot_splits(L.ntiles, N);
+      L.part = ctx->ws<unsigned long long>(S_CPART, static_cast<size_t>(L.ntiles) * L.nsplit * 512);
+      OZR_ALLOC(L.part);
       L.hgm = gm.data();
       L.coop_scratch = ctx->ws<double>(S_CSCR, 5 * static_cast<size_t>(mmax) + 8);
       L.coop_flags = ctx->ws<int>(S_CFLAG, 128);
@@ -844,7 +853,7 @@ ozr_status sweep(ozr_ctx ctx, Exchange* ex, const double* A, int64_t n, int64_t 
       OZR_X(xsum(cT, static_cast<size_t>(nmem) * n));
       OZR_CK(launch_cluster_apply(L, s), "cluster apply");
       ctx->mark("cluster");
-      cluster_launches += 5;
+      cluster_launches += 6;
       OZR_CK(cudaMemcpyAsync(hlam_new.data(), lam, n * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H");
       OZR_X(scalars({demax}, &eEmax));
       rep.n_clusters = ng;
@@ -1146,7 +1155,9 @@ ozr_status ozr_gemm(ozr_ctx ctx, int64_t m, int64_t n, int64_t k, const double* 
     return fail(ctx, OZR_ERR_ARG, "ozr_gemm: plane_stride < m*n");
   }
   DigitOperand oa{da, ldk, ldk * m, kA}, ob{db, ldk, ldk * n, kB};
-  OZR_CK(launch_gemm_i8(oa, ob, static_cast<int>(m), static_cast<int>(n), static_cast<int>(k), pt, planes, ps, m, s),
+  int* cnt = ctx->ws<int>(S_GCNT, 4);
+  OZR_ALLOC(cnt);
+  OZR_CK(launch_gemm_i8(oa, ob, static_cast<int>(m), static_cast<int>(n), static_cast<int>(k), pt, planes, ps, m, s, cnt),
          "slice GEMM");
   launch_recombine_dd(planes, ps, static_cast<int>(m), static_cast<int>(n), rp, ea, eb, 8 * (kA + kB - L), C_hi, C_lo,
                       ldc, s);

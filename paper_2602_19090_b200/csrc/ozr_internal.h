@@ -38,9 +38,10 @@ struct DigitOperand {
 // Launch the tcgen05 INT8 slice-product kernel: for each group g, out_planes[out_plane[g]] (M x N int32,
 // column-major, leading dim ldo) = Σ_{pairs} A_s^T-tile products over K.
 //   A: M "columns" of K bytes each (A operand, K-major), B: N columns of K bytes (B operand, K-major).
+// job_counter: a device int owned by the caller (one per stream/context), reset by the launcher.
 cudaError_t launch_gemm_i8(const DigitOperand& A, const DigitOperand& B, int M, int N, int K,
                            const PairTable& pt, int32_t* out, int64_t out_plane_stride, int64_t ldo,
-                           cudaStream_t stream);
+                           cudaStream_t stream, int* job_counter);
 
 // Reference (SIMT) version of the same contract; used only by the dev harness to cross-check the
 // tensor-core kernel on the GPU. Not on the product path.
