@@ -212,7 +212,7 @@ constexpr int TS = 4;    // stages
 constexpr int kStageBytes = kFastGroups * TR * 4 + 2 * TR * 8;
 constexpr int kTmaSmem = TS * kStageBytes + TS * 8;
 
-template <int NX, class EF, class F>
+template <int NX, bool HI_ONLY = false, class EF, class F>
 __device__ __forceinline__ void for_column_x(const int32_t* __restrict__ planes, long long pstride, long long coloff,
                                              int rows, const RecombPlan& rp, int Lj, const double* const* xcol,
                                              int use_tma, unsigned char* tsm, EF e, F f) {
@@ -265,8 +265,12 @@ __device__ __forceinline__ void for_column_x(const int32_t* __restrict__ planes,
       for (int k = 1; k < kFastGroups / 4; ++k)
         if (k < nl) T = static_cast<i128>(static_cast<u128>(T) << 32) + static_cast<i128>(Lm[k]);
       dd v{0.0, 0.0};
-      bool first = true;
-      flush_chunk(v, first, T, dlast, rp.L, e(i));
+      if (HI_ONLY) {  // the caller uses RN(value) only (its hi part is the same correctly rounded double)
+        v.hi = ldexp_fast(i128_to_f64(T), 8 * (rp.L - dlast) + e(i));
+      } else {
+        bool first = true;
+        flush_chunk(v, first, T, dlast, rp.L, e(i));
+      }
       double xv[NX > 0 ? NX : 1];
 #pragma unroll
       for (int x = 0; x < NX; ++x) xv[x] = reinterpret_cast<const double*>(base + kFastGroups * TR * 4 + x * TR * 8)[tid];
@@ -593,8 +597,8 @@ __global__ void __launch_bounds__(BS, 3)
   const double lj = lam[jg];
   double m = 0.0, s2 = 0.0;
   bool bad = false, unresolved = false;
-  for_column_x<0>(planes, pstride, static_cast<long long>(j) * rows, rows, rp, Lj, nullptr, use_tma, tsm,
-                  [&](int i) { return ellA[i] + eb; }, [&](int i, const dd& wv, const double*) {
+  for_column_x<0, true>(planes, pstride, static_cast<long long>(j) * rows, rows, rp, Lj, nullptr, use_tma, tsm,
+                        [&](int i) { return ellA[i] + eb; }, [&](int i, const dd& wv, const double*) {
     double e;
     if (i == jg) {
       e = r_hi[j] * 0.5;  // ẽ_jj = r_j / 2

@@ -641,8 +641,10 @@ ozr_status sweep(ozr_ctx ctx, Exchange* ex, const double* A, int64_t n, int64_t 
   OZR_X(xgather(lam, nl * sizeof(double)));
   int eRmax = 0;
   std::vector<double> hlam_new(n);
+  std::vector<int> eR_col(nl);
   OZR_CK(cudaMemcpyAsync(hlam_new.data(), lam, n * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H");
-  OZR_X(scalars({demax}, &eRmax));
+  OZR_CK(cudaMemcpyAsync(eR_col.data(), eR, nl * sizeof(int32_t), cudaMemcpyDeviceToHost, s), "D2H eR");
+  OZR_X(scalars({demax}, &eRmax));  // one synchronisation for λ̂, the Res exponents and their maximum
   const double gap_new0 = gap_min_sorted(hlam_new);
   if (!(gap_new0 > 0.0) && P.cluster_mode == 0)
     return fail(ctx, OZR_ERR_DEGENERATE, "equal Rayleigh quotients (gap = 0) with the cluster branch off");
@@ -661,9 +663,6 @@ ozr_status sweep(ozr_ctx ctx, Exchange* ex, const double* A, int64_t n, int64_t 
   ctx->mark("host+splitRes");
 
   // ---- a7: P3  W_{:,J} = X̂^(1)ᵀ Res_J  (Alg. 1 line 4)
-  std::vector<int> eR_col(nl);
-  OZR_CK(cudaMemcpyAsync(eR_col.data(), eR, nl * sizeof(int32_t), cudaMemcpyDeviceToHost, s), "D2H eR");
-  OZR_CK(cudaStreamSynchronize(s), "sync");
   std::vector<double> gaps_new = col_gaps(hlam_new);
   for (double& x : gaps_new)
     if (!(x > 0.0)) x = gap_new;
@@ -710,6 +709,8 @@ ozr_status sweep(ozr_ctx ctx, Exchange* ex, const double* A, int64_t n, int64_t 
   OZR_CK(cudaGetLastError(), "recombine E");
   ctx->mark("recombE");
   int eEmax = 0, nedges = 0;
+  std::vector<int> eE_col(nl);
+  OZR_CK(cudaMemcpyAsync(eE_col.data(), eR, nl * sizeof(int32_t), cudaMemcpyDeviceToHost, s), "D2H eE");
   {
     int o2[2];
     OZR_X(scalars({demax, ecount}, o2));
@@ -855,18 +856,16 @@ ozr_status sweep(ozr_ctx ctx, Exchange* ex, const double* A, int64_t n, int64_t 
       ctx->mark("cluster");
       cluster_launches += 6;
       OZR_CK(cudaMemcpyAsync(hlam_new.data(), lam, n * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H");
+      OZR_CK(cudaMemcpyAsync(eE_col.data(), eR, nl * sizeof(int32_t), cudaMemcpyDeviceToHost, s), "D2H eE");
       OZR_X(scalars({demax}, &eEmax));
       rep.n_clusters = ng;
       rep.max_cluster = mmax;
     }
   }
   if (eEmax == intmin) eEmax = -1074;
+  // g_j = ⌈log2 w_j⌉ + β − 53 (k_x1_split; ⌈log2 0⌉ := 0), so its minimum is known on the host
   int gmin = 100000;
-  {
-    std::vector<int32_t> hg(n);
-    OZR_CK(cudaMemcpy(hg.data(), g, n * sizeof(int32_t), cudaMemcpyDeviceToHost), "D2H g");
-    for (int x : hg) gmin = std::min(gmin, x);
-  }
+  for (double x : hw) gmin = std::min(gmin, (x != 0.0 ? ceil_log2_host(x) : 0) + beta - 53);
 
   // ---- a9: P4  U_J = X̂^(1) Ẽ_{:,J} = Q Ẽ'_{:,J} ; X̂_J ← RN(X̂^(1)_J + U_J)  (Alg. 1 line 6)
   const double tauU = P.theta_U * delta_p;
@@ -876,9 +875,6 @@ ozr_status sweep(ozr_ctx ctx, Exchange* ex, const double* A, int64_t n, int64_t 
   ctx->mark("host+splitE");
   const int SX = 8 * (kx - 1) + 6;
   // R8b for X̂Ẽ: uniform accuracy θ_U·δ', but columns with small corrections need fewer pairs
-  std::vector<int> eE_col(nl);
-  OZR_CK(cudaMemcpyAsync(eE_col.data(), eR, nl * sizeof(int32_t), cudaMemcpyDeviceToHost, s), "D2H eE");
-  OZR_CK(cudaStreamSynchronize(s), "sync");
   for (int64_t j = 0; j < nl; ++j) tau_col[j] = tauU / 2.0;
   unsigned char tileLU[kMaxNTiles];
   double avg_pairs_U = 0.0;
