@@ -430,6 +430,53 @@ __device__ __forceinline__ void split_fixed_body(const double* __restrict__ col,
   }
 }
 
+// k > 7 digits of a plain fp64 column (the A split, 15 digits): p = RNE(m·2^{S−e}) is an integer-valued
+// double y = M·2^{8q + r} with |M| < 2^53, so p = (M·2^r)·256^q: its q lowest digits are 0 and the others
+// are the balanced base-256 digits of M·2^r (|·| < 2^61) — all in 64-bit arithmetic. The balanced
+// digit recurrence d = ((x + 128) mod 256) − 128, x ← (x − d)/256 from the bottom yields exactly the
+// excess-128 digits of R5 (byte_t(p + Σ128·256^t) − 128, top digit = the remaining quotient).
+__device__ __forceinline__ void split_wide_body(const double* __restrict__ col, int rows, int k, int S, int e,
+                                               int8_t* __restrict__ base, long long pstride) {
+  for (int i0 = 4 * threadIdx.x; i0 < rows; i0 += 4 * BS) {
+    long long x[4];
+    int q[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int i = i0 + r;
+      const double y = (i < rows) ? rint(ldexp_fast(col[i], S - e)) : 0.0;
+      if (fabs(y) < 9007199254740992.0) {  // < 2^53: exact as int64
+        x[r] = static_cast<long long>(y);
+        q[r] = 0;
+      } else {
+        const long long bits = __double_as_longlong(y);
+        const int ex = static_cast<int>((bits >> 52) & 0x7FF) - 1075;  // y = ±mant·2^ex, ex ≥ 1
+        long long mant = (bits & 0xFFFFFFFFFFFFFLL) | 0x10000000000000LL;
+        if (bits < 0) mant = -mant;
+        q[r] = ex >> 3;
+        x[r] = mant << (ex & 7);
+      }
+    }
+    // digits from the least significant plane (index k−1) upwards; plane s holds weight 256^{k−1−s}
+    for (int t = 0; t < k; ++t) {  // t = position from the bottom
+      uint32_t packed = 0;
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        int d;
+        if (t < q[r]) {
+          d = 0;
+        } else if (t == k - 1) {
+          d = static_cast<int>(x[r]);  // the top digit takes the rest
+        } else {
+          d = static_cast<int>(((x[r] + 128) & 255)) - 128;
+          x[r] = (x[r] - d) >> 8;
+        }
+        packed |= (static_cast<uint32_t>(d) & 0xFFu) << (8 * r);
+      }
+      *reinterpret_cast<uint32_t*>(base + i0 + (k - 1 - t) * pstride) = packed;
+    }
+  }
+}
+
 __global__ void __launch_bounds__(BS)
     k_split_fixed(const double* __restrict__ M, const double* __restrict__ Mlo, long long ldm, int rows, int k,
                   int8_t* __restrict__ dig, long long ldd, long long pstride, int32_t* __restrict__ ell_out,
@@ -451,6 +498,7 @@ __global__ void __launch_bounds__(BS)
   const int S = 8 * (k - 1) + 6;
   // |p| <= 2^S (+1 for a double-double): 64-bit arithmetic while S <= 54 (k <= 7)
   if (k <= 7) split_fixed_body<long long>(col, cl, rows, k, S, e, dig + j * ldd, pstride);
+  else if (!cl) split_wide_body(col, rows, k, S, e, dig + j * ldd, pstride);
   else split_fixed_body<i128>(col, cl, rows, k, S, e, dig + j * ldd, pstride);
   if (threadIdx.x == 0) ell_out[j] = e - S;
 }
