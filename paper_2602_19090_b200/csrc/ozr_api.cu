@@ -233,20 +233,39 @@ int choose_L(int kA, int kB, int64_t K, int eA, int eB, double tau) {
   return kA + kB;
 }
 
-// Local gaps gap_j = min_{i≠j} |λ̂_i − λ̂_j| from the sorted λ̂ (fl-differences of neighbours).
-std::vector<double> col_gaps(const std::vector<double>& lam) {
+// Everything the planner needs from one λ̂ vector, from ONE ordering (ascending λ̂, ties by index; no sort
+// at all when λ̂ is already ascending, the usual case): gap0 = min neighbour fl-difference,
+// gap_pos = the smallest positive one (R16), colgap_j = min_{i≠j} |λ̂_i − λ̂_j| (R8b), max|λ̂|.
+struct LamStats {
+  double gap0 = INFINITY, gap_pos = 0.0, maxabs = 0.0;
+  std::vector<double> colgap;
+};
+
+LamStats lam_stats(const std::vector<double>& lam) {
   const size_t n = lam.size();
-  std::vector<size_t> idx(n);
-  for (size_t i = 0; i < n; ++i) idx[i] = i;
-  std::stable_sort(idx.begin(), idx.end(), [&](size_t a, size_t b) { return lam[a] < lam[b]; });
-  std::vector<double> g(n, INFINITY);
+  LamStats st;
+  std::vector<int> idx(n);
+  for (size_t i = 0; i < n; ++i) idx[i] = static_cast<int>(i);
+  bool sorted = true;
+  for (size_t i = 1; i < n && sorted; ++i) sorted = !(lam[i] < lam[i - 1]);
+  if (!sorted)
+    std::sort(idx.begin(), idx.end(), [&](int a, int b) { return lam[a] < lam[b] || (lam[a] == lam[b] && a < b); });
+  st.colgap.assign(n, INFINITY);
+  double gp = INFINITY;
   for (size_t p = 0; p < n; ++p) {
-    double a = p > 0 ? lam[idx[p]] - lam[idx[p - 1]] : INFINITY;
-    double b = p + 1 < n ? lam[idx[p + 1]] - lam[idx[p]] : INFINITY;
-    g[idx[p]] = std::min(a, b);
+    st.maxabs = std::max(st.maxabs, std::fabs(lam[p]));
+    if (p > 0) {
+      const double d = lam[idx[p]] - lam[idx[p - 1]];
+      st.gap0 = std::min(st.gap0, d);
+      if (d > 0.0) gp = std::min(gp, d);
+      st.colgap[idx[p]] = std::min(st.colgap[idx[p]], d);
+      st.colgap[idx[p - 1]] = std::min(st.colgap[idx[p - 1]], d);
+    }
   }
-  return g;
+  st.gap_pos = std::isfinite(gp) ? gp : std::max(st.maxabs * kU, 1e-300);
+  return st;
 }
+
 
 int pairs_upto(int kA, int kB, int L) {
   int np = 0;
@@ -328,38 +347,31 @@ int alpha_dense(int64_t n, int beta) {
   return 53 - beta + c;
 }
 
-double gap_min_sorted(std::vector<double> l) {
-  std::sort(l.begin(), l.end());
-  double g = INFINITY;
-  for (size_t i = 1; i < l.size(); ++i) g = std::min(g, l[i] - l[i - 1]);
-  return g;
-}
 
-// Smallest POSITIVE neighbour gap (digit budgets need a finite accuracy target when the cluster branch
-// tolerates equal λ̂); falls back to u·max|λ̂| when every gap is zero.
-double gap_pos_sorted(std::vector<double> l) {
-  std::sort(l.begin(), l.end());
-  double g = INFINITY, mx = 0.0;
-  for (size_t i = 0; i < l.size(); ++i) mx = std::max(mx, std::fabs(l[i]));
-  for (size_t i = 1; i < l.size(); ++i)
-    if (l[i] - l[i - 1] > 0.0) g = std::min(g, l[i] - l[i - 1]);
-  return std::isfinite(g) ? g : std::max(mx * kU, 1e-300);
-}
 
 // ---------------------------------------------------------------- cluster branch (R13): host grouping
 // Connected components of the unresolved-pair graph; members sorted by (λ̂, index), groups by first member.
 // root[i]: the (flattened) device union-find label of column i.
 void unresolved_groups(int64_t n, const std::vector<int>& root, const std::vector<double>& lam,
                        std::vector<int>& members, std::vector<int>& offsets) {
-  std::vector<std::vector<int>> comp(n);
-  for (int64_t i = 0; i < n; ++i) comp[root[i]].push_back(static_cast<int>(i));
-  std::vector<std::vector<int>> groups;
-  for (int64_t r = 0; r < n; ++r)
-    if (comp[r].size() >= 2) {
-      std::vector<int> g = comp[r];
-      std::sort(g.begin(), g.end(), [&](int a, int b) { return lam[a] < lam[b] || (lam[a] == lam[b] && a < b); });
-      groups.push_back(g);
+  std::vector<int> cnt(n, 0);
+  for (int64_t i = 0; i < n; ++i) ++cnt[root[i]];
+  std::vector<int> slot(n, -1);
+  std::vector<std::vector<int>> comp;
+  for (int64_t i = 0; i < n; ++i)
+    if (cnt[root[i]] >= 2) {
+      if (slot[root[i]] < 0) {
+        slot[root[i]] = static_cast<int>(comp.size());
+        comp.emplace_back();
+      }
+      comp[slot[root[i]]].push_back(static_cast<int>(i));
     }
+  std::vector<std::vector<int>> groups;
+  for (auto& cg : comp) {
+    std::vector<int> g = cg;
+    std::sort(g.begin(), g.end(), [&](int a, int b) { return lam[a] < lam[b] || (lam[a] == lam[b] && a < b); });
+    groups.push_back(g);
+  }
   std::sort(groups.begin(), groups.end(), [](const std::vector<int>& a, const std::vector<int>& b) { return a[0] < b[0]; });
   members.clear();
   offsets.assign(1, 0);
@@ -369,13 +381,14 @@ void unresolved_groups(int64_t n, const std::vector<int>& root, const std::vecto
   }
 }
 
+// Σ_j 2^{2⌈log2 w_j⌉} added in ascending exponent order (R3), via a histogram of the exponents.
 double sum_pow2_2c(const std::vector<double>& w) {
-  std::vector<int> cs;
+  std::vector<int> cnt(2200, 0);
   for (double x : w)
-    if (x != 0.0) cs.push_back(ceil_log2_host(x));
-  std::sort(cs.begin(), cs.end());
+    if (x != 0.0) ++cnt[ceil_log2_host(x) + 1100];
   double s = 0.0;
-  for (int c : cs) s = s + std::ldexp(1.0, 2 * c);
+  for (int c = 0; c < 2200; ++c)
+    for (int q = 0; q < cnt[c]; ++q) s = s + std::ldexp(1.0, 2 * (c - 1100));
   return s;
 }
 
@@ -420,31 +433,32 @@ struct SweepState {
   bool have_w = false;  // wnext valid (column maxima of the current X)
 };
 
-ozr_status split_A(ozr_ctx ctx, const double* A, int64_t n, int64_t lda, int kA, SweepState& st) {
+// A → digit planes (a1), stream-ordered; the exponents land in `hell` (host) at the caller's next
+// synchronisation, after which split_A_finish derives e_A,max. Error flags go to derr.
+ozr_status split_A_launch(ozr_ctx ctx, const double* A, int64_t n, int64_t lda, int kA, int* derr,
+                          std::vector<int32_t>& hell) {
   const int64_t ld = round16(n);
   int8_t* adig = ctx->ws<int8_t>(S_ADIG, static_cast<size_t>(kA) * ld * n);
   int32_t* aell = ctx->ws<int32_t>(S_AELL, n);
-  int* derr = ctx->ws<int>(S_ERR, 4);
   OZR_ALLOC(adig);
   OZR_ALLOC(aell);
-  OZR_ALLOC(derr);
-  OZR_CK(cudaMemsetAsync(derr, 0, sizeof(int), ctx->stream), "memset");
   // A symmetric: its columns are its rows, so the COLWISE split of A is the row-wise split of the
   // A operand of V = A·X̂ (K-major) and ℓ_i is its per-row exponent.
   launch_split_fixed(A, nullptr, lda, static_cast<int>(n), static_cast<int>(n), kA, adig, ld, ld * n, aell, derr,
                      ctx->stream);
   OZR_CK(cudaGetLastError(), "split A");
-  ozr_status s = read_err(ctx, derr);
-  if (s != OZR_OK) return s;
-  std::vector<int32_t> h(n);
-  OZR_CK(cudaMemcpy(h.data(), aell, n * sizeof(int32_t), cudaMemcpyDeviceToHost), "D2H ell");
+  hell.resize(n);
+  OZR_CK(cudaMemcpyAsync(hell.data(), aell, n * sizeof(int32_t), cudaMemcpyDeviceToHost, ctx->stream), "D2H ell");
+  return OZR_OK;
+}
+
+void split_A_finish(const double* A, int64_t n, int kA, const std::vector<int32_t>& hell, SweepState& st) {
   int em = -100000;
-  for (int64_t i = 0; i < n; ++i) em = std::max(em, h[i] + 8 * (kA - 1) + 6);
+  for (int64_t i = 0; i < n; ++i) em = std::max(em, hell[i] + 8 * (kA - 1) + 6);
   st.A = A;
   st.nA = n;
   st.kA_split = kA;
   st.eA_max = em;
-  return OZR_OK;
 }
 
 // Block-column partition: rank r of P owns columns [col0, col0 + nl), nl = n/P, col0 = r·nl.
@@ -529,6 +543,10 @@ ozr_status sweep(ozr_ctx ctx, Exchange* ex, const double* A, int64_t n, int64_t 
     OZR_CK(cudaMemcpyAsync(w + col0, wnext + col0, nl * sizeof(double), cudaMemcpyDeviceToDevice, s), "copy w");
   }
   OZR_X(xgather(w, nl * sizeof(double)));
+  // a1 (once per call): the A split runs before the a0 synchronisation, which also brings its exponents
+  const bool new_A = (st.A != A || st.nA != n);
+  std::vector<int32_t> hell;
+  if (new_A) OZR_X(split_A_launch(ctx, A, n, lda, P.kA_split, derr, hell));
   std::vector<double> hw(n), hlam(n);
   OZR_CK(cudaMemcpyAsync(hw.data(), w, n * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H w");
   OZR_CK(cudaMemcpyAsync(hlam.data(), lambda, n * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H lambda");
@@ -536,10 +554,10 @@ ozr_status sweep(ozr_ctx ctx, Exchange* ex, const double* A, int64_t n, int64_t 
   for (double x : hlam)
     if (!std::isfinite(x)) return fail(ctx, OZR_ERR_NONFINITE, "non-finite lambda");
   const double delta_p = P.delta / (P.theta > 0 ? P.theta : 1.0);
-  const double gap0 = gap_min_sorted(hlam);
-  const double gap = (P.cluster_mode && !(gap0 > 0.0)) ? gap_pos_sorted(hlam) : gap0;
-  double maxlam = 0.0;
-  for (double x : hlam) maxlam = std::max(maxlam, std::fabs(x));
+  LamStats ls_prev = lam_stats(hlam);
+  const double gap0 = ls_prev.gap0;
+  const double gap = (P.cluster_mode && !(gap0 > 0.0)) ? ls_prev.gap_pos : gap0;
+  const double maxlam = ls_prev.maxabs;
   if (!(gap0 > 0.0) && P.cluster_mode == 0)
     return fail(ctx, OZR_ERR_DEGENERATE, "equal eigenvalue estimates (gap = 0) with the cluster branch off");
   const double ssum = sum_pow2_2c(hw);
@@ -560,10 +578,10 @@ ozr_status sweep(ozr_ctx ctx, Exchange* ex, const double* A, int64_t n, int64_t 
   rep.max_abs_lambda = maxlam;
 
   // ---- A split (once per refine_to_tol call; A and its digits are replicated on every rank)
-  if (st.A != A || st.nA != n) OZR_X(split_A(ctx, A, n, lda, P.kA_split, st));
+  if (new_A) split_A_finish(A, n, P.kA_split, hell, st);
   ctx->mark("stats+splitA");
   // per-column accuracy of V (R8, R8b): θ_V·δ'·gap_j with the previous λ̂ (this rank's columns)
-  std::vector<double> gaps_prev = col_gaps(hlam);
+  std::vector<double>& gaps_prev = ls_prev.colgap;
   for (double& x : gaps_prev)
     if (!(x > 0.0)) x = gap;  // equal λ̂ (cluster branch): the smallest positive gap sets the budget
   std::vector<double> tau_col(nl);
@@ -645,10 +663,11 @@ ozr_status sweep(ozr_ctx ctx, Exchange* ex, const double* A, int64_t n, int64_t 
   OZR_CK(cudaMemcpyAsync(hlam_new.data(), lam, n * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H");
   OZR_CK(cudaMemcpyAsync(eR_col.data(), eR, nl * sizeof(int32_t), cudaMemcpyDeviceToHost, s), "D2H eR");
   OZR_X(scalars({demax}, &eRmax));  // one synchronisation for λ̂, the Res exponents and their maximum
-  const double gap_new0 = gap_min_sorted(hlam_new);
+  LamStats ls_new = lam_stats(hlam_new);
+  const double gap_new0 = ls_new.gap0;
   if (!(gap_new0 > 0.0) && P.cluster_mode == 0)
     return fail(ctx, OZR_ERR_DEGENERATE, "equal Rayleigh quotients (gap = 0) with the cluster branch off");
-  const double gap_new = (gap_new0 > 0.0) ? gap_new0 : gap_pos_sorted(hlam_new);
+  const double gap_new = (gap_new0 > 0.0) ? gap_new0 : ls_new.gap_pos;
   if (eRmax == intmin) eRmax = -1074;
 
   // ---- a6: Res digits (k_R from the accuracy W needs, R8)
@@ -663,7 +682,7 @@ ozr_status sweep(ozr_ctx ctx, Exchange* ex, const double* A, int64_t n, int64_t 
   ctx->mark("host+splitRes");
 
   // ---- a7: P3  W_{:,J} = X̂^(1)ᵀ Res_J  (Alg. 1 line 4)
-  std::vector<double> gaps_new = col_gaps(hlam_new);
+  std::vector<double>& gaps_new = ls_new.colgap;
   for (double& x : gaps_new)
     if (!(x > 0.0)) x = gap_new;
   for (int64_t j = 0; j < nl; ++j) {
@@ -927,9 +946,9 @@ ozr_status sweep(ozr_ctx ctx, Exchange* ex, const double* A, int64_t n, int64_t 
   st.have_w = true;
   rep.net_update = std::sqrt(nu);
   rep.normE_fro = std::sqrt(ne);
-  double maxlam_new = 0.0;
-  for (double x : hlam_new) maxlam_new = std::max(maxlam_new, std::fabs(x));
-  const double gap_out = gap_pos_sorted(hlam_new);
+  if (rep.n_clusters > 0) ls_new = lam_stats(hlam_new);  // the sub-solve changed λ̂_J
+  const double maxlam_new = ls_new.maxabs;
+  const double gap_out = ls_new.gap_pos;
   rep.predicted_error = rep.net_update * rep.net_update * maxlam_new / (static_cast<double>(n) * gap_out);
   if (ex) {  // report the global pair budgets (each rank planned its own column tiles)
     int hv[3] = {rep.L_V, rep.L_W, rep.L_U}, gv[3];
