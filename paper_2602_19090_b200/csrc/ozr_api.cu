@@ -43,6 +43,8 @@ struct ozr_ctx_s {
   std::vector<DevBuf> bufs;
   std::vector<int> last_members, last_offsets{0};  // unresolved groups of the last sweep (R13)
   cudaEvent_t ev[8];
+  cudaStream_t xstream = nullptr;  // side stream of the digit all-gather (overlaps the V product)
+  cudaEvent_t xev[2];
   bool events = false;
   // tracing (OZR_TRACE=1): named events between the kernels of a sweep, printed to stderr per sweep
   bool trace = false;
@@ -494,12 +496,13 @@ ozr_status sweep(ozr_ctx ctx, Exchange* ex, const double* A, int64_t n, int64_t 
   OZR_CK(cudaMemsetAsync(derr, 0, sizeof(int), s), "memset");
 
   // exchange helpers (no-ops on one GPU)
-  auto xgather = [&](void* base, size_t bytes) -> ozr_status {
+  auto xgather_on = [&](void* base, size_t bytes, cudaStream_t st_) -> ozr_status {
     if (!ex) return OZR_OK;
     ++nexch;
-    if (!ex->allgather(base, bytes, s)) return fail(ctx, OZR_ERR_COMM, "all-gather: %s", ex->err.c_str());
+    if (!ex->allgather(base, bytes, st_)) return fail(ctx, OZR_ERR_COMM, "all-gather: %s", ex->err.c_str());
     return OZR_OK;
   };
+  auto xgather = [&](void* base, size_t bytes) -> ozr_status { return xgather_on(base, bytes, s); };
   auto xsum = [&](double* buf, size_t count) -> ozr_status {
     if (!ex) return OZR_OK;
     ++nexch;
@@ -613,17 +616,22 @@ ozr_status sweep(ozr_ctx ctx, Exchange* ex, const double* A, int64_t n, int64_t 
   launch_x1_split(X, ldx, N, NL, beta, kx, w + col0, X1, n, xdig + col0 * ld, ld, ld * n, g + col0, sh, sl, rh + col0,
                   rl + col0, derr, s);
   OZR_CK(cudaGetLastError(), "x1 split");
+  // a11: the digit planes, g and r of all columns — all-gathered on the side stream while the V product
+  // (which needs only this rank's columns) runs; the main stream joins it before the transpose, i.e.
+  // before any other collective is issued and before anything reads other ranks' columns
   if (ex) {
+    cudaStream_t xs = ctx->xstream;
+    OZR_CK(cudaEventRecord(ctx->xev[0], s), "event");
+    OZR_CK(cudaStreamWaitEvent(xs, ctx->xev[0], 0), "wait");
     if (!ex->group_begin()) return fail(ctx, OZR_ERR_COMM, "%s", ex->err.c_str());
-    for (int p = 0; p < kx; ++p) OZR_X(xgather(xdig + p * ld * n, static_cast<size_t>(nl * ld)));
-    OZR_X(xgather(g, nl * sizeof(int32_t)));
-    OZR_X(xgather(rh, nl * sizeof(double)));
-    OZR_X(xgather(rl, nl * sizeof(double)));
-    if (!ex->group_end(s)) return fail(ctx, OZR_ERR_COMM, "%s", ex->err.c_str());
+    for (int p = 0; p < kx; ++p) OZR_X(xgather_on(xdig + p * ld * n, static_cast<size_t>(nl * ld), xs));
+    OZR_X(xgather_on(g, nl * sizeof(int32_t), xs));
+    OZR_X(xgather_on(rh, nl * sizeof(double), xs));
+    OZR_X(xgather_on(rl, nl * sizeof(double), xs));
+    if (!ex->group_end(xs)) return fail(ctx, OZR_ERR_COMM, "%s", ex->err.c_str());
+    OZR_CK(cudaEventRecord(ctx->xev[1], xs), "event");
   }
-  launch_transpose_i8(xdig, ld, ld * n, xdigT, ld, ld * n, N, N, kx, s);
-  ctx->mark("x1split+exchange+transpose");
-  OZR_CK(cudaGetLastError(), "transpose digits");
+  ctx->mark("x1split");
 
   // ---- a3: P1  V = A·X̂^(1)_J  (Alg. 1 line 1, eq. mat_mul)
   std::vector<Group> gV = plan_groups(kA, kx, LV, n);
@@ -640,6 +648,9 @@ ozr_status sweep(ozr_ctx ctx, Exchange* ex, const double* A, int64_t n, int64_t 
   DigitOperand opX{xdig, ld, ld * n, kx};               // all columns (A operand of W)
   OZR_X(run_gemm(ctx, opA, opXJ, N, NL, N, pt, planes, 0));
   ctx->mark("gemmV");
+  if (ex) OZR_CK(cudaStreamWaitEvent(s, ctx->xev[1], 0), "wait exchange");
+  launch_transpose_i8(xdig, ld, ld * n, xdigT, ld, ld * n, N, N, kx, s);  // A operand of X̂Ẽ
+  OZR_CK(cudaGetLastError(), "transpose digits");
   const double pV = tilesV ? avg_pairs_V : static_cast<double>(count_pairs(gV));
   rep.pairs_V = static_cast<int>(std::lround(pV));
   ops += 2.0 * n * n * nl * pV;
@@ -998,6 +1009,8 @@ ozr_status ozr_create(ozr_ctx* out, int device, void* stream, int64_t n_max) {
   c->device = device;
   c->stream = static_cast<cudaStream_t>(stream);
   for (int i = 0; i < 8; ++i) cudaEventCreate(&c->ev[i]);
+  cudaStreamCreateWithFlags(&c->xstream, cudaStreamNonBlocking);
+  for (int i = 0; i < 2; ++i) cudaEventCreateWithFlags(&c->xev[i], cudaEventDisableTiming);
   c->events = true;
   const char* tr = getenv("OZR_TRACE");
   c->trace = tr && tr[0] == '1';
@@ -1013,6 +1026,8 @@ void ozr_destroy(ozr_ctx ctx) {
     if (b.p) cudaFree(b.p);
   if (ctx->events)
     for (int i = 0; i < 8; ++i) cudaEventDestroy(ctx->ev[i]);
+  for (int i = 0; i < 2; ++i) cudaEventDestroy(ctx->xev[i]);
+  if (ctx->xstream) cudaStreamDestroy(ctx->xstream);
   delete ctx;
 }
 
