@@ -169,6 +169,9 @@ def main():
     ap.add_argument("--ref-cols", type=int, default=8)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--truncate", type=int, default=1,
+                    help="1: the paper's X̂ → X̂^(1) truncation (default); 0: keep all of X̂ — the untruncated "
+                         "two-sided analogue of the prior work the paper compares against (PAPER.md:432-443)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -208,7 +211,7 @@ def main():
     n = cfg["n"]
     delta = cfg["delta"]
     ctx = ozr.Context(local)
-    params = ozr.default_params(delta=delta)
+    params = ozr.default_params(delta=delta, truncate=args.truncate)
     X = X0.clone()
     X = ozr.colmajor(X)
     lam = lam0.clone()
@@ -282,7 +285,8 @@ def main():
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
     t0.record()
-    st, hist = ozr.ozr_refine_to_tol_dist(ctx, comm, A, X, lam, ozr.default_params(delta=delta, max_sweeps=6))
+    st, hist = ozr.ozr_refine_to_tol_dist(ctx, comm, A, X, lam,
+                                          ozr.default_params(delta=delta, max_sweeps=6, truncate=args.truncate))
     t1.record()
     torch.cuda.synchronize()
     ttt = {"ms": t0.elapsed_time(t1), "sweeps": len(hist), "status": int(st), "delta": delta,
@@ -335,6 +339,8 @@ def main():
                "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
                "vs_baseline": None, "dtype": "int8", "data": "synthetic",
                "config": {"workload": f"{name}: " + _describe(cfg, n), "n": n, "delta": delta,
+                          "mode": "proposed (X̂ truncated to X̂^(1))" if args.truncate else
+                                  "untruncated X̂ (prior-work analogue)",
                           "parallelism": f"block-column partition x{ws} (NCCL all-gather of X^(1) digits per sweep)"
                           if ws > 1 else "1 GPU",
                           "l2": "inputs larger than L2 (A + X = %.1f GiB per rank, L2 126 MB)" % (2 * n * n * 8 / 2 ** 30),
