@@ -209,20 +209,24 @@ __device__ __forceinline__ void for_column(const int32_t* __restrict__ planes, l
 // (rows % 4 == 0, even leading dimensions) — checked by the host (`use_tma`); else the register path.
 constexpr int TR = BS;   // rows per stage
 constexpr int TS = 4;    // stages
-constexpr int kStageBytes = kFastGroups * TR * 4 + 2 * TR * 8;
+constexpr int kStageBytes = kFastGroups * TR * 4 + 2 * TR * 8 + TR * 4;  // planes | 2 fp64 sides | 1 int32 side
+constexpr int kSideI = kFastGroups * TR * 4 + 2 * TR * 8;
 constexpr int kTmaSmem = TS * kStageBytes + TS * 8;
 
-template <int NX, bool HI_ONLY = false, class EF, class F>
+// icol (nullable): an int32 per-row vector staged beside the planes (the row exponents); e(i, icol[i]).
+template <int NX, bool HI_ONLY = false, int NG = kFastGroups, class EF, class F>
 __device__ __forceinline__ void for_column_x(const int32_t* __restrict__ planes, long long pstride, long long coloff,
                                              int rows, const RecombPlan& rp, int Lj, const double* const* xcol,
-                                             int use_tma, unsigned char* tsm, EF e, F f) {
+                                             const int32_t* __restrict__ icol, int use_tma, unsigned char* tsm, EF e,
+                                             F f) {
   if (!use_tma) {
-    for_column(planes, pstride, coloff, rows, rp, Lj, e, [&](int i, const dd& v) {
-      double xv[NX > 0 ? NX : 1];
+    for_column(planes, pstride, coloff, rows, rp, Lj, [&](int i) { return e(i, icol ? icol[i] : 0); },
+               [&](int i, const dd& v) {
+                 double xv[NX > 0 ? NX : 1];
 #pragma unroll
-      for (int x = 0; x < NX; ++x) xv[x] = xcol[x][i];
-      f(i, v, xv);
-    });
+                 for (int x = 0; x < NX; ++x) xv[x] = xcol[x][i];
+                 f(i, v, xv);
+               });
     return;
   }
   uint64_t* bar = reinterpret_cast<uint64_t*>(tsm + TS * kStageBytes);
@@ -241,9 +245,10 @@ __device__ __forceinline__ void for_column_x(const int32_t* __restrict__ planes,
     const int st = c % TS, r0 = c * TR, nr = min(TR, rows - r0);
     unsigned char* base = tsm + st * kStageBytes;
     const uint32_t pb = static_cast<uint32_t>(nr) * 4u, xb = static_cast<uint32_t>(nr) * 8u;
-    mbar_arrive_expect_tx(&bar[st], nact * pb + NX * xb);
+    mbar_arrive_expect_tx(&bar[st], nact * pb + NX * xb + (icol ? pb : 0u));
     for (int g = 0; g < nact; ++g) bulk_g2s(base + g * TR * 4, planes + g * pstride + coloff + r0, pb, &bar[st]);
     for (int x = 0; x < NX; ++x) bulk_g2s(base + kFastGroups * TR * 4 + x * TR * 8, xcol[x] + r0, xb, &bar[st]);
+    if (icol) bulk_g2s(base + kSideI, icol + r0, pb, &bar[st]);
   };
   if (tid == 0)
     for (int c = 0; c < TS - 1 && c < nch; ++c) issue(c);
@@ -253,23 +258,25 @@ __device__ __forceinline__ void for_column_x(const int32_t* __restrict__ planes,
     const int i = c * TR + tid;
     if (i < rows) {
       const unsigned char* base = tsm + (c % TS) * kStageBytes;
-      int32_t cv[kFastGroups];
+      // NG: groups compiled for this launch (4, 8 or 12 ≥ ngroups), so small plans do no dead work
+      int32_t cv[NG];
 #pragma unroll
-      for (int g = 0; g < kFastGroups; ++g) cv[g] = (g < nact) ? reinterpret_cast<const int32_t*>(base + g * TR * 4)[tid] : 0;
-      long long Lm[kFastGroups / 4];
+      for (int g = 0; g < NG; ++g) cv[g] = (g < nact) ? reinterpret_cast<const int32_t*>(base + g * TR * 4)[tid] : 0;
+      long long Lm[NG / 4];
 #pragma unroll
-      for (int k = 0; k < kFastGroups / 4; ++k)
+      for (int k = 0; k < NG / 4; ++k)
         Lm[k] = ((static_cast<long long>(cv[4 * k]) * 256 + cv[4 * k + 1]) * 256 + cv[4 * k + 2]) * 256 + cv[4 * k + 3];
       i128 T = Lm[0];
 #pragma unroll
-      for (int k = 1; k < kFastGroups / 4; ++k)
+      for (int k = 1; k < NG / 4; ++k)
         if (k < nl) T = static_cast<i128>(static_cast<u128>(T) << 32) + static_cast<i128>(Lm[k]);
       dd v{0.0, 0.0};
+      const int ee = e(i, icol ? reinterpret_cast<const int32_t*>(base + kSideI)[tid] : 0);
       if (HI_ONLY) {  // the caller uses RN(value) only (its hi part is the same correctly rounded double)
-        v.hi = ldexp_fast(i128_to_f64(T), 8 * (rp.L - dlast) + e(i));
+        v.hi = ldexp_fast(i128_to_f64(T), 8 * (rp.L - dlast) + ee);
       } else {
         bool first = true;
-        flush_chunk(v, first, T, dlast, rp.L, e(i));
+        flush_chunk(v, first, T, dlast, rp.L, ee);
       }
       double xv[NX > 0 ? NX : 1];
 #pragma unroll
@@ -586,6 +593,7 @@ __global__ void k_transpose_f64(const double* __restrict__ src, long long lds, d
   }
 }
 
+template <int NG>
 __global__ void __launch_bounds__(BS, 3)
     k_recombine_V(const int32_t* __restrict__ planes, long long pstride, int rows, const __grid_constant__ RecombPlan rp,
                   const int32_t* __restrict__ ellA, const int32_t* __restrict__ ellB, int scale8,
@@ -601,8 +609,8 @@ __global__ void __launch_bounds__(BS, 3)
   dd t{0.0, 0.0};
   // pass 1: V (Alg. 1 line 1) and x̂_jᵀ v_j (line 3)
   const double* xc[1] = {x1};
-  for_column_x<1>(planes, pstride, static_cast<long long>(j) * rows, rows, rp, Lj, xc, use_tma, tsm,
-                  [&](int i) { return ellA[i] + eb; },
+  for_column_x<1, false, NG>(planes, pstride, static_cast<long long>(j) * rows, rows, rp, Lj, xc, ellA, use_tma, tsm,
+                  [&](int, int ea) { return ea + eb; },
                   [&](int i, const dd& v, const double* xv) {
                     Vh[j * ldv + i] = v.hi;
                     Vl[j * ldv + i] = v.lo;
@@ -629,6 +637,7 @@ __global__ void __launch_bounds__(BS, 3)
   }
 }
 
+template <int NG>
 __global__ void __launch_bounds__(BS, 3)
     k_recombine_E(const int32_t* __restrict__ planes, long long pstride, int rows, const __grid_constant__ RecombPlan rp,
                   const int32_t* __restrict__ ellA, const int32_t* __restrict__ ellB, int scale8,
@@ -645,13 +654,16 @@ __global__ void __launch_bounds__(BS, 3)
   const double lj = lam[jg];
   double m = 0.0, s2 = 0.0;
   bool bad = false, unresolved = false;
-  for_column_x<0, true>(planes, pstride, static_cast<long long>(j) * rows, rows, rp, Lj, nullptr, use_tma, tsm,
-                        [&](int i) { return ellA[i] + eb; }, [&](int i, const dd& wv, const double*) {
+  // the row vectors λ̂_i and ℓ_i of the row operand (X̂^(1)ᵀ: g_i) ride in the shared-memory stages
+  // with the planes
+  const double* xc[1] = {lam};
+  for_column_x<1, true, NG>(planes, pstride, static_cast<long long>(j) * rows, rows, rp, Lj, xc, ellA, use_tma, tsm,
+                            [&](int, int gi) { return gi + eb; }, [&](int i, const dd& wv, const double* xv) {
     double e;
     if (i == jg) {
       e = r_hi[j] * 0.5;  // ẽ_jj = r_j / 2
     } else {
-      const double dl = __dsub_rn(lj, lam[i]);  // λ̃_j − λ̃_i
+      const double dl = __dsub_rn(lj, xv[0]);  // λ̃_j − λ̃_i
       if (eo.mode == 0) {
         if (dl == 0.0) bad = true;
         e = __ddiv_rn(wv.hi, dl);  // ẽ_ij = w_ij / (λ̃_j − λ̃_i)  (Alg. 1 line 5)
@@ -681,6 +693,7 @@ __global__ void __launch_bounds__(BS, 3)
   }
 }
 
+template <int NG>
 __global__ void __launch_bounds__(BS, 3)
     k_final(const int32_t* __restrict__ planes, long long pstride, int rows, const __grid_constant__ RecombPlan rp,
             const int32_t* __restrict__ ellB, int scale8, const double* __restrict__ X1, long long ldx1,
@@ -692,8 +705,8 @@ __global__ void __launch_bounds__(BS, 3)
   const int eb = ellB[j] + scale8;  // the Q operand (digits of X̂^(1)/2^g) has ℓ = 0 on every row
   double s2 = 0.0, m = 0.0;
   const double* xc[2] = {X1 + j * ldx1, X + j * ldx};
-  for_column_x<2>(planes, pstride, static_cast<long long>(j) * rows, rows, rp, Lj, xc, use_tma, tsm,
-                  [&](int) { return eb; }, [&](int i, const dd& u, const double* xv) {
+  for_column_x<2, false, NG>(planes, pstride, static_cast<long long>(j) * rows, rows, rp, Lj, xc, nullptr, use_tma, tsm,
+                  [&](int, int) { return eb; }, [&](int i, const dd& u, const double* xv) {
     const double x1 = xv[0];
     double s, e;
     two_sum(x1, u.hi, s, e);
@@ -734,9 +747,15 @@ int tma_ok(const RecombPlan& rp, const int32_t* planes, long long pstride, int r
            const double* x1, long long ld1) {
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_recombine_V, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem);
-    cudaFuncSetAttribute(k_recombine_E, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem);
-    cudaFuncSetAttribute(k_final, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem);
+    cudaFuncSetAttribute(k_recombine_V<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem);
+    cudaFuncSetAttribute(k_recombine_V<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem);
+    cudaFuncSetAttribute(k_recombine_V<12>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem);
+    cudaFuncSetAttribute(k_recombine_E<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem);
+    cudaFuncSetAttribute(k_recombine_E<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem);
+    cudaFuncSetAttribute(k_recombine_E<12>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem);
+    cudaFuncSetAttribute(k_final<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem);
+    cudaFuncSetAttribute(k_final<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem);
+    cudaFuncSetAttribute(k_final<12>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem);
     attr = true;
   }
   auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
@@ -779,24 +798,39 @@ void launch_recombine_V(const int32_t* planes, long long pstride, int rows, int 
                         const int32_t* ellA, const int32_t* ellB, int scale8, const double* X1, long long ldx1,
                         const double* s_hi, const double* s_lo, double* Vh, double* Vl, long long ldv,
                         double* lam_out, int32_t* eR, int* eR_max, cudaStream_t s) {
-  const int tma = tma_ok(rp, planes, pstride, rows, X1, ldx1, X1, ldx1);
-  k_recombine_V<<<cols, BS, tma ? kTmaSmem : 0, s>>>(planes, pstride, rows, rp, ellA, ellB, scale8, X1, ldx1, s_hi, s_lo,
-                                                     Vh, Vl, ldv, lam_out, eR, eR_max, tma);
+  const int tma = tma_ok(rp, planes, pstride, rows, X1, ldx1, X1, ldx1) && (reinterpret_cast<uintptr_t>(ellA) & 15) == 0;
+#define OZR_RV(NG_)                                                                                          \
+  k_recombine_V<NG_><<<cols, BS, tma ? kTmaSmem : 0, s>>>(planes, pstride, rows, rp, ellA, ellB, scale8, X1, ldx1, s_hi, \
+                                                          s_lo, Vh, Vl, ldv, lam_out, eR, eR_max, tma)
+  if (tma && rp.ngroups <= 4) OZR_RV(4);
+  else if (tma && rp.ngroups <= 8) OZR_RV(8);
+  else OZR_RV(12);
+#undef OZR_RV
 }
 void launch_recombine_E(const int32_t* planes, long long pstride, int rows, int cols, const RecombPlan& rp,
                         const int32_t* ellA, const int32_t* ellB, int scale8, const double* r_hi, const double* lam,
                         const int32_t* gX, int col0, double* Ep, long long lde, double* nrm2, int* eE_max,
                         int32_t* eE_col, int* err, const EdgeOut& eo, cudaStream_t s) {
-  const int tma = tma_ok(rp, planes, pstride, rows, nullptr, 0, nullptr, 0);
-  k_recombine_E<<<cols, BS, tma ? kTmaSmem : 0, s>>>(planes, pstride, rows, rp, ellA, ellB, scale8, r_hi, lam, gX, col0,
-                                                     Ep, lde, nrm2, eE_max, eE_col, err, eo, tma);
+  const int tma = tma_ok(rp, planes, pstride, rows, lam, 0, nullptr, 0) && (reinterpret_cast<uintptr_t>(ellA) & 15) == 0;
+#define OZR_RE(NG_)                                                                                            \
+  k_recombine_E<NG_><<<cols, BS, tma ? kTmaSmem : 0, s>>>(planes, pstride, rows, rp, ellA, ellB, scale8, r_hi, lam, gX, \
+                                                          col0, Ep, lde, nrm2, eE_max, eE_col, err, eo, tma)
+  if (tma && rp.ngroups <= 4) OZR_RE(4);
+  else if (tma && rp.ngroups <= 8) OZR_RE(8);
+  else OZR_RE(12);
+#undef OZR_RE
 }
 void launch_final(const int32_t* planes, long long pstride, int rows, int cols, const RecombPlan& rp,
                   const int32_t* ellB, int scale8, const double* X1, long long ldx1, double* X, long long ldx,
                   double* nu2, double* wnext, cudaStream_t s) {
   const int tma = tma_ok(rp, planes, pstride, rows, X1, ldx1, X, ldx);
-  k_final<<<cols, BS, tma ? kTmaSmem : 0, s>>>(planes, pstride, rows, rp, ellB, scale8, X1, ldx1, X, ldx, nu2, wnext,
-                                               tma);
+#define OZR_FI(NG_)                                                                                                 \
+  k_final<NG_><<<cols, BS, tma ? kTmaSmem : 0, s>>>(planes, pstride, rows, rp, ellB, scale8, X1, ldx1, X, ldx, nu2, wnext, \
+                                                    tma)
+  if (tma && rp.ngroups <= 4) OZR_FI(4);
+  else if (tma && rp.ngroups <= 8) OZR_FI(8);
+  else OZR_FI(12);
+#undef OZR_FI
 }
 void launch_iota(int* p, int n, cudaStream_t s) { k_iota<<<(n + 255) / 256, 256, 0, s>>>(p, n); }
 void launch_uf_flatten(int* parent, int n, cudaStream_t s) { k_uf_flatten<<<(n + 255) / 256, 256, 0, s>>>(parent, n); }
