@@ -108,7 +108,7 @@ ozr_status ozr_gemm_plan(int64_t k, int kA, int kB, int L, int* ngroups, int* gr
  * ------------------------------------------------------------------------------------------------ */
 typedef struct {
   double delta;      /* prescribed forward error δ (> u)                                     */
-  double theta;      /* β is chosen for δ' = δ/θ (R11; default 1)                  */
+  double theta;      /* β and the budgets are chosen for δ' = δ/θ (R11; default 4) */
   int beta_mode;     /* 0: §4.1 tuned β (⌊·⌋, nδ) [default]; 1: §3.3 eq. proposed_beta (⌈·⌉, ξ) */
   double xi;         /* ξ for beta_mode 1 (0 → n)                                            */
   int beta_override; /* > 0: use this β instead of the formula                               */

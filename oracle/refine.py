@@ -19,6 +19,7 @@ from .split import (alpha_dense, alpha_theoretical, beta_dense, beta_theoretical
                     x1_truncate)
 
 BETA_MIN, BETA_MAX = 2, 52  # reading R4: τ + x stays in τ's binade iff β ≥ 2; ≥ 1 bit kept iff β ≤ 52
+THETA_DEFAULT = 4.0  # reading R11: δ' = δ/θ so that the O(δ) result lands at or below δ
 
 
 def col_dot_dd(X, Yh, Yl=None):
@@ -128,7 +129,7 @@ def cluster_subsolve(E, lam, J, X1, Wh, Wl, rh, rl):
     return float(np.max(np.abs(th)) / gK) if gK > 0 else np.inf
 
 
-def sweep(A, X, lam_prev, delta, theta=1.0, beta=None, beta_mode="dense", xi=None, truncate=True,
+def sweep(A, X, lam_prev, delta, theta=THETA_DEFAULT, beta=None, beta_mode="dense", xi=None, truncate=True,
           cluster_mode=1, kappa=KAPPA_DEFAULT, max_cluster=None, groups=None):
     """One iteration of Algorithm 1. Returns (X_new fp64, λ̂ fp64, info dict).
 
@@ -205,7 +206,7 @@ def sweep(A, X, lam_prev, delta, theta=1.0, beta=None, beta_mode="dense", xi=Non
     return Xn, lam, info
 
 
-def refine_to_tol(A, X0, lam0, delta, theta=1.0, max_sweeps=6, beta_mode="dense", xi=None, callback=None,
+def refine_to_tol(A, X0, lam0, delta, theta=THETA_DEFAULT, max_sweeps=6, beta_mode="dense", xi=None, callback=None,
                   cluster_mode=1, kappa=KAPPA_DEFAULT):
     """Driver (reading R12): repeat sweeps; stop after sweep k when ν_k = ‖X_k − X_{k−1}‖_F ≤ δ, or when
     the paper's error model predicts ‖X − X_k‖ ≲ ν_k² max|λ̂| / (n gap) ≤ δ (eq. assume2 / gamma,
@@ -319,7 +320,7 @@ def forward_error(Xh_ref, Xl_ref, X, lam_ref=None, lam=None, power_iters=None):
     return float(np.sqrt(s))
 
 
-def sweep_columns(A, X, lam_prev, delta, J, theta=1.0, beta=None):
+def sweep_columns(A, X, lam_prev, delta, J, theta=THETA_DEFAULT, beta=None):
     """Algorithm 1 restricted to the output columns J (bench.py's bounded CPU sample; identical formulas
     to sweep(), only the products' column sets shrink): V_J = A X̂^(1)_J, λ̂_J, Res_J,
     W_{:,J} = X̂^(1)ᵀ Res_J, Ẽ_{:,J} (needs λ̂ of all columns: λ_prev is used for i ∉ J),
@@ -355,7 +356,7 @@ def sweep_columns(A, X, lam_prev, delta, J, theta=1.0, beta=None):
     return fast_two_sum(s, e + Ul)[0], lamJ, beta
 
 
-def sweep_block(A, X, lam_prev, delta, col0, nl, allgather, theta=1.0):
+def sweep_block(A, X, lam_prev, delta, col0, nl, allgather, theta=THETA_DEFAULT):
     """Algorithm 1 (cluster branch off) for the column block J = [col0, col0 + nl) of one
     rank of the block-column partition: X̂^(1) from the full X̂ (column-local truncation,
     β from the all-gathered column maxima — here the full X̂ is at hand), V_J = A X̂^(1)_J, λ̂_J, then

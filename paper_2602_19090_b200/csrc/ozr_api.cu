@@ -1037,7 +1037,7 @@ void ozr_params_default(ozr_params* p) {
   if (!p) return;
   memset(p, 0, sizeof *p);
   p->delta = 1e-12;
-  p->theta = 1.0;
+  p->theta = 4.0;  // R11: the O(δ) result lands at or below δ
   p->beta_mode = 0;
   p->xi = 0.0;
   p->beta_override = 0;

@@ -95,3 +95,27 @@ def test_c3_fp64_start_stays_linear(ctx):
     Xg, lg, rep, Xo, lo, info, groups = parity_sweep(ctx, A, X0, lam0, 1e-12)
     assert rep["n_clusters"] == 0 and groups == []
     assert np.max(np.abs(Xg - Xo)) <= 1e-13
+
+
+@pytest.mark.parametrize("n", [512])
+def test_c3_fp32_start_exercises_groups(ctx, n):
+    """The c3 spectrum (clusters of 8 eigenvalues 1e-10 apart) from an FP32 eigensolver: inside every
+    cluster the FP32 vectors are arbitrary rotations (|ẽ_ij| ≫ κ), so each cluster becomes an unresolved
+    group; one sweep matches the oracle and refine_to_tol reaches δ = 1e-12 against the reference."""
+    import paper_2602_19090_b200 as ozr
+    A, lam0, X0 = _case("c3", n, "fp32")
+    Xg, lg, rep, Xo, lo, info, groups = parity_sweep(ctx, A, X0, lam0, 1e-12)
+    assert rep["n_clusters"] >= n // 64 and all(len(J) >= 2 for J in groups)
+    inJ = np.zeros(n, dtype=bool)
+    for J in groups:
+        inJ[J] = True
+    assert np.max(np.abs(Xg[:, ~inJ] - Xo[:, ~inJ])) <= 1e-13
+    tol = 1e-13 + 10 * np.sqrt(rep["max_cluster"]) * U * info["cluster_cond"]
+    assert np.max(np.abs(Xg[:, inJ] - Xo[:, inJ])) <= tol
+    lr, Xr = W.initial_eig(A, "fp64")
+    Xh, Xl, lh, ll, _ = orf.reference_eigvecs(A, Xr, lr)
+    Xd, ld = to_dev(X0), vec_dev(lam0)
+    st, hist = ozr.ozr_refine_to_tol(ctx, to_dev(A), Xd, ld, ozr.default_params(delta=1e-12, max_sweeps=10))
+    fe = orf.forward_error(Xh, Xl, to_np(Xd), lh, to_np(ld))
+    assert st == 0, hist
+    assert fe <= 1e-12, (fe, [(h["net_update"], h["n_clusters"]) for h in hist])

@@ -57,9 +57,10 @@ def test_refine_step_fullsize_sampled_lambda(ctx, big):
     A, lam0, X0, cfg, An, ln, Xn = big
     X = ozr.colmajor(X0.clone())
     lam = lam0.clone()
-    rep = ozr.ozr_refine_step(ctx, A, X, lam, ozr.default_params(delta=cfg["delta"]))
+    p = ozr.default_params(delta=cfg["delta"])
+    rep = ozr.ozr_refine_step(ctx, A, X, lam, p)
     w = np.max(np.abs(Xn), axis=0)
-    beta, _ = orf.choose_beta(N, cfg["delta"], ln, osp.ceil_log2(w), w)
+    beta, _ = orf.choose_beta(N, cfg["delta"] / p.theta, ln, osp.ceil_log2(w), w)
     assert rep["beta"] == min(max(beta, 2), 52)
     J = np.array([0, 17, 4096, 8190, 8191])
     X1J = osp.x1_truncate(Xn, rep["beta"])[0][:, J]
