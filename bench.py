@@ -98,23 +98,29 @@ def _dist():
     return ws, rank, local
 
 
-def cpu_oracle_sample(name, n, budget_s=15.0, ncols=None, seed_offset=0):
-    """The oracle (oracle/refine.sweep_columns, dd triple loops) on a column sample of the workload."""
-    import workloads as W
+def cpu_oracle_sample(name, A, X0, lam0, delta, budget_s=12.0):
+    """The oracle (oracle/refine.sweep_columns, dd triple loops) on a column sample of THE SAME n x n
+    problem the GPU step refines (copied to the host): a sweep restricted to |J| output columns costs
+    O(n²·|J|) per product; |J| is sized from a 4-column probe to about `budget_s` seconds."""
     from oracle import _clib
     from oracle import refine as orf
-    cfg = dict(W.CONFIGS[name])
-    n_eff = min(n, 2048)  # the CPU generator/eigensolver for the sample matrix is O(n^3) too
-    A, _ = W.make_matrix(n_eff, cfg["kind"], cfg["cnd"], cfg["seed"] + seed_offset)
-    lam0, X0 = W.initial_eig(A, cfg["start"])
-    J = np.arange(ncols or 8)
+    n = A.shape[0]
+    probes = []
+    for c in (8, 32):  # fixed cost (the full-matrix truncation and statistics) + per-column cost
+        t0 = time.perf_counter()
+        orf.sweep_columns(A, X0, lam0, delta, np.arange(min(c, n)))
+        probes.append(time.perf_counter() - t0)
+    slope = max((probes[1] - probes[0]) / 24.0, 1e-6)
+    fixed = max(probes[0] - 8 * slope, 0.0)
+    ncols = int(max(8, min(n, (budget_s - fixed) / slope)))
+    J = np.linspace(0, n - 1, ncols).astype(np.int64)
     t0 = time.perf_counter()
-    orf.sweep_columns(A, X0, lam0, cfg["delta"], J)
+    orf.sweep_columns(A, X0, lam0, delta, J)
     dt = time.perf_counter() - t0
-    flops = 3 * 2.0 * n_eff * n_eff * len(J)
+    flops = 3 * 2.0 * n * n * len(J)
     return {"value": flops / dt / 1e12, "unit": "TFLOP/s", "cores": _clib.num_threads(), "kind": "oracle",
-            "sample": f"oracle sweep restricted to {len(J)} of {n_eff} columns (dd triple loops, O(n^2·|J|) per "
-                      f"product) of the {name} recipe at n={n_eff}; {dt:.2f} s",
+            "sample": f"oracle sweep (dd triple loops) restricted to {len(J)} evenly spaced of the {n} output "
+                      f"columns of the same {name} problem, O(n^2·|J|) per product; {dt:.2f} s",
             "seconds": dt}
 
 
@@ -166,7 +172,7 @@ def main():
     ap.add_argument("--config", default="c4p")
     ap.add_argument("--n", type=int, default=0)
     ap.add_argument("--impl", default="ozr", choices=["ozr", "reference"])
-    ap.add_argument("--ref-cols", type=int, default=8)
+    ap.add_argument("--ref-cols", type=int, default=64)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--truncate", type=int, default=1,
@@ -329,7 +335,7 @@ def main():
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         try:
-            cpu = cpu_oracle_sample(name, n)
+            cpu = cpu_oracle_sample(name, A.cpu().numpy(), X0.cpu().numpy(), lam0.cpu().numpy(), delta)
         except Exception as ex:  # the oracle C library missing on the box is a setup error: report it
             cpu = {"value": None, "unit": "TFLOP/s", "cores": os.cpu_count(), "kind": "oracle", "sample": f"failed: {ex}"}
 

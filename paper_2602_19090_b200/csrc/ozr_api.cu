@@ -3,6 +3,7 @@
 // few device->host reads of scalars the choices depend on. No math of the method runs on the host
 // except the choice of β (§4.1 lines 458-463 / §3.3) from O(n) statistics.
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -50,6 +51,7 @@ struct ozr_ctx_s {
   bool trace = false;
   std::vector<cudaEvent_t> tev;
   std::vector<const char*> tname;
+  std::vector<double> thost;  // host wall clock (ms) when the mark was recorded
   int tn = 0;
   void mark(const char* name) {
     if (!trace) return;
@@ -58,8 +60,10 @@ struct ozr_ctx_s {
       cudaEventCreate(&e);
       tev.push_back(e);
       tname.push_back(name);
+      thost.push_back(0.0);
     }
     tname[tn] = name;
+    thost[tn] = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
     cudaEventRecord(tev[tn++], stream);
   }
   void dump() {
@@ -68,11 +72,11 @@ struct ozr_ctx_s {
       return;
     }
     cudaEventSynchronize(tev[tn - 1]);
-    fprintf(stderr, "[ozr trace]");
+    fprintf(stderr, "[ozr trace] gpu ms between marks (host ms in brackets):");
     for (int i = 1; i < tn; ++i) {
       float ms = 0.f;
       cudaEventElapsedTime(&ms, tev[i - 1], tev[i]);
-      fprintf(stderr, " %s=%.3f", tname[i], ms);
+      fprintf(stderr, " %s=%.3f[%.3f]", tname[i], ms, thost[i] - thost[i - 1]);
     }
     fprintf(stderr, "\n");
     tn = 0;
