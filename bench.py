@@ -148,7 +148,7 @@ def run_reference(args):
     val = flops / dt / 1e12
     out = {"impl": "reference", "metric": METRIC, "value": val, "unit": "TFLOP/s", "n_gpus": ws,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
-           "scaling": "weak", "vs_baseline": None, "dtype": "f64 (double-double)", "data": "synthetic",
+           "scaling": "strong", "vs_baseline": None, "dtype": "f64 (double-double)", "data": "synthetic",
            "config": {"workload": f"{name}: " + _describe(cfg, n), "sample_n": n_eff, "sample_cols": len(J)},
            "cpu_baseline": {"value": val, "unit": "TFLOP/s", "cores": _clib.num_threads(), "kind": "oracle",
                             "sample": f"each step: oracle sweep on {len(J)} of {n_eff} columns of the {name} "
