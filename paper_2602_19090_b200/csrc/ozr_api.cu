@@ -9,6 +9,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <memory>
 #include <string>
 #include <vector>
@@ -45,6 +46,7 @@ struct ozr_ctx_s {
   std::vector<int> last_members, last_offsets{0};  // unresolved groups of the last sweep (R13)
   cudaEvent_t ev[8];
   cudaStream_t xstream = nullptr;  // side stream of the digit all-gather (overlaps the V product)
+  cudaEvent_t ev_sync = nullptr;   // the host waits on this instead of the whole stream
   cudaEvent_t xev[2];
   bool events = false;
   // tracing (OZR_TRACE=1): named events between the kernels of a sweep, printed to stderr per sweep
@@ -108,7 +110,7 @@ namespace {
 enum Slot {
   S_ADIG, S_AELL, S_W, S_X1, S_XDIG, S_XDIGT, S_G, S_SH, S_SL, S_RH, S_RL, S_PLANES, S_VH, S_VL, S_LAM, S_ER,
   S_ERR, S_EMAX, S_RDIG, S_RELL, S_EP, S_NRM2, S_NU2, S_WNEXT, S_ZEROELL, S_TMP1, S_TMP2, S_BELL, S_AT, S_ONES,
-  S_EDGES, S_ECOUNT, S_CINT, S_CDBL, S_CM, S_CR, S_CK, S_CV, S_CZ, S_CT, S_CSCR, S_CFLAG, S_SCAL, S_UFALL, S_CPART, S_GCNT
+  S_EDGES, S_ECOUNT, S_CINT, S_CDBL, S_CM, S_CR, S_CK, S_CV, S_CZ, S_CT, S_CSCR, S_CFLAG, S_SCAL, S_UFALL, S_CPART, S_GCNT, S_WA
 };
 
 ozr_status fail(ozr_ctx c, ozr_status st, const char* fmt, ...) {
@@ -442,7 +444,7 @@ struct SweepState {
 // A → digit planes (a1), stream-ordered; the exponents land in `hell` (host) at the caller's next
 // synchronisation, after which split_A_finish derives e_A,max. Error flags go to derr.
 ozr_status split_A_launch(ozr_ctx ctx, const double* A, int64_t n, int64_t lda, int kA, int* derr,
-                          std::vector<int32_t>& hell) {
+                          std::vector<int32_t>& /*hell*/) {
   const int64_t ld = round16(n);
   int8_t* adig = ctx->ws<int8_t>(S_ADIG, static_cast<size_t>(kA) * ld * n);
   int32_t* aell = ctx->ws<int32_t>(S_AELL, n);
@@ -453,14 +455,13 @@ ozr_status split_A_launch(ozr_ctx ctx, const double* A, int64_t n, int64_t lda, 
   launch_split_fixed(A, nullptr, lda, static_cast<int>(n), static_cast<int>(n), kA, adig, ld, ld * n, aell, derr,
                      ctx->stream);
   OZR_CK(cudaGetLastError(), "split A");
-  hell.resize(n);
-  OZR_CK(cudaMemcpyAsync(hell.data(), aell, n * sizeof(int32_t), cudaMemcpyDeviceToHost, ctx->stream), "D2H ell");
   return OZR_OK;
 }
 
-void split_A_finish(const double* A, int64_t n, int kA, const std::vector<int32_t>& hell, SweepState& st) {
+// e_A,max = max_i ℓ_i + S_kA = max_i ⌈log2 max_j |a_ij|⌉ (the split's per-line exponent, 0 for a zero line)
+void split_A_finish(const double* A, int64_t n, const std::vector<double>& hwA, int kA, SweepState& st) {
   int em = -100000;
-  for (int64_t i = 0; i < n; ++i) em = std::max(em, hell[i] + 8 * (kA - 1) + 6);
+  for (int64_t i = 0; i < n; ++i) em = std::max(em, hwA[i] != 0.0 ? ceil_log2_host(hwA[i]) : 0);
   st.A = A;
   st.nA = n;
   st.kA_split = kA;
@@ -515,7 +516,10 @@ ozr_status sweep(ozr_ctx ctx, Exchange* ex, const double* A, int64_t n, int64_t 
   };
   // Up to 3 device ints combined over the ranks (max) plus the error flags (OR), with ONE host
   // synchronisation; pending host copies queued on the stream complete with it. Fails on error flags.
-  auto scalars = [&](std::initializer_list<const int*> dvs, int* outs) -> ozr_status {
+  // post (nullable): work to enqueue after the reads and before waiting for them, so that the GPU keeps
+  // running it while the host takes its decisions
+  auto scalars = [&](std::initializer_list<const int*> dvs, int* outs,
+                     const std::function<ozr_status()>& post = nullptr) -> ozr_status {
     int k = 0;
     for (const int* dv : dvs) {
       OZR_CK(cudaMemcpyAsync(scal + 4 * RK + k, dv, sizeof(int), cudaMemcpyDeviceToDevice, s), "D2D");
@@ -526,7 +530,12 @@ ozr_status sweep(ozr_ctx ctx, Exchange* ex, const double* A, int64_t n, int64_t 
     if (e != OZR_OK) return e;
     std::vector<int> h(4 * NP);
     OZR_CK(cudaMemcpyAsync(h.data(), scal, h.size() * sizeof(int), cudaMemcpyDeviceToHost, s), "D2H");
-    OZR_CK(cudaStreamSynchronize(s), "sync");
+    OZR_CK(cudaEventRecord(ctx->ev_sync, s), "event");
+    if (post) {
+      ozr_status pe = post();
+      if (pe != OZR_OK) return pe;
+    }
+    OZR_CK(cudaEventSynchronize(ctx->ev_sync), "sync");
     int bits = 0;
     for (int r = 0; r < NP; ++r) bits |= h[4 * r + 3];
     for (int q = 0; q < k; ++q) {
@@ -550,14 +559,25 @@ ozr_status sweep(ozr_ctx ctx, Exchange* ex, const double* A, int64_t n, int64_t 
     OZR_CK(cudaMemcpyAsync(w + col0, wnext + col0, nl * sizeof(double), cudaMemcpyDeviceToDevice, s), "copy w");
   }
   OZR_X(xgather(w, nl * sizeof(double)));
-  // a1 (once per call): the A split runs before the a0 synchronisation, which also brings its exponents
+  // a1 (once per call): the column maxima of A give e_A,max now; the A split itself is enqueued after the
+  // a0 reads and runs while the host chooses β and the budgets
   const bool new_A = (st.A != A || st.nA != n);
   std::vector<int32_t> hell;
-  if (new_A) OZR_X(split_A_launch(ctx, A, n, lda, P.kA_split, derr, hell));
+  std::vector<double> hwA;
+  if (new_A) {
+    double* wA = ctx->ws<double>(S_WA, n);
+    OZR_ALLOC(wA);
+    launch_colmax(A, lda, N, N, wA, derr, s);
+    OZR_CK(cudaGetLastError(), "colmax A");
+    hwA.resize(n);
+    OZR_CK(cudaMemcpyAsync(hwA.data(), wA, n * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H wA");
+  }
   std::vector<double> hw(n), hlam(n);
   OZR_CK(cudaMemcpyAsync(hw.data(), w, n * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H w");
   OZR_CK(cudaMemcpyAsync(hlam.data(), lambda, n * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H lambda");
-  OZR_X(scalars({}, nullptr));
+  OZR_X(scalars({}, nullptr, [&]() -> ozr_status {
+    return new_A ? split_A_launch(ctx, A, n, lda, P.kA_split, derr, hell) : OZR_OK;
+  }));
   for (double x : hlam)
     if (!std::isfinite(x)) return fail(ctx, OZR_ERR_NONFINITE, "non-finite lambda");
   const double delta_p = P.delta / (P.theta > 0 ? P.theta : 1.0);
@@ -585,7 +605,7 @@ ozr_status sweep(ozr_ctx ctx, Exchange* ex, const double* A, int64_t n, int64_t 
   rep.max_abs_lambda = maxlam;
 
   // ---- A split (once per refine_to_tol call; A and its digits are replicated on every rank)
-  if (new_A) split_A_finish(A, n, P.kA_split, hell, st);
+  if (new_A) split_A_finish(A, n, hwA, P.kA_split, st);
   ctx->mark("stats+splitA");
   // per-column accuracy of V (R8, R8b): θ_V·δ'·gap_j with the previous λ̂ (this rank's columns)
   std::vector<double>& gaps_prev = ls_prev.colgap;
@@ -652,9 +672,8 @@ ozr_status sweep(ozr_ctx ctx, Exchange* ex, const double* A, int64_t n, int64_t 
   DigitOperand opX{xdig, ld, ld * n, kx};               // all columns (A operand of W)
   OZR_X(run_gemm(ctx, opA, opXJ, N, NL, N, pt, planes, 0));
   ctx->mark("gemmV");
+  // join the digit exchange before any other collective (λ̂ below) and before reading other ranks' digits
   if (ex) OZR_CK(cudaStreamWaitEvent(s, ctx->xev[1], 0), "wait exchange");
-  launch_transpose_i8(xdig, ld, ld * n, xdigT, ld, ld * n, N, N, kx, s);  // A operand of X̂Ẽ
-  OZR_CK(cudaGetLastError(), "transpose digits");
   const double pV = tilesV ? avg_pairs_V : static_cast<double>(count_pairs(gV));
   rep.pairs_V = static_cast<int>(std::lround(pV));
   ops += 2.0 * n * n * nl * pV;
@@ -677,7 +696,13 @@ ozr_status sweep(ozr_ctx ctx, Exchange* ex, const double* A, int64_t n, int64_t 
   std::vector<int> eR_col(nl);
   OZR_CK(cudaMemcpyAsync(hlam_new.data(), lam, n * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H");
   OZR_CK(cudaMemcpyAsync(eR_col.data(), eR, nl * sizeof(int32_t), cudaMemcpyDeviceToHost, s), "D2H eR");
-  OZR_X(scalars({demax}, &eRmax));  // one synchronisation for λ̂, the Res exponents and their maximum
+  // one synchronisation for λ̂, the Res exponents and their maximum; the digit transpose (A operand of
+  // X̂Ẽ, after the exchange) runs meanwhile
+  OZR_X(scalars({demax}, &eRmax, [&]() -> ozr_status {
+    launch_transpose_i8(xdig, ld, ld * n, xdigT, ld, ld * n, N, N, kx, s);
+    OZR_CK(cudaGetLastError(), "transpose digits");
+    return OZR_OK;
+  }));
   LamStats ls_new = lam_stats(hlam_new);
   const double gap_new0 = ls_new.gap0;
   if (!(gap_new0 > 0.0) && P.cluster_mode == 0)
@@ -1014,6 +1039,7 @@ ozr_status ozr_create(ozr_ctx* out, int device, void* stream, int64_t n_max) {
   c->stream = static_cast<cudaStream_t>(stream);
   for (int i = 0; i < 8; ++i) cudaEventCreate(&c->ev[i]);
   cudaStreamCreateWithFlags(&c->xstream, cudaStreamNonBlocking);
+  cudaEventCreateWithFlags(&c->ev_sync, cudaEventDisableTiming);
   for (int i = 0; i < 2; ++i) cudaEventCreateWithFlags(&c->xev[i], cudaEventDisableTiming);
   c->events = true;
   const char* tr = getenv("OZR_TRACE");
@@ -1032,6 +1058,7 @@ void ozr_destroy(ozr_ctx ctx) {
     for (int i = 0; i < 8; ++i) cudaEventDestroy(ctx->ev[i]);
   for (int i = 0; i < 2; ++i) cudaEventDestroy(ctx->xev[i]);
   if (ctx->xstream) cudaStreamDestroy(ctx->xstream);
+  if (ctx->ev_sync) cudaEventDestroy(ctx->ev_sync);
   delete ctx;
 }
 
