@@ -124,6 +124,10 @@ typedef struct {
   int tile_budgets;  /* 1: per-256-column pair budgets from the local gaps gap_j (R8b) [default]  */
   double kappa;      /* cluster_mode 1: linearisation threshold κ on |ẽ_ij| (default 2^-10)     */
   int max_cluster;   /* cluster_mode 1: largest group solved (default 4096; larger → OZR_ERR_RANGE) */
+  int form_R;        /* 1: also form R = I − X̂^(1)ᵀX̂^(1) by INT8 slice products (to θ_W·δ' absolute; the
+                        R/S form's first product, PAPER.md:241-250 — Algorithm 1's W-form needs only its
+                        diagonal, which is always exact); reports ‖R‖_F and the OA threshold ω, and
+                        ozr_last_R returns R. Default 0 */
 } ozr_params;
 
 void ozr_params_default(ozr_params* p);
@@ -144,6 +148,10 @@ typedef struct {
   double predicted_error;           /* ν² max|λ̂| / (n gap) (eq. assume2 with ξ = n), information       */
   double ms_total, ms_gemm;         /* device time of the sweep and of its slice-product kernels       */
   double int8_ops;                  /* 2·m·n·k·pairs summed over the sweep's slice products            */
+  int pairs_G;                      /* form_R: pairs of the X̂ᵀX̂ slice product                          */
+  double normR_fro, normW_fro;      /* form_R: ‖R‖_F, ‖W‖_F                                            */
+  double omega_oa;                  /* form_R: ω = 2(‖W‖_F + 2·max|λ̂|·‖R‖_F), the Frobenius form of the
+                                       OA-2018 cluster threshold 2(‖S − D̃‖ + ‖A‖‖R‖) (diagnostic, R13) */
 } ozr_step_report;
 
 /* One sweep on columns [0, n): A (n x n, symmetric — only its columns are read), X (n x n, in/out:
@@ -152,6 +160,10 @@ typedef struct {
  * Errors: OZR_ERR_ARG, OZR_ERR_RANGE (δ ≤ u), OZR_ERR_DEGENERATE, OZR_ERR_CUDA, OZR_ERR_NOMEM. */
 ozr_status ozr_refine_step(ozr_ctx ctx, const double* A, int64_t n, int64_t lda, double* X, int64_t ldx,
                            double* lambda, const ozr_params* params, ozr_step_report* report);
+
+/* The R = I − X̂^(1)ᵀX̂^(1) of the context's last sweep run with params.form_R = 1: this rank's columns
+ * (n x n_local, column-major) copied to R (device, ldr ≥ n). OZR_ERR_ARG if none was formed. */
+ozr_status ozr_last_R(ozr_ctx ctx, double* R, int64_t ldr);
 
 /* Host: the unresolved groups of the context's last sweep (cluster_mode 1). members receives the global
  * column indices of every group, concatenated, each group in ascending (λ̂, index) order; offsets[g] is

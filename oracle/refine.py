@@ -130,7 +130,7 @@ def cluster_subsolve(E, lam, J, X1, Wh, Wl, rh, rl):
 
 
 def sweep(A, X, lam_prev, delta, theta=THETA_DEFAULT, beta=None, beta_mode="dense", xi=None, truncate=True,
-          cluster_mode=1, kappa=KAPPA_DEFAULT, max_cluster=None, groups=None):
+          cluster_mode=1, kappa=KAPPA_DEFAULT, max_cluster=None, groups=None, form_R=False):
     """One iteration of Algorithm 1. Returns (X_new fp64, λ̂ fp64, info dict).
 
     cluster_mode 0: the paper's Algorithm 1 (distinct eigenvalues assumed); equal
@@ -171,6 +171,16 @@ def sweep(A, X, lam_prev, delta, theta=THETA_DEFAULT, beta=None, beta_mode="dens
     Wh, Wl = _clib.dd_gemm_nt(np.ascontiguousarray(X1.T), np.ascontiguousarray(Rh.T), None,
                               np.ascontiguousarray(Rl.T))
     W = Wh + Wl
+    if form_R:
+        # R = I − X̂ᵀX̂ (the R/S form): off the diagonal −x̂_iᵀx̂_j in dd, on it the r_i of
+        # line 2; and ‖W‖_F (for the OA-2018 threshold diagnostic, reading R13)
+        X1T = np.ascontiguousarray(X1.T)
+        Gh, Gl = _clib.dd_gemm_nt(X1T, X1T)
+        R = -(Gh + Gl)
+        R[np.arange(n), np.arange(n)] = rh + rl
+        info["R"] = R
+        info["normW_fro"] = float(np.sqrt(np.sum(Wh * Wh)))
+        info["normR_fro"] = float(np.sqrt(np.sum(R * R)))
     # line 5: ẽ_ij = w_ij / (λ̃_j − λ̃_i), i ≠ j;  ẽ_ii = r_i / 2
     dl = lam[None, :] - lam[:, None]
     off = ~np.eye(n, dtype=bool)

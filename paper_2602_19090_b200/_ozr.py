@@ -20,7 +20,7 @@ STATUS = {0: "OZR_OK", 1: "OZR_ERR_ARG", 2: "OZR_ERR_NONFINITE", 3: "OZR_ERR_RAN
 EXPORTS = ["ozr_version", "ozr_create", "ozr_destroy", "ozr_last_error", "ozr_split", "ozr_gemm", "ozr_gemm_plan",
            "ozr_params_default", "ozr_refine_step", "ozr_refine_to_tol", "ozr_last_clusters", "ozr_comm_nccl_id",
            "ozr_comm_create_nccl", "ozr_comm_create_host_group", "ozr_comm_destroy", "ozr_comm_size", "ozr_comm_rank",
-           "ozr_refine_step_dist", "ozr_refine_to_tol_dist"]
+           "ozr_refine_step_dist", "ozr_refine_to_tol_dist", "ozr_last_R"]
 
 
 class OzrError(RuntimeError):
@@ -35,7 +35,8 @@ class Params(ctypes.Structure):
                 ("max_sweeps", ctypes.c_int), ("kA_split", ctypes.c_int), ("theta_V", ctypes.c_double),
                 ("theta_W", ctypes.c_double), ("theta_U", ctypes.c_double), ("L_V", ctypes.c_int),
                 ("L_W", ctypes.c_int), ("L_U", ctypes.c_int), ("cluster_mode", ctypes.c_int),
-                ("tile_budgets", ctypes.c_int), ("kappa", ctypes.c_double), ("max_cluster", ctypes.c_int)]
+                ("tile_budgets", ctypes.c_int), ("kappa", ctypes.c_double), ("max_cluster", ctypes.c_int),
+                ("form_R", ctypes.c_int)]
 
 
 class StepReport(ctypes.Structure):
@@ -43,7 +44,9 @@ class StepReport(ctypes.Structure):
                                               "L_W", "L_U", "pairs_V", "pairs_W", "pairs_U", "n_clusters", "max_cluster",
                                               "launches", "exchanges"]] +
                 [(f, ctypes.c_double) for f in ["gap_min", "max_abs_lambda", "normE_fro", "net_update",
-                                                 "predicted_error", "ms_total", "ms_gemm", "int8_ops"]])
+                                                 "predicted_error", "ms_total", "ms_gemm", "int8_ops"]] +
+                [("pairs_G", ctypes.c_int)] +
+                [(f, ctypes.c_double) for f in ["normR_fro", "normW_fro", "omega_oa"]])
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
@@ -102,6 +105,8 @@ def lib():
         L.ozr_refine_to_tol_dist.argtypes = [vp, vp, vp, i64, i64, vp, i64, vp, ctypes.POINTER(Params),
                                              ctypes.POINTER(StepReport), i32, ip]
         L.ozr_refine_to_tol_dist.restype = i32
+        L.ozr_last_R.argtypes = [vp, vp, i64]
+        L.ozr_last_R.restype = i32
         _lib = L
     return _lib
 
@@ -318,3 +323,10 @@ def ozr_refine_to_tol_dist(ctx, comm, A, X, lam, params, raise_on_nonconvergence
     if st != 0 and (st != 5 or raise_on_nonconvergence):
         ctx.check(st)
     return st, [H[i].as_dict() for i in range(done.value)]
+
+
+def ozr_last_R(ctx, n, n_local=None):
+    """R = I − X̂^(1)ᵀX̂^(1) of the last sweep run with form_R=1 (this rank's columns), column-major."""
+    R = colmajor(torch.empty((n, n_local or n), dtype=torch.float64, device=torch.device("cuda", ctx.device)))
+    ctx.check(lib().ozr_last_R(ctx.h, _ptr(R), n))
+    return R

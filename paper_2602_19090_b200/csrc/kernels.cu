@@ -644,7 +644,7 @@ __global__ void __launch_bounds__(BS, 3)
                   const double* __restrict__ r_hi, const double* __restrict__ lam, const int32_t* __restrict__ gX,
                   int col0, double* __restrict__ Ep, long long lde, double* __restrict__ nrm2,
                   int* __restrict__ eE_max, int32_t* __restrict__ eE_col, int* __restrict__ err,
-                  const EdgeOut eo, int use_tma) {
+                  const EdgeOut eo, int use_tma, double* __restrict__ nW2) {
   extern __shared__ __align__(128) unsigned char tsm[];
   __shared__ double sh[BS / 32];
   const int j = blockIdx.x;        // local column
@@ -652,7 +652,7 @@ __global__ void __launch_bounds__(BS, 3)
   const int jg = col0 + j;         // global index of column j (its λ̂)
   const int eb = ellB[j] + scale8;
   const double lj = lam[jg];
-  double m = 0.0, s2 = 0.0;
+  double m = 0.0, s2 = 0.0, w2 = 0.0;
   bool bad = false, unresolved = false;
   // the row vectors λ̂_i and ℓ_i of the row operand (X̂^(1)ᵀ: g_i) ride in the shared-memory stages
   // with the planes
@@ -660,6 +660,7 @@ __global__ void __launch_bounds__(BS, 3)
   for_column_x<1, true, NG>(planes, pstride, static_cast<long long>(j) * rows, rows, rp, Lj, xc, ellA, use_tma, tsm,
                             [&](int, int gi) { return gi + eb; }, [&](int i, const dd& wv, const double* xv) {
     double e;
+    w2 = __fma_rn(wv.hi, wv.hi, w2);
     if (i == jg) {
       e = r_hi[j] * 0.5;  // ẽ_jj = r_j / 2
     } else {
@@ -686,11 +687,35 @@ __global__ void __launch_bounds__(BS, 3)
   if (__syncthreads_or(unresolved) && threadIdx.x == 0) atomicOr(eo.any, 1);
   m = block_max(m, sh);
   s2 = block_sum(s2, sh);
+  w2 = block_sum(w2, sh);
   if (threadIdx.x == 0) {
     nrm2[j] = s2;
+    if (nW2) nW2[j] = w2;
     eE_col[j] = (m > 0.0) ? ceil_log2_d(m) : -100000;
     if (m > 0.0) atomicMax(eE_max, ceil_log2_d(m));
   }
+}
+
+// R = I − X̂^(1)ᵀX̂^(1) for the local columns (form_R): r_ij = −RN(g_ij) off the diagonal, the exact
+// r_j on it (R10); ‖r_j‖² per column (fixed-shape reduction).
+__global__ void __launch_bounds__(BS)
+    k_form_R(const int32_t* __restrict__ planes, long long pstride, int rows, const __grid_constant__ RecombPlan rp,
+             const int32_t* __restrict__ g, int scale8, int col0, const double* __restrict__ r_hi,
+             const double* __restrict__ r_lo, double* __restrict__ R, long long ldr, double* __restrict__ nR2) {
+  __shared__ double sh[BS / 32];
+  const int j = blockIdx.x;
+  const int jg = col0 + j;
+  const int Lj = rp.tile_budgets ? rp.tileL[j / 256] : rp.L;
+  const int eb = g[jg] + scale8;
+  double s2 = 0.0;
+  for_column(planes, pstride, static_cast<long long>(j) * rows, rows, rp, Lj, [&](int i) { return g[i] + eb; },
+             [&](int i, const dd& v) {
+               const double r = (i == jg) ? (r_hi[jg] + r_lo[jg]) : -(v.hi + v.lo);
+               R[static_cast<long long>(j) * ldr + i] = r;
+               s2 = __fma_rn(r, r, s2);
+             });
+  s2 = block_sum(s2, sh);
+  if (threadIdx.x == 0) nR2[j] = s2;
 }
 
 template <int NG>
@@ -810,11 +835,11 @@ void launch_recombine_V(const int32_t* planes, long long pstride, int rows, int 
 void launch_recombine_E(const int32_t* planes, long long pstride, int rows, int cols, const RecombPlan& rp,
                         const int32_t* ellA, const int32_t* ellB, int scale8, const double* r_hi, const double* lam,
                         const int32_t* gX, int col0, double* Ep, long long lde, double* nrm2, int* eE_max,
-                        int32_t* eE_col, int* err, const EdgeOut& eo, cudaStream_t s) {
+                        int32_t* eE_col, int* err, const EdgeOut& eo, double* nW2, cudaStream_t s) {
   const int tma = tma_ok(rp, planes, pstride, rows, lam, 0, nullptr, 0) && (reinterpret_cast<uintptr_t>(ellA) & 15) == 0;
 #define OZR_RE(NG_)                                                                                            \
   k_recombine_E<NG_><<<cols, BS, tma ? kTmaSmem : 0, s>>>(planes, pstride, rows, rp, ellA, ellB, scale8, r_hi, lam, gX, \
-                                                          col0, Ep, lde, nrm2, eE_max, eE_col, err, eo, tma)
+                                                          col0, Ep, lde, nrm2, eE_max, eE_col, err, eo, tma, nW2)
   if (tma && rp.ngroups <= 4) OZR_RE(4);
   else if (tma && rp.ngroups <= 8) OZR_RE(8);
   else OZR_RE(12);
@@ -831,6 +856,11 @@ void launch_final(const int32_t* planes, long long pstride, int rows, int cols, 
   else if (tma && rp.ngroups <= 8) OZR_FI(8);
   else OZR_FI(12);
 #undef OZR_FI
+}
+void launch_form_R(const int32_t* planes, long long pstride, int rows, int cols, const RecombPlan& rp, const int32_t* g,
+                   int scale8, int col0, const double* r_hi, const double* r_lo, double* R, long long ldr, double* nR2,
+                   cudaStream_t s) {
+  k_form_R<<<cols, BS, 0, s>>>(planes, pstride, rows, rp, g, scale8, col0, r_hi, r_lo, R, ldr, nR2);
 }
 void launch_iota(int* p, int n, cudaStream_t s) { k_iota<<<(n + 255) / 256, 256, 0, s>>>(p, n); }
 void launch_uf_flatten(int* parent, int n, cudaStream_t s) { k_uf_flatten<<<(n + 255) / 256, 256, 0, s>>>(parent, n); }

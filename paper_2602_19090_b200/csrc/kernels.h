@@ -57,7 +57,12 @@ void launch_uf_flatten(int* parent, int n, cudaStream_t s);  // parent[i] ← ro
 void launch_recombine_E(const int32_t* planes, long long pstride, int rows, int cols, const RecombPlan& rp,
                         const int32_t* ellA, const int32_t* ellB, int scale8, const double* r_hi, const double* lam,
                         const int32_t* gX, int col0, double* Ep, long long lde, double* nrm2, int* eE_max,
-                        int32_t* eE_col, int* err, const EdgeOut& eo, cudaStream_t s);
+                        int32_t* eE_col, int* err, const EdgeOut& eo, double* nW2 /* nullable: ‖w_j‖² */,
+                        cudaStream_t s);
+// form_R: R = I − X̂^(1)ᵀX̂^(1) (local columns) from the G slice-product planes, ‖r_j‖² in nR2[j]
+void launch_form_R(const int32_t* planes, long long pstride, int rows, int cols, const RecombPlan& rp, const int32_t* g,
+                   int scale8, int col0, const double* r_hi, const double* r_lo, double* R, long long ldr, double* nR2,
+                   cudaStream_t s);
 
 // Cluster sub-solve (cluster.cu). Groups g = 0..ngroups-1 with members mem[goff[g] .. goff[g]+gm[g]) (global
 // column indices, ascending (λ̂, index)); per-group m x m workspaces at offset gsq[g] (Σ m²) in M/R/K/V/Z.

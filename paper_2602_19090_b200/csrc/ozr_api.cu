@@ -44,7 +44,9 @@ struct ozr_ctx_s {
   std::string err;
   std::vector<DevBuf> bufs;
   std::vector<int> last_members, last_offsets{0};  // unresolved groups of the last sweep (R13)
-  cudaEvent_t ev[8];
+  cudaEvent_t ev[10];
+  const double* last_R = nullptr;  // form_R: R of the last sweep (workspace), n x nl
+  int64_t last_R_n = 0, last_R_nl = 0;
   cudaStream_t xstream = nullptr;  // side stream of the digit all-gather (overlaps the V product)
   cudaEvent_t ev_sync = nullptr;   // the host waits on this instead of the whole stream
   cudaEvent_t xev[2];
@@ -110,7 +112,7 @@ namespace {
 enum Slot {
   S_ADIG, S_AELL, S_W, S_X1, S_XDIG, S_XDIGT, S_G, S_SH, S_SL, S_RH, S_RL, S_PLANES, S_VH, S_VL, S_LAM, S_ER,
   S_ERR, S_EMAX, S_RDIG, S_RELL, S_EP, S_NRM2, S_NU2, S_WNEXT, S_ZEROELL, S_TMP1, S_TMP2, S_BELL, S_AT, S_ONES,
-  S_EDGES, S_ECOUNT, S_CINT, S_CDBL, S_CM, S_CR, S_CK, S_CV, S_CZ, S_CT, S_CSCR, S_CFLAG, S_SCAL, S_UFALL, S_CPART, S_GCNT, S_WA
+  S_EDGES, S_ECOUNT, S_CINT, S_CDBL, S_CM, S_CR, S_CK, S_CV, S_CZ, S_CT, S_CSCR, S_CFLAG, S_SCAL, S_UFALL, S_CPART, S_GCNT, S_WA, S_GPLANES, S_RMAT, S_NR2, S_NW2
 };
 
 ozr_status fail(ozr_ctx c, ozr_status st, const char* fmt, ...) {
@@ -400,7 +402,7 @@ double sum_pow2_2c(const std::vector<double>& w) {
   return s;
 }
 
-// Slice GEMM `idx` (0: V, 1: W, 2: U) of a sweep, bracketed by events ev[2+2idx], ev[3+2idx]
+// Slice GEMM `idx` (0: V, 1: W, 2: U, 3: G = X̂ᵀX̂ with form_R) of a sweep, bracketed by events ev[2+2idx], ev[3+2idx]
 // (read after the sweep's final synchronisation; no extra host sync here).
 ozr_status run_gemm(ozr_ctx ctx, const DigitOperand& A, const DigitOperand& B, int M, int N, int K,
                     const PairTable& pt, int32_t* planes, int idx) {
@@ -594,6 +596,9 @@ ozr_status sweep(ozr_ctx ctx, Exchange* ex, const double* A, int64_t n, int64_t 
   int beta = std::min(std::max(beta_raw, kBetaMin), kBetaMax);
   if (!P.truncate) beta = kBetaMin;
   const int kx = kx_for_beta(beta);
+  // R8: an X̂^(1) operand enters the dropped-pair tail bound with exponent c + slack, slack = S_kx − (53 − β)
+  // (0..7: its leading digit is not normalised like the fixed-point splits' digits)
+  const int xslack = (8 * (kx - 1) + 6) - (53 - beta);
   int cmax = -100000;
   for (double x : hw)
     if (x != 0.0) cmax = std::max(cmax, ceil_log2_host(x));
@@ -615,7 +620,9 @@ ozr_status sweep(ozr_ctx ctx, Exchange* ex, const double* A, int64_t n, int64_t 
   std::vector<int> c_col(nl);
   for (int64_t j = 0; j < nl; ++j) {
     tau_col[j] = P.theta_V * delta_p * (P.tile_budgets ? gaps_prev[col0 + j] : gap);
-    c_col[j] = hw[col0 + j] != 0.0 ? ceil_log2_host(hw[col0 + j]) : -100000;
+    // the X̂^(1) digits of column j sit on the grid 2^{g_j}, g_j = c_j + β − 53, with S_kx ≥ 53 − β bits:
+    // for the tail bound of choose_L their "line exponent" is g_j + S_kx = c_j + slack (R8)
+    c_col[j] = hw[col0 + j] != 0.0 ? ceil_log2_host(hw[col0 + j]) + xslack : -100000;
   }
   unsigned char tileLV[kMaxNTiles];
   double avg_pairs_V = 0.0;
@@ -674,6 +681,28 @@ ozr_status sweep(ozr_ctx ctx, Exchange* ex, const double* A, int64_t n, int64_t 
   ctx->mark("gemmV");
   // join the digit exchange before any other collective (λ̂ below) and before reading other ranks' digits
   if (ex) OZR_CK(cudaStreamWaitEvent(s, ctx->xev[1], 0), "wait exchange");
+  // optional: R = I − X̂^(1)ᵀX̂^(1) (the R/S form's first product) to θ_W·δ' absolute
+  double* nR2 = nullptr;
+  if (P.form_R) {
+    const int LG = std::min(choose_L(kx, kx, n, cmax + xslack, cmax + xslack, 0.5 * P.theta_W * delta_p), 2 * kx);
+    std::vector<Group> gG = plan_groups(kx, kx, LG, n);
+    PairTable ptG;
+    RecombPlan rpG;
+    if (!make_tables(gG, LG, n, ptG, rpG)) return fail(ctx, OZR_ERR_RANGE, "R plan too large");
+    int32_t* planesG = ctx->ws<int32_t>(S_GPLANES, gG.size() * nnl);
+    double* Rm = ctx->ws<double>(S_RMAT, nnl);
+    nR2 = ctx->ws<double>(S_NR2, n);
+    OZR_ALLOC(planesG); OZR_ALLOC(Rm); OZR_ALLOC(nR2);
+    OZR_X(run_gemm(ctx, opX, opXJ, N, NL, N, ptG, planesG, 3));
+    launch_form_R(planesG, nnl, N, NL, rpG, g, 8 * (2 * kx - LG), static_cast<int>(col0), rh, rl, Rm, n, nR2 + col0, s);
+    OZR_CK(cudaGetLastError(), "form R");
+    rep.pairs_G = count_pairs(gG);
+    ops += 2.0 * n * n * nl * rep.pairs_G;
+    ctx->last_R = Rm;
+    ctx->last_R_n = n;
+    ctx->last_R_nl = nl;
+    ctx->mark("gemmG+R");
+  }
   const double pV = tilesV ? avg_pairs_V : static_cast<double>(count_pairs(gV));
   rep.pairs_V = static_cast<int>(std::lround(pV));
   ops += 2.0 * n * n * nl * pV;
@@ -731,7 +760,7 @@ ozr_status sweep(ozr_ctx ctx, Exchange* ex, const double* A, int64_t n, int64_t 
   }
   unsigned char tileLW[kMaxNTiles];
   double avg_pairs_W = 0.0;
-  int LW = tile_budgets(kx, kR, n, cmax, eR_col, tau_col, tileLW, &avg_pairs_W);
+  int LW = tile_budgets(kx, kR, n, cmax + xslack, eR_col, tau_col, tileLW, &avg_pairs_W);
   if (P.L_W > 0) LW = P.L_W;
   LW = std::min(LW, kx + kR);
   std::vector<Group> gW = plan_groups(kx, kR, LW, n);
@@ -763,8 +792,10 @@ ozr_status sweep(ozr_ctx ctx, Exchange* ex, const double* A, int64_t n, int64_t 
   OZR_CK(cudaMemsetAsync(ecount, 0, sizeof(int), s), "memset");
   if (P.cluster_mode) launch_iota(uf, N, s);
   const EdgeOut eo{P.cluster_mode, P.kappa, uf, ecount};
+  double* nW2 = P.form_R ? ctx->ws<double>(S_NW2, n) : nullptr;
+  if (P.form_R) OZR_ALLOC(nW2);
   launch_recombine_E(planes, nnl, N, NL, rp, g, rell, 8 * (kx + kR - LW), rh + col0, lam, g, static_cast<int>(col0), Ep, n,
-                     nrm2 + col0, demax, eR, derr, eo, s);
+                     nrm2 + col0, demax, eR, derr, eo, nW2 ? nW2 + col0 : nullptr, s);
   OZR_CK(cudaGetLastError(), "recombine E");
   ctx->mark("recombE");
   int eEmax = 0, nedges = 0;
@@ -965,6 +996,15 @@ ozr_status sweep(ozr_ctx ctx, Exchange* ex, const double* A, int64_t n, int64_t 
   ctx->mark("final");
   OZR_X(xgather(nu2, nl * sizeof(double)));
   OZR_X(xgather(nrm2, nl * sizeof(double)));
+  std::vector<double> hR2, hW2;
+  if (P.form_R) {
+    OZR_X(xgather(nR2, nl * sizeof(double)));
+    OZR_X(xgather(nW2, nl * sizeof(double)));
+    hR2.resize(n);
+    hW2.resize(n);
+    OZR_CK(cudaMemcpyAsync(hR2.data(), nR2, n * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H");
+    OZR_CK(cudaMemcpyAsync(hW2.data(), nW2, n * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H");
+  }
   OZR_CK(cudaMemcpyAsync(lambda, lam, n * sizeof(double), cudaMemcpyDeviceToDevice, s), "copy lambda");
   cudaEventRecord(ctx->ev[1], s);
   std::vector<double> hnu(n), hnrm(n);
@@ -978,10 +1018,20 @@ ozr_status sweep(ozr_ctx ctx, Exchange* ex, const double* A, int64_t n, int64_t 
   }
   float tot = 0.f;
   cudaEventElapsedTime(&tot, ctx->ev[0], ctx->ev[1]);
-  for (int q = 0; q < 3; ++q) {
+  for (int q = 0; q < (P.form_R ? 4 : 3); ++q) {
     float t = 0.f;
     cudaEventElapsedTime(&t, ctx->ev[2 + 2 * q], ctx->ev[3 + 2 * q]);
     gemm_ms += t;
+  }
+  if (P.form_R) {
+    double r2 = 0.0, w2 = 0.0;
+    for (int64_t j = 0; j < n; ++j) {
+      r2 += hR2[j];
+      w2 += hW2[j];
+    }
+    rep.normR_fro = std::sqrt(r2);
+    rep.normW_fro = std::sqrt(w2);
+    rep.omega_oa = 2.0 * (rep.normW_fro + 2.0 * maxlam * rep.normR_fro);
   }
   st.have_w = true;
   rep.net_update = std::sqrt(nu);
@@ -1037,7 +1087,7 @@ ozr_status ozr_create(ozr_ctx* out, int device, void* stream, int64_t n_max) {
   ozr_ctx c = new ozr_ctx_s();
   c->device = device;
   c->stream = static_cast<cudaStream_t>(stream);
-  for (int i = 0; i < 8; ++i) cudaEventCreate(&c->ev[i]);
+  for (int i = 0; i < 10; ++i) cudaEventCreate(&c->ev[i]);
   cudaStreamCreateWithFlags(&c->xstream, cudaStreamNonBlocking);
   cudaEventCreateWithFlags(&c->ev_sync, cudaEventDisableTiming);
   for (int i = 0; i < 2; ++i) cudaEventCreateWithFlags(&c->xev[i], cudaEventDisableTiming);
@@ -1055,7 +1105,7 @@ void ozr_destroy(ozr_ctx ctx) {
   for (auto& b : ctx->bufs)
     if (b.p) cudaFree(b.p);
   if (ctx->events)
-    for (int i = 0; i < 8; ++i) cudaEventDestroy(ctx->ev[i]);
+    for (int i = 0; i < 10; ++i) cudaEventDestroy(ctx->ev[i]);
   for (int i = 0; i < 2; ++i) cudaEventDestroy(ctx->xev[i]);
   if (ctx->xstream) cudaStreamDestroy(ctx->xstream);
   if (ctx->ev_sync) cudaEventDestroy(ctx->ev_sync);
@@ -1082,6 +1132,7 @@ void ozr_params_default(ozr_params* p) {
   p->tile_budgets = 1;
   p->kappa = 0x1p-10;
   p->max_cluster = 4096;
+  p->form_R = 0;
 }
 
 ozr_status ozr_split(ozr_ctx ctx, const double* M, const double* M_lo, int64_t rows, int64_t cols, int64_t ldm,
@@ -1150,6 +1201,15 @@ ozr_status ozr_split(ozr_ctx ctx, const double* M, const double* M_lo, int64_t r
   OZR_CK(cudaGetLastError(), "ozr_split");
   if (k_out) *k_out = k;
   return read_err(ctx, derr);
+}
+
+ozr_status ozr_last_R(ozr_ctx ctx, double* R, int64_t ldr) {
+  if (!ctx || !R || !ctx->last_R || ldr < ctx->last_R_n) return OZR_ERR_ARG;
+  OZR_CK(cudaMemcpy2DAsync(R, ldr * sizeof(double), ctx->last_R, ctx->last_R_n * sizeof(double),
+                           ctx->last_R_n * sizeof(double), ctx->last_R_nl, cudaMemcpyDeviceToDevice, ctx->stream),
+         "copy R");
+  OZR_CK(cudaStreamSynchronize(ctx->stream), "sync");
+  return OZR_OK;
 }
 
 ozr_status ozr_last_clusters(ozr_ctx ctx, int* members, int max_members, int* offsets, int max_groups, int* ngroups) {

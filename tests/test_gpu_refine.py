@@ -83,3 +83,23 @@ def test_refine_step_errors(ctx):
     with pytest.raises(ozr.OzrError) as e:   # equal eigenvalue estimates, cluster branch off
         _gpu_sweep(ctx, A, X, np.array([1.0, 1.0, 3, 4]), 1e-10, cluster_mode=0)
     assert e.value.status == 4
+
+
+@pytest.mark.parametrize("cfg,n,start", [("c2", 512, "fp64"), ("c3", 1024, "fp64")])
+def test_form_R_matches_oracle(ctx, cfg, n, start):
+    """form_R = 1: R = I − X̂^(1)ᵀX̂^(1) by INT8 slice products (the R/S form's first product)
+    against the oracle's double-double product, and the reported ‖R‖_F, ‖W‖_F and OA threshold ω."""
+    import paper_2602_19090_b200 as ozr
+    A, lam0, X0 = _case(cfg, n, start)
+    delta = 1e-12
+    th = 1e-16 / delta
+    p = ozr.default_params(delta=delta, form_R=1, theta_V=th, theta_W=th, theta_U=th)
+    Xd, ld = to_dev(X0), vec_dev(lam0)
+    rep = ozr.ozr_refine_step(ctx, to_dev(A), Xd, ld, p)
+    Rg = to_np(ozr.ozr_last_R(ctx, n))
+    Xo, lo, info = orf.sweep(A, X0, lam0, delta, theta=p.theta, form_R=True)
+    assert rep["beta"] == info["beta"] and rep["pairs_G"] > 0
+    assert np.max(np.abs(Rg - info["R"])) <= 1e-16
+    assert abs(rep["normR_fro"] - info["normR_fro"]) <= 1e-6 * info["normR_fro"]
+    assert abs(rep["normW_fro"] - info["normW_fro"]) <= 1e-6 * info["normW_fro"] + 1e-30
+    assert rep["omega_oa"] == pytest.approx(2 * (rep["normW_fro"] + 2 * np.max(np.abs(lam0)) * rep["normR_fro"]))
