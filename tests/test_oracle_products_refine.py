@@ -176,3 +176,13 @@ def test_sweep_columns_matches_sweep():
     assert beta == info["beta"]
     assert np.max(np.abs(XJ - Xn[:, J])) < 1e-15
     assert np.max(np.abs(lamJ - lam[J])) < 1e-15
+
+
+def test_form_R_and_W_vanish_on_exact_eigensystem():
+    """Pin of the oracle's R = I − X̂ᵀX̂ and W (form_R): on the Householder family A = H diag(λ) H with
+    X̂ = H EXACTLY, untruncated, both are exactly zero and every λ̂ is exact."""
+    A, lam, X, H, lam_cols = W.householder_exact(6, lam_bits=12, seed=5)
+    Xn, lamn, info = orf.sweep(A, X, lam, 1e-12, truncate=False, form_R=True)
+    assert np.all(info["R"] == 0.0) and info["normR_fro"] == 0.0
+    assert info["normW_fro"] == 0.0
+    assert np.array_equal(lamn, lam) and np.array_equal(Xn, X)
