@@ -1056,7 +1056,7 @@ ozr_status sweep(ozr_ctx ctx, Exchange* ex, const double* A, int64_t n, int64_t 
   rep.exchanges = nexch;
   ctx->dump();
   // kernels of this sweep: [colmax] x1_split transpose GEMM recombine_V split GEMM recombine_E split GEMM final
-  rep.launches = (fresh_w ? 1 : 0) + 10 + cluster_launches;
+  rep.launches = (fresh_w ? 1 : 0) + 10 + cluster_launches + (new_A ? 2 : 0) + (P.form_R ? 2 : 0);
 #undef OZR_X
   return OZR_OK;
 }
