@@ -196,7 +196,7 @@ def main():
     comm = None
     if ws > 1:
         # one problem, block-column partition: rank 0 builds it, every rank receives A, X̂₀, λ̂₀
-        from paper_2602_19090_b200.dist import comm_from_process_group, partition
+        from paper_2602_19090_b200.dist import broadcast_tensor, comm_from_process_group, partition
         if rank == 0:
             A, lam0, X0, cfg = W.make_config_torch(name, dev, n=args.n or None)
         else:
@@ -208,7 +208,7 @@ def main():
             X0 = ozr.colmajor(torch.empty((nn_, nn_), dtype=torch.float64, device=dev))
             lam0 = torch.empty(nn_, dtype=torch.float64, device=dev)
         for t_ in (A, X0, lam0):
-            dist.broadcast(t_, src=0)
+            broadcast_tensor(t_, src=0)
         comm = comm_from_process_group(local)
         col0, nl = partition(cfg["n"], ws, rank)
     else:
@@ -358,7 +358,10 @@ def main():
                "time_to_target": ttt}
         print(json.dumps(out))
     ctx.close()
+    if comm is not None:
+        comm.close()
     if ws > 1:
+        dist.barrier()
         dist.destroy_process_group()
     return 0
 

@@ -26,3 +26,18 @@ def comm_from_process_group(device, group=None):
     rank, ws = dist.get_rank(group), dist.get_world_size(group)
     uid = broadcast_id(ozr_comm_nccl_id() if rank == 0 else None, group)
     return ozr_comm_create_nccl(uid, ws, rank, device)
+
+
+def broadcast_tensor(t, src=0, group=None):
+    """torch.distributed.broadcast of a vector or a COLUMN-MAJOR matrix (stride (1, ld), the library's
+    layout): collectives need contiguous tensors, and the transpose of a column-major matrix is a
+    contiguous row-major view of the same memory."""
+    import torch.distributed as dist
+    if t.dim() == 2 and not t.is_contiguous():
+        v = t.t()
+        if not v.is_contiguous():
+            raise ValueError("expected a contiguous column-major matrix")
+        dist.broadcast(v, src=src, group=group)
+    else:
+        dist.broadcast(t, src=src, group=group)
+    return t

@@ -12,7 +12,7 @@ import torch.multiprocessing as mp
 
 import workloads as W
 from oracle import refine as orf
-from paper_2602_19090_b200.dist import broadcast_id, partition
+from paper_2602_19090_b200.dist import broadcast_id, broadcast_tensor, partition
 
 
 def _free_port():
@@ -94,3 +94,23 @@ def test_host_group_comm_on_cpu():
     assert [c.rank for c in cs] == [0, 1, 2, 3] and {c.size for c in cs} == {4}
     for c in cs:
         c.close()
+
+
+def _bcast_colmajor(rank, ws):
+    import torch
+    n = 6
+    t = torch.empty((n, n), dtype=torch.float64).t()   # column-major view (stride (1, n)), as bench.py holds A
+    if rank == 0:
+        t.copy_(torch.arange(n * n, dtype=torch.float64).reshape(n, n))
+    broadcast_tensor(t, src=0)
+    lam = torch.arange(n, dtype=torch.float64) if rank == 0 else torch.zeros(n, dtype=torch.float64)
+    broadcast_tensor(lam, src=0)
+    return t.numpy().copy(), lam.numpy().copy(), tuple(t.stride())
+
+
+def test_broadcast_colmajor_gloo():
+    """bench.py's N > 1 set-up broadcasts the column-major A and X̂₀ from rank 0 (collectives need
+    contiguous tensors; the helper broadcasts the contiguous transposed view of the same memory)."""
+    (a0, l0, s0), (a1, l1, s1) = _run(_bcast_colmajor)
+    assert np.array_equal(a0, a1) and np.array_equal(l0, l1)
+    assert np.array_equal(a1, np.arange(36, dtype=np.float64).reshape(6, 6)) and s1 == (1, 6)
