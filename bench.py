@@ -154,7 +154,7 @@ def run_reference(args):
                             "sample": f"each step: oracle sweep on {len(J)} of {n_eff} columns of the {name} "
                                       f"recipe at n={n_eff}"},
            "e2e": {"value": val, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(out))
+    emit(out)
     return 0
 
 
@@ -164,7 +164,24 @@ def _describe(cfg, n):
            f"delta={cfg['delta']:.0e}"
 
 
+_JSON_FD = None
+
+
+def emit(obj):
+    """The ONE JSON line on the original stdout (everything else, e.g. NCCL banners, goes to stderr)."""
+    line = (json.dumps(obj) + "\n").encode()
+    if _JSON_FD is not None:
+        os.write(_JSON_FD, line)
+    else:
+        sys.stdout.write(line.decode())
+        sys.stdout.flush()
+
+
 def main():
+    global _JSON_FD
+    sys.stdout.flush()
+    _JSON_FD = os.dup(1)
+    os.dup2(2, 1)  # C-level prints (NCCL's version banner, ...) must not precede the JSON line
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
@@ -187,14 +204,19 @@ def main():
     ws, rank, local = _dist()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if ws > 1:
-        dist.init_process_group("nccl", device_id=dev)
+    # OZR_BENCH_DIST=1 runs the partitioned (N > 1) code path even on one rank, through a real 1-rank
+    # NCCL communicator — the way to exercise it on a single GPU
+    dist_mode = ws > 1 or os.environ.get("OZR_BENCH_DIST") == "1"
+    if dist_mode:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29541")
+        dist.init_process_group("nccl", device_id=dev, rank=rank, world_size=ws)
     import paper_2602_19090_b200 as ozr
     import workloads as W
 
     name = args.config
     comm = None
-    if ws > 1:
+    if dist_mode:
         # one problem, block-column partition: rank 0 builds it, every rank receives A, X̂₀, λ̂₀
         from paper_2602_19090_b200.dist import broadcast_tensor, comm_from_process_group, partition
         if rank == 0:
@@ -237,7 +259,7 @@ def main():
     sampler = ClockSampler(local)
     sampler.start()
     time.sleep(0.3)
-    if ws > 1:
+    if dist_mode:
         dist.barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -247,11 +269,11 @@ def main():
         reps.append(step())
     e1.record()
     torch.cuda.synchronize()
-    if ws > 1:
+    if dist_mode:
         dist.barrier()
     clocks = sampler.stop()
     ms = e0.elapsed_time(e1)
-    if ws > 1:
+    if dist_mode:
         t = torch.tensor([ms], device=dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
@@ -308,7 +330,7 @@ def main():
     hl = torch.empty_like(hl0).pin_memory()
     Ad = ozr.colmajor(torch.empty_like(A))
     torch.cuda.synchronize()
-    if ws > 1:
+    if dist_mode:
         dist.barrier()
     s0 = torch.cuda.Event(enable_timing=True)
     s1 = torch.cuda.Event(enable_timing=True)
@@ -323,7 +345,7 @@ def main():
     s1.record()
     torch.cuda.synchronize()
     e2e_ms = s0.elapsed_time(s1) / args.e2e_steps
-    if ws > 1:
+    if dist_mode:
         t = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t.item())
@@ -348,7 +370,7 @@ def main():
                           "mode": "proposed (X̂ truncated to X̂^(1))" if args.truncate else
                                   "untruncated X̂ (prior-work analogue)",
                           "parallelism": f"block-column partition x{ws} (NCCL all-gather of X^(1) digits per sweep)"
-                          if ws > 1 else "1 GPU",
+                          if dist_mode else "1 GPU",
                           "l2": "inputs larger than L2 (A + X = %.1f GiB per rank, L2 126 MB)" % (2 * n * n * 8 / 2 ** 30),
                           "flops_per_step": "3 x 2n^3 (V=AX, W=X^T Res, U=X E)",
                           "sweep": {k: r0[k] for k in ("beta", "alpha", "kX", "kA", "kR", "kE", "L_V", "L_W", "L_U",
@@ -356,11 +378,11 @@ def main():
                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                "gpu_launches": int(sum(r["launches"] for r in reps)), "clocks": clocks,
                "time_to_target": ttt}
-        print(json.dumps(out))
+        emit(out)
     ctx.close()
     if comm is not None:
         comm.close()
-    if ws > 1:
+    if dist_mode:
         dist.barrier()
         dist.destroy_process_group()
     return 0
