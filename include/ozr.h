@@ -123,11 +123,18 @@ typedef struct {
                            in span(X̂^(1)_J) (R13) [default]                          */
   int tile_budgets;  /* 1: per-256-column pair budgets from the local gaps gap_j (R8b) [default]  */
   double kappa;      /* cluster_mode 1: linearisation threshold κ on |ẽ_ij| (default 2^-10)     */
-  int max_cluster;   /* cluster_mode 1: largest group solved (default 4096; larger → OZR_ERR_RANGE) */
+  int max_cluster;   /* cluster_mode 1: largest group solved (default 16384; larger → OZR_ERR_RANGE) */
   int form_R;        /* 1: also form R = I − X̂^(1)ᵀX̂^(1) by INT8 slice products (to θ_W·δ' absolute; the
                         R/S form's first product, PAPER.md:241-250 — Algorithm 1's W-form needs only its
                         diagonal, which is always exact); reports ‖R‖_F and the OA threshold ω, and
                         ozr_last_R returns R. Default 0 */
+  int dense_cluster; /* cluster_mode 1: groups of at least this many columns are solved by a dense symmetric
+                        eigensolver (cuSOLVER syevd, loaded on first use; OZR_ERR_CUDA if it cannot be
+                        loaded) instead of the parallel Jacobi; same K, same conventions (R13).
+                        Default 1024 */
+  int max_escalations; /* ozr_refine_to_tol: when the net update stagnates above δ (the truncated iteration's
+                          noise floor, R12), continue with θ × 16 (β two bits lower) at most this many
+                          times before OZR_ERR_NOT_CONVERGED. Default 2 */
 } ozr_params;
 
 void ozr_params_default(ozr_params* p);
@@ -152,6 +159,7 @@ typedef struct {
   double normR_fro, normW_fro;      /* form_R: ‖R‖_F, ‖W‖_F                                            */
   double omega_oa;                  /* form_R: ω = 2(‖W‖_F + 2·max|λ̂|·‖R‖_F), the Frobenius form of the
                                        OA-2018 cluster threshold 2(‖S − D̃‖ + ‖A‖‖R‖) (diagnostic, R13) */
+  double theta;                     /* the θ this sweep used (params.theta, × 16 per escalation)       */
 } ozr_step_report;
 
 /* One sweep on columns [0, n): A (n x n, symmetric — only its columns are read), X (n x n, in/out:

@@ -217,24 +217,28 @@ def sweep(A, X, lam_prev, delta, theta=THETA_DEFAULT, beta=None, beta_mode="dens
 
 
 def refine_to_tol(A, X0, lam0, delta, theta=THETA_DEFAULT, max_sweeps=6, beta_mode="dense", xi=None, callback=None,
-                  cluster_mode=1, kappa=KAPPA_DEFAULT):
+                  cluster_mode=1, kappa=KAPPA_DEFAULT, max_escalations=2, truncate=True):
     """Driver (reading R12): repeat sweeps; stop after sweep k when ν_k = ‖X_k − X_{k−1}‖_F ≤ δ, or when
     the paper's error model predicts ‖X − X_k‖ ≲ ν_k² max|λ̂| / (n gap) ≤ δ (eq. assume2 / gamma,
-    PAPER.md:341-373 with ξ = n as in §4.1), or at stagnation (ν_k > ν_{k−1}/2), or at max_sweeps."""
+    PAPER.md:341-373 with ξ = n as in §4.1), or at stagnation (ν_k > ν_{k−1}/2 between two sweeps without
+    unresolved groups: a Rayleigh–Ritz sub-solve (R13) rotates its group's columns, so its ν is not a
+    contraction measure), or at max_sweeps. Stagnation above δ with truncation on first escalates θ ← 16θ
+    (β two bits lower: the truncated iteration's noise floor is quadratic in the truncation) at most
+    max_escalations times."""
     X, lam = np.asarray(X0, dtype=np.float64), np.asarray(lam0, dtype=np.float64)
     n = X.shape[0]
     hist = []
     nu_prev = None
     for k in range(max_sweeps):
         Xn, lamn, info = sweep(A, X, lam, delta, theta, beta_mode=beta_mode, xi=xi, cluster_mode=cluster_mode,
-                               kappa=kappa)
+                               kappa=kappa, truncate=truncate)
         nu = info["net_update"]
         ls = np.sort(lamn)
         d = np.diff(ls)
         gpos = np.min(d[d > 0]) if np.any(d > 0) else max(np.max(np.abs(lamn)) * U, 1e-300)
         pred = nu * nu * np.max(np.abs(lamn)) / (n * gpos)
         rec = dict(sweep=k + 1, beta=info["beta"], alpha=info["alpha"], net_update=nu, predicted=pred,
-                   normE_fro=info["normE_fro"])
+                   normE_fro=info["normE_fro"], theta=theta)
         X, lam = Xn, lamn
         if callback:
             rec.update(callback(X, lam))
@@ -242,7 +246,15 @@ def refine_to_tol(A, X0, lam0, delta, theta=THETA_DEFAULT, max_sweeps=6, beta_mo
         if nu <= delta or pred <= delta:
             rec["stop"] = "converged"
             break
+        if info["clusters"]:
+            nu_prev = None
+            continue
         if nu_prev is not None and nu > nu_prev / 2:
+            if truncate and max_escalations > 0:
+                max_escalations -= 1
+                theta = theta * 16.0
+                nu_prev = None
+                continue
             rec["stop"] = "stagnation"
             break
         nu_prev = nu
@@ -251,12 +263,42 @@ def refine_to_tol(A, X0, lam0, delta, theta=THETA_DEFAULT, max_sweeps=6, beta_mo
 
 # ----------------------------------------------------------------------------- reference solution
 
-def reference_eigvecs(A, X0, lam0, tol=1e-27, max_sweeps=10):
+def _reference_rr(E, lh, ll, J, Sh, Sl, Gh, Gl, R):
+    """Rayleigh–Ritz of one unresolved group J inside reference_eigvecs ("use the cluster
+    branch when [the first-order correction fails]"; the construction of reading R13 on the dd products of
+    the R/S form): μ = mean λ̃_J, M = S_JJ − μG_JJ (dd, rounded once), K = C·(M + Mᵀ)/2·C with
+    C = I + R_JJ/2, K = YΘYᵀ by LAPACK (numpy.linalg.eigh; its u‖K‖/gap_K error is removed by the dd
+    sweeps that follow), Z = CY: Ẽ_JJ ← Z − I, Ẽ_{i,J} ← Ẽ_{i,J}Z (i ∉ J), λ̃_J ← μ + Θ."""
+    J = np.asarray(J)
+    m = len(J)
+    mu = float(np.mean(lh[J]))
+    ix = np.ix_(J, J)
+    ph, pl = two_prod(Gh[ix], mu)
+    M = (Sh[ix] - ph) + (Sl[ix] - pl - Gl[ix] * mu)
+    C = np.eye(m) + 0.5 * R[ix]
+    K = C @ ((M + M.T) * 0.5) @ C
+    th, Y = np.linalg.eigh((K + K.T) * 0.5)
+    for k in range(m):
+        piv = Y[k, k] if Y[k, k] != 0 else Y[np.argmax(np.abs(Y[:, k])), k]
+        if piv < 0:
+            Y[:, k] = -Y[:, k]
+    Z = C @ Y
+    notJ = np.setdiff1d(np.arange(E.shape[0]), J)
+    E[np.ix_(notJ, J)] = E[np.ix_(notJ, J)] @ Z
+    E[ix] = Z - np.eye(m)
+    lh[J] = mu + th
+    ll[J] = 0.0
+
+
+def reference_eigvecs(A, X0, lam0, tol=1e-27, max_sweeps=10, cluster_kappa=None):
     """Reference eigenvectors of the STORED A (PAPER.md:62 uses a pseudo-quadruple reference): the
     Ogita–Aishima iteration (the R/S form ẽ_ij = (s_ij + λ̃_j r_ij)/(λ̃_j − λ̃_i))
     with X̂ kept in double-double and every product in double-double, untruncated, from an LAPACK
-    start, until ‖Ẽ‖_F ≤ tol. Returns (Xh, Xl, λh, λl, history). Certified separately by
-    residual_certificate() and pinned against __float128 Jacobi (n ≤ 32) and exact families."""
+    start, until ‖Ẽ‖_F ≤ tol. cluster_kappa (None: off): groups of pairs with |ẽ_ij| > cluster_kappa
+    (unresolved_groups) get a Rayleigh–Ritz step (_reference_rr) — needed where the LAPACK start is not in
+    the linear regime (BASELINE c4: cnd 1e14, gaps below u‖A‖). Returns (Xh, Xl, λh, λl, history).
+    Certified separately by residual_certificate() and pinned against __float128 Jacobi (n ≤ 32) and
+    exact families."""
     A = np.asarray(A, dtype=np.float64)
     n = A.shape[0]
     Xh, Xl = np.array(X0, dtype=np.float64), np.zeros((n, n))
@@ -281,6 +323,9 @@ def reference_eigvecs(A, X0, lam0, tol=1e-27, max_sweeps=10):
         off = ~np.eye(n, dtype=bool)
         E = np.where(off, (Nh + Nl) / np.where(off, dlam, 1.0), 0.0)
         E[np.arange(n), np.arange(n)] = np.diag(R) / 2
+        if cluster_kappa is not None:
+            for J in unresolved_groups(E, lh, cluster_kappa):
+                _reference_rr(E, lh, ll, J, Sh, Sl, Gh, Gl, R)
         Uh, Ul = _clib.dd_gemm_nt(Xh, np.ascontiguousarray(E.T), Xl, None)  # U = X Ẽ
         Xh, Xl = dd_add(Xh, Xl, Uh, Ul)
         nE = float(np.sqrt(np.sum(E * E)))

@@ -36,7 +36,8 @@ class Params(ctypes.Structure):
                 ("theta_W", ctypes.c_double), ("theta_U", ctypes.c_double), ("L_V", ctypes.c_int),
                 ("L_W", ctypes.c_int), ("L_U", ctypes.c_int), ("cluster_mode", ctypes.c_int),
                 ("tile_budgets", ctypes.c_int), ("kappa", ctypes.c_double), ("max_cluster", ctypes.c_int),
-                ("form_R", ctypes.c_int)]
+                ("form_R", ctypes.c_int), ("dense_cluster", ctypes.c_int),
+                ("max_escalations", ctypes.c_int)]
 
 
 class StepReport(ctypes.Structure):
@@ -46,7 +47,7 @@ class StepReport(ctypes.Structure):
                 [(f, ctypes.c_double) for f in ["gap_min", "max_abs_lambda", "normE_fro", "net_update",
                                                  "predicted_error", "ms_total", "ms_gemm", "int8_ops"]] +
                 [("pairs_G", ctypes.c_int)] +
-                [(f, ctypes.c_double) for f in ["normR_fro", "normW_fro", "omega_oa"]])
+                [(f, ctypes.c_double) for f in ["normR_fro", "normW_fro", "omega_oa", "theta"]])
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}

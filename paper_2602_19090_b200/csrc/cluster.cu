@@ -336,11 +336,12 @@ __global__ void __launch_bounds__(JT)
     k_cluster_jacobi(const int* __restrict__ goff, const int* __restrict__ gsq, const int* __restrict__ gm,
                      const int* __restrict__ mem, const double* __restrict__ mu, const double* __restrict__ Mbuf,
                      const double* __restrict__ Rbuf, double* __restrict__ Kbuf, double* __restrict__ Vbuf,
-                     double* __restrict__ Zbuf, double* __restrict__ lam, int* __restrict__ sweeps_out) {
+                     double* __restrict__ Zbuf, double* __restrict__ lam, int* __restrict__ sweeps_out,
+                     int dense_min) {
   extern __shared__ double jsm[];  // cs[np] sn[np] th[m] sg[m] perm[m] | amax
   const int grp = blockIdx.x;
   const int m = gm[grp];
-  if (m >= kCoopMin) return;  // solved by the cooperative kernel
+  if (m >= kCoopMin || m >= dense_min) return;  // solved by the cooperative kernel / the dense solver
   const int mm = m + (m & 1), np = mm / 2;
   double* cs = jsm;
   double* sn = cs + np;
@@ -502,7 +503,7 @@ cudaError_t launch_cluster_build(const ClusterLaunch& L, cudaStream_t s) {
 cudaError_t launch_cluster_solve(const ClusterLaunch& L, cudaStream_t s) {
   const size_t sm = cluster_jacobi_smem(L.mmax);
   k_cluster_jacobi<<<L.ngroups, JT, sm, s>>>(L.goff, L.gsq, L.gm, L.mem, L.mu, L.Mbuf, L.Rbuf, L.Kbuf, L.Vbuf, L.Zbuf,
-                                              L.lam, L.sweeps);
+                                              L.lam, L.sweeps, L.dense_min);
   // large groups: one cooperative whole-GPU launch each
   static int coop_grid = 0;
   if (coop_grid == 0) {
@@ -513,7 +514,7 @@ cudaError_t launch_cluster_solve(const ClusterLaunch& L, cudaStream_t s) {
     coop_grid = nsm * std::max(1, std::min(per, 2));
   }
   for (int q = 0; q < L.ngroups; ++q) {
-    if (L.hgm[q] < kCoopMin) continue;
+    if (L.hgm[q] < kCoopMin || L.hgm[q] >= L.dense_min) continue;
     cudaError_t e = cudaMemsetAsync(L.coop_flags, 0, 128 * sizeof(int), s);
     if (e != cudaSuccess) return e;
     int grp = q;

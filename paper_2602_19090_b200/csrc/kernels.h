@@ -1,6 +1,8 @@
 // kernels.h — launchers of the HBM-bound ozr kernels (kernels.cu). Internal, not ABI.
 #pragma once
 #include <cstdint>
+#include <string>
+
 #include <cuda_runtime.h>
 
 namespace ozr {
@@ -95,7 +97,23 @@ struct ClusterLaunch {
   const int* hgm;          // host copy of gm (which groups take the cooperative whole-GPU Jacobi)
   double* coop_scratch;    // >= 5·mmax + 8 doubles
   int* coop_flags;         // >= 128 ints
+  int dense_min;           // groups of at least this many columns take the dense solver (dense_eig.cu)
+  int* err;                // error flags (ERR_RANGE when the dense solver reports failure)
 };
+// Dense symmetric eigensolver state of one context (cuSOLVER syevd, dlopen'ed; dense_eig.cu).
+struct DenseEig {
+  void* handle = nullptr;
+  double* work = nullptr;
+  int lwork = 0;
+  int* info = nullptr;
+  ~DenseEig();
+};
+bool dense_eig_available(std::string* why);
+long long dense_eig_lwork(DenseEig& de, int m, cudaStream_t s);
+// The sub-solve of group grp (m members, workspace offset o = gsq[grp], device member list J) by the dense
+// solver; the Jacobi kernels skip it. Stream-ordered on s.
+cudaError_t launch_cluster_dense(const ClusterLaunch& L, DenseEig& de, int m, long long o, double mu, const int* J,
+                                 cudaStream_t s);
 size_t cluster_jacobi_smem(int mmax);
 int cluster_dot_splits(int ntiles, int rows);
 // build: R_JJ (all), M_JJ and T = Ẽ'[:, J] on this rank's columns (zero elsewhere; all-reduced between);

@@ -50,6 +50,7 @@ struct ozr_ctx_s {
   cudaStream_t xstream = nullptr;  // side stream of the digit all-gather (overlaps the V product)
   cudaEvent_t ev_sync = nullptr;   // the host waits on this instead of the whole stream
   cudaEvent_t xev[2];
+  DenseEig dense;  // cuSOLVER handle of the dense cluster sub-solve (created on first use)
   bool events = false;
   // tracing (OZR_TRACE=1): named events between the kernels of a sweep, printed to stderr per sweep
   bool trace = false;
@@ -112,7 +113,7 @@ namespace {
 enum Slot {
   S_ADIG, S_AELL, S_W, S_X1, S_XDIG, S_XDIGT, S_G, S_SH, S_SL, S_RH, S_RL, S_PLANES, S_VH, S_VL, S_LAM, S_ER,
   S_ERR, S_EMAX, S_RDIG, S_RELL, S_EP, S_NRM2, S_NU2, S_WNEXT, S_ZEROELL, S_TMP1, S_TMP2, S_BELL, S_AT, S_ONES,
-  S_EDGES, S_ECOUNT, S_CINT, S_CDBL, S_CM, S_CR, S_CK, S_CV, S_CZ, S_CT, S_CSCR, S_CFLAG, S_SCAL, S_UFALL, S_CPART, S_GCNT, S_WA, S_GPLANES, S_RMAT, S_NR2, S_NW2
+  S_EDGES, S_ECOUNT, S_CINT, S_CDBL, S_CM, S_CR, S_CK, S_CV, S_CZ, S_CT, S_CSCR, S_CFLAG, S_SCAL, S_UFALL, S_CPART, S_GCNT, S_WA, S_GPLANES, S_RMAT, S_NR2, S_NW2, S_DWORK, S_DINFO
 };
 
 ozr_status fail(ozr_ctx c, ozr_status st, const char* fmt, ...) {
@@ -936,11 +937,28 @@ ozr_status sweep(ozr_ctx ctx, Exchange* ex, const double* A, int64_t n, int64_t 
       L.coop_scratch = ctx->ws<double>(S_CSCR, 5 * static_cast<size_t>(mmax) + 8);
       L.coop_flags = ctx->ws<int>(S_CFLAG, 128);
       OZR_ALLOC(L.coop_scratch); OZR_ALLOC(L.coop_flags);
+      L.dense_min = P.dense_cluster > 0 ? P.dense_cluster : (1 << 30);
+      L.err = derr;
+      if (mmax >= L.dense_min) {  // workspace of the dense solver (dense_eig.cu), sized for the largest group
+        std::string why;
+        if (!dense_eig_available(&why)) return fail(ctx, OZR_ERR_CUDA, "dense cluster solver: %s", why.c_str());
+        const long long lw = dense_eig_lwork(ctx->dense, mmax, s);
+        if (lw < 0) return fail(ctx, OZR_ERR_CUDA, "dense cluster solver: syevd workspace query failed");
+        ctx->dense.work = ctx->ws<double>(S_DWORK, static_cast<size_t>(lw));
+        ctx->dense.info = ctx->ws<int>(S_DINFO, 4);
+        OZR_ALLOC(ctx->dense.work); OZR_ALLOC(ctx->dense.info);
+        ctx->dense.lwork = static_cast<int>(lw);
+      }
       // (1) M_JJ columns owned by this rank, (2) all-reduce → full M on every rank, (3) Jacobi (replicated),
       // (4) T = Ẽ'[:, J] owned columns, all-reduce, (5) apply + column statistics on owned columns
       OZR_CK(launch_cluster_build(L, s), "cluster build");
       OZR_X(xsum(cM, sq));
       OZR_CK(launch_cluster_solve(L, s), "cluster solve");
+      for (int q = 0; q < ng; ++q)
+        if (gm[q] >= L.dense_min) {
+          OZR_CK(launch_cluster_dense(L, ctx->dense, gm[q], gsq[q], mu[q], dpk + o_mem + off[q], s), "dense cluster solve");
+          cluster_launches += 6;
+        }
       OZR_X(xsum(cT, static_cast<size_t>(nmem) * n));
       OZR_CK(launch_cluster_apply(L, s), "cluster apply");
       ctx->mark("cluster");
@@ -1131,8 +1149,10 @@ void ozr_params_default(ozr_params* p) {
   p->cluster_mode = 1;
   p->tile_budgets = 1;
   p->kappa = 0x1p-10;
-  p->max_cluster = 4096;
+  p->max_cluster = 16384;
   p->form_R = 0;
+  p->dense_cluster = 1024;
+  p->max_escalations = 2;
 }
 
 ozr_status ozr_split(ozr_ctx ctx, const double* M, const double* M_lo, int64_t rows, int64_t cols, int64_t ldm,
@@ -1354,6 +1374,7 @@ ozr_status ozr_refine_step_dist(ozr_ctx ctx, ozr_comm comm, const double* A, int
   ozr_step_report rep;
   st = sweep(ctx, comm ? comm->ex.get() : nullptr, A, n, lda, X, ldx, lambda, *params, rep, ss);
   rep.sweep = 1;
+  rep.theta = params->theta;
   if (report) *report = rep;
   return st;
 }
@@ -1369,9 +1390,12 @@ ozr_status ozr_refine_to_tol_dist(ozr_ctx ctx, ozr_comm comm, const double* A, i
   ozr_status result = OZR_ERR_NOT_CONVERGED;
   ctx->err.clear();
   const int maxs = params->max_sweeps > 0 ? params->max_sweeps : 6;
+  ozr_params P = *params;
+  int escalations = 0;
   for (int k = 0; k < maxs; ++k) {
     ozr_step_report rep;
-    st = sweep(ctx, comm ? comm->ex.get() : nullptr, A, n, lda, X, ldx, lambda, *params, rep, ss);
+    st = sweep(ctx, comm ? comm->ex.get() : nullptr, A, n, lda, X, ldx, lambda, P, rep, ss);
+    rep.theta = P.theta;
     rep.sweep = k + 1;
     if (st != OZR_OK) {
       if (sweeps_done) *sweeps_done = done;
@@ -1383,7 +1407,19 @@ ozr_status ozr_refine_to_tol_dist(ozr_ctx ctx, ozr_comm comm, const double* A, i
       result = OZR_OK;
       break;
     }
+    if (rep.n_clusters > 0) {  // a Rayleigh–Ritz sub-solve rotates its group: no contraction measure (R12)
+      nu_prev = -1.0;
+      continue;
+    }
     if (nu_prev >= 0.0 && rep.net_update > nu_prev / 2) {
+      // the truncated iteration sits at its noise floor above δ (R12): lower it by 2 bits of β (θ × 16,
+      // the floor is quadratic in the truncation) and keep going; stagnation again → NOT_CONVERGED
+      if (P.truncate && escalations < params->max_escalations) {
+        ++escalations;
+        P.theta = (P.theta > 0 ? P.theta : 1.0) * 16.0;
+        nu_prev = -1.0;
+        continue;
+      }
       fail(ctx, OZR_ERR_NOT_CONVERGED, "stagnation: net update %.3e > previous %.3e / 2", rep.net_update, nu_prev);
       break;
     }

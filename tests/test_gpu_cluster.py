@@ -26,10 +26,12 @@ def _case(cfg, n, start):
     return A, lam0, X0
 
 
-@pytest.mark.parametrize("n", [128, 256])
-def test_fp32_start_sweep_parity(ctx, n):
+@pytest.mark.parametrize("n,dense", [(128, 1024), (256, 1024), (256, 2)])
+def test_fp32_start_sweep_parity(ctx, n, dense):
+    """dense = 2: every group takes the dense sub-solve (dense_eig.cu, cuSOLVER syevd) instead of Jacobi;
+    the same K, so the same tolerance against the oracle's __float128 Jacobi."""
     A, lam0, X0 = _case("c2", n, "fp32")
-    Xg, lg, rep, Xo, lo, info, groups = parity_sweep(ctx, A, X0, lam0, 1e-14)
+    Xg, lg, rep, Xo, lo, info, groups = parity_sweep(ctx, A, X0, lam0, 1e-14, dense_cluster=dense)
     assert rep["beta"] == info["beta"]
     assert len(groups) >= 1 and rep["n_clusters"] == len(groups)
     assert rep["max_cluster"] == max(len(J) for J in groups)
@@ -97,14 +99,14 @@ def test_c3_fp64_start_stays_linear(ctx):
     assert np.max(np.abs(Xg - Xo)) <= 1e-13
 
 
-@pytest.mark.parametrize("n", [512])
-def test_c3_fp32_start_exercises_groups(ctx, n):
+@pytest.mark.parametrize("n,dense", [(512, 1024), (512, 2)])
+def test_c3_fp32_start_exercises_groups(ctx, n, dense):
     """The c3 spectrum (clusters of 8 eigenvalues 1e-10 apart) from an FP32 eigensolver: inside every
     cluster the FP32 vectors are arbitrary rotations (|ẽ_ij| ≫ κ), so each cluster becomes an unresolved
     group; one sweep matches the oracle and refine_to_tol reaches δ = 1e-12 against the reference."""
     import paper_2602_19090_b200 as ozr
     A, lam0, X0 = _case("c3", n, "fp32")
-    Xg, lg, rep, Xo, lo, info, groups = parity_sweep(ctx, A, X0, lam0, 1e-12)
+    Xg, lg, rep, Xo, lo, info, groups = parity_sweep(ctx, A, X0, lam0, 1e-12, dense_cluster=dense)
     assert rep["n_clusters"] >= n // 64 and all(len(J) >= 2 for J in groups)
     inJ = np.zeros(n, dtype=bool)
     for J in groups:
@@ -115,7 +117,28 @@ def test_c3_fp32_start_exercises_groups(ctx, n):
     lr, Xr = W.initial_eig(A, "fp64")
     Xh, Xl, lh, ll, _ = orf.reference_eigvecs(A, Xr, lr)
     Xd, ld = to_dev(X0), vec_dev(lam0)
-    st, hist = ozr.ozr_refine_to_tol(ctx, to_dev(A), Xd, ld, ozr.default_params(delta=1e-12, max_sweeps=10))
+    st, hist = ozr.ozr_refine_to_tol(ctx, to_dev(A), Xd, ld,
+                                     ozr.default_params(delta=1e-12, max_sweeps=10, dense_cluster=dense))
     fe = orf.forward_error(Xh, Xl, to_np(Xd), lh, to_np(ld))
     assert st == 0, hist
     assert fe <= 1e-12, (fe, [(h["net_update"], h["n_clusters"]) for h in hist])
+
+
+@pytest.mark.parametrize("n,delta", [(512, 1e-10), pytest.param(1024, 1e-10, marks=pytest.mark.slow)])
+def test_c4_recipe_fp32_start_converges(ctx, n, delta):
+    """BASELINE.json c4's recipe (geometric cnd 1e14, FP32 eigensolver start) at reduced n: the FP32 start
+    resolves almost none of the bottom spectrum, so the first sweep meets one group holding most columns
+    (the dense sub-solve); the following sweeps resolve it and the forward error against the oracle's
+    reference eigenvectors of the stored A reaches δ (proposed gate 1e-10)."""
+    import paper_2602_19090_b200 as ozr
+    A, lam0, X0 = _case("c4", n, "fp32")
+    lr, Xr = W.initial_eig(A, "fp64")
+    Xh, Xl, lh, ll, _ = orf.reference_eigvecs(A, Xr, lr, max_sweeps=30, cluster_kappa=2.0 ** -10)
+    Xd, ld = to_dev(X0), vec_dev(lam0)
+    st, hist = ozr.ozr_refine_to_tol(ctx, to_dev(A), Xd, ld,
+                                     ozr.default_params(delta=delta, max_sweeps=12, dense_cluster=64))
+    fe = orf.forward_error(Xh, Xl, to_np(Xd), lh, to_np(ld))
+    trail = [(h["net_update"], h["n_clusters"], h["max_cluster"]) for h in hist]
+    assert hist[0]["max_cluster"] >= n // 4, trail
+    assert st == 0, trail
+    assert fe <= delta, (fe, trail)

@@ -102,6 +102,43 @@ def test_reference_eigvecs_vs_quad_jacobi():
     assert np.max(np.abs((Xh - Vh * s) + (Xl - Vl * s))) < 1e-24
 
 
+def test_reference_cluster_branch_vs_quad_jacobi():
+    """The reference's Rayleigh–Ritz branch (cluster_kappa): from an FP32 eigensolver start on the c4 recipe
+    (cnd 1e14), where the first-order correction is not in its linear regime for the small eigenvalues, the
+    dd iteration with the branch reaches the __float128 Jacobi eigensystem."""
+    A, _ = W.make_matrix(24, "geometric", 1e14, 1004)
+    lam0, X0 = W.initial_eig(A, "fp32")
+    wh, wl, Vh, Vl, sw = _clib.jacobi_q(A)
+    s0 = np.sign(np.sum(X0 * Vh, axis=0))
+    assert np.max(np.abs(X0 - Vh * s0)) > 1e-3  # the start is far from the eigenvectors
+    Xh, Xl, lh, ll, hist = orf.reference_eigvecs(A, X0, lam0, max_sweeps=30, cluster_kappa=2.0 ** -10)
+    p, q = np.argsort(lh), np.argsort(wh)
+    Xh, Xl, lh, ll, Vh, Vl, wh, wl = Xh[:, p], Xl[:, p], lh[p], ll[p], Vh[:, q], Vl[:, q], wh[q], wl[q]
+    s = np.sign(np.sum(Xh * Vh, axis=0))
+    assert np.max(np.abs((Xh - Vh * s) + (Xl - Vl * s))) < 1e-20, hist
+    assert np.max(np.abs((lh - wh) + (ll - wl))) < 1e-28
+
+
+def test_reference_cluster_branch_certified_c4_recipe():
+    """Pin P8 for the c4 recipe (n = 128, cnd 1e14, eigenvalue gaps down to 3e-15) from the FP32 eigensolver
+    start (BASELINE c4): the plain dd iteration diverges, the one with the Rayleigh–Ritz branch converges,
+    and its residual certificate bounds every column's error by ‖A x_j − λ_j x_j‖/gap_j (Davis–Kahan)
+    ≤ 1e-15 with ‖I − XᵀX‖ ≤ 1e-17."""
+    A, _ = W.make_matrix(128, "geometric", 1e14, 1004)
+    lam0, X0 = W.initial_eig(A, "fp32")
+    with np.errstate(all="ignore"):
+        _, _, _, _, plain = orf.reference_eigvecs(A, X0, lam0, max_sweeps=6)
+    assert not (np.isfinite(plain[-1]) and plain[-1] < 1e-15), plain
+    Xh, Xl, lh, ll, hist = orf.reference_eigvecs(A, X0, lam0, max_sweeps=30, cluster_kappa=2.0 ** -10)
+    res, orth = orf.residual_certificate(A, Xh, Xl, lh, ll)
+    order = np.argsort(lh)
+    d = np.diff(lh[order])
+    gap = np.empty_like(lh)
+    gap[order] = np.minimum(np.r_[np.inf, d], np.r_[d, np.inf])
+    assert np.max(res / gap) <= 1e-15, (np.max(res / gap), hist)
+    assert orth <= 1e-17
+
+
 def test_reference_on_exact_householder_family():
     """Pin P6: A = H diag(λ) H exactly representable, X = H exactly."""
     A, lam, X, H, lam_cols = W.householder_exact(6, lam_bits=12, seed=3)
