@@ -77,13 +77,18 @@ struct ozr_ctx_s {
       return;
     }
     cudaEventSynchronize(tev[tn - 1]);
+    // a "~" mark is recorded just before a launch: the segment ending there is GPU time not spent in the
+    // sweep's kernels (host decisions, synchronisations, small copies)
     fprintf(stderr, "[ozr trace] gpu ms between marks (host ms in brackets):");
+    double gap = 0.0, tot = 0.0;
     for (int i = 1; i < tn; ++i) {
       float ms = 0.f;
       cudaEventElapsedTime(&ms, tev[i - 1], tev[i]);
       fprintf(stderr, " %s=%.3f[%.3f]", tname[i], ms, thost[i] - thost[i - 1]);
+      tot += ms;
+      if (tname[i][0] == '~') gap += ms;
     }
-    fprintf(stderr, "\n");
+    fprintf(stderr, " | total %.3f, between kernels %.3f\n", tot, gap);
     tn = 0;
   }
 
@@ -579,6 +584,7 @@ ozr_status sweep(ozr_ctx ctx, Exchange* ex, const double* A, int64_t n, int64_t 
   OZR_CK(cudaMemcpyAsync(hw.data(), w, n * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H w");
   OZR_CK(cudaMemcpyAsync(hlam.data(), lambda, n * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H lambda");
   OZR_X(scalars({}, nullptr, [&]() -> ozr_status {
+    ctx->mark("~");
     return new_A ? split_A_launch(ctx, A, n, lda, P.kA_split, derr, hell) : OZR_OK;
   }));
   for (double x : hlam)
@@ -612,7 +618,7 @@ ozr_status sweep(ozr_ctx ctx, Exchange* ex, const double* A, int64_t n, int64_t 
 
   // ---- A split (once per refine_to_tol call; A and its digits are replicated on every rank)
   if (new_A) split_A_finish(A, n, hwA, P.kA_split, st);
-  ctx->mark("stats+splitA");
+  ctx->mark("splitA");
   // per-column accuracy of V (R8, R8b): θ_V·δ'·gap_j with the previous λ̂ (this rank's columns)
   std::vector<double>& gaps_prev = ls_prev.colgap;
   for (double& x : gaps_prev)
@@ -645,6 +651,7 @@ ozr_status sweep(ozr_ctx ctx, Exchange* ex, const double* A, int64_t n, int64_t 
   double* rl = ctx->ws<double>(S_RL, n);
   OZR_ALLOC(X1); OZR_ALLOC(xdig); OZR_ALLOC(xdigT); OZR_ALLOC(g); OZR_ALLOC(sh); OZR_ALLOC(sl); OZR_ALLOC(rh);
   OZR_ALLOC(rl);
+  ctx->mark("~");
   launch_x1_split(X, ldx, N, NL, beta, kx, w + col0, X1, n, xdig + col0 * ld, ld, ld * n, g + col0, sh, sl, rh + col0,
                   rl + col0, derr, s);
   OZR_CK(cudaGetLastError(), "x1 split");
@@ -678,6 +685,7 @@ ozr_status sweep(ozr_ctx ctx, Exchange* ex, const double* A, int64_t n, int64_t 
   DigitOperand opA{reinterpret_cast<const int8_t*>(ctx->bufs[S_ADIG].p), ld, ld * n, st.kA_split};
   DigitOperand opXJ{xdig + col0 * ld, ld, ld * n, kx};  // local columns (B operand of V)
   DigitOperand opX{xdig, ld, ld * n, kx};               // all columns (A operand of W)
+  ctx->mark("~");
   OZR_X(run_gemm(ctx, opA, opXJ, N, NL, N, pt, planes, 0));
   ctx->mark("gemmV");
   // join the digit exchange before any other collective (λ̂ below) and before reading other ranks' digits
@@ -716,6 +724,7 @@ ozr_status sweep(ozr_ctx ctx, Exchange* ex, const double* A, int64_t n, int64_t 
   OZR_ALLOC(Vh); OZR_ALLOC(Vl); OZR_ALLOC(lam); OZR_ALLOC(eR);
   const int intmin = -(1 << 30);
   OZR_CK(cudaMemcpyAsync(demax, &intmin, sizeof(int), cudaMemcpyHostToDevice, s), "H2D");
+  ctx->mark("~");
   launch_recombine_V(planes, nnl, N, NL, rp, reinterpret_cast<const int32_t*>(ctx->bufs[S_AELL].p), g + col0,
                      8 * (st.kA_split + kx - LV), X1, n, sh, sl, Vh, Vl, n, lam + col0, eR, demax, s);
   OZR_CK(cudaGetLastError(), "recombine V");
@@ -729,7 +738,9 @@ ozr_status sweep(ozr_ctx ctx, Exchange* ex, const double* A, int64_t n, int64_t 
   // one synchronisation for λ̂, the Res exponents and their maximum; the digit transpose (A operand of
   // X̂Ẽ, after the exchange) runs meanwhile
   OZR_X(scalars({demax}, &eRmax, [&]() -> ozr_status {
+    ctx->mark("~");
     launch_transpose_i8(xdig, ld, ld * n, xdigT, ld, ld * n, N, N, kx, s);
+    ctx->mark("transpose");
     OZR_CK(cudaGetLastError(), "transpose digits");
     return OZR_OK;
   }));
@@ -747,9 +758,10 @@ ozr_status sweep(ozr_ctx ctx, Exchange* ex, const double* A, int64_t n, int64_t 
   int8_t* rdig = ctx->ws<int8_t>(S_RDIG, static_cast<size_t>(kMaxDigits) * ld * nl);
   int32_t* rell = ctx->ws<int32_t>(S_RELL, nl);
   OZR_ALLOC(rdig); OZR_ALLOC(rell);
+  ctx->mark("~");
   launch_split_res(Vh, Vl, n, X1, n, lam + col0, N, NL, kR, eR, rdig, ld, ld * nl, rell, s);
   OZR_CK(cudaGetLastError(), "split Res");
-  ctx->mark("host+splitRes");
+  ctx->mark("splitRes");
 
   // ---- a7: P3  W_{:,J} = X̂^(1)ᵀ Res_J  (Alg. 1 line 4)
   std::vector<double>& gaps_new = ls_new.colgap;
@@ -774,8 +786,9 @@ ozr_status sweep(ozr_ctx ctx, Exchange* ex, const double* A, int64_t n, int64_t 
     OZR_ALLOC(planes);
   }
   DigitOperand opR{rdig, ld, ld * nl, kR};
+  ctx->mark("~");
   OZR_X(run_gemm(ctx, opX, opR, N, NL, N, pt, planes, 1));
-  ctx->mark("host+gemmW");
+  ctx->mark("gemmW");
   rep.kR = kR;
   rep.L_W = LW;
   const double pW = tilesW ? avg_pairs_W : static_cast<double>(count_pairs(gW));
@@ -795,6 +808,7 @@ ozr_status sweep(ozr_ctx ctx, Exchange* ex, const double* A, int64_t n, int64_t 
   const EdgeOut eo{P.cluster_mode, P.kappa, uf, ecount};
   double* nW2 = P.form_R ? ctx->ws<double>(S_NW2, n) : nullptr;
   if (P.form_R) OZR_ALLOC(nW2);
+  ctx->mark("~");
   launch_recombine_E(planes, nnl, N, NL, rp, g, rell, 8 * (kx + kR - LW), rh + col0, lam, g, static_cast<int>(col0), Ep, n,
                      nrm2 + col0, demax, eR, derr, eo, nW2 ? nW2 + col0 : nullptr, s);
   OZR_CK(cudaGetLastError(), "recombine E");
@@ -978,9 +992,10 @@ ozr_status sweep(ozr_ctx ctx, Exchange* ex, const double* A, int64_t n, int64_t 
   // ---- a9: P4  U_J = X̂^(1) Ẽ_{:,J} = Q Ẽ'_{:,J} ; X̂_J ← RN(X̂^(1)_J + U_J)  (Alg. 1 line 6)
   const double tauU = P.theta_U * delta_p;
   const int kE = digits_for(eEmax, static_cast<int>(std::floor(std::log2(tauU / 2.0))) + gmin);
+  ctx->mark("~");
   launch_split_fixed(Ep, nullptr, n, N, NL, kE, rdig, ld, ld * nl, rell, derr, s);
   OZR_CK(cudaGetLastError(), "split E");
-  ctx->mark("host+splitE");
+  ctx->mark("splitE");
   const int SX = 8 * (kx - 1) + 6;
   // R8b for X̂Ẽ: uniform accuracy θ_U·δ', but columns with small corrections need fewer pairs
   for (int64_t j = 0; j < nl; ++j) tau_col[j] = tauU / 2.0;
@@ -1000,6 +1015,7 @@ ozr_status sweep(ozr_ctx ctx, Exchange* ex, const double* A, int64_t n, int64_t 
   }
   DigitOperand opQ{xdigT, ld, ld * n, kx};
   DigitOperand opE{rdig, ld, ld * nl, kE};
+  ctx->mark("~");
   OZR_X(run_gemm(ctx, opQ, opE, N, NL, N, pt, planes, 2));
   ctx->mark("gemmU");
   rep.kE = kE;
@@ -1009,6 +1025,7 @@ ozr_status sweep(ozr_ctx ctx, Exchange* ex, const double* A, int64_t n, int64_t 
   ops += 2.0 * n * n * nl * pU;
   double* nu2 = ctx->ws<double>(S_NU2, n);
   OZR_ALLOC(nu2);
+  ctx->mark("~");
   launch_final(planes, nnl, N, NL, rp, rell, 8 * (kx + kE - LU), X1, n, X, ldx, nu2 + col0, wnext + col0, s);
   OZR_CK(cudaGetLastError(), "final update");
   ctx->mark("final");
@@ -1029,6 +1046,7 @@ ozr_status sweep(ozr_ctx ctx, Exchange* ex, const double* A, int64_t n, int64_t 
   OZR_CK(cudaMemcpyAsync(hnu.data(), nu2, n * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H");
   OZR_CK(cudaMemcpyAsync(hnrm.data(), nrm2, n * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H");
   OZR_X(scalars({}, nullptr));
+  ctx->mark("~end");
   double nu = 0.0, ne = 0.0;
   for (int64_t j = 0; j < n; ++j) {
     nu += hnu[j];
