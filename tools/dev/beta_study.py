@@ -18,7 +18,7 @@ for cfg, n, start, delta in cases:
     Xh, Xl, lh, ll, _ = orf.reference_eigvecs(A, Xr, lr)
     Ad = to_dev(A)
     rows = []
-    for bm, xi, th in [(0, 0, 1.0), (0, 0, 4.0), (1, 0, 1.0), (1, 0, 4.0), (1, n * n, 1.0)]:
+    for bm, xi, th in [(0, 0, 1.0), (0, 0, 4.0), (1, 1, 1.0), (1, 0, 1.0), (1, 0, 4.0)]:
         Xd, ld = to_dev(X0), vec_dev(lam0)
         p = ozr.default_params(delta=delta, beta_mode=bm, xi=float(xi), theta=th, max_sweeps=10)
         torch.cuda.synchronize()
@@ -27,7 +27,7 @@ for cfg, n, start, delta in cases:
         torch.cuda.synchronize()
         ms = (time.perf_counter() - t0) * 1e3
         fe = orf.forward_error(Xh, Xl, to_np(Xd), lh, to_np(ld))
-        rows.append(dict(beta_mode=bm, xi=xi or n, theta=th, status=st, sweeps=len(hist),
+        rows.append(dict(beta_mode=bm, xi=xi if bm else n, theta=th, status=st, sweeps=len(hist),
                          betas=[h['beta'] for h in hist], ms=round(ms, 2), fe_over_delta=round(fe / delta, 3)))
     print(cfg, n, delta)
     for r in rows:
