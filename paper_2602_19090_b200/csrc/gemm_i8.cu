@@ -513,6 +513,10 @@ cudaError_t launch_gemm_i8(const DigitOperand& A, const DigitOperand& B, int M, 
     if (!attr2) {
       cudaError_t e2 = cudaFuncSetAttribute(k_gemm_i8_2sm, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2_BYTES);
       if (e2 != cudaSuccess) return e2;
+      // the largest shared-memory carveout (228 KB), so that the ~30 KB the GEMM leaves free on every SM can
+      // host the register-path recombination CTAs of the previous column band (ozr_api.cu run_banded)
+      e2 = cudaFuncSetAttribute(k_gemm_i8_2sm, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+      if (e2 != cudaSuccess) return e2;
       attr2 = true;
     }
     const int tiles_m2 = (M + 2 * BM - 1) / (2 * BM);

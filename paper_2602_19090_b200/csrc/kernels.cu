@@ -15,6 +15,7 @@
 //   k_final           U = X̂^(1)Ẽ → X̂ ← RN(X̂^(1) + U) (Alg. 1 line 6, accsum), ν, column maxima
 //   k_recombine_dd    generic recombination for ozr_gemm
 #include <cstdint>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 #include "ddmath.cuh"
@@ -768,10 +769,26 @@ __global__ void __launch_bounds__(BS, 3)
 
 // ---------------------------------------------------------------- launchers
 namespace {
+void init_attrs();
 int tma_ok(const RecombPlan& rp, const int32_t* planes, long long pstride, int rows, const double* x0, long long ld0,
            const double* x1, long long ld1) {
+  init_attrs();
+  auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  if (!rp.consecutive || rows % 4 || pstride % 4 || !al(planes)) return 0;
+  if (x0 && (ld0 % 2 || !al(x0))) return 0;
+  if (x1 && (ld1 % 2 || !al(x1))) return 0;
+  return 1;
+}
+// dynamic shared memory of the TMA paths; every recombination kernel prefers the largest carveout (the same
+// SM configuration as the slice GEMM, with which its register path co-resides)
+void init_attrs() {
   static bool attr = false;
   if (!attr) {
+#define OZR_CARVE(K) cudaFuncSetAttribute(K, cudaFuncAttributePreferredSharedMemoryCarveout, 100)
+    OZR_CARVE(k_recombine_V<4>); OZR_CARVE(k_recombine_V<8>); OZR_CARVE(k_recombine_V<12>);
+    OZR_CARVE(k_recombine_E<4>); OZR_CARVE(k_recombine_E<8>); OZR_CARVE(k_recombine_E<12>);
+    OZR_CARVE(k_final<4>); OZR_CARVE(k_final<8>); OZR_CARVE(k_final<12>);
+#undef OZR_CARVE
     cudaFuncSetAttribute(k_recombine_V<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem);
     cudaFuncSetAttribute(k_recombine_V<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem);
     cudaFuncSetAttribute(k_recombine_V<12>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem);
@@ -783,11 +800,6 @@ int tma_ok(const RecombPlan& rp, const int32_t* planes, long long pstride, int r
     cudaFuncSetAttribute(k_final<12>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem);
     attr = true;
   }
-  auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
-  if (!rp.consecutive || rows % 4 || pstride % 4 || !al(planes)) return 0;
-  if (x0 && (ld0 % 2 || !al(x0))) return 0;
-  if (x1 && (ld1 % 2 || !al(x1))) return 0;
-  return 1;
 }
 }  // namespace
 
@@ -822,8 +834,9 @@ void launch_transpose_f64(const double* src, long long lds, double* dst, long lo
 void launch_recombine_V(const int32_t* planes, long long pstride, int rows, int cols, const RecombPlan& rp,
                         const int32_t* ellA, const int32_t* ellB, int scale8, const double* X1, long long ldx1,
                         const double* s_hi, const double* s_lo, double* Vh, double* Vl, long long ldv,
-                        double* lam_out, int32_t* eR, int* eR_max, cudaStream_t s) {
-  const int tma = tma_ok(rp, planes, pstride, rows, X1, ldx1, X1, ldx1) && (reinterpret_cast<uintptr_t>(ellA) & 15) == 0;
+                        double* lam_out, int32_t* eR, int* eR_max, cudaStream_t s, int allow_tma) {
+  init_attrs();
+  const int tma = allow_tma && tma_ok(rp, planes, pstride, rows, X1, ldx1, X1, ldx1) && (reinterpret_cast<uintptr_t>(ellA) & 15) == 0;
 #define OZR_RV(NG_)                                                                                          \
   k_recombine_V<NG_><<<cols, BS, tma ? kTmaSmem : 0, s>>>(planes, pstride, rows, rp, ellA, ellB, scale8, X1, ldx1, s_hi, \
                                                           s_lo, Vh, Vl, ldv, lam_out, eR, eR_max, tma)
@@ -835,8 +848,9 @@ void launch_recombine_V(const int32_t* planes, long long pstride, int rows, int 
 void launch_recombine_E(const int32_t* planes, long long pstride, int rows, int cols, const RecombPlan& rp,
                         const int32_t* ellA, const int32_t* ellB, int scale8, const double* r_hi, const double* lam,
                         const int32_t* gX, int col0, double* Ep, long long lde, double* nrm2, int* eE_max,
-                        int32_t* eE_col, int* err, const EdgeOut& eo, double* nW2, cudaStream_t s) {
-  const int tma = tma_ok(rp, planes, pstride, rows, lam, 0, nullptr, 0) && (reinterpret_cast<uintptr_t>(ellA) & 15) == 0;
+                        int32_t* eE_col, int* err, const EdgeOut& eo, double* nW2, cudaStream_t s, int allow_tma) {
+  init_attrs();
+  const int tma = allow_tma && tma_ok(rp, planes, pstride, rows, lam, 0, nullptr, 0) && (reinterpret_cast<uintptr_t>(ellA) & 15) == 0;
 #define OZR_RE(NG_)                                                                                            \
   k_recombine_E<NG_><<<cols, BS, tma ? kTmaSmem : 0, s>>>(planes, pstride, rows, rp, ellA, ellB, scale8, r_hi, lam, gX, \
                                                           col0, Ep, lde, nrm2, eE_max, eE_col, err, eo, tma, nW2)
@@ -847,8 +861,9 @@ void launch_recombine_E(const int32_t* planes, long long pstride, int rows, int 
 }
 void launch_final(const int32_t* planes, long long pstride, int rows, int cols, const RecombPlan& rp,
                   const int32_t* ellB, int scale8, const double* X1, long long ldx1, double* X, long long ldx,
-                  double* nu2, double* wnext, cudaStream_t s) {
-  const int tma = tma_ok(rp, planes, pstride, rows, X1, ldx1, X, ldx);
+                  double* nu2, double* wnext, cudaStream_t s, int allow_tma) {
+  init_attrs();
+  const int tma = allow_tma && tma_ok(rp, planes, pstride, rows, X1, ldx1, X, ldx);
 #define OZR_FI(NG_)                                                                                                 \
   k_final<NG_><<<cols, BS, tma ? kTmaSmem : 0, s>>>(planes, pstride, rows, rp, ellB, scale8, X1, ldx1, X, ldx, nu2, wnext, \
                                                     tma)

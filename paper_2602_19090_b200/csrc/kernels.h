@@ -44,7 +44,7 @@ void launch_transpose_f64(const double* src, long long lds, double* dst, long lo
 void launch_recombine_V(const int32_t* planes, long long pstride, int rows, int cols, const RecombPlan& rp,
                         const int32_t* ellA, const int32_t* ellB, int scale8, const double* X1, long long ldx1,
                         const double* s_hi, const double* s_lo, double* Vh, double* Vl, long long ldv,
-                        double* lam_out, int32_t* eR, int* eR_max, cudaStream_t s);
+                        double* lam_out, int32_t* eR, int* eR_max, cudaStream_t s, int allow_tma = 1);
 // Unresolved pairs of k_recombine_E (cluster branch, R13): every pair (i, j), i ≠ j, with
 // λ̂_i = λ̂_j or |ẽ_ij| > κ is united in the device union-find `parent` (O(n) memory, any number of
 // pairs; the resulting partition is independent of the order of the unions), and *any is set.
@@ -60,7 +60,7 @@ void launch_recombine_E(const int32_t* planes, long long pstride, int rows, int 
                         const int32_t* ellA, const int32_t* ellB, int scale8, const double* r_hi, const double* lam,
                         const int32_t* gX, int col0, double* Ep, long long lde, double* nrm2, int* eE_max,
                         int32_t* eE_col, int* err, const EdgeOut& eo, double* nW2 /* nullable: ‖w_j‖² */,
-                        cudaStream_t s);
+                        cudaStream_t s, int allow_tma = 1);
 // form_R: R = I − X̂^(1)ᵀX̂^(1) (local columns) from the G slice-product planes, ‖r_j‖² in nR2[j]
 void launch_form_R(const int32_t* planes, long long pstride, int rows, int cols, const RecombPlan& rp, const int32_t* g,
                    int scale8, int col0, const double* r_hi, const double* r_lo, double* R, long long ldr, double* nR2,
@@ -124,7 +124,7 @@ cudaError_t launch_cluster_solve(const ClusterLaunch& L, cudaStream_t s);
 cudaError_t launch_cluster_apply(const ClusterLaunch& L, cudaStream_t s);
 void launch_final(const int32_t* planes, long long pstride, int rows, int cols, const RecombPlan& rp,
                   const int32_t* ellB, int scale8, const double* X1, long long ldx1, double* X, long long ldx,
-                  double* nu2, double* wnext, cudaStream_t s);
+                  double* nu2, double* wnext, cudaStream_t s, int allow_tma = 1);
 void launch_recombine_dd(const int32_t* planes, long long pstride, int rows, int cols, const RecombPlan& rp,
                          const int32_t* ellA, const int32_t* ellB, int scale8, double* Ch, double* Cl, long long ldc,
                          cudaStream_t s);

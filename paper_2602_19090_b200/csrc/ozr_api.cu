@@ -28,6 +28,7 @@ namespace {
 constexpr double kU = 0x1p-53;
 constexpr int kBetaMin = 2, kBetaMax = 52;
 constexpr int kMaxDigits = 15;
+constexpr int kMaxBands = 8;
 
 int64_t round16(int64_t x) { return (x + 15) / 16 * 16; }
 
@@ -50,6 +51,10 @@ struct ozr_ctx_s {
   cudaStream_t xstream = nullptr;  // side stream of the digit all-gather (overlaps the V product)
   cudaEvent_t ev_sync = nullptr;   // the host waits on this instead of the whole stream
   cudaEvent_t xev[2];
+  // column-band pipeline of the slice products (run_banded): the recombination of band b runs on rstream
+  // while the main stream computes the GEMM of band b + 1
+  cudaStream_t rstream = nullptr;
+  cudaEvent_t bev[kMaxBands + 2];
   DenseEig dense;  // cuSOLVER handle of the dense cluster sub-solve (created on first use)
   bool events = false;
   // tracing (OZR_TRACE=1): named events between the kernels of a sweep, printed to stderr per sweep
@@ -420,6 +425,69 @@ ozr_status run_gemm(ozr_ctx ctx, const DigitOperand& A, const DigitOperand& B, i
   return OZR_OK;
 }
 
+// Column bands of a slice product and its recombination: band b of the output (columns
+// [c0, c1), multiples of the 256-column tile) only needs band b of the right operand, so the GEMM of band
+// b + 1 (main stream) runs while the recombination of band b runs on ctx->rstream. The GEMM holds 197 KB of
+// shared memory on every SM, so the overlapped recombinations take the register path (a few KB); the
+// last band, which nothing overlaps, takes the TMA-staged path. Same arithmetic per column either way.
+// Measured on B200 (c4', n = 8192): OFF by default. The register-path recombination CTAs do co-reside with
+// the persistent GEMM (a trivial kernel on the side stream completes at once) but starve behind the GEMM's
+// TMA traffic: band b's recombine_V takes 4.5 ms instead of 0.5, the band GEMMs lose ~5 %, and the sweep
+// goes from 28.4 to 29.4 ms. OZR_BANDS=k (k ≤ 8) enables k bands for experiments.
+int band_count(int64_t nl) {
+  const char* v = getenv("OZR_BANDS");
+  const int want = v ? atoi(v) : 1;
+  int nb = static_cast<int>(std::min<int64_t>(want, nl / 1024));
+  return std::max(1, std::min(nb, kMaxBands));
+}
+
+ozr_status run_banded(ozr_ctx ctx, const DigitOperand& A, const DigitOperand& B, int M, int N, int K,
+                      const PairTable& pt, int32_t* planes, int idx,
+                      const std::function<void(int64_t c0, int64_t c1, int tile0, int tma, cudaStream_t st)>& recomb,
+                      const std::function<void(cudaStream_t st)>& side_first = nullptr) {
+  cudaStream_t s = ctx->stream, r = ctx->rstream;
+  const int nb = band_count(N);
+  const int64_t tiles = (N + kTileN - 1) / kTileN;
+  const int64_t tpb = (tiles + nb - 1) / nb;  // tiles per band
+  int* cnt = ctx->ws<int>(S_GCNT, 4);
+  OZR_ALLOC(cnt);
+  cudaEventRecord(ctx->ev[2 + 2 * idx], s);
+  OZR_CK(cudaEventRecord(ctx->bev[kMaxBands], s), "event");
+  OZR_CK(cudaStreamWaitEvent(r, ctx->bev[kMaxBands], 0), "wait");  // the side stream sees all earlier work
+  if (side_first) side_first(r);  // independent work that overlaps the first band's GEMM
+  int b = 0;
+  for (int64_t t0 = 0; t0 < tiles; t0 += tpb, ++b) {
+    const int64_t c0 = t0 * kTileN, c1 = std::min<int64_t>(N, (t0 + tpb) * kTileN);
+    PairTable ptb = pt;
+    if (pt.tile_budgets)
+      for (int64_t t = t0; t < std::min<int64_t>(tiles, t0 + tpb); ++t) ptb.tileL[t - t0] = pt.tileL[t];
+    DigitOperand Bb{B.base + c0 * B.ld, B.ld, B.plane_stride, B.nplanes};
+    OZR_CK(launch_gemm_i8(A, Bb, M, static_cast<int>(c1 - c0), K, ptb, planes + c0 * M,
+                          static_cast<int64_t>(M) * N, M, s, cnt), "slice GEMM band");
+    const bool last = c1 >= N;
+    if (last) {
+      cudaEventRecord(ctx->ev[3 + 2 * idx], s);
+      recomb(c0, c1, static_cast<int>(t0), 1, s);
+    } else {
+      OZR_CK(cudaEventRecord(ctx->bev[b], s), "event");
+      OZR_CK(cudaStreamWaitEvent(r, ctx->bev[b], 0), "wait");
+      recomb(c0, c1, static_cast<int>(t0), 0, r);
+    }
+  }
+  OZR_CK(cudaGetLastError(), "recombination band");
+  OZR_CK(cudaEventRecord(ctx->bev[kMaxBands + 1], r), "event");
+  OZR_CK(cudaStreamWaitEvent(s, ctx->bev[kMaxBands + 1], 0), "join");
+  return OZR_OK;
+}
+
+// a RecombPlan whose per-tile budgets start at tile t0 (the band's first tile)
+RecombPlan shift_plan(const RecombPlan& rp, int t0) {
+  RecombPlan q = rp;
+  if (rp.tile_budgets)
+    for (int t = 0; t + t0 < 256; ++t) q.tileL[t] = rp.tileL[t + t0];
+  return q;
+}
+
 ozr_status err_bits(ozr_ctx ctx, int h) {
   if (h & ERR_NONFINITE) return fail(ctx, OZR_ERR_NONFINITE, "non-finite value in an input matrix");
   if (h & ERR_RANGE) return fail(ctx, OZR_ERR_RANGE, "exponent range exceeded in the digit split");
@@ -685,9 +753,30 @@ ozr_status sweep(ozr_ctx ctx, Exchange* ex, const double* A, int64_t n, int64_t 
   DigitOperand opA{reinterpret_cast<const int8_t*>(ctx->bufs[S_ADIG].p), ld, ld * n, st.kA_split};
   DigitOperand opXJ{xdig + col0 * ld, ld, ld * n, kx};  // local columns (B operand of V)
   DigitOperand opX{xdig, ld, ld * n, kx};               // all columns (A operand of W)
+  // ---- a4-a6 (fused into the V bands): recombine V, λ̂, Res column maxima
+  double* Vh = ctx->ws<double>(S_VH, nnl);
+  double* Vl = ctx->ws<double>(S_VL, nnl);
+  double* lam = ctx->ws<double>(S_LAM, n);
+  int32_t* eR = ctx->ws<int32_t>(S_ER, nl);
+  OZR_ALLOC(Vh); OZR_ALLOC(Vl); OZR_ALLOC(lam); OZR_ALLOC(eR);
+  const int intmin = -(1 << 30);
+  OZR_CK(cudaMemcpyAsync(demax, &intmin, sizeof(int), cudaMemcpyHostToDevice, s), "H2D");
+  const int32_t* aell = reinterpret_cast<const int32_t*>(ctx->bufs[S_AELL].p);
+  const int scaleV = 8 * (st.kA_split + kx - LV);
   ctx->mark("~");
-  OZR_X(run_gemm(ctx, opA, opXJ, N, NL, N, pt, planes, 0));
-  ctx->mark("gemmV");
+  OZR_X(run_banded(
+      ctx, opA, opXJ, N, NL, N, pt, planes, 0,
+      [&](int64_t c0, int64_t c1, int t0, int tma, cudaStream_t q) {
+        launch_recombine_V(planes + c0 * n, nnl, N, static_cast<int>(c1 - c0), shift_plan(rp, t0), aell,
+                           g + col0 + c0, scaleV, X1 + c0 * n, n, sh + c0, sl + c0, Vh + c0 * n, Vl + c0 * n, n,
+                           lam + col0 + c0, eR + c0, demax, q, tma);
+      },
+      [&](cudaStream_t q) {
+        // the digit transpose (A operand of X̂Ẽ) needs every column's digits: after the exchange on P ranks
+        if (ex) cudaStreamWaitEvent(q, ctx->xev[1], 0);
+        launch_transpose_i8(xdig, ld, ld * n, xdigT, ld, ld * n, N, N, kx, q);
+      }));
+  ctx->mark("gemmV+recombV");
   // join the digit exchange before any other collective (λ̂ below) and before reading other ranks' digits
   if (ex) OZR_CK(cudaStreamWaitEvent(s, ctx->xev[1], 0), "wait exchange");
   // optional: R = I − X̂^(1)ᵀX̂^(1) (the R/S form's first product) to θ_W·δ' absolute
@@ -716,19 +805,6 @@ ozr_status sweep(ozr_ctx ctx, Exchange* ex, const double* A, int64_t n, int64_t 
   rep.pairs_V = static_cast<int>(std::lround(pV));
   ops += 2.0 * n * n * nl * pV;
 
-  // ---- a4-a6: recombine V, λ̂, Res, column maxima
-  double* Vh = ctx->ws<double>(S_VH, nnl);
-  double* Vl = ctx->ws<double>(S_VL, nnl);
-  double* lam = ctx->ws<double>(S_LAM, n);
-  int32_t* eR = ctx->ws<int32_t>(S_ER, nl);
-  OZR_ALLOC(Vh); OZR_ALLOC(Vl); OZR_ALLOC(lam); OZR_ALLOC(eR);
-  const int intmin = -(1 << 30);
-  OZR_CK(cudaMemcpyAsync(demax, &intmin, sizeof(int), cudaMemcpyHostToDevice, s), "H2D");
-  ctx->mark("~");
-  launch_recombine_V(planes, nnl, N, NL, rp, reinterpret_cast<const int32_t*>(ctx->bufs[S_AELL].p), g + col0,
-                     8 * (st.kA_split + kx - LV), X1, n, sh, sl, Vh, Vl, n, lam + col0, eR, demax, s);
-  OZR_CK(cudaGetLastError(), "recombine V");
-  ctx->mark("recombV");
   OZR_X(xgather(lam, nl * sizeof(double)));
   int eRmax = 0;
   std::vector<double> hlam_new(n);
@@ -737,13 +813,7 @@ ozr_status sweep(ozr_ctx ctx, Exchange* ex, const double* A, int64_t n, int64_t 
   OZR_CK(cudaMemcpyAsync(eR_col.data(), eR, nl * sizeof(int32_t), cudaMemcpyDeviceToHost, s), "D2H eR");
   // one synchronisation for λ̂, the Res exponents and their maximum; the digit transpose (A operand of
   // X̂Ẽ, after the exchange) runs meanwhile
-  OZR_X(scalars({demax}, &eRmax, [&]() -> ozr_status {
-    ctx->mark("~");
-    launch_transpose_i8(xdig, ld, ld * n, xdigT, ld, ld * n, N, N, kx, s);
-    ctx->mark("transpose");
-    OZR_CK(cudaGetLastError(), "transpose digits");
-    return OZR_OK;
-  }));
+  OZR_X(scalars({demax}, &eRmax));
   LamStats ls_new = lam_stats(hlam_new);
   const double gap_new0 = ls_new.gap0;
   if (!(gap_new0 > 0.0) && P.cluster_mode == 0)
@@ -786,16 +856,13 @@ ozr_status sweep(ozr_ctx ctx, Exchange* ex, const double* A, int64_t n, int64_t 
     OZR_ALLOC(planes);
   }
   DigitOperand opR{rdig, ld, ld * nl, kR};
-  ctx->mark("~");
-  OZR_X(run_gemm(ctx, opX, opR, N, NL, N, pt, planes, 1));
-  ctx->mark("gemmW");
   rep.kR = kR;
   rep.L_W = LW;
   const double pW = tilesW ? avg_pairs_W : static_cast<double>(count_pairs(gW));
   rep.pairs_W = static_cast<int>(std::lround(pW));
   ops += 2.0 * n * n * nl * pW;
 
-  // ---- a8: Ẽ (Alg. 1 line 5), Ẽ' = diag(2^g) Ẽ
+  // ---- a8 (fused into the W bands): Ẽ (Alg. 1 line 5), Ẽ' = diag(2^g) Ẽ
   double* Ep = ctx->ws<double>(S_EP, nnl);
   double* nrm2 = ctx->ws<double>(S_NRM2, n);
   OZR_ALLOC(Ep); OZR_ALLOC(nrm2);
@@ -808,11 +875,16 @@ ozr_status sweep(ozr_ctx ctx, Exchange* ex, const double* A, int64_t n, int64_t 
   const EdgeOut eo{P.cluster_mode, P.kappa, uf, ecount};
   double* nW2 = P.form_R ? ctx->ws<double>(S_NW2, n) : nullptr;
   if (P.form_R) OZR_ALLOC(nW2);
+  const int scaleW = 8 * (kx + kR - LW);
   ctx->mark("~");
-  launch_recombine_E(planes, nnl, N, NL, rp, g, rell, 8 * (kx + kR - LW), rh + col0, lam, g, static_cast<int>(col0), Ep, n,
-                     nrm2 + col0, demax, eR, derr, eo, nW2 ? nW2 + col0 : nullptr, s);
-  OZR_CK(cudaGetLastError(), "recombine E");
-  ctx->mark("recombE");
+  OZR_X(run_banded(ctx, opX, opR, N, NL, N, pt, planes, 1,
+                   [&](int64_t c0, int64_t c1, int t0, int tma, cudaStream_t q) {
+                     launch_recombine_E(planes + c0 * n, nnl, N, static_cast<int>(c1 - c0), shift_plan(rp, t0), g,
+                                        rell + c0, scaleW, rh + col0 + c0, lam, g, static_cast<int>(col0 + c0),
+                                        Ep + c0 * n, n, nrm2 + col0 + c0, demax, eR + c0, derr, eo,
+                                        nW2 ? nW2 + col0 + c0 : nullptr, q, tma);
+                   }));
+  ctx->mark("gemmW+recombE");
   int eEmax = 0, nedges = 0;
   std::vector<int> eE_col(nl);
   OZR_CK(cudaMemcpyAsync(eE_col.data(), eR, nl * sizeof(int32_t), cudaMemcpyDeviceToHost, s), "D2H eE");
@@ -1015,9 +1087,6 @@ ozr_status sweep(ozr_ctx ctx, Exchange* ex, const double* A, int64_t n, int64_t 
   }
   DigitOperand opQ{xdigT, ld, ld * n, kx};
   DigitOperand opE{rdig, ld, ld * nl, kE};
-  ctx->mark("~");
-  OZR_X(run_gemm(ctx, opQ, opE, N, NL, N, pt, planes, 2));
-  ctx->mark("gemmU");
   rep.kE = kE;
   rep.L_U = LU;
   const double pU = tilesU ? avg_pairs_U : static_cast<double>(count_pairs(gU));
@@ -1025,10 +1094,14 @@ ozr_status sweep(ozr_ctx ctx, Exchange* ex, const double* A, int64_t n, int64_t 
   ops += 2.0 * n * n * nl * pU;
   double* nu2 = ctx->ws<double>(S_NU2, n);
   OZR_ALLOC(nu2);
+  const int scaleU = 8 * (kx + kE - LU);
   ctx->mark("~");
-  launch_final(planes, nnl, N, NL, rp, rell, 8 * (kx + kE - LU), X1, n, X, ldx, nu2 + col0, wnext + col0, s);
-  OZR_CK(cudaGetLastError(), "final update");
-  ctx->mark("final");
+  OZR_X(run_banded(ctx, opQ, opE, N, NL, N, pt, planes, 2,
+                   [&](int64_t c0, int64_t c1, int t0, int tma, cudaStream_t q) {
+                     launch_final(planes + c0 * n, nnl, N, static_cast<int>(c1 - c0), shift_plan(rp, t0), rell + c0,
+                                  scaleU, X1 + c0 * n, n, X + c0 * ldx, ldx, nu2 + col0 + c0, wnext + col0 + c0, q, tma);
+                   }));
+  ctx->mark("gemmU+final");
   OZR_X(xgather(nu2, nl * sizeof(double)));
   OZR_X(xgather(nrm2, nl * sizeof(double)));
   std::vector<double> hR2, hW2;
@@ -1091,8 +1164,9 @@ ozr_status sweep(ozr_ctx ctx, Exchange* ex, const double* A, int64_t n, int64_t 
   rep.int8_ops = ops;
   rep.exchanges = nexch;
   ctx->dump();
-  // kernels of this sweep: [colmax] x1_split transpose GEMM recombine_V split GEMM recombine_E split GEMM final
-  rep.launches = (fresh_w ? 1 : 0) + 10 + cluster_launches + (new_A ? 2 : 0) + (P.form_R ? 2 : 0);
+  // kernels of this sweep: [colmax] x1_split transpose split_res split_E, and per column band of each of the
+  // three products its GEMM and its recombination (recombine_V / recombine_E / final)
+  rep.launches = (fresh_w ? 1 : 0) + 4 + 6 * band_count(NL) + cluster_launches + (new_A ? 2 : 0) + (P.form_R ? 2 : 0);
 #undef OZR_X
   return OZR_OK;
 }
@@ -1127,6 +1201,12 @@ ozr_status ozr_create(ozr_ctx* out, int device, void* stream, int64_t n_max) {
   cudaStreamCreateWithFlags(&c->xstream, cudaStreamNonBlocking);
   cudaEventCreateWithFlags(&c->ev_sync, cudaEventDisableTiming);
   for (int i = 0; i < 2; ++i) cudaEventCreateWithFlags(&c->xev[i], cudaEventDisableTiming);
+  {
+    int lo = 0, hi = 0;  // the recombination bands get the higher priority: their CTAs fill the SM room the
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);  // persistent GEMM leaves as soon as they are ready
+    cudaStreamCreateWithPriority(&c->rstream, cudaStreamNonBlocking, getenv("OZR_RPRIO0") ? lo : hi);
+  }
+  for (int i = 0; i < kMaxBands + 2; ++i) cudaEventCreateWithFlags(&c->bev[i], cudaEventDisableTiming);
   c->events = true;
   const char* tr = getenv("OZR_TRACE");
   c->trace = tr && tr[0] == '1';
@@ -1144,6 +1224,11 @@ void ozr_destroy(ozr_ctx ctx) {
     for (int i = 0; i < 10; ++i) cudaEventDestroy(ctx->ev[i]);
   for (int i = 0; i < 2; ++i) cudaEventDestroy(ctx->xev[i]);
   if (ctx->xstream) cudaStreamDestroy(ctx->xstream);
+  if (ctx->rstream) {
+    cudaStreamSynchronize(ctx->rstream);
+    cudaStreamDestroy(ctx->rstream);
+  }
+  for (int i = 0; i < kMaxBands + 2; ++i) cudaEventDestroy(ctx->bev[i]);
   if (ctx->ev_sync) cudaEventDestroy(ctx->ev_sync);
   delete ctx;
 }

@@ -103,3 +103,19 @@ def test_form_R_matches_oracle(ctx, cfg, n, start):
     assert abs(rep["normR_fro"] - info["normR_fro"]) <= 1e-6 * info["normR_fro"]
     assert abs(rep["normW_fro"] - info["normW_fro"]) <= 1e-6 * info["normW_fro"] + 1e-30
     assert rep["omega_oa"] == pytest.approx(2 * (rep["normW_fro"] + 2 * np.max(np.abs(lam0)) * rep["normR_fro"]))
+
+
+@pytest.mark.parametrize("cfg,start", [("c4p", "fp64"), ("c2", "fp32")])
+def test_column_bands_bit_identical(ctx, cfg, start, monkeypatch):
+    """The column-band pipeline of the slice products (ozr_api.cu run_banded, OZR_BANDS=k: band b's
+    recombination on the side stream next to band b + 1's GEMM, register path; the last band TMA-staged)
+    computes every column with the same arithmetic as the single launch: X̂, λ̂ and the report agree bit for
+    bit, including a sweep with unresolved groups (FP32 start)."""
+    A, lam0, X0 = _case(cfg, 4096, start)
+    X1, l1, r1 = _gpu_sweep(ctx, A, X0, lam0, 1e-12)
+    monkeypatch.setenv("OZR_BANDS", "4")
+    X4, l4, r4 = _gpu_sweep(ctx, A, X0, lam0, 1e-12)
+    assert np.array_equal(X1, X4) and np.array_equal(l1, l4)
+    for k in ("beta", "kX", "kA", "kR", "kE", "L_V", "L_W", "L_U", "n_clusters", "max_cluster"):
+        assert r1[k] == r4[k], k
+    assert r4["launches"] > r1["launches"]
