@@ -160,6 +160,8 @@ typedef struct {
   double omega_oa;                  /* form_R: ω = 2(‖W‖_F + 2·max|λ̂|·‖R‖_F), the Frobenius form of the
                                        OA-2018 cluster threshold 2(‖S − D̃‖ + ‖A‖‖R‖) (diagnostic, R13) */
   double theta;                     /* the θ this sweep used (params.theta, × 16 per escalation)       */
+  double update_2norm;              /* ozr_refine_to_tol at a stagnating ν: power-iteration estimate of
+                                       ‖X̂_k − X̂_{k−1}‖₂ (0 when not evaluated; R12)                     */
 } ozr_step_report;
 
 /* One sweep on columns [0, n): A (n x n, symmetric — only its columns are read), X (n x n, in/out:

@@ -222,7 +222,8 @@ def refine_to_tol(A, X0, lam0, delta, theta=THETA_DEFAULT, max_sweeps=6, beta_mo
     the paper's error model predicts ‖X − X_k‖ ≲ ν_k² max|λ̂| / (n gap) ≤ δ (eq. assume2 / gamma,
     PAPER.md:341-373 with ξ = n as in §4.1), or at stagnation (ν_k > ν_{k−1}/2 between two sweeps without
     unresolved groups: a Rayleigh–Ritz sub-solve (R13) rotates its group's columns, so its ν is not a
-    contraction measure), or at max_sweeps. Stagnation above δ with truncation on first escalates θ ← 16θ
+    contraction measure), or at max_sweeps. At a stagnating ν the update's 2-norm ‖X_k − X_{k−1}‖₂ ≤ δ
+    also stops (converged); otherwise, with truncation on, the driver first escalates θ ← 16θ
     (β two bits lower: the truncated iteration's noise floor is quadratic in the truncation) at most
     max_escalations times."""
     X, lam = np.asarray(X0, dtype=np.float64), np.asarray(lam0, dtype=np.float64)
@@ -239,7 +240,7 @@ def refine_to_tol(A, X0, lam0, delta, theta=THETA_DEFAULT, max_sweeps=6, beta_mo
         pred = nu * nu * np.max(np.abs(lamn)) / (n * gpos)
         rec = dict(sweep=k + 1, beta=info["beta"], alpha=info["alpha"], net_update=nu, predicted=pred,
                    normE_fro=info["normE_fro"], theta=theta)
-        X, lam = Xn, lamn
+        X_prev, X, lam = X, Xn, lamn
         if callback:
             rec.update(callback(X, lam))
         hist.append(rec)
@@ -250,6 +251,13 @@ def refine_to_tol(A, X0, lam0, delta, theta=THETA_DEFAULT, max_sweeps=6, beta_mo
             nu_prev = None
             continue
         if nu_prev is not None and nu > nu_prev / 2:
+            # stagnating Frobenius ν: the paper's measure is the 2-norm; the update's exact
+            # 2-norm decides (the library estimates it by power iteration)
+            d2 = float(np.linalg.norm(X - X_prev, 2))
+            rec["update_2norm"] = d2
+            if d2 <= delta:
+                rec["stop"] = "converged (2-norm of the update)"
+                break
             if truncate and max_escalations > 0:
                 max_escalations -= 1
                 theta = theta * 16.0

@@ -47,7 +47,7 @@ class StepReport(ctypes.Structure):
                 [(f, ctypes.c_double) for f in ["gap_min", "max_abs_lambda", "normE_fro", "net_update",
                                                  "predicted_error", "ms_total", "ms_gemm", "int8_ops"]] +
                 [("pairs_G", ctypes.c_int)] +
-                [(f, ctypes.c_double) for f in ["normR_fro", "normW_fro", "omega_oa", "theta"]])
+                [(f, ctypes.c_double) for f in ["normR_fro", "normW_fro", "omega_oa", "theta", "update_2norm"]])
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}

@@ -723,7 +723,8 @@ template <int NG>
 __global__ void __launch_bounds__(BS, 3)
     k_final(const int32_t* __restrict__ planes, long long pstride, int rows, const __grid_constant__ RecombPlan rp,
             const int32_t* __restrict__ ellB, int scale8, const double* __restrict__ X1, long long ldx1,
-            double* __restrict__ X, long long ldx, double* __restrict__ nu2, double* __restrict__ wnext, int use_tma) {
+            double* __restrict__ X, long long ldx, double* __restrict__ nu2, double* __restrict__ wnext, int use_tma,
+            double* __restrict__ D) {
   extern __shared__ __align__(128) unsigned char tsm[];
   __shared__ double sh[BS / 32];
   const int j = blockIdx.x;
@@ -742,6 +743,7 @@ __global__ void __launch_bounds__(BS, 3)
     s2 = __fma_rn(d, d, s2);
     m = fmax(m, fabs(xn));
     X[j * ldx + i] = xn;
+    if (D) D[static_cast<long long>(j) * rows + i] = d;  // the update, for its 2-norm estimate (R12)
   });
   s2 = block_sum(s2, sh);
   m = block_max(m, sh);
@@ -763,6 +765,61 @@ __global__ void __launch_bounds__(BS, 3)
                Ch[j * ldc + i] = v.hi;
                if (Cl) Cl[j * ldc + i] = v.lo;
              });
+}
+
+// ---------------------------------------------------------------- ‖D‖₂ by power iteration (R12)
+// D: rows x cols, column-major (ld = rows). y = D·v in PS column splits (partials, fixed order), z = Dᵀ·y
+// one CTA per column; all reductions deterministic.
+constexpr int PS = 64;
+__global__ void __launch_bounds__(BS) k_dv_part(const double* __restrict__ D, int rows, int cols,
+                                               const double* __restrict__ v, double* __restrict__ part) {
+  const int i = blockIdx.x * BS + threadIdx.x;
+  if (i >= rows) return;
+  const int per = (cols + PS - 1) / PS;
+  const int j0 = blockIdx.y * per, j1 = min(cols, j0 + per);
+  double acc = 0.0;
+  for (int j = j0; j < j1; ++j) acc = fma(D[static_cast<long long>(j) * rows + i], v[j], acc);
+  part[static_cast<long long>(blockIdx.y) * rows + i] = acc;
+}
+__global__ void k_dv_sum(const double* __restrict__ part, int rows, double* __restrict__ y) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= rows) return;
+  double acc = 0.0;
+  for (int q = 0; q < PS; ++q) acc += part[static_cast<long long>(q) * rows + i];
+  y[i] = acc;
+}
+__global__ void __launch_bounds__(BS) k_dtv(const double* __restrict__ D, int rows, const double* __restrict__ y,
+                                           double* __restrict__ z) {
+  __shared__ double sh[BS / 32];
+  const double* col = D + static_cast<long long>(blockIdx.x) * rows;
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < rows; i += BS) acc = fma(col[i], y[i], acc);
+  acc = block_sum(acc, sh);
+  if (threadIdx.x == 0) z[blockIdx.x] = acc;
+}
+// out[0] = Σ x_j² (one CTA, fixed order)
+__global__ void __launch_bounds__(BS) k_sumsq(const double* __restrict__ x, int n, double* __restrict__ out) {
+  __shared__ double sh[BS / 32];
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < n; i += BS) acc = fma(x[i], x[i], acc);
+  acc = block_sum(acc, sh);
+  if (threadIdx.x == 0) out[0] = acc;
+}
+// v = z / sqrt(nrm2[0]) (nrm2[0] > 0), or a deterministic start vector (seed: the global column index)
+__global__ void k_normalize(double* __restrict__ v, const double* __restrict__ z, int n, const double* __restrict__ nrm2,
+                            int col0) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  if (!z) {
+    unsigned int h = static_cast<unsigned int>(col0 + j) * 2654435761u;
+    h ^= h >> 15;
+    h *= 2246822519u;
+    h ^= h >> 13;
+    v[j] = (static_cast<double>(h & 0xFFFFFF) / 16777216.0) - 0.5;
+    return;
+  }
+  const double s = nrm2[0];
+  v[j] = s > 0.0 ? z[j] / sqrt(s) : 0.0;
 }
 
 }  // namespace
@@ -861,12 +918,12 @@ void launch_recombine_E(const int32_t* planes, long long pstride, int rows, int 
 }
 void launch_final(const int32_t* planes, long long pstride, int rows, int cols, const RecombPlan& rp,
                   const int32_t* ellB, int scale8, const double* X1, long long ldx1, double* X, long long ldx,
-                  double* nu2, double* wnext, cudaStream_t s, int allow_tma) {
+                  double* nu2, double* wnext, cudaStream_t s, int allow_tma, double* D) {
   init_attrs();
   const int tma = allow_tma && tma_ok(rp, planes, pstride, rows, X1, ldx1, X, ldx);
 #define OZR_FI(NG_)                                                                                                 \
   k_final<NG_><<<cols, BS, tma ? kTmaSmem : 0, s>>>(planes, pstride, rows, rp, ellB, scale8, X1, ldx1, X, ldx, nu2, wnext, \
-                                                    tma)
+                                                    tma, D)
   if (tma && rp.ngroups <= 4) OZR_FI(4);
   else if (tma && rp.ngroups <= 8) OZR_FI(8);
   else OZR_FI(12);
@@ -876,6 +933,17 @@ void launch_form_R(const int32_t* planes, long long pstride, int rows, int cols,
                    int scale8, int col0, const double* r_hi, const double* r_lo, double* R, long long ldr, double* nR2,
                    cudaStream_t s) {
   k_form_R<<<cols, BS, 0, s>>>(planes, pstride, rows, rp, g, scale8, col0, r_hi, r_lo, R, ldr, nR2);
+}
+void launch_norm2_step(const double* D, int rows, int cols, const double* v, double* part, double* y, cudaStream_t s) {
+  k_dv_part<<<dim3((rows + BS - 1) / BS, PS), BS, 0, s>>>(D, rows, cols, v, part);
+  k_dv_sum<<<(rows + 255) / 256, 256, 0, s>>>(part, rows, y);
+}
+void launch_norm2_back(const double* D, int rows, int cols, const double* y, double* z, cudaStream_t s) {
+  k_dtv<<<cols, BS, 0, s>>>(D, rows, y, z);
+}
+void launch_sumsq(const double* x, int n, double* out, cudaStream_t s) { k_sumsq<<<1, BS, 0, s>>>(x, n, out); }
+void launch_normalize(double* v, const double* z, int n, const double* nrm2, int col0, cudaStream_t s) {
+  k_normalize<<<(n + 255) / 256, 256, 0, s>>>(v, z, n, nrm2, col0);
 }
 void launch_iota(int* p, int n, cudaStream_t s) { k_iota<<<(n + 255) / 256, 256, 0, s>>>(p, n); }
 void launch_uf_flatten(int* parent, int n, cudaStream_t s) { k_uf_flatten<<<(n + 255) / 256, 256, 0, s>>>(parent, n); }

@@ -123,7 +123,7 @@ namespace {
 enum Slot {
   S_ADIG, S_AELL, S_W, S_X1, S_XDIG, S_XDIGT, S_G, S_SH, S_SL, S_RH, S_RL, S_PLANES, S_VH, S_VL, S_LAM, S_ER,
   S_ERR, S_EMAX, S_RDIG, S_RELL, S_EP, S_NRM2, S_NU2, S_WNEXT, S_ZEROELL, S_TMP1, S_TMP2, S_BELL, S_AT, S_ONES,
-  S_EDGES, S_ECOUNT, S_CINT, S_CDBL, S_CM, S_CR, S_CK, S_CV, S_CZ, S_CT, S_CSCR, S_CFLAG, S_SCAL, S_UFALL, S_CPART, S_GCNT, S_WA, S_GPLANES, S_RMAT, S_NR2, S_NW2, S_DWORK, S_DINFO
+  S_EDGES, S_ECOUNT, S_CINT, S_CDBL, S_CM, S_CR, S_CK, S_CV, S_CZ, S_CT, S_CSCR, S_CFLAG, S_SCAL, S_UFALL, S_CPART, S_GCNT, S_WA, S_GPLANES, S_RMAT, S_NR2, S_NW2, S_DWORK, S_DINFO, S_PI_V, S_PI_Z, S_PI_Y, S_PI_P, S_PI_S
 };
 
 ozr_status fail(ozr_ctx c, ozr_status st, const char* fmt, ...) {
@@ -552,8 +552,10 @@ void split_A_finish(const double* A, int64_t n, const std::vector<double>& hwA, 
 // ranks — their W_JJ / Ẽ_{:,J} blocks (all-reduce of zero-padded buffers, exact). Every host decision is
 // taken from all-gathered data in the 1-GPU order, so a P-rank sweep equals the 1-GPU sweep bit for bit
 // when nl is a multiple of the 256-column tile.
+// keepD: the final kernel also stores the update D = X̂_new − X̂_old of the rank's columns in the V buffer
+// (dead by then) for update_norm2.
 ozr_status sweep(ozr_ctx ctx, Exchange* ex, const double* A, int64_t n, int64_t lda, double* Xfull, int64_t ldx,
-                 double* lambda, const ozr_params& P, ozr_step_report& rep, SweepState& st) {
+                 double* lambda, const ozr_params& P, ozr_step_report& rep, SweepState& st, bool keepD = false) {
   memset(&rep, 0, sizeof rep);
   cudaStream_t s = ctx->stream;
   const int NP = ex ? ex->P : 1, RK = ex ? ex->rank : 0;
@@ -1099,7 +1101,8 @@ ozr_status sweep(ozr_ctx ctx, Exchange* ex, const double* A, int64_t n, int64_t 
   OZR_X(run_banded(ctx, opQ, opE, N, NL, N, pt, planes, 2,
                    [&](int64_t c0, int64_t c1, int t0, int tma, cudaStream_t q) {
                      launch_final(planes + c0 * n, nnl, N, static_cast<int>(c1 - c0), shift_plan(rp, t0), rell + c0,
-                                  scaleU, X1 + c0 * n, n, X + c0 * ldx, ldx, nu2 + col0 + c0, wnext + col0 + c0, q, tma);
+                                  scaleU, X1 + c0 * n, n, X + c0 * ldx, ldx, nu2 + col0 + c0, wnext + col0 + c0, q, tma,
+                                  keepD ? Vh + c0 * n : nullptr);
                    }));
   ctx->mark("gemmU+final");
   OZR_X(xgather(nu2, nl * sizeof(double)));
@@ -1168,6 +1171,47 @@ ozr_status sweep(ozr_ctx ctx, Exchange* ex, const double* A, int64_t n, int64_t 
   // three products its GEMM and its recombination (recombine_V / recombine_E / final)
   rep.launches = (fresh_w ? 1 : 0) + 4 + 6 * band_count(NL) + cluster_launches + (new_A ? 2 : 0) + (P.form_R ? 2 : 0);
 #undef OZR_X
+  return OZR_OK;
+}
+
+// ‖D‖₂ of the last sweep's update (stored by sweep(keepD)), by 12 power iterations on DᵀD from a fixed start
+// vector (R12): the stop rule's ν is a Frobenius norm, √n-pessimistic for a noise-like update, while the
+// paper's forward error is the 2-norm. Estimate from below (converges to σ_max). On P ranks D is
+// column-partitioned: D·v is all-reduced, Dᵀy is local.
+ozr_status update_norm2(ozr_ctx ctx, Exchange* ex, int64_t n, double* out) {
+  const int NP = ex ? ex->P : 1, RK = ex ? ex->rank : 0;
+  const int64_t nl = n / NP, col0 = RK * nl;
+  cudaStream_t s = ctx->stream;
+  const double* D = static_cast<const double*>(ctx->bufs[S_VH].p);
+  double* v = ctx->ws<double>(S_PI_V, nl);
+  double* z = ctx->ws<double>(S_PI_Z, nl);
+  double* y = ctx->ws<double>(S_PI_Y, n);
+  double* part = ctx->ws<double>(S_PI_P, 64 * static_cast<size_t>(n));
+  double* sc = ctx->ws<double>(S_PI_S, 2);
+  OZR_ALLOC(v); OZR_ALLOC(z); OZR_ALLOC(y); OZR_ALLOC(part); OZR_ALLOC(sc);
+  auto allsum = [&](double* b, size_t c) -> ozr_status {
+    if (ex && !ex->allreduce_sum(b, c, s)) return fail(ctx, OZR_ERR_COMM, "all-reduce: %s", ex->err.c_str());
+    return OZR_OK;
+  };
+  const int N = static_cast<int>(n), NL = static_cast<int>(nl);
+  launch_normalize(v, nullptr, NL, nullptr, static_cast<int>(col0), s);
+  launch_sumsq(v, NL, sc, s);
+  ozr_status e = allsum(sc, 1);
+  if (e != OZR_OK) return e;
+  launch_normalize(z, v, NL, sc, 0, s);  // z = v/‖v‖
+  for (int it = 0; it < 12; ++it) {
+    launch_norm2_step(D, N, NL, z, part, y, s);  // y = D z (this rank's columns)
+    if ((e = allsum(y, n)) != OZR_OK) return e;
+    launch_norm2_back(D, N, NL, y, v, s);  // v = Dᵀ y
+    launch_sumsq(v, NL, sc, s);
+    if ((e = allsum(sc, 1)) != OZR_OK) return e;
+    launch_normalize(z, v, NL, sc, 0, s);
+  }
+  OZR_CK(cudaGetLastError(), "update norm");
+  double h = 0.0;
+  OZR_CK(cudaMemcpyAsync(&h, sc, sizeof(double), cudaMemcpyDeviceToHost, s), "D2H");
+  OZR_CK(cudaStreamSynchronize(s), "sync");
+  *out = std::sqrt(std::sqrt(h));  // ‖DᵀD z‖ ≈ σ_max² for the unit z
   return OZR_OK;
 }
 
@@ -1497,7 +1541,7 @@ ozr_status ozr_refine_to_tol_dist(ozr_ctx ctx, ozr_comm comm, const double* A, i
   int escalations = 0;
   for (int k = 0; k < maxs; ++k) {
     ozr_step_report rep;
-    st = sweep(ctx, comm ? comm->ex.get() : nullptr, A, n, lda, X, ldx, lambda, P, rep, ss);
+    st = sweep(ctx, comm ? comm->ex.get() : nullptr, A, n, lda, X, ldx, lambda, P, rep, ss, true);
     rep.theta = P.theta;
     rep.sweep = k + 1;
     if (st != OZR_OK) {
@@ -1515,8 +1559,22 @@ ozr_status ozr_refine_to_tol_dist(ozr_ctx ctx, ozr_comm comm, const double* A, i
       continue;
     }
     if (nu_prev >= 0.0 && rep.net_update > nu_prev / 2) {
-      // the truncated iteration sits at its noise floor above δ (R12): lower it by 2 bits of β (θ × 16,
-      // the floor is quadratic in the truncation) and keep going; stagnation again → NOT_CONVERGED
+      // stagnation of the Frobenius ν above δ: the update's 2-norm (the paper's measure) may already be
+      // ≤ δ — a noise-like update has ‖D‖₂ ≈ 2‖D‖_F/√n (R12)
+      double d2 = 0.0;
+      st = update_norm2(ctx, comm ? comm->ex.get() : nullptr, n, &d2);
+      if (st != OZR_OK) {
+        if (sweeps_done) *sweeps_done = done;
+        return st;
+      }
+      rep.update_2norm = d2;
+      if (history && k < max_hist) history[k] = rep;
+      if (d2 <= params->delta) {
+        result = OZR_OK;
+        break;
+      }
+      // the truncated iteration sits at its noise floor above δ: lower it by 2 bits of β (θ × 16; the
+      // floor falls with the truncation) and keep going; stagnation again → NOT_CONVERGED
       if (P.truncate && escalations < params->max_escalations) {
         ++escalations;
         P.theta = (P.theta > 0 ? P.theta : 1.0) * 16.0;

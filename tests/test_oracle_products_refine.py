@@ -223,3 +223,40 @@ def test_form_R_and_W_vanish_on_exact_eigensystem():
     assert np.all(info["R"] == 0.0) and info["normR_fro"] == 0.0
     assert info["normW_fro"] == 0.0
     assert np.array_equal(lamn, lam) and np.array_equal(Xn, X)
+
+
+def test_driver_stop_rules(monkeypatch):
+    """Reading R12 (the paper gives no iteration rule): the oracle driver's decisions on scripted sweeps —
+    Frobenius ν ≤ δ stops; a stagnating ν (> ν_prev/2) stops as converged when the update's exact 2-norm is
+    ≤ δ (a noise-like n x n update has ‖D‖₂ ≈ 2‖D‖_F/√n), else escalates θ ← 16θ; a sweep with unresolved
+    groups (Rayleigh–Ritz rotation) never counts as stagnation."""
+    n = 64
+    rng = np.random.default_rng(0)
+    noise = rng.standard_normal((n, n))
+    script = []
+
+    def fake_sweep(A, X, lam, delta, theta, **kw):
+        scale, clusters = script.pop(0)
+        info = dict(beta=20, alpha=40, normE_fro=0.0, clusters=clusters)
+        D = scale * noise / np.linalg.norm(noise)  # ‖D‖_F = scale
+        info["net_update"] = float(np.linalg.norm(D))
+        return X + D, lam, info
+
+    monkeypatch.setattr(orf, "sweep", fake_sweep)
+    A, X0, lam0 = np.eye(n), np.eye(n), np.arange(n, dtype=float)
+    lam0[1] = 1e-20  # a tiny gap: the error model's prediction ν² max|λ̂|/(n gap) never stops the scripts
+    s2f = np.linalg.norm(noise, 2) / np.linalg.norm(noise)  # ‖D‖₂ / ‖D‖_F ≈ 2/√n
+    # stagnation at ν_F = 1e-8 with ‖D‖₂ = s2f·1e-8 ≤ δ = 1e-8·s2f·1.01: converged by the 2-norm
+    script[:] = [(1e-4, []), (1e-8, []), (0.9e-8, [])]
+    _, _, h = orf.refine_to_tol(A, X0, lam0, 1.01e-8 * s2f, max_sweeps=6)
+    assert len(h) == 3 and h[-1]["stop"].startswith("converged (2-norm")
+    assert abs(h[-1]["update_2norm"] / (0.9e-8 * s2f) - 1) < 1e-6  # X + D is rounded
+    # stagnation with ‖D‖₂ > δ: θ escalates (×16) twice, then NOT converged (stagnation)
+    script[:] = [(1e-4, []), (1e-8, []), (0.9e-8, []), (0.8e-8, []), (0.7e-8, []), (0.6e-8, []), (0.5e-8, [])]
+    _, _, h = orf.refine_to_tol(A, X0, lam0, 1e-12, max_sweeps=7)
+    assert [r["theta"] for r in h] == [4.0, 4.0, 4.0, 64.0, 64.0, 1024.0, 1024.0]
+    assert h[-1]["stop"] == "stagnation"
+    # cluster sweeps are not compared: ν rising through a Rayleigh–Ritz sweep keeps iterating
+    script[:] = [(1.0, [[0, 1]]), (2.0, [[0, 1]]), (1e-3, []), (1e-7, []), (1e-13, [])]
+    _, _, h = orf.refine_to_tol(A, X0, lam0, 1e-12, max_sweeps=6)
+    assert len(h) == 5 and h[-1]["stop"] == "converged"
