@@ -233,17 +233,32 @@ constexpr int STAGES2 = 6;
 constexpr int B_HALF_BYTES = (BN / 2) * BK;
 constexpr int SMEM2_BYTES = STAGES2 * (A_STAGE_BYTES + B_HALF_BYTES) + 1024 /*align*/ + 512 /*barriers*/;
 
-__device__ __forceinline__ JobInfo job_info2(int job, const PairTable& pt, int N, int tiles_m2) {
+// order 0: (band, m-tile, n-tile, group) — a tile's groups back to back;
+// order 1: (band, m-tile, group, n-tile) — the band's n-tiles of one group back to back: those jobs read the
+// same A rows and planes at the same time (A is the larger operand: k_A planes vs k_X), so each A K-block is
+// fetched from DRAM once and served to all BAND readers from L2.
+__device__ __forceinline__ JobInfo job_info2(int job, const PairTable& pt, int N, int tiles_m2, int order, int BANDW) {
   const int G = pt.ngroups;
-  JobInfo ji;
-  ji.g = job % G;
-  const int tile = job / G;
   const int tiles_n = (N + BN - 1) / BN;
-  const int band = tile / (BAND * tiles_m2);
-  const int r = tile - band * (BAND * tiles_m2);
-  const int nb = min(BAND, tiles_n - band * BAND);
-  ji.m0 = (r / nb) * (2 * BM);  // the pair's 256 rows
-  ji.n0 = (band * BAND + r % nb) * BN;
+  JobInfo ji;
+  if (order & 1) {
+    const int per_band = tiles_m2 * BANDW * G;
+    const int band = job / per_band;
+    const int r = job - band * per_band;
+    const int nb = min(BANDW, tiles_n - band * BANDW);
+    const int q = r / nb;
+    ji.g = q % G;
+    ji.m0 = (q / G) * (2 * BM);
+    ji.n0 = (band * BANDW + r % nb) * BN;
+  } else {
+    ji.g = job % G;
+    const int tile = job / G;
+    const int band = tile / (BANDW * tiles_m2);
+    const int r = tile - band * (BANDW * tiles_m2);
+    const int nb = min(BANDW, tiles_n - band * BANDW);
+    ji.m0 = (r / nb) * (2 * BM);  // the pair's 256 rows
+    ji.n0 = (band * BANDW + r % nb) * BN;
+  }
   ji.skip = (pt.tile_budgets && pt.diag[ji.g] > pt.tileL[ji.n0 / BN]) ? 1 : 0;
   return ji;
 }
@@ -251,7 +266,8 @@ __device__ __forceinline__ JobInfo job_info2(int job, const PairTable& pt, int N
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NWARPS * 32, 1)
     k_gemm_i8_2sm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                   const __grid_constant__ PairTable pt, int32_t* __restrict__ out, long long out_plane_stride,
-                  long long ldo, int M, int N, int K, int tiles_m2, int njobs, int* __restrict__ job_counter) {
+                  long long ldo, int M, int N, int K, int tiles_m2, int njobs, int* __restrict__ job_counter,
+                  int l2hint, int order, int bandw) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
@@ -301,6 +317,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NWARPS * 32, 1)
   if (warp == 0) {
     if (lane == 0) {
       // ---------------- job fetch (leader) + TMA producer (both CTAs)
+      // L2 policies (l2hint bit 0: A rows evict-first — they are reused only by the jobs in flight on the same
+      // m-tile; bit 1: the band's B columns evict-last — reused by every m-tile of the band)
+      const uint64_t polA = (l2hint & 1) ? l2_policy_evict_first() : l2_policy_evict_normal();
+      const uint64_t polB = (l2hint & 2) ? l2_policy_evict_last() : l2_policy_evict_normal();
       int it = 0;
       for (int jn = 0;; ++jn) {
         const int slot = jn % JQ;
@@ -320,21 +340,32 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NWARPS * 32, 1)
           mbar_arrive_remote(mapa_u32(&jq_empty[slot], 0));
         }
         if (job < 0) break;
-        const JobInfo ji = job_info2(job, pt, N, tiles_m2);
+        const JobInfo ji = job_info2(job, pt, N, tiles_m2, order, bandw);
         if (ji.skip) continue;
         const int p0 = pt.first[ji.g];
-        const int total = (pt.first[ji.g + 1] - p0) * nkb;
+        const int npg = pt.first[ji.g + 1] - p0;
+        const int total = npg * nkb;
+        const bool kouter = (order & 2) != 0;
         for (int q = 0; q < total; ++q, ++it) {
           const int stage = it % STAGES2;
           const uint32_t phase = (it / STAGES2) & 1;
           mbar_wait(&empty[stage], phase ^ 1);
           if (leader) mbar_arrive_expect_tx(&full[stage], 2 * (A_STAGE_BYTES + B_HALF_BYTES));
-          const int p = p0 + q / nkb;
-          const int kb = q - (q / nkb) * nkb;
+          // kouter: K-block outer, the group's pairs inner — at any moment every job of a tile's neighbourhood
+          // reads the same K-block of the A planes, so L2 serves them all from one DRAM fetch
+          int p, kb;
+          if (kouter) {
+            kb = q / npg;
+            p = p0 + (q - kb * npg);
+          } else {
+            p = p0 + q / nkb;
+            kb = q - (q / nkb) * nkb;
+          }
           const uint32_t fb = mapa_u32(&full[stage], 0);  // the leader's barrier counts both CTAs' bytes
-          tma_load_3d_2sm(sA + stage * A_STAGE_BYTES, &tmA, fb, kb * BK, ji.m0 + static_cast<int>(rank) * BM, pt.s[p]);
-          tma_load_3d_2sm(sB + stage * B_HALF_BYTES, &tmB, fb, kb * BK, ji.n0 + static_cast<int>(rank) * (BN / 2),
-                          pt.t[p]);
+          tma_load_3d_2sm_hint(sA + stage * A_STAGE_BYTES, &tmA, fb, kb * BK, ji.m0 + static_cast<int>(rank) * BM,
+                               pt.s[p], polA);
+          tma_load_3d_2sm_hint(sB + stage * B_HALF_BYTES, &tmB, fb, kb * BK, ji.n0 + static_cast<int>(rank) * (BN / 2),
+                               pt.t[p], polB);
         }
       }
     }
@@ -350,7 +381,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NWARPS * 32, 1)
         const int job = *reinterpret_cast<volatile int*>(&jq[slot]);
         mbar_arrive(&jq_empty[slot]);
         if (job < 0) break;
-        const JobInfo ji = job_info2(job, pt, N, tiles_m2);
+        const JobInfo ji = job_info2(job, pt, N, tiles_m2, order, bandw);
         if (ji.skip) continue;
         const int buf = t & 1;
         mbar_wait_cluster(&acc_empty[buf], ((t >> 1) & 1) ^ 1);  // both CTAs' epilogues drained it
@@ -391,7 +422,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NWARPS * 32, 1)
         else mbar_arrive_remote(mapa_u32(&jq_empty[slot], 0));
       }
       if (job < 0) break;
-      const JobInfo ji = job_info2(job, pt, N, tiles_m2);
+      const JobInfo ji = job_info2(job, pt, N, tiles_m2, order, bandw);
       if (ji.skip) continue;
       const int buf = t & 1;
       mbar_wait(&acc_full[buf], (t >> 1) & 1);
@@ -482,7 +513,7 @@ bool make_tmap(CUtensorMap* tm, const DigitOperand& op, int K, int cols, int box
 
 cudaError_t launch_gemm_i8(const DigitOperand& A, const DigitOperand& B, int M, int N, int K,
                            const PairTable& pt, int32_t* out, int64_t out_plane_stride, int64_t ldo,
-                           cudaStream_t stream, int* job_counter) {
+                           cudaStream_t stream, int* job_counter, int job_order) {
   if (M <= 0 || N <= 0 || pt.ngroups <= 0) return cudaSuccess;
   if (K <= 0 || (A.ld % 16) || (B.ld % 16) || (A.plane_stride % 16) || (B.plane_stride % 16))
     return cudaErrorInvalidValue;
@@ -525,9 +556,20 @@ cudaError_t launch_gemm_i8(const DigitOperand& A, const DigitOperand& B, int M, 
     if (!job_counter) return cudaErrorInvalidValue;
     cudaError_t e = cudaMemsetAsync(job_counter, 0, sizeof(int), stream);
     if (e != cudaSuccess) return e;
+    // L2 policy: the band's B columns evict-last (measured: V launch DRAM read 30.3 → 18.2 GB with job order 1)
+    static int l2hint = -1, env_order = -1, bandw = BAND;
+    if (l2hint < 0) {
+      const char* h = getenv("OZR_L2HINT");
+      l2hint = h ? atoi(h) : 2;
+      const char* o = getenv("OZR_GEMM_ORDER");
+      env_order = o ? atoi(o) : -1;
+      const char* b = getenv("OZR_GEMM_BAND");
+      bandw = b ? atoi(b) : BAND;
+    }
+    const int order = env_order >= 0 ? env_order : (job_order >= 0 ? job_order : 1);
     k_gemm_i8_2sm<<<2 * clusters, NWARPS * 32, SMEM2_BYTES, stream>>>(tmA, tmB, pt, out, out_plane_stride, ldo, M, N,
                                                                        K, tiles_m2, static_cast<int>(jobs2),
-                                                                       job_counter);
+                                                                       job_counter, l2hint, order, bandw);
     return cudaGetLastError();
   }
   const int grid = static_cast<int>(std::min<long long>(jobs, nsm));

@@ -463,7 +463,8 @@ ozr_status run_banded(ozr_ctx ctx, const DigitOperand& A, const DigitOperand& B,
       for (int64_t t = t0; t < std::min<int64_t>(tiles, t0 + tpb); ++t) ptb.tileL[t - t0] = pt.tileL[t];
     DigitOperand Bb{B.base + c0 * B.ld, B.ld, B.plane_stride, B.nplanes};
     OZR_CK(launch_gemm_i8(A, Bb, M, static_cast<int>(c1 - c0), K, ptb, planes + c0 * M,
-                          static_cast<int64_t>(M) * N, M, s, cnt), "slice GEMM band");
+                          static_cast<int64_t>(M) * N, M, s, cnt, A.nplanes > B.nplanes ? 3 : 1),
+           "slice GEMM band");
     const bool last = c1 >= N;
     if (last) {
       cudaEventRecord(ctx->ev[3 + 2 * idx], s);

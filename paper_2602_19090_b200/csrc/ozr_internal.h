@@ -39,9 +39,13 @@ struct DigitOperand {
 // column-major, leading dim ldo) = Σ_{pairs} A_s^T-tile products over K.
 //   A: M "columns" of K bytes each (A operand, K-major), B: N columns of K bytes (B operand, K-major).
 // job_counter: a device int owned by the caller (one per stream/context), reset by the launcher.
+// job_order (CTA-pair form): bit 0 — the BAND n-tiles of one pair group run back to back (they read the same
+// A rows and planes at the same time); bit 1 — K-block outer, the group's pairs inner (every job near a tile
+// reads the same A K-block at once). Measured best: 3 when the A operand has more planes than B (V = A·X̂),
+// else 1 (W, U). −1: 1 (OZR_GEMM_ORDER overrides for experiments).
 cudaError_t launch_gemm_i8(const DigitOperand& A, const DigitOperand& B, int M, int N, int K,
                            const PairTable& pt, int32_t* out, int64_t out_plane_stride, int64_t ldo,
-                           cudaStream_t stream, int* job_counter);
+                           cudaStream_t stream, int* job_counter, int job_order = -1);
 
 // Reference (SIMT) version of the same contract; used only by the dev harness to cross-check the
 // tensor-core kernel on the GPU. Not on the product path.
