@@ -14,6 +14,7 @@
 //   k_recombine_E     W → Ẽ (Alg. 1 line 5), scaled Ẽ' = diag(2^g)Ẽ, column maxima, ‖Ẽ‖_F parts
 //   k_final           U = X̂^(1)Ẽ → X̂ ← RN(X̂^(1) + U) (Alg. 1 line 6, accsum), ν, column maxima
 //   k_recombine_dd    generic recombination for ozr_gemm
+#include <algorithm>
 #include <cstdint>
 #include <cstdlib>
 #include <cuda_runtime.h>
@@ -822,6 +823,18 @@ __global__ void k_normalize(double* __restrict__ v, const double* __restrict__ z
   v[j] = s > 0.0 ? z[j] / sqrt(s) : 0.0;
 }
 
+// small host <-> device transfers through mapped pinned memory (no copy engine involved)
+__global__ void k_copy_bytes(char* __restrict__ dst, const char* __restrict__ src, size_t bytes, int a8) {
+  const size_t t = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x, st = static_cast<size_t>(gridDim.x) * blockDim.x;
+  if (a8) {
+    const size_t n8 = bytes / 8;
+    for (size_t i = t; i < n8; i += st)
+      reinterpret_cast<unsigned long long*>(dst)[i] = reinterpret_cast<const unsigned long long*>(src)[i];
+  } else {
+    for (size_t i = t; i < bytes; i += st) dst[i] = src[i];
+  }
+}
+
 }  // namespace
 
 // ---------------------------------------------------------------- launchers
@@ -944,6 +957,13 @@ void launch_norm2_back(const double* D, int rows, int cols, const double* y, dou
 void launch_sumsq(const double* x, int n, double* out, cudaStream_t s) { k_sumsq<<<1, BS, 0, s>>>(x, n, out); }
 void launch_normalize(double* v, const double* z, int n, const double* nrm2, int col0, cudaStream_t s) {
   k_normalize<<<(n + 255) / 256, 256, 0, s>>>(v, z, n, nrm2, col0);
+}
+void launch_copy_bytes(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+  if (bytes == 0) return;
+  const bool a8 = ((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src) | bytes) & 7) == 0;
+  const size_t units = a8 ? bytes / 8 : bytes;
+  const int grid = static_cast<int>(std::min<size_t>((units + 255) / 256, 1024));
+  k_copy_bytes<<<grid, 256, 0, s>>>(static_cast<char*>(dst), static_cast<const char*>(src), bytes, a8 ? 1 : 0);
 }
 void launch_iota(int* p, int n, cudaStream_t s) { k_iota<<<(n + 255) / 256, 256, 0, s>>>(p, n); }
 void launch_uf_flatten(int* parent, int n, cudaStream_t s) { k_uf_flatten<<<(n + 255) / 256, 256, 0, s>>>(parent, n); }

@@ -55,6 +55,8 @@ struct EdgeOut {
   int* any;
 };
 void launch_iota(int* p, int n, cudaStream_t s);
+// dst/src: device-accessible (device or mapped pinned host memory); 8-byte units when all are 8-aligned
+void launch_copy_bytes(void* dst, const void* src, size_t bytes, cudaStream_t s);
 void launch_uf_flatten(int* parent, int n, cudaStream_t s);  // parent[i] ← root of i
 void launch_recombine_E(const int32_t* planes, long long pstride, int rows, int cols, const RecombPlan& rp,
                         const int32_t* ellA, const int32_t* ellB, int scale8, const double* r_hi, const double* lam,

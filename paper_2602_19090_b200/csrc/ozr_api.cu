@@ -56,6 +56,42 @@ struct ozr_ctx_s {
   cudaStream_t rstream = nullptr;
   cudaEvent_t bev[kMaxBands + 2];
   DenseEig dense;  // cuSOLVER handle of the dense cluster sub-solve (created on first use)
+  // Host staging of the sweep's small reads and writes (mapped pinned memory, moved by a kernel — not by a
+  // copy engine, which may be busy with a caller's large transfers on another stream): d2h() queues a read
+  // that lands in `dst` at the next flush(), after the synchronisation that covers it.
+  char* hst = nullptr;
+  size_t hst_cap = 0, hst_off = 0;
+  struct Pend {
+    void* dst;
+    const char* src;
+    size_t n;
+  };
+  std::vector<Pend> pend;
+  char* stage(size_t bytes) {
+    const size_t off = (hst_off + 15) & ~static_cast<size_t>(15);
+    if (off + bytes > hst_cap) return nullptr;
+    hst_off = off + bytes;
+    return hst + off;
+  }
+  bool d2h(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+    char* st = stage(bytes);
+    if (!st) return false;
+    ozr::launch_copy_bytes(st, src, bytes, s);
+    pend.push_back({dst, st, bytes});
+    return true;
+  }
+  bool h2d(void* ddst, const void* src, size_t bytes, cudaStream_t s) {
+    char* st = stage(bytes);
+    if (!st) return false;
+    memcpy(st, src, bytes);
+    ozr::launch_copy_bytes(ddst, st, bytes, s);
+    return true;
+  }
+  void flush() {
+    for (auto& p : pend) memcpy(p.dst, p.src, p.n);
+    pend.clear();
+    hst_off = 0;
+  }
   bool events = false;
   // tracing (OZR_TRACE=1): named events between the kernels of a sweep, printed to stderr per sweep
   bool trace = false;
@@ -147,6 +183,18 @@ ozr_status cuda_check(ozr_ctx c, cudaError_t e, const char* what) {
   do {                                                      \
     ozr_status st__ = cuda_check(ctx, (expr), (what));      \
     if (st__ != OZR_OK) return st__;                        \
+  } while (0)
+// staged small transfers; a transfer larger than the staging area (the cluster branch's packed upload for
+// very large groups) falls back to a plain (synchronous, pageable) copy
+#define OZR_D2H(dst, src, bytes)                                                                               \
+  do {                                                                                                         \
+    if (!ctx->d2h((dst), (src), (bytes), s))                                                                   \
+      OZR_CK(cudaMemcpyAsync((dst), (src), (bytes), cudaMemcpyDeviceToHost, s), "D2H");                     \
+  } while (0)
+#define OZR_H2D(dst, src, bytes)                                                                               \
+  do {                                                                                                         \
+    if (!ctx->h2d((dst), (src), (bytes), s))                                                                   \
+      OZR_CK(cudaMemcpyAsync((dst), (src), (bytes), cudaMemcpyHostToDevice, s), "H2D");                     \
   } while (0)
 #define OZR_ALLOC(ptr)                                                        \
   do {                                                                        \
@@ -571,6 +619,19 @@ ozr_status sweep(ozr_ctx ctx, Exchange* ex, const double* A, int64_t n, int64_t 
   double ops = 0.0;
   int nexch = 0;
 
+  {  // host staging: the largest phase reads ~5 n-vectors (+ the P·n union-find labels)
+    const size_t need = 48 * static_cast<size_t>(n) + 8 * static_cast<size_t>(NP) * n + (1 << 20);
+    if (ctx->hst_cap < need) {
+      OZR_CK(cudaStreamSynchronize(s), "sync");
+      if (ctx->hst) cudaFreeHost(ctx->hst);
+      ctx->hst = nullptr;
+      ctx->hst_cap = 0;
+      OZR_CK(cudaHostAlloc(reinterpret_cast<void**>(&ctx->hst), need, cudaHostAllocMapped), "host staging");
+      ctx->hst_cap = need;
+    }
+    ctx->pend.clear();
+    ctx->hst_off = 0;
+  }
   int* derr = ctx->ws<int>(S_ERR, 4);
   int* demax = ctx->ws<int>(S_EMAX, 4);
   int* scal = ctx->ws<int>(S_SCAL, 4 * static_cast<size_t>(NP) + 4);
@@ -608,13 +669,14 @@ ozr_status sweep(ozr_ctx ctx, Exchange* ex, const double* A, int64_t n, int64_t 
     ozr_status e = xgather(scal + 0, 4 * sizeof(int));
     if (e != OZR_OK) return e;
     std::vector<int> h(4 * NP);
-    OZR_CK(cudaMemcpyAsync(h.data(), scal, h.size() * sizeof(int), cudaMemcpyDeviceToHost, s), "D2H");
+    OZR_D2H(h.data(), scal, h.size() * sizeof(int));
     OZR_CK(cudaEventRecord(ctx->ev_sync, s), "event");
     if (post) {
       ozr_status pe = post();
       if (pe != OZR_OK) return pe;
     }
     OZR_CK(cudaEventSynchronize(ctx->ev_sync), "sync");
+    ctx->flush();
     int bits = 0;
     for (int r = 0; r < NP; ++r) bits |= h[4 * r + 3];
     for (int q = 0; q < k; ++q) {
@@ -649,11 +711,11 @@ ozr_status sweep(ozr_ctx ctx, Exchange* ex, const double* A, int64_t n, int64_t 
     launch_colmax(A, lda, N, N, wA, derr, s);
     OZR_CK(cudaGetLastError(), "colmax A");
     hwA.resize(n);
-    OZR_CK(cudaMemcpyAsync(hwA.data(), wA, n * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H wA");
+    OZR_D2H(hwA.data(), wA, n * sizeof(double));
   }
   std::vector<double> hw(n), hlam(n);
-  OZR_CK(cudaMemcpyAsync(hw.data(), w, n * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H w");
-  OZR_CK(cudaMemcpyAsync(hlam.data(), lambda, n * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H lambda");
+  OZR_D2H(hw.data(), w, n * sizeof(double));
+  OZR_D2H(hlam.data(), lambda, n * sizeof(double));
   OZR_X(scalars({}, nullptr, [&]() -> ozr_status {
     ctx->mark("~");
     return new_A ? split_A_launch(ctx, A, n, lda, P.kA_split, derr, hell) : OZR_OK;
@@ -763,7 +825,7 @@ ozr_status sweep(ozr_ctx ctx, Exchange* ex, const double* A, int64_t n, int64_t 
   int32_t* eR = ctx->ws<int32_t>(S_ER, nl);
   OZR_ALLOC(Vh); OZR_ALLOC(Vl); OZR_ALLOC(lam); OZR_ALLOC(eR);
   const int intmin = -(1 << 30);
-  OZR_CK(cudaMemcpyAsync(demax, &intmin, sizeof(int), cudaMemcpyHostToDevice, s), "H2D");
+  OZR_H2D(demax, &intmin, sizeof(int));
   const int32_t* aell = reinterpret_cast<const int32_t*>(ctx->bufs[S_AELL].p);
   const int scaleV = 8 * (st.kA_split + kx - LV);
   ctx->mark("~");
@@ -812,8 +874,8 @@ ozr_status sweep(ozr_ctx ctx, Exchange* ex, const double* A, int64_t n, int64_t 
   int eRmax = 0;
   std::vector<double> hlam_new(n);
   std::vector<int> eR_col(nl);
-  OZR_CK(cudaMemcpyAsync(hlam_new.data(), lam, n * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H");
-  OZR_CK(cudaMemcpyAsync(eR_col.data(), eR, nl * sizeof(int32_t), cudaMemcpyDeviceToHost, s), "D2H eR");
+  OZR_D2H(hlam_new.data(), lam, n * sizeof(double));
+  OZR_D2H(eR_col.data(), eR, nl * sizeof(int32_t));
   // one synchronisation for λ̂, the Res exponents and their maximum; the digit transpose (A operand of
   // X̂Ẽ, after the exchange) runs meanwhile
   OZR_X(scalars({demax}, &eRmax));
@@ -869,7 +931,7 @@ ozr_status sweep(ozr_ctx ctx, Exchange* ex, const double* A, int64_t n, int64_t 
   double* Ep = ctx->ws<double>(S_EP, nnl);
   double* nrm2 = ctx->ws<double>(S_NRM2, n);
   OZR_ALLOC(Ep); OZR_ALLOC(nrm2);
-  OZR_CK(cudaMemcpyAsync(demax, &intmin, sizeof(int), cudaMemcpyHostToDevice, s), "H2D");
+  OZR_H2D(demax, &intmin, sizeof(int));
   int* uf = ctx->ws<int>(S_EDGES, n);
   int* ecount = ctx->ws<int>(S_ECOUNT, 4);
   OZR_ALLOC(uf); OZR_ALLOC(ecount);
@@ -890,7 +952,7 @@ ozr_status sweep(ozr_ctx ctx, Exchange* ex, const double* A, int64_t n, int64_t 
   ctx->mark("gemmW+recombE");
   int eEmax = 0, nedges = 0;
   std::vector<int> eE_col(nl);
-  OZR_CK(cudaMemcpyAsync(eE_col.data(), eR, nl * sizeof(int32_t), cudaMemcpyDeviceToHost, s), "D2H eE");
+  OZR_D2H(eE_col.data(), eR, nl * sizeof(int32_t));
   {
     int o2[2];
     OZR_X(scalars({demax, ecount}, o2));
@@ -906,16 +968,18 @@ ozr_status sweep(ozr_ctx ctx, Exchange* ex, const double* A, int64_t n, int64_t 
     launch_uf_flatten(uf, N, s);
     std::vector<int> root(n);
     if (NP == 1) {
-      OZR_CK(cudaMemcpyAsync(root.data(), uf, n * sizeof(int), cudaMemcpyDeviceToHost, s), "D2H labels");
+      OZR_D2H(root.data(), uf, n * sizeof(int));
       OZR_CK(cudaStreamSynchronize(s), "sync");
+      ctx->flush();
     } else {  // every rank's partition of the pairs it saw → one union on the host, in rank order
       int* ufall = ctx->ws<int>(S_UFALL, static_cast<size_t>(NP) * n);
       OZR_ALLOC(ufall);
       OZR_CK(cudaMemcpyAsync(ufall + RK * n, uf, n * sizeof(int), cudaMemcpyDeviceToDevice, s), "D2D");
       OZR_X(xgather(ufall, n * sizeof(int)));
       std::vector<int> lab(static_cast<size_t>(NP) * n);
-      OZR_CK(cudaMemcpyAsync(lab.data(), ufall, lab.size() * sizeof(int), cudaMemcpyDeviceToHost, s), "D2H labels");
+      OZR_D2H(lab.data(), ufall, lab.size() * sizeof(int));
       OZR_CK(cudaStreamSynchronize(s), "sync");
+      ctx->flush();
       for (int64_t i = 0; i < n; ++i) root[i] = static_cast<int>(i);
       auto find = [&](int a) {
         while (root[a] != a) {
@@ -981,8 +1045,8 @@ ozr_status sweep(ozr_ctx ctx, Exchange* ex, const double* A, int64_t n, int64_t 
       double* cT = ctx->ws<double>(S_CT, static_cast<size_t>(nmem) * n);
       OZR_ALLOC(dpk); OZR_ALLOC(dmu); OZR_ALLOC(cM); OZR_ALLOC(cR); OZR_ALLOC(cK); OZR_ALLOC(cV); OZR_ALLOC(cZ);
       OZR_ALLOC(cT);
-      OZR_CK(cudaMemcpyAsync(dpk, pk.data(), pk.size() * sizeof(int), cudaMemcpyHostToDevice, s), "H2D");
-      OZR_CK(cudaMemcpyAsync(dmu, mu.data(), ng * sizeof(double), cudaMemcpyHostToDevice, s), "H2D");
+      OZR_H2D(dpk, pk.data(), pk.size() * sizeof(int));
+      OZR_H2D(dmu, mu.data(), ng * sizeof(double));
       ClusterLaunch L{};
       L.ngroups = ng;
       L.nmembers = nmem;
@@ -1052,8 +1116,8 @@ ozr_status sweep(ozr_ctx ctx, Exchange* ex, const double* A, int64_t n, int64_t 
       OZR_CK(launch_cluster_apply(L, s), "cluster apply");
       ctx->mark("cluster");
       cluster_launches += 6;
-      OZR_CK(cudaMemcpyAsync(hlam_new.data(), lam, n * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H");
-      OZR_CK(cudaMemcpyAsync(eE_col.data(), eR, nl * sizeof(int32_t), cudaMemcpyDeviceToHost, s), "D2H eE");
+      OZR_D2H(hlam_new.data(), lam, n * sizeof(double));
+      OZR_D2H(eE_col.data(), eR, nl * sizeof(int32_t));
       OZR_X(scalars({demax}, &eEmax));
       rep.n_clusters = ng;
       rep.max_cluster = mmax;
@@ -1114,14 +1178,14 @@ ozr_status sweep(ozr_ctx ctx, Exchange* ex, const double* A, int64_t n, int64_t 
     OZR_X(xgather(nW2, nl * sizeof(double)));
     hR2.resize(n);
     hW2.resize(n);
-    OZR_CK(cudaMemcpyAsync(hR2.data(), nR2, n * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H");
-    OZR_CK(cudaMemcpyAsync(hW2.data(), nW2, n * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H");
+    OZR_D2H(hR2.data(), nR2, n * sizeof(double));
+    OZR_D2H(hW2.data(), nW2, n * sizeof(double));
   }
   OZR_CK(cudaMemcpyAsync(lambda, lam, n * sizeof(double), cudaMemcpyDeviceToDevice, s), "copy lambda");
   cudaEventRecord(ctx->ev[1], s);
   std::vector<double> hnu(n), hnrm(n);
-  OZR_CK(cudaMemcpyAsync(hnu.data(), nu2, n * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H");
-  OZR_CK(cudaMemcpyAsync(hnrm.data(), nrm2, n * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H");
+  OZR_D2H(hnu.data(), nu2, n * sizeof(double));
+  OZR_D2H(hnrm.data(), nrm2, n * sizeof(double));
   OZR_X(scalars({}, nullptr));
   ctx->mark("~end");
   double nu = 0.0, ne = 0.0;
@@ -1155,7 +1219,7 @@ ozr_status sweep(ozr_ctx ctx, Exchange* ex, const double* A, int64_t n, int64_t 
   rep.predicted_error = rep.net_update * rep.net_update * maxlam_new / (static_cast<double>(n) * gap_out);
   if (ex) {  // report the global pair budgets (each rank planned its own column tiles)
     int hv[3] = {rep.L_V, rep.L_W, rep.L_U}, gv[3];
-    OZR_CK(cudaMemcpyAsync(scal + 4 * NP, hv, sizeof hv, cudaMemcpyHostToDevice, s), "H2D");
+    OZR_H2D(scal + 4 * NP, hv, sizeof hv);
     int* d = scal + 4 * NP;
     OZR_X(scalars({d, d + 1, d + 2}, gv));
     rep.L_V = gv[0];
@@ -1210,8 +1274,11 @@ ozr_status update_norm2(ozr_ctx ctx, Exchange* ex, int64_t n, double* out) {
   }
   OZR_CK(cudaGetLastError(), "update norm");
   double h = 0.0;
-  OZR_CK(cudaMemcpyAsync(&h, sc, sizeof(double), cudaMemcpyDeviceToHost, s), "D2H");
+  ctx->pend.clear();
+  ctx->hst_off = 0;
+  OZR_D2H(&h, sc, sizeof(double));
   OZR_CK(cudaStreamSynchronize(s), "sync");
+  ctx->flush();
   *out = std::sqrt(std::sqrt(h));  // ‖DᵀD z‖ ≈ σ_max² for the unit z
   return OZR_OK;
 }
@@ -1275,6 +1342,7 @@ void ozr_destroy(ozr_ctx ctx) {
   }
   for (int i = 0; i < kMaxBands + 2; ++i) cudaEventDestroy(ctx->bev[i]);
   if (ctx->ev_sync) cudaEventDestroy(ctx->ev_sync);
+  if (ctx->hst) cudaFreeHost(ctx->hst);
   delete ctx;
 }
 
