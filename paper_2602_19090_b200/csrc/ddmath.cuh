@@ -86,6 +86,18 @@ __device__ __forceinline__ double i128_to_f64(i128 x) {
   }
   return neg ? -r : r;
 }
+// RN(L0·2^32 + L1) for |L0|, |L1| < 2^55 (two recombination limbs) without 128-bit arithmetic: with
+// s = L0 + ⌊L1/2^32⌋ and b = L1 mod 2^32 the value is s·2^32 + b. For |s| < 2^47 both are exact doubles and
+// one fma rounds once; otherwise the value has ≥ 80 bits, so its bits below 2^25 only act as a sticky bit:
+// RN((s·2^7 + ⌊b/2^25⌋) | sticky)·2^25.
+__device__ __forceinline__ double limbs2_rn(long long L0, long long L1) {
+  const long long s = L0 + (L1 >> 32);
+  const unsigned long long b = static_cast<unsigned long long>(L1) & 0xFFFFFFFFull;
+  if (s > -(1LL << 47) && s < (1LL << 47)) return fma(static_cast<double>(s), 4294967296.0, static_cast<double>(b));
+  long long t = s * 128 + static_cast<long long>(b >> 25);
+  if (b & 0x1FFFFFFull) t |= 1;
+  return __ll2double_rn(t) * 33554432.0;
+}
 // Exact conversion of an integer-valued fp64 to int128 (bit-level: mantissa << exponent).
 __device__ __forceinline__ i128 f64int_to_i128(double h) {
   if (fabs(h) < 9007199254740992.0) return static_cast<i128>(__double2ll_rz(h));

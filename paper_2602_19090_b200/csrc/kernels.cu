@@ -268,17 +268,22 @@ __device__ __forceinline__ void for_column_x(const int32_t* __restrict__ planes,
 #pragma unroll
       for (int k = 0; k < NG / 4; ++k)
         Lm[k] = ((static_cast<long long>(cv[4 * k]) * 256 + cv[4 * k + 1]) * 256 + cv[4 * k + 2]) * 256 + cv[4 * k + 3];
-      i128 T = Lm[0];
-#pragma unroll
-      for (int k = 1; k < NG / 4; ++k)
-        if (k < nl) T = static_cast<i128>(static_cast<u128>(T) << 32) + static_cast<i128>(Lm[k]);
       dd v{0.0, 0.0};
       const int ee = e(i, icol ? reinterpret_cast<const int32_t*>(base + kSideI)[tid] : 0);
-      if (HI_ONLY) {  // the caller uses RN(value) only (its hi part is the same correctly rounded double)
-        v.hi = ldexp_fast(i128_to_f64(T), 8 * (rp.L - dlast) + ee);
+      if (HI_ONLY && NG <= 8) {  // RN(value) from the one or two limbs, without 128-bit arithmetic
+        const double h = (nl == 1) ? __ll2double_rn(Lm[0]) : limbs2_rn(Lm[0], Lm[NG / 4 - 1]);
+        v.hi = ldexp_fast(h, 8 * (rp.L - dlast) + ee);
       } else {
-        bool first = true;
-        flush_chunk(v, first, T, dlast, rp.L, ee);
+        i128 T = Lm[0];
+#pragma unroll
+        for (int k = 1; k < NG / 4; ++k)
+          if (k < nl) T = static_cast<i128>(static_cast<u128>(T) << 32) + static_cast<i128>(Lm[k]);
+        if (HI_ONLY) {  // the caller uses RN(value) only (its hi part is the same correctly rounded double)
+          v.hi = ldexp_fast(i128_to_f64(T), 8 * (rp.L - dlast) + ee);
+        } else {
+          bool first = true;
+          flush_chunk(v, first, T, dlast, rp.L, ee);
+        }
       }
       double xv[NX > 0 ? NX : 1];
 #pragma unroll
@@ -440,48 +445,60 @@ __device__ __forceinline__ void split_fixed_body(const double* __restrict__ col,
 }
 
 // k > 7 digits of a plain fp64 column (the A split, 15 digits): p = RNE(m·2^{S−e}) is an integer-valued
-// double y = M·2^{8q + r} with |M| < 2^53, so p = (M·2^r)·256^q: its q lowest digits are 0 and the others
-// are the balanced base-256 digits of M·2^r (|·| < 2^61) — all in 64-bit arithmetic. The balanced
-// digit recurrence d = ((x + 128) mod 256) − 128, x ← (x − d)/256 from the bottom yields exactly the
-// excess-128 digits of R5 (byte_t(p + Σ128·256^t) − 128, top digit = the remaining quotient).
-__device__ __forceinline__ void split_wide_body(const double* __restrict__ col, int rows, int k, int S, int e,
-                                               int8_t* __restrict__ base, long long pstride) {
+// double y = M·2^{8q + r} with |M| < 2^53, so p = x·256^q with x = M·2^r (|x| < 2^60): its q lowest digits
+// are 0 and the others are the balanced base-256 digits of x, all in 64-bit arithmetic (the balanced
+// recurrence d = ((x + 128) mod 256) − 128, x ← (x − d)/256 yields exactly the excess-128 digits of R5).
+// With byte permutes: per row, the excess-128 digits
+// at positions t = 0..k−1 (from the bottom) are the bytes of the 16-byte string
+//   E = [0x80 × q] [bytes of w = x + 0x8080808080808080 (mod 2^64)] [0x80 ...]
+// XOR 0x80 — positions below q are zero digits, the window holds x's eight balanced digits, and above it
+// the digits are zero (|p| ≤ 2^{S_k} keeps x + 0x0080…80 in [0, 2^56), so no carry leaves the window).
+// Four rows' digits of one plane are gathered with three PRMTs into one 32-bit store.
+__device__ __forceinline__ void split_wide_body_prmt(const double* __restrict__ col, int rows, int k, int S, int e,
+                                                    int8_t* __restrict__ base, long long pstride) {
+  constexpr unsigned long long P80 = 0x8080808080808080ULL;
   for (int i0 = 4 * threadIdx.x; i0 < rows; i0 += 4 * BS) {
-    long long x[4];
-    int q[4];
+    uint32_t E[4][4];
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
       const int i = i0 + r;
       const double y = (i < rows) ? rint(ldexp_fast(col[i], S - e)) : 0.0;
-      if (fabs(y) < 9007199254740992.0) {  // < 2^53: exact as int64
-        x[r] = static_cast<long long>(y);
-        q[r] = 0;
+      long long x;
+      int q;
+      if (fabs(y) < 9007199254740992.0) {
+        x = static_cast<long long>(y);
+        q = 0;
       } else {
         const long long bits = __double_as_longlong(y);
-        const int ex = static_cast<int>((bits >> 52) & 0x7FF) - 1075;  // y = ±mant·2^ex, ex ≥ 1
+        const int ex = static_cast<int>((bits >> 52) & 0x7FF) - 1075;
         long long mant = (bits & 0xFFFFFFFFFFFFFLL) | 0x10000000000000LL;
         if (bits < 0) mant = -mant;
-        q[r] = ex >> 3;
-        x[r] = mant << (ex & 7);
+        q = ex >> 3;
+        x = mant << (ex & 7);
       }
+      const unsigned long long w = static_cast<unsigned long long>(x) + P80;
+      unsigned long long lo, hi;
+      if (q == 0) {
+        lo = w;
+        hi = P80;
+      } else {
+        lo = (w << (8 * q)) | (P80 >> (64 - 8 * q));
+        hi = (w >> (64 - 8 * q)) | (P80 << (8 * q));
+      }
+      E[r][0] = static_cast<uint32_t>(lo);
+      E[r][1] = static_cast<uint32_t>(lo >> 32);
+      E[r][2] = static_cast<uint32_t>(hi);
+      E[r][3] = static_cast<uint32_t>(hi >> 32);
     }
-    // digits from the least significant plane (index k−1) upwards; plane s holds weight 256^{k−1−s}
-    for (int t = 0; t < k; ++t) {  // t = position from the bottom
-      uint32_t packed = 0;
 #pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        int d;
-        if (t < q[r]) {
-          d = 0;
-        } else if (t == k - 1) {
-          d = static_cast<int>(x[r]);  // the top digit takes the rest
-        } else {
-          d = static_cast<int>(((x[r] + 128) & 255)) - 128;
-          x[r] = (x[r] - d) >> 8;
-        }
-        packed |= (static_cast<uint32_t>(d) & 0xFFu) << (8 * r);
+    for (int t = 0; t < 16; ++t) {
+      if (t < k) {
+        const unsigned sel = (t & 3) | (((t & 3) + 4) << 4);
+        const uint32_t a = __byte_perm(E[0][t >> 2], E[1][t >> 2], sel);
+        const uint32_t b = __byte_perm(E[2][t >> 2], E[3][t >> 2], sel);
+        const uint32_t packed = __byte_perm(a, b, 0x5410) ^ 0x80808080u;
+        *reinterpret_cast<uint32_t*>(base + i0 + static_cast<long long>(k - 1 - t) * pstride) = packed;
       }
-      *reinterpret_cast<uint32_t*>(base + i0 + (k - 1 - t) * pstride) = packed;
     }
   }
 }
@@ -507,7 +524,7 @@ __global__ void __launch_bounds__(BS)
   const int S = 8 * (k - 1) + 6;
   // |p| <= 2^S (+1 for a double-double): 64-bit arithmetic while S <= 54 (k <= 7)
   if (k <= 7) split_fixed_body<long long>(col, cl, rows, k, S, e, dig + j * ldd, pstride);
-  else if (!cl) split_wide_body(col, rows, k, S, e, dig + j * ldd, pstride);
+  else if (!cl) split_wide_body_prmt(col, rows, k, S, e, dig + j * ldd, pstride);
   else split_fixed_body<i128>(col, cl, rows, k, S, e, dig + j * ldd, pstride);
   if (threadIdx.x == 0) ell_out[j] = e - S;
 }
