@@ -222,8 +222,9 @@ def refine_to_tol(A, X0, lam0, delta, theta=THETA_DEFAULT, max_sweeps=6, beta_mo
     the paper's error model predicts ‖X − X_k‖ ≲ ν_k² max|λ̂| / (n gap) ≤ δ (eq. assume2 / gamma,
     PAPER.md:341-373 with ξ = n as in §4.1), or at stagnation (ν_k > ν_{k−1}/2 between two sweeps without
     unresolved groups: a Rayleigh–Ritz sub-solve (R13) rotates its group's columns, so its ν is not a
-    contraction measure), or at max_sweeps. At a stagnating ν the update's 2-norm ‖X_k − X_{k−1}‖₂ ≤ δ
-    also stops (converged); otherwise, with truncation on, the driver first escalates θ ← 16θ
+    contraction measure), or at max_sweeps. Once ν ≤ √n·δ (‖D‖₂ ≥ ‖D‖_F/√n) the update's 2-norm
+    ‖X_k − X_{k−1}‖₂ ≤ δ also stops (converged); at a stagnating ν above it, with truncation on, the driver
+    first escalates θ ← 16θ
     (β two bits lower: the truncated iteration's noise floor is quadratic in the truncation) at most
     max_escalations times."""
     X, lam = np.asarray(X0, dtype=np.float64), np.asarray(lam0, dtype=np.float64)
@@ -247,14 +248,22 @@ def refine_to_tol(A, X0, lam0, delta, theta=THETA_DEFAULT, max_sweeps=6, beta_mo
         if nu <= delta or pred <= delta:
             rec["stop"] = "converged"
             break
+        d2 = None
+        if not info["clusters"] and nu <= np.sqrt(n) * delta:  # ‖D‖₂ ≥ ‖D‖_F/√n
+            d2 = float(np.linalg.norm(X - X_prev, 2))
+            rec["update_2norm"] = d2
+            if d2 <= delta:
+                rec["stop"] = "converged (2-norm of the update)"
+                break
         if info["clusters"]:
             nu_prev = None
             continue
         if nu_prev is not None and nu > nu_prev / 2:
             # stagnating Frobenius ν: the paper's measure is the 2-norm; the update's exact
             # 2-norm decides (the library estimates it by power iteration)
-            d2 = float(np.linalg.norm(X - X_prev, 2))
-            rec["update_2norm"] = d2
+            if d2 is None:
+                d2 = float(np.linalg.norm(X - X_prev, 2))
+                rec["update_2norm"] = d2
             if d2 <= delta:
                 rec["stop"] = "converged (2-norm of the update)"
                 break

@@ -1623,14 +1623,9 @@ ozr_status ozr_refine_to_tol_dist(ozr_ctx ctx, ozr_comm comm, const double* A, i
       result = OZR_OK;
       break;
     }
-    if (rep.n_clusters > 0) {  // a Rayleigh–Ritz sub-solve rotates its group: no contraction measure (R12)
-      nu_prev = -1.0;
-      continue;
-    }
-    if (nu_prev >= 0.0 && rep.net_update > nu_prev / 2) {
-      // stagnation of the Frobenius ν above δ: the update's 2-norm (the paper's measure) may already be
-      // ≤ δ — a noise-like update has ‖D‖₂ ≈ 2‖D‖_F/√n (R12)
-      double d2 = 0.0;
+    // ‖D‖₂ ≥ ‖D‖_F/√n: once ν_F ≤ √n·δ the update's 2-norm (the paper's measure) may already be ≤ δ (R12)
+    double d2 = -1.0;
+    if (rep.n_clusters == 0 && rep.net_update <= std::sqrt(static_cast<double>(n)) * params->delta) {
       st = update_norm2(ctx, comm ? comm->ex.get() : nullptr, n, &d2);
       if (st != OZR_OK) {
         if (sweeps_done) *sweeps_done = done;
@@ -1638,6 +1633,27 @@ ozr_status ozr_refine_to_tol_dist(ozr_ctx ctx, ozr_comm comm, const double* A, i
       }
       rep.update_2norm = d2;
       if (history && k < max_hist) history[k] = rep;
+      if (d2 <= params->delta) {
+        result = OZR_OK;
+        break;
+      }
+    }
+    if (rep.n_clusters > 0) {  // a Rayleigh–Ritz sub-solve rotates its group: no contraction measure (R12)
+      nu_prev = -1.0;
+      continue;
+    }
+    if (nu_prev >= 0.0 && rep.net_update > nu_prev / 2) {
+      // stagnation of the Frobenius ν above δ: the update's 2-norm (the paper's measure) may already be
+      // ≤ δ — a noise-like update has ‖D‖₂ ≈ 2‖D‖_F/√n (R12)
+      if (d2 < 0.0) {
+        st = update_norm2(ctx, comm ? comm->ex.get() : nullptr, n, &d2);
+        if (st != OZR_OK) {
+          if (sweeps_done) *sweeps_done = done;
+          return st;
+        }
+        rep.update_2norm = d2;
+        if (history && k < max_hist) history[k] = rep;
+      }
       if (d2 <= params->delta) {
         result = OZR_OK;
         break;

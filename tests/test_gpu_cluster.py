@@ -142,3 +142,20 @@ def test_c4_recipe_fp32_start_converges(ctx, n, delta):
     assert hist[0]["max_cluster"] >= n // 4, trail
     assert st == 0, trail
     assert fe <= delta, (fe, trail)
+
+
+def test_c4_recipe_default_dense_path(ctx):
+    """BASELINE c4's recipe at n = 2048 with the DEFAULT parameters: the FP32 start leaves one group of more
+    than dense_cluster = 1024 columns, which takes the dense sub-solve (cuSOLVER syevd); the refinement
+    converges (status OK) to an orthonormal eigenbasis: max_j ‖A x_j − λ_j x_j‖ and ‖XᵀX − I‖_max at the
+    fp64 level (the forward error itself is checked at n = 512 / 1024 above)."""
+    import paper_2602_19090_b200 as ozr
+    A, lam0, X0 = _case("c4", 2048, "fp32")
+    Xd, ld = to_dev(X0), vec_dev(lam0)
+    st, hist = ozr.ozr_refine_to_tol(ctx, to_dev(A), Xd, ld, ozr.default_params(delta=1e-10, max_sweeps=12))
+    trail = [(h["net_update"], h["n_clusters"], h["max_cluster"], h["update_2norm"]) for h in hist]
+    assert hist[0]["max_cluster"] >= 1024, trail
+    assert st == 0, trail
+    X, lam = to_np(Xd), to_np(ld)
+    assert np.max(np.linalg.norm(A @ X - X * lam[None, :], axis=0)) <= 1e-12, trail
+    assert np.max(np.abs(X.T @ X - np.eye(2048))) <= 1e-12

@@ -246,11 +246,15 @@ def test_driver_stop_rules(monkeypatch):
     A, X0, lam0 = np.eye(n), np.eye(n), np.arange(n, dtype=float)
     lam0[1] = 1e-20  # a tiny gap: the error model's prediction ν² max|λ̂|/(n gap) never stops the scripts
     s2f = np.linalg.norm(noise, 2) / np.linalg.norm(noise)  # ‖D‖₂ / ‖D‖_F ≈ 2/√n
-    # stagnation at ν_F = 1e-8 with ‖D‖₂ = s2f·1e-8 ≤ δ = 1e-8·s2f·1.01: converged by the 2-norm
+    # ν_F = 1e-8 ≤ √n·δ with ‖D‖₂ = s2f·1e-8 ≤ δ = 1.01e-8·s2f: converged by the 2-norm right away
     script[:] = [(1e-4, []), (1e-8, []), (0.9e-8, [])]
     _, _, h = orf.refine_to_tol(A, X0, lam0, 1.01e-8 * s2f, max_sweeps=6)
-    assert len(h) == 3 and h[-1]["stop"].startswith("converged (2-norm")
-    assert abs(h[-1]["update_2norm"] / (0.9e-8 * s2f) - 1) < 1e-6  # X + D is rounded
+    assert len(h) == 2 and h[-1]["stop"].startswith("converged (2-norm")
+    assert abs(h[-1]["update_2norm"] / (1e-8 * s2f) - 1) < 1e-6  # X + D is rounded
+    # ν_F ≤ √n·δ but ‖D‖₂ > δ: keeps iterating; the next (smaller) update passes
+    script[:] = [(1e-4, []), (1e-8, []), (1e-9, [])]
+    _, _, h = orf.refine_to_tol(A, X0, lam0, 0.5e-8 * s2f, max_sweeps=6)
+    assert len(h) == 3 and h[1]["update_2norm"] > 0.5e-8 * s2f and h[-1]["stop"].startswith("converged")
     # stagnation with ‖D‖₂ > δ: θ escalates (×16) twice, then NOT converged (stagnation)
     script[:] = [(1e-4, []), (1e-8, []), (0.9e-8, []), (0.8e-8, []), (0.7e-8, []), (0.6e-8, []), (0.5e-8, [])]
     _, _, h = orf.refine_to_tol(A, X0, lam0, 1e-12, max_sweeps=7)
