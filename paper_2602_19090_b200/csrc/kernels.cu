@@ -351,6 +351,30 @@ __global__ void __launch_bounds__(BS) k_colmax(const double* __restrict__ X, lon
 }
 
 // Digits of four consecutive rows, packed per plane into one 32-bit store (byte r = row i0 + r).
+// k <= 8 with |p| ≤ 2^{8(k−1)+6} + 1 (every split of R5/R6): the excess-128 digits are the bytes of
+// w = p + 0x8080808080808080 (mod 2^64) XOR 0x80 — the top digit is |d| ≤ 65, so nothing carries past byte
+// k−1 — gathered across the four rows with byte permutes.
+__device__ __forceinline__ void store_digits4_prmt(const long long (&p)[4], int k, int8_t* __restrict__ base,
+                                                   long long pstride) {
+  uint32_t lo[4], hi[4];
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const unsigned long long w = static_cast<unsigned long long>(p[r]) + 0x8080808080808080ULL;
+    lo[r] = static_cast<uint32_t>(w);
+    hi[r] = static_cast<uint32_t>(w >> 32);
+  }
+#pragma unroll
+  for (int t = 0; t < 8; ++t) {
+    if (t < k) {
+      const unsigned sel = (t & 3) | (((t & 3) + 4) << 4);
+      const uint32_t a = __byte_perm(t < 4 ? lo[0] : hi[0], t < 4 ? lo[1] : hi[1], sel);
+      const uint32_t b = __byte_perm(t < 4 ? lo[2] : hi[2], t < 4 ? lo[3] : hi[3], sel);
+      *reinterpret_cast<uint32_t*>(base + static_cast<long long>(k - 1 - t) * pstride) =
+          __byte_perm(a, b, 0x5410) ^ 0x80808080u;
+    }
+  }
+}
+
 // Integer type T: long long when |p| < 2^62 (k <= 7), i128 otherwise.
 template <typename T>
 __device__ __forceinline__ void store_digits4(const T (&p)[4], int k, int8_t* __restrict__ base, long long pstride) {
@@ -400,7 +424,7 @@ __global__ void __launch_bounds__(BS)
       q[r] = __double2ll_rn(ldexp_fast(x1, -g));  // exact integer, |q| <= 2^{53-β}
       sq += static_cast<i128>(q[r]) * q[r];
     }
-    store_digits4<long long>(q, kx, dig + j * ldd + i0, pstride);
+    store_digits4_prmt(q, kx, dig + j * ldd + i0, pstride);
   }
   const i128 SQ = block_sum_i128(sq, shq);
   if (threadIdx.x == 0) {
@@ -440,7 +464,8 @@ __device__ __forceinline__ void split_fixed_body(const double* __restrict__ col,
       p[r] = (i < rows) ? rint_to<T>(ldexp_fast(col[i], S - e)) : T(0);
       if (cl && i < rows) p[r] += rint_to<T>(ldexp_fast(cl[i], S - e));
     }
-    store_digits4<T>(p, k, base + i0, pstride);
+    if constexpr (sizeof(T) == 8) store_digits4_prmt(p, k, base + i0, pstride);
+    else store_digits4<T>(p, k, base + i0, pstride);
   }
 }
 
@@ -548,7 +573,8 @@ __device__ __forceinline__ void split_res_body(const double* __restrict__ vh, co
         p[r] = rint_to<T>(ldexp_fast(rr.hi, S - e)) + rint_to<T>(ldexp_fast(rr.lo, S - e));
       }
     }
-    store_digits4<T>(p, k, base + i0, pstride);
+    if constexpr (sizeof(T) == 8) store_digits4_prmt(p, k, base + i0, pstride);
+    else store_digits4<T>(p, k, base + i0, pstride);
   }
 }
 
