@@ -411,20 +411,32 @@ __global__ void __launch_bounds__(BS)
   const int g = c + beta - 53;
   const double tau = (wj == 0.0) ? 0.0 : scalbn(0.75, c + beta);  // eq. (tau)
   i128 sq = 0;
-  // 4 consecutive rows per thread: the digit planes get one 32-bit store per plane (ldd % 16 == 0,
-  // so rounding `rows` up to 4 stays inside the column's padding).
-  for (int i0 = 4 * threadIdx.x; i0 < rows; i0 += 4 * BS) {
-    long long q[4];
+  // 4 consecutive rows per thread per group, two groups in flight (their loads issued together): the digit
+  // planes get one 32-bit store per plane (ldd % 16 == 0, so rounding `rows` up to 4 stays inside the
+  // column's padding). Σq² in two 64-bit halves per group (|q| ≤ 2^52: q² < 2^104 needs 128 bits).
+  for (int i0 = 4 * threadIdx.x; i0 < rows; i0 += 8 * BS) {
+    double xv[2][4];
 #pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      const int i = i0 + r;
-      const double x = (i < rows) ? col[i] : 0.0;
-      const double x1 = __dsub_rn(__dadd_rn(tau, x), tau);  // eq. (x), s = 1: fl(fl(τ + x) − τ)
-      if (i < rows) x1c[i] = x1;
-      q[r] = __double2ll_rn(ldexp_fast(x1, -g));  // exact integer, |q| <= 2^{53-β}
-      sq += static_cast<i128>(q[r]) * q[r];
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int i = i0 + h * 4 * BS + r;
+        xv[h][r] = (i < rows) ? col[i] : 0.0;
+      }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int ib = i0 + h * 4 * BS;
+      if (ib >= rows) break;
+      long long q[4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const double x1 = __dsub_rn(__dadd_rn(tau, xv[h][r]), tau);  // eq. (x), s = 1: fl(fl(τ + x) − τ)
+        if (ib + r < rows) x1c[ib + r] = x1;
+        q[r] = __double2ll_rn(ldexp_fast(x1, -g));  // exact integer, |q| <= 2^{53-β}
+        sq += static_cast<i128>(q[r]) * q[r];
+      }
+      store_digits4_prmt(q, kx, dig + j * ldd + ib, pstride);
     }
-    store_digits4_prmt(q, kx, dig + j * ldd + i0, pstride);
   }
   const i128 SQ = block_sum_i128(sq, shq);
   if (threadIdx.x == 0) {
