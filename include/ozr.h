@@ -109,7 +109,8 @@ ozr_status ozr_gemm_plan(int64_t k, int kA, int kB, int L, int* ngroups, int* gr
 typedef struct {
   double delta;      /* prescribed forward error δ (> u)                                     */
   double theta;      /* β and the budgets are chosen for δ' = δ/θ (R11; default 4) */
-  int beta_mode;     /* 0: §4.1 tuned β (⌊·⌋, nδ) [default]; 1: §3.3 eq. proposed_beta (⌈·⌉, ξ) */
+  int beta_mode;     /* 0: §4.1 tuned β (⌊·⌋, nδ) [default]; 1: §3.3 eq. proposed_beta (⌈·⌉, ξ);
+                        2: §4.3 sparse β (γ·min(k, √n), k = row_nnz)              */
   double xi;         /* ξ for beta_mode 1 (0 → n)                                            */
   int beta_override; /* > 0: use this β instead of the formula                               */
   int truncate;      /* 1: X̂ → X̂^(1) (the proposed method) [default]; 0: keep all of X̂        */
@@ -131,7 +132,9 @@ typedef struct {
   int dense_cluster; /* cluster_mode 1: groups of at least this many columns are solved by a dense symmetric
                         eigensolver (cuSOLVER syevd, loaded on first use; OZR_ERR_CUDA if it cannot be
                         loaded) instead of the parallel Jacobi; same K, same conventions (R13).
-                        Default 1024 */
+                        Default 192 (smaller groups: one Jacobi CTA each, all groups in one launch) */
+  int row_nnz;       /* k = maximum number of nonzeros in a row of A (beta_mode 2; also the contraction
+                        length of the V-product's dropped-pair bound, R8). 0 → n (dense)            */
   int max_escalations; /* ozr_refine_to_tol: when the net update stagnates above δ (the truncated iteration's
                           noise floor, R12), continue with θ × 16 (β two bits lower) at most this many
                           times before OZR_ERR_NOT_CONVERGED. Default 2 */

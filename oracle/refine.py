@@ -15,7 +15,7 @@ import numpy as np
 
 from . import _clib
 from .fp import U, ceil_log2, dd_add, dd_div_dd, fast_two_sum, two_prod, two_sum
-from .split import (alpha_dense, alpha_theoretical, beta_dense, beta_theoretical, gap_min, gap_pos, sum_pow2_2c,
+from .split import (alpha_dense, alpha_sparse, alpha_theoretical, beta_dense, beta_sparse, beta_theoretical, gap_min, gap_pos, sum_pow2_2c,
                     x1_truncate)
 
 BETA_MIN, BETA_MAX = 2, 52  # reading R4: τ + x stays in τ's binade iff β ≥ 2; ≥ 1 bit kept iff β ≤ 52
@@ -35,15 +35,20 @@ def col_dot_dd(X, Yh, Yl=None):
     return sh, sl
 
 
-def choose_beta(n, delta_p, lam_prev, c, w, beta_mode="dense", xi=None, cluster_mode=1):
+def choose_beta(n, delta_p, lam_prev, c, w, beta_mode="dense", xi=None, cluster_mode=1, row_nnz=None):
     """β for this sweep from the PREVIOUS sweep's λ̂ (reading R9; the paper computes λ̂ only after V).
-    With the cluster branch, equal estimates are tolerated and the smallest positive gap is used (R13)."""
+    With the cluster branch, equal estimates are tolerated and the smallest positive gap is used (R13).
+    beta_mode: "dense" (§4.1), "theoretical" (§3.3, ξ), "sparse" (§4.3, k = row_nnz)."""
     gap = gap_min(lam_prev)
     if cluster_mode and not gap > 0:
         gap = gap_pos(lam_prev)
     if beta_mode == "dense":
         b = beta_dense(n, delta_p, lam_prev, c, w, gap)
         a = alpha_dense(n, min(max(b, BETA_MIN), BETA_MAX))
+    elif beta_mode == "sparse":
+        k = row_nnz if row_nnz and row_nnz < n else n
+        b = beta_sparse(n, k, delta_p, lam_prev, c, w, gap)
+        a = alpha_sparse(k, min(max(b, BETA_MIN), BETA_MAX))
     else:
         b = beta_theoretical(xi if xi else n, delta_p, lam_prev, c, w, gap)
         a = alpha_theoretical(n, min(max(b, BETA_MIN), BETA_MAX))
@@ -130,7 +135,7 @@ def cluster_subsolve(E, lam, J, X1, Wh, Wl, rh, rl):
 
 
 def sweep(A, X, lam_prev, delta, theta=THETA_DEFAULT, beta=None, beta_mode="dense", xi=None, truncate=True,
-          cluster_mode=1, kappa=KAPPA_DEFAULT, max_cluster=None, groups=None, form_R=False):
+          cluster_mode=1, kappa=KAPPA_DEFAULT, max_cluster=None, groups=None, form_R=False, row_nnz=None):
     """One iteration of Algorithm 1. Returns (X_new fp64, λ̂ fp64, info dict).
 
     cluster_mode 0: the paper's Algorithm 1 (distinct eigenvalues assumed); equal
@@ -146,7 +151,7 @@ def sweep(A, X, lam_prev, delta, theta=THETA_DEFAULT, beta=None, beta_mode="dens
     w = np.max(np.abs(X), axis=0)
     c = ceil_log2(w)
     if beta is None:
-        beta, alpha = choose_beta(n, delta / theta, lam_prev, c, w, beta_mode, xi, cluster_mode)
+        beta, alpha = choose_beta(n, delta / theta, lam_prev, c, w, beta_mode, xi, cluster_mode, row_nnz)
     else:
         alpha = alpha_dense(n, beta)
     info["beta_raw"] = int(beta)
@@ -217,7 +222,7 @@ def sweep(A, X, lam_prev, delta, theta=THETA_DEFAULT, beta=None, beta_mode="dens
 
 
 def refine_to_tol(A, X0, lam0, delta, theta=THETA_DEFAULT, max_sweeps=6, beta_mode="dense", xi=None, callback=None,
-                  cluster_mode=1, kappa=KAPPA_DEFAULT, max_escalations=2, truncate=True):
+                  cluster_mode=1, kappa=KAPPA_DEFAULT, max_escalations=2, truncate=True, row_nnz=None):
     """Driver (reading R12): repeat sweeps; stop after sweep k when ν_k = ‖X_k − X_{k−1}‖_F ≤ δ, or when
     the paper's error model predicts ‖X − X_k‖ ≲ ν_k² max|λ̂| / (n gap) ≤ δ (eq. assume2 / gamma,
     PAPER.md:341-373 with ξ = n as in §4.1), or at stagnation (ν_k > ν_{k−1}/2 between two sweeps without
@@ -233,7 +238,7 @@ def refine_to_tol(A, X0, lam0, delta, theta=THETA_DEFAULT, max_sweeps=6, beta_mo
     nu_prev = None
     for k in range(max_sweeps):
         Xn, lamn, info = sweep(A, X, lam, delta, theta, beta_mode=beta_mode, xi=xi, cluster_mode=cluster_mode,
-                               kappa=kappa, truncate=truncate)
+                               kappa=kappa, truncate=truncate, row_nnz=row_nnz)
         nu = info["net_update"]
         ls = np.sort(lamn)
         d = np.diff(ls)

@@ -123,6 +123,22 @@ def beta_theoretical(xi, delta, lam, c, w, gap=None):
     return int(e) - 1 if m == 0.5 else int(e)
 
 
+def beta_sparse(n, k, delta, lam, c, w, gap=None):
+    """§4.3, PAPER.md:585-591 (sparse A, k = the largest number of nonzeros in a row):
+    γ = sqrt(δ·gap/max|λ̂|),  β = ⌊log2(γ·min(k, √n)/(0.75u) · sqrt(1/Σ_j 2^{2⌈log2 w_j⌉}))⌋.
+    γ·min(k,√n)·sqrt(1/Σ) = sqrt(min(k², n)·δ·gap/(max|λ̂|·Σ)), so it is evaluated in the operation order of
+    the §4.1 form (reading R3) with n replaced by min(k², n)."""
+    m2 = min(int(k) * int(k), int(n))
+    Z = _z_value(m2, delta, gap_min(lam) if gap is None else gap, np.max(np.abs(lam)), sum_pow2_2c(c, w))
+    m, e = np.frexp(Z)
+    return int(e) - 1
+
+
+def alpha_sparse(k, beta):
+    """§4.3: α = −(log2 u + β) + ⌈log2 k⌉ (reported only)."""
+    return 53 - int(beta) + int(ceil_log2(float(k)))
+
+
 def alpha_dense(n, beta):
     """§4.1: α = −(log2 u + β) + ⌈log2 √n⌉ = 53 − β + ⌈log2 √n⌉ (reported only)."""
     c = 0

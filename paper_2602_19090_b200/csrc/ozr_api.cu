@@ -399,14 +399,19 @@ int ceil_log2_host(double v) {
   return (m == 0.5) ? e - 1 : e;
 }
 
-// β of §4.1 (mode 0) / §3.3 (mode 1), evaluated in the operation order of DESIGN.md R3.
-int choose_beta(int64_t n, double delta_p, int mode, double xi, double gap, double maxlam, double ssum) {
-  const double c = (mode == 0) ? static_cast<double>(n) : (xi > 0 ? xi : static_cast<double>(n));
+// β of §4.1 (mode 0) / §3.3 (mode 1) / §4.3 sparse (mode 2: γ·min(k, √n) in place of
+// √(nδ·gap/max|λ̂|), i.e. the §4.1 form with n → min(k², n)), evaluated in the operation order of R3.
+int choose_beta(int64_t n, double delta_p, int mode, double xi, double gap, double maxlam, double ssum,
+                int64_t row_nnz) {
+  const int64_t k = (row_nnz > 0 && row_nnz < n) ? row_nnz : n;
+  const double c = (mode == 0) ? static_cast<double>(n)
+                   : (mode == 2) ? static_cast<double>(std::min<int64_t>(k * k, n))
+                                 : (xi > 0 ? xi : static_cast<double>(n));
   const double t = ((c * delta_p) * gap) / (maxlam * ssum);
   const double Z = std::sqrt(t) / (0.75 * kU);
   int e;
   const double m = std::frexp(Z, &e);
-  if (mode == 0) return e - 1;         // ⌊log2 Z⌋
+  if (mode != 1) return e - 1;         // ⌊log2 Z⌋
   return (m == 0.5) ? e - 1 : e;       // ⌈log2 Z⌉
 }
 
@@ -732,7 +737,7 @@ ozr_status sweep(ozr_ctx ctx, Exchange* ex, const double* A, int64_t n, int64_t 
   const double ssum = sum_pow2_2c(hw);
   if (ssum == 0.0 || maxlam == 0.0) return fail(ctx, OZR_ERR_DEGENERATE, "zero X or zero spectrum");
   int beta_raw = (P.beta_override > 0) ? P.beta_override
-                                       : choose_beta(n, delta_p, P.beta_mode, P.xi, gap, maxlam, ssum);
+                                       : choose_beta(n, delta_p, P.beta_mode, P.xi, gap, maxlam, ssum, P.row_nnz);
   int beta = std::min(std::max(beta_raw, kBetaMin), kBetaMax);
   if (!P.truncate) beta = kBetaMin;
   const int kx = kx_for_beta(beta);
@@ -744,7 +749,8 @@ ozr_status sweep(ozr_ctx ctx, Exchange* ex, const double* A, int64_t n, int64_t 
     if (x != 0.0) cmax = std::max(cmax, ceil_log2_host(x));
   rep.beta = beta;
   rep.beta_raw = beta_raw;
-  rep.alpha = alpha_dense(n, beta);
+  rep.alpha = (P.beta_mode == 2) ? 53 - beta + ceil_log2_host(static_cast<double>(P.row_nnz > 0 && P.row_nnz < n ? P.row_nnz : n))
+                                 : alpha_dense(n, beta);
   rep.kX = kx;
   rep.gap_min = gap0;
   rep.max_abs_lambda = maxlam;
@@ -766,7 +772,10 @@ ozr_status sweep(ozr_ctx ctx, Exchange* ex, const double* A, int64_t n, int64_t 
   }
   unsigned char tileLV[kMaxNTiles];
   double avg_pairs_V = 0.0;
-  int LV = tile_budgets(st.kA_split, kx, n, st.eA_max, c_col, tau_col, tileLV, &avg_pairs_V);
+  // a row of a sparse A (row_nnz nonzeros) contributes row_nnz terms to v_ij: the statistical tail bound of
+  // the dropped pairs uses that contraction length (R8; the int32 capacity still uses n)
+  const int64_t K_V = (P.row_nnz > 0 && P.row_nnz < n) ? P.row_nnz : n;
+  int LV = tile_budgets(st.kA_split, kx, K_V, st.eA_max, c_col, tau_col, tileLV, &avg_pairs_V);
   if (P.L_V > 0) LV = P.L_V;
   LV = std::min(LV, st.kA_split + kx);
   const int kA = std::min(st.kA_split, LV - 1);
@@ -1367,7 +1376,7 @@ void ozr_params_default(ozr_params* p) {
   p->kappa = 0x1p-10;
   p->max_cluster = 16384;
   p->form_R = 0;
-  p->dense_cluster = 1024;
+  p->dense_cluster = 192;  // = the cooperative-Jacobi threshold: measured 12x faster at m = 739 (c2)
   p->max_escalations = 2;
 }
 

@@ -26,10 +26,11 @@ def _case(cfg, n, start):
     return A, lam0, X0
 
 
-@pytest.mark.parametrize("n,dense", [(128, 1024), (256, 1024), (256, 2)])
+@pytest.mark.parametrize("n,dense", [(128, 1 << 20), (256, 1 << 20), (256, 2), (256, 192)])
 def test_fp32_start_sweep_parity(ctx, n, dense):
-    """dense = 2: every group takes the dense sub-solve (dense_eig.cu, cuSOLVER syevd) instead of Jacobi;
-    the same K, so the same tolerance against the oracle's __float128 Jacobi."""
+    """dense = 2: every group takes the dense sub-solve (dense_eig.cu, cuSOLVER syevd) instead of Jacobi; 2^20:
+    every group takes a Jacobi (per-CTA, or whole-GPU cooperative from 192 columns); 192: the default. The
+    same K, so the same tolerance against the oracle's __float128 Jacobi."""
     A, lam0, X0 = _case("c2", n, "fp32")
     Xg, lg, rep, Xo, lo, info, groups = parity_sweep(ctx, A, X0, lam0, 1e-14, dense_cluster=dense)
     assert rep["beta"] == info["beta"]
@@ -99,7 +100,7 @@ def test_c3_fp64_start_stays_linear(ctx):
     assert np.max(np.abs(Xg - Xo)) <= 1e-13
 
 
-@pytest.mark.parametrize("n,dense", [(512, 1024), (512, 2)])
+@pytest.mark.parametrize("n,dense", [(512, 1 << 20), (512, 2)])
 def test_c3_fp32_start_exercises_groups(ctx, n, dense):
     """The c3 spectrum (clusters of 8 eigenvalues 1e-10 apart) from an FP32 eigensolver: inside every
     cluster the FP32 vectors are arbitrary rotations (|ẽ_ij| ≫ κ), so each cluster becomes an unresolved
@@ -146,7 +147,7 @@ def test_c4_recipe_fp32_start_converges(ctx, n, delta):
 
 def test_c4_recipe_default_dense_path(ctx):
     """BASELINE c4's recipe at n = 2048 with the DEFAULT parameters: the FP32 start leaves one group of more
-    than dense_cluster = 1024 columns, which takes the dense sub-solve (cuSOLVER syevd); the refinement
+    than 1024 columns, which takes the dense sub-solve (cuSOLVER syevd); the refinement
     converges (status OK) to an orthonormal eigenbasis: max_j ‖A x_j − λ_j x_j‖ and ‖XᵀX − I‖_max at the
     fp64 level (the forward error itself is checked at n = 512 / 1024 above)."""
     import paper_2602_19090_b200 as ozr

@@ -141,3 +141,29 @@ def test_update_2norm_stop(ctx):
     assert abs(last["update_2norm"] / exact - 1) < 1e-2, (last["update_2norm"], exact)
     Xh, Xl, lh, ll, _ = orf.reference_eigvecs(A, X0, lam0)
     assert orf.forward_error(Xh, Xl, to_np(Xd), lh, to_np(ld)) <= delta
+
+
+def test_sparse_beta_banded(ctx):
+    """§4.3's sparse constants on the banded stand-in for the paper's sparse matrices
+    (workloads.banded_sym, k = 17 nonzeros per row, n = 1024, cnd 1e8, FP64 start): one sweep with
+    beta_mode = 2 matches the oracle sweep with beta_mode "sparse" (same β, X̂ and D̂ within 1e-13), the
+    V product's budget uses the row length k, and ozr_refine_to_tol reaches δ = 1e-12 against the oracle
+    reference."""
+    import paper_2602_19090_b200 as ozr
+    A, lam, k = W.banded_sym(1024, layers=4, cnd=1e8, seed=11)
+    lam0, X0 = W.initial_eig(A, "fp64")
+    delta = 1e-12
+    Xg, lg, rep = _gpu_sweep(ctx, A, X0, lam0, delta, beta_mode=2, row_nnz=k)
+    Xo, lo, info = orf.sweep(A, X0, lam0, delta, beta_mode="sparse", row_nnz=k)
+    assert rep["beta"] == info["beta"] and rep["alpha"] == info["alpha"]
+    assert np.max(np.abs(Xg - Xo)) <= 1e-13
+    assert np.max(np.abs(lg - lo)) <= 1e-13 * np.max(np.abs(lam0))
+    _, _, rep_dense = _gpu_sweep(ctx, A, X0, lam0, delta)
+    assert rep["beta"] <= rep_dense["beta"]          # min(k, √n) ≤ √n: the sparse rule keeps more bits
+    assert rep["pairs_V"] <= rep_dense["pairs_V"] + 5 * (rep_dense["beta"] - rep["beta"] + 1)
+    Xh, Xl, lh, ll, _ = orf.reference_eigvecs(A, X0, lam0)
+    Xd, ld = to_dev(X0), vec_dev(lam0)
+    st, hist = ozr.ozr_refine_to_tol(ctx, to_dev(A), Xd, ld,
+                                     ozr.default_params(delta=delta, beta_mode=2, row_nnz=k, max_sweeps=6))
+    assert st == 0
+    assert orf.forward_error(Xh, Xl, to_np(Xd), lh, to_np(ld)) <= delta

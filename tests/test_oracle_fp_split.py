@@ -10,6 +10,8 @@ import numpy as np
 import pytest
 
 from oracle import fp, split
+from oracle import split as osp
+import workloads as W
 
 GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "closed_forms.json")))
 
@@ -210,3 +212,43 @@ def test_x1_digits():
             for i in range(50):
                 assert F(int(q[i, j])) * F(2) ** int(g[j]) == F(X1[i, j])
                 assert abs(int(q[i, j])) <= 2 ** (53 - beta)
+
+
+def test_beta_sparse_closed_form_and_dense_limit():
+    """§4.3 sparse β: γ = sqrt(δ·gap/max|λ̂|), β = ⌊log2(γ·min(k,√n)/(0.75u)·sqrt(1/Σ))⌋.
+    Closed form: n = 100, k = 1 (diagonal A), all w_j = 1 (Σ = 100), δ·gap/max|λ̂| = 1e-8 →
+    β = ⌊log2(1e-4 · 2^53/0.75 / 10)⌋ = ⌊log2(1.2010e11)⌋ = 36, α = 53 − 36 + ⌈log2 1⌉ = 17.
+    k ≥ √n reduces to the dense §4.1 β; for k < √n it matches the literal formula evaluated in fp64
+    away from the integer boundaries of log2."""
+    n = 100
+    lam = np.linspace(-1.0, 1.0, n)
+    w = np.ones(n)
+    c = osp.ceil_log2(w)
+    b = osp.beta_sparse(n, 1, 1.0, lam, c, w, gap=1e-8)
+    assert b == 36 and 2.0 ** 36 <= 1e-4 * 2.0 ** 53 / 0.75 / 10 < 2.0 ** 37
+    assert osp.alpha_sparse(1, b) == 17
+    rng = np.random.default_rng(4)
+    for _ in range(200):
+        n = int(rng.integers(16, 5000))
+        lam = np.sort(rng.uniform(-1, 1, n))
+        w = rng.uniform(0.01, 0.5, n)
+        c = osp.ceil_log2(w)
+        delta = 10.0 ** rng.uniform(-15, -6)
+        for k in (int(np.ceil(np.sqrt(n))), n, 10 * n):
+            assert osp.beta_sparse(n, k, delta, lam, c, w) == osp.beta_dense(n, delta, lam, c, w)
+        k = int(rng.integers(1, int(np.sqrt(n))))
+        gamma = np.sqrt(delta * osp.gap_min(lam) / np.max(np.abs(lam)))
+        lit = np.log2(gamma * k / (0.75 * 2.0 ** -53) * np.sqrt(1.0 / osp.sum_pow2_2c(c, w)))
+        if abs(lit - np.round(lit)) > 1e-9:
+            assert osp.beta_sparse(n, k, delta, lam, c, w) == int(np.floor(lit))
+
+
+def test_banded_stand_in():
+    """The sparse stand-in (workloads.banded_sym): bandwidth 2·layers, at most 4·layers + 1 nonzeros per
+    row, exact zeros outside the band, symmetric, and the eigenvalues of the stored A are the intended
+    geometric spectrum up to the formation rounding."""
+    A, lam, k = W.banded_sym(300, layers=4, cnd=1e8, seed=3)
+    ii, jj = np.indices(A.shape)
+    assert np.all(A[np.abs(ii - jj) > 8] == 0.0) and np.array_equal(A, A.T)
+    assert k == int((A != 0).sum(axis=1).max()) and k <= 17
+    assert np.max(np.abs(np.sort(np.linalg.eigvalsh(A)) - np.sort(lam))) <= 1e-14

@@ -138,6 +138,31 @@ def make_config_torch(name, device, n=None, seed_offset=0):
     return colmajor(A), lam0.contiguous(), colmajor(X0), cfg
 
 
+def banded_sym(n, layers=4, cnd=1e8, seed=0):
+    """Sparse stand-in for the paper's ELSES matrices (the collection is not in the
+    container): A = Q·diag(λ)·Qᵀ with geometric λ and Q a product of `layers` layers of disjoint 2x2 Givens
+    rotations with seeded angles — odd layers on the pairs (0,1), (2,3), …, even layers on (1,2), (3,4), … —
+    so Q has bandwidth `layers` and A bandwidth 2·layers: at most k = 4·layers + 1 nonzeros per row. A is
+    formed in fp64, entries outside the band are exact zeros, symmetrised as (A + Aᵀ)/2.
+    Returns (A, λ, k) with k the realised largest number of nonzeros in a row."""
+    rng = np.random.default_rng(seed)
+    lam = geometric_spectrum(n, cnd)
+    Q = np.eye(n)
+    for l in range(layers):
+        i0 = l % 2
+        for i in range(i0, n - 1, 2):
+            t = rng.uniform(0.0, 2.0 * np.pi)
+            c, s = np.cos(t), np.sin(t)
+            qi, qj = Q[:, i].copy(), Q[:, i + 1].copy()
+            Q[:, i], Q[:, i + 1] = c * qi - s * qj, s * qi + c * qj
+    A = (Q * lam[None, :]) @ Q.T
+    bw = 2 * layers
+    ii, jj = np.indices((n, n))
+    A[np.abs(ii - jj) > bw] = 0.0
+    A = (A + A.T) * 0.5
+    return A, lam, int((A != 0).sum(axis=1).max())
+
+
 def householder_exact(m, lam_bits=12, seed=0):
     """Pin family: n = 2^m, v ∈ {±1}^n, H = I − (2/n) v vᵀ (exactly orthogonal,
     symmetric, dyadic). λ_k = distinct dyadic numbers with `lam_bits`-bit numerators in (0, 1].
