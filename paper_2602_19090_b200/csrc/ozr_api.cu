@@ -67,6 +67,7 @@ struct ozr_ctx_s {
     size_t n;
   };
   std::vector<Pend> pend;
+  int staged_launches = 0;  // k_copy_bytes launches of the current sweep (counted in the step report)
   char* stage(size_t bytes) {
     const size_t off = (hst_off + 15) & ~static_cast<size_t>(15);
     if (off + bytes > hst_cap) return nullptr;
@@ -78,6 +79,7 @@ struct ozr_ctx_s {
     if (!st) return false;
     ozr::launch_copy_bytes(st, src, bytes, s);
     pend.push_back({dst, st, bytes});
+    ++staged_launches;
     return true;
   }
   bool h2d(void* ddst, const void* src, size_t bytes, cudaStream_t s) {
@@ -85,6 +87,7 @@ struct ozr_ctx_s {
     if (!st) return false;
     memcpy(st, src, bytes);
     ozr::launch_copy_bytes(ddst, st, bytes, s);
+    ++staged_launches;
     return true;
   }
   void flush() {
@@ -636,6 +639,7 @@ ozr_status sweep(ozr_ctx ctx, Exchange* ex, const double* A, int64_t n, int64_t 
     }
     ctx->pend.clear();
     ctx->hst_off = 0;
+    ctx->staged_launches = 0;
   }
   int* derr = ctx->ws<int>(S_ERR, 4);
   int* demax = ctx->ws<int>(S_EMAX, 4);
@@ -1243,7 +1247,8 @@ ozr_status sweep(ozr_ctx ctx, Exchange* ex, const double* A, int64_t n, int64_t 
   ctx->dump();
   // kernels of this sweep: [colmax] x1_split transpose split_res split_E, and per column band of each of the
   // three products its GEMM and its recombination (recombine_V / recombine_E / final)
-  rep.launches = (fresh_w ? 1 : 0) + 4 + 6 * band_count(NL) + cluster_launches + (new_A ? 2 : 0) + (P.form_R ? 2 : 0);
+  rep.launches = (fresh_w ? 1 : 0) + 4 + 6 * band_count(NL) + cluster_launches + (new_A ? 2 : 0) + (P.form_R ? 2 : 0) +
+                 ctx->staged_launches;
 #undef OZR_X
   return OZR_OK;
 }
