@@ -209,8 +209,9 @@ __device__ __forceinline__ void for_column(const int32_t* __restrict__ planes, l
 // (cp.async.bulk + mbarrier), one stage = TR rows = one row per thread. f(i, v, xv) gets the recombined
 // element and the side-column values of row i. Requires rp.consecutive and 16-byte aligned segments
 // (rows % 4 == 0, even leading dimensions) — checked by the host (`use_tma`); else the register path.
-constexpr int TR = BS;   // rows per stage
-constexpr int TS = 4;    // stages
+constexpr int RPT = 2;         // rows per thread per stage (two independent element chains per thread)
+constexpr int TR = RPT * BS;   // rows per stage
+constexpr int TS = 2;          // stages
 constexpr int kStageBytes = kFastGroups * TR * 4 + 2 * TR * 8 + TR * 4;  // planes | 2 fp64 sides | 1 int32 side
 constexpr int kSideI = kFastGroups * TR * 4 + 2 * TR * 8;
 constexpr int kTmaSmem = TS * kStageBytes + TS * 8;
@@ -257,19 +258,22 @@ __device__ __forceinline__ void for_column_x(const int32_t* __restrict__ planes,
   for (int c = 0; c < nch; ++c) {
     if (tid == 0 && c + TS - 1 < nch) issue(c + TS - 1);  // its stage was released by the last barrier
     mbar_wait(&bar[c % TS], (c / TS) & 1);
-    const int i = c * TR + tid;
+#pragma unroll
+    for (int h = 0; h < RPT; ++h) {
+    const int tl = tid + h * BS;  // row within the stage
+    const int i = c * TR + tl;
     if (i < rows) {
       const unsigned char* base = tsm + (c % TS) * kStageBytes;
       // NG: groups compiled for this launch (4, 8 or 12 ≥ ngroups), so small plans do no dead work
       int32_t cv[NG];
 #pragma unroll
-      for (int g = 0; g < NG; ++g) cv[g] = (g < nact) ? reinterpret_cast<const int32_t*>(base + g * TR * 4)[tid] : 0;
+      for (int g = 0; g < NG; ++g) cv[g] = (g < nact) ? reinterpret_cast<const int32_t*>(base + g * TR * 4)[tl] : 0;
       long long Lm[NG / 4];
 #pragma unroll
       for (int k = 0; k < NG / 4; ++k)
         Lm[k] = ((static_cast<long long>(cv[4 * k]) * 256 + cv[4 * k + 1]) * 256 + cv[4 * k + 2]) * 256 + cv[4 * k + 3];
       dd v{0.0, 0.0};
-      const int ee = e(i, icol ? reinterpret_cast<const int32_t*>(base + kSideI)[tid] : 0);
+      const int ee = e(i, icol ? reinterpret_cast<const int32_t*>(base + kSideI)[tl] : 0);
       if (HI_ONLY && NG <= 8) {  // RN(value) from the one or two limbs, without 128-bit arithmetic
         const double h = (nl == 1) ? __ll2double_rn(Lm[0]) : limbs2_rn(Lm[0], Lm[NG / 4 - 1]);
         v.hi = ldexp_fast(h, 8 * (rp.L - dlast) + ee);
@@ -287,8 +291,9 @@ __device__ __forceinline__ void for_column_x(const int32_t* __restrict__ planes,
       }
       double xv[NX > 0 ? NX : 1];
 #pragma unroll
-      for (int x = 0; x < NX; ++x) xv[x] = reinterpret_cast<const double*>(base + kFastGroups * TR * 4 + x * TR * 8)[tid];
+      for (int x = 0; x < NX; ++x) xv[x] = reinterpret_cast<const double*>(base + kFastGroups * TR * 4 + x * TR * 8)[tl];
       f(i, v, xv);
+    }
     }
     __syncthreads();
   }
