@@ -38,7 +38,7 @@ METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.
            "gpu__compute_memory_throughput.avg.pct_of_peak_sustained_elapsed",
            "dram__throughput.avg.pct_of_peak_sustained_elapsed",
            "sm__throughput.avg.pct_of_peak_sustained_elapsed",
-           "sm__pipe_tensor_op_imma_cycles_active.avg.pct_of_peak_sustained_elapsed",
+           "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed",
            "sm__inst_executed_pipe_tensor_op_imma.avg.pct_of_peak_sustained_active",
            "launch__registers_per_thread", "launch__grid_size", "smsp__cycles_active.avg.pct_of_peak_sustained_elapsed",
            "sm__cycles_elapsed.avg.per_second", "lts__t_sector_hit_rate.pct"]
@@ -62,13 +62,14 @@ def num(d, u, k):
         return None
     v = float(v.replace(",", ""))
     unit = u.get(k, "")
-    scale = {"Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "byte": 1.0, "nsecond": 1e-6, "usecond": 1e-3,
-             "msecond": 1.0, "cycle/nsecond": 1e3, "cycle/usecond": 1.0, "Ghz": 1e3, "Mhz": 1.0}.get(unit, 1.0)
+    scale = {"Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "byte": 1.0, "KB": 1e3, "MB": 1e6, "GB": 1e9,
+             "nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0, "ns": 1e-6, "us": 1e-3, "ms": 1.0, "s": 1e3,
+             "cycle/nsecond": 1e3, "cycle/usecond": 1.0, "Ghz": 1e3, "Mhz": 1.0}.get(unit, 1.0)
     return v * scale
 
 
 def full_table(rep, hbm_peak):
-    out = ["| kernel | grid | ms | DRAM rd+wr GB | achieved GB/s | % of HBM peak | dram % (ncu) | SM % | imma % | regs |",
+    out = ["| kernel | grid | ms | DRAM rd+wr GB | achieved GB/s | % of HBM peak | dram % (ncu) | SM % | tensor pipe % | regs |",
            "|---|---|---|---|---|---|---|---|---|---|"]
     for d, u in raw(rep):
         name = d.get("Kernel Name", "?").split("(")[0].replace("ozr::", "").replace("(anonymous namespace)::", "")
@@ -81,7 +82,7 @@ def full_table(rep, hbm_peak):
         out.append(f"| {name} | {d.get('launch__grid_size', '?')} | {ms:.3f} | {gb:.3f} | {gbs:.0f} | "
                    f"{100 * gbs / hbm_peak:.1f} | {f('dram__throughput.avg.pct_of_peak_sustained_elapsed')} | "
                    f"{f('sm__throughput.avg.pct_of_peak_sustained_elapsed')} | "
-                   f"{f('sm__pipe_tensor_op_imma_cycles_active.avg.pct_of_peak_sustained_elapsed')} | "
+                   f"{f('sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed')} | "
                    f"{d.get('launch__registers_per_thread', '?')} |")
     return "\n".join(out)
 
