@@ -339,6 +339,21 @@ LamStats lam_stats(const std::vector<double>& lam) {
 }
 
 
+// The first pair of exactly equal estimates in ascending (λ̂, index) order (for the error message when the
+// cluster branch is off; PAPER.md:333 assumes distinct eigenvalues). Returns false when all are distinct.
+bool equal_pair(const std::vector<double>& lam, int* a, int* b) {
+  std::vector<int> idx(lam.size());
+  for (size_t i = 0; i < lam.size(); ++i) idx[i] = static_cast<int>(i);
+  std::sort(idx.begin(), idx.end(), [&](int x, int y) { return lam[x] < lam[y] || (lam[x] == lam[y] && x < y); });
+  for (size_t q = 1; q < idx.size(); ++q)
+    if (lam[idx[q]] == lam[idx[q - 1]]) {
+      *a = idx[q - 1];
+      *b = idx[q];
+      return true;
+    }
+  return false;
+}
+
 int pairs_upto(int kA, int kB, int L) {
   int np = 0;
   for (int s = 1; s <= kA; ++s)
@@ -736,8 +751,12 @@ ozr_status sweep(ozr_ctx ctx, Exchange* ex, const double* A, int64_t n, int64_t 
   const double gap0 = ls_prev.gap0;
   const double gap = (P.cluster_mode && !(gap0 > 0.0)) ? ls_prev.gap_pos : gap0;
   const double maxlam = ls_prev.maxabs;
-  if (!(gap0 > 0.0) && P.cluster_mode == 0)
-    return fail(ctx, OZR_ERR_DEGENERATE, "equal eigenvalue estimates (gap = 0) with the cluster branch off");
+  if (!(gap0 > 0.0) && P.cluster_mode == 0) {
+    int pa = -1, pb = -1;
+    equal_pair(hlam, &pa, &pb);
+    return fail(ctx, OZR_ERR_DEGENERATE, "equal eigenvalue estimates λ̂_%d = λ̂_%d (gap = 0) with the cluster branch off",
+                pa, pb);
+  }
   const double ssum = sum_pow2_2c(hw);
   if (ssum == 0.0 || maxlam == 0.0) return fail(ctx, OZR_ERR_DEGENERATE, "zero X or zero spectrum");
   int beta_raw = (P.beta_override > 0) ? P.beta_override
@@ -894,8 +913,12 @@ ozr_status sweep(ozr_ctx ctx, Exchange* ex, const double* A, int64_t n, int64_t 
   OZR_X(scalars({demax}, &eRmax));
   LamStats ls_new = lam_stats(hlam_new);
   const double gap_new0 = ls_new.gap0;
-  if (!(gap_new0 > 0.0) && P.cluster_mode == 0)
-    return fail(ctx, OZR_ERR_DEGENERATE, "equal Rayleigh quotients (gap = 0) with the cluster branch off");
+  if (!(gap_new0 > 0.0) && P.cluster_mode == 0) {  // name the offending pair (PAPER.md:333 assumes none)
+    int pa = -1, pb = -1;
+    equal_pair(hlam_new, &pa, &pb);
+    return fail(ctx, OZR_ERR_DEGENERATE, "equal Rayleigh quotients λ̂_%d = λ̂_%d (gap = 0) with the cluster branch off",
+                pa, pb);
+  }
   const double gap_new = (gap_new0 > 0.0) ? gap_new0 : ls_new.gap_pos;
   if (eRmax == intmin) eRmax = -1074;
 
@@ -1330,7 +1353,8 @@ ozr_status ozr_create(ozr_ctx* out, int device, void* stream, int64_t n_max) {
   {
     int lo = 0, hi = 0;  // the recombination bands get the higher priority: their CTAs fill the SM room the
     cudaDeviceGetStreamPriorityRange(&lo, &hi);  // persistent GEMM leaves as soon as they are ready
-    cudaStreamCreateWithPriority(&c->rstream, cudaStreamNonBlocking, getenv("OZR_RPRIO0") ? lo : hi);
+    (void)lo;
+    cudaStreamCreateWithPriority(&c->rstream, cudaStreamNonBlocking, hi);
   }
   for (int i = 0; i < kMaxBands + 2; ++i) cudaEventCreateWithFlags(&c->bev[i], cudaEventDisableTiming);
   c->events = true;

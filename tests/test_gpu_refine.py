@@ -82,7 +82,7 @@ def test_refine_step_errors(ctx):
     assert e.value.status == 3
     with pytest.raises(ozr.OzrError) as e:   # equal eigenvalue estimates, cluster branch off
         _gpu_sweep(ctx, A, X, np.array([1.0, 1.0, 3, 4]), 1e-10, cluster_mode=0)
-    assert e.value.status == 4
+    assert e.value.status == 4 and "λ̂_0 = λ̂_1" in str(e.value)  # the error names the offending pair
 
 
 @pytest.mark.parametrize("cfg,n,start", [("c2", 512, "fp64"), ("c3", 1024, "fp64")])
