@@ -55,6 +55,30 @@ def test_params_default(libozr):
     import paper_2602_19090_b200 as ozr
     p = ozr.default_params()
     assert p.kA_split == 15 and p.truncate == 1 and p.beta_mode == 0 and abs(p.theta_V - 1 / 16) < 1e-18
+    # the ctypes mirror of ozr_params matches the C layout up to its last field
+    assert p.theta == 4.0 and p.cluster_mode == 1 and p.max_cluster == 16384 and p.form_R == 0
+    assert p.dense_cluster == 192 and p.row_nnz == 0 and p.max_escalations == 2
+
+def test_ctypes_structs_match_header(tmp_path):
+    """The binding's ctypes mirrors of ozr_params / ozr_step_report have the C header's size and field
+    offsets (compiled with gcc against include/ozr.h)."""
+    import paper_2602_19090_b200 as ozr
+    fields_p = [f for f, _ in ozr.Params._fields_]
+    fields_r = [f for f, _ in ozr.StepReport._fields_]
+    src = ["#include <stddef.h>", "#include <stdio.h>", '#include "ozr.h"', "int main(void) {",
+           '  printf("%zu %zu\\n", sizeof(ozr_params), sizeof(ozr_step_report));']
+    src += [f'  printf("%zu\\n", offsetof(ozr_params, {f}));' for f in fields_p]
+    src += [f'  printf("%zu\\n", offsetof(ozr_step_report, {f}));' for f in fields_r]
+    src += ["  return 0;", "}"]
+    c = tmp_path / "layout.c"
+    c.write_text("\n".join(src) + "\n")
+    exe = tmp_path / "layout"
+    subprocess.check_call(["gcc", "-I", os.path.join(ROOT, "include"), "-o", str(exe), str(c)])
+    vals = subprocess.check_output([str(exe)]).decode().split()
+    assert int(vals[0]) == ctypes.sizeof(ozr.Params) and int(vals[1]) == ctypes.sizeof(ozr.StepReport)
+    offs = [int(v) for v in vals[2:]]
+    assert offs[:len(fields_p)] == [getattr(ozr.Params, f).offset for f in fields_p]
+    assert offs[len(fields_p):] == [getattr(ozr.StepReport, f).offset for f in fields_r]
 
 
 def test_no_cpu_fallback(libozr):
