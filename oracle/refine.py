@@ -397,11 +397,11 @@ def forward_error(Xh_ref, Xl_ref, X, lam_ref=None, lam=None, power_iters=None):
     return float(np.sqrt(s))
 
 
-def sweep_columns(A, X, lam_prev, delta, J, theta=THETA_DEFAULT, beta=None):
+def sweep_columns(A, X, lam_prev, delta, J, theta=THETA_DEFAULT, beta=None, lam_rows=None):
     """Algorithm 1 restricted to the output columns J (bench.py's bounded CPU sample; identical formulas
     to sweep(), only the products' column sets shrink): V_J = A X̂^(1)_J, λ̂_J, Res_J,
-    W_{:,J} = X̂^(1)ᵀ Res_J, Ẽ_{:,J} (needs λ̂ of all columns: λ_prev is used for i ∉ J),
-    U_J = X̂^(1) Ẽ_{:,J}. Returns (X_new[:, J], λ̂_J, β)."""
+    W_{:,J} = X̂^(1)ᵀ Res_J, Ẽ_{:,J} (needs λ̂ of all columns: `lam_rows` for i ∉ J — the full sweep's
+    Rayleigh quotients when given, else λ_prev), U_J = X̂^(1) Ẽ_{:,J}. Returns (X_new[:, J], λ̂_J, β)."""
     A = np.asarray(A, dtype=np.float64)
     X = np.asarray(X, dtype=np.float64)
     n = A.shape[0]
@@ -423,7 +423,7 @@ def sweep_columns(A, X, lam_prev, delta, J, theta=THETA_DEFAULT, beta=None):
     Rh, Rl = dd_add(Vh, Vl, -ph, -pl)
     Wh, Wl = _clib.dd_gemm_nt(np.ascontiguousarray(X1.T), np.ascontiguousarray(Rh.T), None,
                               np.ascontiguousarray(Rl.T))
-    lam = np.array(lam_prev, dtype=np.float64)
+    lam = np.array(lam_prev if lam_rows is None else lam_rows, dtype=np.float64)
     lam[J] = lamJ
     dl = lamJ[None, :] - lam[:, None]
     E = np.where(dl != 0, (Wh + Wl) / np.where(dl != 0, dl, 1.0), 0.0)

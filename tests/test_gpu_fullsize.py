@@ -71,6 +71,14 @@ def test_refine_step_fullsize_sampled_lambda(ctx, big):
     dl = np.abs(to_np(lam)[J] - (lh + ll)) / np.max(np.abs(ln))
     assert np.max(dl) <= 1e-13, dl
     assert rep["net_update"] > 0 and np.all(np.isfinite(to_np(X)[:, J]))
+    # X̂_new of sampled columns (outside the sweep's unresolved groups) vs the oracle's column-restricted
+    # sweep with exact products; λ̂_i of the other rows of Ẽ from the GPU sweep (semi-independent: those were
+    # checked column by column above and in the n ≤ 4096 parity tests)
+    groups = ozr.ozr_last_clusters(ctx)
+    inJ = set(j for g in groups for j in g)
+    J2 = np.array([j for j in (1, 2, 1000, 4095, 6000, 8189) if j not in inJ])
+    Xo, lo, bo = orf.sweep_columns(An, Xn, ln, cfg["delta"], J2, theta=p.theta, beta=rep["beta"], lam_rows=to_np(lam))
+    assert np.max(np.abs(to_np(X)[:, J2] - Xo)) <= 1e-13
 
 
 def test_refine_to_tol_fullsize_residual_properties(ctx, big):
