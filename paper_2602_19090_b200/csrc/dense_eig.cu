@@ -161,7 +161,7 @@ __global__ void __launch_bounds__(256)
   for (int l = threadIdx.x; l < m; l += 256) y[l] *= sg;
   if (threadIdx.x == 0) {
     lam[J[k]] = mu + th[k];
-    if (k == 0 && *info != 0) atomicOr(err, ERR_RANGE);
+    if (k == 0 && *info != 0) atomicOr(err, ERR_SOLVER);
   }
 }
 

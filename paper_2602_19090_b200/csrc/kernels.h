@@ -7,7 +7,7 @@
 
 namespace ozr {
 
-enum { ERR_NONFINITE = 1, ERR_RANGE = 2, ERR_DEGENERATE = 4 };
+enum { ERR_NONFINITE = 1, ERR_RANGE = 2, ERR_DEGENERATE = 4, ERR_SOLVER = 8 };
 
 constexpr int kMaxChunks = 8;
 constexpr int kPlanGroups = 96;
@@ -100,7 +100,7 @@ struct ClusterLaunch {
   double* coop_scratch;    // >= 5·mmax + 8 doubles
   int* coop_flags;         // >= 128 ints
   int dense_min;           // groups of at least this many columns take the dense solver (dense_eig.cu)
-  int* err;                // error flags (ERR_RANGE when the dense solver reports failure)
+  int* err;                // error flags (ERR_SOLVER when the dense solver reports failure)
 };
 // Dense symmetric eigensolver state of one context (cuSOLVER syevd, dlopen'ed; dense_eig.cu).
 struct DenseEig {

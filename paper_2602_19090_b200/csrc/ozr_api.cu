@@ -561,6 +561,7 @@ RecombPlan shift_plan(const RecombPlan& rp, int t0) {
 }
 
 ozr_status err_bits(ozr_ctx ctx, int h) {
+  if (h & ERR_SOLVER) return fail(ctx, OZR_ERR_CUDA, "dense cluster sub-solve: syevd reported failure (info != 0)");
   if (h & ERR_NONFINITE) return fail(ctx, OZR_ERR_NONFINITE, "non-finite value in an input matrix");
   if (h & ERR_RANGE) return fail(ctx, OZR_ERR_RANGE, "exponent range exceeded in the digit split");
   if (h & ERR_DEGENERATE)
