@@ -773,8 +773,10 @@ ozr_status sweep(ozr_ctx ctx, Exchange* ex, const double* A, int64_t n, int64_t 
     if (x != 0.0) cmax = std::max(cmax, ceil_log2_host(x));
   rep.beta = beta;
   rep.beta_raw = beta_raw;
-  rep.alpha = (P.beta_mode == 2) ? 53 - beta + ceil_log2_host(static_cast<double>(P.row_nnz > 0 && P.row_nnz < n ? P.row_nnz : n))
-                                 : alpha_dense(n, beta);
+  // α (reported only): §4.1 53 − β + ⌈log2 √n⌉; §3.3 53 − β + ⌈log2 n⌉ (eq. proposed_beta); §4.3 53 − β + ⌈log2 k⌉
+  rep.alpha = (P.beta_mode == 2)   ? 53 - beta + ceil_log2_host(static_cast<double>(P.row_nnz > 0 && P.row_nnz < n ? P.row_nnz : n))
+              : (P.beta_mode == 1) ? 53 - beta + ceil_log2_host(static_cast<double>(n))
+                                   : alpha_dense(n, beta);
   rep.kX = kx;
   rep.gap_min = gap0;
   rep.max_abs_lambda = maxlam;

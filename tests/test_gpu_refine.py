@@ -167,3 +167,23 @@ def test_sparse_beta_banded(ctx):
                                      ozr.default_params(delta=delta, beta_mode=2, row_nnz=k, max_sweeps=6))
     assert st == 0
     assert orf.forward_error(Xh, Xl, to_np(Xd), lh, to_np(ld)) <= delta
+
+
+@pytest.mark.parametrize("mode", ["untruncated", "theoretical_xi_n", "theoretical_xi_1"])
+def test_sweep_modes_match_oracle(ctx, mode):
+    """The other β / truncation readings against the oracle sweep with the same settings (c2 recipe, n = 512,
+    FP64 start, δ = 1e-14): truncate = 0 (X̂ kept whole — the prior work's untruncated two-sided analogue,
+    PAPER.md:432-443) and §3.3's eq. proposed_beta (⌈·⌉) with ξ = n and ξ = 1."""
+    A, lam0, X0 = _case("c2", 512, "fp64")
+    delta = 1e-14
+    gkw, okw = {
+        "untruncated": (dict(truncate=0), dict(truncate=False)),
+        "theoretical_xi_n": (dict(beta_mode=1, xi=0.0), dict(beta_mode="theoretical", xi=None)),
+        "theoretical_xi_1": (dict(beta_mode=1, xi=1.0), dict(beta_mode="theoretical", xi=1.0)),
+    }[mode]
+    Xg, lg, rep = _gpu_sweep(ctx, A, X0, lam0, delta, **gkw)
+    Xo, lo, info = orf.sweep(A, X0, lam0, delta, **okw)
+    if mode != "untruncated":
+        assert rep["beta"] == info["beta"] and rep["alpha"] == info["alpha"]
+    assert np.max(np.abs(Xg - Xo)) <= 1e-13
+    assert np.max(np.abs(lg - lo)) <= 1e-13 * np.max(np.abs(lam0))
