@@ -169,17 +169,23 @@ def test_sparse_beta_banded(ctx):
     assert orf.forward_error(Xh, Xl, to_np(Xd), lh, to_np(ld)) <= delta
 
 
-@pytest.mark.parametrize("mode", ["untruncated", "theoretical_xi_n", "theoretical_xi_1"])
+@pytest.mark.parametrize("mode", ["untruncated", "theoretical_xi_n", "theoretical_xi_1", "theta_1", "global_budgets",
+                                  "paper_alg1"])
 def test_sweep_modes_match_oracle(ctx, mode):
     """The other β / truncation readings against the oracle sweep with the same settings (c2 recipe, n = 512,
     FP64 start, δ = 1e-14): truncate = 0 (X̂ kept whole — the prior work's untruncated two-sided analogue,
-    PAPER.md:432-443) and §3.3's eq. proposed_beta (⌈·⌉) with ξ = n and ξ = 1."""
+    PAPER.md:432-443), §3.3's eq. proposed_beta (⌈·⌉) with ξ = n and ξ = 1, θ = 1 (the
+    paper's own δ), one pair budget per product instead of per 256-column tile (R8 without R8b), and the
+    paper's Algorithm 1 without the cluster branch (cluster_mode 0)."""
     A, lam0, X0 = _case("c2", 512, "fp64")
     delta = 1e-14
     gkw, okw = {
         "untruncated": (dict(truncate=0), dict(truncate=False)),
         "theoretical_xi_n": (dict(beta_mode=1, xi=0.0), dict(beta_mode="theoretical", xi=None)),
         "theoretical_xi_1": (dict(beta_mode=1, xi=1.0), dict(beta_mode="theoretical", xi=1.0)),
+        "theta_1": (dict(theta=1.0), dict(theta=1.0)),
+        "global_budgets": (dict(tile_budgets=0), dict()),
+        "paper_alg1": (dict(cluster_mode=0), dict(cluster_mode=0)),
     }[mode]
     Xg, lg, rep = _gpu_sweep(ctx, A, X0, lam0, delta, **gkw)
     Xo, lo, info = orf.sweep(A, X0, lam0, delta, **okw)
