@@ -111,3 +111,33 @@ def test_refine_to_tol_fullsize_residual_properties(ctx, big):
         est.append(np.sqrt(np.sum((C[:, q] / d) ** 2) + (1.0 - G[q, q]) ** 2 / 4))
     est = np.array(est)
     assert np.all(est[:4] <= cfg["delta"]), est        # columns with gap_j ≥ δ-resolvable spectra
+
+
+def test_c5_fullsize_sampled_sweep(ctx):
+    """BASELINE c5 at its full size (n = 16384, cnd 1e10, FP64 start, δ = 1e-15): the contraction length
+    caps a diagonal's int32 group at ⌊(2^31 − 1)/(16384·2^14)⌋ = 7 pairs, so the V product runs with more
+    than 12 pair groups (the general multi-chunk recombination path). One sweep on the GPU vs the oracle's
+    column-restricted sweep with exact products on sampled columns: same β, λ̂_J and X̂_new[:, J] within
+    1e-13 (λ̂ of the other rows of Ẽ from the GPU sweep, as in the n = 8192 test)."""
+    import torch
+
+    import paper_2602_19090_b200 as ozr
+    import workloads as W
+    A, lam0, X0, cfg = W.make_config_torch("c5", torch.device("cuda", 0))
+    n = cfg["n"]
+    X = ozr.colmajor(X0.clone())
+    lam = lam0.clone()
+    p = ozr.default_params(delta=cfg["delta"])
+    rep = ozr.ozr_refine_step(ctx, A, X, lam, p)
+    assert len(ozr.ozr_gemm_plan(n, rep["kA"], rep["kX"], rep["L_V"])) > 12  # the multi-chunk path
+    An, ln, Xn = to_np(A), to_np(lam0), to_np(X0)
+    del A, X0
+    w = np.max(np.abs(Xn), axis=0)
+    beta, _ = orf.choose_beta(n, cfg["delta"] / p.theta, ln, osp.ceil_log2(w), w)
+    assert rep["beta"] == min(max(beta, 2), 52)
+    groups = ozr.ozr_last_clusters(ctx)
+    inJ = set(j for g in groups for j in g)
+    J = np.array([j for j in (3, 5000, 9000, 16383) if j not in inJ])
+    Xo, lo, bo = orf.sweep_columns(An, Xn, ln, cfg["delta"], J, theta=p.theta, beta=rep["beta"], lam_rows=to_np(lam))
+    assert np.max(np.abs(to_np(lam)[J] - lo)) <= 1e-13 * np.max(np.abs(ln))
+    assert np.max(np.abs(to_np(X)[:, J] - Xo)) <= 1e-13
