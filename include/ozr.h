@@ -184,10 +184,13 @@ ozr_status ozr_last_R(ozr_ctx ctx, double* R, int64_t ldr);
  * (*ngroups / offsets still tell the sizes needed when offsets has room). */
 ozr_status ozr_last_clusters(ozr_ctx ctx, int* members, int max_members, int* offsets, int max_groups, int* ngroups);
 
-/* Repeat sweeps until the stop rule (R12): after sweep k stop when ν_k ≤ δ or ν_k² max|λ̂| /
- * (n gap) ≤ δ; report OZR_ERR_NOT_CONVERGED on stagnation (ν_k > ν_{k−1}/2) or when max_sweeps is
- * reached without converging — X / lambda then hold the last completed sweep. history (host, nullable)
- * receives up to max_hist reports; sweeps_done (host, nullable). */
+/* Repeat sweeps until the stop rule (R12), with ν_k = ‖X̂_k − X̂_{k−1}‖_F: after sweep k stop
+ * when ν_k ≤ δ, or ν_k² max|λ̂| / (n gap) ≤ δ, or — once ν_k ≤ √n·δ — when a power-iteration estimate of
+ * ‖X̂_k − X̂_{k−1}‖₂ (the paper's measure, reported as update_2norm) is ≤ δ. Sweeps with unresolved groups
+ * (cluster sub-solves rotate columns) are not compared for stagnation; otherwise stagnation
+ * (ν_k > ν_{k−1}/2) first escalates θ ← 16θ up to max_escalations times, then reports
+ * OZR_ERR_NOT_CONVERGED, as does reaching max_sweeps — X / lambda then hold the last completed sweep.
+ * history (host, nullable) receives up to max_hist reports; sweeps_done (host, nullable). */
 ozr_status ozr_refine_to_tol(ozr_ctx ctx, const double* A, int64_t n, int64_t lda, double* X, int64_t ldx,
                              double* lambda, const ozr_params* params, ozr_step_report* history, int max_hist,
                              int* sweeps_done);
