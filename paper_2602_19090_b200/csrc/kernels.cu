@@ -499,12 +499,21 @@ __device__ __forceinline__ void split_fixed_body(const double* __restrict__ col,
 __device__ __forceinline__ void split_wide_body_prmt(const double* __restrict__ col, int rows, int k, int S, int e,
                                                     int8_t* __restrict__ base, long long pstride) {
   constexpr unsigned long long P80 = 0x8080808080808080ULL;
+  double xin[4];  // the next group's rows are loaded while this group is packed
+#pragma unroll
+  for (int r = 0; r < 4; ++r) xin[r] = (4 * threadIdx.x + r < rows) ? col[4 * threadIdx.x + r] : 0.0;
   for (int i0 = 4 * threadIdx.x; i0 < rows; i0 += 4 * BS) {
+    double xcur[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      xcur[r] = xin[r];
+      const int inext = i0 + 4 * BS + r;
+      xin[r] = (inext < rows) ? col[inext] : 0.0;
+    }
     uint32_t E[4][4];
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
-      const int i = i0 + r;
-      const double y = (i < rows) ? rint(ldexp_fast(col[i], S - e)) : 0.0;
+      const double y = rint(ldexp_fast(xcur[r], S - e));
       long long x;
       int q;
       if (fabs(y) < 9007199254740992.0) {
