@@ -91,6 +91,18 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
+def _int8_microbench(achieved):
+    """The tcgen05 kind::i8 peak measured by tools/i8_peak.cu on this pool's B200s (profiles/int8_peak.json),
+    reported beside the contract's denominator (2 x the measured bf16 peak)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "int8_peak.json")) as f:
+            mb = json.load(f)
+        return {"int8_microbench_tops": {"burst": mb["int8_tops_burst"], "sustained": mb["int8_tops_sustained"]},
+                "frac_of_microbench_burst": achieved / mb["int8_tops_burst"]}
+    except Exception:
+        return {}
+
+
 def _dist():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -303,6 +315,7 @@ def main():
                 "peak_source": f"2 x bf16_tflops (burst) of {src} MEASURED_PEAKS.json (nominal int8:bf16 = 4.5:2.25)",
                 "frac_of_sustained_peak": achieved / int8_sus,
                 "frac_of_nominal_peak": achieved / 4500.0,
+                **_int8_microbench(achieved),
                 "nominal_peak_note": "4.5 POPS = the datasheet dense INT8 figure (2 x the 2.25 PFLOP/s bf16 nominal)",
                 "kernel": "k_gemm_i8 (tcgen05 kind::i8 slice products; V, W, U launches of the timed sweeps)",
                 "gemm_share_of_step": gemm_ms / ms,

@@ -15,7 +15,7 @@ using namespace ozr;
 constexpr int BM = 128, BN = 256, BK = 128, UMMA_K = 32;
 constexpr int A_BYTES = BM * BK, B_HALF = (BN / 2) * BK;
 
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1) k_i8_peak(long long iters, int* sink) {
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1) k_i8_peak(long long iters, int* sink, int random_bits) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
@@ -24,8 +24,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1) k_i8_peak(lo
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const bool leader = cluster_ctarank() == 0;
-  for (int i = threadIdx.x; i < (A_BYTES + B_HALF) / 4; i += blockDim.x)
-    reinterpret_cast<uint32_t*>(smem)[i] = 0x01010101u * (i & 7);
+  // operand bytes: pseudo-random (random_bits = 1, the power a real digit plane draws) or a low-toggle
+  // pattern (random_bits = 0)
+  for (int i = threadIdx.x; i < (A_BYTES + B_HALF) / 4; i += blockDim.x) {
+    uint32_t h = static_cast<uint32_t>(i + 977 * blockIdx.x) * 2654435761u;
+    h ^= h >> 15;
+    h *= 2246822519u;
+    h ^= h >> 13;
+    reinterpret_cast<uint32_t*>(smem)[i] = random_bits ? h : 0x01010101u * (i & 7);
+  }
   if (threadIdx.x == 0) {
     mbar_init(done, 1);
     fence_mbar_init();
@@ -73,29 +80,32 @@ int main() {
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
-  double res[2] = {0, 0};
+  double res[2][2] = {{0, 0}, {0, 0}};  // [random_bits][burst, sustained]
   const double target_s[2] = {0.2, 4.0};
   long long iters = 2000;
-  k_i8_peak<<<grid, 128, smem>>>(iters, sink);  // warm-up
+  k_i8_peak<<<grid, 128, smem>>>(iters, sink, 1);  // warm-up
   cudaDeviceSynchronize();
-  for (int m = 0; m < 2; ++m) {
-    cudaEventRecord(e0);
-    k_i8_peak<<<grid, 128, smem>>>(iters, sink);
-    cudaEventRecord(e1);
-    cudaEventSynchronize(e1);
-    float ms = 0.f;
-    cudaEventElapsedTime(&ms, e0, e1);
-    const long long it2 = static_cast<long long>(iters * (target_s[m] * 1e3 / ms));  // scale to the target
-    cudaEventRecord(e0);
-    k_i8_peak<<<grid, 128, smem>>>(it2, sink);
-    cudaEventRecord(e1);
-    cudaEventSynchronize(e1);
-    cudaEventElapsedTime(&ms, e0, e1);
-    const double ops = 2.0 * (grid / 2) * static_cast<double>(it2) * (BK / UMMA_K) * (2.0 * BM) * BN * UMMA_K;
-    res[m] = ops / (ms * 1e-3) / 1e12;
-  }
+  for (int rb = 0; rb < 2; ++rb)
+    for (int m = 0; m < 2; ++m) {
+      cudaEventRecord(e0);
+      k_i8_peak<<<grid, 128, smem>>>(iters, sink, rb);
+      cudaEventRecord(e1);
+      cudaEventSynchronize(e1);
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, e0, e1);
+      const long long it2 = static_cast<long long>(iters * (target_s[m] * 1e3 / ms));  // scale to the target
+      cudaEventRecord(e0);
+      k_i8_peak<<<grid, 128, smem>>>(it2, sink, rb);
+      cudaEventRecord(e1);
+      cudaEventSynchronize(e1);
+      cudaEventElapsedTime(&ms, e0, e1);
+      const double ops = 2.0 * (grid / 2) * static_cast<double>(it2) * (BK / UMMA_K) * (2.0 * BM) * BN * UMMA_K;
+      res[rb][m] = ops / (ms * 1e-3) / 1e12;
+    }
   const cudaError_t err = cudaGetLastError();
-  printf("{\"int8_tops_burst\": %.1f, \"int8_tops_sustained\": %.1f, \"ctas\": %d, \"error\": \"%s\"}\n", res[0], res[1],
-         grid, cudaGetErrorString(err));
+  printf("{\"int8_tops_burst\": %.1f, \"int8_tops_sustained\": %.1f, \"low_toggle_burst\": %.1f, "
+         "\"low_toggle_sustained\": %.1f, \"ctas\": %d, \"operands\": \"pseudo-random bytes (first pair), a "
+         "low-toggle pattern (second pair)\", \"error\": \"%s\"}\n",
+         res[1][0], res[1][1], res[0][0], res[0][1], grid, cudaGetErrorString(err));
   return err == cudaSuccess ? 0 : 1;
 }
