@@ -229,9 +229,15 @@ __global__ void __launch_bounds__(NWARPS * 32, 1)
 // peer's. Per SM, the shared-memory fill per K-block drops from 48 KB to 32 KB for the same MMA work
 // (the single-CTA form is bound by L2 → SM operand traffic). Roles per CTA as in the single-CTA form; the
 // leader fetches the jobs and mirrors them into the peer's queue (DSMEM), the MMA warp is the leader's.
-constexpr int STAGES2 = 6;
+// A stage holds KH2 = 2 K-blocks of 128 B (two swizzle atoms per operand, loaded by separate TMA boxes): the
+// MMA issuer commits the stage back to the producer once per 8 MMAs instead of once per 4 — a tcgen05.commit
+// per 4 MMAs costs 37 % of the MMA rate, per 8 MMAs 16 % (tools/i8_peak.cu). Same 192 KB ring.
+constexpr int KH2 = 2;
+constexpr int STAGES2 = 3;
 constexpr int B_HALF_BYTES = (BN / 2) * BK;
-constexpr int SMEM2_BYTES = STAGES2 * (A_STAGE_BYTES + B_HALF_BYTES) + 1024 /*align*/ + 512 /*barriers*/;
+constexpr int A_STAGE2 = KH2 * A_STAGE_BYTES;
+constexpr int B_STAGE2 = KH2 * B_HALF_BYTES;
+constexpr int SMEM2_BYTES = STAGES2 * (A_STAGE2 + B_STAGE2) + 1024 /*align*/ + 512 /*barriers*/;
 
 // order 0: (band, m-tile, n-tile, group) — a tile's groups back to back;
 // order 1: (band, m-tile, group, n-tile) — the band's n-tiles of one group back to back: those jobs read the
@@ -271,8 +277,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NWARPS * 32, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
-  uint8_t* sB = smem + STAGES2 * A_STAGE_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES2 * B_HALF_BYTES);
+  uint8_t* sB = smem + STAGES2 * A_STAGE2;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES2 * B_STAGE2);
   uint64_t* empty = full + STAGES2;
   uint64_t* acc_full = empty + STAGES2;  // [2]
   uint64_t* acc_empty = acc_full + 2;    // [2] (leader's)
@@ -285,7 +291,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NWARPS * 32, 1)
   const int lane = threadIdx.x & 31;
   const uint32_t rank = cluster_ctarank();
   const bool leader = (rank == 0);
-  const int nkb = (K + BK - 1) / BK;
+  const int nkb = (K + KH2 * BK - 1) / (KH2 * BK);  // stages of KH2 K-blocks
 
   if (threadIdx.x == 0) {
     tma_prefetch(&tmA);
@@ -350,7 +356,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NWARPS * 32, 1)
           const int stage = it % STAGES2;
           const uint32_t phase = (it / STAGES2) & 1;
           mbar_wait(&empty[stage], phase ^ 1);
-          if (leader) mbar_arrive_expect_tx(&full[stage], 2 * (A_STAGE_BYTES + B_HALF_BYTES));
+          if (leader) mbar_arrive_expect_tx(&full[stage], 2 * (A_STAGE2 + B_STAGE2));
           // kouter: K-block outer, the group's pairs inner — at any moment every job of a tile's neighbourhood
           // reads the same K-block of the A planes, so L2 serves them all from one DRAM fetch
           int p, kb;
@@ -362,10 +368,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NWARPS * 32, 1)
             kb = q - (q / nkb) * nkb;
           }
           const uint32_t fb = mapa_u32(&full[stage], 0);  // the leader's barrier counts both CTAs' bytes
-          tma_load_3d_2sm_hint(sA + stage * A_STAGE_BYTES, &tmA, fb, kb * BK, ji.m0 + static_cast<int>(rank) * BM,
-                               pt.s[p], polA);
-          tma_load_3d_2sm_hint(sB + stage * B_HALF_BYTES, &tmB, fb, kb * BK, ji.n0 + static_cast<int>(rank) * (BN / 2),
-                               pt.t[p], polB);
+#pragma unroll
+          for (int h = 0; h < KH2; ++h) {  // K beyond the extent is zero-filled by the tensor map
+            tma_load_3d_2sm_hint(sA + stage * A_STAGE2 + h * A_STAGE_BYTES, &tmA, fb, (kb * KH2 + h) * BK,
+                                 ji.m0 + static_cast<int>(rank) * BM, pt.s[p], polA);
+            tma_load_3d_2sm_hint(sB + stage * B_STAGE2 + h * B_HALF_BYTES, &tmB, fb, (kb * KH2 + h) * BK,
+                                 ji.n0 + static_cast<int>(rank) * (BN / 2), pt.t[p], polB);
+          }
         }
       }
     }
@@ -393,14 +402,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NWARPS * 32, 1)
           const uint32_t phase = (it / STAGES2) & 1;
           mbar_wait(&full[stage], phase);
           tc_fence_after();
-          const uint32_t a_addr = smem_u32(sA + stage * A_STAGE_BYTES);
-          const uint32_t b_addr = smem_u32(sB + stage * B_HALF_BYTES);
+          const uint32_t a_addr = smem_u32(sA + stage * A_STAGE2);
+          const uint32_t b_addr = smem_u32(sB + stage * B_STAGE2);
 #pragma unroll
-          for (int k = 0; k < BK / UMMA_K; ++k) {
-            const uint64_t ad = umma_desc_kmajor_sw128(a_addr + k * UMMA_K);
-            const uint64_t bd = umma_desc_kmajor_sw128(b_addr + k * UMMA_K);
-            mma_i8_2sm(acc, ad, bd, idesc, (q > 0 || k > 0) ? 1u : 0u);
-          }
+          for (int h = 0; h < KH2; ++h)
+#pragma unroll
+            for (int k = 0; k < BK / UMMA_K; ++k) {
+              const uint64_t ad = umma_desc_kmajor_sw128(a_addr + h * A_STAGE_BYTES + k * UMMA_K);
+              const uint64_t bd = umma_desc_kmajor_sw128(b_addr + h * B_HALF_BYTES + k * UMMA_K);
+              mma_i8_2sm(acc, ad, bd, idesc, (q > 0 || h > 0 || k > 0) ? 1u : 0u);
+            }
           mma_commit_2sm(&empty[stage], 0x3);  // frees the stage in both CTAs
         }
         mma_commit_2sm(&acc_full[buf], 0x3);
