@@ -312,7 +312,7 @@ def _reference_rr(E, lh, ll, J, Sh, Sl, Gh, Gl, R):
     ll[J] = 0.0
 
 
-def reference_eigvecs(A, X0, lam0, tol=1e-27, max_sweeps=10, cluster_kappa=None):
+def reference_eigvecs(A, X0, lam0, tol=1e-27, max_sweeps=10, cluster_kappa=None, X0_lo=None):
     """Reference eigenvectors of the STORED A (PAPER.md:62 uses a pseudo-quadruple reference): the
     Ogita–Aishima iteration (the R/S form ẽ_ij = (s_ij + λ̃_j r_ij)/(λ̃_j − λ̃_i))
     with X̂ kept in double-double and every product in double-double, untruncated, from an LAPACK
@@ -323,7 +323,8 @@ def reference_eigvecs(A, X0, lam0, tol=1e-27, max_sweeps=10, cluster_kappa=None)
     exact families."""
     A = np.asarray(A, dtype=np.float64)
     n = A.shape[0]
-    Xh, Xl = np.array(X0, dtype=np.float64), np.zeros((n, n))
+    Xh = np.array(X0, dtype=np.float64)  # X0_lo: resume from a double-double state of an earlier call
+    Xl = np.zeros((n, n)) if X0_lo is None else np.array(X0_lo, dtype=np.float64)
     hist = []
     lh = ll = None
     for k in range(max_sweeps):
