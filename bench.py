@@ -203,6 +203,7 @@ def main():
     ap.add_argument("--impl", default="ozr", choices=["ozr", "reference"])
     ap.add_argument("--ref-cols", type=int, default=16)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-c4", action="store_true", help="skip the BASELINE c4 time-to-target line")
     ap.add_argument("--e2e-steps", type=int, default=16)
     ap.add_argument("--truncate", type=int, default=1,
                     help="1: the paper's X̂ → X̂^(1) truncation (default); 0: keep all of X̂ — the untruncated "
@@ -334,7 +335,24 @@ def main():
     torch.cuda.synchronize()
     ttt = {"ms": t0.elapsed_time(t1), "sweeps": len(hist), "status": int(st), "delta": delta,
            "net_update_per_sweep": [h["net_update"] for h in hist],
-           "note": "self-certified stop (DESIGN.md R12); forward error vs oracle reference verified in tests at n<=1024"}
+           "note": "self-certified stop (DESIGN.md R12); oracle-verified first hit at n=4096: 2 sweeps "
+                   "(profiles/r01_ttt_verified_n4096.json); forward error vs the oracle in tests at n<=2048"}
+    # BASELINE c4 (the n = 8192 configuration as BASELINE.json states it: cnd 1e14, FP32-eigensolver start,
+    # gate 1e-10): its time to target beside the headline c4' (1 GPU only; the group sub-solve is replicated)
+    ttt_c4 = None
+    if not dist_mode and not args.no_c4 and name == "c4p" and not args.n:
+        A4, l4, X4, cfg4 = W.make_config_torch("c4", dev)
+        X4 = ozr.colmajor(X4)
+        torch.cuda.synchronize()
+        t0.record()
+        st4, h4 = ozr.ozr_refine_to_tol(ctx, A4, X4, l4, ozr.default_params(delta=cfg4["delta"], max_sweeps=12))
+        t1.record()
+        torch.cuda.synchronize()
+        ttt_c4 = {"ms": t0.elapsed_time(t1), "sweeps": len(h4), "status": int(st4), "delta": cfg4["delta"],
+                  "largest_group": max(h["max_cluster"] for h in h4),
+                  "workload": "c4: " + _describe(cfg4, cfg4["n"]),
+                  "note": "FP32 start: the first sweep's 6628-column group takes the dense sub-solve (cuSOLVER syevd)"}
+        del A4, X4, l4
 
     # e2e: a stream of independent problems through the public API with HOST (pinned) buffers. Every step
     # copies its A, X̂₀, λ̂₀ in and its X̂, λ̂ out; the copies of the neighbouring steps run on two copy streams
@@ -426,7 +444,7 @@ def main():
                                                        "pairs_V", "pairs_W", "pairs_U", "n_clusters", "max_cluster")}},
                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                "gpu_launches": int(sum(r["launches"] for r in reps)), "clocks": clocks,
-               "time_to_target": ttt}
+               "time_to_target": ttt, "time_to_target_c4": ttt_c4}
         emit(out)
     ctx.close()
     if comm is not None:
