@@ -342,17 +342,19 @@ def main():
     ttt_c4 = None
     if not dist_mode and not args.no_c4 and name == "c4p" and not args.n:
         A4, l4, X4, cfg4 = W.make_config_torch("c4", dev)
-        X4 = ozr.colmajor(X4)
-        torch.cuda.synchronize()
-        t0.record()
-        st4, h4 = ozr.ozr_refine_to_tol(ctx, A4, X4, l4, ozr.default_params(delta=cfg4["delta"], max_sweeps=12))
-        t1.record()
-        torch.cuda.synchronize()
+        p4 = ozr.default_params(delta=cfg4["delta"], max_sweeps=12)
+        for _ in range(2):  # the first run grows the context's workspace (group buffers); the second is timed
+            Xw, lw = ozr.colmajor(X4.clone()), l4.clone()
+            torch.cuda.synchronize()
+            t0.record()
+            st4, h4 = ozr.ozr_refine_to_tol(ctx, A4, Xw, lw, p4)
+            t1.record()
+            torch.cuda.synchronize()
         ttt_c4 = {"ms": t0.elapsed_time(t1), "sweeps": len(h4), "status": int(st4), "delta": cfg4["delta"],
                   "largest_group": max(h["max_cluster"] for h in h4),
                   "workload": "c4: " + _describe(cfg4, cfg4["n"]),
                   "note": "FP32 start: the first sweep's 6628-column group takes the dense sub-solve (cuSOLVER syevd)"}
-        del A4, X4, l4
+        del A4, X4, l4, Xw, lw
 
     # e2e: a stream of independent problems through the public API with HOST (pinned) buffers. Every step
     # copies its A, X̂₀, λ̂₀ in and its X̂, λ̂ out; the copies of the neighbouring steps run on two copy streams
