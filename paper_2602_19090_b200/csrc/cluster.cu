@@ -117,25 +117,32 @@ __global__ void __launch_bounds__(TB* TB)
                     const double* __restrict__ r_hi, const double* __restrict__ r_lo, const int32_t* __restrict__ wplanes,
                     long long wpstride, const __grid_constant__ RecombPlan rpW, const int32_t* __restrict__ ellR,
                     int scale8, const double* __restrict__ lam, double* __restrict__ Mbuf, double* __restrict__ Rbuf,
-                    int col0, int ncols) {
+                    int col0, int ncols, int ntiles_dot, const double* __restrict__ Gbuf) {
   const int4 t = tiles[blockIdx.x];  // (group, a0, b0, m)
   const int grp = t.x, a0 = t.y, b0 = t.z, m = t.w;
   const int tx = threadIdx.x % TB, ty = threadIdx.x / TB;
   const int a = a0 + ty, b = b0 + tx;
   const int* J = mem + goff[grp];
+  const bool from_digits = static_cast<int>(blockIdx.x) < ntiles_dot;
   unsigned long long lo = 0;
   long long hi = 0;
-  for (int q = 0; q < nsplit; ++q) {  // fixed order (exact anyway)
-    const unsigned long long* p = part + ((static_cast<long long>(blockIdx.x) * nsplit + q) * (TB * TB) + threadIdx.x) * 2;
-    const unsigned long long s = lo + p[0];
-    hi += static_cast<long long>(p[1]) + (s < lo ? 1 : 0);
-    lo = s;
-  }
+  if (from_digits)
+    for (int q = 0; q < nsplit; ++q) {  // fixed order (exact anyway)
+      const unsigned long long* p = part + ((static_cast<long long>(blockIdx.x) * nsplit + q) * (TB * TB) + threadIdx.x) * 2;
+      const unsigned long long s = lo + p[0];
+      hi += static_cast<long long>(p[1]) + (s < lo ? 1 : 0);
+      lo = s;
+    }
   if (a >= m || b >= m) return;
   const int i = J[a], j = J[b];
-  const i128 SQ = static_cast<i128>((static_cast<u128>(static_cast<unsigned long long>(hi)) << 64) | lo);
-  const dd gdd = i128_to_dd(SQ);
-  const double g = ldexp_fast(gdd.hi, gexp[i] + gexp[j]);
+  double g;
+  if (from_digits) {
+    const i128 SQ = static_cast<i128>((static_cast<u128>(static_cast<unsigned long long>(hi)) << 64) | lo);
+    const dd gdd = i128_to_dd(SQ);
+    g = ldexp_fast(gdd.hi, gexp[i] + gexp[j]);
+  } else {  // RN of the same exact integer, scaled by the same power of two (tensor-core Gram)
+    g = Gbuf[static_cast<long long>(gsq[grp]) + static_cast<long long>(b) * m + a];
+  }
   const double r = (a == b) ? (r_hi[i] + r_lo[i]) : -g;
   const long long o = static_cast<long long>(gsq[grp]) + static_cast<long long>(b) * m + a;
   Rbuf[o] = r;  // every rank (from the all-gathered digits)
@@ -474,7 +481,22 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+__global__ void k_gather_digit_cols(const int8_t* __restrict__ dig, long long ld, long long pstride, const int* __restrict__ J,
+                                    int8_t* __restrict__ out, long long opstride, const int32_t* __restrict__ g,
+                                    int32_t* __restrict__ gJ) {
+  const int a = blockIdx.x, p = blockIdx.y;  // ld % 16 == 0: 16-byte copies
+  const int4* src = reinterpret_cast<const int4*>(dig + p * pstride + static_cast<long long>(J[a]) * ld);
+  int4* dst = reinterpret_cast<int4*>(out + p * opstride + static_cast<long long>(a) * ld);
+  for (long long e = threadIdx.x; e < ld / 16; e += blockDim.x) dst[e] = src[e];
+  if (p == 0 && threadIdx.x == 0) gJ[a] = g[J[a]];
+}
+
 }  // namespace
+
+void launch_gather_digit_cols(const int8_t* dig, long long ld, long long pstride, int k, const int* J, int m,
+                              int8_t* out, long long opstride, const int32_t* g, int32_t* gJ, cudaStream_t s) {
+  k_gather_digit_cols<<<dim3(m, k), 256, 0, s>>>(dig, ld, pstride, J, out, opstride, g, gJ);
+}
 
 size_t cluster_jacobi_smem(int mmax) {
   const int m = std::min(mmax, kCoopMin);
@@ -488,13 +510,14 @@ int cluster_dot_splits(int ntiles, int rows) {
 }
 
 cudaError_t launch_cluster_build(const ClusterLaunch& L, cudaStream_t s) {
-  if (L.ntiles > 0) {
-    k_cluster_dot<<<dim3(L.ntiles, L.nsplit), TB * TB, 0, s>>>(L.tiles, L.goff, L.mem, L.xdig, L.ldd, L.pstride, L.kx,
-                                                               L.rows, L.nsplit, L.part);
+  if (L.ntiles_dot > 0)
+    k_cluster_dot<<<dim3(L.ntiles_dot, L.nsplit), TB * TB, 0, s>>>(L.tiles, L.goff, L.mem, L.xdig, L.ldd, L.pstride,
+                                                                   L.kx, L.rows, L.nsplit, L.part);
+  if (L.ntiles > 0)
     k_cluster_build<<<L.ntiles, TB * TB, 0, s>>>(L.tiles, L.goff, L.gsq, L.mem, L.mu, L.nsplit, L.part, L.rows,
                                                  L.gexp, L.r_hi, L.r_lo, L.wplanes, L.wpstride, *L.rpW, L.ellR,
-                                                 L.scale8, L.lam, L.Mbuf, L.Rbuf, L.col0, L.ncols);
-  }
+                                                 L.scale8, L.lam, L.Mbuf, L.Rbuf, L.col0, L.ncols, L.ntiles_dot,
+                                                 L.Gbuf);
   dim3 gg(L.nmembers, (L.rows + 255) / 256 < 64 ? (L.rows + 255) / 256 : 64);
   k_cluster_gather<<<gg, 256, 0, s>>>(L.mem, L.nmembers, L.Ep, L.lde, L.rows, L.T, L.col0, L.ncols);
   return cudaGetLastError();

@@ -99,6 +99,9 @@ struct ClusterLaunch {
   const int* hgm;          // host copy of gm (which groups take the cooperative whole-GPU Jacobi)
   double* coop_scratch;    // >= 5·mmax + 8 doubles
   int* coop_flags;         // >= 128 ints
+  int ntiles_dot;          // the first ntiles_dot tiles (small groups) sum their Gram block from the digits
+                           // (k_cluster_dot); the rest read it from Gbuf (tensor-core Gram, ozr_api.cu)
+  const double* Gbuf;      // G_JJ = X̂_JᵀX̂_J rounded to fp64, at offset gsq[g] for those groups
   int dense_min;           // groups of at least this many columns take the dense solver (dense_eig.cu)
   int* err;                // error flags (ERR_SOLVER when the dense solver reports failure)
 };
@@ -122,6 +125,9 @@ int cluster_dot_splits(int ntiles, int rows);
 // solve: Jacobi of every group (replicated on every rank); apply: Ẽ'[:, J] and column statistics of the
 // owned columns.
 cudaError_t launch_cluster_build(const ClusterLaunch& L, cudaStream_t s);
+// digit columns J of the k planes of `dig` (ld bytes per column) → contiguous columns of `out`; g[J] → gJ
+void launch_gather_digit_cols(const int8_t* dig, long long ld, long long pstride, int k, const int* J, int m,
+                              int8_t* out, long long opstride, const int32_t* g, int32_t* gJ, cudaStream_t s);
 cudaError_t launch_cluster_solve(const ClusterLaunch& L, cudaStream_t s);
 cudaError_t launch_cluster_apply(const ClusterLaunch& L, cudaStream_t s);
 void launch_final(const int32_t* planes, long long pstride, int rows, int cols, const RecombPlan& rp,

@@ -162,7 +162,7 @@ namespace {
 enum Slot {
   S_ADIG, S_AELL, S_W, S_X1, S_XDIG, S_XDIGT, S_G, S_SH, S_SL, S_RH, S_RL, S_PLANES, S_VH, S_VL, S_LAM, S_ER,
   S_ERR, S_EMAX, S_RDIG, S_RELL, S_EP, S_NRM2, S_NU2, S_WNEXT, S_ZEROELL, S_TMP1, S_TMP2, S_BELL, S_AT, S_ONES,
-  S_EDGES, S_ECOUNT, S_CINT, S_CDBL, S_CM, S_CR, S_CK, S_CV, S_CZ, S_CT, S_CSCR, S_CFLAG, S_SCAL, S_UFALL, S_CPART, S_GCNT, S_WA, S_GPLANES, S_RMAT, S_NR2, S_NW2, S_DWORK, S_DINFO, S_PI_V, S_PI_Z, S_PI_Y, S_PI_P, S_PI_S
+  S_EDGES, S_ECOUNT, S_CINT, S_CDBL, S_CM, S_CR, S_CK, S_CV, S_CZ, S_CT, S_CSCR, S_CFLAG, S_SCAL, S_UFALL, S_CPART, S_GCNT, S_WA, S_GPLANES, S_RMAT, S_NR2, S_NW2, S_DWORK, S_DINFO, S_PI_V, S_PI_Z, S_PI_Y, S_PI_P, S_PI_S, S_CXG, S_CGJ, S_CGP
 };
 
 ozr_status fail(ozr_ctx c, ozr_status st, const char* fmt, ...) {
@@ -1042,7 +1042,11 @@ ozr_status sweep(ozr_ctx ctx, Exchange* ex, const double* A, int64_t n, int64_t 
       int mmax = 0;
       std::vector<int> gm(ng), gsq(ng + 1, 0), grp_of(n, -1), pos_of(n, 0);
       std::vector<double> mu(ng);
-      std::vector<int4> tiles;
+      std::vector<int4> tiles, tiles_tc;
+      // groups from this size on get their Gram block G_JJ = X̂_JᵀX̂_J from the INT8 slice GEMM (all digit
+      // pairs: the same exact integers as k_cluster_dot's int64 sums, rounded once) — OZR_TC_GRAM=0 disables
+      const bool tc_on = !(getenv("OZR_TC_GRAM") && getenv("OZR_TC_GRAM")[0] == '0');
+      const int tc_min = tc_on ? std::max(2, P.dense_cluster) : (1 << 30);
       for (int q = 0; q < ng; ++q) {
         const int m = off[q + 1] - off[q];
         gm[q] = m;
@@ -1056,9 +1060,12 @@ ozr_status sweep(ozr_ctx ctx, Exchange* ex, const double* A, int64_t n, int64_t 
           pos_of[j] = a;
         }
         mu[q] = sm / m;
+        std::vector<int4>& tl = (m >= tc_min) ? tiles_tc : tiles;
         for (int a0 = 0; a0 < m; a0 += 16)
-          for (int b0 = 0; b0 < m; b0 += 16) tiles.push_back(make_int4(q, a0, b0, m));
+          for (int b0 = 0; b0 < m; b0 += 16) tl.push_back(make_int4(q, a0, b0, m));
       }
+      const int ntiles_dot = static_cast<int>(tiles.size());  // small groups first: k_cluster_dot covers them
+      tiles.insert(tiles.end(), tiles_tc.begin(), tiles_tc.end());
       if (mmax > P.max_cluster)
         return fail(ctx, OZR_ERR_RANGE, "unresolved group of %d columns exceeds max_cluster = %d", mmax, P.max_cluster);
       const int nmem = off[ng];
@@ -1091,6 +1098,8 @@ ozr_status sweep(ozr_ctx ctx, Exchange* ex, const double* A, int64_t n, int64_t 
       L.nmembers = nmem;
       L.mmax = mmax;
       L.ntiles = static_cast<int>(tiles.size());
+      L.ntiles_dot = ntiles_dot;
+      L.Gbuf = cK;  // K is only written by the solve, after the build has read G
       L.rows = N;
       L.col0 = static_cast<int>(col0);
       L.ncols = NL;
@@ -1122,8 +1131,8 @@ ozr_status sweep(ozr_ctx ctx, Exchange* ex, const double* A, int64_t n, int64_t 
       L.nrm2 = nrm2;
       L.eE_col = eR;
       L.eE_max = demax;
-      L.nsplit = cluster_dot_splits(L.ntiles, N);
-      L.part = ctx->ws<unsigned long long>(S_CPART, static_cast<size_t>(L.ntiles) * L.nsplit * 512);
+      L.nsplit = cluster_dot_splits(std::max(1, L.ntiles_dot), N);
+      L.part = ctx->ws<unsigned long long>(S_CPART, static_cast<size_t>(std::max(1, L.ntiles_dot)) * L.nsplit * 512);
       OZR_ALLOC(L.part);
       L.hgm = gm.data();
       L.coop_scratch = ctx->ws<double>(S_CSCR, 5 * static_cast<size_t>(mmax) + 8);
@@ -1143,6 +1152,30 @@ ozr_status sweep(ozr_ctx ctx, Exchange* ex, const double* A, int64_t n, int64_t 
       }
       // (1) M_JJ columns owned by this rank, (2) all-reduce → full M on every rank, (3) Jacobi (replicated),
       // (4) T = Ẽ'[:, J] owned columns, all-reduce, (5) apply + column statistics on owned columns
+      // tensor-core Gram of the large groups: gather their digit columns, all-pairs slice GEMM, exact
+      // recombination rounded once to fp64 (scaled by 2^{g_a + g_b}), into G = cK at the group's offset
+      for (int q = 0; q < ng; ++q) {
+        if (gm[q] < tc_min) continue;
+        const int m = gm[q];
+        int8_t* xg = ctx->ws<int8_t>(S_CXG, static_cast<size_t>(kx) * ld * m);
+        int32_t* gJ = ctx->ws<int32_t>(S_CGJ, m);
+        OZR_ALLOC(xg); OZR_ALLOC(gJ);
+        launch_gather_digit_cols(xdig, ld, ld * n, kx, dpk + o_mem + off[q], m, xg, ld * m, g, gJ, s);
+        const int LG = 2 * kx;
+        std::vector<Group> gG = plan_groups(kx, kx, LG, n);
+        PairTable ptG;
+        RecombPlan rpG;
+        if (!make_tables(gG, LG, n, ptG, rpG)) return fail(ctx, OZR_ERR_RANGE, "Gram plan too large");
+        const size_t mm = static_cast<size_t>(m) * m;
+        int32_t* gplanes = ctx->ws<int32_t>(S_CGP, gG.size() * mm);
+        int* cnt = ctx->ws<int>(S_GCNT, 4);
+        OZR_ALLOC(gplanes); OZR_ALLOC(cnt);
+        const DigitOperand opG{xg, ld, ld * m, kx};
+        OZR_CK(launch_gemm_i8(opG, opG, m, m, N, ptG, gplanes, static_cast<int64_t>(mm), m, s, cnt), "Gram GEMM");
+        launch_recombine_dd(gplanes, static_cast<long long>(mm), m, m, rpG, gJ, gJ, 0, cK + gsq[q], nullptr, m, s);
+        OZR_CK(cudaGetLastError(), "Gram recombination");
+        cluster_launches += 3;
+      }
       OZR_CK(launch_cluster_build(L, s), "cluster build");
       OZR_X(xsum(cM, sq));
       OZR_CK(launch_cluster_solve(L, s), "cluster solve");

@@ -160,3 +160,22 @@ def test_c4_recipe_default_dense_path(ctx):
     X, lam = to_np(Xd), to_np(ld)
     assert np.max(np.linalg.norm(A @ X - X * lam[None, :], axis=0)) <= 1e-12, trail
     assert np.max(np.abs(X.T @ X - np.eye(2048))) <= 1e-12
+
+
+@pytest.mark.parametrize("cfg,n,start,dense", [("c2", 512, "fp32", 192), ("c4", 1024, "fp32", 64), ("c3", 512, "fp32", 2)])
+def test_tensor_core_gram_bit_identical(ctx, cfg, n, start, dense, monkeypatch):
+    """The Gram blocks G_JJ = X̂_JᵀX̂_J of the groups that take the dense sub-solve come from the INT8 slice
+    GEMM with every digit pair (the same exact integers as the int64 column sums of k_cluster_dot, rounded
+    once): the sweep is bit-identical with and without it (OZR_TC_GRAM=0)."""
+    import paper_2602_19090_b200 as ozr
+    A, lam0, X0 = _case(cfg, n, start)
+    p = ozr.default_params(delta=1e-12, dense_cluster=dense)
+    out = []
+    for flag in ("1", "0"):
+        monkeypatch.setenv("OZR_TC_GRAM", flag)
+        Xd, ld = to_dev(X0), vec_dev(lam0)
+        rep = ozr.ozr_refine_step(ctx, to_dev(A), Xd, ld, p)
+        out.append((to_np(Xd), to_np(ld), rep))
+    assert out[0][2]["max_cluster"] >= dense
+    assert np.array_equal(out[0][0], out[1][0]) and np.array_equal(out[0][1], out[1][1])
+    assert out[0][2]["launches"] > out[1][2]["launches"]
