@@ -372,6 +372,27 @@ int tile_budgets(int kA, int kB, int64_t K, int eA, const std::vector<int>& eB_c
   const int64_t nt = (n + kTileN - 1) / kTileN;
   int Lmax = 2;
   double pw = 0.0;
+  // choose_L's tail sums with eA + eB factored out: every term carries the same power of two, so
+  // ldexp(base[L], eA + eB) is bit-for-bit the sum choose_L forms (exact scaling), once per product instead of
+  // once per tile
+  std::vector<double> base(kA + kB + 1, 0.0);
+  for (int L = 2; L < kA + kB; ++L) {
+    double tail = 0.0;
+    for (int d = L + 1; d <= kA + kB; ++d) {
+      int np = 0;
+      for (int s = 1; s <= kA; ++s)
+        if (d - s >= 1 && d - s <= kB) ++np;
+      tail += np * 2.0 * std::sqrt(static_cast<double>(K)) * std::ldexp(1.0, 14 + 4 - 8 * d);
+    }
+    base[L] = tail;
+  }
+  std::vector<int> pairs_of(kA + kB + 1, 0);
+  for (int L = 2; L <= kA + kB; ++L) pairs_of[L] = pairs_upto(kA, kB, L);
+  auto choose = [&](int eB, double tau) {
+    for (int L = 2; L < kA + kB; ++L)
+      if (std::ldexp(base[L], eA + eB) <= tau) return L;
+    return kA + kB;
+  };
   for (int64_t t = 0; t < nt; ++t) {
     double tau = INFINITY;
     int eB = -100000;
@@ -380,11 +401,11 @@ int tile_budgets(int kA, int kB, int64_t K, int eA, const std::vector<int>& eB_c
       tau = std::min(tau, tau_col[j]);
       eB = std::max(eB, eB_col[j]);
     }
-    int L = (eB == -100000) ? 2 : choose_L(kA, kB, K, eA, eB, tau);
+    int L = (eB == -100000) ? 2 : choose(eB, tau);
     L = std::max(2, std::min(L, kA + kB));
     tileL[t] = static_cast<unsigned char>(L);
     Lmax = std::max(Lmax, L);
-    pw += static_cast<double>(pairs_upto(kA, kB, L)) * static_cast<double>(j1 - t * kTileN);
+    pw += static_cast<double>(pairs_of[L]) * static_cast<double>(j1 - t * kTileN);
   }
   *avg_pairs = pw / static_cast<double>(n);
   return Lmax;
