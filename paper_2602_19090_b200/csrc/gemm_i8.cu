@@ -31,7 +31,7 @@ constexpr int A_STAGE_BYTES = BM * BK;
 constexpr int B_STAGE_BYTES = BN * BK;
 constexpr int SMEM_BYTES = STAGES * (A_STAGE_BYTES + B_STAGE_BYTES) + 1024 /*align*/ + 256 /*barriers*/;
 constexpr int TMEM_COLS = 256;
-constexpr int BAND = 4;  // n-tiles per rasterisation band
+constexpr int BAND = 3;  // n-tiles per rasterisation band (3 vs 4: same time, −8 % DRAM reads on V, −18 % on W)
 
 // Persistent form: one CTA per SM; its first job is blockIdx.x, the next ones come from a global atomic
 // counter, so the jobs in flight at any moment stay neighbours in the rasterised order (as with the
