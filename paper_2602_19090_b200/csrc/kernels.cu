@@ -212,9 +212,11 @@ __device__ __forceinline__ void for_column(const int32_t* __restrict__ planes, l
 constexpr int RPT = 2;         // rows per thread per stage (two independent element chains per thread)
 constexpr int TR = RPT * BS;   // rows per stage
 constexpr int TS = 2;          // stages
-constexpr int kStageBytes = kFastGroups * TR * 4 + 2 * TR * 8 + TR * 4;  // planes | 2 fp64 sides | 1 int32 side
-constexpr int kSideI = kFastGroups * TR * 4 + 2 * TR * 8;
-constexpr int kTmaSmem = TS * kStageBytes + TS * 8;
+// stage layout for NG compiled groups: planes | 2 fp64 sides | 1 int32 side (smaller plans, smaller
+// stages: more CTAs per SM)
+__host__ __device__ constexpr int stage_bytes(int ng) { return ng * TR * 4 + 2 * TR * 8 + TR * 4; }
+__host__ __device__ constexpr int side_i(int ng) { return ng * TR * 4 + 2 * TR * 8; }
+__host__ __device__ constexpr int tma_smem(int ng) { return TS * stage_bytes(ng) + TS * 8; }
 
 // icol (nullable): an int32 per-row vector staged beside the planes (the row exponents); e(i, icol[i]).
 template <int NX, bool HI_ONLY = false, int NG = kFastGroups, class EF, class F>
@@ -232,6 +234,7 @@ __device__ __forceinline__ void for_column_x(const int32_t* __restrict__ planes,
                });
     return;
   }
+  constexpr int kStageBytes = stage_bytes(NG), kSideI = side_i(NG);
   uint64_t* bar = reinterpret_cast<uint64_t*>(tsm + TS * kStageBytes);
   const int tid = threadIdx.x;
   const int d0 = rp.diag[0];
@@ -250,7 +253,7 @@ __device__ __forceinline__ void for_column_x(const int32_t* __restrict__ planes,
     const uint32_t pb = static_cast<uint32_t>(nr) * 4u, xb = static_cast<uint32_t>(nr) * 8u;
     mbar_arrive_expect_tx(&bar[st], nact * pb + NX * xb + (icol ? pb : 0u));
     for (int g = 0; g < nact; ++g) bulk_g2s(base + g * TR * 4, planes + g * pstride + coloff + r0, pb, &bar[st]);
-    for (int x = 0; x < NX; ++x) bulk_g2s(base + kFastGroups * TR * 4 + x * TR * 8, xcol[x] + r0, xb, &bar[st]);
+    for (int x = 0; x < NX; ++x) bulk_g2s(base + NG * TR * 4 + x * TR * 8, xcol[x] + r0, xb, &bar[st]);
     if (icol) bulk_g2s(base + kSideI, icol + r0, pb, &bar[st]);
   };
   if (tid == 0)
@@ -291,7 +294,7 @@ __device__ __forceinline__ void for_column_x(const int32_t* __restrict__ planes,
       }
       double xv[NX > 0 ? NX : 1];
 #pragma unroll
-      for (int x = 0; x < NX; ++x) xv[x] = reinterpret_cast<const double*>(base + kFastGroups * TR * 4 + x * TR * 8)[tl];
+      for (int x = 0; x < NX; ++x) xv[x] = reinterpret_cast<const double*>(base + NG * TR * 4 + x * TR * 8)[tl];
       f(i, v, xv);
     }
     }
@@ -709,7 +712,7 @@ __global__ void __launch_bounds__(BS, 3)
 }
 
 template <int NG>
-__global__ void __launch_bounds__(BS, 3)
+__global__ void __launch_bounds__(BS, NG <= 8 ? 4 : 3)
     k_recombine_E(const int32_t* __restrict__ planes, long long pstride, int rows, const __grid_constant__ RecombPlan rp,
                   const int32_t* __restrict__ ellA, const int32_t* __restrict__ ellB, int scale8,
                   const double* __restrict__ r_hi, const double* __restrict__ lam, const int32_t* __restrict__ gX,
@@ -790,7 +793,7 @@ __global__ void __launch_bounds__(BS)
 }
 
 template <int NG>
-__global__ void __launch_bounds__(BS, 3)
+__global__ void __launch_bounds__(BS, NG <= 8 ? 4 : 3)
     k_final(const int32_t* __restrict__ planes, long long pstride, int rows, const __grid_constant__ RecombPlan rp,
             const int32_t* __restrict__ ellB, int scale8, const double* __restrict__ X1, long long ldx1,
             double* __restrict__ X, long long ldx, double* __restrict__ nu2, double* __restrict__ wnext, int use_tma,
@@ -928,15 +931,15 @@ void init_attrs() {
     OZR_CARVE(k_recombine_E<4>); OZR_CARVE(k_recombine_E<8>); OZR_CARVE(k_recombine_E<12>);
     OZR_CARVE(k_final<4>); OZR_CARVE(k_final<8>); OZR_CARVE(k_final<12>);
 #undef OZR_CARVE
-    cudaFuncSetAttribute(k_recombine_V<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem);
-    cudaFuncSetAttribute(k_recombine_V<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem);
-    cudaFuncSetAttribute(k_recombine_V<12>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem);
-    cudaFuncSetAttribute(k_recombine_E<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem);
-    cudaFuncSetAttribute(k_recombine_E<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem);
-    cudaFuncSetAttribute(k_recombine_E<12>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem);
-    cudaFuncSetAttribute(k_final<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem);
-    cudaFuncSetAttribute(k_final<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem);
-    cudaFuncSetAttribute(k_final<12>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem);
+    cudaFuncSetAttribute(k_recombine_V<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, tma_smem(4));
+    cudaFuncSetAttribute(k_recombine_V<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, tma_smem(8));
+    cudaFuncSetAttribute(k_recombine_V<12>, cudaFuncAttributeMaxDynamicSharedMemorySize, tma_smem(12));
+    cudaFuncSetAttribute(k_recombine_E<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, tma_smem(4));
+    cudaFuncSetAttribute(k_recombine_E<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, tma_smem(8));
+    cudaFuncSetAttribute(k_recombine_E<12>, cudaFuncAttributeMaxDynamicSharedMemorySize, tma_smem(12));
+    cudaFuncSetAttribute(k_final<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, tma_smem(4));
+    cudaFuncSetAttribute(k_final<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, tma_smem(8));
+    cudaFuncSetAttribute(k_final<12>, cudaFuncAttributeMaxDynamicSharedMemorySize, tma_smem(12));
     attr = true;
   }
 }
@@ -977,7 +980,7 @@ void launch_recombine_V(const int32_t* planes, long long pstride, int rows, int 
   init_attrs();
   const int tma = allow_tma && tma_ok(rp, planes, pstride, rows, X1, ldx1, X1, ldx1) && (reinterpret_cast<uintptr_t>(ellA) & 15) == 0;
 #define OZR_RV(NG_)                                                                                          \
-  k_recombine_V<NG_><<<cols, BS, tma ? kTmaSmem : 0, s>>>(planes, pstride, rows, rp, ellA, ellB, scale8, X1, ldx1, s_hi, \
+  k_recombine_V<NG_><<<cols, BS, tma ? tma_smem(NG_) : 0, s>>>(planes, pstride, rows, rp, ellA, ellB, scale8, X1, ldx1, s_hi, \
                                                           s_lo, Vh, Vl, ldv, lam_out, eR, eR_max, tma)
   if (tma && rp.ngroups <= 4) OZR_RV(4);
   else if (tma && rp.ngroups <= 8) OZR_RV(8);
@@ -991,7 +994,7 @@ void launch_recombine_E(const int32_t* planes, long long pstride, int rows, int 
   init_attrs();
   const int tma = allow_tma && tma_ok(rp, planes, pstride, rows, lam, 0, nullptr, 0) && (reinterpret_cast<uintptr_t>(ellA) & 15) == 0;
 #define OZR_RE(NG_)                                                                                            \
-  k_recombine_E<NG_><<<cols, BS, tma ? kTmaSmem : 0, s>>>(planes, pstride, rows, rp, ellA, ellB, scale8, r_hi, lam, gX, \
+  k_recombine_E<NG_><<<cols, BS, tma ? tma_smem(NG_) : 0, s>>>(planes, pstride, rows, rp, ellA, ellB, scale8, r_hi, lam, gX, \
                                                           col0, Ep, lde, nrm2, eE_max, eE_col, err, eo, tma, nW2)
   if (tma && rp.ngroups <= 4) OZR_RE(4);
   else if (tma && rp.ngroups <= 8) OZR_RE(8);
@@ -1004,7 +1007,7 @@ void launch_final(const int32_t* planes, long long pstride, int rows, int cols, 
   init_attrs();
   const int tma = allow_tma && tma_ok(rp, planes, pstride, rows, X1, ldx1, X, ldx);
 #define OZR_FI(NG_)                                                                                                 \
-  k_final<NG_><<<cols, BS, tma ? kTmaSmem : 0, s>>>(planes, pstride, rows, rp, ellB, scale8, X1, ldx1, X, ldx, nu2, wnext, \
+  k_final<NG_><<<cols, BS, tma ? tma_smem(NG_) : 0, s>>>(planes, pstride, rows, rp, ellB, scale8, X1, ldx1, X, ldx, nu2, wnext, \
                                                     tma, D)
   if (tma && rp.ngroups <= 4) OZR_FI(4);
   else if (tma && rp.ngroups <= 8) OZR_FI(8);
