@@ -246,6 +246,11 @@ __device__ __forceinline__ void for_column_x(const int32_t* __restrict__ planes,
     for (int st = 0; st < TS; ++st) mbar_init(&bar[st], 1);
     fence_mbar_init();
   }
+  // the group slots the plan leaves empty (nact < NG) are never filled by the copies: zero them once, so
+  // the element loop reads all NG slots without a per-element guard
+  for (int st = 0; st < TS; ++st)
+    for (int g = nact; g < NG; ++g)
+      for (int r = tid; r < TR; r += BS) reinterpret_cast<int32_t*>(tsm + st * kStageBytes + g * TR * 4)[r] = 0;
   __syncthreads();
   auto issue = [&](int c) {
     const int st = c % TS, r0 = c * TR, nr = min(TR, rows - r0);
@@ -270,7 +275,7 @@ __device__ __forceinline__ void for_column_x(const int32_t* __restrict__ planes,
       // NG: groups compiled for this launch (4, 8 or 12 ≥ ngroups), so small plans do no dead work
       int32_t cv[NG];
 #pragma unroll
-      for (int g = 0; g < NG; ++g) cv[g] = (g < nact) ? reinterpret_cast<const int32_t*>(base + g * TR * 4)[tl] : 0;
+      for (int g = 0; g < NG; ++g) cv[g] = reinterpret_cast<const int32_t*>(base + g * TR * 4)[tl];
       long long Lm[NG / 4];
 #pragma unroll
       for (int k = 0; k < NG / 4; ++k)
