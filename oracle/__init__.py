@@ -19,6 +19,6 @@ Modules
             eigenvectors and forward error
   _clib     ctypes loader for ddmm.c (double-double GEMM, __float128 Jacobi)
 
-Parity status: every function is pinned by a ``-m "not gpu"`` test in tests/test_oracle_*.py except
-those whose docstring says "parity unpinned" (listed in DESIGN.md).
+Parity status: every function is pinned by a ``-m "not gpu"`` test in tests/test_oracle_*.py (closed forms,
+exact rationals, exactly known eigensystems, __float128 Jacobi); none is "parity unpinned".
 """

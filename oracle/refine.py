@@ -94,7 +94,9 @@ def unresolved_groups(E, lam, kappa=KAPPA_DEFAULT):
 
 def cluster_subsolve(E, lam, J, X1, Wh, Wl, rh, rl):
     """Rayleigh–Ritz in span(X̂^(1)_J) for one unresolved group J (reading R13; the construction follows
-    the cited Ogita–Aishima cluster refinement, restated here — parity unpinned).
+    the cited Ogita–Aishima cluster refinement, restated here). Pinned by
+    tests/test_oracle_pins.py: exact double / dyadic near-double eigenvalues of the Householder family (the
+    eigenspace, the undone 30° and 69° rotations) and, through refine_to_tol, __float128 Jacobi.
     With G = X̂ᵀX̂ = I − R and S = X̂ᵀAX̂ = W + (I − R)D̂ (Alg. 1 line 4):
       μ = mean λ̂_J,  M = S_JJ − μ G_JJ = W_JJ + (I − R_JJ)(D̂_J − μI),  K₀ = (M + Mᵀ)/2,
       C = I + R_JJ/2  (= G_JJ^{-1/2} to first order),  K = C K₀ C = Y Θ Yᵀ  (Θ ascending),
@@ -140,7 +142,7 @@ def sweep(A, X, lam_prev, delta, theta=THETA_DEFAULT, beta=None, beta_mode="dens
 
     cluster_mode 0: the paper's Algorithm 1 (distinct eigenvalues assumed); equal
     λ̂ raise. cluster_mode 1: unresolved groups get a Rayleigh–Ritz sub-solve (cluster_subsolve,
-    DESIGN.md reading R13; not in the paper — parity unpinned beyond the tests listed there).
+    DESIGN.md reading R13; not in the paper — pinned against exact eigensystems, tests/test_oracle_pins.py).
     groups: use these unresolved groups instead of finding them (parity runs: a pair whose |ẽ_ij| sits
     at κ may be classified differently by the GPU's digit-budget W; the tests check that is the only
     difference, then evaluate the same groups)."""

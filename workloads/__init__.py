@@ -189,3 +189,20 @@ def pivot_2x2(theta):
     c, s = np.cos(theta), np.sin(theta)
     X = np.array([[c, -s], [s, c]])
     return A, X
+
+
+def householder_pair(m=6, pair=(10, 11), split=0.0, angle=0.0, noise=1e-9, lam_bits=12, seed=3):
+    """Householder-exact family with a designed pair: λ_b = λ_a + `split` (split = 0: an exactly
+    double eigenvalue; a dyadic split keeps A exact), A = X diag(λ) Xᵀ with the exact eigenvectors X
+    (columns of H). The start X̂₀ rotates the pair's two exact eigenvectors by `angle` (radians) and adds
+    seeded N(0, noise²) entries. Returns (A, λ, X exact, X̂₀)."""
+    A0, lam, X, H, lam_cols = householder_exact(m, lam_bits=lam_bits, seed=seed)
+    a, b = pair
+    lam = lam.copy()
+    lam[b] = lam[a] + split
+    A = (X * lam[None, :]) @ X.T
+    X0 = X.copy()
+    c, s = np.cos(angle), np.sin(angle)
+    X0[:, a], X0[:, b] = c * X[:, a] - s * X[:, b], s * X[:, a] + c * X[:, b]
+    X0 = X0 + noise * np.random.default_rng(seed + 4).standard_normal(X.shape)
+    return A, lam, X, X0
