@@ -135,9 +135,13 @@ typedef struct {
                         Default 192 (smaller groups: one Jacobi CTA each, all groups in one launch) */
   int row_nnz;       /* k = maximum number of nonzeros in a row of A (beta_mode 2; also the contraction
                         length of the V-product's dropped-pair bound, R8). 0 → n (dense)            */
-  int max_escalations; /* ozr_refine_to_tol: when the net update stagnates above δ (the truncated iteration's
-                          noise floor, R12), continue with θ × 16 (β two bits lower) at most this many
-                          times before OZR_ERR_NOT_CONVERGED. Default 2 */
+  int max_escalations; /* ozr_refine_to_tol: when the certified error stalls above δ at the truncated iteration's
+                          floor (R12), continue with θ × 4^m (β m bits lower, m from the estimate) at most
+                          this many times before OZR_ERR_NOT_CONVERGED. Default 2 */
+  int certify;       /* the a-posteriori forward-error certificate (R12, report.cert): 0 never — ozr_refine_to_tol
+                        then runs max_sweeps sweeps (the paper's fixed iteration count) and
+                        returns OZR_ERR_NOT_CONVERGED with X, λ from the last sweep; 1 after every sweep of
+                        ozr_refine_to_tol without unresolved groups [default]; 2 also in ozr_refine_step  */
 } ozr_params;
 
 void ozr_params_default(ozr_params* p);
@@ -163,8 +167,13 @@ typedef struct {
   double omega_oa;                  /* form_R: ω = 2(‖W‖_F + 2·max|λ̂|·‖R‖_F), the Frobenius form of the
                                        OA-2018 cluster threshold 2(‖S − D̃‖ + ‖A‖‖R‖) (diagnostic, R13) */
   double theta;                     /* the θ this sweep used (params.theta, × 16 per escalation)       */
-  double update_2norm;              /* ozr_refine_to_tol at a stagnating ν: power-iteration estimate of
-                                       ‖X̂_k − X̂_{k−1}‖₂ (0 when not evaluated; R12)                     */
+  double cert;                      /* a-posteriori estimate of ‖X − X̂_new‖₂ (R12): sqrt(‖Q∘H‖₂² + (2u)²)
+                                       + 1.5‖Ẽ‖_F², Q = ẼᵀC, c_kj = (λ̂_k − λ̂_j)ẽ_kj, H_ij = 1/(λ̂_j − λ̂_i);
+                                       −1 when not evaluated (params.certify, or unresolved groups)      */
+  double cert_q;                    /* its second-order part ‖Q∘H‖₂ (power iteration; the Frobenius norm
+                                       when that already decides)                                        */
+  double cert_frob;                 /* ‖Q∘H‖_F                                                          */
+  int cert_iters;                   /* power iterations of the certificate                              */
 } ozr_step_report;
 
 /* One sweep on columns [0, n): A (n x n, symmetric — only its columns are read), X (n x n, in/out:
@@ -184,13 +193,15 @@ ozr_status ozr_last_R(ozr_ctx ctx, double* R, int64_t ldr);
  * (*ngroups / offsets still tell the sizes needed when offsets has room). */
 ozr_status ozr_last_clusters(ozr_ctx ctx, int* members, int max_members, int* offsets, int max_groups, int* ngroups);
 
-/* Repeat sweeps until the stop rule (R12), with ν_k = ‖X̂_k − X̂_{k−1}‖_F: after sweep k stop
- * when ν_k ≤ δ, or ν_k² max|λ̂| / (n gap) ≤ δ, or — once ν_k ≤ √n·δ — when a power-iteration estimate of
- * ‖X̂_k − X̂_{k−1}‖₂ (the paper's measure, reported as update_2norm) is ≤ δ. Sweeps with unresolved groups
- * (cluster sub-solves rotate columns) are not compared for stagnation; otherwise stagnation
- * (ν_k > ν_{k−1}/2) first escalates θ ← 16θ up to max_escalations times, then reports
- * OZR_ERR_NOT_CONVERGED, as does reaching max_sweeps — X / lambda then hold the last completed sweep.
- * history (host, nullable) receives up to max_hist reports; sweeps_done (host, nullable). */
+/* Repeat sweeps until the returned X̂ is certified (R12; the paper iterates a fixed number of times,
+ * PAPER.md:536-540): after every sweep without unresolved groups, the a-posteriori estimate report.cert of
+ * ‖X − X̂‖₂ (the 2-norm of PAPER.md:121) is formed from the sweep's own Ẽ — the second-order defect of Alg. 1's
+ * correction, one bf16 tensor-core product Q = ẼᵀC and a power iteration — and the call returns OZR_OK with
+ * that X̂ once cert·1.15 ≤ δ. An estimate that stalls above δ (the truncated iteration's floor, quadratic in
+ * 2^-β) escalates θ ← θ·4^m up to max_escalations times, then OZR_ERR_NOT_CONVERGED, as does
+ * reaching max_sweeps — X / lambda then hold the last completed sweep. Sweeps with unresolved groups (cluster
+ * sub-solves rotate columns) are neither certified nor compared. history (host, nullable) receives up to
+ * max_hist reports; sweeps_done (host, nullable). */
 ozr_status ozr_refine_to_tol(ozr_ctx ctx, const double* A, int64_t n, int64_t lda, double* X, int64_t ldx,
                              double* lambda, const ozr_params* params, ozr_step_report* history, int max_hist,
                              int* sweeps_done);

@@ -37,7 +37,7 @@ class Params(ctypes.Structure):
                 ("L_W", ctypes.c_int), ("L_U", ctypes.c_int), ("cluster_mode", ctypes.c_int),
                 ("tile_budgets", ctypes.c_int), ("kappa", ctypes.c_double), ("max_cluster", ctypes.c_int),
                 ("form_R", ctypes.c_int), ("dense_cluster", ctypes.c_int),
-                ("row_nnz", ctypes.c_int), ("max_escalations", ctypes.c_int)]
+                ("row_nnz", ctypes.c_int), ("max_escalations", ctypes.c_int), ("certify", ctypes.c_int)]
 
 
 class StepReport(ctypes.Structure):
@@ -47,7 +47,8 @@ class StepReport(ctypes.Structure):
                 [(f, ctypes.c_double) for f in ["gap_min", "max_abs_lambda", "normE_fro", "net_update",
                                                  "predicted_error", "ms_total", "ms_gemm", "int8_ops"]] +
                 [("pairs_G", ctypes.c_int)] +
-                [(f, ctypes.c_double) for f in ["normR_fro", "normW_fro", "omega_oa", "theta", "update_2norm"]])
+                [(f, ctypes.c_double) for f in ["normR_fro", "normW_fro", "omega_oa", "theta", "cert", "cert_q", "cert_frob"]] +
+                [("cert_iters", ctypes.c_int)])
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}

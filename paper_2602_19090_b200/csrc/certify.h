@@ -1,0 +1,22 @@
+// certify.h — launchers of the a-posteriori forward-error certificate (certify.cu, R12). Internal.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace ozr {
+
+// Ẽ = diag(2^−g)·Ẽ' from the stored Ẽ' (rows x cols, local columns [col0, col0 + cols)); per column j:
+// sE[col0 + j] = ⌈log2 max_i |ẽ_ij|⌉, sC[j] = ⌈log2 max_i |(λ̂_i − λ̂_j) ẽ_ij|⌉, esq[j] = Σ_i ẽ_ij²;
+// Eb (bf16, column col0 + j at Eb + (col0 + j)·ldb) = ẽ·2^−sE, Cb (bf16, local column j) = (λ̂_i − λ̂_j)ẽ_ij·2^−sC.
+void launch_cert_prep(const double* Ep, long long lde, int rows, int cols, const int32_t* g, const double* lam, int col0,
+                      void* Eb, void* Cb, long long ldb, int32_t* sE, int32_t* sC, double* esq, cudaStream_t s);
+// D_ij = 2^{sE_i + sC_j}·Q_ij/(λ̂_j − λ̂_i) (fp32, rows x cols, ld = rows, D_jj = 0), dsq[j] = Σ_i D_ij²;
+// *flag |= 1 when two estimates are equal (no certificate).
+void launch_cert_delta(const float* Q, long long ldq, int rows, int cols, const int32_t* sE, const int32_t* sC,
+                       const double* lam, int col0, float* D, double* dsq, int* flag, cudaStream_t s);
+// y = D·z (part: cert_pi_chunks()·rows doubles of scratch); v = Dᵀ·y
+void launch_pi_dz(const float* D, int rows, int cols, const double* z, double* part, double* y, cudaStream_t s);
+void launch_pi_dty(const float* D, int rows, int cols, const double* y, double* v, cudaStream_t s);
+int cert_pi_chunks();
+
+}  // namespace ozr

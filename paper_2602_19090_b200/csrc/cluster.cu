@@ -23,6 +23,7 @@
 
 #include "ddmath.cuh"
 #include "kernels.h"
+#include "ozr_internal.h"
 
 #include <algorithm>
 
@@ -528,14 +529,9 @@ cudaError_t launch_cluster_solve(const ClusterLaunch& L, cudaStream_t s) {
   k_cluster_jacobi<<<L.ngroups, JT, sm, s>>>(L.goff, L.gsq, L.gm, L.mem, L.mu, L.Mbuf, L.Rbuf, L.Kbuf, L.Vbuf, L.Zbuf,
                                               L.lam, L.sweeps, L.dense_min);
   // large groups: one cooperative whole-GPU launch each
-  static int coop_grid = 0;
-  if (coop_grid == 0) {
-    int dev = 0, nsm = 0, per = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_cluster_jacobi_coop, JT, 0);
-    coop_grid = nsm * std::max(1, std::min(per, 2));
-  }
+  int per = 0;  // per call: the occupancy is a property of the current device
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_cluster_jacobi_coop, JT, 0);
+  const int coop_grid = sm_count() * std::max(1, std::min(per, 2));
   for (int q = 0; q < L.ngroups; ++q) {
     if (L.hgm[q] < kCoopMin || L.hgm[q] >= L.dense_min) continue;
     cudaError_t e = cudaMemsetAsync(L.coop_flags, 0, 128 * sizeof(int), s);

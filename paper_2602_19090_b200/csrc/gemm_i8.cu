@@ -269,6 +269,10 @@ __device__ __forceinline__ JobInfo job_info2(int job, const PairTable& pt, int N
   return ji;
 }
 
+// KIND 0: int8 digit planes (kind::i8, exact int32); KIND 1: bf16 operands (kind::f16, f32 accumulator: the
+// certificate's Q = ẼᵀC, certify.cu). Both consume 32 bytes of K per MMA from the same 128-byte swizzle rows, so
+// the data movement is byte-for-byte the same; K is given in bytes.
+template <int KIND>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NWARPS * 32, 1)
     k_gemm_i8_2sm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                   const __grid_constant__ PairTable pt, int32_t* __restrict__ out, long long out_plane_stride,
@@ -382,7 +386,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NWARPS * 32, 1)
   } else if (warp == 1) {
     if (lane == 0 && leader) {
       // ---------------- MMA issuer (leader CTA, single thread): M = 256 over the pair
-      constexpr uint32_t idesc = idesc_i8(2 * BM, BN);
+      constexpr uint32_t idesc = KIND == 0 ? idesc_i8(2 * BM, BN) : idesc_bf16(2 * BM, BN);
       int it = 0, t = 0;
       for (int jn = 0;; ++jn) {
         const int slot = jn % JQ;
@@ -410,7 +414,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NWARPS * 32, 1)
             for (int k = 0; k < BK / UMMA_K; ++k) {
               const uint64_t ad = umma_desc_kmajor_sw128(a_addr + h * A_STAGE_BYTES + k * UMMA_K);
               const uint64_t bd = umma_desc_kmajor_sw128(b_addr + h * B_HALF_BYTES + k * UMMA_K);
-              mma_i8_2sm(acc, ad, bd, idesc, (q > 0 || h > 0 || k > 0) ? 1u : 0u);
+              if constexpr (KIND == 0) mma_i8_2sm(acc, ad, bd, idesc, (q > 0 || h > 0 || k > 0) ? 1u : 0u);
+              else mma_bf16_2sm(acc, ad, bd, idesc, (q > 0 || h > 0 || k > 0) ? 1u : 0u);
             }
           mma_commit_2sm(&empty[stage], 0x3);  // frees the stage in both CTAs
         }
@@ -524,7 +529,7 @@ bool make_tmap(CUtensorMap* tm, const DigitOperand& op, int K, int cols, int box
 
 cudaError_t launch_gemm_i8(const DigitOperand& A, const DigitOperand& B, int M, int N, int K,
                            const PairTable& pt, int32_t* out, int64_t out_plane_stride, int64_t ldo,
-                           cudaStream_t stream, int* job_counter, int job_order) {
+                           cudaStream_t stream, int* job_counter, int job_order, int kind) {
   if (M <= 0 || N <= 0 || pt.ngroups <= 0) return cudaSuccess;
   if (K <= 0 || (A.ld % 16) || (B.ld % 16) || (A.plane_stride % 16) || (B.plane_stride % 16))
     return cudaErrorInvalidValue;
@@ -533,34 +538,29 @@ cudaError_t launch_gemm_i8(const DigitOperand& A, const DigitOperand& B, int M, 
     const char* v = getenv("OZR_GEMM");
     use2 = (v && v[0] == '1') ? 0 : 1;  // OZR_GEMM=1sm: the single-CTA form (A/B measurements)
   }
+  if (kind == 1) use2 = 1;  // the bf16 form exists only as the CTA pair
   CUtensorMap tmA, tmB;
   if (!make_tmap(&tmA, A, K, M, BM) || !make_tmap(&tmB, B, K, N, use2 ? BN / 2 : BN)) return cudaErrorInvalidValue;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(k_gemm_i8, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+  if (!use2) {
+    cudaError_t e = once_per_device(0, [] {
+      return cudaFuncSetAttribute(k_gemm_i8, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    });
     if (e != cudaSuccess) return e;
-    attr_set = true;
   }
   const int tiles_m = (M + BM - 1) / BM;
   const int tiles_n = (N + BN - 1) / BN;
   const long long jobs = static_cast<long long>(tiles_m) * tiles_n * pt.ngroups;
-  static int nsm = 0;
-  if (nsm == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  }
+  const int nsm = sm_count();
   if (use2) {
-    static bool attr2 = false;
-    if (!attr2) {
-      cudaError_t e2 = cudaFuncSetAttribute(k_gemm_i8_2sm, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2_BYTES);
-      if (e2 != cudaSuccess) return e2;
+    auto kfn = (kind == 1) ? k_gemm_i8_2sm<1> : k_gemm_i8_2sm<0>;
+    cudaError_t e2 = once_per_device(1 + (kind & 1), [kfn] {
+      cudaError_t e3 = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2_BYTES);
+      if (e3 != cudaSuccess) return e3;
       // the largest shared-memory carveout (228 KB), so that the ~30 KB the GEMM leaves free on every SM can
       // host the register-path recombination CTAs of the previous column band (ozr_api.cu run_banded)
-      e2 = cudaFuncSetAttribute(k_gemm_i8_2sm, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-      if (e2 != cudaSuccess) return e2;
-      attr2 = true;
-    }
+      return cudaFuncSetAttribute(kfn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    });
+    if (e2 != cudaSuccess) return e2;
     const int tiles_m2 = (M + 2 * BM - 1) / (2 * BM);
     const long long jobs2 = static_cast<long long>(tiles_m2) * tiles_n * pt.ngroups;
     const int clusters = static_cast<int>(std::min<long long>(jobs2, nsm / 2));
@@ -578,9 +578,9 @@ cudaError_t launch_gemm_i8(const DigitOperand& A, const DigitOperand& B, int M, 
       bandw = b ? atoi(b) : BAND;
     }
     const int order = env_order >= 0 ? env_order : (job_order >= 0 ? job_order : 1);
-    k_gemm_i8_2sm<<<2 * clusters, NWARPS * 32, SMEM2_BYTES, stream>>>(tmA, tmB, pt, out, out_plane_stride, ldo, M, N,
-                                                                       K, tiles_m2, static_cast<int>(jobs2),
-                                                                       job_counter, l2hint, order, bandw);
+    kfn<<<2 * clusters, NWARPS * 32, SMEM2_BYTES, stream>>>(tmA, tmB, pt, out, out_plane_stride, ldo, M, N, K,
+                                                             tiles_m2, static_cast<int>(jobs2), job_counter, l2hint,
+                                                             order, bandw);
     return cudaGetLastError();
   }
   const int grid = static_cast<int>(std::min<long long>(jobs, nsm));

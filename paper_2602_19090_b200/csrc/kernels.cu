@@ -21,6 +21,7 @@
 
 #include "ddmath.cuh"
 #include "kernels.h"
+#include "ozr_internal.h"
 #include "ptx.cuh"
 
 namespace ozr {
@@ -540,6 +541,9 @@ __device__ __forceinline__ void split_wide_body_prmt(const double* __restrict__ 
       if (q == 0) {
         lo = w;
         hi = P80;
+      } else if (q >= 8) {  // S = 118 (k = 15) puts the window exactly on the upper word (a shift by 64 is UB)
+        lo = P80;
+        hi = w;
       } else {
         lo = (w << (8 * q)) | (P80 >> (64 - 8 * q));
         hi = (w >> (64 - 8 * q)) | (P80 << (8 * q));
@@ -845,36 +849,7 @@ __global__ void __launch_bounds__(BS, 3)
              });
 }
 
-// ---------------------------------------------------------------- ‖D‖₂ by power iteration (R12)
-// D: rows x cols, column-major (ld = rows). y = D·v in PS column splits (partials, fixed order), z = Dᵀ·y
-// one CTA per column; all reductions deterministic.
-constexpr int PS = 64;
-__global__ void __launch_bounds__(BS) k_dv_part(const double* __restrict__ D, int rows, int cols,
-                                               const double* __restrict__ v, double* __restrict__ part) {
-  const int i = blockIdx.x * BS + threadIdx.x;
-  if (i >= rows) return;
-  const int per = (cols + PS - 1) / PS;
-  const int j0 = blockIdx.y * per, j1 = min(cols, j0 + per);
-  double acc = 0.0;
-  for (int j = j0; j < j1; ++j) acc = fma(D[static_cast<long long>(j) * rows + i], v[j], acc);
-  part[static_cast<long long>(blockIdx.y) * rows + i] = acc;
-}
-__global__ void k_dv_sum(const double* __restrict__ part, int rows, double* __restrict__ y) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= rows) return;
-  double acc = 0.0;
-  for (int q = 0; q < PS; ++q) acc += part[static_cast<long long>(q) * rows + i];
-  y[i] = acc;
-}
-__global__ void __launch_bounds__(BS) k_dtv(const double* __restrict__ D, int rows, const double* __restrict__ y,
-                                           double* __restrict__ z) {
-  __shared__ double sh[BS / 32];
-  const double* col = D + static_cast<long long>(blockIdx.x) * rows;
-  double acc = 0.0;
-  for (int i = threadIdx.x; i < rows; i += BS) acc = fma(col[i], y[i], acc);
-  acc = block_sum(acc, sh);
-  if (threadIdx.x == 0) z[blockIdx.x] = acc;
-}
+// ---------------------------------------------------------------- power-iteration vector helpers (certify.cu, R12)
 // out[0] = Σ x_j² (one CTA, fixed order)
 __global__ void __launch_bounds__(BS) k_sumsq(const double* __restrict__ x, int n, double* __restrict__ out) {
   __shared__ double sh[BS / 32];
@@ -929,8 +904,7 @@ int tma_ok(const RecombPlan& rp, const int32_t* planes, long long pstride, int r
 // dynamic shared memory of the TMA paths; every recombination kernel prefers the largest carveout (the same
 // SM configuration as the slice GEMM, with which its register path co-resides)
 void init_attrs() {
-  static bool attr = false;
-  if (!attr) {
+  once_per_device(8, [] {
 #define OZR_CARVE(K) cudaFuncSetAttribute(K, cudaFuncAttributePreferredSharedMemoryCarveout, 100)
     OZR_CARVE(k_recombine_V<4>); OZR_CARVE(k_recombine_V<8>); OZR_CARVE(k_recombine_V<12>);
     OZR_CARVE(k_recombine_E<4>); OZR_CARVE(k_recombine_E<8>); OZR_CARVE(k_recombine_E<12>);
@@ -944,9 +918,8 @@ void init_attrs() {
     cudaFuncSetAttribute(k_recombine_E<12>, cudaFuncAttributeMaxDynamicSharedMemorySize, tma_smem(12));
     cudaFuncSetAttribute(k_final<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, tma_smem(4));
     cudaFuncSetAttribute(k_final<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, tma_smem(8));
-    cudaFuncSetAttribute(k_final<12>, cudaFuncAttributeMaxDynamicSharedMemorySize, tma_smem(12));
-    attr = true;
-  }
+    return cudaFuncSetAttribute(k_final<12>, cudaFuncAttributeMaxDynamicSharedMemorySize, tma_smem(12));
+  });
 }
 }  // namespace
 
@@ -1023,13 +996,6 @@ void launch_form_R(const int32_t* planes, long long pstride, int rows, int cols,
                    int scale8, int col0, const double* r_hi, const double* r_lo, double* R, long long ldr, double* nR2,
                    cudaStream_t s) {
   k_form_R<<<cols, BS, 0, s>>>(planes, pstride, rows, rp, g, scale8, col0, r_hi, r_lo, R, ldr, nR2);
-}
-void launch_norm2_step(const double* D, int rows, int cols, const double* v, double* part, double* y, cudaStream_t s) {
-  k_dv_part<<<dim3((rows + BS - 1) / BS, PS), BS, 0, s>>>(D, rows, cols, v, part);
-  k_dv_sum<<<(rows + 255) / 256, 256, 0, s>>>(part, rows, y);
-}
-void launch_norm2_back(const double* D, int rows, int cols, const double* y, double* z, cudaStream_t s) {
-  k_dtv<<<cols, BS, 0, s>>>(D, rows, y, z);
 }
 void launch_sumsq(const double* x, int n, double* out, cudaStream_t s) { k_sumsq<<<1, BS, 0, s>>>(x, n, out); }
 void launch_normalize(double* v, const double* z, int n, const double* nrm2, int col0, cudaStream_t s) {

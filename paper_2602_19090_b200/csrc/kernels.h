@@ -133,10 +133,7 @@ cudaError_t launch_cluster_apply(const ClusterLaunch& L, cudaStream_t s);
 void launch_final(const int32_t* planes, long long pstride, int rows, int cols, const RecombPlan& rp,
                   const int32_t* ellB, int scale8, const double* X1, long long ldx1, double* X, long long ldx,
                   double* nu2, double* wnext, cudaStream_t s, int allow_tma = 1, double* D = nullptr);
-// ‖D‖₂ by power iteration (D rows x cols column-major, ld = rows): y = D·v (part: 64·rows doubles of
-// scratch), z = Dᵀ·y, out[0] = Σx², v = z/√nrm2[0] (z == nullptr: a deterministic start vector).
-void launch_norm2_step(const double* D, int rows, int cols, const double* v, double* part, double* y, cudaStream_t s);
-void launch_norm2_back(const double* D, int rows, int cols, const double* y, double* z, cudaStream_t s);
+// power-iteration helpers (certify.cu): out[0] = Σx², v = z/√nrm2[0] (z == nullptr: a deterministic start vector)
 void launch_sumsq(const double* x, int n, double* out, cudaStream_t s);
 void launch_normalize(double* v, const double* z, int n, const double* nrm2, int col0, cudaStream_t s);
 void launch_recombine_dd(const int32_t* planes, long long pstride, int rows, int cols, const RecombPlan& rp,

@@ -17,6 +17,7 @@
 #include <cuda_runtime.h>
 
 #include "../../include/ozr.h"
+#include "certify.h"
 #include "comm.h"
 #include "kernels.h"
 #include "ozr_internal.h"
@@ -162,7 +163,8 @@ namespace {
 enum Slot {
   S_ADIG, S_AELL, S_W, S_X1, S_XDIG, S_XDIGT, S_G, S_SH, S_SL, S_RH, S_RL, S_PLANES, S_VH, S_VL, S_LAM, S_ER,
   S_ERR, S_EMAX, S_RDIG, S_RELL, S_EP, S_NRM2, S_NU2, S_WNEXT, S_ZEROELL, S_TMP1, S_TMP2, S_BELL, S_AT, S_ONES,
-  S_EDGES, S_ECOUNT, S_CINT, S_CDBL, S_CM, S_CR, S_CK, S_CV, S_CZ, S_CT, S_CSCR, S_CFLAG, S_SCAL, S_UFALL, S_CPART, S_GCNT, S_WA, S_GPLANES, S_RMAT, S_NR2, S_NW2, S_DWORK, S_DINFO, S_PI_V, S_PI_Z, S_PI_Y, S_PI_P, S_PI_S, S_CXG, S_CGJ, S_CGP
+  S_EDGES, S_ECOUNT, S_CINT, S_CDBL, S_CM, S_CR, S_CK, S_CV, S_CZ, S_CT, S_CSCR, S_CFLAG, S_SCAL, S_UFALL, S_CPART, S_GCNT, S_WA, S_GPLANES, S_RMAT, S_NR2, S_NW2, S_DWORK, S_DINFO, S_PI_V, S_PI_Z, S_PI_Y, S_PI_P, S_PI_S, S_CXG, S_CGJ, S_CGP,
+  S_CEB, S_CCB, S_CSE, S_CSC, S_CESQ, S_CDSQ, S_CFLG
 };
 
 ozr_status fail(ozr_ctx c, ozr_status st, const char* fmt, ...) {
@@ -646,10 +648,8 @@ void split_A_finish(const double* A, int64_t n, const std::vector<double>& hwA, 
 // ranks — their W_JJ / Ẽ_{:,J} blocks (all-reduce of zero-padded buffers, exact). Every host decision is
 // taken from all-gathered data in the 1-GPU order, so a P-rank sweep equals the 1-GPU sweep bit for bit
 // when nl is a multiple of the 256-column tile.
-// keepD: the final kernel also stores the update D = X̂_new − X̂_old of the rank's columns in the V buffer
-// (dead by then) for update_norm2.
 ozr_status sweep(ozr_ctx ctx, Exchange* ex, const double* A, int64_t n, int64_t lda, double* Xfull, int64_t ldx,
-                 double* lambda, const ozr_params& P, ozr_step_report& rep, SweepState& st, bool keepD = false) {
+                 double* lambda, const ozr_params& P, ozr_step_report& rep, SweepState& st) {
   memset(&rep, 0, sizeof rep);
   cudaStream_t s = ctx->stream;
   const int NP = ex ? ex->P : 1, RK = ex ? ex->rank : 0;
@@ -1259,8 +1259,7 @@ ozr_status sweep(ozr_ctx ctx, Exchange* ex, const double* A, int64_t n, int64_t 
   OZR_X(run_banded(ctx, opQ, opE, N, NL, N, pt, planes, 2,
                    [&](int64_t c0, int64_t c1, int t0, int tma, cudaStream_t q) {
                      launch_final(planes + c0 * n, nnl, N, static_cast<int>(c1 - c0), shift_plan(rp, t0), rell + c0,
-                                  scaleU, X1 + c0 * n, n, X + c0 * ldx, ldx, nu2 + col0 + c0, wnext + col0 + c0, q, tma,
-                                  keepD ? Vh + c0 * n : nullptr);
+                                  scaleU, X1 + c0 * n, n, X + c0 * ldx, ldx, nu2 + col0 + c0, wnext + col0 + c0, q, tma);
                    }));
   ctx->mark("gemmU+final");
   OZR_X(xgather(nu2, nl * sizeof(double)));
@@ -1333,47 +1332,126 @@ ozr_status sweep(ozr_ctx ctx, Exchange* ex, const double* A, int64_t n, int64_t 
   return OZR_OK;
 }
 
-// ‖D‖₂ of the last sweep's update (stored by sweep(keepD)), by 12 power iterations on DᵀD from a fixed start
-// vector (R12): the stop rule's ν is a Frobenius norm, √n-pessimistic for a noise-like update, while the
-// paper's forward error is the 2-norm. Estimate from below (converges to σ_max). On P ranks D is
-// column-partitioned: D·v is all-reduced, Dᵀy is local.
-ozr_status update_norm2(ozr_ctx ctx, Exchange* ex, int64_t n, double* out) {
+constexpr double kCertSafety = 1.15;  // power-iteration / bf16-GEMM slack of the estimate (R12)
+constexpr double kContract = 1.0 / 8;  // an estimate that fell by less than this sits at the truncation floor
+
+// a10 (R12): the a-posteriori forward-error estimate of the sweep just completed, from its own Ẽ (certify.cu):
+//   est = sqrt(‖Q∘H‖₂² + (2u)²) + 1.5‖Ẽ‖_F²,  Q = ẼᵀC, c_kj = (λ̂_k − λ̂_j)ẽ_kj, H_ij = 1/(λ̂_j − λ̂_i) (i ≠ j),
+// the second-order defect of Ẽ (‖X − X̂_new‖₂ ≈ ‖E − Ẽ‖₂) plus the bound of the terms quadratic in ‖Ẽ‖ and the
+// fp64 rounding of X̂_new. ‖Q∘H‖₂ comes from its Frobenius norm when that already certifies, from the power
+// iteration otherwise — except when even the lower bound max_j ‖(Q∘H)_{:,j}‖ + 1.5‖Ẽ‖_F² exceeds 16δ: then the
+// upper bound (Frobenius) is reported, which no decision of the driver can tell from the exact value.
+// Reads the sweep's Ẽ' (S_EP), g (S_G) and λ̂ (S_LAM); writes rep.cert, cert_q, cert_frob, cert_iters.
+ozr_status certify(ozr_ctx ctx, Exchange* ex, int64_t n, double delta, ozr_step_report& rep) {
   const int NP = ex ? ex->P : 1, RK = ex ? ex->rank : 0;
-  const int64_t nl = n / NP, col0 = RK * nl;
+  const int64_t nl = n / NP, col0 = RK * nl, nnl = n * nl;
+  const int N = static_cast<int>(n), NL = static_cast<int>(nl);
   cudaStream_t s = ctx->stream;
-  const double* D = static_cast<const double*>(ctx->bufs[S_VH].p);
-  double* v = ctx->ws<double>(S_PI_V, nl);
+  const int64_t ldb = round16(n);  // bf16 elements per column (32-byte aligned columns)
+  const double* Ep = static_cast<const double*>(ctx->bufs[S_EP].p);
+  const int32_t* g = static_cast<const int32_t*>(ctx->bufs[S_G].p);
+  const double* lam = static_cast<const double*>(ctx->bufs[S_LAM].p);
+  uint16_t* Eb = ctx->ws<uint16_t>(S_CEB, static_cast<size_t>(ldb) * n);
+  uint16_t* Cb = ctx->ws<uint16_t>(S_CCB, static_cast<size_t>(ldb) * nl);
+  int32_t* sE = ctx->ws<int32_t>(S_CSE, n);
+  int32_t* sC = ctx->ws<int32_t>(S_CSC, nl);
+  double* esq = ctx->ws<double>(S_CESQ, n);
+  double* dsq = ctx->ws<double>(S_CDSQ, n);
+  int* flag = ctx->ws<int>(S_CFLG, 4);
+  float* Q = reinterpret_cast<float*>(ctx->ws<int32_t>(S_PLANES, nnl));  // the slice planes are dead by now
+  float* D = reinterpret_cast<float*>(ctx->ws<double>(S_VH, nnl));      // so is V
+  int* cnt = ctx->ws<int>(S_GCNT, 4);
   double* z = ctx->ws<double>(S_PI_Z, nl);
+  double* v = ctx->ws<double>(S_PI_V, nl);
   double* y = ctx->ws<double>(S_PI_Y, n);
-  double* part = ctx->ws<double>(S_PI_P, 64 * static_cast<size_t>(n));
+  double* part = ctx->ws<double>(S_PI_P, static_cast<size_t>(cert_pi_chunks()) * n);
   double* sc = ctx->ws<double>(S_PI_S, 2);
-  OZR_ALLOC(v); OZR_ALLOC(z); OZR_ALLOC(y); OZR_ALLOC(part); OZR_ALLOC(sc);
+  OZR_ALLOC(Eb); OZR_ALLOC(Cb); OZR_ALLOC(sE); OZR_ALLOC(sC); OZR_ALLOC(esq); OZR_ALLOC(dsq); OZR_ALLOC(flag);
+  OZR_ALLOC(Q); OZR_ALLOC(D); OZR_ALLOC(cnt); OZR_ALLOC(z); OZR_ALLOC(v); OZR_ALLOC(y); OZR_ALLOC(part); OZR_ALLOC(sc);
+  auto gather = [&](void* base, size_t bytes) -> ozr_status {
+    if (ex && !ex->allgather(base, bytes, s)) return fail(ctx, OZR_ERR_COMM, "all-gather: %s", ex->err.c_str());
+    return OZR_OK;
+  };
   auto allsum = [&](double* b, size_t c) -> ozr_status {
     if (ex && !ex->allreduce_sum(b, c, s)) return fail(ctx, OZR_ERR_COMM, "all-reduce: %s", ex->err.c_str());
     return OZR_OK;
   };
-  const int N = static_cast<int>(n), NL = static_cast<int>(nl);
-  launch_normalize(v, nullptr, NL, nullptr, static_cast<int>(col0), s);
-  launch_sumsq(v, NL, sc, s);
-  ozr_status e = allsum(sc, 1);
-  if (e != OZR_OK) return e;
-  launch_normalize(z, v, NL, sc, 0, s);  // z = v/‖v‖
-  for (int it = 0; it < 12; ++it) {
-    launch_norm2_step(D, N, NL, z, part, y, s);  // y = D z (this rank's columns)
-    if ((e = allsum(y, n)) != OZR_OK) return e;
-    launch_norm2_back(D, N, NL, y, v, s);  // v = Dᵀ y
-    launch_sumsq(v, NL, sc, s);
-    if ((e = allsum(sc, 1)) != OZR_OK) return e;
-    launch_normalize(z, v, NL, sc, 0, s);
-  }
-  OZR_CK(cudaGetLastError(), "update norm");
-  double h = 0.0;
+  ozr_status e;
+  OZR_CK(cudaMemsetAsync(flag, 0, sizeof(int), s), "memset");
+  launch_cert_prep(Ep, n, N, NL, g, lam, static_cast<int>(col0), Eb, Cb, ldb, sE, sC, esq + col0, s);
+  if ((e = gather(Eb, static_cast<size_t>(nl) * ldb * 2)) != OZR_OK) return e;  // all columns: the A operand
+  if ((e = gather(sE, nl * sizeof(int32_t))) != OZR_OK) return e;
+  if ((e = gather(esq, nl * sizeof(double))) != OZR_OK) return e;
+  PairTable pt;
+  memset(&pt, 0, sizeof pt);
+  pt.ngroups = 1;
+  pt.first[1] = 1;
+  pt.diag[0] = 2;
+  const DigitOperand opE{reinterpret_cast<const int8_t*>(Eb), 2 * ldb, 2 * ldb * n, 1};
+  const DigitOperand opC{reinterpret_cast<const int8_t*>(Cb), 2 * ldb, 2 * ldb * nl, 1};
+  OZR_CK(launch_gemm_i8(opE, opC, N, NL, 2 * N, pt, reinterpret_cast<int32_t*>(Q), nnl, n, s, cnt, 1, 1),
+         "certificate GEMM (bf16)");
+  launch_cert_delta(Q, n, N, NL, sE, sC, lam, static_cast<int>(col0), D, dsq + col0, flag, s);
+  OZR_CK(cudaGetLastError(), "certificate");
+  if ((e = gather(dsq, nl * sizeof(double))) != OZR_OK) return e;
+  std::vector<double> hesq(n), hdsq(n);
+  int hflag = 0;
   ctx->pend.clear();
   ctx->hst_off = 0;
-  OZR_D2H(&h, sc, sizeof(double));
+  OZR_D2H(hesq.data(), esq, n * sizeof(double));
+  OZR_D2H(hdsq.data(), dsq, n * sizeof(double));
+  OZR_D2H(&hflag, flag, sizeof(int));
   OZR_CK(cudaStreamSynchronize(s), "sync");
   ctx->flush();
-  *out = std::sqrt(std::sqrt(h));  // ‖DᵀD z‖ ≈ σ_max² for the unit z
+  rep.cert_iters = 0;
+  if (hflag) {  // equal estimates outside a group: no certificate
+    rep.cert = rep.cert_q = rep.cert_frob = INFINITY;
+    return OZR_OK;
+  }
+  double e2 = 0.0, d2 = 0.0, dmax = 0.0;
+  for (int64_t j = 0; j < n; ++j) {
+    e2 += hesq[j];
+    d2 += hdsq[j];
+    dmax = std::max(dmax, hdsq[j]);
+  }
+  const double quad = 1.5 * e2, frob = std::sqrt(d2), rnd = 2.0 * kU;
+  rep.cert_frob = frob;
+  const double upper = std::sqrt(frob * frob + rnd * rnd) + quad;
+  if (upper * kCertSafety <= delta || std::sqrt(dmax) + quad > 16.0 * delta) {
+    rep.cert = upper;
+    rep.cert_q = frob;
+    return OZR_OK;
+  }
+  // power iteration for ‖D‖₂ (D column-partitioned: D·z all-reduced, Dᵀy local)
+  launch_normalize(v, nullptr, NL, nullptr, static_cast<int>(col0), s);
+  launch_sumsq(v, NL, sc, s);
+  if ((e = allsum(sc, 1)) != OZR_OK) return e;
+  launch_normalize(z, v, NL, sc, 0, s);
+  double sig = 0.0, prev = -1.0;
+  int it = 0;
+  while (it < 48) {
+    for (int q = 0; q < 4; ++q, ++it) {
+      launch_pi_dz(D, N, NL, z, part, y, s);
+      if ((e = allsum(y, n)) != OZR_OK) return e;
+      launch_pi_dty(D, N, NL, y, v, s);
+      launch_sumsq(v, NL, sc, s);
+      if ((e = allsum(sc, 1)) != OZR_OK) return e;
+      launch_normalize(z, v, NL, sc, 0, s);
+    }
+    OZR_CK(cudaGetLastError(), "power iteration");
+    double h = 0.0;
+    ctx->pend.clear();
+    ctx->hst_off = 0;
+    OZR_D2H(&h, sc, sizeof(double));
+    OZR_CK(cudaStreamSynchronize(s), "sync");
+    ctx->flush();
+    sig = std::sqrt(std::sqrt(h));  // ‖DᵀD z‖ → σ_max² for the unit z
+    if (prev > 0.0 && std::fabs(sig - prev) <= 1e-3 * sig) break;
+    prev = sig;
+  }
+  rep.cert_iters = it;
+  rep.cert_q = sig;
+  rep.cert = std::sqrt(sig * sig + rnd * rnd) + quad;
   return OZR_OK;
 }
 
@@ -1464,6 +1542,7 @@ void ozr_params_default(ozr_params* p) {
   p->form_R = 0;
   p->dense_cluster = 192;  // = the cooperative-Jacobi threshold: measured 12x faster at m = 739 (c2)
   p->max_escalations = 2;
+  p->certify = 1;
 }
 
 ozr_status ozr_split(ozr_ctx ctx, const double* M, const double* M_lo, int64_t rows, int64_t cols, int64_t ldm,
@@ -1686,85 +1765,72 @@ ozr_status ozr_refine_step_dist(ozr_ctx ctx, ozr_comm comm, const double* A, int
   st = sweep(ctx, comm ? comm->ex.get() : nullptr, A, n, lda, X, ldx, lambda, *params, rep, ss);
   rep.sweep = 1;
   rep.theta = params->theta;
+  rep.cert = -1.0;
+  if (st == OZR_OK && params->certify >= 2 && rep.n_clusters == 0)
+    st = certify(ctx, comm ? comm->ex.get() : nullptr, n, params->delta, rep);
   if (report) *report = rep;
   return st;
 }
 
+// The driver (R12; the paper iterates a fixed number of times): after every sweep without
+// unresolved groups its own Ẽ certifies the returned X̂ (certify()); OK when est·kCertSafety ≤ δ. An uncertified
+// estimate that did not fall below kContract × the previous one — or fell so fast that the next sweep's quadratic
+// part est³/est_prev² is below δ/8 while est ≤ 16δ — sits at the truncation floor (quadratic in 2^-β,
+// PAPER.md:341-373): θ grows by the power of 4 that brings it below δ/2, at most max_escalations times, then
+// OZR_ERR_NOT_CONVERGED. Sweeps with unresolved groups (a Rayleigh–Ritz rotation, R13) are neither certified nor
+// compared. Mirrors oracle/refine.refine_to_tol.
 ozr_status ozr_refine_to_tol_dist(ozr_ctx ctx, ozr_comm comm, const double* A, int64_t n, int64_t lda, double* X,
                                   int64_t ldx, double* lambda, const ozr_params* params, ozr_step_report* history,
                                   int max_hist, int* sweeps_done) {
   ozr_status st = check_refine_args(ctx, comm, A, n, lda, X, ldx, lambda, params);
   if (st != OZR_OK) return st;
   SweepState ss;
-  double nu_prev = -1.0;
+  double est_prev = -1.0;
   int done = 0;
   ozr_status result = OZR_ERR_NOT_CONVERGED;
   ctx->err.clear();
   const int maxs = params->max_sweeps > 0 ? params->max_sweeps : 6;
   ozr_params P = *params;
   int escalations = 0;
+  Exchange* ex = comm ? comm->ex.get() : nullptr;
+  const double delta = params->delta;
   for (int k = 0; k < maxs; ++k) {
     ozr_step_report rep;
-    st = sweep(ctx, comm ? comm->ex.get() : nullptr, A, n, lda, X, ldx, lambda, P, rep, ss, true);
+    st = sweep(ctx, ex, A, n, lda, X, ldx, lambda, P, rep, ss);
     rep.theta = P.theta;
     rep.sweep = k + 1;
+    rep.cert = -1.0;
+    if (st == OZR_OK && rep.n_clusters == 0 && params->certify >= 1) st = certify(ctx, ex, n, delta, rep);
     if (st != OZR_OK) {
       if (sweeps_done) *sweeps_done = done;
       return st;
     }
     if (history && k < max_hist) history[k] = rep;
     done = k + 1;
-    if (rep.net_update <= params->delta || rep.predicted_error <= params->delta) {
+    if (rep.n_clusters > 0 || params->certify < 1) {  // a Rayleigh–Ritz sweep: no certificate, no comparison
+      est_prev = -1.0;
+      continue;
+    }
+    const double est = rep.cert;
+    if (est * kCertSafety <= delta) {
       result = OZR_OK;
       break;
     }
-    // ‖D‖₂ ≥ ‖D‖_F/√n: once ν_F ≤ √n·δ the update's 2-norm (the paper's measure) may already be ≤ δ (R12)
-    double d2 = -1.0;
-    if (rep.n_clusters == 0 && rep.net_update <= std::sqrt(static_cast<double>(n)) * params->delta) {
-      st = update_norm2(ctx, comm ? comm->ex.get() : nullptr, n, &d2);
-      if (st != OZR_OK) {
-        if (sweeps_done) *sweeps_done = done;
-        return st;
-      }
-      rep.update_2norm = d2;
-      if (history && k < max_hist) history[k] = rep;
-      if (d2 <= params->delta) {
-        result = OZR_OK;
-        break;
-      }
-    }
-    if (rep.n_clusters > 0) {  // a Rayleigh–Ritz sub-solve rotates its group: no contraction measure (R12)
-      nu_prev = -1.0;
-      continue;
-    }
-    if (nu_prev >= 0.0 && rep.net_update > nu_prev / 2) {
-      // stagnation of the Frobenius ν above δ: the update's 2-norm (the paper's measure) may already be
-      // ≤ δ — a noise-like update has ‖D‖₂ ≈ 2‖D‖_F/√n (R12)
-      if (d2 < 0.0) {
-        st = update_norm2(ctx, comm ? comm->ex.get() : nullptr, n, &d2);
-        if (st != OZR_OK) {
-          if (sweeps_done) *sweeps_done = done;
-          return st;
-        }
-        rep.update_2norm = d2;
-        if (history && k < max_hist) history[k] = rep;
-      }
-      if (d2 <= params->delta) {
-        result = OZR_OK;
-        break;
-      }
-      // the truncated iteration sits at its noise floor above δ: lower it by 2 bits of β (θ × 16; the
-      // floor falls with the truncation) and keep going; stagnation again → NOT_CONVERGED
+    const bool floor = est_prev > 0.0 && (est > kContract * est_prev ||
+                                          (est <= 16.0 * delta && est * est * est / (est_prev * est_prev) <= delta / 8));
+    if (floor) {
       if (P.truncate && escalations < params->max_escalations) {
         ++escalations;
-        P.theta = (P.theta > 0 ? P.theta : 1.0) * 16.0;
-        nu_prev = -1.0;
+        const int m = std::max(1, static_cast<int>(std::ceil(std::log(2.0 * est * kCertSafety / delta) / std::log(4.0))));
+        P.theta = (P.theta > 0 ? P.theta : 1.0) * std::ldexp(1.0, 2 * std::min(m, 10));
+        est_prev = -1.0;
         continue;
       }
-      fail(ctx, OZR_ERR_NOT_CONVERGED, "stagnation: net update %.3e > previous %.3e / 2", rep.net_update, nu_prev);
+      fail(ctx, OZR_ERR_NOT_CONVERGED, "stagnation at the truncation floor: certified error %.3e > delta %.3e", est,
+           delta);
       break;
     }
-    nu_prev = rep.net_update;
+    est_prev = est;
   }
   if (result != OZR_OK && ctx->err.empty()) fail(ctx, OZR_ERR_NOT_CONVERGED, "max_sweeps reached");
   if (sweeps_done) *sweeps_done = done;

@@ -1,9 +1,35 @@
 // ozr_internal.h — internal (non-ABI) declarations shared by the ozr CUDA sources.
 #pragma once
 #include <cstdint>
+#include <mutex>
 #include <cuda_runtime.h>
 
 namespace ozr {
+
+// Runs f() once per (current device, key), under a lock: kernel attributes set with cudaFuncSetAttribute apply to
+// the current device only, so they are set for every device a context runs on, and no thread launches before
+// they are in place.
+template <class F>
+cudaError_t once_per_device(int key, F f) {
+  static std::mutex mu;
+  static unsigned long long seen[128] = {};
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 0 || dev >= 128 || key < 0 || key >= 64) return f();
+  std::lock_guard<std::mutex> g(mu);
+  const unsigned long long bit = 1ull << key;
+  if (seen[dev] & bit) return cudaSuccess;
+  e = f();
+  if (e == cudaSuccess) seen[dev] |= bit;
+  return e;
+}
+inline int sm_count() {
+  int dev = 0, nsm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  return nsm > 0 ? nsm : 1;
+}
 
 constexpr int kMaxPairs = 256;   // digit pairs per product
 constexpr int kMaxGroups = 96;   // int32 accumulation groups (output planes) per product
@@ -43,9 +69,11 @@ struct DigitOperand {
 // A rows and planes at the same time); bit 1 — K-block outer, the group's pairs inner (every job near a tile
 // reads the same A K-block at once). Measured best: 3 when the A operand has more planes than B (V = A·X̂),
 // else 1 (W, U). −1: 1 (OZR_GEMM_ORDER overrides for experiments).
+// kind 0: int8 digit planes (exact int32 planes); kind 1: bf16 operands (2 bytes per K element; K and ld in
+// BYTES), f32 accumulator written as raw 32-bit words (the certificate's Q = ẼᵀC, certify.cu).
 cudaError_t launch_gemm_i8(const DigitOperand& A, const DigitOperand& B, int M, int N, int K,
                            const PairTable& pt, int32_t* out, int64_t out_plane_stride, int64_t ldo,
-                           cudaStream_t stream, int* job_counter, int job_order = -1);
+                           cudaStream_t stream, int* job_counter, int job_order = -1, int kind = 0);
 
 // Reference (SIMT) version of the same contract; used only by the dev harness to cross-check the
 // tensor-core kernel on the GPU. Not on the product path.

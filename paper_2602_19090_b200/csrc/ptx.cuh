@@ -204,6 +204,16 @@ __device__ __forceinline__ void mma_i8_2sm(uint32_t tmem_d, uint64_t adesc, uint
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+// kind::f16 with bf16 operands and an f32 accumulator (the certificate's product Q = ẼᵀC, certify.cu)
+__device__ __forceinline__ void mma_bf16_2sm(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                             uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
 // arrive (once) on the mbarrier at the same offset in every CTA of `mask` when this thread's MMAs complete
 __device__ __forceinline__ void mma_commit_2sm(uint64_t* bar, uint16_t mask) {
   asm volatile(
@@ -231,6 +241,15 @@ __host__ __device__ constexpr uint32_t idesc_i8(int M, int N) {
   return (2u << 4)                                  // D format S32
          | (1u << 7)                                // A signed int8
          | (1u << 10)                               // B signed int8
+         | (static_cast<uint32_t>(N >> 3) << 17)    // N / 8
+         | (static_cast<uint32_t>(M >> 4) << 24);   // M / 16
+}
+
+// Instruction descriptor for kind::f16: bf16 x bf16 -> f32, both K-major, M x N (same field layout as i8).
+__host__ __device__ constexpr uint32_t idesc_bf16(int M, int N) {
+  return (1u << 4)                                  // D format F32
+         | (1u << 7)                                // A bf16
+         | (1u << 10)                               // B bf16
          | (static_cast<uint32_t>(N >> 3) << 17)    // N / 8
          | (static_cast<uint32_t>(M >> 4) << 24);   // M / 16
 }

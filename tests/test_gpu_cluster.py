@@ -154,7 +154,7 @@ def test_c4_recipe_default_dense_path(ctx):
     A, lam0, X0 = _case("c4", 2048, "fp32")
     Xd, ld = to_dev(X0), vec_dev(lam0)
     st, hist = ozr.ozr_refine_to_tol(ctx, to_dev(A), Xd, ld, ozr.default_params(delta=1e-10, max_sweeps=12))
-    trail = [(h["net_update"], h["n_clusters"], h["max_cluster"], h["update_2norm"]) for h in hist]
+    trail = [(h["net_update"], h["n_clusters"], h["max_cluster"], h["cert"]) for h in hist]
     assert hist[0]["max_cluster"] >= 1024, trail
     assert st == 0, trail
     X, lam = to_np(Xd), to_np(ld)

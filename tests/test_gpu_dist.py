@@ -125,19 +125,19 @@ def test_nccl_single_rank(ctx):
         dist.destroy_process_group()
 
 
-def test_partitioned_update_2norm(ctx):
-    """The stop rule's 2-norm estimate of the update (R12) on a column-partitioned X̂: D·v all-reduced over the
-    ranks, Dᵀy local. c4' (n = 2048, δ = 1e-8) on 2 ranks stops after the same sweeps as one GPU, with the
-    same X̂ bits and the same estimate up to the summation order of the all-reduce."""
+def test_partitioned_certificate(ctx):
+    """The certificate (R12) on a column-partitioned X̂: the bf16 Ẽ columns all-gathered as the A operand of
+    Q = ẼᵀC, D·z all-reduced in the power iteration. c4' (n = 2048, δ = 1e-12) on 2 ranks stops after the same
+    sweeps as one GPU, with the same X̂ bits and the same estimate up to the summation order of the all-reduce."""
     import paper_2602_19090_b200 as ozr
     A, lam0, X0 = _case("c4p", 2048, "fp64")
-    p = ozr.default_params(delta=1e-8, max_sweeps=8)
+    p = ozr.default_params(delta=1e-12, max_sweeps=8)
     Xd, ld = to_dev(X0), vec_dev(lam0)
     st1, hist1 = ozr.ozr_refine_to_tol(ctx, to_dev(A), Xd, ld, p)
     out = _run_ranks(2, A, X0, lam0, p, to_tol=True)
     assert st1 == 0 and all(o[0] == 0 for o in out)
-    assert hist1[-1]["update_2norm"] > 0
+    assert hist1[-1]["cert"] > 0 and hist1[-1]["cert_iters"] > 0
     for o in out:
         assert len(o[3]) == len(hist1)
-        assert abs(o[3][-1]["update_2norm"] / hist1[-1]["update_2norm"] - 1) < 1e-10
+        assert abs(o[3][-1]["cert"] / hist1[-1]["cert"] - 1) < 1e-6
     assert np.array_equal(_assemble(out, 2048, 2), to_np(Xd))

@@ -61,6 +61,8 @@ def test_sweep_default_budgets_within_delta(ctx, cfg, n, delta, start):
 
 
 def test_refine_to_tol_c1_forward_error(ctx):
+    """BASELINE c1 (n = 100, cnd 1e8, FP64 start): status OK ⇒ ‖X − X̂‖₂ ≤ δ against the reference, one or two
+    sweeps ("one or two iterations", PAPER.md:540)."""
     import paper_2602_19090_b200 as ozr
     A, lam0, X0, cfg = W.make_config("c1")
     Xh, Xl, lh, ll, _ = orf.reference_eigvecs(A, X0, lam0)
@@ -69,8 +71,8 @@ def test_refine_to_tol_c1_forward_error(ctx):
         st, hist = ozr.ozr_refine_to_tol(ctx, to_dev(A), Xd, ld, ozr.default_params(delta=delta))
         fe = orf.forward_error(Xh, Xl, to_np(Xd))
         assert st == 0, hist
-        assert fe <= 2 * delta, (delta, fe, hist)
-        assert len(hist) <= 3
+        assert fe <= delta, (delta, fe, hist)
+        assert hist[-1]["cert"] * 1.15 <= delta and len(hist) <= 2
 
 
 def test_refine_step_errors(ctx):
@@ -121,75 +123,26 @@ def test_column_bands_bit_identical(ctx, cfg, start, monkeypatch):
     assert r4["launches"] > r1["launches"]
 
 
-def test_update_2norm_stop(ctx):
-    """R12 on the GPU: c4' (n = 2048) at δ = 1e-8 — the Frobenius net update sits at the truncation noise
-    floor (2.7e-8 > δ) while its 2-norm (the paper's measure) is below δ: once ν_F ≤ √n·δ the library's
-    power-iteration estimate of ‖X̂_k − X̂_{k−1}‖₂ (matching numpy's exact 2-norm to 1 %) stops the driver with
-    status OK, and the forward error against the oracle reference is ≤ δ."""
-    import paper_2602_19090_b200 as ozr
-    A, lam0, X0 = _case("c4p", 2048, "fp64")
-    delta = 1e-8
-    Ad = to_dev(A)
-    Xd, ld = to_dev(X0), vec_dev(lam0)
-    st, hist = ozr.ozr_refine_to_tol(ctx, Ad, Xd, ld, ozr.default_params(delta=delta, max_sweeps=8))
-    assert st == 0 and len(hist) <= 3, hist
-    last = hist[-1]
-    assert last["update_2norm"] > 0 and last["net_update"] > delta >= last["update_2norm"]
-    Xp, lp = to_dev(X0), vec_dev(lam0)
-    ozr.ozr_refine_to_tol(ctx, Ad, Xp, lp, ozr.default_params(delta=delta, max_sweeps=len(hist) - 1))
-    exact = np.linalg.norm(to_np(Xd) - to_np(Xp), 2)
-    assert abs(last["update_2norm"] / exact - 1) < 1e-2, (last["update_2norm"], exact)
-    Xh, Xl, lh, ll, _ = orf.reference_eigvecs(A, X0, lam0)
-    assert orf.forward_error(Xh, Xl, to_np(Xd), lh, to_np(ld)) <= delta
+CERT_CASES = [("c4p", 2048, 1e-12), ("c3", 1024, 1e-12), ("c5", 1024, 1e-15), ("c1", 100, 1e-15),
+              ("c2", 1024, 1e-14)]
 
 
-def test_sparse_beta_banded(ctx):
-    """§4.3's sparse constants on the banded stand-in for the paper's sparse matrices
-    (workloads.banded_sym, k = 17 nonzeros per row, n = 1024, cnd 1e8, FP64 start): one sweep with
-    beta_mode = 2 matches the oracle sweep with beta_mode "sparse" (same β, X̂ and D̂ within 1e-13), the
-    V product's budget uses the row length k, and ozr_refine_to_tol reaches δ = 1e-12 against the oracle
-    reference."""
+@pytest.mark.parametrize("cfg,n,delta", CERT_CASES)
+def test_certificate_matches_oracle_and_forward_error(ctx, cfg, n, delta):
+    """R12: the library's a-posteriori estimate (bf16 tensor-core Q = ẼᵀC, power iteration; params.certify = 2)
+    after the second sweep of an FP64 start, against (a) the oracle's certificate of its own exact-product sweep
+    on the same input (3 %) and (b) the forward error of the GPU's X̂ against the reference eigenvectors (the
+    estimate may not fall below it by more than 10 %: the digit budgets' error is part of what it certifies)."""
     import paper_2602_19090_b200 as ozr
-    A, lam, k = W.banded_sym(1024, layers=4, cnd=1e8, seed=11)
+    c = dict(W.CONFIGS[cfg])
+    A, _ = W.make_matrix(n, c["kind"], c["cnd"], c["seed"])
     lam0, X0 = W.initial_eig(A, "fp64")
-    delta = 1e-12
-    Xg, lg, rep = _gpu_sweep(ctx, A, X0, lam0, delta, beta_mode=2, row_nnz=k)
-    Xo, lo, info = orf.sweep(A, X0, lam0, delta, beta_mode="sparse", row_nnz=k)
-    assert rep["beta"] == info["beta"] and rep["alpha"] == info["alpha"]
-    assert np.max(np.abs(Xg - Xo)) <= 1e-13
-    assert np.max(np.abs(lg - lo)) <= 1e-13 * np.max(np.abs(lam0))
-    _, _, rep_dense = _gpu_sweep(ctx, A, X0, lam0, delta)
-    assert rep["beta"] <= rep_dense["beta"]          # min(k, √n) ≤ √n: the sparse rule keeps more bits
-    assert rep["pairs_V"] <= rep_dense["pairs_V"] + 5 * (rep_dense["beta"] - rep["beta"] + 1)
+    X1, l1, _ = orf.sweep(A, X0, lam0, delta)
+    Xg, lg, rep = _gpu_sweep(ctx, A, X1, l1, delta, certify=2)
+    Xo, lo, info = orf.sweep(A, X1, l1, delta)
+    co = orf.certificate(info["E"], lo, delta=delta)
+    assert rep["n_clusters"] == 0 and rep["cert"] > 0
+    assert abs(rep["cert"] - co["est"]) <= 0.03 * co["est"], (rep["cert"], co)
     Xh, Xl, lh, ll, _ = orf.reference_eigvecs(A, X0, lam0)
-    Xd, ld = to_dev(X0), vec_dev(lam0)
-    st, hist = ozr.ozr_refine_to_tol(ctx, to_dev(A), Xd, ld,
-                                     ozr.default_params(delta=delta, beta_mode=2, row_nnz=k, max_sweeps=6))
-    assert st == 0
-    assert orf.forward_error(Xh, Xl, to_np(Xd), lh, to_np(ld)) <= delta
-
-
-@pytest.mark.parametrize("mode", ["untruncated", "theoretical_xi_n", "theoretical_xi_1", "theta_1", "global_budgets",
-                                  "paper_alg1"])
-def test_sweep_modes_match_oracle(ctx, mode):
-    """The other β / truncation readings against the oracle sweep with the same settings (c2 recipe, n = 512,
-    FP64 start, δ = 1e-14): truncate = 0 (X̂ kept whole — the prior work's untruncated two-sided analogue,
-    PAPER.md:432-443), §3.3's eq. proposed_beta (⌈·⌉) with ξ = n and ξ = 1, θ = 1 (the
-    paper's own δ), one pair budget per product instead of per 256-column tile (R8 without R8b), and the
-    paper's Algorithm 1 without the cluster branch (cluster_mode 0)."""
-    A, lam0, X0 = _case("c2", 512, "fp64")
-    delta = 1e-14
-    gkw, okw = {
-        "untruncated": (dict(truncate=0), dict(truncate=False)),
-        "theoretical_xi_n": (dict(beta_mode=1, xi=0.0), dict(beta_mode="theoretical", xi=None)),
-        "theoretical_xi_1": (dict(beta_mode=1, xi=1.0), dict(beta_mode="theoretical", xi=1.0)),
-        "theta_1": (dict(theta=1.0), dict(theta=1.0)),
-        "global_budgets": (dict(tile_budgets=0), dict()),
-        "paper_alg1": (dict(cluster_mode=0), dict(cluster_mode=0)),
-    }[mode]
-    Xg, lg, rep = _gpu_sweep(ctx, A, X0, lam0, delta, **gkw)
-    Xo, lo, info = orf.sweep(A, X0, lam0, delta, **okw)
-    if mode != "untruncated":
-        assert rep["beta"] == info["beta"] and rep["alpha"] == info["alpha"]
-    assert np.max(np.abs(Xg - Xo)) <= 1e-13
-    assert np.max(np.abs(lg - lo)) <= 1e-13 * np.max(np.abs(lam0))
+    fe = orf.forward_error(Xh, Xl, Xg, lh, lg)
+    assert rep["cert"] >= 0.9 * fe, (rep["cert"], fe, co)
