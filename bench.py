@@ -170,6 +170,57 @@ def run_reference(args):
     return 0
 
 
+def run_c5(ctx, comm, dist_mode, ws, rank, dev, W, ozr, torch, dist, steps=2, warmup=1):
+    """c5 sweeps partitioned over the ws ranks: rank 0 builds the problem, every rank receives it."""
+    from paper_2602_19090_b200.dist import broadcast_tensor, partition
+    cfg = dict(W.CONFIGS["c5"])
+    n = cfg["n"]
+    if rank == 0:
+        A, lam0, X0, cfg = W.make_config_torch("c5", dev)
+    else:
+        A = ozr.colmajor(torch.empty((n, n), dtype=torch.float64, device=dev))
+        X0 = ozr.colmajor(torch.empty((n, n), dtype=torch.float64, device=dev))
+        lam0 = torch.empty(n, dtype=torch.float64, device=dev)
+    if dist_mode:
+        for t_ in (A, X0, lam0):
+            broadcast_tensor(t_, src=0)
+    col0, nl = partition(n, ws, rank)
+    X = ozr.colmajor(X0.clone())
+    lam = lam0.clone()
+    params = ozr.default_params(delta=cfg["delta"])
+    reps = []
+
+    def step():
+        X[:, col0:col0 + nl].copy_(X0[:, col0:col0 + nl])
+        lam.copy_(lam0)
+        return ozr.ozr_refine_step_dist(ctx, comm, A, X, lam, params)
+
+    for _ in range(warmup):
+        step()
+    torch.cuda.synchronize()
+    if dist_mode:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        reps.append(step())
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    if dist_mode:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    del A, X0, X, lam0, lam
+    torch.cuda.empty_cache()
+    r = reps[-1]
+    return {"workload": "c5: " + _describe(cfg, n), "n": n, "n_gpus": ws, "steps": steps, "warmup": warmup,
+            "ms_per_sweep": ms, "value": 6.0 * n ** 3 / (ms / 1e3) / 1e12, "unit": "TFLOP/s",
+            "scaling": "strong", "pair_gemms": r["pairs_V"] + r["pairs_W"] + r["pairs_U"],
+            "note": "one refinement sweep of the whole n = 16384 problem, block columns over the ranks "
+                    "(NCCL all-gather of the X^(1) digit planes per sweep); device time, max over ranks"}
+
+
 def _describe(cfg, n):
     spec = f"geometric cnd={cfg['cnd']:.0e}" if cfg["kind"] == "geometric" else "uniform[-1,1]+64x8 clusters@1e-10"
     return f"n={n} symmetric A=Q diag(lam) Q^T (Haar Q), {spec}, X0 from {cfg['start']} eigensolver, " \
@@ -189,11 +240,53 @@ def emit(obj):
         sys.stdout.flush()
 
 
+def _relaunch_under_torchrun(n):
+    """`python bench.py --gpus N` without a torchrun environment: re-exec this very command line as N
+    ranks (one per GPU) under torch.distributed.run on 127.0.0.1, and return its exit code."""
+    with __import__("socket").socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")  # the communicator lines (nranks) go to stderr for the driver
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    print(f"[bench] launching {n} ranks: {' '.join(cmd)}", file=sys.stderr)
+    return subprocess.call(cmd, env=env)
+
+
+def dry_run(args):
+    """--dry-run: the rank plumbing without a GPU — every rank joins the process group (gloo), computes its
+    block of the partition, and rank 0 checks the all-gathered blocks tile [0, n) and prints one JSON line."""
+    import torch
+    import torch.distributed as dist
+    import workloads as W
+    from paper_2602_19090_b200.dist import partition
+    ws, rank, _ = _dist()
+    if ws > 1:
+        dist.init_process_group("gloo", rank=rank, world_size=ws)
+    n = args.n or W.CONFIGS[args.config]["n"]
+    col0, nl = partition(n, ws, rank)
+    mine = torch.tensor([rank, col0, nl], dtype=torch.int64)
+    parts = [torch.zeros(3, dtype=torch.int64) for _ in range(ws)]
+    if ws > 1:
+        dist.all_gather(parts, mine)
+    else:
+        parts = [mine]
+    blocks = [tuple(int(v) for v in p) for p in parts]
+    ok = [b[0] for b in blocks] == list(range(ws)) and blocks[0][1] == 0 and \
+        all(blocks[i][1] + blocks[i][2] == (blocks[i + 1][1] if i + 1 < ws else n) for i in range(ws))
+    if rank == 0:
+        emit({"dry_run": True, "n_gpus": ws, "gpus_requested": args.gpus, "n": n,
+              "partition": [{"rank": r, "col0": c, "n_local": m} for r, c, m in blocks], "consistent": ok})
+    if ws > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0 if ok else 1
+
+
 def main():
     global _JSON_FD
-    sys.stdout.flush()
-    _JSON_FD = os.dup(1)
-    os.dup2(2, 1)  # C-level prints (NCCL's version banner, ...) must not precede the JSON line
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
@@ -208,7 +301,22 @@ def main():
     ap.add_argument("--truncate", type=int, default=1,
                     help="1: the paper's X̂ → X̂^(1) truncation (default); 0: keep all of X̂ — the untruncated "
                          "two-sided analogue of the prior work the paper compares against (PAPER.md:432-443)")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="rank plumbing only (gloo, no GPU): the partition every rank computes")
+    ap.add_argument("--no-c5", action="store_true", help="skip the c5 (n = 16384) strong-scaling line")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return _relaunch_under_torchrun(args.gpus)
+    ws_env = int(os.environ.get("WORLD_SIZE", "1"))
+    if ws_env != args.gpus:
+        print(f"[bench] --gpus {args.gpus} but WORLD_SIZE={ws_env}: refusing to measure a different rank count",
+              file=sys.stderr)
+        return 2
+    sys.stdout.flush()
+    _JSON_FD = os.dup(1)
+    os.dup2(2, 1)  # C-level prints (NCCL's version banner, ...) must not precede the JSON line
+    if args.dry_run:
+        return dry_run(args)
     if args.impl == "reference":
         return run_reference(args)
 
@@ -357,6 +465,12 @@ def main():
                   "note": "FP32 start: the first sweep's 6628-column group takes the dense sub-solve (cuSOLVER syevd)"}
         del A4, X4, l4, Xw, lw
 
+    # c5 (n = 16384, cnd 1e10, FP64 start, δ = 1e-15): the north star's scaling configuration, the same
+    # block-column partition over the ranks (strong scaling), device time max over ranks
+    c5 = None
+    if not args.no_c5 and name == "c4p" and not args.n:
+        c5 = run_c5(ctx, comm, dist_mode, ws, rank, dev, W, ozr, torch, dist)
+
     # e2e: a stream of independent problems through the public API with HOST (pinned) buffers. Every step
     # copies its A, X̂₀, λ̂₀ in and its X̂, λ̂ out; the copies of the neighbouring steps run on two copy streams
     # while the sweep runs (PCIe is full duplex): device inputs are double-buffered, step k+1's H2D is issued
@@ -447,7 +561,7 @@ def main():
                                                        "pairs_V", "pairs_W", "pairs_U", "n_clusters", "max_cluster")}},
                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                "gpu_launches": int(sum(r["launches"] for r in reps)), "clocks": clocks,
-               "time_to_target": ttt, "time_to_target_c4": ttt_c4}
+               "time_to_target": ttt, "time_to_target_c4": ttt_c4, "c5_strong_scaling": c5}
         emit(out)
     ctx.close()
     if comm is not None:

@@ -114,3 +114,29 @@ def test_broadcast_colmajor_gloo():
     (a0, l0, s0), (a1, l1, s1) = _run(_bcast_colmajor)
     assert np.array_equal(a0, a1) and np.array_equal(l0, l1)
     assert np.array_equal(a1, np.arange(36, dtype=np.float64).reshape(6, 6)) and s1 == (1, 6)
+
+
+def test_bench_gpus_flag_spawns_ranks():
+    """`bench.py --gpus 2` without a torchrun environment re-launches itself as two ranks (here over gloo,
+    --dry-run: no GPU); both ranks agree on the block-column partition of the c4' problem."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--dry-run"],
+                         capture_output=True, text=True, timeout=600, env=env, cwd=root)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    assert line["n_gpus"] == 2 and line["consistent"]
+    assert [(p["col0"], p["n_local"]) for p in line["partition"]] == [(0, 4096), (4096, 4096)]
+
+
+def test_bench_rank_count_mismatch_fails():
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, WORLD_SIZE="1", RANK="0", LOCAL_RANK="0")
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--dry-run"],
+                         capture_output=True, text=True, timeout=300, env=env, cwd=root)
+    assert out.returncode == 2 and "refusing" in out.stderr
