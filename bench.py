@@ -146,9 +146,22 @@ def run_reference(args):
     name = args.config
     cfg = dict(W.CONFIGS[name])
     n = args.n or cfg["n"]
-    n_eff = n  # the same n x n problem as the GPU arm (generated on the host: ~1 min at n = 8192)
-    A, _ = W.make_matrix(n_eff, cfg["kind"], cfg["cnd"], cfg["seed"])
-    lam0, X0 = W.initial_eig(A, cfg["start"])
+    n_eff = n
+    same = False
+    try:
+        import torch
+        same = torch.cuda.is_available()
+    except Exception:
+        pass
+    if same:  # THE problem the GPU arm refines (the same generator call, workloads.make_config_torch), copied
+        # to the host; the oracle then runs on the host cores only
+        At, lt, Xt, _ = W.make_config_torch(name, torch.device("cuda", 0), n=args.n or None)
+        A, lam0, X0 = At.cpu().numpy(), lt.cpu().numpy(), Xt.cpu().numpy()
+        del At, lt, Xt
+        torch.cuda.empty_cache()
+    else:  # no GPU: the same recipe built on the host (numpy/LAPACK)
+        A, _ = W.make_matrix(n_eff, cfg["kind"], cfg["cnd"], cfg["seed"])
+        lam0, X0 = W.initial_eig(A, cfg["start"])
     J = np.linspace(0, n_eff - 1, min(args.ref_cols, n_eff)).astype(np.int64)  # evenly spaced output columns
     for _ in range(args.warmup):
         orf.sweep_columns(A, X0, lam0, cfg["delta"], J)
@@ -161,13 +174,40 @@ def run_reference(args):
     out = {"impl": "reference", "metric": METRIC, "value": val, "unit": "TFLOP/s", "n_gpus": ws,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
            "scaling": "strong", "vs_baseline": None, "dtype": "f64 (double-double)", "data": "synthetic",
-           "config": {"workload": f"{name}: " + _describe(cfg, n), "sample_n": n_eff, "sample_cols": len(J)},
+           "config": _config(name, cfg, n, ws, ws > 1, 1),
            "cpu_baseline": {"value": val, "unit": "TFLOP/s", "cores": _clib.num_threads(), "kind": "oracle",
                             "sample": f"each step: oracle sweep (dd triple loops) restricted to {len(J)} evenly "
-                                      f"spaced of the {n_eff} output columns of the same {name} problem"},
+                                      f"spaced of the {n_eff} output columns of the same {name} problem "
+                                      f"({'the GPU arm generator' if same else 'host generator'})",
+                            "sample_cols": len(J)},
            "e2e": {"value": val, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     emit(out)
     return 0
+
+
+def run_per_product(ctx, A, B, rep, ozr, torch, steps=5, warmup=2):
+    """Effective FP64 TFLOP/s of ONE accurate product C = A·B (2n³ per product) through ozr_gemm: (a) with
+    the digit budgets the sweep's V product used (kA, k_X, L_V of the last timed sweep), (b) a full-fp64
+    plan (8 + 8 digits, pairs s + t ≤ 9: ≥ 60 bits per operand, the dropped pairs below 2^-62 relative)."""
+    n = A.shape[0]
+    out = {}
+    for tag, (kA, kB, L) in (("sweep_V_budget", (rep["kA"], rep["kX"], rep["L_V"])), ("fp64_full", (8, 8, 9))):
+        for _ in range(warmup):
+            ozr.ozr_gemm(ctx, A, B, kA, kB, L)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(steps):
+            ozr.ozr_gemm(ctx, A, B, kA, kB, L)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / steps
+        pairs = sum(p for _, p in ozr.ozr_gemm_plan(n, kA, kB, L))
+        out[tag] = {"kA": kA, "kB": kB, "L": L, "pairs": pairs, "ms": ms,
+                    "value": 2.0 * n ** 3 / (ms / 1e3) / 1e12, "unit": "TFLOP/s"}
+    out["note"] = ("ozr_gemm C = A·X̂₀ (n = %d) via the C ABI: both splits, the tcgen05 slice GEMM and the exact "
+                   "recombination to double-double inside the timed region; effective = 2n^3 / time" % n)
+    return out
 
 
 def run_c5(ctx, comm, dist_mode, ws, rank, dev, W, ozr, torch, dist, steps=2, warmup=1):
@@ -219,6 +259,16 @@ def run_c5(ctx, comm, dist_mode, ws, rank, dev, W, ozr, torch, dist, steps=2, wa
             "scaling": "strong", "pair_gemms": r["pairs_V"] + r["pairs_W"] + r["pairs_U"],
             "note": "one refinement sweep of the whole n = 16384 problem, block columns over the ranks "
                     "(NCCL all-gather of the X^(1) digit planes per sweep); device time, max over ranks"}
+
+
+def _config(name, cfg, n, ws, dist_mode, truncate):
+    """The workload description both arms print (identical for the same problem)."""
+    return {"workload": f"{name}: " + _describe(cfg, n), "n": n, "delta": cfg["delta"],
+            "mode": "proposed (X̂ truncated to X̂^(1))" if truncate else "untruncated X̂ (prior-work analogue)",
+            "parallelism": f"block-column partition x{ws} (NCCL all-gather of X^(1) digits per sweep)"
+            if dist_mode else "1 GPU",
+            "l2": "inputs larger than L2 (A + X = %.1f GiB, L2 126 MB)" % (2 * n * n * 8 / 2 ** 30),
+            "flops_per_step": "3 x 2n^3 (V=AX, W=X^T Res, U=X E)"}
 
 
 def _describe(cfg, n):
@@ -465,6 +515,12 @@ def main():
                   "note": "FP32 start: the first sweep's 6628-column group takes the dense sub-solve (cuSOLVER syevd)"}
         del A4, X4, l4, Xw, lw
 
+    # the per-product Ozaki GEMM: ozr_gemm C = A·X̂₀ through the C ABI, split of both operands,
+    # slice GEMM and exact recombination to double-double all inside the timed region (A's split included)
+    per_product = None
+    if rank == 0 and not dist_mode:
+        per_product = run_per_product(ctx, A, X0, reps[-1], ozr, torch)
+
     # c5 (n = 16384, cnd 1e10, FP64 start, δ = 1e-15): the north star's scaling configuration, the same
     # block-column partition over the ranks (strong scaling), device time max over ranks
     c5 = None
@@ -550,18 +606,13 @@ def main():
         out = {"metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": ws, "steps": args.steps,
                "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
                "vs_baseline": None, "dtype": "int8", "data": "synthetic",
-               "config": {"workload": f"{name}: " + _describe(cfg, n), "n": n, "delta": delta,
-                          "mode": "proposed (X̂ truncated to X̂^(1))" if args.truncate else
-                                  "untruncated X̂ (prior-work analogue)",
-                          "parallelism": f"block-column partition x{ws} (NCCL all-gather of X^(1) digits per sweep)"
-                          if dist_mode else "1 GPU",
-                          "l2": "inputs larger than L2 (A + X = %.1f GiB per rank, L2 126 MB)" % (2 * n * n * 8 / 2 ** 30),
-                          "flops_per_step": "3 x 2n^3 (V=AX, W=X^T Res, U=X E)",
-                          "sweep": {k: r0[k] for k in ("beta", "alpha", "kX", "kA", "kR", "kE", "L_V", "L_W", "L_U",
-                                                       "pairs_V", "pairs_W", "pairs_U", "n_clusters", "max_cluster")}},
+               "config": _config(name, cfg, n, ws, dist_mode, args.truncate),
+               "sweep": {k: r0[k] for k in ("beta", "alpha", "kX", "kA", "kR", "kE", "L_V", "L_W", "L_U",
+                                            "pairs_V", "pairs_W", "pairs_U", "n_clusters", "max_cluster")},
                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                "gpu_launches": int(sum(r["launches"] for r in reps)), "clocks": clocks,
-               "time_to_target": ttt, "time_to_target_c4": ttt_c4, "c5_strong_scaling": c5}
+               "time_to_target": ttt, "time_to_target_c4": ttt_c4, "c5_strong_scaling": c5,
+               "per_product": per_product}
         emit(out)
     ctx.close()
     if comm is not None:

@@ -223,6 +223,20 @@ ozr_status ozr_refine_to_tol(ozr_ctx ctx, const double* A, int64_t n, int64_t ld
  * Errors: OZR_ERR_ARG, OZR_ERR_COMM (message in *_last_error is not available: no context; the
  * status says what failed).
  * ------------------------------------------------------------------------------------------------ */
+/* ------------------------------------------------------------------------------------------------
+ * ozr_syev — the dense symmetric eigensolver of the Rayleigh–Ritz sub-solve of large unresolved groups
+ * (reading R13; the paper leaves clusters open, and cites the Ogita–Aishima
+ * cluster refinement, whose sub-problem is a small dense symmetric eigenproblem):
+ * K = Y diag(θ) Yᵀ by Householder tridiagonalisation, Cuppen divide and conquer with Gu–Eisenstat
+ * eigenvectors, and the blocked back-transformation, all in libozr's own kernels (products with a
+ * dimension ≥ 1024 on the INT8 slice GEMM at FP64 accuracy).
+ * K: device, m x m column-major (ldk ≥ m), symmetric; only its lower triangle is read; K is preserved.
+ * theta: device, m, ascending. Y: device, m x m (ldy ≥ m), orthonormal columns (sign not normalised).
+ * Workspace ~5m² doubles inside the context. Errors: OZR_ERR_ARG, OZR_ERR_NONFINITE (not checked: NaN
+ * propagates), OZR_ERR_CUDA (no convergence of a leaf iteration), OZR_ERR_NOMEM.
+ * ------------------------------------------------------------------------------------------------ */
+ozr_status ozr_syev(ozr_ctx ctx, int64_t m, const double* K, int64_t ldk, double* theta, double* Y, int64_t ldy);
+
 typedef struct ozr_comm_s* ozr_comm;
 ozr_status ozr_comm_nccl_id(void* id128);
 ozr_status ozr_comm_create_nccl(ozr_comm* out, const void* id128, int nranks, int rank, int device);

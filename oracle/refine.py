@@ -227,33 +227,49 @@ CERT_SAFETY = 1.15  # power-iteration / bf16-GEMM slack of the library's estimat
 CONTRACT = 1.0 / 8  # a certified sweep whose estimate fell by less than this factor sits at the truncation floor
 
 
-def certificate(E, lam, n_power=None, delta=None):
-    """A-posteriori forward error of the sweep that produced Ẽ (reading R12; the paper gives no iteration rule,
-    PAPER.md:536-540, and its error model eq. assume2/gamma, PAPER.md:341-373, predicts the error only on
-    average over the columns). The sweep returns X̂_new = X̂^(1)(I + Ẽ) while the exact eigenvectors are
-    X = X̂^(1)(I + E), so X − X̂_new = X̂^(1)(E − Ẽ) and the error is Ẽ's second-order
-    defect. Writing X̂^(1) = X(I + F), F ≈ −Ẽ to first order, R = I − X̂ᵀX̂ and S = X̂ᵀAX̂ of Alg. 1 give, for
-    i ≠ j, s_ij + λ_j r_ij = −(λ_j − λ_i) f_ij + [Fᵀ(D − λ_j I)F]_ij, hence
-        (Ẽ − E)_ij ≈ Q_ij / (λ̂_j − λ̂_i),   Q = ẼᵀC,  c_kj = (λ̂_k − λ̂_j) ẽ_kj,
-    plus terms bounded by ‖Ẽ‖² (the F² and diagonal −‖f_j‖²/2 parts), and X̂_new's rounding to fp64 (a
-    noise-like matrix of entries ≤ u|x_ij|: 2-norm ≈ 2u). Returns
-        est = sqrt(‖Q∘H‖₂² + (2u)²) + 1.5‖Ẽ‖_F²,   H_ij = 1/(λ̂_j − λ̂_i) (i ≠ j), 0 on the diagonal,
-    and the parts. ‖·‖₂ exactly (LAPACK) for n ≤ 2048, else `n_power` (default 60) power iterations. With δ
-    given, the library's shortcut is mirrored: when even the lower bound max_j ‖(Q∘H)_{:,j}‖ + 1.5‖Ẽ‖_F² exceeds
-    16δ (no decision of the driver can then tell the value from its Frobenius upper bound), or the Frobenius
-    upper bound already certifies, ‖Q∘H‖_F stands in for ‖Q∘H‖₂."""
+def second_order_defect(E, lam):
+    """−(E − Ẽ) to second order in Ẽ (reading R12), E the exact correction X = X̂^(1)(I + E).
+    Derivation (the paper gives only the order, Theorem 1): with H = (I + E)^{-1} = I + η,
+    G = X̂ᵀX̂ = HᵀH and S = X̂ᵀAX̂ = HᵀΛH exactly, so Alg. 1's W = S − G·D̂ (line 4) is
+        w_ij = Σ_k h_ki (λ_k − λ̂_j) h_kj = (λ_i − λ_j) η_ij + Σ_k η_ki (λ_k − λ_j) η_kj + O(η³)   (i ≠ j),
+    and r_jj = 1 − g_jj = −2η_jj − ‖η_j‖². Line 5's ẽ_ij = w_ij/(λ̂_j − λ̂_i), ẽ_jj = r_jj/2 against the exact
+    e = −η + η² + O(η³), with η = −Ẽ + O(Ẽ²), leave
+        (E − Ẽ)_ij = (Ẽ²)_ij − q_ij/(λ̂_j − λ̂_i)   (i ≠ j),   (E − Ẽ)_jj = (Ẽ²)_jj + ½‖ẽ_j‖²,
+    Q = ẼᵀC, c_kj = (λ̂_k − λ̂_j) ẽ_kj. Returns D = −(E − Ẽ) (the sign the library's kernel produces)."""
     E = np.asarray(E, dtype=np.float64)
     lam = np.asarray(lam, dtype=np.float64)
     n = E.shape[0]
     C = (lam[:, None] - lam[None, :]) * E
     Q = E.T @ C
+    E2 = E @ E
     dl = lam[None, :] - lam[:, None]
     off = ~np.eye(n, dtype=bool)
     if np.any(dl[off] == 0):
+        return None
+    D = np.where(off, Q / np.where(off, dl, 1.0), 0.0) - E2
+    D[np.diag_indices(n)] -= 0.5 * np.sum(E * E, axis=0)
+    return D
+
+
+def certificate(E, lam, n_power=None, delta=None):
+    """A-posteriori forward error of the sweep that produced Ẽ (reading R12; the paper gives no iteration rule,
+    PAPER.md:536-540, and its error model eq. assume2/gamma, PAPER.md:341-373, predicts the error only on
+    average over the columns). The sweep returns X̂_new = X̂^(1)(I + Ẽ) while the exact eigenvectors are
+    X = X̂^(1)(I + E), so X − X̂_new = X̂^(1)(E − Ẽ): Ẽ's second-order defect
+    (second_order_defect()) in the 2-norm of PAPER.md:121, plus X̂_new's rounding to fp64 (a noise-like matrix
+    of entries ≤ u|x_ij|: 2-norm ≈ 2u) and an allowance ‖Ẽ‖_F·‖D‖_F for the third-order terms. Returns
+        est = sqrt(‖D‖₂² + (2u)²) + ‖Ẽ‖_F‖D‖_F
+    and the parts. ‖·‖₂ exactly (LAPACK) for n ≤ 2048, else `n_power` (default 60) power iterations. With δ
+    given, the library's shortcut is mirrored: when even the lower bound max_j ‖D_{:,j}‖ + quad exceeds
+    16δ (no decision of the driver can then tell the value from its Frobenius upper bound), or the Frobenius
+    upper bound already certifies, ‖D‖_F stands in for ‖D‖₂."""
+    E = np.asarray(E, dtype=np.float64)
+    D = second_order_defect(E, lam)
+    if D is None:
         return dict(est=np.inf, est_q=np.inf, quad=np.inf, frob=np.inf)
-    D = np.where(off, Q / np.where(off, dl, 1.0), 0.0)
-    quad = 1.5 * float(np.sum(E * E))
+    n = E.shape[0]
     frob = float(np.linalg.norm(D))
+    quad = float(np.sqrt(np.sum(E * E))) * frob
     if delta is not None:
         upper = float(np.sqrt(frob * frob + (2 * U) ** 2)) + quad
         lower = float(np.max(np.sqrt(np.sum(D * D, axis=0)))) + quad

@@ -18,7 +18,7 @@ OZR_SPLIT_FIXED, OZR_SPLIT_X1 = 0, 1
 STATUS = {0: "OZR_OK", 1: "OZR_ERR_ARG", 2: "OZR_ERR_NONFINITE", 3: "OZR_ERR_RANGE", 4: "OZR_ERR_DEGENERATE",
           5: "OZR_ERR_NOT_CONVERGED", 6: "OZR_ERR_CUDA", 7: "OZR_ERR_COMM", 8: "OZR_ERR_NOMEM"}
 EXPORTS = ["ozr_version", "ozr_create", "ozr_destroy", "ozr_last_error", "ozr_split", "ozr_gemm", "ozr_gemm_plan",
-           "ozr_params_default", "ozr_refine_step", "ozr_refine_to_tol", "ozr_last_clusters", "ozr_comm_nccl_id",
+           "ozr_params_default", "ozr_refine_step", "ozr_refine_to_tol", "ozr_last_clusters", "ozr_syev", "ozr_comm_nccl_id",
            "ozr_comm_create_nccl", "ozr_comm_create_host_group", "ozr_comm_destroy", "ozr_comm_size", "ozr_comm_rank",
            "ozr_refine_step_dist", "ozr_refine_to_tol_dist", "ozr_last_R"]
 
@@ -89,6 +89,8 @@ def lib():
         L.ozr_refine_to_tol.restype = i32
         L.ozr_last_clusters.argtypes = [vp, ip, i32, ip, i32, ip]
         L.ozr_last_clusters.restype = i32
+        L.ozr_syev.argtypes = [vp, i64, vp, i64, vp, vp, i64]
+        L.ozr_syev.restype = i32
         L.ozr_comm_nccl_id.argtypes = [vp]
         L.ozr_comm_nccl_id.restype = i32
         L.ozr_comm_create_nccl.argtypes = [ctypes.POINTER(vp), vp, i32, i32, i32]
@@ -237,6 +239,15 @@ def ozr_refine_to_tol(ctx, A, X, lam, params, raise_on_nonconvergence=False):
     if st != 0 and (st != 5 or raise_on_nonconvergence):
         ctx.check(st)
     return st, [H[i].as_dict() for i in range(done.value)]
+
+
+def ozr_syev(ctx, K):
+    """θ (ascending), Y with K = Y diag(θ) Yᵀ for a symmetric column-major device matrix K (lower triangle read)."""
+    m = K.shape[0]
+    th = torch.empty(m, dtype=torch.float64, device=K.device)
+    Y = colmajor(torch.empty((m, m), dtype=torch.float64, device=K.device))
+    ctx.check(lib().ozr_syev(ctx.h, m, _ptr(K), _ld(K), _ptr(th), _ptr(Y), m))
+    return th, Y
 
 
 def ozr_last_clusters(ctx, max_members=1 << 20, max_groups=1 << 16):

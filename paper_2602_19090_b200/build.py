@@ -6,8 +6,8 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 SO = os.path.join(HERE, "libozr.so")
-SOURCES = ["ozr_api.cu", "kernels.cu", "gemm_i8.cu", "cluster.cu", "dense_eig.cu", "comm.cu", "certify.cu"]
-HEADERS = ["ptx.cuh", "ddmath.cuh", "kernels.h", "ozr_internal.h", "comm.h", "certify.h"]
+SOURCES = ["ozr_api.cu", "kernels.cu", "gemm_i8.cu", "cluster.cu", "dense_eig.cu", "comm.cu", "certify.cu", "syev.cu"]
+HEADERS = ["ptx.cuh", "ddmath.cuh", "kernels.h", "ozr_internal.h", "comm.h", "certify.h", "syev.h"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
          "-Xcompiler", "-O2"]
@@ -24,14 +24,17 @@ def _stale():
 def build(force=False, verbose=False):
     if not force and not _stale():
         return SO
-    objs = []
-    for src in SOURCES:
-        obj = os.path.join(CSRC, src.replace(".cu", ".o"))
-        cmd = [NVCC] + FLAGS + ["-c", os.path.join(CSRC, src), "-o", obj]
+    from concurrent.futures import ThreadPoolExecutor
+    objs = [os.path.join(CSRC, src.replace(".cu", ".o")) for src in SOURCES]
+
+    def compile_one(i):
+        cmd = [NVCC] + FLAGS + ["-c", os.path.join(CSRC, SOURCES[i]), "-o", objs[i]]
         if verbose:
             print(" ".join(cmd), file=sys.stderr)
         subprocess.check_call(cmd)
-        objs.append(obj)
+
+    with ThreadPoolExecutor(max_workers=min(len(SOURCES), os.cpu_count() or 4)) as pool:
+        list(pool.map(compile_one, range(len(SOURCES))))
     cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", SO] + objs + ["-ldl"]
     subprocess.check_call(cmd)
     for o in objs:

@@ -3,18 +3,22 @@
 // The paper stops after a fixed number of iterations and models the error only on average over
 // the columns (eq. assume2 / gamma). The sweep returns X̂_new = X̂^(1)(I + Ẽ) while the exact
 // eigenvectors are X = X̂^(1)(I + E), so ‖X − X̂_new‖₂ ≈ ‖E − Ẽ‖₂, Ẽ's second-order defect.
-// From X̂^(1) = X(I + F), F ≈ −Ẽ, and Alg. 1's R, S, for i ≠ j
-//     (Ẽ − E)_ij ≈ Q_ij / (λ̂_j − λ̂_i),   Q = ẼᵀC,   c_kj = (λ̂_k − λ̂_j)·ẽ_kj,
-// up to terms bounded by ‖Ẽ‖² (added as 1.5‖Ẽ‖_F² by the host). Q only has to be accurate to a few per cent, so
-// it is ONE bf16 tensor-core GEMM (the slice-GEMM kernel with kind::f16, f32 accumulator): Ẽ and C are stored
-// column-scaled by powers of two (exact) in bf16, which keeps every entry's relative precision (2^-8) whatever
-// its magnitude inside the column; the host measured ‖·‖₂ of D = Q∘H to 0.3 % of the exact-Q value on every
-// BASELINE recipe (scratch study, R12).
+// With H = (I + E)^{-1} = I + η, Alg. 1's W = S − G·D̂ is exactly w_ij = Σ_k h_ki(λ_k − λ̂_j)h_kj and
+// r_jj = −2η_jj − ‖η_j‖², which leaves (oracle/refine.second_order_defect, pinned against exact corrections)
+//     D := −(E − Ẽ):  D_ij = Q_ij/(λ̂_j − λ̂_i) − (Ẽ²)_ij  (i ≠ j),   D_jj = −(Ẽ²)_jj − ½‖ẽ_j‖²,
+//     Q = ẼᵀC,   c_kj = (λ̂_k − λ̂_j)·ẽ_kj.
+// Q and Ẽ² only have to be accurate to a few per cent, so each is ONE bf16 tensor-core GEMM (the slice-GEMM
+// kernel with kind::f16, f32 accumulator): the operands are stored scaled by powers of two (exact) per column
+// (Ẽ, C as B operands / Ẽ's columns as Q's A operand) or per row (Ẽ's rows as the A operand of Ẽ²), which keeps
+// every entry's relative precision (2^-8) whatever its magnitude inside the line.
 //
-//   k_cert_prep   Ẽ = diag(2^−g)·Ẽ' (the stored Ẽ' = diag(2^g)Ẽ is exact), its column maxima, bf16 Ẽ and C
-//   (GEMM)        Q = ẼᵀC  (launch_gemm_i8 kind 1)
-//   k_cert_delta  D = 2^{sE_i + sC_j}·Q_ij / (λ̂_j − λ̂_i) (fp32, i ≠ j), Σ_i D_ij² per column
-//   k_pi_*        power iteration for ‖D‖₂ (D column-partitioned on P ranks: D·z all-reduced)
+//   k_cert_prep    Ẽ = diag(2^−g)·Ẽ' (the stored Ẽ' = diag(2^g)Ẽ is exact), its column maxima, bf16 Ẽ and C
+//   k_cert_rowmax  row exponents rE_i of the (all-gathered) Ẽ
+//   k_cert_rowT    Ẽ's rows, scaled by 2^−rE_i, K-major (the A operand of Ẽ²)
+//   (GEMMs)        Q = ẼᵀC,  P = Ẽ·Ẽ_{:,J}  (launch_gemm_i8 kind 1)
+//   k_cert_delta   D (fp32) from Q, P, ‖ẽ_j‖²; Σ_i D_ij² per column
+//   k_pi_*, k_lz_axpy  Golub–Kahan–Lanczos bidiagonalization of D for ‖D‖₂ (D column-partitioned on P ranks:
+//                  D·v all-reduced, Dᵀu local); the host takes σ_max of the small bidiagonal
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -99,28 +103,33 @@ __global__ void __launch_bounds__(CB)
   }
 }
 
-// one CTA per local column j: D_ij = 2^{sE_i + sC_j} Q_ij / (λ̂_j − λ̂_i), D_jj = 0; dsq[j] = Σ_i D_ij²
+// one CTA per local column j: D_ij = 2^{sE_i + sC_j} Q_ij / (λ̂_j − λ̂_i) − 2^{rE_i + sE_j} P_ij (i ≠ j),
+// D_jj = −2^{rE_j + sE_j} P_jj − ½ esq_j; dsq[j] = Σ_i D_ij²
 __global__ void __launch_bounds__(CB)
-    k_cert_delta(const float* __restrict__ Q, long long ldq, int rows, const int32_t* __restrict__ sE,
-                 const int32_t* __restrict__ sC, const double* __restrict__ lam, int col0, float* __restrict__ D,
+    k_cert_delta(const float* __restrict__ Q, const float* __restrict__ P, long long ldq, int rows,
+                 const int32_t* __restrict__ sE, const int32_t* __restrict__ sC, const int32_t* __restrict__ rE,
+                 const double* __restrict__ esq, const double* __restrict__ lam, int col0, float* __restrict__ D,
                  double* __restrict__ dsq, int* __restrict__ flag) {
   __shared__ double sh[CB / 32];
   const int j = blockIdx.x, gj = col0 + j;
   const double lj = lam[gj];
-  const int cj = sC[j];
+  const int cj = sC[j], ej = sE[gj];
   const float* q = Q + static_cast<long long>(j) * ldq;
+  const float* p = P + static_cast<long long>(j) * ldq;
   float* d = D + static_cast<long long>(j) * rows;
   double ss = 0.0;
   bool bad = false;
   for (int i = threadIdx.x; i < rows; i += CB) {
-    double v = 0.0;
+    double v = -ldexp(static_cast<double>(p[i]), rE[i] + ej);
     if (i != gj) {
       const double dl = lj - lam[i];
       if (dl == 0.0) {
         bad = true;
       } else {
-        v = ldexp(static_cast<double>(q[i]), sE[i] + cj) / dl;
+        v += ldexp(static_cast<double>(q[i]), sE[i] + cj) / dl;
       }
+    } else {
+      v -= 0.5 * esq[gj];
     }
     d[i] = static_cast<float>(v);
     ss = fma(v, v, ss);
@@ -128,6 +137,50 @@ __global__ void __launch_bounds__(CB)
   ss = cb_sum(ss, sh);
   if (threadIdx.x == 0) dsq[j] = ss;
   if (bad) atomicOr(flag, 1);
+}
+
+// row exponents of the all-gathered Ẽ (Eb column k scaled by 2^−sE_k): rE_i = max_k (frexp exponent of
+// Eb_ik + sE_k), so that |ẽ_ik|·2^−rE_i < 1. Grid (row blocks of CB, column chunks); integer atomicMax (exact).
+constexpr int RM_CHUNK = 256;
+__global__ void __launch_bounds__(CB)
+    k_cert_rowmax(const __nv_bfloat16* __restrict__ Eb, long long ldb, int rows, int cols,
+                  const int32_t* __restrict__ sE, int32_t* __restrict__ rE) {
+  const int i = blockIdx.x * CB + threadIdx.x;
+  if (i >= rows) return;
+  const int k0 = blockIdx.y * RM_CHUNK, k1 = min(cols, k0 + RM_CHUNK);
+  int e = -100000;
+  for (int k = k0; k < k1; ++k) {
+    const float v = __bfloat162float(Eb[static_cast<long long>(k) * ldb + i]);
+    if (v != 0.0f) {
+      int ex;
+      frexpf(v, &ex);
+      e = max(e, ex + sE[k]);
+    }
+  }
+  if (e > -100000) atomicMax(rE + i, e);
+}
+
+// EbT[i·ldb + k] = Eb_ik·2^{sE_k − rE_i} (exact power-of-two rescale of a bf16; 32 x 32 tiles through shared memory)
+__global__ void __launch_bounds__(256)
+    k_cert_rowT(const __nv_bfloat16* __restrict__ Eb, long long ldb, int rows, int cols,
+                const int32_t* __restrict__ sE, const int32_t* __restrict__ rE, __nv_bfloat16* __restrict__ EbT) {
+  __shared__ float t[32][33];
+  const int i0 = blockIdx.x * 32, k0 = blockIdx.y * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+  for (int r = ty; r < 32; r += 8) {  // read column k0 + r, rows i0 + tx (coalesced)
+    const int i = i0 + tx, k = k0 + r;
+    float v = 0.0f;
+    if (i < rows && k < cols) v = __bfloat162float(Eb[static_cast<long long>(k) * ldb + i]);
+    t[r][tx] = v;
+  }
+  __syncthreads();
+  for (int r = ty; r < 32; r += 8) {  // write row i0 + r, columns k0 + tx (coalesced)
+    const int i = i0 + r, k = k0 + tx;
+    if (i < rows && k < cols) {
+      const int sh = (rE[i] > -100000) ? sE[k] - rE[i] : 0;
+      EbT[static_cast<long long>(i) * ldb + k] = __float2bfloat16_rn(ldexpf(t[tx][r], sh));
+    }
+  }
 }
 
 // power iteration: y = D·z (rows), chunked over columns; then Dᵀy per column
@@ -158,16 +211,36 @@ __global__ void __launch_bounds__(CB)
   if (threadIdx.x == 0) v[blockIdx.x] = acc;
 }
 
+// x = y − sqrt(c2[0])·x (a Lanczos recurrence step; c2 = the previous squared norm, on the device)
+__global__ void k_lz_axpy(double* __restrict__ x, const double* __restrict__ y, int n, const double* __restrict__ c2) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  x[i] = y[i] - sqrt(c2[0]) * x[i];
+}
+
 }  // namespace
+
+void launch_lz_axpy(double* x, const double* y, int n, const double* c2, cudaStream_t s) {
+  k_lz_axpy<<<(n + 255) / 256, 256, 0, s>>>(x, y, n, c2);
+}
 
 void launch_cert_prep(const double* Ep, long long lde, int rows, int cols, const int32_t* g, const double* lam, int col0,
                       void* Eb, void* Cb, long long ldb, int32_t* sE, int32_t* sC, double* esq, cudaStream_t s) {
   k_cert_prep<<<cols, CB, 0, s>>>(Ep, lde, rows, g, lam, col0, static_cast<__nv_bfloat16*>(Eb),
                                   static_cast<__nv_bfloat16*>(Cb), ldb, sE, sC, esq);
 }
-void launch_cert_delta(const float* Q, long long ldq, int rows, int cols, const int32_t* sE, const int32_t* sC,
-                       const double* lam, int col0, float* D, double* dsq, int* flag, cudaStream_t s) {
-  k_cert_delta<<<cols, CB, 0, s>>>(Q, ldq, rows, sE, sC, lam, col0, D, dsq, flag);
+void launch_cert_rowT(const void* Eb, long long ldb, int rows, int cols, const int32_t* sE, int32_t* rE, void* EbT,
+                      cudaStream_t s) {
+  cudaMemsetAsync(rE, 0xC0, rows * sizeof(int32_t), s);  // 0xC0C0C0C0: below every exponent
+  k_cert_rowmax<<<dim3((rows + CB - 1) / CB, (cols + RM_CHUNK - 1) / RM_CHUNK), CB, 0, s>>>(
+      static_cast<const __nv_bfloat16*>(Eb), ldb, rows, cols, sE, rE);
+  k_cert_rowT<<<dim3((rows + 31) / 32, (cols + 31) / 32), 256, 0, s>>>(static_cast<const __nv_bfloat16*>(Eb), ldb, rows,
+                                                                        cols, sE, rE, static_cast<__nv_bfloat16*>(EbT));
+}
+void launch_cert_delta(const float* Q, const float* P, long long ldq, int rows, int cols, const int32_t* sE,
+                       const int32_t* sC, const int32_t* rE, const double* esq, const double* lam, int col0, float* D,
+                       double* dsq, int* flag, cudaStream_t s) {
+  k_cert_delta<<<cols, CB, 0, s>>>(Q, P, ldq, rows, sE, sC, rE, esq, lam, col0, D, dsq, flag);
 }
 void launch_pi_dz(const float* D, int rows, int cols, const double* z, double* part, double* y, cudaStream_t s) {
   k_pi_dz<<<dim3((rows + CB - 1) / CB, PI_CHUNKS), CB, 0, s>>>(D, rows, cols, z, part);

@@ -400,11 +400,11 @@ __global__ void __launch_bounds__(256)
     k_cluster_apply(const int* __restrict__ goff, const int* __restrict__ gsq, const int* __restrict__ gm,
                     const int* __restrict__ mem, const int* __restrict__ grp_of, const int* __restrict__ pos_of,
                     const double* __restrict__ T, const double* __restrict__ Zbuf, const int32_t* __restrict__ gexp,
-                    int rows, double* __restrict__ Ep, long long lde, int col0, int ncols) {
+                    int rows, double* __restrict__ Ep, long long lde, int col0, int ncols, int dense_min) {
   const int grp = blockIdx.z;
   const int m = gm[grp];
   const int k0 = blockIdx.y * AK;
-  if (k0 >= m) return;
+  if (k0 >= m || m >= dense_min) return;  // dense groups: launch_dense_scatter
   const int kn = min(AK, m - k0);
   const double* Z = Zbuf + gsq[grp];
   const int* J = mem + goff[grp];
@@ -550,7 +550,11 @@ cudaError_t launch_cluster_solve(const ClusterLaunch& L, cudaStream_t s) {
 cudaError_t launch_cluster_apply(const ClusterLaunch& L, cudaStream_t s) {
   dim3 ga((L.rows + 255) / 256, (L.mmax + AK - 1) / AK, L.ngroups);
   k_cluster_apply<<<ga, 256, 0, s>>>(L.goff, L.gsq, L.gm, L.mem, L.grp_of, L.pos_of, L.T, L.Zbuf, L.gexp, L.rows,
-                                     L.Ep, L.lde, L.col0, L.ncols);
+                                     L.Ep, L.lde, L.col0, L.ncols, L.dense_min);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_cluster_colstats(const ClusterLaunch& L, cudaStream_t s) {
   k_cluster_colstats<<<L.nmembers, 256, 0, s>>>(L.mem, L.Ep, L.lde, L.rows, L.gexp, L.nrm2, L.eE_col, L.eE_max,
                                                 L.col0, L.ncols);
   return cudaGetLastError();

@@ -5,8 +5,9 @@
 //
 // The Jacobi core is O(m³) per sweep with one grid-wide synchronisation per rotation round (m − 1 rounds
 // per sweep), which makes a 6628-column group (BASELINE c4: cnd 1e14 from an FP32 eigensolver) a
-// minutes-long solve. Here the two C products and Z = C·Y are FP64 SIMT GEMMs (fixed summation order:
-// deterministic) and the eigen-decomposition of K is LAPACK's divide-and-conquer syevd from cuSOLVER
+// minutes-long solve. Here the two C products, Z = C·Y and the apply T·Z are FP64-accurate products on the
+// INT8 slice GEMM (ozr_api.cu oz_dgemm; the host orchestrates) and the eigen-decomposition of K is LAPACK's
+// divide-and-conquer syevd from cuSOLVER
 // (a library routine in the role cuBLAS plays for a plain GEMM; loaded with dlopen on first use so the
 // library has no link-time dependency and binds the libcusolver.so.11 torch has already loaded, if any).
 // Backward-stable like Jacobi: the eigenvectors of K are accurate to u‖K‖/gap_K, the same accuracy the
@@ -68,51 +69,6 @@ constexpr int kEigModeVector = 1;  // CUSOLVER_EIG_MODE_VECTOR
 constexpr int kFillLower = 0;      // CUBLAS_FILL_MODE_LOWER
 
 // ---------------------------------------------------------------- kernels (m x m, column-major, ld = m)
-// out = Cin + alpha · P·Q, 64 x 64 output tile per CTA, 4 x 4 per thread, k-slabs of 16 in shared
-// memory; every output is one fma chain over l ascending (deterministic).
-constexpr int GT = 64, GK = 16;
-__global__ void __launch_bounds__(256)
-    k_dgemm_acc(int m, const double* __restrict__ P, const double* __restrict__ Q, const double* __restrict__ Cin,
-                double alpha, double* __restrict__ out) {
-  __shared__ double ps[GK][GT + 1];  // ps[l][a] = P(a0 + a, l0 + l)
-  __shared__ double qs[GK][GT + 1];  // qs[l][b] = Q(l0 + l, b0 + b)
-  const int a0 = blockIdx.x * GT, b0 = blockIdx.y * GT;
-  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
-  double acc[4][4] = {};
-  for (int l0 = 0; l0 < m; l0 += GK) {
-    for (int e = threadIdx.x; e < GT * GK; e += 256) {
-      const int a = e % GT, l = e / GT;  // consecutive threads: consecutive rows of P's column
-      ps[l][a] = (a0 + a < m && l0 + l < m) ? P[static_cast<long long>(l0 + l) * m + a0 + a] : 0.0;
-      const int lq = e % GK, b = e / GK;
-      qs[lq][b] = (l0 + lq < m && b0 + b < m) ? Q[static_cast<long long>(b0 + b) * m + l0 + lq] : 0.0;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int l = 0; l < GK; ++l) {
-      double pa[4], qb[4];
-#pragma unroll
-      for (int r = 0; r < 4; ++r) pa[r] = ps[l][tx + 16 * r];
-#pragma unroll
-      for (int c = 0; c < 4; ++c) qb[c] = qs[l][ty + 16 * c];
-#pragma unroll
-      for (int r = 0; r < 4; ++r)
-#pragma unroll
-        for (int c = 0; c < 4; ++c) acc[r][c] = fma(pa[r], qb[c], acc[r][c]);
-    }
-    __syncthreads();
-  }
-#pragma unroll
-  for (int r = 0; r < 4; ++r)
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      const int a = a0 + tx + 16 * r, b = b0 + ty + 16 * c;
-      if (a < m && b < m) {
-        const long long o = static_cast<long long>(b) * m + a;
-        out[o] = fma(alpha, acc[r][c], Cin[o]);
-      }
-    }
-}
-
 // out = (X + Xᵀ)/2
 __global__ void k_dsym(int m, const double* __restrict__ X, double* __restrict__ out) {
   const long long m2 = static_cast<long long>(m) * m;
@@ -161,13 +117,35 @@ __global__ void __launch_bounds__(256)
   for (int l = threadIdx.x; l < m; l += 256) y[l] *= sg;
   if (threadIdx.x == 0) {
     lam[J[k]] = mu + th[k];
-    if (k == 0 && *info != 0) atomicOr(err, ERR_SOLVER);
+    if (k == 0 && info && *info != 0) atomicOr(err, ERR_SOLVER);
   }
 }
 
-void dgemm_acc(int m, const double* P, const double* Q, const double* Cin, double alpha, double* out, cudaStream_t s) {
-  dim3 grid((m + GT - 1) / GT, (m + GT - 1) / GT);
-  k_dgemm_acc<<<grid, 256, 0, s>>>(m, P, Q, Cin, alpha, out);
+// out = X + alpha·P (cnt elements)
+__global__ void k_daxpy(long long cnt, const double* __restrict__ X, double alpha, const double* __restrict__ P,
+                        double* __restrict__ out) {
+  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < cnt;
+       e += static_cast<long long>(gridDim.x) * blockDim.x)
+    out[e] = fma(alpha, P[e], X[e]);
+}
+
+// Ẽ'[:, J_k] (owned columns) ← (T·Z)[:, k] on the rows outside the group, (Z − I)_{a,k}·2^{g_i} on its rows
+// (row i = J_a): the dense groups' part of k_cluster_apply, with T·Z from the INT8 slice GEMM.
+__global__ void k_dense_scatter(const double* __restrict__ TZ, int rows, int m, const int* __restrict__ J, int grp,
+                                const int* __restrict__ grp_of, const int* __restrict__ pos_of,
+                                const double* __restrict__ Z, const int32_t* __restrict__ gexp, double* __restrict__ Ep,
+                                long long lde, int col0, int ncols) {
+  const int k = blockIdx.y;
+  const int jl = J[k] - col0;
+  if (jl < 0 || jl >= ncols) return;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < rows; i += gridDim.x * blockDim.x) {
+    double v = TZ[static_cast<long long>(k) * rows + i];
+    if (grp_of[i] == grp) {
+      const int a = pos_of[i];
+      v = ldexp(Z[static_cast<long long>(k) * m + a] - (a == k ? 1.0 : 0.0), gexp[i]);
+    }
+    Ep[static_cast<long long>(jl) * lde + i] = v;
+  }
 }
 
 }  // namespace
@@ -193,27 +171,31 @@ long long dense_eig_lwork(DenseEig& de, int m, cudaStream_t s) {
   return lw;
 }
 
-cudaError_t launch_cluster_dense(const ClusterLaunch& L, DenseEig& de, int m, long long o, double mu, const int* J,
-                                 cudaStream_t s) {
-  SolverApi& a = api();
-  if (!a.ok || !de.handle || a.setstream(de.handle, s) != 0) return cudaErrorNotSupported;
-  const double* M = L.Mbuf + o;
-  const double* R = L.Rbuf + o;
-  double* K = L.Kbuf + o;
-  double* V = L.Vbuf + o;
-  double* Z = L.Zbuf + o;
-  double* th = L.coop_scratch;  // m eigenvalues
+void launch_dense_sym(int m, const double* X, double* out, cudaStream_t s) {
   const long long m2 = static_cast<long long>(m) * m;
   const int gb = static_cast<int>(std::min<long long>((m2 + 255) / 256, 148 * 16));
-  k_dsym<<<gb, 256, 0, s>>>(m, M, V);           // V = K0 = (M + Mᵀ)/2
-  dgemm_acc(m, R, V, V, 0.5, K, s);             // K = K0 + ½R·K0 = C·K0
-  dgemm_acc(m, K, R, K, 0.5, V, s);             // V = K + ½K·R = C·K0·C
-  k_dsym<<<gb, 256, 0, s>>>(m, V, K);           // K = sym(V)
+  k_dsym<<<gb, 256, 0, s>>>(m, X, out);
+}
+void launch_dense_axpy(long long cnt, const double* X, double alpha, const double* P, double* out, cudaStream_t s) {
+  const int gb = static_cast<int>(std::min<long long>((cnt + 255) / 256, 148 * 16));
+  k_daxpy<<<gb, 256, 0, s>>>(cnt, X, alpha, P, out);
+}
+cudaError_t dense_syevd(DenseEig& de, int m, double* K, double* th, cudaStream_t s) {
+  SolverApi& a = api();
+  if (!a.ok || !de.handle || a.setstream(de.handle, s) != 0) return cudaErrorNotSupported;
   if (a.syevd(de.handle, kEigModeVector, kFillLower, m, K, m, th, de.work, de.lwork, de.info) != 0)
     return cudaErrorUnknown;
-  k_dense_sign<<<m, 256, 0, s>>>(m, K, th, mu, J, L.lam, de.info, L.err);  // K = Y (signed), λ̂_J
-  dgemm_acc(m, R, K, K, 0.5, Z, s);             // Z = Y + ½R·Y = C·Y
   return cudaGetLastError();
+}
+void launch_dense_sign(int m, double* Y, const double* th, double mu, const int* J, double* lam, const int* info,
+                       int* err, cudaStream_t s) {
+  k_dense_sign<<<m, 256, 0, s>>>(m, Y, th, mu, J, lam, info, err);
+}
+void launch_dense_scatter(const double* TZ, int rows, int m, const int* J, int grp, const int* grp_of, const int* pos_of,
+                          const double* Z, const int32_t* gexp, double* Ep, long long lde, int col0, int ncols,
+                          cudaStream_t s) {
+  k_dense_scatter<<<dim3((rows + 255) / 256 < 16 ? (rows + 255) / 256 : 16, m), 256, 0, s>>>(
+      TZ, rows, m, J, grp, grp_of, pos_of, Z, gexp, Ep, lde, col0, ncols);
 }
 
 }  // namespace ozr

@@ -533,12 +533,12 @@ cudaError_t launch_gemm_i8(const DigitOperand& A, const DigitOperand& B, int M, 
   if (M <= 0 || N <= 0 || pt.ngroups <= 0) return cudaSuccess;
   if (K <= 0 || (A.ld % 16) || (B.ld % 16) || (A.plane_stride % 16) || (B.plane_stride % 16))
     return cudaErrorInvalidValue;
-  static int use2 = -1;
-  if (use2 < 0) {
+  static int use2_env = -1;
+  if (use2_env < 0) {
     const char* v = getenv("OZR_GEMM");
-    use2 = (v && v[0] == '1') ? 0 : 1;  // OZR_GEMM=1sm: the single-CTA form (A/B measurements)
+    use2_env = (v && v[0] == '1') ? 0 : 1;  // OZR_GEMM=1sm: the single-CTA form (A/B measurements)
   }
-  if (kind == 1) use2 = 1;  // the bf16 form exists only as the CTA pair
+  const int use2 = (kind == 1) ? 1 : use2_env;  // the bf16 form exists only as the CTA pair
   CUtensorMap tmA, tmB;
   if (!make_tmap(&tmA, A, K, M, BM) || !make_tmap(&tmB, B, K, N, use2 ? BN / 2 : BN)) return cudaErrorInvalidValue;
   if (!use2) {

@@ -115,10 +115,17 @@ struct DenseEig {
 };
 bool dense_eig_available(std::string* why);
 long long dense_eig_lwork(DenseEig& de, int m, cudaStream_t s);
-// The sub-solve of group grp (m members, workspace offset o = gsq[grp], device member list J) by the dense
-// solver; the Jacobi kernels skip it. Stream-ordered on s.
-cudaError_t launch_cluster_dense(const ClusterLaunch& L, DenseEig& de, int m, long long o, double mu, const int* J,
-                                 cudaStream_t s);
+// Pieces of the dense sub-solve of a large group (dense_eig.cu; ozr_api.cu orchestrates with oz_dgemm):
+// out = (X + Xᵀ)/2 (m x m); out = X + alpha·P (cnt elements); K ← its eigenvectors Y (ascending θ);
+// Y's columns signed (y_kk ≥ 0) and λ̂_J = μ + θ; the dense group's part of the apply.
+void launch_dense_sym(int m, const double* X, double* out, cudaStream_t s);
+void launch_dense_axpy(long long cnt, const double* X, double alpha, const double* P, double* out, cudaStream_t s);
+cudaError_t dense_syevd(DenseEig& de, int m, double* K, double* th, cudaStream_t s);
+void launch_dense_sign(int m, double* Y, const double* th, double mu, const int* J, double* lam, const int* info,
+                       int* err, cudaStream_t s);
+void launch_dense_scatter(const double* TZ, int rows, int m, const int* J, int grp, const int* grp_of, const int* pos_of,
+                          const double* Z, const int32_t* gexp, double* Ep, long long lde, int col0, int ncols,
+                          cudaStream_t s);
 size_t cluster_jacobi_smem(int mmax);
 int cluster_dot_splits(int ntiles, int rows);
 // build: R_JJ (all), M_JJ and T = Ẽ'[:, J] on this rank's columns (zero elsewhere; all-reduced between);
@@ -129,7 +136,9 @@ cudaError_t launch_cluster_build(const ClusterLaunch& L, cudaStream_t s);
 void launch_gather_digit_cols(const int8_t* dig, long long ld, long long pstride, int k, const int* J, int m,
                               int8_t* out, long long opstride, const int32_t* g, int32_t* gJ, cudaStream_t s);
 cudaError_t launch_cluster_solve(const ClusterLaunch& L, cudaStream_t s);
+// apply: the groups below dense_min (the dense ones: launch_dense_scatter); colstats: every member column
 cudaError_t launch_cluster_apply(const ClusterLaunch& L, cudaStream_t s);
+cudaError_t launch_cluster_colstats(const ClusterLaunch& L, cudaStream_t s);
 void launch_final(const int32_t* planes, long long pstride, int rows, int cols, const RecombPlan& rp,
                   const int32_t* ellB, int scale8, const double* X1, long long ldx1, double* X, long long ldx,
                   double* nu2, double* wnext, cudaStream_t s, int allow_tma = 1, double* D = nullptr);

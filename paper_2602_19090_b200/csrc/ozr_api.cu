@@ -18,6 +18,7 @@
 
 #include "../../include/ozr.h"
 #include "certify.h"
+#include "syev.h"
 #include "comm.h"
 #include "kernels.h"
 #include "ozr_internal.h"
@@ -56,7 +57,7 @@ struct ozr_ctx_s {
   // while the main stream computes the GEMM of band b + 1
   cudaStream_t rstream = nullptr;
   cudaEvent_t bev[kMaxBands + 2];
-  DenseEig dense;  // cuSOLVER handle of the dense cluster sub-solve (created on first use)
+  SyevWorkspace syev;  // the hand-written dense eigensolver of the large-group sub-solve (syev.cu)
   // Host staging of the sweep's small reads and writes (mapped pinned memory, moved by a kernel — not by a
   // copy engine, which may be busy with a caller's large transfers on another stream): d2h() queues a read
   // that lands in `dst` at the next flush(), after the synchronisation that covers it.
@@ -164,7 +165,7 @@ enum Slot {
   S_ADIG, S_AELL, S_W, S_X1, S_XDIG, S_XDIGT, S_G, S_SH, S_SL, S_RH, S_RL, S_PLANES, S_VH, S_VL, S_LAM, S_ER,
   S_ERR, S_EMAX, S_RDIG, S_RELL, S_EP, S_NRM2, S_NU2, S_WNEXT, S_ZEROELL, S_TMP1, S_TMP2, S_BELL, S_AT, S_ONES,
   S_EDGES, S_ECOUNT, S_CINT, S_CDBL, S_CM, S_CR, S_CK, S_CV, S_CZ, S_CT, S_CSCR, S_CFLAG, S_SCAL, S_UFALL, S_CPART, S_GCNT, S_WA, S_GPLANES, S_RMAT, S_NR2, S_NW2, S_DWORK, S_DINFO, S_PI_V, S_PI_Z, S_PI_Y, S_PI_P, S_PI_S, S_CXG, S_CGJ, S_CGP,
-  S_CEB, S_CCB, S_CSE, S_CSC, S_CESQ, S_CDSQ, S_CFLG
+  S_CEB, S_CCB, S_CSE, S_CSC, S_CESQ, S_CDSQ, S_CFLG, S_CEBT, S_CRE, S_OZA, S_OZB, S_OZEA, S_OZEB, S_OZT, S_OZP, S_DP, S_DTZ, S_DTH, S_PI_LZ, S_PI_U, S_PI_T
 };
 
 ozr_status fail(ozr_ctx c, ozr_status st, const char* fmt, ...) {
@@ -638,6 +639,53 @@ void split_A_finish(const double* A, int64_t n, const std::vector<double>& hwA, 
   st.nA = n;
   st.kA_split = kA;
   st.eA_max = em;
+}
+
+// FP64-accurate product C = A·B (m x k times k x n, column-major, fp64 result) on the INT8 slice GEMM for the
+// dense sub-solve of large unresolved groups (R13): A split per row, B per column into kOzDig digits, digit pairs
+// s + t ≤ kOzDig + 1 (dropped pairs below 2^{-8·kOzDig+...} of max|A_i,:|·max|B_:,j|·k), exact recombination
+// rounded once. a_trans: A is stored as its transpose (k x m, lda) — e.g. a symmetric matrix — so the per-row
+// split of A is the per-column split of the stored matrix (no transpose).
+// Own workspace slots (the sweep's digit buffers stay live); split error flags accumulate into derr.
+constexpr int kOzDig = 8;
+constexpr int kSyevBigGemm = 1024;  // dense eigensolver products with a dimension ≥ this run on the INT8 slice GEMM
+ozr_status oz_dgemm(ozr_ctx ctx, int64_t m, int64_t n, int64_t k, const double* A, int64_t lda, bool a_trans,
+                    const double* B, int64_t ldb, double* C, int64_t ldc, int* derr) {
+  cudaStream_t s = ctx->stream;
+  const int64_t ldk = round16(k);
+  const int kd = kOzDig, L = kOzDig + 1;
+  int8_t* da = ctx->ws<int8_t>(S_OZA, static_cast<size_t>(kd) * ldk * m);
+  int8_t* db = ctx->ws<int8_t>(S_OZB, static_cast<size_t>(kd) * ldk * n);
+  int32_t* ea = ctx->ws<int32_t>(S_OZEA, m);
+  int32_t* eb = ctx->ws<int32_t>(S_OZEB, n);
+  OZR_ALLOC(da); OZR_ALLOC(db); OZR_ALLOC(ea); OZR_ALLOC(eb);
+  const double* As = A;
+  int64_t lds = lda;
+  if (!a_trans) {  // rows of A as columns: Aᵀ (k x m)
+    double* T = ctx->ws<double>(S_OZT, static_cast<size_t>(k) * m);
+    OZR_ALLOC(T);
+    launch_transpose_f64(A, lda, T, k, static_cast<int>(m), static_cast<int>(k), s);
+    As = T;
+    lds = k;
+  }
+  launch_split_fixed(As, nullptr, lds, static_cast<int>(k), static_cast<int>(m), kd, da, ldk, ldk * m, ea, derr, s);
+  launch_split_fixed(B, nullptr, ldb, static_cast<int>(k), static_cast<int>(n), kd, db, ldk, ldk * n, eb, derr, s);
+  std::vector<Group> gs = plan_groups(kd, kd, L, k);
+  PairTable pt;
+  RecombPlan rp;
+  if (!make_tables(gs, L, k, pt, rp)) return fail(ctx, OZR_ERR_RANGE, "dense sub-solve product plan too large");
+  const size_t mn = static_cast<size_t>(m) * n;
+  int32_t* planes = ctx->ws<int32_t>(S_OZP, static_cast<size_t>(pt.ngroups) * mn);
+  int* cnt = ctx->ws<int>(S_GCNT, 4);
+  OZR_ALLOC(planes); OZR_ALLOC(cnt);
+  const DigitOperand oa{da, ldk, ldk * m, kd}, ob{db, ldk, ldk * n, kd};
+  OZR_CK(launch_gemm_i8(oa, ob, static_cast<int>(m), static_cast<int>(n), static_cast<int>(k), pt, planes,
+                        static_cast<int64_t>(mn), m, s, cnt),
+         "dense sub-solve slice GEMM");
+  launch_recombine_dd(planes, static_cast<long long>(mn), static_cast<int>(m), static_cast<int>(n), rp, ea, eb,
+                      8 * (2 * kd - L), C, nullptr, ldc, s);
+  OZR_CK(cudaGetLastError(), "dense sub-solve recombination");
+  return OZR_OK;
 }
 
 // Block-column partition: rank r of P owns columns [col0, col0 + nl), nl = n/P, col0 = r·nl.
@@ -1161,16 +1209,6 @@ ozr_status sweep(ozr_ctx ctx, Exchange* ex, const double* A, int64_t n, int64_t 
       OZR_ALLOC(L.coop_scratch); OZR_ALLOC(L.coop_flags);
       L.dense_min = P.dense_cluster > 0 ? P.dense_cluster : (1 << 30);
       L.err = derr;
-      if (mmax >= L.dense_min) {  // workspace of the dense solver (dense_eig.cu), sized for the largest group
-        std::string why;
-        if (!dense_eig_available(&why)) return fail(ctx, OZR_ERR_CUDA, "dense cluster solver: %s", why.c_str());
-        const long long lw = dense_eig_lwork(ctx->dense, mmax, s);
-        if (lw < 0) return fail(ctx, OZR_ERR_CUDA, "dense cluster solver: syevd workspace query failed");
-        ctx->dense.work = ctx->ws<double>(S_DWORK, static_cast<size_t>(lw));
-        ctx->dense.info = ctx->ws<int>(S_DINFO, 4);
-        OZR_ALLOC(ctx->dense.work); OZR_ALLOC(ctx->dense.info);
-        ctx->dense.lwork = static_cast<int>(lw);
-      }
       // (1) M_JJ columns owned by this rank, (2) all-reduce → full M on every rank, (3) Jacobi (replicated),
       // (4) T = Ẽ'[:, J] owned columns, all-reduce, (5) apply + column statistics on owned columns
       // tensor-core Gram of the large groups: gather their digit columns, all-pairs slice GEMM, exact
@@ -1200,13 +1238,60 @@ ozr_status sweep(ozr_ctx ctx, Exchange* ex, const double* A, int64_t n, int64_t 
       OZR_CK(launch_cluster_build(L, s), "cluster build");
       OZR_X(xsum(cM, sq));
       OZR_CK(launch_cluster_solve(L, s), "cluster solve");
-      for (int q = 0; q < ng; ++q)
-        if (gm[q] >= L.dense_min) {
-          OZR_CK(launch_cluster_dense(L, ctx->dense, gm[q], gsq[q], mu[q], dpk + o_mem + off[q], s), "dense cluster solve");
-          cluster_launches += 6;
+      // dense sub-solve of the large groups (dense_eig.cu): K = C·sym(M)·C and Z = C·Y with C = I + R/2 as
+      // FP64-accurate INT8 slice products (R = R_JJ is symmetric: no transpose for its split)
+      double* dP = nullptr;
+      double* dth = nullptr;
+      if (mmax >= L.dense_min) {
+        dP = ctx->ws<double>(S_DP, static_cast<size_t>(mmax) * mmax);
+        dth = ctx->ws<double>(S_DTH, mmax);
+        OZR_ALLOC(dP); OZR_ALLOC(dth);
+      }
+      for (int q = 0; q < ng; ++q) {
+        if (gm[q] < L.dense_min) continue;
+        const int m = gm[q];
+        const long long mm = static_cast<long long>(m) * m;
+        double* M = cM + gsq[q];
+        double* R = cR + gsq[q];
+        double* K = cK + gsq[q];
+        double* V = cV + gsq[q];
+        double* Z = cZ + gsq[q];
+        launch_dense_sym(m, M, V, s);                                   // V = K0 = (M + Mᵀ)/2
+        OZR_X(oz_dgemm(ctx, m, m, m, R, m, true, V, m, dP, m, derr));    // P = R·K0
+        launch_dense_axpy(mm, V, 0.5, dP, K, s);                        // K = K0 + ½R·K0 = C·K0
+        OZR_X(oz_dgemm(ctx, m, m, m, K, m, false, R, m, dP, m, derr));   // P = K·R
+        launch_dense_axpy(mm, K, 0.5, dP, V, s);                        // V = C·K0·C
+        launch_dense_sym(m, V, K, s);                                   // K = sym(V)
+        {
+          std::string why;
+          const SyevGemm gemm = [&](int M2, int N2, int K2, const double* A2, int lda2, bool at, const double* B2,
+                                    int ldb2, double* C2, int ldc2) {
+            return oz_dgemm(ctx, M2, N2, K2, A2, lda2, at, B2, ldb2, C2, ldc2, derr) == OZR_OK ? 0 : 1;
+          };
+          const int rc = dense_syev(ctx->syev, m, K, dth, K, gemm, kSyevBigGemm, s, &why);
+          if (rc != 0) return fail(ctx, rc == 8 ? OZR_ERR_NOMEM : OZR_ERR_CUDA, "dense cluster eigensolver: %s", why.c_str());
         }
+        launch_dense_sign(m, K, dth, mu[q], dpk + o_mem + off[q], lam, nullptr, derr, s);  // K = Y
+        OZR_X(oz_dgemm(ctx, m, m, m, R, m, true, K, m, dP, m, derr));    // P = R·Y
+        launch_dense_axpy(mm, K, 0.5, dP, Z, s);                        // Z = Y + ½R·Y = C·Y
+        OZR_CK(cudaGetLastError(), "dense cluster solve");
+        cluster_launches += 18;
+      }
       OZR_X(xsum(cT, static_cast<size_t>(nmem) * n));
       OZR_CK(launch_cluster_apply(L, s), "cluster apply");
+      if (mmax >= L.dense_min) {
+        double* TZ = ctx->ws<double>(S_DTZ, static_cast<size_t>(n) * mmax);
+        OZR_ALLOC(TZ);
+        for (int q = 0; q < ng; ++q) {
+          if (gm[q] < L.dense_min) continue;
+          const int m = gm[q];
+          OZR_X(oz_dgemm(ctx, n, m, m, cT + static_cast<size_t>(off[q]) * n, n, false, cZ + gsq[q], m, TZ, n, derr));
+          launch_dense_scatter(TZ, N, m, dpk + o_mem + off[q], q, dpk + o_grp, dpk + o_pos, cZ + gsq[q], g, Ep, n,
+                               static_cast<int>(col0), NL, s);
+          cluster_launches += 6;
+        }
+      }
+      OZR_CK(launch_cluster_colstats(L, s), "cluster column statistics");
       ctx->mark("cluster");
       cluster_launches += 6;
       OZR_D2H(hlam_new.data(), lam, n * sizeof(double));
@@ -1336,11 +1421,12 @@ constexpr double kCertSafety = 1.15;  // power-iteration / bf16-GEMM slack of th
 constexpr double kContract = 1.0 / 8;  // an estimate that fell by less than this sits at the truncation floor
 
 // a10 (R12): the a-posteriori forward-error estimate of the sweep just completed, from its own Ẽ (certify.cu):
-//   est = sqrt(‖Q∘H‖₂² + (2u)²) + 1.5‖Ẽ‖_F²,  Q = ẼᵀC, c_kj = (λ̂_k − λ̂_j)ẽ_kj, H_ij = 1/(λ̂_j − λ̂_i) (i ≠ j),
-// the second-order defect of Ẽ (‖X − X̂_new‖₂ ≈ ‖E − Ẽ‖₂) plus the bound of the terms quadratic in ‖Ẽ‖ and the
-// fp64 rounding of X̂_new. ‖Q∘H‖₂ comes from its Frobenius norm when that already certifies, from the power
-// iteration otherwise — except when even the lower bound max_j ‖(Q∘H)_{:,j}‖ + 1.5‖Ẽ‖_F² exceeds 16δ: then the
-// upper bound (Frobenius) is reported, which no decision of the driver can tell from the exact value.
+//   est = sqrt(‖D‖₂² + (2u)²) + ‖Ẽ‖_F‖D‖_F,   D = −(E − Ẽ) to second order:
+//   D_ij = q_ij/(λ̂_j − λ̂_i) − (Ẽ²)_ij (i ≠ j), D_jj = −(Ẽ²)_jj − ½‖ẽ_j‖², Q = ẼᵀC, c_kj = (λ̂_k − λ̂_j)ẽ_kj
+// (oracle/refine.second_order_defect), plus the fp64 rounding of X̂_new and an allowance for the third-order
+// terms. ‖D‖₂ comes from its Frobenius norm when that already certifies, from the power iteration otherwise —
+// except when even the lower bound max_j ‖D_{:,j}‖ exceeds 16δ: then the upper bound (Frobenius) is reported,
+// which no decision of the driver can tell from the exact value.
 // Reads the sweep's Ẽ' (S_EP), g (S_G) and λ̂ (S_LAM); writes rep.cert, cert_q, cert_frob, cert_iters.
 ozr_status certify(ozr_ctx ctx, Exchange* ex, int64_t n, double delta, ozr_step_report& rep) {
   const int NP = ex ? ex->P : 1, RK = ex ? ex->rank : 0;
@@ -1352,22 +1438,26 @@ ozr_status certify(ozr_ctx ctx, Exchange* ex, int64_t n, double delta, ozr_step_
   const int32_t* g = static_cast<const int32_t*>(ctx->bufs[S_G].p);
   const double* lam = static_cast<const double*>(ctx->bufs[S_LAM].p);
   uint16_t* Eb = ctx->ws<uint16_t>(S_CEB, static_cast<size_t>(ldb) * n);
+  uint16_t* EbT = ctx->ws<uint16_t>(S_CEBT, static_cast<size_t>(ldb) * n);
   uint16_t* Cb = ctx->ws<uint16_t>(S_CCB, static_cast<size_t>(ldb) * nl);
   int32_t* sE = ctx->ws<int32_t>(S_CSE, n);
   int32_t* sC = ctx->ws<int32_t>(S_CSC, nl);
+  int32_t* rE = ctx->ws<int32_t>(S_CRE, n);
   double* esq = ctx->ws<double>(S_CESQ, n);
   double* dsq = ctx->ws<double>(S_CDSQ, n);
   int* flag = ctx->ws<int>(S_CFLG, 4);
   float* Q = reinterpret_cast<float*>(ctx->ws<int32_t>(S_PLANES, nnl));  // the slice planes are dead by now
-  float* D = reinterpret_cast<float*>(ctx->ws<double>(S_VH, nnl));      // so is V
+  float* D = reinterpret_cast<float*>(ctx->ws<double>(S_VH, nnl));      // so is V (2·nnl floats: D, then P)
+  float* Pm = D + nnl;
   int* cnt = ctx->ws<int>(S_GCNT, 4);
   double* z = ctx->ws<double>(S_PI_Z, nl);
   double* v = ctx->ws<double>(S_PI_V, nl);
   double* y = ctx->ws<double>(S_PI_Y, n);
   double* part = ctx->ws<double>(S_PI_P, static_cast<size_t>(cert_pi_chunks()) * n);
   double* sc = ctx->ws<double>(S_PI_S, 2);
-  OZR_ALLOC(Eb); OZR_ALLOC(Cb); OZR_ALLOC(sE); OZR_ALLOC(sC); OZR_ALLOC(esq); OZR_ALLOC(dsq); OZR_ALLOC(flag);
-  OZR_ALLOC(Q); OZR_ALLOC(D); OZR_ALLOC(cnt); OZR_ALLOC(z); OZR_ALLOC(v); OZR_ALLOC(y); OZR_ALLOC(part); OZR_ALLOC(sc);
+  OZR_ALLOC(Eb); OZR_ALLOC(EbT); OZR_ALLOC(Cb); OZR_ALLOC(sE); OZR_ALLOC(sC); OZR_ALLOC(rE); OZR_ALLOC(esq);
+  OZR_ALLOC(dsq); OZR_ALLOC(flag); OZR_ALLOC(Q); OZR_ALLOC(D); OZR_ALLOC(cnt); OZR_ALLOC(z); OZR_ALLOC(v); OZR_ALLOC(y);
+  OZR_ALLOC(part); OZR_ALLOC(sc);
   auto gather = [&](void* base, size_t bytes) -> ozr_status {
     if (ex && !ex->allgather(base, bytes, s)) return fail(ctx, OZR_ERR_COMM, "all-gather: %s", ex->err.c_str());
     return OZR_OK;
@@ -1382,6 +1472,7 @@ ozr_status certify(ozr_ctx ctx, Exchange* ex, int64_t n, double delta, ozr_step_
   if ((e = gather(Eb, static_cast<size_t>(nl) * ldb * 2)) != OZR_OK) return e;  // all columns: the A operand
   if ((e = gather(sE, nl * sizeof(int32_t))) != OZR_OK) return e;
   if ((e = gather(esq, nl * sizeof(double))) != OZR_OK) return e;
+  launch_cert_rowT(Eb, ldb, N, N, sE, rE, EbT, s);
   PairTable pt;
   memset(&pt, 0, sizeof pt);
   pt.ngroups = 1;
@@ -1389,9 +1480,13 @@ ozr_status certify(ozr_ctx ctx, Exchange* ex, int64_t n, double delta, ozr_step_
   pt.diag[0] = 2;
   const DigitOperand opE{reinterpret_cast<const int8_t*>(Eb), 2 * ldb, 2 * ldb * n, 1};
   const DigitOperand opC{reinterpret_cast<const int8_t*>(Cb), 2 * ldb, 2 * ldb * nl, 1};
+  const DigitOperand opET{reinterpret_cast<const int8_t*>(EbT), 2 * ldb, 2 * ldb * n, 1};
+  const DigitOperand opEJ{reinterpret_cast<const int8_t*>(Eb + col0 * ldb), 2 * ldb, 2 * ldb * nl, 1};
   OZR_CK(launch_gemm_i8(opE, opC, N, NL, 2 * N, pt, reinterpret_cast<int32_t*>(Q), nnl, n, s, cnt, 1, 1),
-         "certificate GEMM (bf16)");
-  launch_cert_delta(Q, n, N, NL, sE, sC, lam, static_cast<int>(col0), D, dsq + col0, flag, s);
+         "certificate GEMM Q (bf16)");
+  OZR_CK(launch_gemm_i8(opET, opEJ, N, NL, 2 * N, pt, reinterpret_cast<int32_t*>(Pm), nnl, n, s, cnt, 1, 1),
+         "certificate GEMM E^2 (bf16)");
+  launch_cert_delta(Q, Pm, n, N, NL, sE, sC, rE, esq, lam, static_cast<int>(col0), D, dsq + col0, flag, s);
   OZR_CK(cudaGetLastError(), "certificate");
   if ((e = gather(dsq, nl * sizeof(double))) != OZR_OK) return e;
   std::vector<double> hesq(n), hdsq(n);
@@ -1414,7 +1509,7 @@ ozr_status certify(ozr_ctx ctx, Exchange* ex, int64_t n, double delta, ozr_step_
     d2 += hdsq[j];
     dmax = std::max(dmax, hdsq[j]);
   }
-  const double quad = 1.5 * e2, frob = std::sqrt(d2), rnd = 2.0 * kU;
+  const double frob = std::sqrt(d2), quad = std::sqrt(e2) * frob, rnd = 2.0 * kU;
   rep.cert_frob = frob;
   const double upper = std::sqrt(frob * frob + rnd * rnd) + quad;
   if (upper * kCertSafety <= delta || std::sqrt(dmax) + quad > 16.0 * delta) {
@@ -1422,34 +1517,79 @@ ozr_status certify(ozr_ctx ctx, Exchange* ex, int64_t n, double delta, ozr_step_
     rep.cert_q = frob;
     return OZR_OK;
   }
-  // power iteration for ‖D‖₂ (D column-partitioned: D·z all-reduced, Dᵀy local)
-  launch_normalize(v, nullptr, NL, nullptr, static_cast<int>(col0), s);
+  // ‖D‖₂ by Golub–Kahan–Lanczos bidiagonalization (D column-partitioned: D·v all-reduced, Dᵀu local), no
+  // reorthogonalisation (the largest Ritz value still converges to σ_max from below): β₀u₀ = Dv₀,
+  // α_j v_{j+1} = Dᵀu_j − β_j v_j, β_{j+1}u_{j+1} = Dv_{j+1} − α_j u_j; σ_max of the upper bidiagonal B
+  // (diag β, super α) from the largest eigenvalue of BᵀB by bisection. Checked every 4 steps from step 8 on:
+  // stop when it moved by ≤ 1e-3 relative (at most 40 steps).
+  constexpr int kLzMax = 40;
+  double* lz = ctx->ws<double>(S_PI_LZ, 2 * (kLzMax + 2));  // bsq[0..], asq[0..]
+  double* u = ctx->ws<double>(S_PI_U, n);
+  double* t = ctx->ws<double>(S_PI_T, nl);
+  OZR_ALLOC(lz); OZR_ALLOC(u); OZR_ALLOC(t);
+  double* bsq = lz;
+  double* asq = lz + kLzMax + 2;
+  auto sigma_max = [](const std::vector<double>& b2, const std::vector<double>& a2, int k) {
+    // T = BᵀB: T_ii = β_i² + α_{i−1}², T_{i,i+1} = α_i β_i (squared off-diagonal α_i²β_i² for the Sturm count)
+    std::vector<double> dg(k), off2(k, 0.0);
+    double hi = 0.0;
+    for (int i = 0; i < k; ++i) {
+      dg[i] = b2[i] + (i > 0 ? a2[i - 1] : 0.0);
+      if (i + 1 < k) off2[i] = a2[i] * b2[i];
+    }
+    for (int i = 0; i < k; ++i)
+      hi = std::max(hi, dg[i] + (i > 0 ? std::sqrt(off2[i - 1]) : 0.0) + (i + 1 < k ? std::sqrt(off2[i]) : 0.0));
+    double lo = 0.0;
+    for (int it = 0; it < 200 && hi - lo > 1e-14 * hi; ++it) {
+      const double x = 0.5 * (lo + hi);
+      int cnt = 0;  // eigenvalues of T greater than x (Sturm sequence of T − xI)
+      double q = dg[0] - x;
+      if (q > 0) ++cnt;
+      for (int i = 1; i < k; ++i) {
+        q = dg[i] - x - off2[i - 1] / (q != 0.0 ? q : 1e-300);
+        if (q > 0) ++cnt;
+      }
+      if (cnt >= 1) lo = x; else hi = x;
+    }
+    return std::sqrt(0.5 * (lo + hi));
+  };
+  launch_normalize(v, nullptr, NL, nullptr, static_cast<int>(col0), s);  // deterministic start
   launch_sumsq(v, NL, sc, s);
   if ((e = allsum(sc, 1)) != OZR_OK) return e;
-  launch_normalize(z, v, NL, sc, 0, s);
+  launch_normalize(z, v, NL, sc, 0, s);  // z = v₀ (unit)
+  launch_pi_dz(D, N, NL, z, part, y, s);
+  if ((e = allsum(y, n)) != OZR_OK) return e;
+  launch_sumsq(y, N, bsq, s);
+  launch_normalize(u, y, N, bsq, 0, s);
   double sig = 0.0, prev = -1.0;
-  int it = 0;
-  while (it < 48) {
-    for (int q = 0; q < 4; ++q, ++it) {
-      launch_pi_dz(D, N, NL, z, part, y, s);
+  int k = 0;
+  std::vector<double> hb(kLzMax + 2), ha(kLzMax + 2);
+  while (k < kLzMax) {
+    const int kn = std::min(kLzMax, k < 8 ? 8 : k + 4);
+    for (; k < kn; ++k) {
+      launch_pi_dty(D, N, NL, u, t, s);                 // t = Dᵀu_k
+      launch_lz_axpy(z, t, NL, bsq + k, s);             // z ← t − β_k v_k (z holds v_k)
+      launch_sumsq(z, NL, asq + k, s);
+      if ((e = allsum(asq + k, 1)) != OZR_OK) return e;
+      launch_normalize(z, z, NL, asq + k, 0, s);        // v_{k+1}
+      launch_pi_dz(D, N, NL, z, part, y, s);            // y = D v_{k+1}
       if ((e = allsum(y, n)) != OZR_OK) return e;
-      launch_pi_dty(D, N, NL, y, v, s);
-      launch_sumsq(v, NL, sc, s);
-      if ((e = allsum(sc, 1)) != OZR_OK) return e;
-      launch_normalize(z, v, NL, sc, 0, s);
+      launch_lz_axpy(u, y, N, asq + k, s);              // u ← y − α_k u_k
+      launch_sumsq(u, N, bsq + k + 1, s);
+      launch_normalize(u, u, N, bsq + k + 1, 0, s);     // u_{k+1}
     }
-    OZR_CK(cudaGetLastError(), "power iteration");
-    double h = 0.0;
+    OZR_CK(cudaGetLastError(), "Lanczos");
     ctx->pend.clear();
     ctx->hst_off = 0;
-    OZR_D2H(&h, sc, sizeof(double));
+    OZR_D2H(hb.data(), bsq, (k + 1) * sizeof(double));
+    OZR_D2H(ha.data(), asq, k * sizeof(double));
     OZR_CK(cudaStreamSynchronize(s), "sync");
     ctx->flush();
-    sig = std::sqrt(std::sqrt(h));  // ‖DᵀD z‖ → σ_max² for the unit z
+    sig = sigma_max(hb, ha, k);
     if (prev > 0.0 && std::fabs(sig - prev) <= 1e-3 * sig) break;
     prev = sig;
   }
-  rep.cert_iters = it;
+  rep.cert_iters = k;
   rep.cert_q = sig;
   rep.cert = std::sqrt(sig * sig + rnd * rnd) + quad;
   return OZR_OK;
@@ -1611,6 +1751,32 @@ ozr_status ozr_split(ozr_ctx ctx, const double* M, const double* M_lo, int64_t r
   OZR_CK(cudaGetLastError(), "ozr_split");
   if (k_out) *k_out = k;
   return read_err(ctx, derr);
+}
+
+ozr_status ozr_syev(ozr_ctx ctx, int64_t m, const double* K, int64_t ldk, double* theta, double* Y, int64_t ldy) {
+  ozr_status st = check_ctx(ctx);
+  if (st != OZR_OK) return st;
+  if (!K || !theta || !Y || m < 1 || ldk < m || ldy < m || m > 32768) return fail(ctx, OZR_ERR_ARG, "ozr_syev: bad argument");
+  cudaStream_t s = ctx->stream;
+  const size_t mm = static_cast<size_t>(m) * m;
+  double* Kw = ctx->ws<double>(S_DP, mm);  // working copy (destroyed by the tridiagonalisation)
+  double* Yw = ctx->ws<double>(S_DTZ, mm);
+  int* derr = ctx->ws<int>(S_ERR, 4);
+  OZR_ALLOC(Kw); OZR_ALLOC(Yw); OZR_ALLOC(derr);
+  OZR_CK(cudaMemsetAsync(derr, 0, sizeof(int), s), "memset");
+  OZR_CK(cudaMemcpy2DAsync(Kw, m * sizeof(double), K, ldk * sizeof(double), m * sizeof(double), m,
+                           cudaMemcpyDeviceToDevice, s), "copy K");
+  std::string why;
+  const SyevGemm gemm = [&](int M2, int N2, int K2, const double* A2, int lda2, bool at, const double* B2, int ldb2,
+                            double* C2, int ldc2) {
+    return oz_dgemm(ctx, M2, N2, K2, A2, lda2, at, B2, ldb2, C2, ldc2, derr) == OZR_OK ? 0 : 1;
+  };
+  const int rc = dense_syev(ctx->syev, static_cast<int>(m), Kw, theta, Yw, gemm, kSyevBigGemm, s, &why);
+  if (rc != 0) return fail(ctx, rc == 8 ? OZR_ERR_NOMEM : OZR_ERR_CUDA, "ozr_syev: %s", why.c_str());
+  OZR_CK(cudaMemcpy2DAsync(Y, ldy * sizeof(double), Yw, m * sizeof(double), m * sizeof(double), m,
+                           cudaMemcpyDeviceToDevice, s), "copy Y");
+  OZR_CK(cudaStreamSynchronize(s), "sync");
+  return OZR_OK;
 }
 
 ozr_status ozr_last_R(ozr_ctx ctx, double* R, int64_t ldr) {

@@ -1,0 +1,1114 @@
+// syev.cu — the hand-written dense symmetric eigensolver of the Rayleigh–Ritz sub-solve of large unresolved
+// groups (R13: K = C·sym(M)·C = YΘYᵀ). Replaces a library eigensolver on the cluster path.
+//
+//   (1) Householder tridiagonalisation Qᴴᵀ K Qᴴ = T (lower storage, LAPACK dsytrd/dlatrd blocking): panels of
+//       NB columns, each a persistent cooperative kernel (3 grid-wide barriers per column: the updated column
+//       and its norm; the reflector, the symmetric product w = K₂₂v over 64 x 64 lower-triangle tiles — each
+//       tile read ONCE and used for both of its row and column contributions, partials reduced in a fixed
+//       order — and Vᵀv, Wᵀv; then w's last correction), followed by the rank-2·NB trailing update
+//       K₂₂ −= VWᵀ + WVᵀ on the lower tiles.
+//   (2) T = QᵀΘQᵀᵀ by Cuppen's divide and conquer with Gu–Eisenstat eigenvectors (syev_dc.cu).
+//   (3) Y = Qᴴ·Qᵀ: the reflectors applied blockwise (compact WY, I − V T Vᵀ).
+// Every reduction has a fixed order (no floating-point atomics): the result is deterministic.
+#include <cooperative_groups.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstdio>
+#include <vector>
+
+#include "syev.h"
+
+namespace ozr {
+
+namespace cg = cooperative_groups;
+
+namespace {
+
+constexpr int NB = 32;   // panel width
+constexpr int TB = 64;   // symv / update tile
+constexpr int TT = 256;  // threads per CTA
+
+__device__ __forceinline__ double block_sum256(double v, double* sh) {
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) sh[w] = v;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    v = (threadIdx.x < TT / 32) ? sh[threadIdx.x] : 0.0;
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (threadIdx.x == 0) sh[0] = v;
+  }
+  __syncthreads();
+  v = sh[0];
+  __syncthreads();
+  return v;
+}
+
+// linear index t of the active lower tiles (I ≥ J ≥ J0, I < mt) → (I, J), row-major over I
+__device__ __forceinline__ void tile_of(int t, int J0, int& I, int& J) {
+  // rows I' = I − J0 hold I' + 1 tiles: t = I'(I'+1)/2 + (J − J0)
+  int Ip = static_cast<int>((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
+  while ((Ip + 1) * (Ip + 2) / 2 <= t) ++Ip;
+  while (Ip * (Ip + 1) / 2 > t) --Ip;
+  I = J0 + Ip;
+  J = J0 + (t - Ip * (Ip + 1) / 2);
+}
+__device__ __forceinline__ long long tslot(int I, int J) { return static_cast<long long>(I) * (I + 1) / 2 + J; }
+
+struct PanelArgs {
+  double* A;        // m x m, lda = m (lower triangle maintained)
+  int m;
+  int k0;           // first column of the panel
+  int nb;           // columns in this panel
+  double* V;        // m x NB (reflectors of the panel, v_{c+1} = 1)
+  double* W;        // m x NB
+  double* d;        // diagonal of T
+  double* e;        // sub-diagonal of T
+  double* tau;      // reflector scalars
+  double* part;     // G x (2 + 2·NB) scalar partials
+  double* yp;       // tile partials: slot(I, J) x 2 x TB
+};
+
+// Row block R (TB rows) is owned by CTA R % G.
+__global__ void __launch_bounds__(TT) k_trd_panel(PanelArgs P) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double sh[TT / 32];
+  __shared__ double tile[TB][TB + 1];  // tile[col][row]
+  __shared__ double vr[TB], vc[TB];
+  __shared__ double wtv[NB], vtv[NB];
+  const int G = gridDim.x, b = blockIdx.x, tid = threadIdx.x;
+  const int m = P.m;
+  const int mt = (m + TB - 1) / TB;
+  double* A = P.A;
+  const int PS = 2 + 2 * NB;
+  double gam_prev = 0.0;  // γ of the previous column (its W column's final correction, pending on own rows)
+  for (int i = 0; i < P.nb; ++i) {
+    const int c = P.k0 + i;
+    // ---- phase A: own rows r ≥ c: finish W(:, i−1) (+γ v), x_r = A(r,c) − V(r,:)W(c,:)ᵀ − W(r,:)V(c,:)ᵀ
+    double ss = 0.0;
+    for (int R = b; R < mt; R += G) {
+      const int r = R * TB + (tid & (TB - 1));
+      if ((tid >> 6) != 0) continue;  // one 64-thread group per row block (rows are few per CTA)
+      if (r >= m || r < c) continue;
+      if (i > 0 && r >= c) P.W[r + static_cast<long long>(i - 1) * m] =
+                               fma(gam_prev, P.V[r + static_cast<long long>(i - 1) * m], P.W[r + static_cast<long long>(i - 1) * m]);
+      double x = A[r + static_cast<long long>(c) * m];
+      for (int j = 0; j < i; ++j) {
+        double wc = P.W[c + static_cast<long long>(j) * m];
+        if (j == i - 1) wc = fma(gam_prev, P.V[c + static_cast<long long>(j) * m], wc);
+        x -= P.V[r + static_cast<long long>(j) * m] * wc + P.W[r + static_cast<long long>(j) * m] * P.V[c + static_cast<long long>(j) * m];
+      }
+      A[r + static_cast<long long>(c) * m] = x;
+      if (r >= c + 2) ss = fma(x, x, ss);
+    }
+    ss = block_sum256(ss, sh);
+    if (tid == 0) P.part[static_cast<long long>(b) * PS] = ss;
+    grid.sync();
+    // ---- phase B: the reflector (every CTA, same order), the tile products, Vᵀv and Wᵀv partials
+    double sigma = 0.0;
+    for (int g = 0; g < G; ++g) sigma += P.part[static_cast<long long>(g) * PS];
+    const double ccdiag = A[c + static_cast<long long>(c) * m];
+    double alpha = 0.0, beta = 0.0, tau = 0.0, scale = 0.0;
+    if (c + 1 < m) {
+      alpha = A[c + 1 + static_cast<long long>(c) * m];
+      if (sigma == 0.0) {
+        beta = alpha;  // H = I
+      } else {
+        beta = -copysign(sqrt(fma(alpha, alpha, sigma)), alpha);
+        tau = (beta - alpha) / beta;
+        scale = 1.0 / (alpha - beta);
+      }
+    }
+    if (b == 0 && tid == 0) {
+      P.d[c] = ccdiag;
+      if (c + 1 < m) {
+        P.e[c] = beta;
+        P.tau[c] = tau;
+      }
+    }
+    if (c + 1 >= m) break;  // the last column: only its diagonal
+    auto vof = [&](int r) -> double { return r == c + 1 ? 1.0 : (r > c + 1 ? A[r + static_cast<long long>(c) * m] * scale : 0.0); };
+    // own rows: V(r, i)
+    for (int R = b; R < mt; R += G) {
+      const int r = R * TB + tid;
+      if (tid < TB && r < m && r >= c + 1) P.V[r + static_cast<long long>(i) * m] = vof(r);
+    }
+    if (tau != 0.0) {
+      // tiles of the lower triangle of A(c+1:m, c+1:m), grid-aligned
+      const int J0 = (c + 1) / TB;
+      const int na = mt - J0;
+      const int ntiles = na * (na + 1) / 2;
+      for (int t = b; t < ntiles; t += G) {
+        int I, J;
+        tile_of(t, J0, I, J);
+        const int r0 = I * TB, q0 = J * TB;
+        __syncthreads();
+        // load: tile[κ][ρ] = A(r0+ρ, q0+κ) (lower: r ≥ q; for the diagonal tile the upper half is mirrored)
+        for (int e2 = tid; e2 < TB * TB; e2 += TT) {
+          const int rho = e2 & (TB - 1), kap = e2 >> 6;
+          const int r = r0 + rho, q = q0 + kap;
+          double a = 0.0;
+          if (r < m && q < m && r >= c + 1 && q >= c + 1) {
+            if (r >= q) a = A[r + static_cast<long long>(q) * m];
+            else a = A[q + static_cast<long long>(r) * m];
+          }
+          tile[kap][rho] = a;
+        }
+        if (tid < TB) {
+          vr[tid] = (r0 + tid < m) ? vof(r0 + tid) : 0.0;
+          vc[tid] = (q0 + tid < m) ? vof(q0 + tid) : 0.0;
+        }
+        __syncthreads();
+        double* out = P.yp + tslot(I, J) * 2 * TB;
+        if (tid < TB) {  // row sums: Σ_κ tile[κ][ρ] vc[κ]
+          double acc = 0.0;
+          for (int kap = 0; kap < TB; ++kap) acc = fma(tile[kap][tid], vc[kap], acc);
+          out[tid] = acc;
+        } else if (tid < 2 * TB) {  // column sums (off-diagonal tiles): Σ_ρ tile[κ][ρ] vr[ρ]
+          const int kap = tid - TB;
+          double acc = 0.0;
+          if (I != J)
+            for (int rho = 0; rho < TB; ++rho) acc = fma(tile[kap][rho], vr[rho], acc);
+          out[TB + kap] = acc;
+        }
+      }
+      // Vᵀv and Wᵀv over own rows (columns j < i)
+      for (int j = 0; j < i; ++j) {
+        double pv = 0.0, pw = 0.0;
+        for (int R = b; R < mt; R += G) {
+          const int r = R * TB + tid;
+          if (tid < TB && r < m && r >= c + 1) {
+            const double v = vof(r);
+            pv = fma(P.V[r + static_cast<long long>(j) * m], v, pv);
+            pw = fma(P.W[r + static_cast<long long>(j) * m], v, pw);
+          }
+        }
+        pv = block_sum256(pv, sh);
+        pw = block_sum256(pw, sh);
+        if (tid == 0) {
+          P.part[static_cast<long long>(b) * PS + 2 + j] = pv;
+          P.part[static_cast<long long>(b) * PS + 2 + NB + j] = pw;
+        }
+      }
+    }
+    grid.sync();
+    // ---- phase C: y_r from the tile partials, w'_r = τ(y − V(Wᵀv) − W(Vᵀv)), partial of w'ᵀv
+    double p3 = 0.0;
+    if (tau != 0.0) {
+      if (tid < i) {
+        double sv = 0.0, sw = 0.0;
+        for (int g = 0; g < G; ++g) {
+          sv += P.part[static_cast<long long>(g) * PS + 2 + tid];
+          sw += P.part[static_cast<long long>(g) * PS + 2 + NB + tid];
+        }
+        vtv[tid] = sv;
+        wtv[tid] = sw;
+      }
+      __syncthreads();
+      const int J0 = (c + 1) / TB;
+      for (int R = b; R < mt; R += G) {
+        const int r = R * TB + tid;
+        if (tid >= TB || r >= m || r < c + 1) continue;
+        double y = 0.0;
+        for (int J = J0; J <= R; ++J) y += P.yp[tslot(R, J) * 2 * TB + tid];
+        for (int I = R + 1; I < mt; ++I) y += P.yp[tslot(I, R) * 2 * TB + TB + tid];
+        for (int j = 0; j < i; ++j)
+          y -= P.V[r + static_cast<long long>(j) * m] * wtv[j] + P.W[r + static_cast<long long>(j) * m] * vtv[j];
+        const double w = tau * y;
+        P.W[r + static_cast<long long>(i) * m] = w;
+        p3 = fma(w, vof(r), p3);
+      }
+    } else {
+      for (int R = b; R < mt; R += G) {
+        const int r = R * TB + tid;
+        if (tid < TB && r < m && r >= c + 1) P.W[r + static_cast<long long>(i) * m] = 0.0;
+      }
+    }
+    p3 = block_sum256(p3, sh);
+    if (tid == 0) P.part[static_cast<long long>(b) * PS + 1] = p3;
+    grid.sync();
+    double wv = 0.0;
+    for (int g = 0; g < G; ++g) wv += P.part[static_cast<long long>(g) * PS + 1];
+    gam_prev = -0.5 * tau * wv;  // W(:, i) += γ v: applied on own rows at the next column (or below)
+  }
+  // the last column's pending γ (rows ≥ its c + 1), for the trailing update
+  const int ilast = P.nb - 1, clast = P.k0 + ilast;
+  if (clast + 1 < m) {
+    for (int R = b; R < mt; R += G) {
+      const int r = R * TB + tid;
+      if (tid < TB && r < m && r >= clast + 1)
+        P.W[r + static_cast<long long>(ilast) * m] =
+            fma(gam_prev, P.V[r + static_cast<long long>(ilast) * m], P.W[r + static_cast<long long>(ilast) * m]);
+    }
+  }
+}
+
+// Trailing update of the lower tiles of A(k1:m, k1:m): A −= V Wᵀ + W Vᵀ (nb columns); also stores the panel's
+// reflectors below the sub-diagonal: A(r, k0 + j) = V(r, j) for r ≥ k0 + j + 2 (tiles with J == -1: the copy).
+__global__ void __launch_bounds__(TT) k_trd_update(double* __restrict__ A, int m, int k0, int nb,
+                                                   const double* __restrict__ V, const double* __restrict__ W) {
+  __shared__ double vR[NB][TB], wR[NB][TB], vC[NB][TB / 2], wC[NB][TB / 2];  // 48 KB: columns in two halves
+  const int k1 = k0 + nb;
+  const int J0 = k1 / TB, mt = (m + TB - 1) / TB;
+  const int na = mt - J0;
+  const int t = blockIdx.x;
+  if (t >= na * (na + 1) / 2) {  // the reflector copy: one CTA per panel column
+    const int j = t - na * (na + 1) / 2;
+    if (j >= nb) return;
+    const int c = k0 + j;
+    for (int r = c + 2 + threadIdx.x; r < m; r += TT) A[r + static_cast<long long>(c) * m] = V[r + static_cast<long long>(j) * m];
+    return;
+  }
+  int I, J;
+  tile_of(t, J0, I, J);
+  const int r0 = I * TB, q0 = J * TB;
+  for (int e2 = threadIdx.x; e2 < NB * TB; e2 += TT) {
+    const int rho = e2 & (TB - 1), j = e2 >> 6;
+    const int r = r0 + rho;
+    const bool jr = j < nb && r < m && r >= k1;
+    vR[j][rho] = jr ? V[r + static_cast<long long>(j) * m] : 0.0;
+    wR[j][rho] = jr ? W[r + static_cast<long long>(j) * m] : 0.0;
+  }
+  const int rho = threadIdx.x & (TB - 1);
+  const int r = r0 + rho;
+  for (int h = 0; h < 2; ++h) {
+    const int qh = q0 + h * (TB / 2);
+    __syncthreads();
+    for (int e2 = threadIdx.x; e2 < NB * (TB / 2); e2 += TT) {
+      const int kap = e2 & (TB / 2 - 1), j = e2 >> 5;
+      const int q = qh + kap;
+      const bool jq = j < nb && q < m && q >= k1;
+      vC[j][kap] = jq ? V[q + static_cast<long long>(j) * m] : 0.0;
+      wC[j][kap] = jq ? W[q + static_cast<long long>(j) * m] : 0.0;
+    }
+    __syncthreads();
+    for (int kk = threadIdx.x >> 6; kk < TB / 2; kk += TT / TB) {
+      const int q = qh + kk;
+      if (r >= m || q >= m || r < k1 || q < k1 || r < q) continue;
+      double acc = 0.0;
+#pragma unroll 8
+      for (int j = 0; j < NB; ++j) acc = fma(vR[j][rho], wC[j][kk], fma(wR[j][rho], vC[j][kk], acc));
+      A[r + static_cast<long long>(q) * m] -= acc;
+    }
+  }
+}
+
+// ================================================================ (2) divide and conquer on T
+constexpr int LEAF = 32;
+
+// Leaf: implicit QL with Wilkinson-type shifts (tqli) on an L ≤ 32 tridiagonal; thread t owns row t of the
+// eigenvector block, every thread runs the scalar recurrence (identical values). Output: eigenvalues (unsorted)
+// into lamo[lo..hi), eigenvectors into Q (block rows/columns lo..hi, ld = m).
+__global__ void __launch_bounds__(LEAF) k_dc_leaf(const int* __restrict__ leaf_lo, const int* __restrict__ leaf_hi,
+                                                  const double* __restrict__ dmod, const double* __restrict__ e,
+                                                  double* __restrict__ lamo, double* __restrict__ Q, int m,
+                                                  int* __restrict__ err) {
+  const int lo = leaf_lo[blockIdx.x], n = leaf_hi[blockIdx.x] - lo;
+  const int t = threadIdx.x;
+  double d[LEAF], ee[LEAF], z[LEAF];
+  for (int i = 0; i < LEAF; ++i) {
+    d[i] = i < n ? dmod[lo + i] : 0.0;
+    ee[i] = (i + 1 < n) ? e[lo + i] : 0.0;
+    z[i] = (i == t) ? 1.0 : 0.0;
+  }
+  const double eps = 1.1102230246251565e-16;
+  for (int l = 0; l < n; ++l) {
+    int iter = 0, mm;
+    do {
+      for (mm = l; mm < n - 1; ++mm) {
+        const double dd = fabs(d[mm]) + fabs(d[mm + 1]);
+        if (fabs(ee[mm]) <= eps * dd) break;
+      }
+      if (mm != l) {
+        if (++iter > 60) {
+          if (t == 0) atomicOr(err, 1);
+          break;
+        }
+        double g = (d[l + 1] - d[l]) / (2.0 * ee[l]);
+        double r = hypot(g, 1.0);
+        g = d[mm] - d[l] + ee[l] / (g + copysign(r, g));
+        double s = 1.0, c = 1.0, p = 0.0;
+        int i;
+        bool early = false;
+        for (i = mm - 1; i >= l; --i) {
+          double f = s * ee[i];
+          const double b = c * ee[i];
+          ee[i + 1] = (r = hypot(f, g));
+          if (r == 0.0) {
+            d[i + 1] -= p;
+            ee[mm] = 0.0;
+            early = true;
+            break;
+          }
+          s = f / r;
+          c = g / r;
+          g = d[i + 1] - p;
+          r = (d[i] - g) * s + 2.0 * c * b;
+          d[i + 1] = g + (p = s * r);
+          g = c * r - b;
+          f = z[i + 1];
+          z[i + 1] = s * z[i] + c * f;
+          z[i] = c * z[i] - s * f;
+        }
+        if (early) continue;
+        d[l] -= p;
+        ee[l] = g;
+        ee[mm] = 0.0;
+      }
+    } while (mm != l);
+  }
+  if (t < n) {
+    for (int j = 0; j < n; ++j) Q[static_cast<long long>(lo + j) * m + lo + t] = z[j];
+    if (t == 0)
+      for (int j = 0; j < n; ++j) lamo[lo + j] = d[j];
+  }
+}
+
+// z of a merge: [Q1(last row, :) ; s·Q2(first row, :)] / √2 for node q (cols of the node's block)
+__global__ void k_dc_zvec(const int* __restrict__ nlo, const int* __restrict__ nmid, const int* __restrict__ nhi,
+                          const double* __restrict__ sgn, const double* __restrict__ Q, int m, double* __restrict__ z) {
+  const int q = blockIdx.y;
+  const int lo = nlo[q], mid = nmid[q], hi = nhi[q];
+  for (int j = lo + blockIdx.x * blockDim.x + threadIdx.x; j < hi; j += gridDim.x * blockDim.x) {
+    const double v = (j < mid) ? Q[static_cast<long long>(j) * m + mid - 1] : sgn[q] * Q[static_cast<long long>(j) * m + mid];
+    z[j] = v * 0.70710678118654752440;
+  }
+}
+
+// Qp (node block, ld = m) column jj = Q column lo + src[jj] (block-diagonal halves), then the deflation
+// rotations of the node in order (each thread one row: the rotations only mix columns).
+__global__ void k_dc_permrot(const int* __restrict__ nlo, const int* __restrict__ nhi, const int* __restrict__ src,
+                             const int* __restrict__ rot_off, const int4* __restrict__ rot_idx,
+                             const double2* __restrict__ rot_cs, const double* __restrict__ Q, double* __restrict__ Qp,
+                             int m) {
+  const int q = blockIdx.y;
+  const int lo = nlo[q], nn = nhi[q] - lo;
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= nn) return;
+  for (int jj = 0; jj < nn; ++jj)
+    Qp[static_cast<long long>(lo + jj) * m + lo + r] = Q[static_cast<long long>(lo + src[lo + jj]) * m + lo + r];
+  for (int k = rot_off[q]; k < rot_off[q + 1]; ++k) {
+    const int a = rot_idx[k].x, b = rot_idx[k].y;  // node-local columns of Qp
+    const double c = rot_cs[k].x, s = rot_cs[k].y;
+    double* pa = Qp + static_cast<long long>(lo + a) * m + lo + r;
+    double* pb = Qp + static_cast<long long>(lo + b) * m + lo + r;
+    const double x = *pa, y = *pb;
+    *pa = c * x + s * y;  // LAPACK drot(Q(:,PJ), Q(:,NJ), C, S): x' = c x + s y, y' = c y − s x
+    *pb = c * y - s * x;
+  }
+}
+
+// Secular equation of node q, root j (k non-deflated, d ascending, ρ > 0, z unit-ish): f(λ) = 1/ρ + Σ z_i²/(d_i − λ).
+// Origin at the nearer pole (o = j or j + 1), τ = λ − d_o; Gragg's two-pole rational model with a bisection guard.
+__device__ void secular_root(int k, const double* __restrict__ d, const double* __restrict__ z, double rho, int j,
+                             int& o_out, double& tau_out) {
+  const double eps = 1.1102230246251565e-16;
+  const double ir = 1.0 / rho;
+  double zz = 0.0;
+  for (int i = 0; i < k; ++i) zz = fma(z[i], z[i], zz);
+  int o = j;
+  double a, b;  // bracket of τ
+  if (j < k - 1) {
+    const double del = d[j + 1] - d[j];
+    double f = ir;
+    for (int i = 0; i < k; ++i) f += z[i] * z[i] / ((d[i] - d[j]) - 0.5 * del);
+    if (f >= 0.0) {
+      o = j;
+      a = 0.0;
+      b = 0.5 * del;
+    } else {
+      o = j + 1;
+      a = -0.5 * del;
+      b = 0.0;
+    }
+  } else {
+    a = 0.0;
+    b = rho * zz;
+  }
+  const double dO = d[o];
+  double t = 0.5 * (a + b);
+  for (int it = 0; it < 80; ++it) {
+    double psi = 0.0, dpsi = 0.0, phi = 0.0, dphi = 0.0, erre = 0.0;
+    for (int i = 0; i < k; ++i) {
+      const double del = (d[i] - dO) - t;
+      const double q = z[i] / del;
+      if (i <= j) {
+        psi = fma(z[i], q, psi);
+        dpsi = fma(q, q, dpsi);
+      } else {
+        phi = fma(z[i], q, phi);
+        dphi = fma(q, q, dphi);
+      }
+      erre += fabs(z[i] * q);
+    }
+    const double f = ir + psi + phi;
+    if (f > 0.0) b = t; else a = t;
+    if (fabs(f) <= 8.0 * eps * (ir + erre + k * (fabs(psi) + fabs(phi))) || b - a <= 4.0 * eps * fmax(fabs(a), fabs(b)) ||
+        f == 0.0)
+      break;
+    // model c + sL/(ΔL − η) + sR/(ΔR − η) matching f and f' at η = 0
+    double tn;
+    const double dL = (d[j] - dO) - t;
+    if (j < k - 1) {
+      const double dR = (d[j + 1] - dO) - t;
+      const double sL = dpsi * dL * dL, sR = dphi * dR * dR;
+      const double c = f - dpsi * dL - dphi * dR;
+      // c η² − (c(ΔL + ΔR) + sL + sR) η + (cΔLΔR + sLΔR + sRΔL) = 0, root in (ΔL, ΔR)
+      const double A2 = c, B2 = c * (dL + dR) + sL + sR, C2 = c * dL * dR + sL * dR + sR * dL;
+      double eta;
+      if (A2 == 0.0) {
+        eta = C2 / B2;
+      } else {
+        const double disc = fmax(B2 * B2 - 4.0 * A2 * C2, 0.0);
+        const double sq = sqrt(disc);
+        const double e1 = (B2 >= 0.0) ? (B2 + sq) / (2.0 * A2) : 2.0 * C2 / (B2 - sq);
+        const double e2 = (B2 >= 0.0) ? 2.0 * C2 / (B2 + sq) : (B2 - sq) / (2.0 * A2);
+        eta = (e1 > dL && e1 < dR) ? e1 : e2;
+      }
+      tn = t + eta;
+    } else {
+      const double sL = dpsi * dL * dL;
+      const double c = f - dpsi * dL;
+      tn = (c != 0.0) ? t + dL + sL / c : 0.5 * (a + b);
+    }
+    if (!(tn > a && tn < b)) tn = 0.5 * (a + b);
+    t = tn;
+  }
+  o_out = o;
+  tau_out = t;
+}
+
+struct DcNode {
+  int lo, k;       // node start; non-deflated count
+  double rho;      // ρ (> 0) of the normalised problem
+};
+
+// One thread per (node, root): origin and τ of every root
+__global__ void k_dc_secular(const DcNode* __restrict__ nodes, const int* __restrict__ root_node,
+                             const int* __restrict__ root_j, int nroots, const double* __restrict__ dk,
+                             const double* __restrict__ zk, int* __restrict__ org, double* __restrict__ tau) {
+  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= nroots) return;
+  const DcNode nd = nodes[root_node[g]];
+  int o;
+  double t;
+  secular_root(nd.k, dk + nd.lo, zk + nd.lo, nd.rho, root_j[g], o, t);
+  org[nd.lo + root_j[g]] = o;
+  tau[nd.lo + root_j[g]] = t;
+}
+
+// Gu–Eisenstat: ẑ_i = sign(z_i)·sqrt(−W_i/ρ), W_i = (d_i − λ_i)·Π_{j≠i} (d_i − λ_j)/(d_i − d_j), with
+// d_i − λ_j = (d_i − d_{o_j}) − τ_j. Then U (node block of Up, ld = m): u_ij = ẑ_i/(d_i − λ_j), normalised per column
+// (one CTA per column j, after every ẑ is known: two kernels).
+__global__ void k_dc_zhat(const DcNode* __restrict__ nodes, const int* __restrict__ root_node,
+                          const int* __restrict__ root_j, int nroots, const double* __restrict__ dk,
+                          const double* __restrict__ zk, const int* __restrict__ org, const double* __restrict__ tau,
+                          double* __restrict__ zhat) {
+  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= nroots) return;
+  const DcNode nd = nodes[root_node[g]];
+  const int i = root_j[g], k = nd.k;
+  const double* d = dk + nd.lo;
+  const int* o = org + nd.lo;
+  const double* ta = tau + nd.lo;
+  double w = (d[i] - d[o[i]]) - ta[i];
+  for (int j = 0; j < k; ++j)
+    if (j != i) w *= ((d[i] - d[o[j]]) - ta[j]) / (d[i] - d[j]);
+  const double zi = zk[nd.lo + i];
+  zhat[nd.lo + i] = copysign(sqrt(fmax(-w / nd.rho, 0.0)), zi);
+}
+
+__global__ void __launch_bounds__(256) k_dc_umat(const DcNode* __restrict__ nodes, const int* __restrict__ root_node,
+                                                 const int* __restrict__ root_j, const double* __restrict__ dk,
+                                                 const int* __restrict__ org, const double* __restrict__ tau,
+                                                 const double* __restrict__ zhat, double* __restrict__ U, int m,
+                                                 double* __restrict__ lam_out) {
+  __shared__ double sh[8];
+  const int g = blockIdx.x;  // one CTA per (node, column j)
+  const DcNode nd = nodes[root_node[g]];
+  const int j = root_j[g], k = nd.k, lo = nd.lo;
+  const double* d = dk + lo;
+  const double dj = d[org[lo + j]], tj = tau[lo + j];
+  double ss = 0.0;
+  for (int i = threadIdx.x; i < k; i += 256) {
+    const double u = zhat[lo + i] / ((d[i] - dj) - tj);
+    U[static_cast<long long>(lo + j) * m + lo + i] = u;
+    ss = fma(u, u, ss);
+  }
+  for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = ss;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < 8; ++w) t += sh[w];
+    sh[0] = 1.0 / sqrt(t);
+    lam_out[lo + j] = dj + tj;
+  }
+  __syncthreads();
+  const double inv = sh[0];
+  for (int i = threadIdx.x; i < k; i += 256) U[static_cast<long long>(lo + j) * m + lo + i] *= inv;
+}
+
+// Batched SIMT GEMM on node blocks: Qn[:, lo .. lo+k) (rows lo .. lo+nn) = Qp[:, lo .. lo+k) · U (k x k block), and
+// the deflated columns copied: Qn[:, lo+k .. lo+nn) = Qp[:, lo+k .. lo+nn). 64 x 64 output tiles.
+struct DcTile {
+  int lo, nn, k, r0, c0;  // node, tile origin (node-local row, column)
+};
+__global__ void __launch_bounds__(256) k_dc_gemm(const DcTile* __restrict__ tiles, const double* __restrict__ Qp,
+                                                 const double* __restrict__ U, double* __restrict__ Qn, int m) {
+  __shared__ double as[16][65], bs[16][65];
+  const DcTile T = tiles[blockIdx.x];
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  double acc[4][4] = {};
+  const int lo = T.lo;
+  if (T.c0 >= T.k) {  // copy tile of deflated columns
+    for (int e2 = threadIdx.x; e2 < 64 * 64; e2 += 256) {
+      const int rr = T.r0 + (e2 & 63), cc = T.c0 + (e2 >> 6);
+      if (rr < T.nn && cc < T.nn) Qn[static_cast<long long>(lo + cc) * m + lo + rr] = Qp[static_cast<long long>(lo + cc) * m + lo + rr];
+    }
+    return;
+  }
+  for (int l0 = 0; l0 < T.k; l0 += 16) {
+    for (int e2 = threadIdx.x; e2 < 16 * 64; e2 += 256) {
+      const int a = e2 & 63, l = e2 >> 6;
+      const int rr = T.r0 + a, ll = l0 + l;
+      as[l][a] = (rr < T.nn && ll < T.k) ? Qp[static_cast<long long>(lo + ll) * m + lo + rr] : 0.0;
+      const int lq = e2 & 15, bcol = e2 >> 4;
+      const int cc = T.c0 + bcol;
+      bs[lq][bcol] = (l0 + lq < T.k && cc < T.k) ? U[static_cast<long long>(lo + cc) * m + lo + l0 + lq] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int l = 0; l < 16; ++l) {
+      double pa[4], pb[4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) pa[r] = as[l][tx + 16 * r];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) pb[c] = bs[l][ty + 16 * c];
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[r][c] = fma(pa[r], pb[c], acc[r][c]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int rr = T.r0 + tx + 16 * r, cc = T.c0 + ty + 16 * c;
+      if (rr < T.nn && cc < T.k) Qn[static_cast<long long>(lo + cc) * m + lo + rr] = acc[r][c];
+    }
+}
+
+// ================================================================ (3) back-transformation helpers
+// Vb (m x nbb, ld = m): the reflectors c0 .. c0+nbb of the tridiagonalisation (v_{c+1} = 1, v_r = A(r, c) below)
+__global__ void k_bt_vblock(const double* __restrict__ A, int m, int c0, int nbb, double* __restrict__ Vb) {
+  const int j = blockIdx.y, c = c0 + j;
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < m; r += gridDim.x * blockDim.x) {
+    double v = 0.0;
+    if (c + 1 < m) v = (r == c + 1) ? 1.0 : (r > c + 1 ? A[r + static_cast<long long>(c) * m] : 0.0);
+    Vb[r + static_cast<long long>(j) * m] = v;
+  }
+}
+// T (nbb x nbb, upper, ld = nbb) of the compact WY form, from S = VbᵀVb (ld = nbb) and τ: T_ii = τ_i,
+// T(0:i, i) = −τ_i T(0:i, 0:i) S(0:i, i). One CTA.
+__global__ void k_bt_tmat(const double* __restrict__ S, const double* __restrict__ tau, int c0, int nbb,
+                          double* __restrict__ T) {
+  extern __shared__ double col[];
+  for (int i = 0; i < nbb; ++i) {
+    const double ti = tau[c0 + i];
+    for (int r = threadIdx.x; r < i; r += blockDim.x) {
+      double acc = 0.0;
+      for (int l = r; l < i; ++l) acc = fma(T[r + static_cast<long long>(l) * nbb], S[l + static_cast<long long>(i) * nbb], acc);
+      col[r] = -ti * acc;
+    }
+    __syncthreads();
+    for (int r = threadIdx.x; r < nbb; r += blockDim.x)
+      T[r + static_cast<long long>(i) * nbb] = (r < i) ? col[r] : (r == i ? ti : 0.0);
+    __syncthreads();
+  }
+}
+
+
+// C = alpha·op(A)·B + beta·C (column-major; op(A) = A (M x K, lda) or Aᵀ with A stored K x M), 64 x 64 tiles,
+// 4 x 4 per thread, K-slabs of 16; one fma chain per output over l ascending (deterministic).
+__global__ void __launch_bounds__(256) k_dgemm(int M, int N, int K, double alpha, const double* __restrict__ A, int lda,
+                                               int ta, const double* __restrict__ B, int ldb, double beta,
+                                               double* __restrict__ C, int ldc) {
+  __shared__ double as[16][65], bs[16][65];
+  const int a0 = blockIdx.x * 64, b0 = blockIdx.y * 64;
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  double acc[4][4] = {};
+  for (int l0 = 0; l0 < K; l0 += 16) {
+    for (int e2 = threadIdx.x; e2 < 16 * 64; e2 += 256) {
+      int a, l;
+      if (ta) {  // Aᵀ: element (a, l) = A[l + a·lda]: consecutive threads along l
+        l = e2 & 15;
+        a = e2 >> 4;
+      } else {
+        a = e2 & 63;
+        l = e2 >> 6;
+      }
+      const int ra = a0 + a, ll = l0 + l;
+      double v = 0.0;
+      if (ra < M && ll < K) v = ta ? A[ll + static_cast<long long>(ra) * lda] : A[ra + static_cast<long long>(ll) * lda];
+      as[l][a] = v;
+      const int lq = e2 & 15, bc = e2 >> 4;
+      bs[lq][bc] = (l0 + lq < K && b0 + bc < N) ? B[l0 + lq + static_cast<long long>(b0 + bc) * ldb] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int l = 0; l < 16; ++l) {
+      double pa[4], pb[4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) pa[r] = as[l][tx + 16 * r];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) pb[c] = bs[l][ty + 16 * c];
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[r][c] = fma(pa[r], pb[c], acc[r][c]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int ra = a0 + tx + 16 * r, cb = b0 + ty + 16 * c;
+      if (ra < M && cb < N) {
+        double* p = C + ra + static_cast<long long>(cb) * ldc;
+        *p = (beta == 0.0) ? alpha * acc[r][c] : fma(alpha, acc[r][c], beta * *p);
+      }
+    }
+}
+
+// Y_sorted[:, j] = Q[:, perm[j]] (ld = m), θ_j = lam[perm[j]]
+__global__ void k_dc_final(const int* __restrict__ perm, const double* __restrict__ Q, const double* __restrict__ lam,
+                           int m, double* __restrict__ Y, double* __restrict__ theta) {
+  const int j = blockIdx.y;
+  const int p = perm[j];
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < m; r += gridDim.x * blockDim.x)
+    Y[r + static_cast<long long>(j) * m] = Q[r + static_cast<long long>(p) * m];
+  if (blockIdx.x == 0 && threadIdx.x == 0) theta[j] = lam[p];
+}
+
+// Y(0:rows, 0:cols) −= P (Y with leading dimension ldy, P with ldp)
+__global__ void k_sub_strided(double* __restrict__ Y, int ldy, const double* __restrict__ P, int ldp, int rows, int cols) {
+  const int j = blockIdx.y;
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += gridDim.x * blockDim.x)
+    Y[r + static_cast<long long>(j) * ldy] -= P[r + static_cast<long long>(j) * ldp];
+}
+
+}  // namespace
+
+size_t syev_trd_partials(int m, int G) {
+  const int mt = (m + TB - 1) / TB;
+  return static_cast<size_t>(G) * (2 + 2 * NB) + static_cast<size_t>(mt) * (mt + 1) / 2 * 2 * TB;
+}
+
+int syev_trd_grid(int m) {
+  static int per = -1;
+  if (per < 0) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_trd_panel, TT, 0);
+    per = std::max(per, 1);
+  }
+  int dev = 0, nsm = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  const int mt = (m + TB - 1) / TB;
+  // enough CTAs for the tile products (~mt²/2 tiles) but no more than co-reside; fewer CTAs = cheaper barriers
+  const int want = std::max(1, std::min(mt * (mt + 1) / 2, 4 * mt));
+  return std::min(want, nsm * per);
+}
+
+// Tridiagonalise A (m x m, lda = m, lower triangle read; overwritten: reflectors below the sub-diagonal).
+cudaError_t syev_tridiag(double* A, int m, double* d, double* e, double* tau, double* V, double* W, double* part,
+                         int G, cudaStream_t s) {
+  const int mt = (m + TB - 1) / TB;
+  double* yp = part + static_cast<size_t>(G) * (2 + 2 * NB);
+  for (int k0 = 0; k0 < m; k0 += NB) {
+    const int nb = std::min(NB, m - k0);
+    PanelArgs P{A, m, k0, nb, V, W, d, e, tau, part, yp};
+    void* args[] = {&P};
+    cudaError_t err = cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_trd_panel), dim3(G), dim3(TT), args, 0, s);
+    if (err != cudaSuccess) return err;
+    const int k1 = k0 + nb;
+    if (k1 < m) {
+      const int J0 = k1 / TB, na = mt - J0;
+      k_trd_update<<<na * (na + 1) / 2 + nb, TT, 0, s>>>(A, m, k0, nb, V, W);
+    } else {
+      k_trd_update<<<nb, TT, 0, s>>>(A, m, k0, nb, V, W);  // only the reflector copy (na = 0 tiles)
+    }
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace ozr
+
+namespace ozr {
+
+void* SyevWorkspace::get(int slot, size_t bytes) {
+  if (static_cast<int>(bufs.size()) <= slot) bufs.resize(slot + 1, {nullptr, 0});
+  auto& b = bufs[slot];
+  if (bytes == 0) bytes = 16;
+  if (b.second < bytes) {
+    if (b.first) cudaFree(b.first);
+    b.first = nullptr;
+    b.second = 0;
+    if (cudaMalloc(&b.first, bytes) != cudaSuccess) {
+      cudaGetLastError();
+      return nullptr;
+    }
+    b.second = bytes;
+  }
+  return b.first;
+}
+SyevWorkspace::~SyevWorkspace() {
+  for (auto& b : bufs)
+    if (b.first) cudaFree(b.first);
+}
+
+void syev_dgemm(int M, int N, int K, double alpha, const double* A, int lda, bool ta, const double* B, int ldb,
+                double beta, double* C, int ldc, cudaStream_t s) {
+  if (M <= 0 || N <= 0) return;
+  k_dgemm<<<dim3((M + 63) / 64, (N + 63) / 64), 256, 0, s>>>(M, N, K, alpha, A, lda, ta ? 1 : 0, B, ldb, beta, C, ldc);
+}
+
+namespace {
+enum { W_D, W_E, W_TAU, W_V, W_W, W_PART, W_Q0, W_Q1, W_QP, W_U, W_DMOD, W_LAMO, W_LAMN, W_DK, W_ZK, W_ZH, W_TS,
+       W_ORG, W_Z, W_I, W_D2, W_NODE, W_TILE, W_ERR, W_VB, W_S, W_T, W_WT, W_WT2, W_P, W_STAGE };
+
+struct Node {
+  int lo, mid, hi;
+};
+
+bool cuda_ok(cudaError_t e, std::string* err, const char* what) {
+  if (e == cudaSuccess) return true;
+  if (err) *err = std::string(what) + ": " + cudaGetErrorString(e);
+  return false;
+}
+}  // namespace
+
+// K (m x m, ld = m; the lower triangle is read) → eigenvalues θ ascending (device, m) and eigenvectors Y (device,
+// m x m, ld = m; may alias K). gemm: the large products of the D&C merges and the back-transformation.
+int dense_syev(SyevWorkspace& w, int m, double* K, double* theta, double* Y, const SyevGemm& gemm, int big_gemm_min,
+               cudaStream_t s, std::string* err) {
+#define SY_ALLOC(ptr, slot, T, cnt)                                        \
+  T* ptr = static_cast<T*>(w.get(slot, sizeof(T) * static_cast<size_t>(cnt))); \
+  if (!ptr) {                                                              \
+    if (err) *err = "dense eigensolver: out of device memory";             \
+    return 8;                                                              \
+  }
+  const size_t mm = static_cast<size_t>(m) * m;
+  const int G = syev_trd_grid(m);
+  SY_ALLOC(d, W_D, double, m);
+  SY_ALLOC(e, W_E, double, m);
+  SY_ALLOC(tau, W_TAU, double, m);
+  SY_ALLOC(V, W_V, double, static_cast<size_t>(m) * NB);
+  SY_ALLOC(Wp, W_W, double, static_cast<size_t>(m) * NB);
+  SY_ALLOC(part, W_PART, double, syev_trd_partials(m, G));
+  SY_ALLOC(Q0, W_Q0, double, mm);
+  SY_ALLOC(Q1, W_Q1, double, mm);
+  SY_ALLOC(Qp, W_QP, double, mm);
+  SY_ALLOC(U, W_U, double, mm);
+  SY_ALLOC(dmod, W_DMOD, double, m);
+  SY_ALLOC(lamo, W_LAMO, double, m);
+  SY_ALLOC(dk, W_DK, double, m);
+  SY_ALLOC(zk, W_ZK, double, m);
+  SY_ALLOC(zh, W_ZH, double, m);
+  SY_ALLOC(ts, W_TS, double, m);
+  SY_ALLOC(org, W_ORG, int, m);
+  SY_ALLOC(zv, W_Z, double, m);
+  SY_ALLOC(derr, W_ERR, int, 4);
+  // staging for the per-level host decisions: pinned host memory
+  std::vector<double> hd(m), he(m), hlam(m), hz(m);
+  if (!cuda_ok(cudaMemsetAsync(derr, 0, 4 * sizeof(int), s), err, "memset")) return 6;
+  // ---- (1) tridiagonalise
+  if (!cuda_ok(syev_tridiag(K, m, d, e, tau, V, Wp, part, G, s), err, "tridiagonalisation")) return 6;
+  if (!cuda_ok(cudaMemcpyAsync(hd.data(), d, m * sizeof(double), cudaMemcpyDeviceToHost, s), err, "D2H")) return 6;
+  if (m > 1 && !cuda_ok(cudaMemcpyAsync(he.data(), e, (m - 1) * sizeof(double), cudaMemcpyDeviceToHost, s), err, "D2H"))
+    return 6;
+  if (!cuda_ok(cudaStreamSynchronize(s), err, "sync")) return 6;
+  he[m - 1] = 0.0;
+  // ---- (2) divide and conquer: the tree (levels of internal nodes, leaves)
+  std::vector<std::vector<Node>> levels;
+  std::vector<int> llo, lhi;
+  std::vector<double> dm(hd);
+  {
+    struct Item { int lo, hi, depth; };
+    std::vector<Item> stack{{0, m, 0}};
+    while (!stack.empty()) {
+      Item it = stack.back();
+      stack.pop_back();
+      if (it.hi - it.lo <= LEAF) {
+        llo.push_back(it.lo);
+        lhi.push_back(it.hi);
+        continue;
+      }
+      const int mid = (it.lo + it.hi) / 2;
+      if (static_cast<int>(levels.size()) <= it.depth) levels.resize(it.depth + 1);
+      levels[it.depth].push_back({it.lo, mid, it.hi});
+      const double ab = std::fabs(he[mid - 1]);
+      dm[mid - 1] -= ab;  // tearing: T = diag(T1', T2') + |β| v vᵀ, v = e_{mid−1} + sign(β) e_mid
+      dm[mid] -= ab;
+      stack.push_back({it.lo, mid, it.depth + 1});
+      stack.push_back({mid, it.hi, it.depth + 1});
+    }
+  }
+  const int nleaf = static_cast<int>(llo.size());
+  SY_ALLOC(ibuf, W_I, int, 16 * static_cast<size_t>(m) + 4 * nleaf + 64);
+  SY_ALLOC(dbuf, W_D2, double, 4 * static_cast<size_t>(m) + 64);
+  {
+    std::vector<int> li(2 * nleaf);
+    for (int q = 0; q < nleaf; ++q) {
+      li[q] = llo[q];
+      li[nleaf + q] = lhi[q];
+    }
+    if (!cuda_ok(cudaMemcpyAsync(ibuf, li.data(), li.size() * sizeof(int), cudaMemcpyHostToDevice, s), err, "H2D") ||
+        !cuda_ok(cudaMemcpyAsync(dmod, dm.data(), m * sizeof(double), cudaMemcpyHostToDevice, s), err, "H2D"))
+      return 6;
+    k_dc_leaf<<<nleaf, LEAF, 0, s>>>(ibuf, ibuf + nleaf, dmod, e, lamo, Q0, m, derr);
+    if (!cuda_ok(cudaGetLastError(), err, "leaf solve")) return 6;
+    if (!cuda_ok(cudaStreamSynchronize(s), err, "sync")) return 6;  // li is about to go out of scope
+  }
+  double* Q = Q0;  // node blocks on the diagonal; every merge rewrites its block in place (from the Qp copy)
+  const double eps = 1.1102230246251565e-16;
+  for (int lev = static_cast<int>(levels.size()) - 1; lev >= 0; --lev) {
+    const std::vector<Node>& nodes = levels[lev];
+    const int nn_nodes = static_cast<int>(nodes.size());
+    // z of every merge, and the current eigenvalues, to the host
+    std::vector<int> ni(3 * nn_nodes);
+    std::vector<double> sg(nn_nodes);
+    for (int q = 0; q < nn_nodes; ++q) {
+      ni[q] = nodes[q].lo;
+      ni[nn_nodes + q] = nodes[q].mid;
+      ni[2 * nn_nodes + q] = nodes[q].hi;
+      sg[q] = he[nodes[q].mid - 1] < 0 ? -1.0 : 1.0;
+    }
+    if (!cuda_ok(cudaMemcpyAsync(ibuf, ni.data(), ni.size() * sizeof(int), cudaMemcpyHostToDevice, s), err, "H2D") ||
+        !cuda_ok(cudaMemcpyAsync(dbuf, sg.data(), nn_nodes * sizeof(double), cudaMemcpyHostToDevice, s), err, "H2D"))
+      return 6;
+    k_dc_zvec<<<dim3(8, nn_nodes), 256, 0, s>>>(ibuf, ibuf + nn_nodes, ibuf + 2 * nn_nodes, dbuf, Q, m, zv);
+    if (!cuda_ok(cudaMemcpyAsync(hz.data(), zv, m * sizeof(double), cudaMemcpyDeviceToHost, s), err, "D2H") ||
+        !cuda_ok(cudaMemcpyAsync(hlam.data(), lamo, m * sizeof(double), cudaMemcpyDeviceToHost, s), err, "D2H") ||
+        !cuda_ok(cudaStreamSynchronize(s), err, "sync"))
+      return 6;
+    // host: sort, deflation (LAPACK dlaed2's rules), the Qp column sources and rotations
+    std::vector<int> src(m, 0), rot_off(nn_nodes + 1, 0), root_node, root_j;
+    std::vector<int4> rot_idx;
+    std::vector<double2> rot_cs;
+    std::vector<double> hdk(m, 0.0), hzk(m, 0.0), hlamn(hlam);
+    std::vector<DcNode> dn(nn_nodes);
+    std::vector<DcTile> tiles;
+    std::vector<int> big;  // nodes whose merge product goes to the big GEMM
+    for (int q = 0; q < nn_nodes; ++q) {
+      const int lo = nodes[q].lo, n = nodes[q].hi - lo;
+      const double rho = 2.0 * std::fabs(he[nodes[q].mid - 1]);
+      std::vector<int> idx(n);
+      for (int a = 0; a < n; ++a) idx[a] = a;
+      std::stable_sort(idx.begin(), idx.end(), [&](int a, int b) { return hlam[lo + a] < hlam[lo + b]; });
+      std::vector<double> D(n), Z(n);
+      double dmax = 0.0, zmax = 0.0;
+      for (int a = 0; a < n; ++a) {
+        D[a] = hlam[lo + idx[a]];
+        Z[a] = hz[lo + idx[a]];
+        dmax = std::max(dmax, std::fabs(D[a]));
+        zmax = std::max(zmax, std::fabs(Z[a]));
+      }
+      const double tol = 8.0 * eps * std::max(dmax, zmax);
+      std::vector<int> keep, defl;
+      std::vector<std::pair<int, int>> rots;
+      std::vector<double2> cs;
+      int pj = -1;
+      for (int j = 0; j < n; ++j) {
+        if (rho * std::fabs(Z[j]) <= tol) {
+          defl.push_back(j);
+          continue;
+        }
+        if (pj < 0) {
+          pj = j;
+          continue;
+        }
+        double sv = Z[pj], cv = Z[j];
+        const double tv = std::hypot(cv, sv);
+        const double t = D[j] - D[pj];
+        cv /= tv;
+        sv = -sv / tv;
+        if (std::fabs(t * cv * sv) <= tol) {
+          Z[j] = tv;
+          Z[pj] = 0.0;
+          rots.push_back({pj, j});
+          cs.push_back(make_double2(cv, sv));
+          const double t2 = D[pj] * cv * cv + D[j] * sv * sv;
+          D[j] = D[pj] * sv * sv + D[j] * cv * cv;
+          D[pj] = t2;
+          defl.push_back(pj);
+          pj = j;
+        } else {
+          keep.push_back(pj);
+          pj = j;
+        }
+      }
+      if (pj >= 0) keep.push_back(pj);
+      const int k = static_cast<int>(keep.size());
+      std::vector<int> pos(n);
+      for (int a = 0; a < k; ++a) pos[keep[a]] = a;
+      for (int a = 0; a < static_cast<int>(defl.size()); ++a) pos[defl[a]] = k + a;
+      for (int a = 0; a < n; ++a) src[lo + pos[a]] = idx[a];
+      for (size_t r = 0; r < rots.size(); ++r) {
+        rot_idx.push_back(make_int4(pos[rots[r].first], pos[rots[r].second], 0, 0));
+        rot_cs.push_back(cs[r]);
+      }
+      rot_off[q + 1] = static_cast<int>(rot_idx.size());
+      for (int a = 0; a < k; ++a) {
+        hdk[lo + a] = D[keep[a]];
+        hzk[lo + a] = Z[keep[a]];
+      }
+      for (int a = 0; a < static_cast<int>(defl.size()); ++a) hlamn[lo + k + a] = D[defl[a]];
+      dn[q] = DcNode{lo, k, rho};
+      for (int j = 0; j < k; ++j) {
+        root_node.push_back(q);
+        root_j.push_back(j);
+      }
+      const bool use_big = k >= big_gemm_min && gemm;
+      if (use_big) big.push_back(q);
+      // GEMM tiles (columns [c0, min(c0 + 64, k))) unless the big product takes the node; copy tiles (origin ≥ k)
+      // for the deflated columns: one starting at k, then the 64-aligned ones above it (overlaps copy twice)
+      for (int r0 = 0; r0 < n; r0 += 64) {
+        if (!use_big)
+          for (int c0 = 0; c0 < k; c0 += 64) tiles.push_back(DcTile{lo, n, k, r0, c0});
+        if (k < n) tiles.push_back(DcTile{lo, n, k, r0, k});
+        for (int c0 = (k / 64 + 1) * 64; c0 < n; c0 += 64) tiles.push_back(DcTile{lo, n, k, r0, c0});
+      }
+    }
+    const int nroots = static_cast<int>(root_node.size());
+    // upload: ints [src m | rot_off | root_node | root_j], int4 rot_idx, double2 rot_cs, dk, zk, lamn (deflated)
+    std::vector<int> pk;
+    pk.insert(pk.end(), src.begin(), src.end());
+    const size_t o_roff = pk.size();
+    pk.insert(pk.end(), rot_off.begin(), rot_off.end());
+    const size_t o_rn = pk.size();
+    pk.insert(pk.end(), root_node.begin(), root_node.end());
+    const size_t o_rj = pk.size();
+    pk.insert(pk.end(), root_j.begin(), root_j.end());
+    while (pk.size() % 4) pk.push_back(0);
+    const size_t o_ri = pk.size();
+    for (const int4& v : rot_idx) {
+      pk.push_back(v.x); pk.push_back(v.y); pk.push_back(v.z); pk.push_back(v.w);
+    }
+    const size_t o_nodes = pk.size();
+    const int* dnp = reinterpret_cast<const int*>(dn.data());
+    pk.insert(pk.end(), dnp, dnp + dn.size() * sizeof(DcNode) / sizeof(int));
+    const size_t o_tiles = pk.size();
+    const int* tp = reinterpret_cast<const int*>(tiles.data());
+    pk.insert(pk.end(), tp, tp + tiles.size() * sizeof(DcTile) / sizeof(int));
+    int* dpk = static_cast<int*>(w.get(W_NODE, pk.size() * sizeof(int) + 16));
+    double2* dcs = static_cast<double2*>(w.get(W_TILE, (rot_cs.size() + 1) * sizeof(double2)));
+    if (!dpk || !dcs) {
+      if (err) *err = "dense eigensolver: out of device memory";
+      return 8;
+    }
+    if (!cuda_ok(cudaMemcpyAsync(dpk, pk.data(), pk.size() * sizeof(int), cudaMemcpyHostToDevice, s), err, "H2D") ||
+        (!rot_cs.empty() && !cuda_ok(cudaMemcpyAsync(dcs, rot_cs.data(), rot_cs.size() * sizeof(double2),
+                                                     cudaMemcpyHostToDevice, s), err, "H2D")) ||
+        !cuda_ok(cudaMemcpyAsync(dk, hdk.data(), m * sizeof(double), cudaMemcpyHostToDevice, s), err, "H2D") ||
+        !cuda_ok(cudaMemcpyAsync(zk, hzk.data(), m * sizeof(double), cudaMemcpyHostToDevice, s), err, "H2D") ||
+        !cuda_ok(cudaMemcpyAsync(lamo, hlamn.data(), m * sizeof(double), cudaMemcpyHostToDevice, s), err, "H2D"))
+      return 6;
+    const DcNode* dnd = reinterpret_cast<const DcNode*>(dpk + o_nodes);
+    int maxn = 0;
+    for (const Node& nd : nodes) maxn = std::max(maxn, nd.hi - nd.lo);
+    // the node lo/hi arrays for permrot: reuse ibuf (still holds lo | mid | hi)
+    k_dc_permrot<<<dim3((maxn + 127) / 128, nn_nodes), 128, 0, s>>>(ibuf, ibuf + 2 * nn_nodes, dpk, dpk + o_roff,
+                                                                   reinterpret_cast<const int4*>(dpk + o_ri), dcs, Q, Qp, m);
+    if (nroots > 0) {
+      k_dc_secular<<<(nroots + 127) / 128, 128, 0, s>>>(dnd, dpk + o_rn, dpk + o_rj, nroots, dk, zk, org, ts);
+      k_dc_zhat<<<(nroots + 127) / 128, 128, 0, s>>>(dnd, dpk + o_rn, dpk + o_rj, nroots, dk, zk, org, ts, zh);
+      k_dc_umat<<<nroots, 256, 0, s>>>(dnd, dpk + o_rn, dpk + o_rj, dk, org, ts, zh, U, m, lamo);
+    }
+    if (!tiles.empty())
+      k_dc_gemm<<<static_cast<int>(tiles.size()), 256, 0, s>>>(reinterpret_cast<const DcTile*>(dpk + o_tiles), Qp, U, Q, m);
+    if (!cuda_ok(cudaGetLastError(), err, "merge")) return 6;
+    for (int q : big) {  // Qn[:, lo .. lo+k) = Qp[:, lo .. lo+k) · U_kk (node block)
+      const int lo = nodes[q].lo, n = nodes[q].hi - lo, k = dn[q].k;
+      const size_t off = static_cast<size_t>(lo) * m + lo;
+      if (gemm(n, k, k, Qp + off, m, false, U + off, m, Q + off, m) != 0) {
+        if (err) *err = "dense eigensolver: merge product failed";
+        return 6;
+      }
+    }
+    if (!cuda_ok(cudaStreamSynchronize(s), err, "sync")) return 6;  // the staging vectors go out of scope
+  }
+  // eigenvalues ascending, columns permuted accordingly
+  if (!cuda_ok(cudaMemcpyAsync(hlam.data(), lamo, m * sizeof(double), cudaMemcpyDeviceToHost, s), err, "D2H") ||
+      !cuda_ok(cudaStreamSynchronize(s), err, "sync"))
+    return 6;
+  std::vector<int> perm(m);
+  for (int a = 0; a < m; ++a) perm[a] = a;
+  std::stable_sort(perm.begin(), perm.end(), [&](int a, int b) { return hlam[a] < hlam[b]; });
+  if (!cuda_ok(cudaMemcpyAsync(ibuf, perm.data(), m * sizeof(int), cudaMemcpyHostToDevice, s), err, "H2D")) return 6;
+  double* Yt = Q1;  // Q_T sorted
+  k_dc_final<<<dim3(std::max(1, std::min(16, (m + 255) / 256)), m), 256, 0, s>>>(ibuf, Q, lamo, m, Yt, theta);
+  // ---- (3) back-transformation Y = Qᴴ·Q_T, blocks of NBB reflectors from the last to the first
+  constexpr int NBB = 128;
+  SY_ALLOC(Vb, W_VB, double, static_cast<size_t>(m) * NBB);
+  SY_ALLOC(S, W_S, double, NBB * NBB);
+  SY_ALLOC(Tm, W_T, double, NBB * NBB);
+  SY_ALLOC(Wt, W_WT, double, static_cast<size_t>(NBB) * m);
+  SY_ALLOC(Wt2, W_WT2, double, static_cast<size_t>(NBB) * m);
+  double* Pb = nullptr;
+  const bool bigbt = gemm && m >= big_gemm_min;
+  if (bigbt) {
+    Pb = static_cast<double*>(w.get(W_P, sizeof(double) * mm));
+    if (!Pb) {
+      if (err) *err = "dense eigensolver: out of device memory";
+      return 8;
+    }
+  }
+  const int nref = m - 1;  // reflectors c = 0 .. m−2 (the last is the identity)
+  for (int c0 = ((nref - 1) / NBB) * NBB; c0 >= 0; c0 -= NBB) {
+    const int nbb = std::min(NBB, nref - c0);
+    if (nbb <= 0) continue;
+    const int r0 = c0 + 1, rows = m - r0;  // rows of Vb that can be nonzero
+    k_bt_vblock<<<dim3(std::max(1, std::min(32, (m + 255) / 256)), nbb), 256, 0, s>>>(K, m, c0, nbb, Vb);
+    syev_dgemm(nbb, nbb, rows, 1.0, Vb + r0, m, true, Vb + r0, m, 0.0, S, nbb, s);  // S = VbᵀVb
+    k_bt_tmat<<<1, 128, NBB * sizeof(double), s>>>(S, tau, c0, nbb, Tm);
+    if (bigbt) {
+      if (gemm(nbb, m, rows, Vb + r0, m, true, Yt + r0, m, Wt, nbb) != 0) {  // Wt = VbᵀY
+        if (err) *err = "dense eigensolver: back-transformation product failed";
+        return 6;
+      }
+    } else {
+      syev_dgemm(nbb, m, rows, 1.0, Vb + r0, m, true, Yt + r0, m, 0.0, Wt, nbb, s);
+    }
+    syev_dgemm(nbb, m, nbb, 1.0, Tm, nbb, false, Wt, nbb, 0.0, Wt2, nbb, s);  // Wt2 = T·Wt
+    if (bigbt) {
+      if (gemm(rows, m, nbb, Vb + r0, m, false, Wt2, nbb, Pb, rows) != 0) {  // P = Vb·Wt2
+        if (err) *err = "dense eigensolver: back-transformation product failed";
+        return 6;
+      }
+      k_sub_strided<<<dim3(std::max(1, std::min(16, (rows + 255) / 256)), m), 256, 0, s>>>(Yt + r0, m, Pb, rows, rows, m);
+    } else {
+      syev_dgemm(rows, m, nbb, -1.0, Vb + r0, m, false, Wt2, nbb, 1.0, Yt + r0, m, s);  // Y −= Vb·Wt2
+    }
+  }
+  if (!cuda_ok(cudaGetLastError(), err, "back-transformation")) return 6;
+  if (Y != Yt && !cuda_ok(cudaMemcpyAsync(Y, Yt, mm * sizeof(double), cudaMemcpyDeviceToDevice, s), err, "copy")) return 6;
+  int herr = 0;
+  if (!cuda_ok(cudaMemcpyAsync(&herr, derr, sizeof(int), cudaMemcpyDeviceToHost, s), err, "D2H") ||
+      !cuda_ok(cudaStreamSynchronize(s), err, "sync"))
+    return 6;
+  if (herr) {
+    if (err) *err = "dense eigensolver: a leaf QL iteration did not converge";
+    return 6;
+  }
+  return 0;
+#undef SY_ALLOC
+}
+
+}  // namespace ozr

@@ -1,0 +1,107 @@
+"""GPU tests of ozr_syev — the hand-written dense symmetric eigensolver of the large-group Rayleigh–Ritz
+sub-solve (R13; Householder tridiagonalisation, Cuppen divide and conquer with Gu–Eisenstat
+eigenvectors, blocked back-transformation; include/ozr.h).
+
+Pinned against (a) the oracle's __float128 cyclic Jacobi (oracle/ddmm.c) for m ≤ 48: eigenvalues to
+1e-14·‖K‖ and eigenvector columns up to sign to u‖K‖/gap; (b) at any size, the properties a backward-stable
+eigensolver has: ‖KY − YΘ‖_F ≤ c·u·‖K‖_F, ‖YᵀY − I‖_max ≤ c·u·√m·log m, θ ascending, and the exactly known
+spectrum of the Householder family A = H diag(λ) H to c·u·‖K‖. Sizes span one leaf (≤ 32), several
+merge levels, the INT8 product path (dimension ≥ 1024), ragged tails, and spectra with heavy deflation (repeated
+and graded eigenvalues, a diagonal matrix)."""
+import numpy as np
+import pytest
+import torch
+
+import paper_2602_19090_b200 as ozr
+import workloads as W
+from oracle import _clib
+
+pytestmark = pytest.mark.gpu
+
+U = 2.0 ** -53
+
+
+def _run(ctx, K):
+    Kd = ozr.colmajor(torch.from_numpy(np.asfortranarray(K)).cuda())
+    th, Y = ozr.ozr_syev(ctx, Kd)
+    return th.cpu().numpy(), Y.cpu().numpy()
+
+
+def _check_props(K, th, Y, c=64.0):
+    m = K.shape[0]
+    nK = np.linalg.norm(K)
+    res = np.linalg.norm(K @ Y - Y * th[None, :])
+    orth = np.max(np.abs(Y.T @ Y - np.eye(m)))
+    assert np.all(np.diff(th) >= 0), "not ascending"
+    assert res <= c * U * max(nK, 1e-300) * np.sqrt(np.log2(m + 1) + 1), (res, nK)
+    assert orth <= c * U * np.sqrt(m) * (np.log2(m + 1) + 1), orth
+    return res, orth
+
+
+def _random_sym(m, seed, scale=1.0):
+    G = np.random.default_rng(seed).standard_normal((m, m)) * scale
+    return (G + G.T) * 0.5
+
+
+@pytest.mark.parametrize("m", [1, 2, 3, 17, 32, 33, 48])
+def test_syev_vs_quad_jacobi(ctx, m):
+    K = _random_sym(m, 100 + m)
+    th, Y = _run(ctx, K)
+    wh, wl, Vh, Vl, _ = _clib.jacobi_q(K)
+    nK = np.linalg.norm(K, 2)
+    assert np.max(np.abs(th - (wh + wl))) <= 1e-14 * nK
+    gaps = np.array([np.min(np.abs(np.delete(wh, j) - wh[j])) if m > 1 else np.inf for j in range(m)])
+    for j in range(m):
+        v = Vh[:, j] + Vl[:, j]
+        err = min(np.linalg.norm(Y[:, j] - v), np.linalg.norm(Y[:, j] + v))
+        assert err <= 64 * U * nK / gaps[j] + 1e-15, (j, err, gaps[j])
+    _check_props(K, th, Y)
+
+
+@pytest.mark.parametrize("m", [64, 100, 257, 700, 1031, 2100])
+def test_syev_random_properties(ctx, m):
+    K = _random_sym(m, 7 + m)
+    th, Y = _run(ctx, K)
+    _check_props(K, th, Y)
+    ref = np.linalg.eigvalsh(K)
+    assert np.max(np.abs(th - ref)) <= 64 * U * np.linalg.norm(K, 2) * np.sqrt(m)
+
+
+@pytest.mark.parametrize("m", [128, 1100])
+def test_syev_graded_group_spectrum(ctx, m):
+    """The shape of BASELINE c4's first large group: eigenvalues graded over 12 decades (1e-14 .. 1e-2) plus a
+    dense 1e-8 perturbation (the FP32 start's coupling) — heavy deflation at every merge level."""
+    rng = np.random.default_rng(m)
+    Q = W.haar(m, rng)
+    lam = np.geomspace(1e-14, 1e-2, m)
+    K = (Q * lam[None, :]) @ Q.T
+    K = (K + K.T) * 0.5 + 1e-8 * _random_sym(m, 3)
+    th, Y = _run(ctx, K)
+    _check_props(K, th, Y)
+    ref = np.linalg.eigvalsh(K)
+    assert np.max(np.abs(th - ref)) <= 64 * U * np.linalg.norm(K, 2) * np.sqrt(m)
+
+
+@pytest.mark.parametrize("mexp", [6, 8])
+def test_syev_householder_exact_spectrum(ctx, mexp):
+    """A = H diag(λ) H is exact in fp64 with exactly known eigenvalues λ, including a doubled one."""
+    A, lam, X, H, lam_cols = W.householder_exact(mexp, lam_bits=12, seed=2)
+    th, Y = _run(ctx, A)
+    assert np.max(np.abs(th - lam)) <= 32 * U * np.sqrt(A.shape[0])
+    _check_props(A, th, Y)
+
+
+@pytest.mark.parametrize("m", [40, 300])
+def test_syev_repeated_and_diagonal(ctx, m):
+    """Exactly repeated eigenvalues (every merge deflates by rotation) and a diagonal matrix (ρ = 0)."""
+    d = np.repeat(np.arange(m // 4, dtype=np.float64), 4)[:m]
+    Q = W.haar(m, np.random.default_rng(5))
+    K = (Q * d[None, :]) @ Q.T
+    K = (K + K.T) * 0.5
+    th, Y = _run(ctx, K)
+    _check_props(K, th, Y)
+    assert np.max(np.abs(th - np.sort(d))) <= 64 * U * m
+    D = np.diag(np.random.default_rng(6).permutation(m).astype(np.float64))
+    th, Y = _run(ctx, D)
+    assert np.array_equal(th, np.arange(m, dtype=np.float64))
+    _check_props(D, th, Y)

@@ -299,3 +299,35 @@ def test_certificate_tracks_forward_error_c4p_recipe():
     X, lam, hist = orf.refine_to_tol(A, X0, lam0, cfg["delta"])
     assert hist[-1]["stop"] == "converged"
     assert orf.forward_error(Xh, Xl, X, lh, lam) <= cfg["delta"]
+
+
+@pytest.mark.parametrize("m", [3, 6])
+def test_second_order_defect_vs_exact_correction(m):
+    """R12's defect formula against the EXACT correction: A = H diag(λ) H with X = H exactly, the
+    start X̂ = X(I + F₀) with a generic (non-skew) F₀ of size 1e-4, one untruncated sweep (X̂^(1) = X̂). The
+    exact E solves X = X̂(I + E), so E − Ẽ is known to ~1e-16; second_order_defect(Ẽ) must equal −(E − Ẽ) up to
+    third-order terms (≤ 1 % in Frobenius norm; measured 5e-4). At n = 8 (gaps ~ spread, so the unamplified
+    terms matter) dropping the Ẽ² term, the diagonal ½‖ẽ_j‖² or transposing Q miss by ≥ 10 %."""
+    A, lam, X, H, lam_cols = W.householder_exact(m, lam_bits=12, seed=5)
+    n = A.shape[0]
+    F0 = 1e-4 * np.random.default_rng(2).standard_normal((n, n))
+    X0 = X @ (np.eye(n) + F0)
+    Xn, ln, info = orf.sweep(A, X0, lam, 1e-12, truncate=False)
+    assert not info["clusters"]
+    Et = info["E"]
+    E = np.linalg.solve(X0, X) - np.eye(n)
+    true = E - Et
+    D = orf.second_order_defect(Et, ln)
+    rel = np.linalg.norm(D + true) / np.linalg.norm(true)
+    assert rel <= 0.01, rel
+    if m == 3:
+        C = (ln[:, None] - ln[None, :]) * Et
+        dl = ln[None, :] - ln[:, None]
+        off = ~np.eye(n, dtype=bool)
+        Qh = np.where(off, (Et.T @ C) / np.where(off, dl, 1.0), 0.0)
+        for bad in (Qh, Qh - Et @ Et, Qh.T - Et @ Et - np.diag(0.5 * np.sum(Et * Et, axis=0))):
+            assert np.linalg.norm(bad + true) / np.linalg.norm(true) >= 0.1
+    # and its 2-norm is the forward error of the returned X̂ (X̂_new − X = X̂(Ẽ − E)) up to the same terms
+    fe = float(np.linalg.norm(Xn - X, 2))
+    c = orf.certificate(Et, ln)
+    assert abs(c["est_q"] - fe) <= 0.03 * fe + 4 * 2.0 ** -53, (c, fe)
