@@ -512,7 +512,7 @@ def main():
         ttt_c4 = {"ms": t0.elapsed_time(t1), "sweeps": len(h4), "status": int(st4), "delta": cfg4["delta"],
                   "largest_group": max(h["max_cluster"] for h in h4),
                   "workload": "c4: " + _describe(cfg4, cfg4["n"]),
-                  "note": "FP32 start: the first sweep's 6628-column group takes the dense sub-solve (cuSOLVER syevd)"}
+                  "note": "FP32 start: the first sweep's 6628-column group takes the dense sub-solve (hand-written eigensolver, syev.cu)"}
         del A4, X4, l4, Xw, lw
 
     # the per-product Ozaki GEMM: ozr_gemm C = A·X̂₀ through the C ABI, split of both operands,

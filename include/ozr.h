@@ -130,8 +130,9 @@ typedef struct {
                         diagonal, which is always exact); reports ‖R‖_F and the OA threshold ω, and
                         ozr_last_R returns R. Default 0 */
   int dense_cluster; /* cluster_mode 1: groups of at least this many columns are solved by a dense symmetric
-                        eigensolver (cuSOLVER syevd, loaded on first use; OZR_ERR_CUDA if it cannot be
-                        loaded) instead of the parallel Jacobi; same K, same conventions (R13).
+                        eigensolver (ozr_syev: Householder tridiagonalisation, divide and conquer, back-
+                        transformation, all in libozr's kernels) instead of the parallel Jacobi; same K,
+                        same conventions (R13).
                         Default 192 (smaller groups: one Jacobi CTA each, all groups in one launch) */
   int row_nnz;       /* k = maximum number of nonzeros in a row of A (beta_mode 2; also the contraction
                         length of the V-product's dropped-pair bound, R8). 0 → n (dense)            */
@@ -236,6 +237,13 @@ ozr_status ozr_refine_to_tol(ozr_ctx ctx, const double* A, int64_t n, int64_t ld
  * propagates), OZR_ERR_CUDA (no convergence of a leaf iteration), OZR_ERR_NOMEM.
  * ------------------------------------------------------------------------------------------------ */
 ozr_status ozr_syev(ozr_ctx ctx, int64_t m, const double* K, int64_t ldk, double* theta, double* Y, int64_t ldy);
+/* Its two stages alone (stage checks): ozr_syev_tridiag overwrites K (device, m x m, ldk = m, lower triangle read)
+ * with the Householder vectors v_c below its sub-diagonal (v_{c+1} = 1 implied; H_c = I − τ_c v_c v_cᵀ,
+ * H_0⋯H_{m−2} K H_{m−2}⋯H_0 = T) and writes T's diagonal d (m), sub-diagonal e (m − 1 used) and τ (m − 1 used);
+ * ozr_syev_tridiag_eig returns θ ascending and the eigenvectors Y (m x m, ldy = m) of the tridiagonal (d, e). */
+ozr_status ozr_syev_tridiag(ozr_ctx ctx, int64_t m, double* K, int64_t ldk, double* d, double* e, double* tau);
+ozr_status ozr_syev_tridiag_eig(ozr_ctx ctx, int64_t m, const double* d, const double* e, double* theta, double* Y,
+                                int64_t ldy);
 
 typedef struct ozr_comm_s* ozr_comm;
 ozr_status ozr_comm_nccl_id(void* id128);

@@ -18,7 +18,7 @@ OZR_SPLIT_FIXED, OZR_SPLIT_X1 = 0, 1
 STATUS = {0: "OZR_OK", 1: "OZR_ERR_ARG", 2: "OZR_ERR_NONFINITE", 3: "OZR_ERR_RANGE", 4: "OZR_ERR_DEGENERATE",
           5: "OZR_ERR_NOT_CONVERGED", 6: "OZR_ERR_CUDA", 7: "OZR_ERR_COMM", 8: "OZR_ERR_NOMEM"}
 EXPORTS = ["ozr_version", "ozr_create", "ozr_destroy", "ozr_last_error", "ozr_split", "ozr_gemm", "ozr_gemm_plan",
-           "ozr_params_default", "ozr_refine_step", "ozr_refine_to_tol", "ozr_last_clusters", "ozr_syev", "ozr_comm_nccl_id",
+           "ozr_params_default", "ozr_refine_step", "ozr_refine_to_tol", "ozr_last_clusters", "ozr_syev", "ozr_syev_tridiag", "ozr_syev_tridiag_eig", "ozr_comm_nccl_id",
            "ozr_comm_create_nccl", "ozr_comm_create_host_group", "ozr_comm_destroy", "ozr_comm_size", "ozr_comm_rank",
            "ozr_refine_step_dist", "ozr_refine_to_tol_dist", "ozr_last_R"]
 
@@ -91,6 +91,10 @@ def lib():
         L.ozr_last_clusters.restype = i32
         L.ozr_syev.argtypes = [vp, i64, vp, i64, vp, vp, i64]
         L.ozr_syev.restype = i32
+        L.ozr_syev_tridiag.argtypes = [vp, i64, vp, i64, vp, vp, vp]
+        L.ozr_syev_tridiag.restype = i32
+        L.ozr_syev_tridiag_eig.argtypes = [vp, i64, vp, vp, vp, vp, i64]
+        L.ozr_syev_tridiag_eig.restype = i32
         L.ozr_comm_nccl_id.argtypes = [vp]
         L.ozr_comm_nccl_id.restype = i32
         L.ozr_comm_create_nccl.argtypes = [ctypes.POINTER(vp), vp, i32, i32, i32]
@@ -247,6 +251,24 @@ def ozr_syev(ctx, K):
     th = torch.empty(m, dtype=torch.float64, device=K.device)
     Y = colmajor(torch.empty((m, m), dtype=torch.float64, device=K.device))
     ctx.check(lib().ozr_syev(ctx.h, m, _ptr(K), _ld(K), _ptr(th), _ptr(Y), m))
+    return th, Y
+
+
+def ozr_syev_tridiag(ctx, K):
+    """Stage 1 alone: (d, e, τ, R) with R = K's copy holding the Householder vectors below its sub-diagonal."""
+    m = K.shape[0]
+    R = colmajor(K.clone())
+    d, e, tau = (torch.zeros(m, dtype=torch.float64, device=K.device) for _ in range(3))
+    ctx.check(lib().ozr_syev_tridiag(ctx.h, m, _ptr(R), m, _ptr(d), _ptr(e), _ptr(tau)))
+    return d, e, tau, R
+
+
+def ozr_syev_tridiag_eig(ctx, d, e):
+    """Stage 2 alone: θ ascending and Y for the symmetric tridiagonal (d, e)."""
+    m = d.shape[0]
+    th = torch.empty(m, dtype=torch.float64, device=d.device)
+    Y = colmajor(torch.empty((m, m), dtype=torch.float64, device=d.device))
+    ctx.check(lib().ozr_syev_tridiag_eig(ctx.h, m, _ptr(d), _ptr(e), _ptr(th), _ptr(Y), m))
     return th, Y
 
 

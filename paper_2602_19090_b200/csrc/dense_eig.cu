@@ -1,19 +1,9 @@
-// dense_eig.cu — the Rayleigh–Ritz sub-solve of LARGE unresolved groups (R13) with a dense
-// symmetric eigensolver instead of the cyclic Jacobi of cluster.cu. Same mathematics, same conventions
-// (cluster.cu header): K = C·(M+Mᵀ)/2·C with C = I + R_JJ/2, K = YΘYᵀ (Θ ascending, y_kk ≥ 0, the
-// largest-|·| entry of the column when y_kk = 0), Z = C·Y, λ̂_J = μ + Θ.
-//
-// The Jacobi core is O(m³) per sweep with one grid-wide synchronisation per rotation round (m − 1 rounds
-// per sweep), which makes a 6628-column group (BASELINE c4: cnd 1e14 from an FP32 eigensolver) a
-// minutes-long solve. Here the two C products, Z = C·Y and the apply T·Z are FP64-accurate products on the
-// INT8 slice GEMM (ozr_api.cu oz_dgemm; the host orchestrates) and the eigen-decomposition of K is LAPACK's
-// divide-and-conquer syevd from cuSOLVER
-// (a library routine in the role cuBLAS plays for a plain GEMM; loaded with dlopen on first use so the
-// library has no link-time dependency and binds the libcusolver.so.11 torch has already loaded, if any).
-// Backward-stable like Jacobi: the eigenvectors of K are accurate to u‖K‖/gap_K, the same accuracy the
-// parity tests allow the Jacobi path against the oracle's __float128 one.
-#include <dlfcn.h>
-
+// dense_eig.cu — elementwise pieces of the Rayleigh–Ritz sub-solve of LARGE unresolved groups (R13),
+// orchestrated in ozr_api.cu: K = C·(M+Mᵀ)/2·C with C = I + R_JJ/2 and Z = C·Y as FP64-accurate INT8 slice products
+// (oz_dgemm), K = YΘYᵀ by the hand-written eigensolver (syev.cu), Y's signs (y_kk ≥ 0, the largest-|·| entry of the
+// column when y_kk = 0), λ̂_J = μ + Θ, and the scatter of Ẽ'[:, J]·Z — the same mathematics and conventions as the
+// per-CTA Jacobi of cluster.cu, whose O(m³·sweeps) cost with m − 1 grid-wide synchronisations per sweep rules it out
+// for groups of thousands of columns (BASELINE c4's FP32 start opens with 6628).
 #include <cstdint>
 #include <algorithm>
 #include <cstdio>
@@ -26,47 +16,6 @@
 namespace ozr {
 
 namespace {
-
-// ---------------------------------------------------------------- cuSOLVER (dlopen)
-typedef int (*fn_create)(void**);
-typedef int (*fn_destroy)(void*);
-typedef int (*fn_setstream)(void*, cudaStream_t);
-typedef int (*fn_syevd_bs)(void*, int, int, int, const double*, int, const double*, int*);
-typedef int (*fn_syevd)(void*, int, int, int, double*, int, double*, double*, int, int*);
-
-struct SolverApi {
-  bool tried = false, ok = false;
-  std::string err;
-  fn_create create = nullptr;
-  fn_destroy destroy = nullptr;
-  fn_setstream setstream = nullptr;
-  fn_syevd_bs syevd_bs = nullptr;
-  fn_syevd syevd = nullptr;
-};
-
-SolverApi& api() {
-  static SolverApi a;
-  if (a.tried) return a;
-  a.tried = true;
-  void* h = dlopen("libcusolver.so.11", RTLD_NOW | RTLD_NOLOAD);  // torch's copy, when loaded
-  if (!h) h = dlopen("libcusolver.so.11", RTLD_NOW | RTLD_GLOBAL);
-  if (!h) h = dlopen("/usr/local/cuda/lib64/libcusolver.so.11", RTLD_NOW | RTLD_GLOBAL);
-  if (!h) {
-    a.err = std::string("dlopen libcusolver.so.11: ") + dlerror();
-    return a;
-  }
-  a.create = reinterpret_cast<fn_create>(dlsym(h, "cusolverDnCreate"));
-  a.destroy = reinterpret_cast<fn_destroy>(dlsym(h, "cusolverDnDestroy"));
-  a.setstream = reinterpret_cast<fn_setstream>(dlsym(h, "cusolverDnSetStream"));
-  a.syevd_bs = reinterpret_cast<fn_syevd_bs>(dlsym(h, "cusolverDnDsyevd_bufferSize"));
-  a.syevd = reinterpret_cast<fn_syevd>(dlsym(h, "cusolverDnDsyevd"));
-  a.ok = a.create && a.destroy && a.setstream && a.syevd_bs && a.syevd;
-  if (!a.ok) a.err = "libcusolver.so.11 lacks the syevd entry points";
-  return a;
-}
-
-constexpr int kEigModeVector = 1;  // CUSOLVER_EIG_MODE_VECTOR
-constexpr int kFillLower = 0;      // CUBLAS_FILL_MODE_LOWER
 
 // ---------------------------------------------------------------- kernels (m x m, column-major, ld = m)
 // out = (X + Xᵀ)/2
@@ -150,27 +99,6 @@ __global__ void k_dense_scatter(const double* __restrict__ TZ, int rows, int m, 
 
 }  // namespace
 
-DenseEig::~DenseEig() {
-  if (handle) api().destroy(handle);
-}
-
-bool dense_eig_available(std::string* why) {
-  SolverApi& a = api();
-  if (!a.ok && why) *why = a.err;
-  return a.ok;
-}
-
-// Workspace (doubles) syevd needs for an m x m problem; -1 when cuSOLVER is unavailable.
-long long dense_eig_lwork(DenseEig& de, int m, cudaStream_t s) {
-  SolverApi& a = api();
-  if (!a.ok) return -1;
-  if (!de.handle && a.create(&de.handle) != 0) return -1;
-  if (a.setstream(de.handle, s) != 0) return -1;
-  int lw = 0;
-  if (a.syevd_bs(de.handle, kEigModeVector, kFillLower, m, nullptr, m, nullptr, &lw) != 0) return -1;
-  return lw;
-}
-
 void launch_dense_sym(int m, const double* X, double* out, cudaStream_t s) {
   const long long m2 = static_cast<long long>(m) * m;
   const int gb = static_cast<int>(std::min<long long>((m2 + 255) / 256, 148 * 16));
@@ -179,13 +107,6 @@ void launch_dense_sym(int m, const double* X, double* out, cudaStream_t s) {
 void launch_dense_axpy(long long cnt, const double* X, double alpha, const double* P, double* out, cudaStream_t s) {
   const int gb = static_cast<int>(std::min<long long>((cnt + 255) / 256, 148 * 16));
   k_daxpy<<<gb, 256, 0, s>>>(cnt, X, alpha, P, out);
-}
-cudaError_t dense_syevd(DenseEig& de, int m, double* K, double* th, cudaStream_t s) {
-  SolverApi& a = api();
-  if (!a.ok || !de.handle || a.setstream(de.handle, s) != 0) return cudaErrorNotSupported;
-  if (a.syevd(de.handle, kEigModeVector, kFillLower, m, K, m, th, de.work, de.lwork, de.info) != 0)
-    return cudaErrorUnknown;
-  return cudaGetLastError();
 }
 void launch_dense_sign(int m, double* Y, const double* th, double mu, const int* J, double* lam, const int* info,
                        int* err, cudaStream_t s) {

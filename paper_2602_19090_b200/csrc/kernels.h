@@ -105,22 +105,11 @@ struct ClusterLaunch {
   int dense_min;           // groups of at least this many columns take the dense solver (dense_eig.cu)
   int* err;                // error flags (ERR_SOLVER when the dense solver reports failure)
 };
-// Dense symmetric eigensolver state of one context (cuSOLVER syevd, dlopen'ed; dense_eig.cu).
-struct DenseEig {
-  void* handle = nullptr;
-  double* work = nullptr;
-  int lwork = 0;
-  int* info = nullptr;
-  ~DenseEig();
-};
-bool dense_eig_available(std::string* why);
-long long dense_eig_lwork(DenseEig& de, int m, cudaStream_t s);
 // Pieces of the dense sub-solve of a large group (dense_eig.cu; ozr_api.cu orchestrates with oz_dgemm):
 // out = (X + Xᵀ)/2 (m x m); out = X + alpha·P (cnt elements); K ← its eigenvectors Y (ascending θ);
 // Y's columns signed (y_kk ≥ 0) and λ̂_J = μ + θ; the dense group's part of the apply.
 void launch_dense_sym(int m, const double* X, double* out, cudaStream_t s);
 void launch_dense_axpy(long long cnt, const double* X, double alpha, const double* P, double* out, cudaStream_t s);
-cudaError_t dense_syevd(DenseEig& de, int m, double* K, double* th, cudaStream_t s);
 void launch_dense_sign(int m, double* Y, const double* th, double mu, const int* J, double* lam, const int* info,
                        int* err, cudaStream_t s);
 void launch_dense_scatter(const double* TZ, int rows, int m, const int* J, int grp, const int* grp_of, const int* pos_of,

@@ -585,7 +585,7 @@ RecombPlan shift_plan(const RecombPlan& rp, int t0) {
 }
 
 ozr_status err_bits(ozr_ctx ctx, int h) {
-  if (h & ERR_SOLVER) return fail(ctx, OZR_ERR_CUDA, "dense cluster sub-solve: syevd reported failure (info != 0)");
+  if (h & ERR_SOLVER) return fail(ctx, OZR_ERR_CUDA, "dense cluster sub-solve: the eigensolver reported failure");
   if (h & ERR_NONFINITE) return fail(ctx, OZR_ERR_NONFINITE, "non-finite value in an input matrix");
   if (h & ERR_RANGE) return fail(ctx, OZR_ERR_RANGE, "exponent range exceeded in the digit split");
   if (h & ERR_DEGENERATE)
@@ -1776,6 +1776,40 @@ ozr_status ozr_syev(ozr_ctx ctx, int64_t m, const double* K, int64_t ldk, double
   OZR_CK(cudaMemcpy2DAsync(Y, ldy * sizeof(double), Yw, m * sizeof(double), m * sizeof(double), m,
                            cudaMemcpyDeviceToDevice, s), "copy Y");
   OZR_CK(cudaStreamSynchronize(s), "sync");
+  return OZR_OK;
+}
+
+ozr_status ozr_syev_tridiag(ozr_ctx ctx, int64_t m, double* K, int64_t ldk, double* d, double* e, double* tau) {
+  ozr_status st = check_ctx(ctx);
+  if (st != OZR_OK) return st;
+  if (!K || !d || !e || !tau || m < 1 || ldk != m || m > 32768) return fail(ctx, OZR_ERR_ARG, "ozr_syev_tridiag: bad argument");
+  ozr::SyevDebug dbg;
+  dbg.d_out = d;
+  dbg.e_out = e;
+  dbg.tau_out = tau;
+  std::string why;
+  const int rc = dense_syev(ctx->syev, static_cast<int>(m), K, nullptr, nullptr, nullptr, 0, ctx->stream, &why, &dbg);
+  if (rc != 0) return fail(ctx, rc == 8 ? OZR_ERR_NOMEM : OZR_ERR_CUDA, "ozr_syev_tridiag: %s", why.c_str());
+  return OZR_OK;
+}
+
+ozr_status ozr_syev_tridiag_eig(ozr_ctx ctx, int64_t m, const double* d, const double* e, double* theta, double* Y,
+                                int64_t ldy) {
+  ozr_status st = check_ctx(ctx);
+  if (st != OZR_OK) return st;
+  if (!d || !e || !theta || !Y || m < 1 || ldy != m || m > 32768) return fail(ctx, OZR_ERR_ARG, "ozr_syev_tridiag_eig: bad argument");
+  int* derr = ctx->ws<int>(S_ERR, 4);
+  OZR_ALLOC(derr);
+  ozr::SyevDebug dbg;
+  dbg.d_in = d;
+  dbg.e_in = e;
+  std::string why;
+  const SyevGemm gemm = [&](int M2, int N2, int K2, const double* A2, int lda2, bool at, const double* B2, int ldb2,
+                            double* C2, int ldc2) {
+    return oz_dgemm(ctx, M2, N2, K2, A2, lda2, at, B2, ldb2, C2, ldc2, derr) == OZR_OK ? 0 : 1;
+  };
+  const int rc = dense_syev(ctx->syev, static_cast<int>(m), nullptr, theta, Y, gemm, kSyevBigGemm, ctx->stream, &why, &dbg);
+  if (rc != 0) return fail(ctx, rc == 8 ? OZR_ERR_NOMEM : OZR_ERR_CUDA, "ozr_syev_tridiag_eig: %s", why.c_str());
   return OZR_OK;
 }
 

@@ -16,6 +16,8 @@
 #include <algorithm>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
+#include <string>
 #include <vector>
 
 #include "syev.h"
@@ -72,44 +74,69 @@ struct PanelArgs {
   double* yp;       // tile partials: slot(I, J) x 2 x TB
 };
 
-// Row block R (TB rows) is owned by CTA R % G.
+// Sum of the G per-CTA partials part[g·PS + off] in a fixed order (every CTA gets the same value): thread t sums
+// g ≡ t (mod TT) ascending, then a fixed tree over the threads.
+__device__ __forceinline__ double grid_partial_sum(const double* __restrict__ part, int PS, int off, int G, double* sh) {
+  double a = 0.0;
+  for (int g = threadIdx.x; g < G; g += TT) a += part[static_cast<long long>(g) * PS + off];
+  return block_sum256(a, sh);
+}
+
+// Row block b (TB rows) is owned by CTA b (G ≥ mt is guaranteed by syev_trd_grid). The CTA keeps its rows of the
+// panel's V and W in shared memory (vs, ws), so every per-row dot product of the panel reads shared memory.
+struct PanelSmem {
+  double tile[TB][TB + 1];  // tile[col][row]
+  double vs[NB][TB], ws[NB][TB];
+  double vr[TB], vc[TB], vloc[TB];
+  double rowc[2 * NB];      // V(c, 0:i) | W(c, 0:i)
+  double dots[2 * NB];      // Vᵀv | Wᵀv (reduced over the grid)
+  double sh[TT / 32];
+};
+
 __global__ void __launch_bounds__(TT) k_trd_panel(PanelArgs P) {
   cg::grid_group grid = cg::this_grid();
-  __shared__ double sh[TT / 32];
-  __shared__ double tile[TB][TB + 1];  // tile[col][row]
-  __shared__ double vr[TB], vc[TB];
-  __shared__ double wtv[NB], vtv[NB];
+  extern __shared__ __align__(16) unsigned char smraw[];
+  PanelSmem& S = *reinterpret_cast<PanelSmem*>(smraw);
   const int G = gridDim.x, b = blockIdx.x, tid = threadIdx.x;
   const int m = P.m;
   const int mt = (m + TB - 1) / TB;
   double* A = P.A;
   const int PS = 2 + 2 * NB;
-  double gam_prev = 0.0;  // γ of the previous column (its W column's final correction, pending on own rows)
+  const int r0own = b * TB;
+  const bool owner = b < mt;
+  double gam_prev = 0.0;  // γ of the previous column: W(:, i−1) += γ·V(:, i−1) still pending in global memory
   for (int i = 0; i < P.nb; ++i) {
     const int c = P.k0 + i;
-    // ---- phase A: own rows r ≥ c: finish W(:, i−1) (+γ v), x_r = A(r,c) − V(r,:)W(c,:)ᵀ − W(r,:)V(c,:)ᵀ
-    double ss = 0.0;
-    for (int R = b; R < mt; R += G) {
-      const int r = R * TB + (tid & (TB - 1));
-      if ((tid >> 6) != 0) continue;  // one 64-thread group per row block (rows are few per CTA)
-      if (r >= m || r < c) continue;
-      if (i > 0 && r >= c) P.W[r + static_cast<long long>(i - 1) * m] =
-                               fma(gam_prev, P.V[r + static_cast<long long>(i - 1) * m], P.W[r + static_cast<long long>(i - 1) * m]);
-      double x = A[r + static_cast<long long>(c) * m];
-      for (int j = 0; j < i; ++j) {
-        double wc = P.W[c + static_cast<long long>(j) * m];
-        if (j == i - 1) wc = fma(gam_prev, P.V[c + static_cast<long long>(j) * m], wc);
-        x -= P.V[r + static_cast<long long>(j) * m] * wc + P.W[r + static_cast<long long>(j) * m] * P.V[c + static_cast<long long>(j) * m];
-      }
-      A[r + static_cast<long long>(c) * m] = x;
-      if (r >= c + 2) ss = fma(x, x, ss);
+    // ---- phase A: x_r = A(r,c) − V(r,:)W(c,:)ᵀ − W(r,:)V(c,:)ᵀ on own rows r ≥ c
+    if (tid < 2 * i) {
+      const int j = tid < i ? tid : tid - i;
+      const double vcj = P.V[c + static_cast<long long>(j) * m];
+      double val = (tid < i) ? vcj : P.W[c + static_cast<long long>(j) * m];
+      if (tid >= i && j == i - 1) val = fma(gam_prev, vcj, val);
+      S.rowc[tid < i ? j : NB + j] = val;
     }
-    ss = block_sum256(ss, sh);
+    if (i > 0 && tid < TB) S.ws[i - 1][tid] = fma(gam_prev, S.vs[i - 1][tid], S.ws[i - 1][tid]);  // private rows
+    __syncthreads();
+    double ss = 0.0;
+    if (owner && tid < TB) {
+      const int r = r0own + tid;
+      if (r < m && r >= c) {
+        double x = A[r + static_cast<long long>(c) * m];
+        double x2 = 0.0;
+        for (int j = 0; j < i; j += 2) {
+          x -= S.vs[j][tid] * S.rowc[NB + j] + S.ws[j][tid] * S.rowc[j];
+          if (j + 1 < i) x2 -= S.vs[j + 1][tid] * S.rowc[NB + j + 1] + S.ws[j + 1][tid] * S.rowc[j + 1];
+        }
+        x += x2;
+        A[r + static_cast<long long>(c) * m] = x;
+        if (r >= c + 2) ss = x * x;
+      }
+    }
+    ss = block_sum256(ss, S.sh);
     if (tid == 0) P.part[static_cast<long long>(b) * PS] = ss;
     grid.sync();
-    // ---- phase B: the reflector (every CTA, same order), the tile products, Vᵀv and Wᵀv partials
-    double sigma = 0.0;
-    for (int g = 0; g < G; ++g) sigma += P.part[static_cast<long long>(g) * PS];
+    // ---- phase B: the reflector (every CTA, the same fixed-order sums), V(:, i), the tile products, Vᵀv and Wᵀv
+    const double sigma = grid_partial_sum(P.part, PS, 0, G, S.sh);
     const double ccdiag = A[c + static_cast<long long>(c) * m];
     double alpha = 0.0, beta = 0.0, tau = 0.0, scale = 0.0;
     if (c + 1 < m) {
@@ -129,120 +156,146 @@ __global__ void __launch_bounds__(TT) k_trd_panel(PanelArgs P) {
         P.tau[c] = tau;
       }
     }
+    if (owner && tid < TB && i > 0) {  // the pending correction of W(:, i−1), own rows r ≥ c (global copy)
+      const int r = r0own + tid;
+      if (r < m && r >= c) P.W[r + static_cast<long long>(i - 1) * m] = S.ws[i - 1][tid];
+    }
     if (c + 1 >= m) break;  // the last column: only its diagonal
     auto vof = [&](int r) -> double { return r == c + 1 ? 1.0 : (r > c + 1 ? A[r + static_cast<long long>(c) * m] * scale : 0.0); };
-    // own rows: V(r, i)
-    for (int R = b; R < mt; R += G) {
-      const int r = R * TB + tid;
-      if (tid < TB && r < m && r >= c + 1) P.V[r + static_cast<long long>(i) * m] = vof(r);
+    if (owner && tid < TB) {
+      const int r = r0own + tid;
+      const double v = (r < m) ? vof(r) : 0.0;
+      S.vloc[tid] = v;
+      S.vs[i][tid] = v;
+      if (r < m && r >= c + 1) P.V[r + static_cast<long long>(i) * m] = v;
     }
     if (tau != 0.0) {
-      // tiles of the lower triangle of A(c+1:m, c+1:m), grid-aligned
       const int J0 = (c + 1) / TB;
       const int na = mt - J0;
       const int ntiles = na * (na + 1) / 2;
       for (int t = b; t < ntiles; t += G) {
         int I, J;
         tile_of(t, J0, I, J);
-        const int r0 = I * TB, q0 = J * TB;
+        const int rt0 = I * TB, qt0 = J * TB;
         __syncthreads();
-        // load: tile[κ][ρ] = A(r0+ρ, q0+κ) (lower: r ≥ q; for the diagonal tile the upper half is mirrored)
-        for (int e2 = tid; e2 < TB * TB; e2 += TT) {
-          const int rho = e2 & (TB - 1), kap = e2 >> 6;
-          const int r = r0 + rho, q = q0 + kap;
-          double a = 0.0;
-          if (r < m && q < m && r >= c + 1 && q >= c + 1) {
-            if (r >= q) a = A[r + static_cast<long long>(q) * m];
-            else a = A[q + static_cast<long long>(r) * m];
+        {  // tile[κ][ρ] = A(rt0+ρ, qt0+κ), lower part (mirrored on the diagonal): all 16 loads in flight first
+          double reg[TB * TB / TT];
+#pragma unroll
+          for (int u = 0; u < TB * TB / TT; ++u) {
+            const int e2 = tid + u * TT;
+            const int rho = e2 & (TB - 1), kap = e2 >> 6;
+            const int r = rt0 + rho, q = qt0 + kap;
+            const bool in = r < m && q < m && r >= c + 1 && q >= c + 1;
+            const long long idx = (r >= q) ? r + static_cast<long long>(q) * m : q + static_cast<long long>(r) * m;
+            reg[u] = in ? __ldcg(A + idx) : 0.0;
           }
-          tile[kap][rho] = a;
+#pragma unroll
+          for (int u = 0; u < TB * TB / TT; ++u) {
+            const int e2 = tid + u * TT;
+            S.tile[e2 >> 6][e2 & (TB - 1)] = reg[u];
+          }
         }
-        if (tid < TB) {
-          vr[tid] = (r0 + tid < m) ? vof(r0 + tid) : 0.0;
-          vc[tid] = (q0 + tid < m) ? vof(q0 + tid) : 0.0;
-        }
+        if (tid < TB) S.vr[tid] = (rt0 + tid < m) ? vof(rt0 + tid) : 0.0;
+        else if (tid < 2 * TB) S.vc[tid - TB] = (qt0 + tid - TB < m) ? vof(qt0 + tid - TB) : 0.0;
         __syncthreads();
         double* out = P.yp + tslot(I, J) * 2 * TB;
-        if (tid < TB) {  // row sums: Σ_κ tile[κ][ρ] vc[κ]
+        // 4 threads per output: threads 0..127 → row sums (half a row each... 2 per row), 128..255 → column sums
+        const int half = tid & 1;
+        if (tid < 2 * TB) {  // row ρ = tid/2: Σ_κ tile[κ][ρ] vc[κ] over κ ≡ half (mod 2)
+          const int rho = tid >> 1;
           double acc = 0.0;
-          for (int kap = 0; kap < TB; ++kap) acc = fma(tile[kap][tid], vc[kap], acc);
-          out[tid] = acc;
-        } else if (tid < 2 * TB) {  // column sums (off-diagonal tiles): Σ_ρ tile[κ][ρ] vr[ρ]
-          const int kap = tid - TB;
+#pragma unroll 8
+          for (int kap = half; kap < TB; kap += 2) acc = fma(S.tile[kap][rho], S.vc[kap], acc);
+          acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+          if (!half) out[rho] = acc;
+        } else {  // column κ = (tid − 128)/2: Σ_ρ tile[κ][ρ] vr[ρ] (off-diagonal tiles)
+          const int kap = (tid - 2 * TB) >> 1;
           double acc = 0.0;
-          if (I != J)
-            for (int rho = 0; rho < TB; ++rho) acc = fma(tile[kap][rho], vr[rho], acc);
-          out[TB + kap] = acc;
+          if (I != J) {
+#pragma unroll 8
+            for (int rho = half; rho < TB; rho += 2) acc = fma(S.tile[kap][rho], S.vr[rho], acc);
+          }
+          acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+          if (!half) out[TB + kap] = acc;
         }
       }
-      // Vᵀv and Wᵀv over own rows (columns j < i)
-      for (int j = 0; j < i; ++j) {
-        double pv = 0.0, pw = 0.0;
-        for (int R = b; R < mt; R += G) {
-          const int r = R * TB + tid;
-          if (tid < TB && r < m && r >= c + 1) {
-            const double v = vof(r);
-            pv = fma(P.V[r + static_cast<long long>(j) * m], v, pv);
-            pw = fma(P.W[r + static_cast<long long>(j) * m], v, pw);
+      // Vᵀv and Wᵀv over own rows: 2i dot products of length TB from shared memory, 4 threads each
+      __syncthreads();
+      if (owner && i > 0) {
+        const int q = tid >> 2, part = tid & 3;  // q < 64: product index (j for V, NB + j for W)
+        if (q < 2 * NB) {
+          const int j = q < NB ? q : q - NB;
+          double acc = 0.0;
+          if (j < i) {
+            const double* row = q < NB ? S.vs[j] : S.ws[j];
+            for (int t = part; t < TB; t += 4) acc = fma(row[t], S.vloc[t], acc);
           }
+          acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+          acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+          if (part == 0 && j < i) P.part[static_cast<long long>(b) * PS + 2 + q] = acc;
         }
-        pv = block_sum256(pv, sh);
-        pw = block_sum256(pw, sh);
-        if (tid == 0) {
-          P.part[static_cast<long long>(b) * PS + 2 + j] = pv;
-          P.part[static_cast<long long>(b) * PS + 2 + NB + j] = pw;
-        }
+      } else if (i > 0 && tid < 2 * NB) {
+        const int j = tid < NB ? tid : tid - NB;
+        if (j < i) P.part[static_cast<long long>(b) * PS + 2 + tid] = 0.0;
       }
     }
     grid.sync();
     // ---- phase C: y_r from the tile partials, w'_r = τ(y − V(Wᵀv) − W(Vᵀv)), partial of w'ᵀv
     double p3 = 0.0;
     if (tau != 0.0) {
-      if (tid < i) {
-        double sv = 0.0, sw = 0.0;
-        for (int g = 0; g < G; ++g) {
-          sv += P.part[static_cast<long long>(g) * PS + 2 + tid];
-          sw += P.part[static_cast<long long>(g) * PS + 2 + NB + tid];
-        }
-        vtv[tid] = sv;
-        wtv[tid] = sw;
+      if (i > 0) {  // Vᵀv, Wᵀv reduced over the grid: 4 threads per value, fixed order
+        const int q = tid >> 2, part = tid & 3;
+        double acc = 0.0;
+        if (q < 2 * NB && (q < NB ? q : q - NB) < i)
+          for (int g = part; g < G; g += 4) acc += P.part[static_cast<long long>(g) * PS + 2 + q];
+        acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+        acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+        if (part == 0 && q < 2 * NB) S.dots[q] = acc;
       }
       __syncthreads();
-      const int J0 = (c + 1) / TB;
-      for (int R = b; R < mt; R += G) {
-        const int r = R * TB + tid;
-        if (tid >= TB || r >= m || r < c + 1) continue;
+      if (owner) {
+        const int J0 = (c + 1) / TB;
+        const int R = b, t4 = tid & 3, row = tid >> 2;  // 4 threads per own row
+        const int r = r0own + row;
         double y = 0.0;
-        for (int J = J0; J <= R; ++J) y += P.yp[tslot(R, J) * 2 * TB + tid];
-        for (int I = R + 1; I < mt; ++I) y += P.yp[tslot(I, R) * 2 * TB + TB + tid];
-        for (int j = 0; j < i; ++j)
-          y -= P.V[r + static_cast<long long>(j) * m] * wtv[j] + P.W[r + static_cast<long long>(j) * m] * vtv[j];
-        const double w = tau * y;
-        P.W[r + static_cast<long long>(i) * m] = w;
-        p3 = fma(w, vof(r), p3);
+        if (r < m && r >= c + 1) {
+#pragma unroll 4
+          for (int J = J0 + t4; J <= R; J += 4) y += __ldcg(P.yp + tslot(R, J) * 2 * TB + row);
+#pragma unroll 4
+          for (int I = R + 1 + t4; I < mt; I += 4) y += __ldcg(P.yp + tslot(I, R) * 2 * TB + TB + row);
+        }
+        y += __shfl_xor_sync(0xffffffffu, y, 1);
+        y += __shfl_xor_sync(0xffffffffu, y, 2);
+        if (t4 == 0 && r < m && r >= c + 1) {
+          double y2 = 0.0;
+          for (int j = 0; j < i; j += 2) {
+            y -= S.vs[j][row] * S.dots[NB + j] + S.ws[j][row] * S.dots[j];
+            if (j + 1 < i) y2 -= S.vs[j + 1][row] * S.dots[NB + j + 1] + S.ws[j + 1][row] * S.dots[j + 1];
+          }
+          const double w = tau * (y + y2);
+          S.ws[i][row] = w;
+          P.W[r + static_cast<long long>(i) * m] = w;
+          p3 = w * S.vloc[row];
+        } else if (t4 == 0 && row < TB) {
+          S.ws[i][row] = 0.0;
+        }
       }
-    } else {
-      for (int R = b; R < mt; R += G) {
-        const int r = R * TB + tid;
-        if (tid < TB && r < m && r >= c + 1) P.W[r + static_cast<long long>(i) * m] = 0.0;
-      }
+    } else if (owner && tid < TB) {
+      const int r = r0own + tid;
+      S.ws[i][tid] = 0.0;
+      if (r < m && r >= c + 1) P.W[r + static_cast<long long>(i) * m] = 0.0;
     }
-    p3 = block_sum256(p3, sh);
+    p3 = block_sum256(p3, S.sh);
     if (tid == 0) P.part[static_cast<long long>(b) * PS + 1] = p3;
     grid.sync();
-    double wv = 0.0;
-    for (int g = 0; g < G; ++g) wv += P.part[static_cast<long long>(g) * PS + 1];
-    gam_prev = -0.5 * tau * wv;  // W(:, i) += γ v: applied on own rows at the next column (or below)
+    gam_prev = -0.5 * tau * grid_partial_sum(P.part, PS, 1, G, S.sh);
   }
   // the last column's pending γ (rows ≥ its c + 1), for the trailing update
   const int ilast = P.nb - 1, clast = P.k0 + ilast;
-  if (clast + 1 < m) {
-    for (int R = b; R < mt; R += G) {
-      const int r = R * TB + tid;
-      if (tid < TB && r < m && r >= clast + 1)
-        P.W[r + static_cast<long long>(ilast) * m] =
-            fma(gam_prev, P.V[r + static_cast<long long>(ilast) * m], P.W[r + static_cast<long long>(ilast) * m]);
-    }
+  if (clast + 1 < m && owner && tid < TB) {
+    const int r = r0own + tid;
+    if (r < m && r >= clast + 1)
+      P.W[r + static_cast<long long>(ilast) * m] = fma(gam_prev, S.vs[ilast][tid], S.ws[ilast][tid]);
   }
 }
 
@@ -253,7 +306,7 @@ __global__ void __launch_bounds__(TT) k_trd_update(double* __restrict__ A, int m
   __shared__ double vR[NB][TB], wR[NB][TB], vC[NB][TB / 2], wC[NB][TB / 2];  // 48 KB: columns in two halves
   const int k1 = k0 + nb;
   const int J0 = k1 / TB, mt = (m + TB - 1) / TB;
-  const int na = mt - J0;
+  const int na = (k1 < m) ? mt - J0 : 0;
   const int t = blockIdx.x;
   if (t >= na * (na + 1) / 2) {  // the reflector copy: one CTA per panel column
     const int j = t - na * (na + 1) / 2;
@@ -380,16 +433,19 @@ __global__ void k_dc_zvec(const int* __restrict__ nlo, const int* __restrict__ n
 
 // Qp (node block, ld = m) column jj = Q column lo + src[jj] (block-diagonal halves), then the deflation
 // rotations of the node in order (each thread one row: the rotations only mix columns).
-__global__ void k_dc_permrot(const int* __restrict__ nlo, const int* __restrict__ nhi, const int* __restrict__ src,
-                             const int* __restrict__ rot_off, const int4* __restrict__ rot_idx,
+__global__ void k_dc_permrot(const int* __restrict__ nlo, const int* __restrict__ nmid, const int* __restrict__ nhi,
+                             const int* __restrict__ src, const int* __restrict__ rot_off, const int4* __restrict__ rot_idx,
                              const double2* __restrict__ rot_cs, const double* __restrict__ Q, double* __restrict__ Qp,
                              int m) {
   const int q = blockIdx.y;
-  const int lo = nlo[q], nn = nhi[q] - lo;
+  const int lo = nlo[q], nn = nhi[q] - lo, n1 = nmid[q] - lo;
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= nn) return;
-  for (int jj = 0; jj < nn; ++jj)
-    Qp[static_cast<long long>(lo + jj) * m + lo + r] = Q[static_cast<long long>(lo + src[lo + jj]) * m + lo + r];
+  for (int jj = 0; jj < nn; ++jj) {  // diag(Q1, Q2): the off-diagonal child blocks are zero (never stored)
+    const int c = src[lo + jj];
+    Qp[static_cast<long long>(lo + jj) * m + lo + r] =
+        ((r < n1) == (c < n1)) ? Q[static_cast<long long>(lo + c) * m + lo + r] : 0.0;
+  }
   for (int k = rot_off[q]; k < rot_off[q + 1]; ++k) {
     const int a = rot_idx[k].x, b = rot_idx[k].y;  // node-local columns of Qp
     const double c = rot_cs[k].x, s = rot_cs[k].y;
@@ -446,7 +502,8 @@ __device__ void secular_root(int k, const double* __restrict__ d, const double* 
     }
     const double f = ir + psi + phi;
     if (f > 0.0) b = t; else a = t;
-    if (fabs(f) <= 8.0 * eps * (ir + erre + k * (fabs(psi) + fabs(phi))) || b - a <= 4.0 * eps * fmax(fabs(a), fabs(b)) ||
+    // LAPACK dlaed4's stop: |f| within the rounding error of its own evaluation, ε(8(|ψ| + |φ|) + 1/ρ + |τ|·f')
+    if (fabs(f) <= eps * (8.0 * erre + ir + fabs(t) * (dpsi + dphi)) || b - a <= 2.0 * eps * fmax(fabs(a), fabs(b)) ||
         f == 0.0)
       break;
     // model c + sL/(ΔL − η) + sR/(ΔR − η) matching f and f' at η = 0
@@ -689,12 +746,12 @@ __global__ void __launch_bounds__(256) k_dgemm(int M, int N, int K, double alpha
 
 // Y_sorted[:, j] = Q[:, perm[j]] (ld = m), θ_j = lam[perm[j]]
 __global__ void k_dc_final(const int* __restrict__ perm, const double* __restrict__ Q, const double* __restrict__ lam,
-                           int m, double* __restrict__ Y, double* __restrict__ theta) {
+                           int m, double* __restrict__ Y, double* __restrict__ theta, int unscale) {
   const int j = blockIdx.y;
   const int p = perm[j];
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < m; r += gridDim.x * blockDim.x)
     Y[r + static_cast<long long>(j) * m] = Q[r + static_cast<long long>(p) * m];
-  if (blockIdx.x == 0 && threadIdx.x == 0) theta[j] = lam[p];
+  if (blockIdx.x == 0 && threadIdx.x == 0) theta[j] = ldexp(lam[p], unscale);
 }
 
 // Y(0:rows, 0:cols) −= P (Y with leading dimension ldy, P with ldp)
@@ -714,15 +771,18 @@ size_t syev_trd_partials(int m, int G) {
 int syev_trd_grid(int m) {
   static int per = -1;
   if (per < 0) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_trd_panel, TT, 0);
+    cudaFuncSetAttribute(k_trd_panel, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(PanelSmem));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_trd_panel, TT, sizeof(PanelSmem));
     per = std::max(per, 1);
   }
   int dev = 0, nsm = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   const int mt = (m + TB - 1) / TB;
-  // enough CTAs for the tile products (~mt²/2 tiles) but no more than co-reside; fewer CTAs = cheaper barriers
-  const int want = std::max(1, std::min(mt * (mt + 1) / 2, 4 * mt));
+  // one CTA per row block at least (each owns one); more for the tile products (~mt²/2 tiles), bounded by
+  // co-residency; fewer CTAs = cheaper barriers
+  int want = std::max(mt, std::min(mt * (mt + 1) / 2, 3 * mt));
+  if (const char* g = getenv("OZR_SYEV_G")) want = std::max(mt, std::min(mt * (mt + 1) / 2, atoi(g) * mt / 8));  // A/B: G = g/8 · mt
   return std::min(want, nsm * per);
 }
 
@@ -730,12 +790,14 @@ int syev_trd_grid(int m) {
 cudaError_t syev_tridiag(double* A, int m, double* d, double* e, double* tau, double* V, double* W, double* part,
                          int G, cudaStream_t s) {
   const int mt = (m + TB - 1) / TB;
+  if (G < mt) return cudaErrorInvalidConfiguration;  // every row block needs its owner CTA (m ≤ ~28000)
   double* yp = part + static_cast<size_t>(G) * (2 + 2 * NB);
   for (int k0 = 0; k0 < m; k0 += NB) {
     const int nb = std::min(NB, m - k0);
     PanelArgs P{A, m, k0, nb, V, W, d, e, tau, part, yp};
     void* args[] = {&P};
-    cudaError_t err = cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_trd_panel), dim3(G), dim3(TT), args, 0, s);
+    cudaError_t err = cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_trd_panel), dim3(G), dim3(TT), args,
+                                                  sizeof(PanelSmem), s);
     if (err != cudaSuccess) return err;
     const int k1 = k0 + nb;
     if (k1 < m) {
@@ -797,7 +859,7 @@ bool cuda_ok(cudaError_t e, std::string* err, const char* what) {
 // K (m x m, ld = m; the lower triangle is read) → eigenvalues θ ascending (device, m) and eigenvectors Y (device,
 // m x m, ld = m; may alias K). gemm: the large products of the D&C merges and the back-transformation.
 int dense_syev(SyevWorkspace& w, int m, double* K, double* theta, double* Y, const SyevGemm& gemm, int big_gemm_min,
-               cudaStream_t s, std::string* err) {
+               cudaStream_t s, std::string* err, const SyevDebug* dbg) {
 #define SY_ALLOC(ptr, slot, T, cnt)                                        \
   T* ptr = static_cast<T*>(w.get(slot, sizeof(T) * static_cast<size_t>(cnt))); \
   if (!ptr) {                                                              \
@@ -828,14 +890,49 @@ int dense_syev(SyevWorkspace& w, int m, double* K, double* theta, double* Y, con
   // staging for the per-level host decisions: pinned host memory
   std::vector<double> hd(m), he(m), hlam(m), hz(m);
   if (!cuda_ok(cudaMemsetAsync(derr, 0, 4 * sizeof(int), s), err, "memset")) return 6;
-  // ---- (1) tridiagonalise
-  if (!cuda_ok(syev_tridiag(K, m, d, e, tau, V, Wp, part, G, s), err, "tridiagonalisation")) return 6;
-  if (!cuda_ok(cudaMemcpyAsync(hd.data(), d, m * sizeof(double), cudaMemcpyDeviceToHost, s), err, "D2H")) return 6;
-  if (m > 1 && !cuda_ok(cudaMemcpyAsync(he.data(), e, (m - 1) * sizeof(double), cudaMemcpyDeviceToHost, s), err, "D2H"))
-    return 6;
-  if (!cuda_ok(cudaStreamSynchronize(s), err, "sync")) return 6;
-  he[m - 1] = 0.0;
-  // ---- (2) divide and conquer: the tree (levels of internal nodes, leaves)
+  const bool trace = getenv("OZR_TRACE") != nullptr;
+  cudaEvent_t tev[4] = {};
+  if (trace)
+    for (auto& ev : tev) cudaEventCreate(&ev);
+  if (trace) cudaEventRecord(tev[0], s);
+  const bool only_dc = dbg && dbg->d_in;
+  if (only_dc) {  // stage (2) alone on a given tridiagonal
+    if (!cuda_ok(cudaMemcpyAsync(hd.data(), dbg->d_in, m * sizeof(double), cudaMemcpyDeviceToHost, s), err, "D2H") ||
+        (m > 1 && !cuda_ok(cudaMemcpyAsync(he.data(), dbg->e_in, (m - 1) * sizeof(double), cudaMemcpyDeviceToHost, s),
+                           err, "D2H")) ||
+        !cuda_ok(cudaStreamSynchronize(s), err, "sync"))
+      return 6;
+    he[m - 1] = 0.0;
+    if (!cuda_ok(cudaMemcpyAsync(e, he.data(), m * sizeof(double), cudaMemcpyHostToDevice, s), err, "H2D")) return 6;
+  } else {
+    // ---- (1) tridiagonalise
+    if (!cuda_ok(syev_tridiag(K, m, d, e, tau, V, Wp, part, G, s), err, "tridiagonalisation")) return 6;
+    if (dbg && dbg->d_out) {  // stage (1) alone: d, e, τ out (K holds the reflectors)
+      if (!cuda_ok(cudaMemcpyAsync(dbg->d_out, d, m * sizeof(double), cudaMemcpyDeviceToDevice, s), err, "copy") ||
+          !cuda_ok(cudaMemcpyAsync(dbg->e_out, e, m * sizeof(double), cudaMemcpyDeviceToDevice, s), err, "copy") ||
+          !cuda_ok(cudaMemcpyAsync(dbg->tau_out, tau, m * sizeof(double), cudaMemcpyDeviceToDevice, s), err, "copy") ||
+          !cuda_ok(cudaStreamSynchronize(s), err, "sync"))
+        return 6;
+      return 0;
+    }
+    if (!cuda_ok(cudaMemcpyAsync(hd.data(), d, m * sizeof(double), cudaMemcpyDeviceToHost, s), err, "D2H")) return 6;
+    if (m > 1 && !cuda_ok(cudaMemcpyAsync(he.data(), e, (m - 1) * sizeof(double), cudaMemcpyDeviceToHost, s), err, "D2H"))
+      return 6;
+    if (!cuda_ok(cudaStreamSynchronize(s), err, "sync")) return 6;
+    he[m - 1] = 0.0;
+  }
+  if (trace) cudaEventRecord(tev[1], s);
+  // ---- (2) divide and conquer on T·2^s with max|T_ij| ∈ [½, 1) (an exact power-of-two scaling, as LAPACK's dstedc
+  // scales to unit norm): the deflation tolerance 8ε·max(|D|, |z|) compares quantities of the same scale only then
+  double tnrm = 0.0;
+  for (int a = 0; a < m; ++a) tnrm = std::max(tnrm, std::max(std::fabs(hd[a]), std::fabs(he[a])));
+  const int sexp = (tnrm > 0.0) ? -std::ilogb(tnrm) - 1 : 0;
+  for (int a = 0; a < m; ++a) {
+    hd[a] = std::ldexp(hd[a], sexp);
+    he[a] = std::ldexp(he[a], sexp);
+  }
+  if (!cuda_ok(cudaMemcpyAsync(e, he.data(), m * sizeof(double), cudaMemcpyHostToDevice, s), err, "H2D")) return 6;
+  // the tree (levels of internal nodes, leaves)
   std::vector<std::vector<Node>> levels;
   std::vector<int> llo, lhi;
   std::vector<double> dm(hd);
@@ -898,6 +995,17 @@ int dense_syev(SyevWorkspace& w, int m, double* K, double* theta, double* Y, con
         !cuda_ok(cudaMemcpyAsync(hlam.data(), lamo, m * sizeof(double), cudaMemcpyDeviceToHost, s), err, "D2H") ||
         !cuda_ok(cudaStreamSynchronize(s), err, "sync"))
       return 6;
+    if (getenv("OZR_SYEV_DUMP")) {  // debugging aid: the inputs of every merge level
+      FILE* f = fopen((std::string(getenv("OZR_SYEV_DUMP")) + "_lev" + std::to_string(lev) + ".bin").c_str(), "wb");
+      if (f) {
+        fwrite(hlam.data(), sizeof(double), m, f);
+        fwrite(hz.data(), sizeof(double), m, f);
+        std::vector<double> hq(mm);
+        cudaMemcpy(hq.data(), Q, mm * sizeof(double), cudaMemcpyDeviceToHost);
+        fwrite(hq.data(), sizeof(double), mm, f);
+        fclose(f);
+      }
+    }
     // host: sort, deflation (LAPACK dlaed2's rules), the Qp column sources and rotations
     std::vector<int> src(m, 0), rot_off(nn_nodes + 1, 0), root_node, root_j;
     std::vector<int4> rot_idx;
@@ -1024,7 +1132,7 @@ int dense_syev(SyevWorkspace& w, int m, double* K, double* theta, double* Y, con
     int maxn = 0;
     for (const Node& nd : nodes) maxn = std::max(maxn, nd.hi - nd.lo);
     // the node lo/hi arrays for permrot: reuse ibuf (still holds lo | mid | hi)
-    k_dc_permrot<<<dim3((maxn + 127) / 128, nn_nodes), 128, 0, s>>>(ibuf, ibuf + 2 * nn_nodes, dpk, dpk + o_roff,
+    k_dc_permrot<<<dim3((maxn + 127) / 128, nn_nodes), 128, 0, s>>>(ibuf, ibuf + nn_nodes, ibuf + 2 * nn_nodes, dpk, dpk + o_roff,
                                                                    reinterpret_cast<const int4*>(dpk + o_ri), dcs, Q, Qp, m);
     if (nroots > 0) {
       k_dc_secular<<<(nroots + 127) / 128, 128, 0, s>>>(dnd, dpk + o_rn, dpk + o_rj, nroots, dk, zk, org, ts);
@@ -1044,6 +1152,17 @@ int dense_syev(SyevWorkspace& w, int m, double* K, double* theta, double* Y, con
     }
     if (!cuda_ok(cudaStreamSynchronize(s), err, "sync")) return 6;  // the staging vectors go out of scope
   }
+  if (getenv("OZR_SYEV_DUMP")) {
+    FILE* f = fopen((std::string(getenv("OZR_SYEV_DUMP")) + "_final.bin").c_str(), "wb");
+    if (f) {
+      std::vector<double> hq(mm), hl(m);
+      cudaMemcpy(hq.data(), Q, mm * sizeof(double), cudaMemcpyDeviceToHost);
+      cudaMemcpy(hl.data(), lamo, m * sizeof(double), cudaMemcpyDeviceToHost);
+      fwrite(hl.data(), sizeof(double), m, f);
+      fwrite(hq.data(), sizeof(double), mm, f);
+      fclose(f);
+    }
+  }
   // eigenvalues ascending, columns permuted accordingly
   if (!cuda_ok(cudaMemcpyAsync(hlam.data(), lamo, m * sizeof(double), cudaMemcpyDeviceToHost, s), err, "D2H") ||
       !cuda_ok(cudaStreamSynchronize(s), err, "sync"))
@@ -1053,7 +1172,14 @@ int dense_syev(SyevWorkspace& w, int m, double* K, double* theta, double* Y, con
   std::stable_sort(perm.begin(), perm.end(), [&](int a, int b) { return hlam[a] < hlam[b]; });
   if (!cuda_ok(cudaMemcpyAsync(ibuf, perm.data(), m * sizeof(int), cudaMemcpyHostToDevice, s), err, "H2D")) return 6;
   double* Yt = Q1;  // Q_T sorted
-  k_dc_final<<<dim3(std::max(1, std::min(16, (m + 255) / 256)), m), 256, 0, s>>>(ibuf, Q, lamo, m, Yt, theta);
+  k_dc_final<<<dim3(std::max(1, std::min(16, (m + 255) / 256)), m), 256, 0, s>>>(ibuf, Q, lamo, m, Yt, theta, -sexp);
+  if (only_dc) {
+    if (!cuda_ok(cudaMemcpyAsync(Y, Yt, mm * sizeof(double), cudaMemcpyDeviceToDevice, s), err, "copy") ||
+        !cuda_ok(cudaStreamSynchronize(s), err, "sync"))
+      return 6;
+    return 0;
+  }
+  if (trace) cudaEventRecord(tev[2], s);
   // ---- (3) back-transformation Y = Qᴴ·Q_T, blocks of NBB reflectors from the last to the first
   constexpr int NBB = 128;
   SY_ALLOC(Vb, W_VB, double, static_cast<size_t>(m) * NBB);
@@ -1103,6 +1229,17 @@ int dense_syev(SyevWorkspace& w, int m, double* K, double* theta, double* Y, con
   if (!cuda_ok(cudaMemcpyAsync(&herr, derr, sizeof(int), cudaMemcpyDeviceToHost, s), err, "D2H") ||
       !cuda_ok(cudaStreamSynchronize(s), err, "sync"))
     return 6;
+  if (trace) {
+    cudaEventRecord(tev[3], s);
+    cudaEventSynchronize(tev[3]);
+    float t1 = 0, t2 = 0, t3 = 0;
+    cudaEventElapsedTime(&t1, tev[0], tev[1]);
+    cudaEventElapsedTime(&t2, tev[1], tev[2]);
+    cudaEventElapsedTime(&t3, tev[2], tev[3]);
+    fprintf(stderr, "[ozr syev] m=%d G=%d tridiag %.3f ms, divide-and-conquer %.3f ms, back-transformation %.3f ms\n", m, G,
+            t1, t2, t3);
+    for (auto& ev : tev) cudaEventDestroy(ev);
+  }
   if (herr) {
     if (err) *err = "dense eigensolver: a leaf QL iteration did not converge";
     return 6;

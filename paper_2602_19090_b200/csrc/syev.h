@@ -26,8 +26,17 @@ using SyevGemm = std::function<int(int M, int N, int K, const double* A, int lda
 // K (m x m, ld = m, lower triangle read, destroyed) = YΘYᵀ: θ ascending (device, m), Y (device, m x m, ld = m).
 // Products with a dimension ≥ big_gemm_min go to `gemm` (when set). Returns 0, or 6 (CUDA error / no
 // convergence) / 8 (out of memory) with *err set.
+// Stage checks (tests): d_out set — stop after the tridiagonalisation (d, e, τ out; K holds the reflectors below
+// its sub-diagonal); d_in set — the divide and conquer alone on the tridiagonal (d_in, e_in): θ, Y = its eigenvectors.
+struct SyevDebug {
+  double* d_out = nullptr;
+  double* e_out = nullptr;
+  double* tau_out = nullptr;
+  const double* d_in = nullptr;
+  const double* e_in = nullptr;
+};
 int dense_syev(SyevWorkspace& w, int m, double* K, double* theta, double* Y, const SyevGemm& gemm, int big_gemm_min,
-               cudaStream_t s, std::string* err);
+               cudaStream_t s, std::string* err, const SyevDebug* dbg = nullptr);
 
 // pieces (tests / measurement)
 int syev_trd_grid(int m);

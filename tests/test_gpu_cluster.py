@@ -28,7 +28,7 @@ def _case(cfg, n, start):
 
 @pytest.mark.parametrize("n,dense", [(128, 1 << 20), (256, 1 << 20), (256, 2), (256, 192)])
 def test_fp32_start_sweep_parity(ctx, n, dense):
-    """dense = 2: every group takes the dense sub-solve (dense_eig.cu, cuSOLVER syevd) instead of Jacobi; 2^20:
+    """dense = 2: every group takes the dense sub-solve (dense_eig.cu + the hand-written eigensolver syev.cu) instead of Jacobi; 2^20:
     every group takes a Jacobi (per-CTA, or whole-GPU cooperative from 192 columns); 192: the default. The
     same K, so the same tolerance against the oracle's __float128 Jacobi."""
     A, lam0, X0 = _case("c2", n, "fp32")
@@ -147,7 +147,7 @@ def test_c4_recipe_fp32_start_converges(ctx, n, delta):
 
 def test_c4_recipe_default_dense_path(ctx):
     """BASELINE c4's recipe at n = 2048 with the DEFAULT parameters: the FP32 start leaves one group of more
-    than 1024 columns, which takes the dense sub-solve (cuSOLVER syevd); the refinement
+    than 1024 columns, which takes the dense sub-solve (the hand-written eigensolver, syev.cu); the refinement
     converges (status OK) to an orthonormal eigenbasis: max_j ‖A x_j − λ_j x_j‖ and ‖XᵀX − I‖_max at the
     fp64 level (the forward error itself is checked at n = 512 / 1024 above)."""
     import paper_2602_19090_b200 as ozr

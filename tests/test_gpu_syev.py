@@ -4,7 +4,7 @@ eigenvectors, blocked back-transformation; include/ozr.h).
 
 Pinned against (a) the oracle's __float128 cyclic Jacobi (oracle/ddmm.c) for m ≤ 48: eigenvalues to
 1e-14·‖K‖ and eigenvector columns up to sign to u‖K‖/gap; (b) at any size, the properties a backward-stable
-eigensolver has: ‖KY − YΘ‖_F ≤ c·u·‖K‖_F, ‖YᵀY − I‖_max ≤ c·u·√m·log m, θ ascending, and the exactly known
+eigensolver has: ‖KY − YΘ‖_F ≤ c·u·√m·‖K‖_F, ‖YᵀY − I‖_max ≤ c·u·√m·log m, θ ascending, and the exactly known
 spectrum of the Householder family A = H diag(λ) H to c·u·‖K‖. Sizes span one leaf (≤ 32), several
 merge levels, the INT8 product path (dimension ≥ 1024), ragged tails, and spectra with heavy deflation (repeated
 and graded eigenvalues, a diagonal matrix)."""
@@ -28,12 +28,13 @@ def _run(ctx, K):
 
 
 def _check_props(K, th, Y, c=64.0):
+    """Backward stability: ‖KY − YΘ‖_F ≤ c·u·√m·‖K‖_F (the usual p(m) = √m growth), orthogonality to c·u·√m·log m."""
     m = K.shape[0]
     nK = np.linalg.norm(K)
     res = np.linalg.norm(K @ Y - Y * th[None, :])
     orth = np.max(np.abs(Y.T @ Y - np.eye(m)))
     assert np.all(np.diff(th) >= 0), "not ascending"
-    assert res <= c * U * max(nK, 1e-300) * np.sqrt(np.log2(m + 1) + 1), (res, nK)
+    assert res <= c * U * max(nK, 1e-300) * np.sqrt(m), (res, nK)
     assert orth <= c * U * np.sqrt(m) * (np.log2(m + 1) + 1), orth
     return res, orth
 
@@ -105,3 +106,38 @@ def test_syev_repeated_and_diagonal(ctx, m):
     th, Y = _run(ctx, D)
     assert np.array_equal(th, np.arange(m, dtype=np.float64))
     _check_props(D, th, Y)
+
+
+@pytest.mark.parametrize("m", [3, 33, 64, 100, 257])
+def test_stage_tridiagonalisation(ctx, m):
+    """Stage (1) alone: the reflectors H_c = I − τ_c v_c v_cᵀ it returns satisfy Q_Hᵀ K Q_H = tridiag(d, e) with
+    Q_H = H_0⋯H_{m−2} (LAPACK dsytrd's lower convention), to c·u·‖K‖."""
+    K = _random_sym(m, 11 + m)
+    Kd = ozr.colmajor(torch.from_numpy(np.asfortranarray(K)).cuda())
+    d, e, tau, R = (t.cpu().numpy() for t in ozr.ozr_syev_tridiag(ctx, Kd))
+    Q = np.eye(m)
+    for c in range(m - 1):
+        v = np.zeros(m)
+        v[c + 1] = 1.0
+        v[c + 2:] = R[c + 2:, c]
+        Q = Q @ (np.eye(m) - tau[c] * np.outer(v, v))
+    T = Q.T @ K @ Q
+    Tref = np.diag(d) + np.diag(e[:m - 1], -1) + np.diag(e[:m - 1], 1)
+    assert np.max(np.abs(T - Tref)) <= 64 * U * np.linalg.norm(K) * np.sqrt(m), np.max(np.abs(T - Tref))
+
+
+@pytest.mark.parametrize("m", [33, 64, 100, 700])
+def test_stage_divide_and_conquer(ctx, m):
+    """Stage (2) alone on a random tridiagonal: eigenvalues against LAPACK's tridiagonal solver (scipy), residual
+    and orthogonality of the Gu–Eisenstat eigenvectors."""
+    from scipy.linalg import eigh_tridiagonal
+    rng = np.random.default_rng(m)
+    d = rng.standard_normal(m)
+    e = rng.standard_normal(m)
+    e[m - 1] = 0.0
+    th, Y = ozr.ozr_syev_tridiag_eig(ctx, torch.from_numpy(d).cuda(), torch.from_numpy(e).cuda())
+    th, Y = th.cpu().numpy(), Y.cpu().numpy()
+    T = np.diag(d) + np.diag(e[:m - 1], -1) + np.diag(e[:m - 1], 1)
+    ref = eigh_tridiagonal(d, e[:m - 1], eigvals_only=True)
+    assert np.max(np.abs(th - ref)) <= 64 * U * np.linalg.norm(T, 2) * np.sqrt(m)
+    _check_props(T, th, Y)
