@@ -70,8 +70,9 @@ struct PanelArgs {
   double* d;        // diagonal of T
   double* e;        // sub-diagonal of T
   double* tau;      // reflector scalars
-  double* part;     // G x (2 + 2·NB) scalar partials
+  double* part;     // G x (5 + 2·NB) scalar partials
   double* yp;       // tile partials: slot(I, J) x 2 x TB
+  double* gam;      // NB: γ_j of the panel's columns (W = W' + V·diag(γ); W' is what W holds)
 };
 
 // Sum of the G per-CTA partials part[g·PS + off] in a fixed order (every CTA gets the same value): thread t sums
@@ -88,10 +89,30 @@ struct PanelSmem {
   double tile[TB][TB + 1];  // tile[col][row]
   double vs[NB][TB], ws[NB][TB];
   double vr[TB], vc[TB], vloc[TB];
-  double rowc[2 * NB];      // V(c, 0:i) | W(c, 0:i)
+  double rowc[2 * NB];      // V(c, 0:i) | W(c, 0:i−1) (corrected)
+  double gam[NB];           // γ_j of the finished columns
   double dots[2 * NB];      // Vᵀv | Wᵀv (reduced over the grid)
   double sh[TT / 32];
 };
+
+// Two grid-wide barriers per column. W(:, i)'s last correction γ_i·V(:, i) (γ_i = −½τ_i·w'ᵀv, a grid reduction)
+// is never written back during the panel: W holds W', the γ_j are kept, and every use forms W' + γ_j V on the fly.
+// Column i+1's phase A leaves out the terms of column i's W (unknown γ_i, and W'(c, i) of another CTA's row not yet
+// visible); after the first barrier x = x'' − κ·V(r, i), κ = W'(c, i) + 2γ_i V(c, i), so σ = Σx''² − 2κΣx''b + κ²Σb²
+// (b_r = V(r, i)), α and d_c follow from x'', and v_r = x_r·scale is formed on the fly.
+__device__ __forceinline__ void trd_tile_load(const double* __restrict__ A, int m, int c, int I, int J, int tid,
+                                              double (&reg)[TB * TB / TT]) {
+  const int rt0 = I * TB, qt0 = J * TB;
+#pragma unroll
+  for (int u = 0; u < TB * TB / TT; ++u) {
+    const int e2 = tid + u * TT;
+    const int rho = e2 & (TB - 1), kap = e2 >> 6;
+    const int r = rt0 + rho, q = qt0 + kap;
+    const bool in = r < m && q < m && r >= c + 1 && q >= c + 1;
+    const long long idx = (r >= q) ? r + static_cast<long long>(q) * m : q + static_cast<long long>(r) * m;
+    reg[u] = in ? __ldcg(A + idx) : 0.0;
+  }
+}
 
 __global__ void __launch_bounds__(TT) k_trd_panel(PanelArgs P) {
   cg::grid_group grid = cg::this_grid();
@@ -101,46 +122,87 @@ __global__ void __launch_bounds__(TT) k_trd_panel(PanelArgs P) {
   const int m = P.m;
   const int mt = (m + TB - 1) / TB;
   double* A = P.A;
-  const int PS = 2 + 2 * NB;
+  const int PS = 5 + 2 * NB;  // per CTA: Σx''², Σx''b, Σb², w'ᵀv, Σx² (exact, rare) | Vᵀv (NB) | Wᵀv (NB)
   const int r0own = b * TB;
   const bool owner = b < mt;
-  double gam_prev = 0.0;  // γ of the previous column: W(:, i−1) += γ·V(:, i−1) still pending in global memory
+  double tau_prev = 0.0;
   for (int i = 0; i < P.nb; ++i) {
     const int c = P.k0 + i;
-    // ---- phase A: x_r = A(r,c) − V(r,:)W(c,:)ᵀ − W(r,:)V(c,:)ᵀ on own rows r ≥ c
+    // ---- phase A: x''_r = A(r,c) − Σ_{j<i−1} [V(r,j)W(c,j) + W(r,j)V(c,j)] − W'(r,i−1)V(c,i−1), own rows r ≥ c
     if (tid < 2 * i) {
       const int j = tid < i ? tid : tid - i;
       const double vcj = P.V[c + static_cast<long long>(j) * m];
-      double val = (tid < i) ? vcj : P.W[c + static_cast<long long>(j) * m];
-      if (tid >= i && j == i - 1) val = fma(gam_prev, vcj, val);
-      S.rowc[tid < i ? j : NB + j] = val;
+      if (tid < i) S.rowc[j] = vcj;
+      else if (j < i - 1) S.rowc[NB + j] = fma(S.gam[j], vcj, P.W[c + static_cast<long long>(j) * m]);
     }
-    if (i > 0 && tid < TB) S.ws[i - 1][tid] = fma(gam_prev, S.vs[i - 1][tid], S.ws[i - 1][tid]);  // private rows
     __syncthreads();
-    double ss = 0.0;
+    double ss = 0.0, sxb = 0.0, sbb = 0.0;
     if (owner && tid < TB) {
       const int r = r0own + tid;
       if (r < m && r >= c) {
         double x = A[r + static_cast<long long>(c) * m];
         double x2 = 0.0;
-        for (int j = 0; j < i; j += 2) {
+        for (int j = 0; j + 1 < i; j += 2) {
           x -= S.vs[j][tid] * S.rowc[NB + j] + S.ws[j][tid] * S.rowc[j];
-          if (j + 1 < i) x2 -= S.vs[j + 1][tid] * S.rowc[NB + j + 1] + S.ws[j + 1][tid] * S.rowc[j + 1];
+          if (j + 2 < i) x2 -= S.vs[j + 1][tid] * S.rowc[NB + j + 1] + S.ws[j + 1][tid] * S.rowc[j + 1];
         }
+        if (i > 0) x2 -= S.ws[i - 1][tid] * S.rowc[i - 1];  // W'(r, i−1) V(c, i−1)
         x += x2;
         A[r + static_cast<long long>(c) * m] = x;
-        if (r >= c + 2) ss = x * x;
+        if (r >= c + 2) {
+          const double bb = (i > 0) ? S.vs[i - 1][tid] : 0.0;
+          ss = x * x;
+          sxb = x * bb;
+          sbb = bb * bb;
+        }
       }
     }
     ss = block_sum256(ss, S.sh);
-    if (tid == 0) P.part[static_cast<long long>(b) * PS] = ss;
+    sxb = block_sum256(sxb, S.sh);
+    sbb = block_sum256(sbb, S.sh);
+    if (tid == 0) {
+      P.part[static_cast<long long>(b) * PS] = ss;
+      P.part[static_cast<long long>(b) * PS + 1] = sxb;
+      P.part[static_cast<long long>(b) * PS + 2] = sbb;
+    }
     grid.sync();
-    // ---- phase B: the reflector (every CTA, the same fixed-order sums), V(:, i), the tile products, Vᵀv and Wᵀv
-    const double sigma = grid_partial_sum(P.part, PS, 0, G, S.sh);
-    const double ccdiag = A[c + static_cast<long long>(c) * m];
+    // ---- phase B: γ_{i−1}, the reflector (every CTA, the same fixed-order sums), V(:, i), the tile products, Vᵀv, Wᵀv
+    double kap = 0.0;
+    if (i > 0) {
+      const double gam = -0.5 * tau_prev * grid_partial_sum(P.part, PS, 3, G, S.sh);
+      kap = fma(2.0 * gam, S.rowc[i - 1], P.W[c + static_cast<long long>(i - 1) * m]);
+      if (tid == 0) S.gam[i - 1] = gam;
+      if (tid < TB) S.ws[i - 1][tid] = fma(gam, S.vs[i - 1][tid], S.ws[i - 1][tid]);  // private rows
+    }
+    const double sig0 = grid_partial_sum(P.part, PS, 0, G, S.sh);
+    const double sig1 = grid_partial_sum(P.part, PS, 1, G, S.sh);
+    const double sig2 = grid_partial_sum(P.part, PS, 2, G, S.sh);
+    double sigma = sig0 - 2.0 * kap * sig1 + kap * kap * sig2;
+    // the expansion's rounding error (≈ u·(Σx''² + κ²Σb²)) enters the reflector's orthogonality as δσ/σ (τ·vᵀv =
+    // 2 + δσ/(β(β − α))), so it is trusted only without cancellation; otherwise Σ x_r² exactly, one more barrier
+    if (i > 0 && !(sigma >= 0.5 * (sig0 + kap * kap * sig2))) {
+      double sx = 0.0;
+      if (owner && tid < TB) {
+        const int r = r0own + tid;
+        if (r < m && r >= c + 2) {
+          const double x = fma(-kap, S.vs[i - 1][tid], A[r + static_cast<long long>(c) * m]);
+          sx = x * x;
+        }
+      }
+      sx = block_sum256(sx, S.sh);
+      if (tid == 0) P.part[static_cast<long long>(b) * PS + 4] = sx;
+      grid.sync();
+      sigma = grid_partial_sum(P.part, PS, 4, G, S.sh);
+    }
+    sigma = fmax(sigma, 0.0);
+    auto xfin = [&](int r) -> double {  // x_r = x''_r − κ V(r, i−1)
+      const double x = A[r + static_cast<long long>(c) * m];
+      return (i > 0) ? fma(-kap, P.V[r + static_cast<long long>(i - 1) * m], x) : x;
+    };
+    const double ccdiag = xfin(c);
     double alpha = 0.0, beta = 0.0, tau = 0.0, scale = 0.0;
     if (c + 1 < m) {
-      alpha = A[c + 1 + static_cast<long long>(c) * m];
+      alpha = xfin(c + 1);
       if (sigma == 0.0) {
         beta = alpha;  // H = I
       } else {
@@ -156,12 +218,8 @@ __global__ void __launch_bounds__(TT) k_trd_panel(PanelArgs P) {
         P.tau[c] = tau;
       }
     }
-    if (owner && tid < TB && i > 0) {  // the pending correction of W(:, i−1), own rows r ≥ c (global copy)
-      const int r = r0own + tid;
-      if (r < m && r >= c) P.W[r + static_cast<long long>(i - 1) * m] = S.ws[i - 1][tid];
-    }
     if (c + 1 >= m) break;  // the last column: only its diagonal
-    auto vof = [&](int r) -> double { return r == c + 1 ? 1.0 : (r > c + 1 ? A[r + static_cast<long long>(c) * m] * scale : 0.0); };
+    auto vof = [&](int r) -> double { return r == c + 1 ? 1.0 : (r > c + 1 ? xfin(r) * scale : 0.0); };
     if (owner && tid < TB) {
       const int r = r0own + tid;
       const double v = (r < m) ? vof(r) : 0.0;
@@ -173,35 +231,32 @@ __global__ void __launch_bounds__(TT) k_trd_panel(PanelArgs P) {
       const int J0 = (c + 1) / TB;
       const int na = mt - J0;
       const int ntiles = na * (na + 1) / 2;
-      for (int t = b; t < ntiles; t += G) {
-        int I, J;
+      double reg[TB * TB / TT];
+      int t = b, I = 0, J = 0;
+      if (t < ntiles) {
         tile_of(t, J0, I, J);
+        trd_tile_load(A, m, c, I, J, tid, reg);
+      }
+      while (t < ntiles) {
         const int rt0 = I * TB, qt0 = J * TB;
-        __syncthreads();
-        {  // tile[κ][ρ] = A(rt0+ρ, qt0+κ), lower part (mirrored on the diagonal): all 16 loads in flight first
-          double reg[TB * TB / TT];
+        __syncthreads();  // the previous tile's readers are done with shared memory
 #pragma unroll
-          for (int u = 0; u < TB * TB / TT; ++u) {
-            const int e2 = tid + u * TT;
-            const int rho = e2 & (TB - 1), kap = e2 >> 6;
-            const int r = rt0 + rho, q = qt0 + kap;
-            const bool in = r < m && q < m && r >= c + 1 && q >= c + 1;
-            const long long idx = (r >= q) ? r + static_cast<long long>(q) * m : q + static_cast<long long>(r) * m;
-            reg[u] = in ? __ldcg(A + idx) : 0.0;
-          }
-#pragma unroll
-          for (int u = 0; u < TB * TB / TT; ++u) {
-            const int e2 = tid + u * TT;
-            S.tile[e2 >> 6][e2 & (TB - 1)] = reg[u];
-          }
+        for (int u = 0; u < TB * TB / TT; ++u) {
+          const int e2 = tid + u * TT;
+          S.tile[e2 >> 6][e2 & (TB - 1)] = reg[u];
         }
         if (tid < TB) S.vr[tid] = (rt0 + tid < m) ? vof(rt0 + tid) : 0.0;
         else if (tid < 2 * TB) S.vc[tid - TB] = (qt0 + tid - TB < m) ? vof(qt0 + tid - TB) : 0.0;
         __syncthreads();
+        const int tn = t + G;  // prefetch the next tile while this one is reduced
+        int In = 0, Jn = 0;
+        if (tn < ntiles) {
+          tile_of(tn, J0, In, Jn);
+          trd_tile_load(A, m, c, In, Jn, tid, reg);
+        }
         double* out = P.yp + tslot(I, J) * 2 * TB;
-        // 4 threads per output: threads 0..127 → row sums (half a row each... 2 per row), 128..255 → column sums
         const int half = tid & 1;
-        if (tid < 2 * TB) {  // row ρ = tid/2: Σ_κ tile[κ][ρ] vc[κ] over κ ≡ half (mod 2)
+        if (tid < 2 * TB) {  // row ρ = tid/2: Σ_κ tile[κ][ρ] vc[κ], κ ≡ half (mod 2)
           const int rho = tid >> 1;
           double acc = 0.0;
 #pragma unroll 8
@@ -218,36 +273,39 @@ __global__ void __launch_bounds__(TT) k_trd_panel(PanelArgs P) {
           acc += __shfl_xor_sync(0xffffffffu, acc, 1);
           if (!half) out[TB + kap] = acc;
         }
+        t = tn;
+        I = In;
+        J = Jn;
       }
       // Vᵀv and Wᵀv over own rows: 2i dot products of length TB from shared memory, 4 threads each
       __syncthreads();
       if (owner && i > 0) {
-        const int q = tid >> 2, part = tid & 3;  // q < 64: product index (j for V, NB + j for W)
+        const int q = tid >> 2, part = tid & 3;
         if (q < 2 * NB) {
           const int j = q < NB ? q : q - NB;
           double acc = 0.0;
           if (j < i) {
             const double* row = q < NB ? S.vs[j] : S.ws[j];
-            for (int t = part; t < TB; t += 4) acc = fma(row[t], S.vloc[t], acc);
+            for (int t2 = part; t2 < TB; t2 += 4) acc = fma(row[t2], S.vloc[t2], acc);
           }
           acc += __shfl_xor_sync(0xffffffffu, acc, 1);
           acc += __shfl_xor_sync(0xffffffffu, acc, 2);
-          if (part == 0 && j < i) P.part[static_cast<long long>(b) * PS + 2 + q] = acc;
+          if (part == 0 && j < i) P.part[static_cast<long long>(b) * PS + 5 + q] = acc;
         }
       } else if (i > 0 && tid < 2 * NB) {
         const int j = tid < NB ? tid : tid - NB;
-        if (j < i) P.part[static_cast<long long>(b) * PS + 2 + tid] = 0.0;
+        if (j < i) P.part[static_cast<long long>(b) * PS + 5 + tid] = 0.0;
       }
     }
     grid.sync();
-    // ---- phase C: y_r from the tile partials, w'_r = τ(y − V(Wᵀv) − W(Vᵀv)), partial of w'ᵀv
+    // ---- phase C: y_r from the tile partials, w'_r = τ(y − V(Wᵀv) − W(Vᵀv)), partial of w'ᵀv (its γ: next column)
     double p3 = 0.0;
     if (tau != 0.0) {
       if (i > 0) {  // Vᵀv, Wᵀv reduced over the grid: 4 threads per value, fixed order
         const int q = tid >> 2, part = tid & 3;
         double acc = 0.0;
         if (q < 2 * NB && (q < NB ? q : q - NB) < i)
-          for (int g = part; g < G; g += 4) acc += P.part[static_cast<long long>(g) * PS + 2 + q];
+          for (int g = part; g < G; g += 4) acc += P.part[static_cast<long long>(g) * PS + 5 + q];
         acc += __shfl_xor_sync(0xffffffffu, acc, 1);
         acc += __shfl_xor_sync(0xffffffffu, acc, 2);
         if (part == 0 && q < 2 * NB) S.dots[q] = acc;
@@ -286,23 +344,27 @@ __global__ void __launch_bounds__(TT) k_trd_panel(PanelArgs P) {
       if (r < m && r >= c + 1) P.W[r + static_cast<long long>(i) * m] = 0.0;
     }
     p3 = block_sum256(p3, S.sh);
-    if (tid == 0) P.part[static_cast<long long>(b) * PS + 1] = p3;
-    grid.sync();
-    gam_prev = -0.5 * tau * grid_partial_sum(P.part, PS, 1, G, S.sh);
+    if (tid == 0) P.part[static_cast<long long>(b) * PS + 3] = p3;
+    tau_prev = tau;
   }
-  // the last column's pending γ (rows ≥ its c + 1), for the trailing update
+  // the last column's γ (one more barrier for its w'ᵀv); the γ_j go to the trailing update
   const int ilast = P.nb - 1, clast = P.k0 + ilast;
-  if (clast + 1 < m && owner && tid < TB) {
-    const int r = r0own + tid;
-    if (r < m && r >= clast + 1)
-      P.W[r + static_cast<long long>(ilast) * m] = fma(gam_prev, S.vs[ilast][tid], S.ws[ilast][tid]);
+  if (clast + 1 < m) {
+    grid.sync();
+    const double gam = -0.5 * tau_prev * grid_partial_sum(P.part, PS, 3, G, S.sh);
+    if (tid == 0) S.gam[ilast] = gam;
+  } else if (tid == 0) {
+    S.gam[ilast] = 0.0;
   }
+  __syncthreads();
+  if (b == 0 && tid < P.nb) P.gam[tid] = S.gam[tid];
 }
 
 // Trailing update of the lower tiles of A(k1:m, k1:m): A −= V Wᵀ + W Vᵀ (nb columns); also stores the panel's
 // reflectors below the sub-diagonal: A(r, k0 + j) = V(r, j) for r ≥ k0 + j + 2 (tiles with J == -1: the copy).
 __global__ void __launch_bounds__(TT) k_trd_update(double* __restrict__ A, int m, int k0, int nb,
-                                                   const double* __restrict__ V, const double* __restrict__ W) {
+                                                   const double* __restrict__ V, const double* __restrict__ W,
+                                                   const double* __restrict__ gam) {
   __shared__ double vR[NB][TB], wR[NB][TB], vC[NB][TB / 2], wC[NB][TB / 2];  // 48 KB: columns in two halves
   const int k1 = k0 + nb;
   const int J0 = k1 / TB, mt = (m + TB - 1) / TB;
@@ -322,8 +384,9 @@ __global__ void __launch_bounds__(TT) k_trd_update(double* __restrict__ A, int m
     const int rho = e2 & (TB - 1), j = e2 >> 6;
     const int r = r0 + rho;
     const bool jr = j < nb && r < m && r >= k1;
-    vR[j][rho] = jr ? V[r + static_cast<long long>(j) * m] : 0.0;
-    wR[j][rho] = jr ? W[r + static_cast<long long>(j) * m] : 0.0;
+    const double vv = jr ? V[r + static_cast<long long>(j) * m] : 0.0;
+    vR[j][rho] = vv;
+    wR[j][rho] = jr ? fma(gam[j], vv, W[r + static_cast<long long>(j) * m]) : 0.0;
   }
   const int rho = threadIdx.x & (TB - 1);
   const int r = r0 + rho;
@@ -334,8 +397,9 @@ __global__ void __launch_bounds__(TT) k_trd_update(double* __restrict__ A, int m
       const int kap = e2 & (TB / 2 - 1), j = e2 >> 5;
       const int q = qh + kap;
       const bool jq = j < nb && q < m && q >= k1;
-      vC[j][kap] = jq ? V[q + static_cast<long long>(j) * m] : 0.0;
-      wC[j][kap] = jq ? W[q + static_cast<long long>(j) * m] : 0.0;
+      const double vv = jq ? V[q + static_cast<long long>(j) * m] : 0.0;
+      vC[j][kap] = vv;
+      wC[j][kap] = jq ? fma(gam[j], vv, W[q + static_cast<long long>(j) * m]) : 0.0;
     }
     __syncthreads();
     for (int kk = threadIdx.x >> 6; kk < TB / 2; kk += TT / TB) {
@@ -671,21 +735,24 @@ __global__ void k_bt_vblock(const double* __restrict__ A, int m, int c0, int nbb
     Vb[r + static_cast<long long>(j) * m] = v;
   }
 }
-// T (nbb x nbb, upper, ld = nbb) of the compact WY form, from S = VbᵀVb (ld = nbb) and τ: T_ii = τ_i,
-// T(0:i, i) = −τ_i T(0:i, 0:i) S(0:i, i). One CTA.
-__global__ void k_bt_tmat(const double* __restrict__ S, const double* __restrict__ tau, int c0, int nbb,
+// Diagonal block q (columns q·TBT .. +nq) of T (upper, ld = ldt) of the compact WY form, from S = VbᵀVb (ld = ldt)
+// and τ: T_ii = τ_i, T(r, i) = −τ_i Σ_{l=r}^{i−1} T(r, l) S(l, i) within the block. One CTA per block.
+constexpr int TBT = 128;
+__global__ void k_bt_tmat(const double* __restrict__ S, const double* __restrict__ tau, int c0, int nbb, int ldt,
                           double* __restrict__ T) {
-  extern __shared__ double col[];
-  for (int i = 0; i < nbb; ++i) {
+  __shared__ double col[TBT];
+  const int q0 = blockIdx.x * TBT, nq = min(TBT, nbb - q0);
+  for (int ii = 0; ii < nq; ++ii) {
+    const int i = q0 + ii;
     const double ti = tau[c0 + i];
-    for (int r = threadIdx.x; r < i; r += blockDim.x) {
+    for (int r = q0 + threadIdx.x; r < i; r += blockDim.x) {
       double acc = 0.0;
-      for (int l = r; l < i; ++l) acc = fma(T[r + static_cast<long long>(l) * nbb], S[l + static_cast<long long>(i) * nbb], acc);
-      col[r] = -ti * acc;
+      for (int l = r; l < i; ++l) acc = fma(T[r + static_cast<long long>(l) * ldt], S[l + static_cast<long long>(i) * ldt], acc);
+      col[r - q0] = -ti * acc;
     }
     __syncthreads();
-    for (int r = threadIdx.x; r < nbb; r += blockDim.x)
-      T[r + static_cast<long long>(i) * nbb] = (r < i) ? col[r] : (r == i ? ti : 0.0);
+    for (int r = q0 + threadIdx.x; r < q0 + nq; r += blockDim.x)
+      T[r + static_cast<long long>(i) * ldt] = (r < i) ? col[r - q0] : (r == i ? ti : 0.0);
     __syncthreads();
   }
 }
@@ -765,7 +832,7 @@ __global__ void k_sub_strided(double* __restrict__ Y, int ldy, const double* __r
 
 size_t syev_trd_partials(int m, int G) {
   const int mt = (m + TB - 1) / TB;
-  return static_cast<size_t>(G) * (2 + 2 * NB) + static_cast<size_t>(mt) * (mt + 1) / 2 * 2 * TB;
+  return static_cast<size_t>(G) * (5 + 2 * NB) + static_cast<size_t>(mt) * (mt + 1) / 2 * 2 * TB;
 }
 
 int syev_trd_grid(int m) {
@@ -781,7 +848,7 @@ int syev_trd_grid(int m) {
   const int mt = (m + TB - 1) / TB;
   // one CTA per row block at least (each owns one); more for the tile products (~mt²/2 tiles), bounded by
   // co-residency; fewer CTAs = cheaper barriers
-  int want = std::max(mt, std::min(mt * (mt + 1) / 2, 3 * mt));
+  int want = std::max(mt, std::min(mt * (mt + 1) / 2, 5 * mt));
   if (const char* g = getenv("OZR_SYEV_G")) want = std::max(mt, std::min(mt * (mt + 1) / 2, atoi(g) * mt / 8));  // A/B: G = g/8 · mt
   return std::min(want, nsm * per);
 }
@@ -791,10 +858,10 @@ cudaError_t syev_tridiag(double* A, int m, double* d, double* e, double* tau, do
                          int G, cudaStream_t s) {
   const int mt = (m + TB - 1) / TB;
   if (G < mt) return cudaErrorInvalidConfiguration;  // every row block needs its owner CTA (m ≤ ~28000)
-  double* yp = part + static_cast<size_t>(G) * (2 + 2 * NB);
+  double* yp = part + static_cast<size_t>(G) * (5 + 2 * NB);
   for (int k0 = 0; k0 < m; k0 += NB) {
     const int nb = std::min(NB, m - k0);
-    PanelArgs P{A, m, k0, nb, V, W, d, e, tau, part, yp};
+    PanelArgs P{A, m, k0, nb, V, W, d, e, tau, part, yp, part + syev_trd_partials(m, G)};
     void* args[] = {&P};
     cudaError_t err = cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_trd_panel), dim3(G), dim3(TT), args,
                                                   sizeof(PanelSmem), s);
@@ -802,9 +869,9 @@ cudaError_t syev_tridiag(double* A, int m, double* d, double* e, double* tau, do
     const int k1 = k0 + nb;
     if (k1 < m) {
       const int J0 = k1 / TB, na = mt - J0;
-      k_trd_update<<<na * (na + 1) / 2 + nb, TT, 0, s>>>(A, m, k0, nb, V, W);
+      k_trd_update<<<na * (na + 1) / 2 + nb, TT, 0, s>>>(A, m, k0, nb, V, W, P.gam);
     } else {
-      k_trd_update<<<nb, TT, 0, s>>>(A, m, k0, nb, V, W);  // only the reflector copy (na = 0 tiles)
+      k_trd_update<<<nb, TT, 0, s>>>(A, m, k0, nb, V, W, P.gam);  // only the reflector copy (na = 0 tiles)
     }
   }
   return cudaGetLastError();
@@ -843,7 +910,7 @@ void syev_dgemm(int M, int N, int K, double alpha, const double* A, int lda, boo
 
 namespace {
 enum { W_D, W_E, W_TAU, W_V, W_W, W_PART, W_Q0, W_Q1, W_QP, W_U, W_DMOD, W_LAMO, W_LAMN, W_DK, W_ZK, W_ZH, W_TS,
-       W_ORG, W_Z, W_I, W_D2, W_NODE, W_TILE, W_ERR, W_VB, W_S, W_T, W_WT, W_WT2, W_P, W_STAGE };
+       W_ORG, W_Z, W_I, W_D2, W_NODE, W_TILE, W_ERR, W_VB, W_S, W_T, W_WT, W_WT2, W_P, W_STAGE, W_TT };
 
 struct Node {
   int lo, mid, hi;
@@ -873,7 +940,7 @@ int dense_syev(SyevWorkspace& w, int m, double* K, double* theta, double* Y, con
   SY_ALLOC(tau, W_TAU, double, m);
   SY_ALLOC(V, W_V, double, static_cast<size_t>(m) * NB);
   SY_ALLOC(Wp, W_W, double, static_cast<size_t>(m) * NB);
-  SY_ALLOC(part, W_PART, double, syev_trd_partials(m, G));
+  SY_ALLOC(part, W_PART, double, syev_trd_partials(m, G) + NB);  // + the panel's γ_j
   SY_ALLOC(Q0, W_Q0, double, mm);
   SY_ALLOC(Q1, W_Q1, double, mm);
   SY_ALLOC(Qp, W_QP, double, mm);
@@ -1181,10 +1248,11 @@ int dense_syev(SyevWorkspace& w, int m, double* K, double* theta, double* Y, con
   }
   if (trace) cudaEventRecord(tev[2], s);
   // ---- (3) back-transformation Y = Qᴴ·Q_T, blocks of NBB reflectors from the last to the first
-  constexpr int NBB = 128;
+  constexpr int NBB = 512;  // reflectors per pass over Y (blocks of TBT = 128 merged into one compact WY T)
   SY_ALLOC(Vb, W_VB, double, static_cast<size_t>(m) * NBB);
   SY_ALLOC(S, W_S, double, NBB * NBB);
   SY_ALLOC(Tm, W_T, double, NBB * NBB);
+  SY_ALLOC(Tt, W_TT, double, NBB * TBT);
   SY_ALLOC(Wt, W_WT, double, static_cast<size_t>(NBB) * m);
   SY_ALLOC(Wt2, W_WT2, double, static_cast<size_t>(NBB) * m);
   double* Pb = nullptr;
@@ -1203,7 +1271,15 @@ int dense_syev(SyevWorkspace& w, int m, double* K, double* theta, double* Y, con
     const int r0 = c0 + 1, rows = m - r0;  // rows of Vb that can be nonzero
     k_bt_vblock<<<dim3(std::max(1, std::min(32, (m + 255) / 256)), nbb), 256, 0, s>>>(K, m, c0, nbb, Vb);
     syev_dgemm(nbb, nbb, rows, 1.0, Vb + r0, m, true, Vb + r0, m, 0.0, S, nbb, s);  // S = VbᵀVb
-    k_bt_tmat<<<1, 128, NBB * sizeof(double), s>>>(S, tau, c0, nbb, Tm);
+    if (!cuda_ok(cudaMemsetAsync(Tm, 0, sizeof(double) * nbb * nbb, s), err, "memset")) return 6;
+    const int nsub = (nbb + TBT - 1) / TBT;
+    k_bt_tmat<<<nsub, 128, 0, s>>>(S, tau, c0, nbb, nbb, Tm);
+    for (int q = 1; q < nsub; ++q) {  // T(0:k, q) = −T(0:k, 0:k)·S(0:k, q)·T_qq, k = q·TBT
+      const int k = q * TBT, nq = std::min(TBT, nbb - k);
+      syev_dgemm(k, nq, nq, 1.0, S + static_cast<size_t>(k) * nbb, nbb, false, Tm + k + static_cast<size_t>(k) * nbb, nbb,
+                 0.0, Tt, k, s);
+      syev_dgemm(k, nq, k, -1.0, Tm, nbb, false, Tt, k, 0.0, Tm + static_cast<size_t>(k) * nbb, nbb, s);
+    }
     if (bigbt) {
       if (gemm(nbb, m, rows, Vb + r0, m, true, Yt + r0, m, Wt, nbb) != 0) {  // Wt = VbᵀY
         if (err) *err = "dense eigensolver: back-transformation product failed";
