@@ -49,6 +49,27 @@ __device__ __forceinline__ double block_sum256(double v, double* sh) {
   return v;
 }
 
+// Four sums at once (fixed order; every thread receives the results): two block barriers instead of eight.
+__device__ __forceinline__ void block_sum4(double (&v)[4], double* sh /* ≥ 4·(TT/32) + 4 */) {
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+    for (int o = 16; o; o >>= 1) v[k] += __shfl_xor_sync(0xffffffffu, v[k], o);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0)
+#pragma unroll
+    for (int k = 0; k < 4; ++k) sh[4 * w + k] = v[k];
+  __syncthreads();
+  if (threadIdx.x < 4) {
+    double a = 0.0;
+    for (int ww = 0; ww < TT / 32; ++ww) a += sh[4 * ww + threadIdx.x];
+    sh[4 * (TT / 32) + threadIdx.x] = a;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < 4; ++k) v[k] = sh[4 * (TT / 32) + k];
+  __syncthreads();
+}
+
 // linear index t of the active lower tiles (I ≥ J ≥ J0, I < mt) → (I, J), row-major over I
 __device__ __forceinline__ void tile_of(int t, int J0, int& I, int& J) {
   // rows I' = I − J0 hold I' + 1 tiles: t = I'(I'+1)/2 + (J − J0)
@@ -73,7 +94,13 @@ struct PanelArgs {
   double* part;     // G x (5 + 2·NB) scalar partials
   double* yp;       // tile partials: slot(I, J) x 2 x TB
   double* gam;      // NB: γ_j of the panel's columns (W = W' + V·diag(γ); W' is what W holds)
+  unsigned long long* dbg;  // OZR_SYEV_PROBE: accumulated ns per phase (CTA 0), or null
 };
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 
 // Sum of the G per-CTA partials part[g·PS + off] in a fixed order (every CTA gets the same value): thread t sums
 // g ≡ t (mod TT) ascending, then a fixed tree over the threads.
@@ -92,7 +119,7 @@ struct PanelSmem {
   double rowc[2 * NB];      // V(c, 0:i) | W(c, 0:i−1) (corrected)
   double gam[NB];           // γ_j of the finished columns
   double dots[2 * NB];      // Vᵀv | Wᵀv (reduced over the grid)
-  double sh[TT / 32];
+  double sh[4 * (TT / 32) + 4];
 };
 
 // Two grid-wide barriers per column. W(:, i)'s last correction γ_i·V(:, i) (γ_i = −½τ_i·w'ᵀv, a grid reduction)
@@ -114,7 +141,7 @@ __device__ __forceinline__ void trd_tile_load(const double* __restrict__ A, int 
   }
 }
 
-__global__ void __launch_bounds__(TT) k_trd_panel(PanelArgs P) {
+__global__ void __launch_bounds__(TT, 2) k_trd_panel(PanelArgs P) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(16) unsigned char smraw[];
   PanelSmem& S = *reinterpret_cast<PanelSmem*>(smraw);
@@ -126,6 +153,13 @@ __global__ void __launch_bounds__(TT) k_trd_panel(PanelArgs P) {
   const int r0own = b * TB;
   const bool owner = b < mt;
   double tau_prev = 0.0;
+  unsigned long long tlast = gtimer();
+#define PROBE(k)                                          \
+  if (P.dbg && b == 0 && tid == 0) {                      \
+    const unsigned long long tn_ = gtimer();              \
+    P.dbg[k] += tn_ - tlast;                              \
+    tlast = tn_;                                          \
+  }
   for (int i = 0; i < P.nb; ++i) {
     const int c = P.k0 + i;
     // ---- phase A: x''_r = A(r,c) − Σ_{j<i−1} [V(r,j)W(c,j) + W(r,j)V(c,j)] − W'(r,i−1)V(c,i−1), own rows r ≥ c
@@ -157,26 +191,40 @@ __global__ void __launch_bounds__(TT) k_trd_panel(PanelArgs P) {
         }
       }
     }
-    ss = block_sum256(ss, S.sh);
-    sxb = block_sum256(sxb, S.sh);
-    sbb = block_sum256(sbb, S.sh);
-    if (tid == 0) {
-      P.part[static_cast<long long>(b) * PS] = ss;
-      P.part[static_cast<long long>(b) * PS + 1] = sxb;
-      P.part[static_cast<long long>(b) * PS + 2] = sbb;
+    {
+      double v4[4] = {ss, sxb, sbb, 0.0};
+      block_sum4(v4, S.sh);
+      if (tid < 3) P.part[static_cast<long long>(b) * PS + tid] = v4[tid];
     }
+    PROBE(6);
     grid.sync();
+    PROBE(0);
     // ---- phase B: γ_{i−1}, the reflector (every CTA, the same fixed-order sums), V(:, i), the tile products, Vᵀv, Wᵀv
+    // every global value phase B needs, loaded at once (independent of the reductions below)
+    const double w_ci = (i > 0) ? __ldcg(P.W + c + static_cast<long long>(i - 1) * m) : 0.0;
+    const double a_cc = __ldcg(A + c + static_cast<long long>(c) * m);
+    const double a_c1 = (c + 1 < m) ? __ldcg(A + c + 1 + static_cast<long long>(c) * m) : 0.0;
+    const double v_c1 = (i > 0 && c + 1 < m) ? __ldcg(P.V + c + 1 + static_cast<long long>(i - 1) * m) : 0.0;
+    const int rown = r0own + (tid & (TB - 1));
+    const bool ownrow = owner && tid < TB && rown < m;
+    const double a_rc = ownrow ? __ldcg(A + rown + static_cast<long long>(c) * m) : 0.0;
     double kap = 0.0;
+    double sums[4] = {0.0, 0.0, 0.0, 0.0};  // Σ_g of slots 0..3, fixed order (g ≡ tid mod TT, then the block tree)
+    for (int g = tid; g < G; g += TT) {
+      const double* pg = P.part + static_cast<long long>(g) * PS;
+      sums[0] += pg[0];
+      sums[1] += pg[1];
+      sums[2] += pg[2];
+      sums[3] += pg[3];
+    }
+    block_sum4(sums, S.sh);
     if (i > 0) {
-      const double gam = -0.5 * tau_prev * grid_partial_sum(P.part, PS, 3, G, S.sh);
-      kap = fma(2.0 * gam, S.rowc[i - 1], P.W[c + static_cast<long long>(i - 1) * m]);
+      const double gam = -0.5 * tau_prev * sums[3];
+      kap = fma(2.0 * gam, S.rowc[i - 1], w_ci);
       if (tid == 0) S.gam[i - 1] = gam;
       if (tid < TB) S.ws[i - 1][tid] = fma(gam, S.vs[i - 1][tid], S.ws[i - 1][tid]);  // private rows
     }
-    const double sig0 = grid_partial_sum(P.part, PS, 0, G, S.sh);
-    const double sig1 = grid_partial_sum(P.part, PS, 1, G, S.sh);
-    const double sig2 = grid_partial_sum(P.part, PS, 2, G, S.sh);
+    const double sig0 = sums[0], sig1 = sums[1], sig2 = sums[2];
     double sigma = sig0 - 2.0 * kap * sig1 + kap * kap * sig2;
     // the expansion's rounding error (≈ u·(Σx''² + κ²Σb²)) enters the reflector's orthogonality as δσ/σ (τ·vᵀv =
     // 2 + δσ/(β(β − α))), so it is trusted only without cancellation; otherwise Σ x_r² exactly, one more barrier
@@ -199,10 +247,10 @@ __global__ void __launch_bounds__(TT) k_trd_panel(PanelArgs P) {
       const double x = A[r + static_cast<long long>(c) * m];
       return (i > 0) ? fma(-kap, P.V[r + static_cast<long long>(i - 1) * m], x) : x;
     };
-    const double ccdiag = xfin(c);
+    const double ccdiag = (i > 0) ? fma(-kap, S.rowc[i - 1], a_cc) : a_cc;  // V(c, i−1) = rowc[i−1]
     double alpha = 0.0, beta = 0.0, tau = 0.0, scale = 0.0;
     if (c + 1 < m) {
-      alpha = xfin(c + 1);
+      alpha = (i > 0) ? fma(-kap, v_c1, a_c1) : a_c1;
       if (sigma == 0.0) {
         beta = alpha;  // H = I
       } else {
@@ -222,11 +270,14 @@ __global__ void __launch_bounds__(TT) k_trd_panel(PanelArgs P) {
     auto vof = [&](int r) -> double { return r == c + 1 ? 1.0 : (r > c + 1 ? xfin(r) * scale : 0.0); };
     if (owner && tid < TB) {
       const int r = r0own + tid;
-      const double v = (r < m) ? vof(r) : 0.0;
+      // v_r from the hoisted x''_r (own row; V(r, i−1) is the CTA's own shared copy)
+      const double xr = (i > 0) ? fma(-kap, S.vs[i - 1][tid], a_rc) : a_rc;
+      const double v = (r >= m) ? 0.0 : (r == c + 1 ? 1.0 : (r > c + 1 ? xr * scale : 0.0));
       S.vloc[tid] = v;
       S.vs[i][tid] = v;
       if (r < m && r >= c + 1) P.V[r + static_cast<long long>(i) * m] = v;
     }
+    PROBE(1);
     if (tau != 0.0) {
       const int J0 = (c + 1) / TB;
       const int na = mt - J0;
@@ -277,6 +328,7 @@ __global__ void __launch_bounds__(TT) k_trd_panel(PanelArgs P) {
         I = In;
         J = Jn;
       }
+      PROBE(2);
       // Vᵀv and Wᵀv over own rows: 2i dot products of length TB from shared memory, 4 threads each
       __syncthreads();
       if (owner && i > 0) {
@@ -297,15 +349,24 @@ __global__ void __launch_bounds__(TT) k_trd_panel(PanelArgs P) {
         if (j < i) P.part[static_cast<long long>(b) * PS + 5 + tid] = 0.0;
       }
     }
+    PROBE(3);
     grid.sync();
     // ---- phase C: y_r from the tile partials, w'_r = τ(y − V(Wᵀv) − W(Vᵀv)), partial of w'ᵀv (its γ: next column)
     double p3 = 0.0;
+    PROBE(4);
     if (tau != 0.0) {
       if (i > 0) {  // Vᵀv, Wᵀv reduced over the grid: 4 threads per value, fixed order
         const int q = tid >> 2, part = tid & 3;
         double acc = 0.0;
-        if (q < 2 * NB && (q < NB ? q : q - NB) < i)
-          for (int g = part; g < G; g += 4) acc += P.part[static_cast<long long>(g) * PS + 5 + q];
+        if (q < 2 * NB && (q < NB ? q : q - NB) < i) {
+          double a8[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // independent partial sums: the loads stay in flight
+          int g = part;
+          for (; g + 28 < G; g += 32)
+#pragma unroll
+            for (int u = 0; u < 8; ++u) a8[u] += __ldcg(P.part + static_cast<long long>(g + 4 * u) * PS + 5 + q);
+          for (; g < G; g += 4) a8[0] += __ldcg(P.part + static_cast<long long>(g) * PS + 5 + q);
+          acc = ((a8[0] + a8[1]) + (a8[2] + a8[3])) + ((a8[4] + a8[5]) + (a8[6] + a8[7]));
+        }
         acc += __shfl_xor_sync(0xffffffffu, acc, 1);
         acc += __shfl_xor_sync(0xffffffffu, acc, 2);
         if (part == 0 && q < 2 * NB) S.dots[q] = acc;
@@ -346,6 +407,7 @@ __global__ void __launch_bounds__(TT) k_trd_panel(PanelArgs P) {
     p3 = block_sum256(p3, S.sh);
     if (tid == 0) P.part[static_cast<long long>(b) * PS + 3] = p3;
     tau_prev = tau;
+    PROBE(5);
   }
   // the last column's γ (one more barrier for its w'ᵀv); the γ_j go to the trailing update
   const int ilast = P.nb - 1, clast = P.k0 + ilast;
@@ -856,12 +918,17 @@ int syev_trd_grid(int m) {
 // Tridiagonalise A (m x m, lda = m, lower triangle read; overwritten: reflectors below the sub-diagonal).
 cudaError_t syev_tridiag(double* A, int m, double* d, double* e, double* tau, double* V, double* W, double* part,
                          int G, cudaStream_t s) {
+  unsigned long long* dbg = nullptr;
+  if (getenv("OZR_SYEV_PROBE")) {
+    cudaMalloc(&dbg, 8 * sizeof(unsigned long long));
+    cudaMemsetAsync(dbg, 0, 8 * sizeof(unsigned long long), s);
+  }
   const int mt = (m + TB - 1) / TB;
   if (G < mt) return cudaErrorInvalidConfiguration;  // every row block needs its owner CTA (m ≤ ~28000)
   double* yp = part + static_cast<size_t>(G) * (5 + 2 * NB);
   for (int k0 = 0; k0 < m; k0 += NB) {
     const int nb = std::min(NB, m - k0);
-    PanelArgs P{A, m, k0, nb, V, W, d, e, tau, part, yp, part + syev_trd_partials(m, G)};
+    PanelArgs P{A, m, k0, nb, V, W, d, e, tau, part, yp, part + syev_trd_partials(m, G), dbg};
     void* args[] = {&P};
     cudaError_t err = cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_trd_panel), dim3(G), dim3(TT), args,
                                                   sizeof(PanelSmem), s);
@@ -873,6 +940,14 @@ cudaError_t syev_tridiag(double* A, int m, double* d, double* e, double* tau, do
     } else {
       k_trd_update<<<nb, TT, 0, s>>>(A, m, k0, nb, V, W, P.gam);  // only the reflector copy (na = 0 tiles)
     }
+  }
+  if (dbg) {
+    unsigned long long h[8];
+    cudaMemcpyAsync(h, dbg, sizeof h, cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    fprintf(stderr, "[ozr syev probe] m=%d G=%d ms: A %.2f sync1 %.2f B-head %.2f tiles %.2f dots %.2f sync2 %.2f C %.2f\n", m, G,
+            h[6] * 1e-6, h[0] * 1e-6, h[1] * 1e-6, h[2] * 1e-6, h[3] * 1e-6, h[4] * 1e-6, h[5] * 1e-6);
+    cudaFree(dbg);
   }
   return cudaGetLastError();
 }
