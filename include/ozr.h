@@ -143,6 +143,11 @@ typedef struct {
                         then runs max_sweeps sweeps (the paper's fixed iteration count) and
                         returns OZR_ERR_NOT_CONVERGED with X, λ from the last sweep; 1 after every sweep of
                         ozr_refine_to_tol without unresolved groups [default]; 2 also in ozr_refine_step  */
+  int fixed_k;       /* > 0: the prior work's two-sided fixed-slice plan instead of the proposed method
+                        (PAPER.md:217-227 eq. mat3-mat10, cost model PAPER.md:437-443): X̂ is not truncated
+                        and every product keeps the ½k(k+1) leading digit pairs s + t ≤ k + 1 (truncate = 0,
+                        L_V = L_W = L_U = k + 1; the products of ozr_gemm(kA = kB = k, L = k + 1)).
+                        Default 0 (the proposed method)                                              */
 } ozr_params;
 
 void ozr_params_default(ozr_params* p);

@@ -74,3 +74,18 @@ def digit_product(DA, ellA, KA, DB, ellB, KB, L):
     e = np.asarray(ellA)[:, None] + np.asarray(ellB)[None, :] + 8 * (KA + KB - L)
     hi, lo = to_dd(T, e)
     return hi, lo, planes, groups
+
+
+def accmul_fixed_k(A, B, k):
+    """The prior work's two-sided accurate product with a FIXED number of slices (eq. mat3 -
+    mat10; cost model PAPER.md:437-443: n_A = n_X = k slices and the ½k(k+1) slice products A^(s)X^(t) with
+    s + t ≤ k + 1), in the build's INT8 digit reading (R5-R7): A split row-wise and B column-wise into k digits
+    (fixed point per line, RNE), the pairs s + t ≤ k + 1 summed exactly, rounded once to double-double.
+    Returns (hi, lo, npairs)."""
+    from .split import split_digits_cols
+    A = np.asarray(A, dtype=np.float64)
+    B = np.asarray(B, dtype=np.float64)
+    DA, eA = split_digits_cols(A.T, k)  # rows of A = columns of Aᵀ (contraction index first)
+    DB, eB = split_digits_cols(B, k)
+    hi, lo, _, groups = digit_product(DA, eA, k, DB, eB, k, k + 1)
+    return hi, lo, sum(len(p) for _, p in groups)

@@ -37,7 +37,8 @@ class Params(ctypes.Structure):
                 ("L_W", ctypes.c_int), ("L_U", ctypes.c_int), ("cluster_mode", ctypes.c_int),
                 ("tile_budgets", ctypes.c_int), ("kappa", ctypes.c_double), ("max_cluster", ctypes.c_int),
                 ("form_R", ctypes.c_int), ("dense_cluster", ctypes.c_int),
-                ("row_nnz", ctypes.c_int), ("max_escalations", ctypes.c_int), ("certify", ctypes.c_int)]
+                ("row_nnz", ctypes.c_int), ("max_escalations", ctypes.c_int), ("certify", ctypes.c_int),
+                ("fixed_k", ctypes.c_int)]
 
 
 class StepReport(ctypes.Structure):

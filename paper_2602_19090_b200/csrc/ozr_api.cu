@@ -1683,6 +1683,7 @@ void ozr_params_default(ozr_params* p) {
   p->dense_cluster = 192;  // = the cooperative-Jacobi threshold: measured 12x faster at m = 739 (c2)
   p->max_escalations = 2;
   p->certify = 1;
+  p->fixed_k = 0;
 }
 
 ozr_status ozr_split(ozr_ctx ctx, const double* M, const double* M_lo, int64_t rows, int64_t cols, int64_t ldm,
@@ -1941,6 +1942,16 @@ int ozr_comm_size(ozr_comm comm) { return comm ? comm->ex->P : 1; }
 int ozr_comm_rank(ozr_comm comm) { return comm ? comm->ex->rank : 0; }
 
 namespace {
+// params.fixed_k: the prior work's fixed-slice plan as a digit plan
+ozr_params effective_params(const ozr_params& in) {
+  ozr_params P = in;
+  if (P.fixed_k > 0) {
+    P.truncate = 0;
+    P.L_V = P.L_W = P.L_U = P.fixed_k + 1;
+  }
+  return P;
+}
+
 ozr_status check_refine_args(ozr_ctx ctx, ozr_comm comm, const double* A, int64_t n, int64_t lda, const double* X,
                              int64_t ldx, const double* lambda, const ozr_params* params) {
   ozr_status st = check_ctx(ctx);
@@ -1962,7 +1973,8 @@ ozr_status ozr_refine_step_dist(ozr_ctx ctx, ozr_comm comm, const double* A, int
   if (st != OZR_OK) return st;
   SweepState ss;
   ozr_step_report rep;
-  st = sweep(ctx, comm ? comm->ex.get() : nullptr, A, n, lda, X, ldx, lambda, *params, rep, ss);
+  const ozr_params P = effective_params(*params);
+  st = sweep(ctx, comm ? comm->ex.get() : nullptr, A, n, lda, X, ldx, lambda, P, rep, ss);
   rep.sweep = 1;
   rep.theta = params->theta;
   rep.cert = -1.0;
@@ -1990,7 +2002,7 @@ ozr_status ozr_refine_to_tol_dist(ozr_ctx ctx, ozr_comm comm, const double* A, i
   ozr_status result = OZR_ERR_NOT_CONVERGED;
   ctx->err.clear();
   const int maxs = params->max_sweeps > 0 ? params->max_sweeps : 6;
-  ozr_params P = *params;
+  ozr_params P = effective_params(*params);
   int escalations = 0;
   Exchange* ex = comm ? comm->ex.get() : nullptr;
   const double delta = params->delta;

@@ -331,3 +331,38 @@ def test_second_order_defect_vs_exact_correction(m):
     fe = float(np.linalg.norm(Xn - X, 2))
     c = orf.certificate(Et, ln)
     assert abs(c["est_q"] - fe) <= 0.03 * fe + 4 * 2.0 ** -53, (c, fe)
+
+
+def test_accmul_fixed_k_vs_rationals():
+    """§8(f) rank 1: the prior work's ½k(k+1)-product scheme pinned against exact
+    rationals: (a) ½k(k+1) pairs; (b) hi + lo is the correctly rounded exact sum of the kept digit-pair
+    products (Fractions from the digit values); (c) the error against the exact AB falls by ≥ 2^7 per extra
+    slice and is within the bound Σ_i |a_i| |b_j| (2^{1−S_k}) + the dropped-pair tail."""
+    from fractions import Fraction
+    from oracle import split as osp
+    rng = np.random.default_rng(4)
+    A = rng.standard_normal((5, 7)) * np.exp(rng.uniform(-20, 20, (5, 1)))
+    B = rng.standard_normal((7, 4))
+    exact = [[sum(Fraction(A[i, l]) * Fraction(B[l, j]) for l in range(7)) for j in range(4)] for i in range(5)]
+    errs = []
+    for k in (2, 3, 4, 5):
+        hi, lo, npairs = opr.accmul_fixed_k(A, B, k)
+        assert npairs == k * (k + 1) // 2
+        DA, eA = osp.split_digits_cols(A.T, k)
+        DB, eB = osp.split_digits_cols(B, k)
+        for i in range(5):
+            for j in range(4):
+                s = Fraction(0)
+                for a in range(1, k + 1):
+                    for b in range(1, k + 2 - a):
+                        da = sum(int(DA[a - 1, l, i]) * int(DB[b - 1, l, j]) for l in range(7))
+                        s += Fraction(da) * Fraction(2) ** int(eA[i] + eB[j] + 8 * (k - a) + 8 * (k - b))
+                h = float(s)
+                assert hi[i, j] == h and lo[i, j] == float(s - Fraction(h))
+        e = max(abs(Fraction(hi[i, j]) + Fraction(lo[i, j]) - exact[i][j]) / (sum(abs(Fraction(A[i, l]) * Fraction(B[l, j]))
+                                                                                  for l in range(7)))
+                for i in range(5) for j in range(4))
+        errs.append(float(e))
+        assert e <= 2.0 ** (-(8 * (k - 1) + 6) + 2) * (k + 2)  # both splits' rounding + the dropped diagonal
+    for a, b in zip(errs, errs[1:]):
+        assert b <= a / 2 ** 7
