@@ -146,7 +146,8 @@ typedef struct {
   int fixed_k;       /* > 0: the prior work's two-sided fixed-slice plan instead of the proposed method
                         (PAPER.md:217-227 eq. mat3-mat10, cost model PAPER.md:437-443): X̂ is not truncated
                         and every product keeps the ½k(k+1) leading digit pairs s + t ≤ k + 1 (truncate = 0,
-                        L_V = L_W = L_U = k + 1; the products of ozr_gemm(kA = kB = k, L = k + 1)).
+                        L_V = L_W = L_U = k + 1, Res and Ẽ' split into exactly k digits; the products of
+                        ozr_gemm(kA = kB = k, L = k + 1)).
                         Default 0 (the proposed method)                                              */
 } ozr_params;
 

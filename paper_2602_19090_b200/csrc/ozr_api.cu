@@ -997,7 +997,9 @@ ozr_status sweep(ozr_ctx ctx, Exchange* ex, const double* A, int64_t n, int64_t 
   // ---- a6: Res digits (k_R from the accuracy W needs, R8)
   const double gapW = std::min(gap, gap_new);
   const double tauW = P.theta_W * delta_p * gapW;
-  const int kR = digits_for(eRmax, static_cast<int>(std::floor(std::log2(tauW / 2.0))));
+  // the fixed-slice plan (params.fixed_k) splits every operand into exactly k slices
+  const int kR = P.fixed_k > 0 ? std::min(P.fixed_k, kMaxDigits)
+                               : digits_for(eRmax, static_cast<int>(std::floor(std::log2(tauW / 2.0))));
   int8_t* rdig = ctx->ws<int8_t>(S_RDIG, static_cast<size_t>(kMaxDigits) * ld * nl);
   int32_t* rell = ctx->ws<int32_t>(S_RELL, nl);
   OZR_ALLOC(rdig); OZR_ALLOC(rell);
@@ -1308,7 +1310,8 @@ ozr_status sweep(ozr_ctx ctx, Exchange* ex, const double* A, int64_t n, int64_t 
 
   // ---- a9: P4  U_J = X̂^(1) Ẽ_{:,J} = Q Ẽ'_{:,J} ; X̂_J ← RN(X̂^(1)_J + U_J)  (Alg. 1 line 6)
   const double tauU = P.theta_U * delta_p;
-  const int kE = digits_for(eEmax, static_cast<int>(std::floor(std::log2(tauU / 2.0))) + gmin);
+  const int kE = P.fixed_k > 0 ? std::min(P.fixed_k, kMaxDigits)
+                               : digits_for(eEmax, static_cast<int>(std::floor(std::log2(tauU / 2.0))) + gmin);
   ctx->mark("~");
   launch_split_fixed(Ep, nullptr, n, N, NL, kE, rdig, ld, ld * nl, rell, derr, s);
   OZR_CK(cudaGetLastError(), "split E");

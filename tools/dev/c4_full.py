@@ -32,6 +32,6 @@ orth = (X.T @ X - torch.eye(n, dtype=torch.float64, device=dev)).abs().max()
 out = {"config": name, "n": n, "delta": cfg["delta"], "status": int(st), "error": ozr.lib().ozr_last_error(ctx.h).decode() if st else "",
        "wall_s": wall, "sweeps": [{k: h[k] for k in ("theta", "beta", "kA", "kR", "kE", "pairs_V", "pairs_W", "pairs_U",
                                                     "n_clusters", "max_cluster", "net_update", "predicted_error",
-                                                    "normE_fro", "update_2norm", "ms_total", "ms_gemm")} for h in hist],
+                                                    "normE_fro", "cert", "ms_total", "ms_gemm")} for h in hist],
        "max_residual": float(res.max()), "orth_max": float(orth)}
 print(json.dumps(out))
