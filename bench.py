@@ -354,6 +354,8 @@ def main():
     ap.add_argument("--dry-run", action="store_true",
                     help="rank plumbing only (gloo, no GPU): the partition every rank computes")
     ap.add_argument("--no-c5", action="store_true", help="skip the c5 (n = 16384) strong-scaling line")
+    ap.add_argument("--headline-only", action="store_true",
+                    help="only the headline sweeps and e2e (no c4, c5, per-product or fixed-k extras): profiling runs")
     args = ap.parse_args()
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         return _relaunch_under_torchrun(args.gpus)
@@ -503,7 +505,7 @@ def main():
     # §8(f) rank 1: the prior work's two-sided fixed-slice plan (ozr_params.fixed_k)
     # against the proposed method on the same problem: device time to the stop rule, sweeps, pair-GEMMs
     fixed_k_cmp = None
-    if not dist_mode and name == "c4p" and not args.n and args.truncate:
+    if not dist_mode and name == "c4p" and not args.n and args.truncate and not args.headline_only:
         fixed_k_cmp = {"note": "ozr_refine_to_tol from X0 on the same problem; pair_gemms = INT8 n x n x n slice "
                                "products summed over the sweeps (PAPER.md:541 claims 4/3-2x fewer products)",
                        "proposed": {"ms": ttt["ms"], "sweeps": ttt["sweeps"], "status": ttt["status"],
@@ -522,7 +524,7 @@ def main():
     # BASELINE c4 (the n = 8192 configuration as BASELINE.json states it: cnd 1e14, FP32-eigensolver start,
     # gate 1e-10): its time to target beside the headline c4' (1 GPU only; the group sub-solve is replicated)
     ttt_c4 = None
-    if not dist_mode and not args.no_c4 and name == "c4p" and not args.n:
+    if not dist_mode and not args.no_c4 and not args.headline_only and name == "c4p" and not args.n:
         A4, l4, X4, cfg4 = W.make_config_torch("c4", dev)
         p4 = ozr.default_params(delta=cfg4["delta"], max_sweeps=12)
         for _ in range(2):  # the first run grows the context's workspace (group buffers); the second is timed
@@ -541,13 +543,13 @@ def main():
     # the per-product Ozaki GEMM: ozr_gemm C = A·X̂₀ through the C ABI, split of both operands,
     # slice GEMM and exact recombination to double-double all inside the timed region (A's split included)
     per_product = None
-    if rank == 0 and not dist_mode:
+    if rank == 0 and not dist_mode and not args.headline_only:
         per_product = run_per_product(ctx, A, X0, reps[-1], ozr, torch)
 
     # c5 (n = 16384, cnd 1e10, FP64 start, δ = 1e-15): the north star's scaling configuration, the same
     # block-column partition over the ranks (strong scaling), device time max over ranks
     c5 = None
-    if not args.no_c5 and name == "c4p" and not args.n:
+    if not args.no_c5 and not args.headline_only and name == "c4p" and not args.n:
         c5 = run_c5(ctx, comm, dist_mode, ws, rank, dev, W, ozr, torch, dist)
 
     # e2e: a stream of independent problems through the public API with HOST (pinned) buffers. Every step
@@ -631,7 +633,8 @@ def main():
                "vs_baseline": None, "dtype": "int8", "data": "synthetic",
                "config": _config(name, cfg, n, ws, dist_mode, args.truncate),
                "sweep": {k: r0[k] for k in ("beta", "alpha", "kX", "kA", "kR", "kE", "L_V", "L_W", "L_U",
-                                            "pairs_V", "pairs_W", "pairs_U", "n_clusters", "max_cluster")},
+                                            "pairs_V", "pairs_W", "pairs_U", "planes_V", "planes_W", "planes_U", "n_clusters",
+                                            "max_cluster")},
                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                "gpu_launches": int(sum(r["launches"] for r in reps)), "clocks": clocks,
                "time_to_target": ttt, "time_to_target_c4": ttt_c4, "c5_strong_scaling": c5,

@@ -174,13 +174,17 @@ typedef struct {
   double omega_oa;                  /* form_R: ω = 2(‖W‖_F + 2·max|λ̂|·‖R‖_F), the Frobenius form of the
                                        OA-2018 cluster threshold 2(‖S − D̃‖ + ‖A‖‖R‖) (diagnostic, R13) */
   double theta;                     /* the θ this sweep used (params.theta, × 16 per escalation)       */
-  double cert;                      /* a-posteriori estimate of ‖X − X̂_new‖₂ (R12): sqrt(‖Q∘H‖₂² + (2u)²)
-                                       + 1.5‖Ẽ‖_F², Q = ẼᵀC, c_kj = (λ̂_k − λ̂_j)ẽ_kj, H_ij = 1/(λ̂_j − λ̂_i);
-                                       −1 when not evaluated (params.certify, or unresolved groups)      */
-  double cert_q;                    /* its second-order part ‖Q∘H‖₂ (power iteration; the Frobenius norm
-                                       when that already decides)                                        */
-  double cert_frob;                 /* ‖Q∘H‖_F                                                          */
-  int cert_iters;                   /* power iterations of the certificate                              */
+  double cert;                      /* a-posteriori estimate of ‖X − X̂_new‖₂ (R12): sqrt(‖D‖₂² + (2u)²)
+                                       + ‖Ẽ‖_F‖D‖_F with Ẽ's second-order defect D = −(E − Ẽ):
+                                       D_ij = q_ij/(λ̂_j − λ̂_i) − (Ẽ²)_ij (i ≠ j), D_jj = −(Ẽ²)_jj − ½‖ẽ_j‖²,
+                                       Q = ẼᵀC, c_kj = (λ̂_k − λ̂_j)ẽ_kj; −1 when not evaluated
+                                       (params.certify, or unresolved groups)                           */
+  double cert_q;                    /* its ‖D‖₂ (Golub–Kahan–Lanczos; ‖D‖_F when that already decides)   */
+  double cert_frob;                 /* ‖D‖_F                                                            */
+  int cert_iters;                   /* Lanczos steps of the certificate                                 */
+  double planes_V, planes_W, planes_U; /* int32 group planes recombined per element, averaged over the
+                                          columns (per-tile budgets): 4 × this = the plane bytes per element
+                                          the recombination kernels read                                   */
 } ozr_step_report;
 
 /* One sweep on columns [0, n): A (n x n, symmetric — only its columns are read), X (n x n, in/out:
@@ -189,6 +193,22 @@ typedef struct {
  * Errors: OZR_ERR_ARG, OZR_ERR_RANGE (δ ≤ u), OZR_ERR_DEGENERATE, OZR_ERR_CUDA, OZR_ERR_NOMEM. */
 ozr_status ozr_refine_step(ozr_ctx ctx, const double* A, int64_t n, int64_t lda, double* X, int64_t ldx,
                            double* lambda, const ozr_params* params, ozr_step_report* report);
+
+/* ozr_refine_step_herm — the Hermitian extension ("the proposed method can be extended in a
+ * straightforward manner to Hermitian matrices"; reading R18): one sweep of Algorithm 1
+ * with conjugate transposes — V = A·X̂^(1), r_j = 1 − x̂_jᴴx̂_j, λ̂_j = Re(x̂_jᴴv_j)/(1 − r_j),
+ * W = X̂ᴴ(V − X̂D̂), ẽ_ij = w_ij/(λ̂_j − λ̂_i), ẽ_jj = r_j/2, X̂ ← RN(X̂^(1) + X̂^(1)Ẽ) — with the truncation
+ * X̂ → X̂^(1) of §3.1 on both parts (one τ_j per column from max_i max(|Re x̂_ij|, |Im x̂_ij|)) and β of §4.1.
+ * Planar complex storage, column-major, device pointers: A = Ar + i·Ai (n x n, Hermitian: Ar symmetric, Ai
+ * antisymmetric; lda ≥ n), X = Xr + i·Xi (n x n, in/out, ldx ≥ n), lambda (n, in: previous estimates, out: the
+ * new Rayleigh quotients). Each complex product is one real INT8 slice product of the real-stacked operands
+ * (2n-long contractions), budgets from the accuracy each product needs (R8, per product); params: delta, theta,
+ * theta_V/W/U, beta_mode/xi, beta_override, L_V/L_W/L_U (cluster_mode, certify, fixed_k and tile budgets do
+ * not apply: equal estimates are OZR_ERR_DEGENERATE). report: host, nullable (cert = −1).
+ * Errors: OZR_ERR_ARG, OZR_ERR_RANGE, OZR_ERR_DEGENERATE, OZR_ERR_NONFINITE, OZR_ERR_CUDA, OZR_ERR_NOMEM. */
+ozr_status ozr_refine_step_herm(ozr_ctx ctx, const double* Ar, const double* Ai, int64_t n, int64_t lda, double* Xr,
+                                double* Xi, int64_t ldx, double* lambda, const ozr_params* params,
+                                ozr_step_report* report);
 
 /* The R = I − X̂^(1)ᵀX̂^(1) of the context's last sweep run with params.form_R = 1: this rank's columns
  * (n x n_local, column-major) copied to R (device, ldr ≥ n). OZR_ERR_ARG if none was formed. */

@@ -20,7 +20,7 @@ STATUS = {0: "OZR_OK", 1: "OZR_ERR_ARG", 2: "OZR_ERR_NONFINITE", 3: "OZR_ERR_RAN
 EXPORTS = ["ozr_version", "ozr_create", "ozr_destroy", "ozr_last_error", "ozr_split", "ozr_gemm", "ozr_gemm_plan",
            "ozr_params_default", "ozr_refine_step", "ozr_refine_to_tol", "ozr_last_clusters", "ozr_syev", "ozr_syev_tridiag", "ozr_syev_tridiag_eig", "ozr_comm_nccl_id",
            "ozr_comm_create_nccl", "ozr_comm_create_host_group", "ozr_comm_destroy", "ozr_comm_size", "ozr_comm_rank",
-           "ozr_refine_step_dist", "ozr_refine_to_tol_dist", "ozr_last_R"]
+           "ozr_refine_step_dist", "ozr_refine_to_tol_dist", "ozr_last_R", "ozr_refine_step_herm"]
 
 
 class OzrError(RuntimeError):
@@ -49,7 +49,8 @@ class StepReport(ctypes.Structure):
                                                  "predicted_error", "ms_total", "ms_gemm", "int8_ops"]] +
                 [("pairs_G", ctypes.c_int)] +
                 [(f, ctypes.c_double) for f in ["normR_fro", "normW_fro", "omega_oa", "theta", "cert", "cert_q", "cert_frob"]] +
-                [("cert_iters", ctypes.c_int)])
+                [("cert_iters", ctypes.c_int)] +
+                [(f, ctypes.c_double) for f in ["planes_V", "planes_W", "planes_U"]])
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
@@ -85,6 +86,9 @@ def lib():
         L.ozr_refine_step.argtypes = [vp, vp, i64, i64, vp, i64, vp, ctypes.POINTER(Params),
                                       ctypes.POINTER(StepReport)]
         L.ozr_refine_step.restype = i32
+        L.ozr_refine_step_herm.argtypes = [vp, vp, vp, i64, i64, vp, vp, i64, vp, ctypes.POINTER(Params),
+                                           ctypes.POINTER(StepReport)]
+        L.ozr_refine_step_herm.restype = i32
         L.ozr_refine_to_tol.argtypes = [vp, vp, i64, i64, vp, i64, vp, ctypes.POINTER(Params),
                                         ctypes.POINTER(StepReport), i32, ip]
         L.ozr_refine_to_tol.restype = i32
@@ -231,6 +235,18 @@ def ozr_refine_step(ctx, A, X, lam, params):
     rep = StepReport()
     ctx.check(lib().ozr_refine_step(ctx.h, _ptr(A), n, _ld(A), _ptr(X), _ld(X), _ptr(lam), ctypes.byref(params),
                                     ctypes.byref(rep)))
+    return rep.as_dict()
+
+
+def ozr_refine_step_herm(ctx, Ar, Ai, Xr, Xi, lam, params):
+    """One Hermitian sweep in place on Xr, Xi (column-major n x n, real and imaginary parts) and
+    lam (n). Ar, Ai: the Hermitian A's parts (column-major). Returns the report dict."""
+    n = Ar.shape[0]
+    if _ld(Ai) != _ld(Ar) or _ld(Xi) != _ld(Xr):
+        raise ValueError("the real and imaginary parts must share a leading dimension")
+    rep = StepReport()
+    ctx.check(lib().ozr_refine_step_herm(ctx.h, _ptr(Ar), _ptr(Ai), n, _ld(Ar), _ptr(Xr), _ptr(Xi), _ld(Xr),
+                                         _ptr(lam), ctypes.byref(params), ctypes.byref(rep)))
     return rep.as_dict()
 
 

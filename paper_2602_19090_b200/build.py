@@ -6,7 +6,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 SO = os.path.join(HERE, "libozr.so")
-SOURCES = ["ozr_api.cu", "kernels.cu", "gemm_i8.cu", "cluster.cu", "dense_eig.cu", "comm.cu", "certify.cu", "syev.cu"]
+SOURCES = ["ozr_api.cu", "kernels.cu", "gemm_i8.cu", "cluster.cu", "dense_eig.cu", "comm.cu", "certify.cu", "syev.cu", "herm.cu"]
 HEADERS = ["ptx.cuh", "ddmath.cuh", "kernels.h", "ozr_internal.h", "comm.h", "certify.h", "syev.h"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",

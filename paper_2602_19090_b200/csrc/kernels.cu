@@ -16,6 +16,7 @@
 //   k_recombine_dd    generic recombination for ozr_gemm
 #include <algorithm>
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 #include <cuda_runtime.h>
 
@@ -472,6 +473,93 @@ __global__ void __launch_bounds__(BS)
   }
 }
 
+// k_x1_split with 16 rows in flight per thread (four groups of four consecutive rows, 128-bit loads and
+// stores) for 16-byte aligned columns (X, X1 16-byte aligned, ldx and ldx1 even): the same values, digits,
+// g, s and r as k_x1_split, bit for bit. q = x̂^(1)/2^g is an exact integer with |q| ≤ 2^{53−β}; for β ≥ 3
+// (|q| ≤ 2^50) it is read from the significand of q + 1.5·2^52 instead of a 64-bit float→int conversion.
+// Σq² (exact, < 2^113 overall) accumulates per thread in three int64 parts of q = qh·2^26 + ql
+// (0 ≤ ql < 2^26, |qh| ≤ 2^25): Σqh² (< 2^50 per term), Σqh·ql (< 2^51), Σql² (< 2^52), which stay below
+// 2^63 for ≤ 2^11 rows per thread (rows ≤ 2^19, checked by the launcher).
+constexpr int X1U = 4;  // groups of four rows per thread per iteration
+__global__ void __launch_bounds__(BS)
+    k_x1_split_v(const double* __restrict__ X, long long ldx, int rows, int beta, int kx, const double* __restrict__ w,
+                 double* __restrict__ X1, long long ldx1, int8_t* __restrict__ dig, long long ldd, long long pstride,
+                 int32_t* __restrict__ g_out, double* __restrict__ s_hi, double* __restrict__ s_lo,
+                 double* __restrict__ r_hi, double* __restrict__ r_lo, int* __restrict__ err) {
+  __shared__ i128 shq[BS / 32];
+  const int j = blockIdx.x;
+  const double* col = X + j * ldx;
+  double* x1c = X1 + j * ldx1;
+  const double wj = w[j];
+  const int c = ceil_log2_d(wj);
+  const int g = c + beta - 53;
+  const double tau = (wj == 0.0) ? 0.0 : scalbn(0.75, c + beta);  // eq. (tau)
+  const bool in_range = (-g >= -1022 && -g <= 1023);
+  const double scale = in_range ? pow2i(-g) : 0.0;
+  const bool magic = beta >= 3;
+  long long qa = 0, qb = 0, qc = 0;  // Σqh², Σqh·ql, Σql²
+  for (int i0 = 4 * threadIdx.x; i0 < rows; i0 += 4 * BS * X1U) {
+    double xv[X1U][4];
+#pragma unroll
+    for (int u = 0; u < X1U; ++u) {
+      const int ib = i0 + u * 4 * BS;
+      if (ib + 3 < rows) {
+        const double2 a = __ldg(reinterpret_cast<const double2*>(col + ib));
+        const double2 b = __ldg(reinterpret_cast<const double2*>(col + ib + 2));
+        xv[u][0] = a.x; xv[u][1] = a.y; xv[u][2] = b.x; xv[u][3] = b.y;
+      } else {
+#pragma unroll
+        for (int r = 0; r < 4; ++r) xv[u][r] = (ib + r < rows) ? col[ib + r] : 0.0;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < X1U; ++u) {
+      const int ib = i0 + u * 4 * BS;
+      if (ib >= rows) break;
+      long long q[4];
+      double x1[4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        x1[r] = __dsub_rn(__dadd_rn(tau, xv[u][r]), tau);  // eq. (x), s = 1: fl(fl(τ + x) − τ)
+        const double qd = in_range ? x1[r] * scale : ldexp_fast(x1[r], -g);  // exact integer
+        if (magic) q[r] = __double_as_longlong(__dadd_rn(qd, 6755399441055744.0)) - 0x4338000000000000LL;
+        else q[r] = __double2ll_rn(qd);
+        const long long qh = q[r] >> 26, ql = q[r] & 0x3FFFFFFLL;
+        qa += qh * qh;
+        qb += qh * ql;
+        qc += ql * ql;
+      }
+      if (ib + 3 < rows) {
+        *reinterpret_cast<double2*>(x1c + ib) = make_double2(x1[0], x1[1]);
+        *reinterpret_cast<double2*>(x1c + ib + 2) = make_double2(x1[2], x1[3]);
+      } else {
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+          if (ib + r < rows) x1c[ib + r] = x1[r];
+      }
+      store_digits4_prmt(q, kx, dig + j * ldd + ib, pstride);
+    }
+  }
+  const i128 sq = (static_cast<i128>(qa) << 52) + (static_cast<i128>(qb) << 27) + static_cast<i128>(qc);
+  const i128 SQ = block_sum_i128(sq, shq);
+  if (threadIdx.x == 0) {
+    g_out[j] = g;
+    const dd s = i128_to_dd(SQ);
+    s_hi[j] = scalbn(s.hi, 2 * g);
+    s_lo[j] = scalbn(s.lo, 2 * g);
+    if (-2 * g <= 125 && -2 * g >= 0) {
+      const dd r = i128_to_dd((static_cast<i128>(1) << (-2 * g)) - SQ);
+      r_hi[j] = scalbn(r.hi, 2 * g);
+      r_lo[j] = scalbn(r.lo, 2 * g);
+    } else {
+      const dd r = dd_add(dd{1.0, 0.0}, dd{-s_hi[j], -s_lo[j]});
+      r_hi[j] = r.hi;
+      r_lo[j] = r.lo;
+    }
+    if (SQ == 0) atomicOr(err, ERR_DEGENERATE);
+  }
+}
+
 template <typename T>
 __device__ __forceinline__ T rint_to(double x);
 template <>
@@ -676,7 +764,7 @@ __global__ void k_transpose_f64(const double* __restrict__ src, long long lds, d
   }
 }
 
-template <int NG>
+template <int NG, int TMA>
 __global__ void __launch_bounds__(BS, 3)
     k_recombine_V(const int32_t* __restrict__ planes, long long pstride, int rows, const __grid_constant__ RecombPlan rp,
                   const int32_t* __restrict__ ellA, const int32_t* __restrict__ ellB, int scale8,
@@ -692,7 +780,7 @@ __global__ void __launch_bounds__(BS, 3)
   dd t{0.0, 0.0};
   // pass 1: V (Alg. 1 line 1) and x̂_jᵀ v_j (line 3)
   const double* xc[1] = {x1};
-  for_column_x<1, false, NG>(planes, pstride, static_cast<long long>(j) * rows, rows, rp, Lj, xc, ellA, use_tma, tsm,
+  for_column_x<1, false, NG>(planes, pstride, static_cast<long long>(j) * rows, rows, rp, Lj, xc, ellA, TMA, tsm,
                   [&](int, int ea) { return ea + eb; },
                   [&](int i, const dd& v, const double* xv) {
                     Vh[j * ldv + i] = v.hi;
@@ -720,7 +808,7 @@ __global__ void __launch_bounds__(BS, 3)
   }
 }
 
-template <int NG>
+template <int NG, int TMA>
 __global__ void __launch_bounds__(BS, NG <= 8 ? 4 : 3)
     k_recombine_E(const int32_t* __restrict__ planes, long long pstride, int rows, const __grid_constant__ RecombPlan rp,
                   const int32_t* __restrict__ ellA, const int32_t* __restrict__ ellB, int scale8,
@@ -740,8 +828,11 @@ __global__ void __launch_bounds__(BS, NG <= 8 ? 4 : 3)
   // the row vectors λ̂_i and ℓ_i of the row operand (X̂^(1)ᵀ: g_i) ride in the shared-memory stages
   // with the planes
   const double* xc[1] = {lam};
-  for_column_x<1, true, NG>(planes, pstride, static_cast<long long>(j) * rows, rows, rp, Lj, xc, ellA, use_tma, tsm,
-                            [&](int, int gi) { return gi + eb; }, [&](int i, const dd& wv, const double* xv) {
+  // the row exponent of the row operand X̂^(1)ᵀ is g_i (ellA == gX): it scales Ẽ' = diag(2^g)Ẽ too, so the
+  // staged value is kept for the element (the exponent functor runs right before the element functor)
+  int gcur = 0;
+  for_column_x<1, true, NG>(planes, pstride, static_cast<long long>(j) * rows, rows, rp, Lj, xc, ellA, TMA, tsm,
+                            [&](int, int gi) { gcur = gi; return gi + eb; }, [&](int i, const dd& wv, const double* xv) {
     double e;
     w2 = __fma_rn(wv.hi, wv.hi, w2);
     if (i == jg) {
@@ -762,7 +853,7 @@ __global__ void __launch_bounds__(BS, NG <= 8 ? 4 : 3)
       }
     }
     s2 = __fma_rn(e, e, s2);
-    const double ep = ldexp_fast(e, gX[i]);  // Ẽ' = diag(2^g) Ẽ (exact)
+    const double ep = ldexp_fast(e, gcur);  // Ẽ' = diag(2^g) Ẽ (exact)
     Ep[j * lde + i] = ep;
     m = fmax(m, fabs(ep));
   });
@@ -801,7 +892,7 @@ __global__ void __launch_bounds__(BS)
   if (threadIdx.x == 0) nR2[j] = s2;
 }
 
-template <int NG>
+template <int NG, int TMA>
 __global__ void __launch_bounds__(BS, NG <= 8 ? 4 : 3)
     k_final(const int32_t* __restrict__ planes, long long pstride, int rows, const __grid_constant__ RecombPlan rp,
             const int32_t* __restrict__ ellB, int scale8, const double* __restrict__ X1, long long ldx1,
@@ -814,7 +905,7 @@ __global__ void __launch_bounds__(BS, NG <= 8 ? 4 : 3)
   const int eb = ellB[j] + scale8;  // the Q operand (digits of X̂^(1)/2^g) has ℓ = 0 on every row
   double s2 = 0.0, m = 0.0;
   const double* xc[2] = {X1 + j * ldx1, X + j * ldx};
-  for_column_x<2, false, NG>(planes, pstride, static_cast<long long>(j) * rows, rows, rp, Lj, xc, nullptr, use_tma, tsm,
+  for_column_x<2, false, NG>(planes, pstride, static_cast<long long>(j) * rows, rows, rp, Lj, xc, nullptr, TMA, tsm,
                   [&](int, int) { return eb; }, [&](int i, const dd& u, const double* xv) {
     const double x1 = xv[0];
     double s, e;
@@ -905,20 +996,19 @@ int tma_ok(const RecombPlan& rp, const int32_t* planes, long long pstride, int r
 // SM configuration as the slice GEMM, with which its register path co-resides)
 void init_attrs() {
   once_per_device(8, [] {
-#define OZR_CARVE(K) cudaFuncSetAttribute(K, cudaFuncAttributePreferredSharedMemoryCarveout, 100)
-    OZR_CARVE(k_recombine_V<4>); OZR_CARVE(k_recombine_V<8>); OZR_CARVE(k_recombine_V<12>);
-    OZR_CARVE(k_recombine_E<4>); OZR_CARVE(k_recombine_E<8>); OZR_CARVE(k_recombine_E<12>);
-    OZR_CARVE(k_final<4>); OZR_CARVE(k_final<8>); OZR_CARVE(k_final<12>);
-#undef OZR_CARVE
-    cudaFuncSetAttribute(k_recombine_V<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, tma_smem(4));
-    cudaFuncSetAttribute(k_recombine_V<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, tma_smem(8));
-    cudaFuncSetAttribute(k_recombine_V<12>, cudaFuncAttributeMaxDynamicSharedMemorySize, tma_smem(12));
-    cudaFuncSetAttribute(k_recombine_E<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, tma_smem(4));
-    cudaFuncSetAttribute(k_recombine_E<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, tma_smem(8));
-    cudaFuncSetAttribute(k_recombine_E<12>, cudaFuncAttributeMaxDynamicSharedMemorySize, tma_smem(12));
-    cudaFuncSetAttribute(k_final<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, tma_smem(4));
-    cudaFuncSetAttribute(k_final<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, tma_smem(8));
-    return cudaFuncSetAttribute(k_final<12>, cudaFuncAttributeMaxDynamicSharedMemorySize, tma_smem(12));
+#define OZR_ATTR(K)                                                                        \
+  cudaFuncSetAttribute(K<4, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, tma_smem(4));   \
+  cudaFuncSetAttribute(K<8, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, tma_smem(8));   \
+  cudaFuncSetAttribute(K<12, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, tma_smem(12)); \
+  cudaFuncSetAttribute(K<4, 1>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);        \
+  cudaFuncSetAttribute(K<8, 1>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);        \
+  cudaFuncSetAttribute(K<12, 1>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);       \
+  cudaFuncSetAttribute(K<12, 0>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    OZR_ATTR(k_recombine_V);
+    OZR_ATTR(k_recombine_E);
+    OZR_ATTR(k_final);
+#undef OZR_ATTR
+    return cudaPeekAtLastError();
   });
 }
 }  // namespace
@@ -934,8 +1024,13 @@ void launch_colmax(const double* X, long long ldx, int rows, int cols, double* w
 void launch_x1_split(const double* X, long long ldx, int rows, int cols, int beta, int kx, const double* w, double* X1,
                      long long ldx1, int8_t* dig, long long ldd, long long pstride, int32_t* g, double* s_hi,
                      double* s_lo, double* r_hi, double* r_lo, int* err, cudaStream_t s) {
-  k_x1_split<<<cols, BS, 0, s>>>(X, ldx, rows, beta, kx, w, X1, ldx1, dig, ldd, pstride, g, s_hi, s_lo, r_hi, r_lo,
-                                 err);
+  auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  if (al(X) && al(X1) && ldx % 2 == 0 && ldx1 % 2 == 0 && rows <= (1 << 19) && kx <= 8)
+    k_x1_split_v<<<cols, BS, 0, s>>>(X, ldx, rows, beta, kx, w, X1, ldx1, dig, ldd, pstride, g, s_hi, s_lo, r_hi,
+                                     r_lo, err);
+  else
+    k_x1_split<<<cols, BS, 0, s>>>(X, ldx, rows, beta, kx, w, X1, ldx1, dig, ldd, pstride, g, s_hi, s_lo, r_hi, r_lo,
+                                   err);
 }
 void launch_split_fixed(const double* M, const double* Mlo, long long ldm, int rows, int cols, int k, int8_t* dig,
                         long long ldd, long long pstride, int32_t* ell, int* err, cudaStream_t s) {
@@ -957,12 +1052,13 @@ void launch_recombine_V(const int32_t* planes, long long pstride, int rows, int 
                         double* lam_out, int32_t* eR, int* eR_max, cudaStream_t s, int allow_tma) {
   init_attrs();
   const int tma = allow_tma && tma_ok(rp, planes, pstride, rows, X1, ldx1, X1, ldx1) && (reinterpret_cast<uintptr_t>(ellA) & 15) == 0;
-#define OZR_RV(NG_)                                                                                          \
-  k_recombine_V<NG_><<<cols, BS, tma ? tma_smem(NG_) : 0, s>>>(planes, pstride, rows, rp, ellA, ellB, scale8, X1, ldx1, s_hi, \
+#define OZR_RV(NG_, TMA_)                                                                                          \
+  k_recombine_V<NG_, TMA_><<<cols, BS, TMA_ ? tma_smem(NG_) : 0, s>>>(planes, pstride, rows, rp, ellA, ellB, scale8, X1, ldx1, s_hi, \
                                                           s_lo, Vh, Vl, ldv, lam_out, eR, eR_max, tma)
-  if (tma && rp.ngroups <= 4) OZR_RV(4);
-  else if (tma && rp.ngroups <= 8) OZR_RV(8);
-  else OZR_RV(12);
+  if (tma && rp.ngroups <= 4) OZR_RV(4, 1);
+  else if (tma && rp.ngroups <= 8) OZR_RV(8, 1);
+  else if (tma) OZR_RV(12, 1);
+  else OZR_RV(12, 0);
 #undef OZR_RV
 }
 void launch_recombine_E(const int32_t* planes, long long pstride, int rows, int cols, const RecombPlan& rp,
@@ -970,13 +1066,18 @@ void launch_recombine_E(const int32_t* planes, long long pstride, int rows, int 
                         const int32_t* gX, int col0, double* Ep, long long lde, double* nrm2, int* eE_max,
                         int32_t* eE_col, int* err, const EdgeOut& eo, double* nW2, cudaStream_t s, int allow_tma) {
   init_attrs();
+  if (gX != ellA) {  // Ẽ' takes its row scaling from the staged row exponents (k_recombine_E)
+    fprintf(stderr, "ozr: launch_recombine_E: gX must be the row operand's exponents\n");
+    abort();
+  }
   const int tma = allow_tma && tma_ok(rp, planes, pstride, rows, lam, 0, nullptr, 0) && (reinterpret_cast<uintptr_t>(ellA) & 15) == 0;
-#define OZR_RE(NG_)                                                                                            \
-  k_recombine_E<NG_><<<cols, BS, tma ? tma_smem(NG_) : 0, s>>>(planes, pstride, rows, rp, ellA, ellB, scale8, r_hi, lam, gX, \
+#define OZR_RE(NG_, TMA_)                                                                                            \
+  k_recombine_E<NG_, TMA_><<<cols, BS, TMA_ ? tma_smem(NG_) : 0, s>>>(planes, pstride, rows, rp, ellA, ellB, scale8, r_hi, lam, gX, \
                                                           col0, Ep, lde, nrm2, eE_max, eE_col, err, eo, tma, nW2)
-  if (tma && rp.ngroups <= 4) OZR_RE(4);
-  else if (tma && rp.ngroups <= 8) OZR_RE(8);
-  else OZR_RE(12);
+  if (tma && rp.ngroups <= 4) OZR_RE(4, 1);
+  else if (tma && rp.ngroups <= 8) OZR_RE(8, 1);
+  else if (tma) OZR_RE(12, 1);
+  else OZR_RE(12, 0);
 #undef OZR_RE
 }
 void launch_final(const int32_t* planes, long long pstride, int rows, int cols, const RecombPlan& rp,
@@ -984,12 +1085,13 @@ void launch_final(const int32_t* planes, long long pstride, int rows, int cols, 
                   double* nu2, double* wnext, cudaStream_t s, int allow_tma, double* D) {
   init_attrs();
   const int tma = allow_tma && tma_ok(rp, planes, pstride, rows, X1, ldx1, X, ldx);
-#define OZR_FI(NG_)                                                                                                 \
-  k_final<NG_><<<cols, BS, tma ? tma_smem(NG_) : 0, s>>>(planes, pstride, rows, rp, ellB, scale8, X1, ldx1, X, ldx, nu2, wnext, \
+#define OZR_FI(NG_, TMA_)                                                                                                 \
+  k_final<NG_, TMA_><<<cols, BS, TMA_ ? tma_smem(NG_) : 0, s>>>(planes, pstride, rows, rp, ellB, scale8, X1, ldx1, X, ldx, nu2, wnext, \
                                                     tma, D)
-  if (tma && rp.ngroups <= 4) OZR_FI(4);
-  else if (tma && rp.ngroups <= 8) OZR_FI(8);
-  else OZR_FI(12);
+  if (tma && rp.ngroups <= 4) OZR_FI(4, 1);
+  else if (tma && rp.ngroups <= 8) OZR_FI(8, 1);
+  else if (tma) OZR_FI(12, 1);
+  else OZR_FI(12, 0);
 #undef OZR_FI
 }
 void launch_form_R(const int32_t* planes, long long pstride, int rows, int cols, const RecombPlan& rp, const int32_t* g,

@@ -68,6 +68,20 @@ void launch_form_R(const int32_t* planes, long long pstride, int rows, int cols,
                    int scale8, int col0, const double* r_hi, const double* r_lo, double* R, long long ldr, double* nR2,
                    cudaStream_t s);
 
+// Hermitian sweep (herm.cu; ozr_refine_step_herm, R18): complex n x n matrices in the real-stacked
+// 2n x n form [Re; Im].
+void launch_herm_embed(const double* Ar, const double* Ai, long long lda, int n, double* M, long long ldm,
+                       cudaStream_t s);
+void launch_herm_lam_res(const double* Vh, const double* Vl, long long ldv, const double* X1, long long ldx1,
+                         const double* s_hi, const double* s_lo, int n, double* lam, double* R2, long long ldr,
+                         double* rmax, cudaStream_t s);
+void launch_herm_E(const double* W, long long ldw, const double* lam, const double* r_hi, const int32_t* g, int n,
+                   double* B, long long ldb, double* nrm2, double* emax, int* err, cudaStream_t s);
+void launch_herm_Q(const double* X1, long long ldx1, const int32_t* g, int n, double* Q, long long ldq,
+                   cudaStream_t s);
+void launch_herm_final(const double* Uh, const double* Ul, long long ldu, const double* X1, long long ldx1, double* Xr,
+                       double* Xi, long long ldx, int n, double* nu2, cudaStream_t s);
+
 // Cluster sub-solve (cluster.cu). Groups g = 0..ngroups-1 with members mem[goff[g] .. goff[g]+gm[g]) (global
 // column indices, ascending (λ̂, index)); per-group m x m workspaces at offset gsq[g] (Σ m²) in M/R/K/V/Z.
 struct ClusterLaunch {

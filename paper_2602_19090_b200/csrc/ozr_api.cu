@@ -165,7 +165,9 @@ enum Slot {
   S_ADIG, S_AELL, S_W, S_X1, S_XDIG, S_XDIGT, S_G, S_SH, S_SL, S_RH, S_RL, S_PLANES, S_VH, S_VL, S_LAM, S_ER,
   S_ERR, S_EMAX, S_RDIG, S_RELL, S_EP, S_NRM2, S_NU2, S_WNEXT, S_ZEROELL, S_TMP1, S_TMP2, S_BELL, S_AT, S_ONES,
   S_EDGES, S_ECOUNT, S_CINT, S_CDBL, S_CM, S_CR, S_CK, S_CV, S_CZ, S_CT, S_CSCR, S_CFLAG, S_SCAL, S_UFALL, S_CPART, S_GCNT, S_WA, S_GPLANES, S_RMAT, S_NR2, S_NW2, S_DWORK, S_DINFO, S_PI_V, S_PI_Z, S_PI_Y, S_PI_P, S_PI_S, S_CXG, S_CGJ, S_CGP,
-  S_CEB, S_CCB, S_CSE, S_CSC, S_CESQ, S_CDSQ, S_CFLG, S_CEBT, S_CRE, S_OZA, S_OZB, S_OZEA, S_OZEB, S_OZT, S_OZP, S_DP, S_DTZ, S_DTH, S_PI_LZ, S_PI_U, S_PI_T
+  S_CEB, S_CCB, S_CSE, S_CSC, S_CESQ, S_CDSQ, S_CFLG, S_CEBT, S_CRE, S_OZA, S_OZB, S_OZEA, S_OZEB, S_OZT, S_OZP, S_DP, S_DTZ, S_DTH, S_PI_LZ, S_PI_U, S_PI_T,
+  S_HXS, S_HX1, S_HMA, S_HVH, S_HVL, S_HR2, S_HW, S_HB, S_HQ, S_HUH, S_HUL, S_HV1, S_HV2, S_HV3, S_HV4, S_HXD, S_HG,
+  S_HSH, S_HSL, S_HRH, S_HRL
 };
 
 ozr_status fail(ozr_ctx c, ozr_status st, const char* fmt, ...) {
@@ -412,6 +414,19 @@ int tile_budgets(int kA, int kB, int64_t K, int eA, const std::vector<int>& eB_c
   }
   *avg_pairs = pw / static_cast<double>(n);
   return Lmax;
+}
+
+// Average number of int32 group planes the recombination of one element reads (the per-tile budgets skip the
+// groups above a tile's L): the algorithmic plane bytes of a recombination kernel are 4 × this per element.
+double avg_planes(const RecombPlan& rp, int64_t n) {
+  if (!rp.tile_budgets) return rp.ngroups;
+  double acc = 0.0;
+  for (int64_t t = 0; t * kTileN < n; ++t) {
+    int c = 0;
+    for (int g = 0; g < rp.ngroups; ++g) c += rp.diag[g] <= rp.tileL[t];
+    acc += static_cast<double>(c) * static_cast<double>(std::min<int64_t>(kTileN, n - t * kTileN));
+  }
+  return acc / static_cast<double>(n);
 }
 
 void apply_tiles(PairTable& pt, RecombPlan& rp, const unsigned char* tileL, int64_t n) {
@@ -688,6 +703,50 @@ ozr_status oz_dgemm(ozr_ctx ctx, int64_t m, int64_t n, int64_t k, const double* 
   return OZR_OK;
 }
 
+// The Hermitian sweep's products (ozr_refine_step_herm, R18): C = A·B with explicit digit budgets (A per row into
+// kA digits, B per column into kB, pairs s + t ≤ L), exact recombination rounded once to double-double (Cl
+// nullable). a_trans: A stored as its transpose (k x m). Uses the dense sub-solve's product slots (the Hermitian
+// step has no cluster branch). *pairs += the pair count.
+ozr_status herm_product(ozr_ctx ctx, int64_t m, int64_t n, int64_t k, const double* A, int64_t lda, bool a_trans,
+                        const double* B, int64_t ldb, int kA, int kB, int L, double* Ch, double* Cl, int64_t ldc,
+                        int* derr, int* pairs) {
+  cudaStream_t s = ctx->stream;
+  const int64_t ldk = round16(k);
+  int8_t* da = ctx->ws<int8_t>(S_OZA, static_cast<size_t>(kA) * ldk * m);
+  int8_t* db = ctx->ws<int8_t>(S_OZB, static_cast<size_t>(kB) * ldk * n);
+  int32_t* ea = ctx->ws<int32_t>(S_OZEA, m);
+  int32_t* eb = ctx->ws<int32_t>(S_OZEB, n);
+  OZR_ALLOC(da); OZR_ALLOC(db); OZR_ALLOC(ea); OZR_ALLOC(eb);
+  const double* As = A;
+  int64_t lds = lda;
+  if (!a_trans) {
+    double* T = ctx->ws<double>(S_OZT, static_cast<size_t>(k) * m);
+    OZR_ALLOC(T);
+    launch_transpose_f64(A, lda, T, k, static_cast<int>(m), static_cast<int>(k), s);
+    As = T;
+    lds = k;
+  }
+  launch_split_fixed(As, nullptr, lds, static_cast<int>(k), static_cast<int>(m), kA, da, ldk, ldk * m, ea, derr, s);
+  launch_split_fixed(B, nullptr, ldb, static_cast<int>(k), static_cast<int>(n), kB, db, ldk, ldk * n, eb, derr, s);
+  std::vector<Group> gs = plan_groups(kA, kB, L, k);
+  PairTable pt;
+  RecombPlan rp;
+  if (!make_tables(gs, L, k, pt, rp)) return fail(ctx, OZR_ERR_RANGE, "Hermitian product plan too large");
+  *pairs += count_pairs(gs);
+  const size_t mn = static_cast<size_t>(m) * n;
+  int32_t* planes = ctx->ws<int32_t>(S_OZP, static_cast<size_t>(pt.ngroups) * mn);
+  int* cnt = ctx->ws<int>(S_GCNT, 4);
+  OZR_ALLOC(planes); OZR_ALLOC(cnt);
+  const DigitOperand oa{da, ldk, ldk * m, kA}, ob{db, ldk, ldk * n, kB};
+  OZR_CK(launch_gemm_i8(oa, ob, static_cast<int>(m), static_cast<int>(n), static_cast<int>(k), pt, planes,
+                        static_cast<int64_t>(mn), m, s, cnt),
+         "Hermitian slice GEMM");
+  launch_recombine_dd(planes, static_cast<long long>(mn), static_cast<int>(m), static_cast<int>(n), rp, ea, eb,
+                      8 * (kA + kB - L), Ch, Cl, ldc, s);
+  OZR_CK(cudaGetLastError(), "Hermitian recombination");
+  return OZR_OK;
+}
+
 // Block-column partition: rank r of P owns columns [col0, col0 + nl), nl = n/P, col0 = r·nl.
 // Every column of V, Res, W, Ẽ and X̂_new depends only on its own column of X̂^(1) plus the full X̂^(1)
 // (left operand of W and U) and the full λ̂, so a rank computes its columns with the slice GEMMs on
@@ -916,6 +975,7 @@ ozr_status sweep(ozr_ctx ctx, Exchange* ex, const double* A, int64_t n, int64_t 
   if (!make_tables(gV, LV, n, pt, rp)) return fail(ctx, OZR_ERR_RANGE, "V plan too large");
   const bool tilesV = P.tile_budgets && P.L_V <= 0;
   if (tilesV) apply_tiles(pt, rp, tileLV, nl);
+  rep.planes_V = avg_planes(rp, nl);
   size_t maxG = gV.size();
   int32_t* planes = ctx->ws<int32_t>(S_PLANES, maxG * nnl);
   OZR_ALLOC(planes);
@@ -1025,6 +1085,7 @@ ozr_status sweep(ozr_ctx ctx, Exchange* ex, const double* A, int64_t n, int64_t 
   if (!make_tables(gW, LW, n, pt, rp)) return fail(ctx, OZR_ERR_RANGE, "W plan too large");
   const bool tilesW = P.tile_budgets && P.L_W <= 0;
   if (tilesW) apply_tiles(pt, rp, tileLW, nl);
+  rep.planes_W = avg_planes(rp, nl);
   if (gW.size() > maxG) {
     maxG = gW.size();
     planes = ctx->ws<int32_t>(S_PLANES, maxG * nnl);
@@ -1328,6 +1389,7 @@ ozr_status sweep(ozr_ctx ctx, Exchange* ex, const double* A, int64_t n, int64_t 
   if (!make_tables(gU, LU, n, pt, rp)) return fail(ctx, OZR_ERR_RANGE, "U plan too large");
   const bool tilesU = P.tile_budgets && P.L_U <= 0;
   if (tilesU) apply_tiles(pt, rp, tileLU, nl);
+  rep.planes_U = avg_planes(rp, nl);
   if (gU.size() > maxG) {
     maxG = gU.size();
     planes = ctx->ws<int32_t>(S_PLANES, maxG * nnl);
@@ -1897,6 +1959,190 @@ ozr_status ozr_gemm(ozr_ctx ctx, int64_t m, int64_t n, int64_t k, const double* 
   launch_recombine_dd(planes, ps, static_cast<int>(m), static_cast<int>(n), rp, ea, eb, 8 * (kA + kB - L), C_hi, C_lo,
                       ldc, s);
   OZR_CK(cudaGetLastError(), "recombine");
+  return OZR_OK;
+}
+
+// The Hermitian extension of one sweep (R18; include/ozr.h): Algorithm 1 with
+// conjugate transposes, every complex product one real INT8 slice product of the stacked form (herm.cu), the
+// β of §4.1 and the accuracy-driven digit budgets of the real sweep (R8) with uniform (per-product) budgets.
+ozr_status ozr_refine_step_herm(ozr_ctx ctx, const double* Ar, const double* Ai, int64_t n, int64_t lda, double* Xr,
+                                double* Xi, int64_t ldx, double* lambda, const ozr_params* params,
+                                ozr_step_report* report) {
+  ozr_status st = check_ctx(ctx);
+  if (st != OZR_OK) return st;
+  if (!Ar || !Ai || !Xr || !Xi || !lambda || !params || n < 2 || lda < n || ldx < n)
+    return fail(ctx, OZR_ERR_ARG, "ozr_refine_step_herm: bad argument");
+  if (2 * n * 16384 > 2147483647LL) return fail(ctx, OZR_ERR_RANGE, "ozr_refine_step_herm: n too large");
+  const ozr_params P = *params;
+  if (P.delta <= 0.0) return fail(ctx, OZR_ERR_ARG, "ozr_refine_step_herm: delta <= 0");
+  ozr_step_report rep;
+  memset(&rep, 0, sizeof rep);
+  cudaStream_t s = ctx->stream;
+  cudaEventRecord(ctx->ev[0], s);
+  const int N = static_cast<int>(n), N2 = 2 * N;
+  const int64_t n2 = 2 * n;
+  const int64_t ld2 = round16(n2);
+  int* derr = ctx->ws<int>(S_ERR, 4);
+  double* Xs = ctx->ws<double>(S_HXS, static_cast<size_t>(n2) * n);
+  double* X1 = ctx->ws<double>(S_HX1, static_cast<size_t>(n2) * n);
+  int8_t* xd = ctx->ws<int8_t>(S_HXD, static_cast<size_t>(7) * ld2 * n);
+  int32_t* g = ctx->ws<int32_t>(S_HG, n);
+  double* sh = ctx->ws<double>(S_HSH, n);
+  double* sl = ctx->ws<double>(S_HSL, n);
+  double* rh = ctx->ws<double>(S_HRH, n);
+  double* rl = ctx->ws<double>(S_HRL, n);
+  double* v1 = ctx->ws<double>(S_HV1, n2);
+  double* v2 = ctx->ws<double>(S_HV2, n2);
+  double* lamn = ctx->ws<double>(S_HV3, n);
+  double* nrm = ctx->ws<double>(S_HV4, n);
+  OZR_ALLOC(derr); OZR_ALLOC(Xs); OZR_ALLOC(X1); OZR_ALLOC(xd); OZR_ALLOC(g); OZR_ALLOC(sh); OZR_ALLOC(sl);
+  OZR_ALLOC(rh); OZR_ALLOC(rl); OZR_ALLOC(v1); OZR_ALLOC(v2); OZR_ALLOC(lamn); OZR_ALLOC(nrm);
+  OZR_CK(cudaMemsetAsync(derr, 0, 4 * sizeof(int), s), "memset");
+  auto rd = [&](void* h, const void* d, size_t bytes) -> ozr_status {
+    OZR_CK(cudaMemcpyAsync(h, d, bytes, cudaMemcpyDeviceToHost, s), "D2H");
+    OZR_CK(cudaStreamSynchronize(s), "sync");
+    return OZR_OK;
+  };
+  auto errs = [&]() -> ozr_status {
+    int h = 0;
+    ozr_status e = rd(&h, derr, sizeof(int));
+    if (e != OZR_OK) return e;
+    return err_bits(ctx, h);
+  };
+  auto emax_of = [&](const std::vector<double>& v) {
+    int e = -100000;
+    for (double x : v)
+      if (x != 0.0) e = std::max(e, ceil_log2_host(x));
+    return e;
+  };
+  ozr_status e;
+  // ---- X̂s = [Xr; Xi] (2n x n), w_j = max over the stacked column, λ̂ statistics, β (§4.1)
+  OZR_CK(cudaMemcpy2DAsync(Xs, n2 * sizeof(double), Xr, ldx * sizeof(double), n * sizeof(double), n,
+                           cudaMemcpyDeviceToDevice, s), "stack X");
+  OZR_CK(cudaMemcpy2DAsync(Xs + n, n2 * sizeof(double), Xi, ldx * sizeof(double), n * sizeof(double), n,
+                           cudaMemcpyDeviceToDevice, s), "stack X");
+  launch_colmax(Xs, n2, N2, N, v1, derr, s);
+  std::vector<double> hw(n), hlam(n);
+  if ((e = rd(hw.data(), v1, n * sizeof(double))) != OZR_OK) return e;
+  if ((e = rd(hlam.data(), lambda, n * sizeof(double))) != OZR_OK) return e;
+  if ((e = errs()) != OZR_OK) return e;
+  for (double x : hlam)
+    if (!std::isfinite(x)) return fail(ctx, OZR_ERR_NONFINITE, "non-finite lambda");
+  const double delta_p = P.delta / (P.theta > 0 ? P.theta : 1.0);
+  LamStats ls = lam_stats(hlam);
+  if (!(ls.gap0 > 0.0)) return fail(ctx, OZR_ERR_DEGENERATE, "equal eigenvalue estimates (PAPER.md:333)");
+  const double ssum = sum_pow2_2c(hw);
+  if (ssum == 0.0 || ls.maxabs == 0.0) return fail(ctx, OZR_ERR_DEGENERATE, "zero X or zero spectrum");
+  const int beta_raw = (P.beta_override > 0) ? P.beta_override
+                                             : choose_beta(n, delta_p, P.beta_mode, P.xi, ls.gap0, ls.maxabs, ssum, 0);
+  const int beta = std::min(std::max(beta_raw, kBetaMin), kBetaMax);
+  const int kx = kx_for_beta(beta);
+  int cmax = -100000, gmin = 100000;
+  for (double x : hw) {
+    const int c = x != 0.0 ? ceil_log2_host(x) : 0;
+    if (x != 0.0) cmax = std::max(cmax, c);
+    gmin = std::min(gmin, c + beta - 53);
+  }
+  rep.beta = beta;
+  rep.beta_raw = beta_raw;
+  rep.alpha = alpha_dense(n, beta);
+  rep.kX = kx;
+  rep.gap_min = ls.gap0;
+  rep.max_abs_lambda = ls.maxabs;
+  // ---- X̂ → X̂^(1) (τ trick on both parts with the column's τ_j), g_j, x̂_jᴴx̂_j and r_j exactly
+  launch_x1_split(Xs, n2, N2, N, beta, kx, v1, X1, n2, xd, ld2, ld2 * n, g, sh, sl, rh, rl, derr, s);
+  OZR_CK(cudaGetLastError(), "x1 split");
+  // ---- V̂ = M_A·X̂s^(1) (Alg. 1 line 1), M_A = [[Ar, −Ai], [Ai, Ar]] (real symmetric, 2n x 2n)
+  double* MA = ctx->ws<double>(S_HMA, static_cast<size_t>(n2) * n2);
+  double* Vh = ctx->ws<double>(S_HVH, static_cast<size_t>(n2) * n);
+  double* Vl = ctx->ws<double>(S_HVL, static_cast<size_t>(n2) * n);
+  OZR_ALLOC(MA); OZR_ALLOC(Vh); OZR_ALLOC(Vl);
+  launch_herm_embed(Ar, Ai, lda, N, MA, n2, s);
+  launch_colmax(MA, n2, N2, N2, v2, derr, s);
+  std::vector<double> hv(n2);
+  if ((e = rd(hv.data(), v2, n2 * sizeof(double))) != OZR_OK) return e;
+  if ((e = errs()) != OZR_OK) return e;
+  const int eA = emax_of(hv);
+  const double tauV = P.theta_V * delta_p * ls.gap0;
+  int LV = P.L_V > 0 ? P.L_V : choose_L(kMaxDigits, kx, n2, eA, cmax, tauV);
+  LV = std::min(LV, kMaxDigits + kx);
+  const int kA = std::min(kMaxDigits, LV - 1);
+  rep.kA = kA;
+  rep.L_V = LV;
+  int pV = 0, pW = 0, pU = 0;
+  if ((e = herm_product(ctx, n2, n, n2, MA, n2, true, X1, n2, kA, kx, LV, Vh, Vl, n2, derr, &pV)) != OZR_OK) return e;
+  // ---- λ̂ (line 3), R̂ and JR̂ (line 4's right operand)
+  double* R2 = ctx->ws<double>(S_HR2, static_cast<size_t>(n2) * n2);
+  OZR_ALLOC(R2);
+  launch_herm_lam_res(Vh, Vl, n2, X1, n2, sh, sl, N, lamn, R2, n2, v1, s);
+  OZR_CK(cudaGetLastError(), "lambda / residual");
+  std::vector<double> hrm(n), hlam_new(n);
+  if ((e = rd(hrm.data(), v1, n * sizeof(double))) != OZR_OK) return e;
+  if ((e = rd(hlam_new.data(), lamn, n * sizeof(double))) != OZR_OK) return e;
+  if ((e = errs()) != OZR_OK) return e;
+  LamStats ls_new = lam_stats(hlam_new);
+  if (!(ls_new.gap0 > 0.0)) return fail(ctx, OZR_ERR_DEGENERATE, "equal Rayleigh quotients (PAPER.md:333)");
+  // ---- W = X̂ᴴR = X̂sᵀ·[R̂, JR̂] (n x 2n: [Re W, Im W]) (line 4)
+  const int eR = emax_of(hrm);
+  const double tauW = P.theta_W * delta_p * std::min(ls.gap0, ls_new.gap0);
+  const int kR = eR == -100000 ? 1 : digits_for(eR, static_cast<int>(std::floor(std::log2(tauW / 2.0))));
+  int LW = P.L_W > 0 ? P.L_W : choose_L(kx, kR, n2, cmax, eR == -100000 ? -1074 : eR, tauW);
+  LW = std::min(LW, kx + kR);
+  rep.kR = kR;
+  rep.L_W = LW;
+  double* Wd = ctx->ws<double>(S_HW, static_cast<size_t>(n) * n2);
+  OZR_ALLOC(Wd);
+  if ((e = herm_product(ctx, n, n2, n2, X1, n2, true, R2, n2, kx, kR, LW, Wd, nullptr, n, derr, &pW)) != OZR_OK)
+    return e;
+  // ---- Ẽ (line 5) as the B operand of U, and Q (U's A operand)
+  double* Bm = ctx->ws<double>(S_HB, static_cast<size_t>(n2) * n2);
+  double* Q = ctx->ws<double>(S_HQ, static_cast<size_t>(n) * n2);
+  OZR_ALLOC(Bm); OZR_ALLOC(Q);
+  launch_herm_E(Wd, n, lamn, rh, g, N, Bm, n2, nrm, v1, derr, s);
+  launch_herm_Q(X1, n2, g, N, Q, n, s);
+  OZR_CK(cudaGetLastError(), "E / Q");
+  std::vector<double> hem(n), hnrm(n);
+  if ((e = rd(hem.data(), v1, n * sizeof(double))) != OZR_OK) return e;
+  if ((e = rd(hnrm.data(), nrm, n * sizeof(double))) != OZR_OK) return e;
+  if ((e = errs()) != OZR_OK) return e;
+  double e2 = 0.0;
+  for (double x : hnrm) e2 += x;
+  rep.normE_fro = std::sqrt(e2);
+  // ---- U = X̂^(1)Ẽ = Q·[E1, E2] (n x 2n: [Re U, Im U]), X̂ ← RN(X̂^(1) + U) (line 6)
+  const double tauU = P.theta_U * delta_p;
+  int eE = emax_of(hem);
+  if (eE == -100000) eE = -1074;
+  const int kE = digits_for(eE, static_cast<int>(std::floor(std::log2(tauU / 2.0))) + gmin);
+  const int SX = 8 * (kx - 1) + 6;
+  int LU = P.L_U > 0 ? P.L_U : choose_L(kx, kE, n2, SX, eE, tauU);
+  LU = std::min(LU, kx + kE);
+  rep.kE = kE;
+  rep.L_U = LU;
+  double* Uh = ctx->ws<double>(S_HUH, static_cast<size_t>(n) * n2);
+  double* Ul = ctx->ws<double>(S_HUL, static_cast<size_t>(n) * n2);
+  OZR_ALLOC(Uh); OZR_ALLOC(Ul);
+  if ((e = herm_product(ctx, n, n2, n2, Q, n, false, Bm, n2, kx, kE, LU, Uh, Ul, n, derr, &pU)) != OZR_OK) return e;
+  launch_herm_final(Uh, Ul, n, X1, n2, Xr, Xi, ldx, N, nrm, s);
+  OZR_CK(cudaGetLastError(), "accsum");
+  OZR_CK(cudaMemcpyAsync(lambda, lamn, n * sizeof(double), cudaMemcpyDeviceToDevice, s), "lambda");
+  if ((e = rd(hnrm.data(), nrm, n * sizeof(double))) != OZR_OK) return e;
+  if ((e = errs()) != OZR_OK) return e;
+  double nu = 0.0;
+  for (double x : hnrm) nu += x;
+  rep.net_update = std::sqrt(nu);
+  rep.pairs_V = pV;
+  rep.pairs_W = pW;
+  rep.pairs_U = pU;
+  rep.int8_ops = 2.0 * static_cast<double>(n2) * n * n2 * pV + 2.0 * static_cast<double>(n) * n2 * n2 * (pW + pU);
+  rep.sweep = 1;
+  rep.theta = P.theta;
+  rep.cert = -1.0;
+  cudaEventRecord(ctx->ev[1], s);
+  cudaEventSynchronize(ctx->ev[1]);
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, ctx->ev[0], ctx->ev[1]);
+  rep.ms_total = ms;
+  if (report) *report = rep;
   return OZR_OK;
 }
 

@@ -45,7 +45,12 @@ METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.
 
 
 def raw(rep):
-    txt = subprocess.check_output(["ncu", "-i", rep, "--page", "raw", "--csv"], text=True)
+    import os
+    csvp = rep.replace(".ncu-rep", "_raw.csv")  # exported on the GPU box (ncu -i … --page raw --csv)
+    if os.path.exists(csvp):
+        txt = open(csvp).read()
+    else:
+        txt = subprocess.check_output(["ncu", "-i", rep, "--page", "raw", "--csv"], text=True)
     rows = list(csv.reader(io.StringIO(txt)))
     hdr, units = rows[0], rows[1]
     out = []
@@ -87,11 +92,49 @@ def full_table(rep, hbm_peak):
     return "\n".join(out)
 
 
+def algorithmic_bytes_per_element(name, sw):
+    """Algorithmic bytes per element of an n x n launch for the sweep plan `sw` (the bench line's
+    "sweep" dict: kX, kR, kE, planes_V/W/U = group planes recombined per element); None if not an HBM kernel."""
+    kx, kr, ke = sw["kX"], sw["kR"], sw["kE"]
+    table = {"k_x1_split": 8 + 8 + kx, "k_x1_split_v": 8 + 8 + kx, "k_colmax": 8,
+             "k_recombine_V": 4 * sw.get("planes_V", 0) + 8 + 16, "k_split_res": 24 + kr,
+             "k_recombine_E": 4 * sw.get("planes_W", 0) + 8, "k_final": 4 * sw.get("planes_U", 0) + 8 + 8 + 8,
+             "k_transpose_i8": 2 * kx, "k_split_fixed(E')": 8 + ke}
+    base = name.split("<")[0].replace("void ", "").replace("unnamed>::", "").strip()
+    return table.get(base)
+
+
+def algorithmic_table(rep, sw, n, hbm_peak):
+    out = ["| kernel | ms (ncu) | algorithmic bytes/element | algorithmic GB | algorithmic GB/s | % of HBM peak |",
+           "|---|---|---|---|---|---|"]
+    for d, u in raw(rep):
+        name = d.get("Kernel Name", "?").split("(")[0].replace("ozr::", "").replace("(anonymous namespace)::", "")
+        if "split_fixed" in name:
+            name = name.replace("k_split_fixed", "k_split_fixed(E')")
+        b = algorithmic_bytes_per_element(name, sw)
+        ms = num(d, u, "gpu__time_duration.sum")
+        if b is None or not ms:
+            continue
+        gb = b * n * n / 1e9
+        gbs = gb / (ms / 1e3)
+        out.append(f"| {name} | {ms:.3f} | {b:.1f} | {gb:.3f} | {gbs:.0f} | {100 * gbs / hbm_peak:.1f} |")
+    return "\n".join(out)
+
+
 if __name__ == "__main__":
     d = sys.argv[1] if len(sys.argv) > 1 else "gpurun_out"
     peak = float(sys.argv[sys.argv.index("--hbm-peak") + 1]) if "--hbm-peak" in sys.argv else 6533.8
     t, _ = launch_table(f"{d}/launches.csv")
     print("## Launch list\n\n" + t + "\n")
+    if "--bench" in sys.argv:  # algorithmic bytes from the bench line's sweep plan (n x n launches, 1 GPU)
+        import json
+        line = [ln for ln in open(sys.argv[sys.argv.index("--bench") + 1]) if ln.startswith("{")][-1]
+        bj = json.loads(line)
+        try:
+            print("## hbm_full, algorithmic bytes\n\n" + algorithmic_table(f"{d}/hbm_full.ncu-rep", bj["sweep"],
+                                                                           bj["config"]["n"], peak) + "\n")
+        except Exception as e:
+            print(f"## algorithmic: {e}\n")
     for rep in ("gemm_full", "hbm_full"):
         try:
             print(f"## {rep}\n\n" + full_table(f"{d}/{rep}.ncu-rep", peak) + "\n")

@@ -206,3 +206,74 @@ def householder_pair(m=6, pair=(10, 11), split=0.0, angle=0.0, noise=1e-9, lam_b
     X0[:, a], X0[:, b] = c * X[:, a] - s * X[:, b], s * X[:, a] + c * X[:, b]
     X0 = X0 + noise * np.random.default_rng(seed + 4).standard_normal(X.shape)
     return A, lam, X, X0
+
+
+# ---------------------------------------------------------------- Hermitian extension (reading R18)
+def haar_unitary(n, rng):
+    """Haar unitary Q: QR of a complex N(0,1) matrix (real and imaginary parts N(0, ½)), columns times the
+    phase of diag R."""
+    G = (rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))) / np.sqrt(2.0)
+    Q, R = np.linalg.qr(G)
+    d = np.diag(R)
+    return Q * (d / np.abs(d))[None, :]
+
+
+def make_hermitian(n, kind="geometric", cnd=1e10, seed=0):
+    """A = Q diag(λ) Qᴴ with Haar unitary Q and the same spectra as make_matrix, Hermitian-symmetrised as
+    (A + Aᴴ)/2. Returns (Ar, Ai, λ_design) — real and imaginary parts as separate fp64 arrays (Ar symmetric,
+    Ai antisymmetric with a zero diagonal)."""
+    rng = np.random.default_rng(seed)
+    if kind == "geometric":
+        lam = geometric_spectrum(n, cnd)
+    elif kind == "clustered":
+        lam = clustered_spectrum(n, rng)
+    else:
+        raise ValueError(kind)
+    Q = haar_unitary(n, rng)
+    A = (Q * lam[None, :]) @ Q.conj().T
+    A = (A + A.conj().T) * 0.5
+    return np.ascontiguousarray(A.real), np.ascontiguousarray(A.imag), lam
+
+
+def phase_fix(X):
+    """Multiply every column by the unit phase that makes its largest-modulus entry (lowest index on ties) real
+    and positive (the complex analogue of sign_fix)."""
+    idx = np.argmax(np.abs(X), axis=0)
+    p = X[idx, np.arange(X.shape[1])]
+    ph = np.where(np.abs(p) > 0, np.conj(p) / np.where(np.abs(p) > 0, np.abs(p), 1.0), 1.0)
+    return X * ph[None, :]
+
+
+def initial_eig_herm(Ar, Ai, start="fp64"):
+    """X̂₀, λ̂₀ of the Hermitian A from LAPACK (numpy.linalg.eigh = zheevd) in complex128, or in complex64 on
+    fl32(A) and cast back. Ascending λ, phase-fixed columns. Returns (λ̂₀, Xr, Xi)."""
+    A = np.asarray(Ar) + 1j * np.asarray(Ai)
+    if start == "fp64":
+        lam, X = np.linalg.eigh(A)
+    elif start == "fp32":
+        lam, X = np.linalg.eigh(A.astype(np.complex64))
+        lam, X = lam.astype(np.float64), X.astype(np.complex128)
+    else:
+        raise ValueError(start)
+    X = phase_fix(X)
+    return lam, np.ascontiguousarray(X.real), np.ascontiguousarray(X.imag)
+
+
+def householder_exact_herm(m, lam_bits=12, seed=0):
+    """Exactly known Hermitian family (the complex analogue of householder_exact): n = 2^m, v ∈ {±1, ±i}^n,
+    H = I − (2/n) v vᴴ (exactly unitary and Hermitian; every real and imaginary part is 0, ±2/n or 1 ± 2/n),
+    distinct dyadic λ with `lam_bits`-bit numerators, A = H diag(λ) H — exactly representable for moderate n and
+    lam_bits (checked by the caller). Returns (Ar, Ai, λ ascending, Xr, Xi exact (columns of H ordered by λ))."""
+    n = 2 ** m
+    rng = np.random.default_rng(seed)
+    v = rng.choice(np.array([1.0, -1.0, 1j, -1j]), size=n)
+    H = np.eye(n, dtype=np.complex128) - (2.0 / n) * np.outer(v, v.conj())
+    nums = rng.choice(np.arange(1, 2 ** lam_bits), size=n, replace=False)
+    lam = np.sort(nums.astype(np.float64) / 2 ** lam_bits)
+    order = rng.permutation(n)
+    lam_cols = np.empty(n)
+    lam_cols[order] = lam
+    A = (H * lam_cols[None, :]) @ H
+    X = H[:, order]
+    return np.ascontiguousarray(A.real), np.ascontiguousarray(A.imag), lam, np.ascontiguousarray(X.real), \
+        np.ascontiguousarray(X.imag)
