@@ -210,6 +210,45 @@ def run_per_product(ctx, A, B, rep, ozr, torch, steps=5, warmup=2):
     return out
 
 
+def run_hermitian(ctx, ozr, torch, dev, n=4096, steps=3, warmup=1):
+    """Effective FP64 TFLOP/s of one Hermitian sweep (ozr_refine_step_herm): A = Q diag(λ) Qᴴ with Haar unitary Q
+    (complex QR on the GPU, seeded N(0,1) parts from numpy), λ the c4' geometric spectrum (cnd 1e10), X̂₀ from the
+    FP64 (complex128) eigensolver; every step restarts from X̂₀. Flops per sweep: 3 complex products × 8n³."""
+    import workloads as W
+    rng = np.random.default_rng(2014)
+    G = torch.complex(torch.from_numpy(rng.standard_normal((n, n))), torch.from_numpy(rng.standard_normal((n, n))))
+    Q, R = torch.linalg.qr(G.to(dev) / np.sqrt(2.0))
+    d = torch.diagonal(R)
+    Q = Q * (d / d.abs())[None, :]
+    lam = torch.from_numpy(W.geometric_spectrum(n, 1e10)).to(dev)
+    A = (Q * lam[None, :].to(Q.dtype)) @ Q.conj().T
+    A = (A + A.conj().T) * 0.5
+    del Q, R, G
+    l0, X0 = torch.linalg.eigh(A)
+    Ar, Ai = ozr.colmajor(A.real.contiguous()), ozr.colmajor(A.imag.contiguous())
+    X0r, X0i = ozr.colmajor(X0.real.contiguous()), ozr.colmajor(X0.imag.contiguous())
+    del A, X0
+    p = ozr.default_params(delta=1e-12)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    times, rep = [], None
+    for it in range(warmup + steps):
+        Xr, Xi, lw = X0r.clone(), X0i.clone(), l0.clone()
+        torch.cuda.synchronize()
+        e0.record()
+        rep = ozr.ozr_refine_step_herm(ctx, Ar, Ai, Xr, Xi, lw, p)
+        e1.record()
+        torch.cuda.synchronize()
+        if it >= warmup:
+            times.append(e0.elapsed_time(e1))
+    ms = float(np.median(times))
+    return {"workload": f"Hermitian n={n}: A = Q diag(lam) Q^H (Haar unitary Q), geometric cnd=1e10, X0 from the "
+                        "complex128 eigensolver, delta=1e-12", "n": n, "ms_per_sweep": ms,
+            "value": 3 * 8.0 * n ** 3 / (ms / 1e3) / 1e12, "unit": "TFLOP/s",
+            "pairs": [rep["pairs_V"], rep["pairs_W"], rep["pairs_U"]], "beta": rep["beta"],
+            "note": "ozr_refine_step_herm (PAPER.md:731): each complex product one real INT8 slice product of the "
+                    "real-stacked operands (2n contraction); effective = 3 x 8n^3 / sweep time"}
+
+
 def run_c5(ctx, comm, dist_mode, ws, rank, dev, W, ozr, torch, dist, steps=2, warmup=1):
     """c5 sweeps partitioned over the ws ranks: rank 0 builds the problem, every rank receives it."""
     from paper_2602_19090_b200.dist import broadcast_tensor, partition
@@ -499,9 +538,9 @@ def main():
            "note": "ozr_refine_to_tol stops when its a-posteriori certificate (the sweep's own second-order defect, "
                    "DESIGN.md R12) x 1.15 <= delta"}
     if name == "c4p" and not args.n:
-        ttt["oracle_check"] = ("profiles/r01_ttt_verified_n8192.json: on this n = 8192 problem the forward error "
+        ttt["oracle_check"] = ("profiles/r01_ttt_verified_n8192.json: on this c4p n = 8192 problem the forward error "
                                "against the oracle's dd reference is 6.5e-13 = 0.65 delta after 2 sweeps (the "
-                               "certificate: 6.49e-13)")
+                               "certificate: 6.49e-13); other BASELINE recipes: profiles/r02/verify_*.json")
     # §8(f) rank 1: the prior work's two-sided fixed-slice plan (ozr_params.fixed_k)
     # against the proposed method on the same problem: device time to the stop rule, sweeps, pair-GEMMs
     fixed_k_cmp = None
@@ -545,6 +584,12 @@ def main():
     per_product = None
     if rank == 0 and not dist_mode and not args.headline_only:
         per_product = run_per_product(ctx, A, X0, reps[-1], ozr, torch)
+
+    # the Hermitian extension (ozr_refine_step_herm): one sweep of a complex Hermitian problem with
+    # the c4' spectrum at n = 4096 (Haar unitary Q, FP64 zheevd start), 3 complex products × 8n³ real flops
+    herm = None
+    if rank == 0 and not dist_mode and not args.headline_only and name == "c4p" and not args.n:
+        herm = run_hermitian(ctx, ozr, torch, dev)
 
     # c5 (n = 16384, cnd 1e10, FP64 start, δ = 1e-15): the north star's scaling configuration, the same
     # block-column partition over the ranks (strong scaling), device time max over ranks
@@ -637,7 +682,7 @@ def main():
                                             "max_cluster")},
                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                "gpu_launches": int(sum(r["launches"] for r in reps)), "clocks": clocks,
-               "time_to_target": ttt, "time_to_target_c4": ttt_c4, "c5_strong_scaling": c5,
+               "time_to_target": ttt, "time_to_target_c4": ttt_c4, "c5_strong_scaling": c5, "hermitian": herm,
                "fixed_k_comparison": fixed_k_cmp,
                "per_product": per_product}
         emit(out)

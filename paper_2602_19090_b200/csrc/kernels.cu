@@ -165,8 +165,9 @@ __device__ __forceinline__ dd recombine_elem(const int32_t* __restrict__ planes,
   return acc;
 }
 
-// Column sweep with two rows in flight per thread (the plane loads of row i + BS are issued before row
-// i is combined): f(i, v) for every row i of the column at `coloff`, e(i) its exponent.
+__device__ int g_fastdd = 1;  // OZR_FASTDD=0 (A/B only): the limb → double-double fast paths off
+
+// Column sweep (register path): f(i, v) for every row i of the column at `coloff`, e(i) its exponent.
 template <class EF, class F>
 __device__ __forceinline__ void for_column(const int32_t* __restrict__ planes, long long pstride, long long coloff,
                                            int rows, const RecombPlan& rp, int Lj, EF e, F f) {
@@ -196,32 +197,43 @@ __device__ __forceinline__ void for_column(const int32_t* __restrict__ planes, l
     flush_chunk(acc, first, T, dlast, rp.L, ee);
     return acc;
   };
-  int32_t ca[kFastGroups], cb[kFastGroups];
-  for (int i0 = threadIdx.x; i0 < rows; i0 += 2 * BS) {
-    const int i1 = i0 + BS;
+  // one row at a time: the two-rows-in-flight form of this loop (row i + BS's plane loads issued before row i is
+  // combined) gave run-to-run different results in the first row of each pair on sm_100a when compiled at the
+  // register budget of the 2-CTA-per-SM variants (measured: tools/dev/tma_ab.py, OZR_NO_TMA=4); this path is the
+  // fallback for unaligned operands and the experimental column bands, so it takes the plain form
+  int32_t ca[kFastGroups];
+  for (int i0 = threadIdx.x; i0 < rows; i0 += BS) {
     fetch(i0, ca);
-    fetch(i1, cb);
     f(i0, combine(ca, e(i0)));
-    if (i1 < rows) f(i1, combine(cb, e(i1)));
   }
 }
 
 // TMA-staged column sweep (HBM-bound recombination kernels): the column's plane segments and up to two
-// fp64 side columns stream through a TS-stage shared-memory ring filled by 1-D bulk copies
-// (cp.async.bulk + mbarrier), one stage = TR rows = one row per thread. f(i, v, xv) gets the recombined
-// element and the side-column values of row i. Requires rp.consecutive and 16-byte aligned segments
-// (rows % 4 == 0, even leading dimensions) — checked by the host (`use_tma`); else the register path.
+// fp64 side columns stream through a shared-memory ring filled by 1-D bulk copies (cp.async.bulk + mbarrier),
+// one stage = TR rows = two rows per thread. A stage holds only the column's ACTIVE planes (nact ≤ NG: the
+// per-tile budgets skip the groups above the tile's L), so its size follows the column, and the ring takes as
+// many stages as the launch's shared-memory budget holds (≤ kMaxStages): with few active planes more stages —
+// more bytes in flight — keep the copies ahead of the element loop. f(i, v, xv) gets the recombined element and
+// the side-column values of row i. Requires rp.consecutive and 16-byte aligned segments (rows % 4 == 0, even
+// leading dimensions) — checked by the host (`use_tma`); else the register path.
 constexpr int RPT = 2;         // rows per thread per stage (two independent element chains per thread)
 constexpr int TR = RPT * BS;   // rows per stage
-constexpr int TS = 2;          // stages
-// stage layout for NG compiled groups: planes | 2 fp64 sides | 1 int32 side (smaller plans, smaller
-// stages: more CTAs per SM)
-__host__ __device__ constexpr int stage_bytes(int ng) { return ng * TR * 4 + 2 * TR * 8 + TR * 4; }
-__host__ __device__ constexpr int side_i(int ng) { return ng * TR * 4 + 2 * TR * 8; }
-__host__ __device__ constexpr int tma_smem(int ng) { return TS * stage_bytes(ng) + TS * 8; }
+constexpr int kMaxStages = 8;
+// dynamic shared memory of a TMA launch: the ring budget + the stage barriers. Per kernel (measured, n = 8192):
+// recombine_V and final 70 KB (3 CTAs per SM: V's second pass and final's element chain want the extra bytes in
+// flight), recombine_E 54 KB (4 CTAs per SM: its FP64 division wants the warps)
+constexpr int kRingV = 70 * 1024, kRingE = 54 * 1024, kRingF = 70 * 1024;
+// the ring actually allocated: at least two stages of the largest layout of NG planes + NX fp64 sides + the
+// int32 side (so ts ≥ 2 always fits)
+__host__ __device__ constexpr int ring_for(int ring, int ng, int nx) {
+  return ring > 2 * ((ng * TR * 4 + nx * TR * 8 + TR * 4 + 127) / 128 * 128)
+             ? ring
+             : 2 * ((ng * TR * 4 + nx * TR * 8 + TR * 4 + 127) / 128 * 128);
+}
+__host__ __device__ constexpr int tma_smem(int ring) { return ring + kMaxStages * 8; }
 
 // icol (nullable): an int32 per-row vector staged beside the planes (the row exponents); e(i, icol[i]).
-template <int NX, bool HI_ONLY = false, int NG = kFastGroups, class EF, class F>
+template <int NX, bool HI_ONLY = false, int NG = kFastGroups, int RING = kRingV, class EF, class F>
 __device__ __forceinline__ void for_column_x(const int32_t* __restrict__ planes, long long pstride, long long coloff,
                                              int rows, const RecombPlan& rp, int Lj, const double* const* xcol,
                                              const int32_t* __restrict__ icol, int use_tma, unsigned char* tsm, EF e,
@@ -236,48 +248,49 @@ __device__ __forceinline__ void for_column_x(const int32_t* __restrict__ planes,
                });
     return;
   }
-  constexpr int kStageBytes = stage_bytes(NG), kSideI = side_i(NG);
-  uint64_t* bar = reinterpret_cast<uint64_t*>(tsm + TS * kStageBytes);
   const int tid = threadIdx.x;
   const int d0 = rp.diag[0];
   const int nact = max(0, min(rp.ngroups, Lj - d0 + 1));
   const int nl = (rp.ngroups + 3) >> 2;
   const int dlast = d0 + 4 * nl - 1;
+  const int sc0 = 8 * (rp.L - dlast);
   const int nch = (rows + TR - 1) / TR;
+  // this column's stage layout: nact planes | NX fp64 sides | the int32 side
+  const int kSideX = nact * TR * 4, kSideI = kSideX + NX * TR * 8;
+  const int kStageBytes = (kSideI + (icol ? TR * 4 : 0) + 127) & ~127;
+  constexpr int kRing = ring_for(RING, NG, NX);
+  const int ts = max(2, min(kMaxStages, kRing / kStageBytes));  // kRing ≥ 2·kStageBytes by construction
+  uint64_t* bar = reinterpret_cast<uint64_t*>(tsm + kRing);
   if (tid == 0) {
-    for (int st = 0; st < TS; ++st) mbar_init(&bar[st], 1);
+    for (int st = 0; st < ts; ++st) mbar_init(&bar[st], 1);
     fence_mbar_init();
   }
-  // the group slots the plan leaves empty (nact < NG) are never filled by the copies: zero them once, so
-  // the element loop reads all NG slots without a per-element guard
-  for (int st = 0; st < TS; ++st)
-    for (int g = nact; g < NG; ++g)
-      for (int r = tid; r < TR; r += BS) reinterpret_cast<int32_t*>(tsm + st * kStageBytes + g * TR * 4)[r] = 0;
   __syncthreads();
   auto issue = [&](int c) {
-    const int st = c % TS, r0 = c * TR, nr = min(TR, rows - r0);
+    const int st = c % ts, r0 = c * TR, nr = min(TR, rows - r0);
     unsigned char* base = tsm + st * kStageBytes;
     const uint32_t pb = static_cast<uint32_t>(nr) * 4u, xb = static_cast<uint32_t>(nr) * 8u;
     mbar_arrive_expect_tx(&bar[st], nact * pb + NX * xb + (icol ? pb : 0u));
     for (int g = 0; g < nact; ++g) bulk_g2s(base + g * TR * 4, planes + g * pstride + coloff + r0, pb, &bar[st]);
-    for (int x = 0; x < NX; ++x) bulk_g2s(base + NG * TR * 4 + x * TR * 8, xcol[x] + r0, xb, &bar[st]);
+    for (int x = 0; x < NX; ++x) bulk_g2s(base + kSideX + x * TR * 8, xcol[x] + r0, xb, &bar[st]);
     if (icol) bulk_g2s(base + kSideI, icol + r0, pb, &bar[st]);
   };
   if (tid == 0)
-    for (int c = 0; c < TS - 1 && c < nch; ++c) issue(c);
+    for (int c = 0; c < ts - 1 && c < nch; ++c) issue(c);
   for (int c = 0; c < nch; ++c) {
-    if (tid == 0 && c + TS - 1 < nch) issue(c + TS - 1);  // its stage was released by the last barrier
-    mbar_wait(&bar[c % TS], (c / TS) & 1);
+    if (tid == 0 && c + ts - 1 < nch) issue(c + ts - 1);  // its stage was released by the last barrier
+    mbar_wait(&bar[c % ts], (c / ts) & 1);
+    const unsigned char* base = tsm + (c % ts) * kStageBytes;
 #pragma unroll
     for (int h = 0; h < RPT; ++h) {
     const int tl = tid + h * BS;  // row within the stage
     const int i = c * TR + tl;
     if (i < rows) {
-      const unsigned char* base = tsm + (c % TS) * kStageBytes;
-      // NG: groups compiled for this launch (4, 8 or 12 ≥ ngroups), so small plans do no dead work
+      // NG: groups compiled for this launch (4, 8 or 12 ≥ ngroups); the slots above nact read as zero (a
+      // uniform predicate per column, no branch)
       int32_t cv[NG];
 #pragma unroll
-      for (int g = 0; g < NG; ++g) cv[g] = reinterpret_cast<const int32_t*>(base + g * TR * 4)[tl];
+      for (int g = 0; g < NG; ++g) cv[g] = (g < nact) ? reinterpret_cast<const int32_t*>(base + g * TR * 4)[tl] : 0;
       long long Lm[NG / 4];
 #pragma unroll
       for (int k = 0; k < NG / 4; ++k)
@@ -285,15 +298,36 @@ __device__ __forceinline__ void for_column_x(const int32_t* __restrict__ planes,
       dd v{0.0, 0.0};
       const int ee = e(i, icol ? reinterpret_cast<const int32_t*>(base + kSideI)[tl] : 0);
       if (HI_ONLY && NG <= 8) {  // RN(value) from the one or two limbs, without 128-bit arithmetic
-        const double h = (nl == 1) ? __ll2double_rn(Lm[0]) : limbs2_rn(Lm[0], Lm[NG / 4 - 1]);
-        v.hi = ldexp_fast(h, 8 * (rp.L - dlast) + ee);
+        const double hv = (nl == 1) ? __ll2double_rn(Lm[0]) : limbs2_rn(Lm[0], Lm[NG / 4 - 1]);
+        v.hi = ldexp_fast(hv, sc0 + ee);
+      } else if (g_fastdd && (NG == 4 || (NG <= 8 && nl == 1))) {  // one limb (|T| < 2^55): hi = RN(T), lo = T − hi exactly
+        const double hv = __ll2double_rn(Lm[0]);
+        const double lv = static_cast<double>(Lm[0] - __double2ll_rz(hv));
+        v.hi = ldexp_fast(hv, sc0 + ee);
+        v.lo = ldexp_fast(lv, sc0 + ee);
+      } else if (g_fastdd && NG == 8) {  // two limbs: T = s·2^32 + b (s = L0 + ⌊L1/2^32⌋, 0 ≤ b < 2^32)
+        const long long sL = Lm[0] + (Lm[1] >> 32);
+        const double bd = static_cast<double>(static_cast<unsigned long long>(Lm[1]) & 0xFFFFFFFFull);
+        if (sL > -(1LL << 47) && sL < (1LL << 47)) {
+          // |T| < 2^79: hi = RN(s·2^32 + b) in one fma; T − hi = (s·2^32 − hi) + b with s·2^32 − hi exact in
+          // the fma (|T − hi| ≤ ulp(hi)/2 < 2^26, b < 2^32: the sum is an exact integer below 2^34)
+          const double sd = static_cast<double>(sL);
+          const double hv = fma(sd, 4294967296.0, bd);
+          const double lv = fma(sd, 4294967296.0, -hv) + bd;
+          v.hi = ldexp_fast(hv, sc0 + ee);
+          v.lo = ldexp_fast(lv, sc0 + ee);
+        } else {
+          const i128 T = static_cast<i128>(static_cast<u128>(static_cast<i128>(Lm[0])) << 32) + static_cast<i128>(Lm[1]);
+          bool first = true;
+          flush_chunk(v, first, T, dlast, rp.L, ee);
+        }
       } else {
         i128 T = Lm[0];
 #pragma unroll
         for (int k = 1; k < NG / 4; ++k)
           if (k < nl) T = static_cast<i128>(static_cast<u128>(T) << 32) + static_cast<i128>(Lm[k]);
         if (HI_ONLY) {  // the caller uses RN(value) only (its hi part is the same correctly rounded double)
-          v.hi = ldexp_fast(i128_to_f64(T), 8 * (rp.L - dlast) + ee);
+          v.hi = ldexp_fast(i128_to_f64(T), sc0 + ee);
         } else {
           bool first = true;
           flush_chunk(v, first, T, dlast, rp.L, ee);
@@ -301,7 +335,7 @@ __device__ __forceinline__ void for_column_x(const int32_t* __restrict__ planes,
       }
       double xv[NX > 0 ? NX : 1];
 #pragma unroll
-      for (int x = 0; x < NX; ++x) xv[x] = reinterpret_cast<const double*>(base + NG * TR * 4 + x * TR * 8)[tl];
+      for (int x = 0; x < NX; ++x) xv[x] = reinterpret_cast<const double*>(base + kSideX + x * TR * 8)[tl];
       f(i, v, xv);
     }
     }
@@ -747,6 +781,44 @@ __global__ void k_transpose_i8(const int8_t* __restrict__ src, long long lds, lo
   }
 }
 
+// The same transpose with 16-byte global loads and stores (64 x 64-byte tiles, one 16-byte load and one 16-byte
+// store per thread): for 16-byte aligned planes with lds, ldt, sps, tps multiples of 16 and rows, cols ≥ 1 (the
+// 16-byte groups that straddle `rows` / `cols` stay inside each line's padding, as in k_transpose_i8).
+__global__ void __launch_bounds__(256) k_transpose_i8_v(const int8_t* __restrict__ src, long long lds, long long sps,
+                                                        int8_t* __restrict__ dst, long long ldt, long long tps,
+                                                        int rows, int cols) {
+  __shared__ uint32_t t[64][17];  // t[j][i/4]: column j's 64 bytes as 16 words (+1 word: conflict-free columns)
+  const int p = blockIdx.z;
+  const int i0 = blockIdx.x * 64, j0 = blockIdx.y * 64;
+  const int tid = threadIdx.x;
+  {
+    const int jj = tid >> 2, q = tid & 3;  // column j0 + jj, bytes [16q, 16q + 16) of the tile's rows
+    const int i = i0 + 16 * q, j = j0 + jj;
+    uint4 v = make_uint4(0u, 0u, 0u, 0u);
+    if (i < rows && j < cols) v = *reinterpret_cast<const uint4*>(src + p * sps + j * lds + i);
+    t[jj][4 * q + 0] = v.x;
+    t[jj][4 * q + 1] = v.y;
+    t[jj][4 * q + 2] = v.z;
+    t[jj][4 * q + 3] = v.w;
+  }
+  __syncthreads();
+  {
+    const int ii = tid >> 2, q = tid & 3;  // output row i0 + ii, bytes [16q, 16q + 16) = columns j0 + 16q + ..
+    const int i = i0 + ii, j = j0 + 16 * q;
+    if (i < rows && j < cols) {
+      const int w = ii >> 2, sh = 8 * (ii & 3);
+      uint32_t o[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int jb = 16 * q + 4 * k;
+        o[k] = ((t[jb][w] >> sh) & 0xFFu) | (((t[jb + 1][w] >> sh) & 0xFFu) << 8) |
+               (((t[jb + 2][w] >> sh) & 0xFFu) << 16) | (((t[jb + 3][w] >> sh) & 0xFFu) << 24);
+      }
+      *reinterpret_cast<uint4*>(dst + p * tps + static_cast<long long>(i) * ldt + j) = make_uint4(o[0], o[1], o[2], o[3]);
+    }
+  }
+}
+
 __global__ void k_transpose_f64(const double* __restrict__ src, long long lds, double* __restrict__ dst,
                                 long long ldt, int rows, int cols) {
   // dst (cols x rows) = srcᵀ, column-major both
@@ -780,7 +852,7 @@ __global__ void __launch_bounds__(BS, 3)
   dd t{0.0, 0.0};
   // pass 1: V (Alg. 1 line 1) and x̂_jᵀ v_j (line 3)
   const double* xc[1] = {x1};
-  for_column_x<1, false, NG>(planes, pstride, static_cast<long long>(j) * rows, rows, rp, Lj, xc, ellA, TMA, tsm,
+  for_column_x<1, false, NG, kRingV>(planes, pstride, static_cast<long long>(j) * rows, rows, rp, Lj, xc, ellA, TMA, tsm,
                   [&](int, int ea) { return ea + eb; },
                   [&](int i, const dd& v, const double* xv) {
                     Vh[j * ldv + i] = v.hi;
@@ -809,7 +881,7 @@ __global__ void __launch_bounds__(BS, 3)
 }
 
 template <int NG, int TMA>
-__global__ void __launch_bounds__(BS, NG <= 8 ? 4 : 3)
+__global__ void __launch_bounds__(BS, NG <= 8 ? 4 : 2)
     k_recombine_E(const int32_t* __restrict__ planes, long long pstride, int rows, const __grid_constant__ RecombPlan rp,
                   const int32_t* __restrict__ ellA, const int32_t* __restrict__ ellB, int scale8,
                   const double* __restrict__ r_hi, const double* __restrict__ lam, const int32_t* __restrict__ gX,
@@ -831,7 +903,7 @@ __global__ void __launch_bounds__(BS, NG <= 8 ? 4 : 3)
   // the row exponent of the row operand X̂^(1)ᵀ is g_i (ellA == gX): it scales Ẽ' = diag(2^g)Ẽ too, so the
   // staged value is kept for the element (the exponent functor runs right before the element functor)
   int gcur = 0;
-  for_column_x<1, true, NG>(planes, pstride, static_cast<long long>(j) * rows, rows, rp, Lj, xc, ellA, TMA, tsm,
+  for_column_x<1, true, NG, kRingE>(planes, pstride, static_cast<long long>(j) * rows, rows, rp, Lj, xc, ellA, TMA, tsm,
                             [&](int, int gi) { gcur = gi; return gi + eb; }, [&](int i, const dd& wv, const double* xv) {
     double e;
     w2 = __fma_rn(wv.hi, wv.hi, w2);
@@ -893,7 +965,7 @@ __global__ void __launch_bounds__(BS)
 }
 
 template <int NG, int TMA>
-__global__ void __launch_bounds__(BS, NG <= 8 ? 4 : 3)
+__global__ void __launch_bounds__(BS, NG <= 8 ? 3 : 2)
     k_final(const int32_t* __restrict__ planes, long long pstride, int rows, const __grid_constant__ RecombPlan rp,
             const int32_t* __restrict__ ellB, int scale8, const double* __restrict__ X1, long long ldx1,
             double* __restrict__ X, long long ldx, double* __restrict__ nu2, double* __restrict__ wnext, int use_tma,
@@ -905,7 +977,7 @@ __global__ void __launch_bounds__(BS, NG <= 8 ? 4 : 3)
   const int eb = ellB[j] + scale8;  // the Q operand (digits of X̂^(1)/2^g) has ℓ = 0 on every row
   double s2 = 0.0, m = 0.0;
   const double* xc[2] = {X1 + j * ldx1, X + j * ldx};
-  for_column_x<2, false, NG>(planes, pstride, static_cast<long long>(j) * rows, rows, rp, Lj, xc, nullptr, TMA, tsm,
+  for_column_x<2, false, NG, kRingF>(planes, pstride, static_cast<long long>(j) * rows, rows, rp, Lj, xc, nullptr, TMA, tsm,
                   [&](int, int) { return eb; }, [&](int i, const dd& u, const double* xv) {
     const double x1 = xv[0];
     double s, e;
@@ -983,6 +1055,20 @@ __global__ void k_copy_bytes(char* __restrict__ dst, const char* __restrict__ sr
 // ---------------------------------------------------------------- launchers
 namespace {
 void init_attrs();
+// OZR_NO_TMA (A/B only): bit 0 / 1 / 2 forces the register path of recombine_V / recombine_E / final
+int no_tma_mask() {
+  static int m = -1;
+  if (m < 0) {
+    const char* e = getenv("OZR_NO_TMA");
+    m = e ? atoi(e) : 0;
+    const char* f = getenv("OZR_FASTDD");
+    if (f && f[0] == '0') {
+      int z = 0;
+      cudaMemcpyToSymbol(g_fastdd, &z, sizeof z);
+    }
+  }
+  return m;
+}
 int tma_ok(const RecombPlan& rp, const int32_t* planes, long long pstride, int rows, const double* x0, long long ld0,
            const double* x1, long long ld1) {
   init_attrs();
@@ -996,17 +1082,17 @@ int tma_ok(const RecombPlan& rp, const int32_t* planes, long long pstride, int r
 // SM configuration as the slice GEMM, with which its register path co-resides)
 void init_attrs() {
   once_per_device(8, [] {
-#define OZR_ATTR(K)                                                                        \
-  cudaFuncSetAttribute(K<4, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, tma_smem(4));   \
-  cudaFuncSetAttribute(K<8, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, tma_smem(8));   \
-  cudaFuncSetAttribute(K<12, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, tma_smem(12)); \
-  cudaFuncSetAttribute(K<4, 1>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);        \
-  cudaFuncSetAttribute(K<8, 1>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);        \
-  cudaFuncSetAttribute(K<12, 1>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);       \
+#define OZR_ATTR(K, R, NX)                                                                                 \
+  cudaFuncSetAttribute(K<4, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, tma_smem(ring_for(R, 4, NX)));   \
+  cudaFuncSetAttribute(K<8, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, tma_smem(ring_for(R, 8, NX)));   \
+  cudaFuncSetAttribute(K<12, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, tma_smem(ring_for(R, 12, NX))); \
+  cudaFuncSetAttribute(K<4, 1>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);                        \
+  cudaFuncSetAttribute(K<8, 1>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);                        \
+  cudaFuncSetAttribute(K<12, 1>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);                       \
   cudaFuncSetAttribute(K<12, 0>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    OZR_ATTR(k_recombine_V);
-    OZR_ATTR(k_recombine_E);
-    OZR_ATTR(k_final);
+    OZR_ATTR(k_recombine_V, kRingV, 1);
+    OZR_ATTR(k_recombine_E, kRingE, 1);
+    OZR_ATTR(k_final, kRingF, 2);
 #undef OZR_ATTR
     return cudaPeekAtLastError();
   });
@@ -1039,7 +1125,12 @@ void launch_split_fixed(const double* M, const double* Mlo, long long ldm, int r
 void launch_transpose_i8(const int8_t* src, long long lds, long long sps, int8_t* dst, long long ldt, long long tps,
                          int rows, int cols, int planes, cudaStream_t s) {
   dim3 grid((rows + 63) / 64, (cols + 63) / 64, planes);
-  k_transpose_i8<<<grid, 256, 0, s>>>(src, lds, sps, dst, ldt, tps, rows, cols);
+  const bool al = ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0 &&
+                  (lds | sps | ldt | tps) % 16 == 0;
+  if (al)
+    k_transpose_i8_v<<<grid, 256, 0, s>>>(src, lds, sps, dst, ldt, tps, rows, cols);
+  else
+    k_transpose_i8<<<grid, 256, 0, s>>>(src, lds, sps, dst, ldt, tps, rows, cols);
 }
 void launch_transpose_f64(const double* src, long long lds, double* dst, long long ldt, int rows, int cols,
                           cudaStream_t s) {
@@ -1051,9 +1142,9 @@ void launch_recombine_V(const int32_t* planes, long long pstride, int rows, int 
                         const double* s_hi, const double* s_lo, double* Vh, double* Vl, long long ldv,
                         double* lam_out, int32_t* eR, int* eR_max, cudaStream_t s, int allow_tma) {
   init_attrs();
-  const int tma = allow_tma && tma_ok(rp, planes, pstride, rows, X1, ldx1, X1, ldx1) && (reinterpret_cast<uintptr_t>(ellA) & 15) == 0;
+  const int tma = allow_tma && !(no_tma_mask() & 1) && tma_ok(rp, planes, pstride, rows, X1, ldx1, X1, ldx1) && (reinterpret_cast<uintptr_t>(ellA) & 15) == 0;
 #define OZR_RV(NG_, TMA_)                                                                                          \
-  k_recombine_V<NG_, TMA_><<<cols, BS, TMA_ ? tma_smem(NG_) : 0, s>>>(planes, pstride, rows, rp, ellA, ellB, scale8, X1, ldx1, s_hi, \
+  k_recombine_V<NG_, TMA_><<<cols, BS, TMA_ ? tma_smem(ring_for(kRingV, NG_, 1)) : 0, s>>>(planes, pstride, rows, rp, ellA, ellB, scale8, X1, ldx1, s_hi, \
                                                           s_lo, Vh, Vl, ldv, lam_out, eR, eR_max, tma)
   if (tma && rp.ngroups <= 4) OZR_RV(4, 1);
   else if (tma && rp.ngroups <= 8) OZR_RV(8, 1);
@@ -1070,9 +1161,10 @@ void launch_recombine_E(const int32_t* planes, long long pstride, int rows, int 
     fprintf(stderr, "ozr: launch_recombine_E: gX must be the row operand's exponents\n");
     abort();
   }
-  const int tma = allow_tma && tma_ok(rp, planes, pstride, rows, lam, 0, nullptr, 0) && (reinterpret_cast<uintptr_t>(ellA) & 15) == 0;
+  const int tma = allow_tma && !(no_tma_mask() & 2) && tma_ok(rp, planes, pstride, rows, lam, 0, nullptr, 0) &&
+                  (reinterpret_cast<uintptr_t>(ellA) & 15) == 0;
 #define OZR_RE(NG_, TMA_)                                                                                            \
-  k_recombine_E<NG_, TMA_><<<cols, BS, TMA_ ? tma_smem(NG_) : 0, s>>>(planes, pstride, rows, rp, ellA, ellB, scale8, r_hi, lam, gX, \
+  k_recombine_E<NG_, TMA_><<<cols, BS, TMA_ ? tma_smem(ring_for(kRingE, NG_, 1)) : 0, s>>>(planes, pstride, rows, rp, ellA, ellB, scale8, r_hi, lam, gX, \
                                                           col0, Ep, lde, nrm2, eE_max, eE_col, err, eo, tma, nW2)
   if (tma && rp.ngroups <= 4) OZR_RE(4, 1);
   else if (tma && rp.ngroups <= 8) OZR_RE(8, 1);
@@ -1084,9 +1176,9 @@ void launch_final(const int32_t* planes, long long pstride, int rows, int cols, 
                   const int32_t* ellB, int scale8, const double* X1, long long ldx1, double* X, long long ldx,
                   double* nu2, double* wnext, cudaStream_t s, int allow_tma, double* D) {
   init_attrs();
-  const int tma = allow_tma && tma_ok(rp, planes, pstride, rows, X1, ldx1, X, ldx);
+  const int tma = allow_tma && !(no_tma_mask() & 4) && tma_ok(rp, planes, pstride, rows, X1, ldx1, X, ldx);
 #define OZR_FI(NG_, TMA_)                                                                                                 \
-  k_final<NG_, TMA_><<<cols, BS, TMA_ ? tma_smem(NG_) : 0, s>>>(planes, pstride, rows, rp, ellB, scale8, X1, ldx1, X, ldx, nu2, wnext, \
+  k_final<NG_, TMA_><<<cols, BS, TMA_ ? tma_smem(ring_for(kRingF, NG_, 2)) : 0, s>>>(planes, pstride, rows, rp, ellB, scale8, X1, ldx1, X, ldx, nu2, wnext, \
                                                     tma, D)
   if (tma && rp.ngroups <= 4) OZR_FI(4, 1);
   else if (tma && rp.ngroups <= 8) OZR_FI(8, 1);

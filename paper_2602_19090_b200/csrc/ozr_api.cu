@@ -38,6 +38,10 @@ struct DevBuf {
   void* p = nullptr;
   size_t bytes = 0;
 };
+// Guard-band mode (OZR_GUARD=1 at ozr_create; memory-safety checking without compute-sanitizer): every workspace
+// buffer gets kGuardBytes of a fixed pattern behind its end, checked after every ABI call that ran kernels.
+constexpr size_t kGuardBytes = 4096;
+constexpr unsigned char kGuardByte = 0xA5;
 
 }  // namespace
 
@@ -138,6 +142,15 @@ struct ozr_ctx_s {
     tn = 0;
   }
 
+  bool guard = false;
+  int guard_bad = -1;  // a slot whose guard band was found overwritten (reported by guard_check)
+  bool guard_ok(const DevBuf& b) {
+    unsigned char h[kGuardBytes];
+    if (cudaMemcpy(h, static_cast<char*>(b.p) + b.bytes, kGuardBytes, cudaMemcpyDeviceToHost) != cudaSuccess) return false;
+    for (size_t i = 0; i < kGuardBytes; ++i)
+      if (h[i] != kGuardByte) return false;
+    return true;
+  }
   // Workspace slot: grow-only device buffer.
   template <typename T>
   T* ws(int slot, size_t count) {
@@ -146,14 +159,22 @@ struct ozr_ctx_s {
     size_t need = count * sizeof(T);
     if (need == 0) need = 16;
     if (b.bytes < need) {
-      if (b.p) cudaFree(b.p);
+      if (b.p) {
+        if (guard) cudaStreamSynchronize(stream);  // the old buffer's last users are done before it is checked
+        if (guard && !guard_ok(b)) guard_bad = slot;
+        cudaFree(b.p);
+      }
       b.p = nullptr;
       b.bytes = 0;
-      if (cudaMalloc(&b.p, need) != cudaSuccess) {
+      if (cudaMalloc(&b.p, need + (guard ? kGuardBytes : 0)) != cudaSuccess) {
         cudaGetLastError();
         return nullptr;
       }
       b.bytes = need;
+      if (guard) {
+        cudaMemset(static_cast<char*>(b.p) + need, kGuardByte, kGuardBytes);
+        cudaDeviceSynchronize();
+      }
     }
     return static_cast<T*>(b.p);
   }
@@ -1666,6 +1687,17 @@ ozr_status check_ctx(ozr_ctx ctx) {
   return OZR_OK;
 }
 
+// Guard-band mode: every workspace buffer's guard band still holds the pattern (after all queued work)
+ozr_status guard_check(ozr_ctx ctx, ozr_status st) {
+  if (!ctx || !ctx->guard) return st;
+  cudaStreamSynchronize(ctx->stream);
+  int bad = ctx->guard_bad;
+  for (size_t i = 0; i < ctx->bufs.size() && bad < 0; ++i)
+    if (ctx->bufs[i].p && !ctx->guard_ok(ctx->bufs[i])) bad = static_cast<int>(i);
+  if (bad >= 0) return fail(ctx, OZR_ERR_CUDA, "guard band of workspace slot %d overwritten", bad);
+  return st;
+}
+
 }  // namespace
 
 // ================================================================ C ABI
@@ -1700,6 +1732,8 @@ ozr_status ozr_create(ozr_ctx* out, int device, void* stream, int64_t n_max) {
   c->events = true;
   const char* tr = getenv("OZR_TRACE");
   c->trace = tr && tr[0] == '1';
+  const char* gd = getenv("OZR_GUARD");
+  c->guard = gd && gd[0] == '1';
   *out = c;
   return OZR_OK;
 }
@@ -1842,7 +1876,7 @@ ozr_status ozr_syev(ozr_ctx ctx, int64_t m, const double* K, int64_t ldk, double
   OZR_CK(cudaMemcpy2DAsync(Y, ldy * sizeof(double), Yw, m * sizeof(double), m * sizeof(double), m,
                            cudaMemcpyDeviceToDevice, s), "copy Y");
   OZR_CK(cudaStreamSynchronize(s), "sync");
-  return OZR_OK;
+  return guard_check(ctx, OZR_OK);
 }
 
 ozr_status ozr_syev_tridiag(ozr_ctx ctx, int64_t m, double* K, int64_t ldk, double* d, double* e, double* tau) {
@@ -1959,7 +1993,7 @@ ozr_status ozr_gemm(ozr_ctx ctx, int64_t m, int64_t n, int64_t k, const double* 
   launch_recombine_dd(planes, ps, static_cast<int>(m), static_cast<int>(n), rp, ea, eb, 8 * (kA + kB - L), C_hi, C_lo,
                       ldc, s);
   OZR_CK(cudaGetLastError(), "recombine");
-  return OZR_OK;
+  return guard_check(ctx, OZR_OK);
 }
 
 // The Hermitian extension of one sweep (R18; include/ozr.h): Algorithm 1 with
@@ -2143,7 +2177,7 @@ ozr_status ozr_refine_step_herm(ozr_ctx ctx, const double* Ar, const double* Ai,
   cudaEventElapsedTime(&ms, ctx->ev[0], ctx->ev[1]);
   rep.ms_total = ms;
   if (report) *report = rep;
-  return OZR_OK;
+  return guard_check(ctx, OZR_OK);
 }
 
 struct ozr_comm_s {
@@ -2230,7 +2264,7 @@ ozr_status ozr_refine_step_dist(ozr_ctx ctx, ozr_comm comm, const double* A, int
   if (st == OZR_OK && params->certify >= 2 && rep.n_clusters == 0)
     st = certify(ctx, comm ? comm->ex.get() : nullptr, n, params->delta, rep);
   if (report) *report = rep;
-  return st;
+  return guard_check(ctx, st);
 }
 
 // The driver (R12; the paper iterates a fixed number of times): after every sweep without
@@ -2295,7 +2329,7 @@ ozr_status ozr_refine_to_tol_dist(ozr_ctx ctx, ozr_comm comm, const double* A, i
   }
   if (result != OZR_OK && ctx->err.empty()) fail(ctx, OZR_ERR_NOT_CONVERGED, "max_sweeps reached");
   if (sweeps_done) *sweeps_done = done;
-  return result;
+  return guard_check(ctx, result);
 }
 
 ozr_status ozr_refine_step(ozr_ctx ctx, const double* A, int64_t n, int64_t lda, double* X, int64_t ldx,

@@ -378,10 +378,19 @@ __global__ void __launch_bounds__(TT, 2) k_trd_panel(PanelArgs P) {
         const int r = r0own + row;
         double y = 0.0;
         if (r < m && r >= c + 1) {
-#pragma unroll 4
-          for (int J = J0 + t4; J <= R; J += 4) y += __ldcg(P.yp + tslot(R, J) * 2 * TB + row);
-#pragma unroll 4
-          for (int I = R + 1 + t4; I < mt; I += 4) y += __ldcg(P.yp + tslot(I, R) * 2 * TB + TB + row);
+          // eight independent partial sums per thread: the L2 loads of a row's tile partials all stay in flight
+          double a8[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+          int J = J0 + t4;
+          for (; J + 28 <= R; J += 32)
+#pragma unroll
+            for (int u = 0; u < 8; ++u) a8[u] += __ldcg(P.yp + tslot(R, J + 4 * u) * 2 * TB + row);
+          for (; J <= R; J += 4) a8[0] += __ldcg(P.yp + tslot(R, J) * 2 * TB + row);
+          int I = R + 1 + t4;
+          for (; I + 28 < mt; I += 32)
+#pragma unroll
+            for (int u = 0; u < 8; ++u) a8[u] += __ldcg(P.yp + tslot(I + 4 * u, R) * 2 * TB + TB + row);
+          for (; I < mt; I += 4) a8[0] += __ldcg(P.yp + tslot(I, R) * 2 * TB + TB + row);
+          y = ((a8[0] + a8[1]) + (a8[2] + a8[3])) + ((a8[4] + a8[5]) + (a8[6] + a8[7]));
         }
         y += __shfl_xor_sync(0xffffffffu, y, 1);
         y += __shfl_xor_sync(0xffffffffu, y, 2);

@@ -1,7 +1,7 @@
 """Oracle-verified status and forward error of ozr_refine_to_tol on a BASELINE recipe at its stated size.
 
-Phase 2 (GPU box) of tools/dev/verify_prep.py: the problem is rebuilt with the numpy recipe
-(workloads.make_config) and checked against the hashes phase 1 stored; it is refined by the library with DEFAULT
+Phase 2 (GPU box) of tools/dev/verify_prep.py: the problem phase 1 stored (A, X̂₀, λ̂₀) is loaded and checked
+against the hashes phase 1 recorded; it is refined by the library with DEFAULT
 parameters (device time of the whole call, A split included), and its forward error ‖X − X̂‖₂ (and that of
 every intermediate sweep, ozr_refine_step one sweep at a time with the driver's θ schedule) is measured against
 the oracle's double-double reference eigenvectors of the stored A that phase 1 computed on the CPU (its own
@@ -25,7 +25,9 @@ ref_dir = sys.argv[1]
 with open(os.path.join(ref_dir, "meta.json")) as f:
     meta = json.load(f)
 name, n = meta["config"], meta["n"]
-An, lam0n, X0n, cfg = W.make_config(name, n=n)
+cfg = dict(W.CONFIGS[name])
+cfg["n"] = n
+An, X0n, lam0n = (np.load(os.path.join(ref_dir, f)) for f in ("A.npy", "X0.npy", "lam0.npy"))
 sha = lambda a: hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()  # noqa: E731
 assert sha(An) == meta["sha_A"] and sha(X0n) == meta["sha_X0"] and sha(lam0n) == meta["sha_lam0"], \
     "the rebuilt problem differs from the one the reference was computed for"

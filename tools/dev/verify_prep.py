@@ -42,6 +42,11 @@ res = np.sqrt(np.sum((Rh + Rl) ** 2, axis=0))
 gaps = np.array([np.min(np.abs(np.delete(lh, j) - lh[j])) for j in J])
 meta["reference_certificate"] = {"columns": J.tolist(), "residual_max": float(np.max(res)),
                                  "sin_theta_bound_max": float(np.max(res / gaps))}
+# the problem itself travels with the reference: numpy's LAPACK results depend on the thread count, so the GPU
+# box cannot rebuild A and X̂₀ bit for bit from the seed
+np.save(os.path.join(out_dir, "A.npy"), A)
+np.save(os.path.join(out_dir, "X0.npy"), X0)
+np.save(os.path.join(out_dir, "lam0.npy"), lam0)
 np.save(os.path.join(out_dir, "Xh.npy"), Xh)
 np.save(os.path.join(out_dir, "Xl.npy"), Xl.astype(np.float32))  # |Xl| ≤ u|Xh|: fp32 keeps it to 1e-23
 np.save(os.path.join(out_dir, "lh.npy"), lh)
