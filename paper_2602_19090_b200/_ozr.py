@@ -129,6 +129,11 @@ def colmajor(t):
     return t.t().contiguous().t()
 
 
+def empty_colmajor(rows, cols, dtype, device):
+    """An uninitialised column-major rows x cols tensor (no copy kernel)."""
+    return torch.empty((cols, rows), dtype=dtype, device=device).t()
+
+
 def _ld(t):
     if t.dim() != 2 or t.stride(0) != 1 or t.stride(1) < t.shape[0]:
         raise ValueError("expected a column-major 2-D tensor (stride (1, ld), ld >= rows)")
@@ -192,7 +197,7 @@ def ozr_split(ctx, M, k_or_beta, axis=OZR_COLWISE, mode=OZR_SPLIT_FIXED, M_lo=No
     kmax = 7 if mode == OZR_SPLIT_X1 else k_or_beta
     dig = torch.empty((kmax, lines, ldd), dtype=torch.int8, device=M.device)
     ell = torch.empty(lines, dtype=torch.int32, device=M.device)
-    x1 = colmajor(torch.empty((rows, cols), dtype=torch.float64, device=M.device)) if want_x1 else None
+    x1 = empty_colmajor(rows, cols, torch.float64, M.device) if want_x1 else None
     kout = ctypes.c_int(0)
     ctx.check(lib().ozr_split(ctx.h, _ptr(M), _ptr(M_lo), rows, cols, _ld(M), axis, mode, k_or_beta, _ptr(dig), ldd,
                               lines * ldd, _ptr(ell), _ptr(x1), _ld(x1) if x1 is not None else 0,
@@ -217,8 +222,8 @@ def ozr_gemm(ctx, A, B, kA, kB, L=0, want_lo=True, want_planes=False):
     if k != k2:
         raise ValueError("inner dimensions differ")
     dev = A.device
-    Ch = colmajor(torch.empty((m, n), dtype=torch.float64, device=dev))
-    Cl = colmajor(torch.empty((m, n), dtype=torch.float64, device=dev)) if want_lo else None
+    Ch = empty_colmajor(m, n, torch.float64, dev)
+    Cl = empty_colmajor(m, n, torch.float64, dev) if want_lo else None
     planes = None
     if want_planes:
         G = len(ozr_gemm_plan(k, kA, kB, L))
@@ -266,7 +271,7 @@ def ozr_syev(ctx, K):
     """θ (ascending), Y with K = Y diag(θ) Yᵀ for a symmetric column-major device matrix K (lower triangle read)."""
     m = K.shape[0]
     th = torch.empty(m, dtype=torch.float64, device=K.device)
-    Y = colmajor(torch.empty((m, m), dtype=torch.float64, device=K.device))
+    Y = empty_colmajor(m, m, torch.float64, K.device)
     ctx.check(lib().ozr_syev(ctx.h, m, _ptr(K), _ld(K), _ptr(th), _ptr(Y), m))
     return th, Y
 
@@ -284,7 +289,7 @@ def ozr_syev_tridiag_eig(ctx, d, e):
     """Stage 2 alone: θ ascending and Y for the symmetric tridiagonal (d, e)."""
     m = d.shape[0]
     th = torch.empty(m, dtype=torch.float64, device=d.device)
-    Y = colmajor(torch.empty((m, m), dtype=torch.float64, device=d.device))
+    Y = empty_colmajor(m, m, torch.float64, d.device)
     ctx.check(lib().ozr_syev_tridiag_eig(ctx.h, m, _ptr(d), _ptr(e), _ptr(th), _ptr(Y), m))
     return th, Y
 
@@ -379,6 +384,6 @@ def ozr_refine_to_tol_dist(ctx, comm, A, X, lam, params, raise_on_nonconvergence
 
 def ozr_last_R(ctx, n, n_local=None):
     """R = I − X̂^(1)ᵀX̂^(1) of the last sweep run with form_R=1 (this rank's columns), column-major."""
-    R = colmajor(torch.empty((n, n_local or n), dtype=torch.float64, device=torch.device("cuda", ctx.device)))
+    R = empty_colmajor(n, n_local or n, torch.float64, torch.device("cuda", ctx.device))
     ctx.check(lib().ozr_last_R(ctx.h, _ptr(R), n))
     return R

@@ -226,9 +226,9 @@ constexpr int kRingV = 70 * 1024, kRingE = 54 * 1024, kRingF = 70 * 1024;
 // the ring actually allocated: at least two stages of the largest layout of NG planes + NX fp64 sides + the
 // int32 side (so ts ≥ 2 always fits)
 __host__ __device__ constexpr int ring_for(int ring, int ng, int nx) {
-  return ring > 2 * ((ng * TR * 4 + nx * TR * 8 + TR * 4 + 127) / 128 * 128)
+  return ring > 2 * (((ng + 1) * TR * 4 + nx * TR * 8 + TR * 4 + 127) / 128 * 128)
              ? ring
-             : 2 * ((ng * TR * 4 + nx * TR * 8 + TR * 4 + 127) / 128 * 128);
+             : 2 * (((ng + 1) * TR * 4 + nx * TR * 8 + TR * 4 + 127) / 128 * 128);
 }
 __host__ __device__ constexpr int tma_smem(int ring) { return ring + kMaxStages * 8; }
 
@@ -255,8 +255,9 @@ __device__ __forceinline__ void for_column_x(const int32_t* __restrict__ planes,
   const int dlast = d0 + 4 * nl - 1;
   const int sc0 = 8 * (rp.L - dlast);
   const int nch = (rows + TR - 1) / TR;
-  // this column's stage layout: nact planes | NX fp64 sides | the int32 side
-  const int kSideX = nact * TR * 4, kSideI = kSideX + NX * TR * 8;
+  // this column's stage layout: nact planes | one zero plane (read for the slots nact..NG−1, branch-free) |
+  // NX fp64 sides | the int32 side
+  const int kSideX = (nact + 1) * TR * 4, kSideI = kSideX + NX * TR * 8;
   const int kStageBytes = (kSideI + (icol ? TR * 4 : 0) + 127) & ~127;
   constexpr int kRing = ring_for(RING, NG, NX);
   const int ts = max(2, min(kMaxStages, kRing / kStageBytes));  // kRing ≥ 2·kStageBytes by construction
@@ -265,9 +266,11 @@ __device__ __forceinline__ void for_column_x(const int32_t* __restrict__ planes,
     for (int st = 0; st < ts; ++st) mbar_init(&bar[st], 1);
     fence_mbar_init();
   }
+  for (int st = 0; st < ts; ++st)  // the zero planes (never written by the copies)
+    for (int r = tid; r < TR; r += BS) reinterpret_cast<int32_t*>(tsm + st * kStageBytes + nact * TR * 4)[r] = 0;
   __syncthreads();
-  auto issue = [&](int c) {
-    const int st = c % ts, r0 = c * TR, nr = min(TR, rows - r0);
+  auto issue = [&](int c, int st) {  // chunk c into stage st
+    const int r0 = c * TR, nr = min(TR, rows - r0);
     unsigned char* base = tsm + st * kStageBytes;
     const uint32_t pb = static_cast<uint32_t>(nr) * 4u, xb = static_cast<uint32_t>(nr) * 8u;
     mbar_arrive_expect_tx(&bar[st], nact * pb + NX * xb + (icol ? pb : 0u));
@@ -276,21 +279,27 @@ __device__ __forceinline__ void for_column_x(const int32_t* __restrict__ planes,
     if (icol) bulk_g2s(base + kSideI, icol + r0, pb, &bar[st]);
   };
   if (tid == 0)
-    for (int c = 0; c < ts - 1 && c < nch; ++c) issue(c);
+    for (int c = 0; c < ts - 1 && c < nch; ++c) issue(c, c);
+  int st = 0, ph = 0;  // stage and mbarrier parity of chunk c (no per-chunk division by the runtime ts)
   for (int c = 0; c < nch; ++c) {
-    if (tid == 0 && c + ts - 1 < nch) issue(c + ts - 1);  // its stage was released by the last barrier
-    mbar_wait(&bar[c % ts], (c / ts) & 1);
-    const unsigned char* base = tsm + (c % ts) * kStageBytes;
+    // chunk c + ts − 1 goes into the stage chunk c − 1 used, released by the last barrier
+    if (tid == 0 && c + ts - 1 < nch) issue(c + ts - 1, st == 0 ? ts - 1 : st - 1);
+    mbar_wait(&bar[st], ph);
+    const unsigned char* base = tsm + st * kStageBytes;
+    if (++st == ts) {
+      st = 0;
+      ph ^= 1;
+    }
 #pragma unroll
     for (int h = 0; h < RPT; ++h) {
     const int tl = tid + h * BS;  // row within the stage
     const int i = c * TR + tl;
     if (i < rows) {
-      // NG: groups compiled for this launch (4, 8 or 12 ≥ ngroups); the slots above nact read as zero (a
-      // uniform predicate per column, no branch)
+      // NG: groups compiled for this launch (4, 8 or 12 ≥ ngroups); the slots above nact read the zero plane
       int32_t cv[NG];
+      const int32_t* pl = reinterpret_cast<const int32_t*>(base) + tl;
 #pragma unroll
-      for (int g = 0; g < NG; ++g) cv[g] = (g < nact) ? reinterpret_cast<const int32_t*>(base + g * TR * 4)[tl] : 0;
+      for (int g = 0; g < NG; ++g) cv[g] = pl[min(g, nact) * TR];
       long long Lm[NG / 4];
 #pragma unroll
       for (int k = 0; k < NG / 4; ++k)
@@ -865,10 +874,30 @@ __global__ void __launch_bounds__(BS, 3)
   // pass 2: column max of |Res|, Res = V − X̂ D̂ (line 4, inner part) in double-double — Res itself is
   // formed again, identically, by the digit split (k_split_res), so it is never written here
   double m = 0.0;
-  for (int i = threadIdx.x; i < rows; i += BS) {
+  const double* vh = Vh + j * ldv;
+  const double* vl = Vl + j * ldv;
+  constexpr int U2 = 4;  // four rows per thread in flight (12 independent loads; the column was just written, L2)
+  int i = threadIdx.x;
+  for (; i + (U2 - 1) * BS < rows; i += U2 * BS) {
+    double a[U2], b[U2], c[U2];
+#pragma unroll
+    for (int u = 0; u < U2; ++u) {
+      a[u] = x1[i + u * BS];
+      b[u] = vh[i + u * BS];
+      c[u] = vl[i + u * BS];
+    }
+#pragma unroll
+    for (int u = 0; u < U2; ++u) {
+      double ph, pl;
+      two_prod(a[u], l, ph, pl);
+      const dd r = dd_add(dd{b[u], c[u]}, dd{-ph, -pl});
+      m = fmax(m, fabs(r.hi));
+    }
+  }
+  for (; i < rows; i += BS) {
     double ph, pl;
     two_prod(x1[i], l, ph, pl);
-    const dd r = dd_add(dd{Vh[j * ldv + i], Vl[j * ldv + i]}, dd{-ph, -pl});
+    const dd r = dd_add(dd{vh[i], vl[i]}, dd{-ph, -pl});
     m = fmax(m, fabs(r.hi));
   }
   m = block_max(m, sh);
@@ -998,18 +1027,21 @@ __global__ void __launch_bounds__(BS, NG <= 8 ? 3 : 2)
   }
 }
 
-__global__ void __launch_bounds__(BS, 3)
+constexpr int kRingD = 54 * 1024;
+template <int NG, int TMA>
+__global__ void __launch_bounds__(BS, NG <= 8 ? 4 : 2)
     k_recombine_dd(const int32_t* __restrict__ planes, long long pstride, int rows, const __grid_constant__ RecombPlan rp,
                    const int32_t* __restrict__ ellA, const int32_t* __restrict__ ellB, int scale8,
                    double* __restrict__ Ch, double* __restrict__ Cl, long long ldc) {
+  extern __shared__ __align__(128) unsigned char tsm[];
   const int j = blockIdx.x;
   const int Lj = rp.tile_budgets ? rp.tileL[j / 256] : rp.L;
   const int eb = ellB[j] + scale8;
-  for_column(planes, pstride, static_cast<long long>(j) * rows, rows, rp, Lj, [&](int i) { return ellA[i] + eb; },
-             [&](int i, const dd& v) {
-               Ch[j * ldc + i] = v.hi;
-               if (Cl) Cl[j * ldc + i] = v.lo;
-             });
+  for_column_x<0, false, NG, kRingD>(planes, pstride, static_cast<long long>(j) * rows, rows, rp, Lj, nullptr, ellA, TMA,
+                                     tsm, [&](int, int ea) { return ea + eb; }, [&](int i, const dd& v, const double*) {
+                                       Ch[j * ldc + i] = v.hi;
+                                       if (Cl) Cl[j * ldc + i] = v.lo;
+                                     });
 }
 
 // ---------------------------------------------------------------- power-iteration vector helpers (certify.cu, R12)
@@ -1093,6 +1125,7 @@ void init_attrs() {
     OZR_ATTR(k_recombine_V, kRingV, 1);
     OZR_ATTR(k_recombine_E, kRingE, 1);
     OZR_ATTR(k_final, kRingF, 2);
+    OZR_ATTR(k_recombine_dd, kRingD, 0);
 #undef OZR_ATTR
     return cudaPeekAtLastError();
   });
@@ -1207,7 +1240,17 @@ void launch_uf_flatten(int* parent, int n, cudaStream_t s) { k_uf_flatten<<<(n +
 void launch_recombine_dd(const int32_t* planes, long long pstride, int rows, int cols, const RecombPlan& rp,
                          const int32_t* ellA, const int32_t* ellB, int scale8, double* Ch, double* Cl, long long ldc,
                          cudaStream_t s) {
-  k_recombine_dd<<<cols, BS, 0, s>>>(planes, pstride, rows, rp, ellA, ellB, scale8, Ch, Cl, ldc);
+  init_attrs();
+  const int tma = !(no_tma_mask() & 8) && tma_ok(rp, planes, pstride, rows, nullptr, 0, nullptr, 0) &&
+                  (reinterpret_cast<uintptr_t>(ellA) & 15) == 0;
+#define OZR_RD(NG_, TMA_)                                                                                        \
+  k_recombine_dd<NG_, TMA_><<<cols, BS, TMA_ ? tma_smem(ring_for(kRingD, NG_, 0)) : 0, s>>>(planes, pstride, rows, rp, \
+                                                                                          ellA, ellB, scale8, Ch, Cl, ldc)
+  if (tma && rp.ngroups <= 4) OZR_RD(4, 1);
+  else if (tma && rp.ngroups <= 8) OZR_RD(8, 1);
+  else if (tma) OZR_RD(12, 1);
+  else OZR_RD(12, 0);
+#undef OZR_RD
 }
 
 }  // namespace ozr

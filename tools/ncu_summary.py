@@ -99,7 +99,8 @@ def algorithmic_bytes_per_element(name, sw):
     table = {"k_x1_split": 8 + 8 + kx, "k_x1_split_v": 8 + 8 + kx, "k_colmax": 8,
              "k_recombine_V": 4 * sw.get("planes_V", 0) + 8 + 16, "k_split_res": 24 + kr,
              "k_recombine_E": 4 * sw.get("planes_W", 0) + 8, "k_final": 4 * sw.get("planes_U", 0) + 8 + 8 + 8,
-             "k_transpose_i8": 2 * kx, "k_split_fixed(E')": 8 + ke}
+             "k_transpose_i8": 2 * kx, "k_transpose_i8_v": 2 * kx, "k_split_fixed(E')": 8 + ke,
+             "k_split_fixed(A)": 8 + sw.get("kA_split", 15)}
     base = name.split("<")[0].replace("void ", "").replace("unnamed>::", "").strip()
     return table.get(base)
 
@@ -107,10 +108,12 @@ def algorithmic_bytes_per_element(name, sw):
 def algorithmic_table(rep, sw, n, hbm_peak):
     out = ["| kernel | ms (ncu) | algorithmic bytes/element | algorithmic GB | algorithmic GB/s | % of HBM peak |",
            "|---|---|---|---|---|---|"]
+    seen_x1 = False
     for d, u in raw(rep):
         name = d.get("Kernel Name", "?").split("(")[0].replace("ozr::", "").replace("(anonymous namespace)::", "")
-        if "split_fixed" in name:
-            name = name.replace("k_split_fixed", "k_split_fixed(E')")
+        seen_x1 = seen_x1 or "x1_split" in name
+        if "split_fixed" in name:  # the A split (once per call) precedes the sweep's X̂ split; the Ẽ' split follows it
+            name = name.replace("k_split_fixed", "k_split_fixed(E')" if seen_x1 else "k_split_fixed(A)")
         b = algorithmic_bytes_per_element(name, sw)
         ms = num(d, u, "gpu__time_duration.sum")
         if b is None or not ms:
