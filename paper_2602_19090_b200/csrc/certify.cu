@@ -190,13 +190,9 @@ __global__ void __launch_bounds__(CB)
   if (i >= rows) return;
   const int per = (cols + PI_CHUNKS - 1) / PI_CHUNKS;
   const int j0 = blockIdx.y * per, j1 = min(cols, j0 + per);
-  double a8[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // eight loads of D in flight per thread
-  int j = j0;
-  for (; j + 8 <= j1; j += 8)
-#pragma unroll
-    for (int u = 0; u < 8; ++u) a8[u] = fma(static_cast<double>(D[static_cast<long long>(j + u) * rows + i]), z[j + u], a8[u]);
-  for (; j < j1; ++j) a8[0] = fma(static_cast<double>(D[static_cast<long long>(j) * rows + i]), z[j], a8[0]);
-  part[static_cast<long long>(blockIdx.y) * rows + i] = ((a8[0] + a8[1]) + (a8[2] + a8[3])) + ((a8[4] + a8[5]) + (a8[6] + a8[7]));
+  double acc = 0.0;
+  for (int j = j0; j < j1; ++j) acc = fma(static_cast<double>(D[static_cast<long long>(j) * rows + i]), z[j], acc);
+  part[static_cast<long long>(blockIdx.y) * rows + i] = acc;
 }
 __global__ void k_pi_sum(const double* __restrict__ part, int rows, double* __restrict__ y) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -209,13 +205,8 @@ __global__ void __launch_bounds__(CB)
     k_pi_dty(const float* __restrict__ D, int rows, const double* __restrict__ y, double* __restrict__ v) {
   __shared__ double sh[CB / 32];
   const float* c = D + static_cast<long long>(blockIdx.x) * rows;
-  double a4[4] = {0, 0, 0, 0};
-  int i = threadIdx.x;
-  for (; i + 3 * CB < rows; i += 4 * CB)
-#pragma unroll
-    for (int u = 0; u < 4; ++u) a4[u] = fma(static_cast<double>(c[i + u * CB]), y[i + u * CB], a4[u]);
-  for (; i < rows; i += CB) a4[0] = fma(static_cast<double>(c[i]), y[i], a4[0]);
-  double acc = (a4[0] + a4[1]) + (a4[2] + a4[3]);
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < rows; i += CB) acc = fma(static_cast<double>(c[i]), y[i], acc);
   acc = cb_sum(acc, sh);
   if (threadIdx.x == 0) v[blockIdx.x] = acc;
 }

@@ -230,7 +230,7 @@ __host__ __device__ constexpr int ring_for(int ring, int ng, int nx) {
              ? ring
              : 2 * (((ng + 1) * TR * 4 + nx * TR * 8 + TR * 4 + 127) / 128 * 128);
 }
-__host__ __device__ constexpr int tma_smem(int ring) { return ring + kMaxStages * 8; }
+__host__ __device__ constexpr int tma_smem(int ring) { return ring + 2 * kMaxStages * 8; }
 
 // icol (nullable): an int32 per-row vector staged beside the planes (the row exponents); e(i, icol[i]).
 template <int NX, bool HI_ONLY = false, int NG = kFastGroups, int RING = kRingV, class EF, class F>
@@ -261,9 +261,13 @@ __device__ __forceinline__ void for_column_x(const int32_t* __restrict__ planes,
   const int kStageBytes = (kSideI + (icol ? TR * 4 : 0) + 127) & ~127;
   constexpr int kRing = ring_for(RING, NG, NX);
   const int ts = max(2, min(kMaxStages, kRing / kStageBytes));  // kRing ≥ 2·kStageBytes by construction
-  uint64_t* bar = reinterpret_cast<uint64_t*>(tsm + kRing);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(tsm + kRing);  // full[st]: the stage's copies landed
+  uint64_t* ebar = bar + kMaxStages;                          // empty[st]: every warp is done with it
   if (tid == 0) {
-    for (int st = 0; st < ts; ++st) mbar_init(&bar[st], 1);
+    for (int st = 0; st < ts; ++st) {
+      mbar_init(&bar[st], 1);
+      mbar_init(&ebar[st], BS / 32);
+    }
     fence_mbar_init();
   }
   for (int st = 0; st < ts; ++st)  // the zero planes (never written by the copies)
@@ -282,10 +286,16 @@ __device__ __forceinline__ void for_column_x(const int32_t* __restrict__ planes,
     for (int c = 0; c < ts - 1 && c < nch; ++c) issue(c, c);
   int st = 0, ph = 0;  // stage and mbarrier parity of chunk c (no per-chunk division by the runtime ts)
   for (int c = 0; c < nch; ++c) {
-    // chunk c + ts − 1 goes into the stage chunk c − 1 used, released by the last barrier
-    if (tid == 0 && c + ts - 1 < nch) issue(c + ts - 1, st == 0 ? ts - 1 : st - 1);
+    // chunk c + ts − 1 goes into the stage chunk c − 1 used, once every warp has released it (its empty
+    // barrier; the other warps do not wait for one another)
+    if (tid == 0 && c + ts - 1 < nch) {
+      const int sp = st == 0 ? ts - 1 : st - 1;
+      if (c > 0) mbar_wait(&ebar[sp], st == 0 ? (ph ^ 1) : ph);
+      issue(c + ts - 1, sp);
+    }
     mbar_wait(&bar[st], ph);
     const unsigned char* base = tsm + st * kStageBytes;
+    const int st_used = st;
     if (++st == ts) {
       st = 0;
       ph ^= 1;
@@ -348,8 +358,10 @@ __device__ __forceinline__ void for_column_x(const int32_t* __restrict__ planes,
       f(i, v, xv);
     }
     }
-    __syncthreads();
+    __syncwarp();
+    if ((tid & 31) == 0) mbar_arrive(&ebar[st_used]);
   }
+  __syncthreads();  // the caller's block reductions reuse shared memory
 }
 
 // ---------------------------------------------------------------- device union-find (cluster branch)
