@@ -579,6 +579,29 @@ def main():
                   "note": "FP32 start: the first sweep's 6628-column group takes the dense sub-solve (hand-written eigensolver, syev.cu)"}
         del A4, X4, l4, Xw, lw
 
+    # the other BASELINE recipes at their stated sizes (c1 n = 100, c2 n = 1024 FP32 start, c3 n = 4096 clustered):
+    # time to target with the default parameters (second of two runs)
+    ttt_other = None
+    if not dist_mode and not args.headline_only and name == "c4p" and not args.n:
+        ttt_other = {}
+        for cname in ("c1", "c2", "c3"):
+            Ac, lc, Xc, cfgc = W.make_config_torch(cname, dev)
+            pc = ozr.default_params(delta=cfgc["delta"], max_sweeps=12)
+            for _ in range(2):
+                Xw, lw = ozr.colmajor(Xc.clone()), lc.clone()
+                torch.cuda.synchronize()
+                t0.record()
+                stc, hc = ozr.ozr_refine_to_tol(ctx, Ac, Xw, lw, pc)
+                t1.record()
+                torch.cuda.synchronize()
+            ttt_other[cname] = {"ms": t0.elapsed_time(t1), "sweeps": len(hc), "status": int(stc),
+                                "delta": cfgc["delta"], "certificate_per_sweep": [h["cert"] for h in hc],
+                                "largest_group": max(h["max_cluster"] for h in hc),
+                                "workload": cname + ": " + _describe(cfgc, cfgc["n"])}
+            del Ac, lc, Xc, Xw, lw
+        ttt_other["note"] = ("ozr_refine_to_tol, default parameters; c3 at n = 4096 and c4 at n = 4096 are verified "
+                             "against the oracle's reference in profiles/r02/verify_*.json")
+
     # the per-product Ozaki GEMM: ozr_gemm C = A·X̂₀ through the C ABI, split of both operands,
     # slice GEMM and exact recombination to double-double all inside the timed region (A's split included)
     per_product = None
@@ -682,7 +705,7 @@ def main():
                                             "max_cluster")},
                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                "gpu_launches": int(sum(r["launches"] for r in reps)), "clocks": clocks,
-               "time_to_target": ttt, "time_to_target_c4": ttt_c4, "c5_strong_scaling": c5, "hermitian": herm,
+               "time_to_target": ttt, "time_to_target_c4": ttt_c4, "time_to_target_c1_c2_c3": ttt_other, "c5_strong_scaling": c5, "hermitian": herm,
                "fixed_k_comparison": fixed_k_cmp,
                "per_product": per_product}
         emit(out)

@@ -103,6 +103,14 @@ __device__ __forceinline__ void flush_chunk(dd& acc, bool& first, i128 T, int dl
   first = false;
 }
 
+// c0·2^24 + c1·2^16 + c2·2^8 + c3 exactly (|c| < 2^31, |limb| < 2^55), as a depth-2 tree of 64-bit adds (the
+// Horner form is a dependent chain of three 64-bit multiply-adds)
+__device__ __forceinline__ long long limb4(int32_t c0, int32_t c1, int32_t c2, int32_t c3) {
+  const long long a = (static_cast<long long>(c0) << 24) + (static_cast<long long>(c1) << 16);
+  const long long b = (static_cast<long long>(c2) << 8) + static_cast<long long>(c3);
+  return a + b;
+}
+
 constexpr int kRegGroups = 24;  // plans up to this many groups keep every plane value in registers
 constexpr int kFastGroups = 12;  // consecutive-diagonal plans up to this many groups: 64-bit limb Horner
 
@@ -217,7 +225,7 @@ __device__ __forceinline__ void for_column(const int32_t* __restrict__ planes, l
 // the side-column values of row i. Requires rp.consecutive and 16-byte aligned segments (rows % 4 == 0, even
 // leading dimensions) — checked by the host (`use_tma`); else the register path.
 constexpr int RPT = 2;         // rows per thread per stage (two independent element chains per thread)
-constexpr int TR = RPT * BS;   // rows per stage
+
 constexpr int kMaxStages = 8;
 // dynamic shared memory of a TMA launch: the ring budget + the stage barriers. Per kernel (measured, n = 8192):
 // recombine_V and final 70 KB (3 CTAs per SM: V's second pass and final's element chain want the extra bytes in
@@ -225,15 +233,15 @@ constexpr int kMaxStages = 8;
 constexpr int kRingV = 70 * 1024, kRingE = 54 * 1024, kRingF = 70 * 1024;
 // the ring actually allocated: at least two stages of the largest layout of NG planes + NX fp64 sides + the
 // int32 side (so ts ≥ 2 always fits)
-__host__ __device__ constexpr int ring_for(int ring, int ng, int nx) {
-  return ring > 2 * (((ng + 1) * TR * 4 + nx * TR * 8 + TR * 4 + 127) / 128 * 128)
+__host__ __device__ constexpr int ring_for(int ring, int ng, int nx, int rpt = RPT) {
+  return ring > 2 * (((ng + 1) * rpt * BS * 4 + nx * rpt * BS * 8 + rpt * BS * 4 + 127) / 128 * 128)
              ? ring
-             : 2 * (((ng + 1) * TR * 4 + nx * TR * 8 + TR * 4 + 127) / 128 * 128);
+             : 2 * (((ng + 1) * rpt * BS * 4 + nx * rpt * BS * 8 + rpt * BS * 4 + 127) / 128 * 128);
 }
 __host__ __device__ constexpr int tma_smem(int ring) { return ring + 2 * kMaxStages * 8; }
 
 // icol (nullable): an int32 per-row vector staged beside the planes (the row exponents); e(i, icol[i]).
-template <int NX, bool HI_ONLY = false, int NG = kFastGroups, int RING = kRingV, class EF, class F>
+template <int NX, bool HI_ONLY = false, int NG = kFastGroups, int RING = kRingV, int RPTT = RPT, class EF, class F>
 __device__ __forceinline__ void for_column_x(const int32_t* __restrict__ planes, long long pstride, long long coloff,
                                              int rows, const RecombPlan& rp, int Lj, const double* const* xcol,
                                              const int32_t* __restrict__ icol, int use_tma, unsigned char* tsm, EF e,
@@ -248,18 +256,19 @@ __device__ __forceinline__ void for_column_x(const int32_t* __restrict__ planes,
                });
     return;
   }
+  constexpr int TRL = RPTT * BS;  // rows per stage
   const int tid = threadIdx.x;
   const int d0 = rp.diag[0];
   const int nact = max(0, min(rp.ngroups, Lj - d0 + 1));
   const int nl = (rp.ngroups + 3) >> 2;
   const int dlast = d0 + 4 * nl - 1;
   const int sc0 = 8 * (rp.L - dlast);
-  const int nch = (rows + TR - 1) / TR;
+  const int nch = (rows + TRL - 1) / TRL;
   // this column's stage layout: nact planes | one zero plane (read for the slots nact..NG−1, branch-free) |
   // NX fp64 sides | the int32 side
-  const int kSideX = (nact + 1) * TR * 4, kSideI = kSideX + NX * TR * 8;
-  const int kStageBytes = (kSideI + (icol ? TR * 4 : 0) + 127) & ~127;
-  constexpr int kRing = ring_for(RING, NG, NX);
+  const int kSideX = (nact + 1) * TRL * 4, kSideI = kSideX + NX * TRL * 8;
+  const int kStageBytes = (kSideI + (icol ? TRL * 4 : 0) + 127) & ~127;
+  constexpr int kRing = ring_for(RING, NG, NX, RPTT);
   const int ts = max(2, min(kMaxStages, kRing / kStageBytes));  // kRing ≥ 2·kStageBytes by construction
   uint64_t* bar = reinterpret_cast<uint64_t*>(tsm + kRing);  // full[st]: the stage's copies landed
   uint64_t* ebar = bar + kMaxStages;                          // empty[st]: every warp is done with it
@@ -271,15 +280,15 @@ __device__ __forceinline__ void for_column_x(const int32_t* __restrict__ planes,
     fence_mbar_init();
   }
   for (int st = 0; st < ts; ++st)  // the zero planes (never written by the copies)
-    for (int r = tid; r < TR; r += BS) reinterpret_cast<int32_t*>(tsm + st * kStageBytes + nact * TR * 4)[r] = 0;
+    for (int r = tid; r < TRL; r += BS) reinterpret_cast<int32_t*>(tsm + st * kStageBytes + nact * TRL * 4)[r] = 0;
   __syncthreads();
   auto issue = [&](int c, int st) {  // chunk c into stage st
-    const int r0 = c * TR, nr = min(TR, rows - r0);
+    const int r0 = c * TRL, nr = min(TRL, rows - r0);
     unsigned char* base = tsm + st * kStageBytes;
     const uint32_t pb = static_cast<uint32_t>(nr) * 4u, xb = static_cast<uint32_t>(nr) * 8u;
     mbar_arrive_expect_tx(&bar[st], nact * pb + NX * xb + (icol ? pb : 0u));
-    for (int g = 0; g < nact; ++g) bulk_g2s(base + g * TR * 4, planes + g * pstride + coloff + r0, pb, &bar[st]);
-    for (int x = 0; x < NX; ++x) bulk_g2s(base + kSideX + x * TR * 8, xcol[x] + r0, xb, &bar[st]);
+    for (int g = 0; g < nact; ++g) bulk_g2s(base + g * TRL * 4, planes + g * pstride + coloff + r0, pb, &bar[st]);
+    for (int x = 0; x < NX; ++x) bulk_g2s(base + kSideX + x * TRL * 8, xcol[x] + r0, xb, &bar[st]);
     if (icol) bulk_g2s(base + kSideI, icol + r0, pb, &bar[st]);
   };
   if (tid == 0)
@@ -301,19 +310,19 @@ __device__ __forceinline__ void for_column_x(const int32_t* __restrict__ planes,
       ph ^= 1;
     }
 #pragma unroll
-    for (int h = 0; h < RPT; ++h) {
+    for (int h = 0; h < RPTT; ++h) {
     const int tl = tid + h * BS;  // row within the stage
-    const int i = c * TR + tl;
+    const int i = c * TRL + tl;
     if (i < rows) {
       // NG: groups compiled for this launch (4, 8 or 12 ≥ ngroups); the slots above nact read the zero plane
       int32_t cv[NG];
       const int32_t* pl = reinterpret_cast<const int32_t*>(base) + tl;
 #pragma unroll
-      for (int g = 0; g < NG; ++g) cv[g] = pl[min(g, nact) * TR];
+      for (int g = 0; g < NG; ++g) cv[g] = pl[min(g, nact) * TRL];
       long long Lm[NG / 4];
 #pragma unroll
       for (int k = 0; k < NG / 4; ++k)
-        Lm[k] = ((static_cast<long long>(cv[4 * k]) * 256 + cv[4 * k + 1]) * 256 + cv[4 * k + 2]) * 256 + cv[4 * k + 3];
+        Lm[k] = limb4(cv[4 * k], cv[4 * k + 1], cv[4 * k + 2], cv[4 * k + 3]);
       dd v{0.0, 0.0};
       const int ee = e(i, icol ? reinterpret_cast<const int32_t*>(base + kSideI)[tl] : 0);
       if (HI_ONLY && NG <= 8) {  // RN(value) from the one or two limbs, without 128-bit arithmetic
@@ -354,7 +363,7 @@ __device__ __forceinline__ void for_column_x(const int32_t* __restrict__ planes,
       }
       double xv[NX > 0 ? NX : 1];
 #pragma unroll
-      for (int x = 0; x < NX; ++x) xv[x] = reinterpret_cast<const double*>(base + kSideX + x * TR * 8)[tl];
+      for (int x = 0; x < NX; ++x) xv[x] = reinterpret_cast<const double*>(base + kSideX + x * TRL * 8)[tl];
       f(i, v, xv);
     }
     }

@@ -919,7 +919,9 @@ int syev_trd_grid(int m) {
   const int mt = (m + TB - 1) / TB;
   // one CTA per row block at least (each owns one); more for the tile products (~mt²/2 tiles), bounded by
   // co-residency; fewer CTAs = cheaper barriers
-  int want = std::max(mt, std::min(mt * (mt + 1) / 2, 5 * mt));
+  // (measured, tools/dev/syev_time.py: m = 2734 tridiagonalisation 56.6 ms at 3·mt CTAs, 64.3 at 5·mt, 66.6 at
+  // 2·mt; m = 739 within 4 %; m = 6628 at the co-residency cap either way)
+  int want = std::max(mt, std::min(mt * (mt + 1) / 2, 3 * mt));
   if (const char* g = getenv("OZR_SYEV_G")) want = std::max(mt, std::min(mt * (mt + 1) / 2, atoi(g) * mt / 8));  // A/B: G = g/8 · mt
   return std::min(want, nsm * per);
 }
@@ -935,11 +937,19 @@ cudaError_t syev_tridiag(double* A, int m, double* d, double* e, double* tau, do
   const int mt = (m + TB - 1) / TB;
   if (G < mt) return cudaErrorInvalidConfiguration;  // every row block needs its owner CTA (m ≤ ~28000)
   double* yp = part + static_cast<size_t>(G) * (5 + 2 * NB);
+  // OZR_SYEV_GDIV = d (A/B only): CTAs per panel from the panel's trailing size, clamp(m'/d, mt, G) — measured
+  // no better than the fixed G (m = 2734: 77-85 ms for d = 12..28 against 73 ms fixed)
+  static int gfac = -1;
+  if (gfac < 0) {
+    const char* f = getenv("OZR_SYEV_GDIV");  // A/B: G_panel = m'/GDIV (0: the fixed G)
+    gfac = f ? atoi(f) : 0;
+  }
   for (int k0 = 0; k0 < m; k0 += NB) {
     const int nb = std::min(NB, m - k0);
+    const int Gk = gfac > 0 ? std::max(mt, std::min(G, (m - k0) / gfac)) : G;
     PanelArgs P{A, m, k0, nb, V, W, d, e, tau, part, yp, part + syev_trd_partials(m, G), dbg};
     void* args[] = {&P};
-    cudaError_t err = cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_trd_panel), dim3(G), dim3(TT), args,
+    cudaError_t err = cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_trd_panel), dim3(Gk), dim3(TT), args,
                                                   sizeof(PanelSmem), s);
     if (err != cudaSuccess) return err;
     const int k1 = k0 + nb;
