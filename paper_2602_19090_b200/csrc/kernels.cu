@@ -930,8 +930,8 @@ __global__ void __launch_bounds__(BS, 3)
   }
 }
 
-template <int NG, int TMA>
-__global__ void __launch_bounds__(BS, NG <= 8 ? 4 : 2)
+template <int NG, int TMA, int RPTE = RPT>
+__global__ void __launch_bounds__(BS, NG <= 8 ? (RPTE == 4 ? 2 : 4) : 2)
     k_recombine_E(const int32_t* __restrict__ planes, long long pstride, int rows, const __grid_constant__ RecombPlan rp,
                   const int32_t* __restrict__ ellA, const int32_t* __restrict__ ellB, int scale8,
                   const double* __restrict__ r_hi, const double* __restrict__ lam, const int32_t* __restrict__ gX,
@@ -953,7 +953,7 @@ __global__ void __launch_bounds__(BS, NG <= 8 ? 4 : 2)
   // the row exponent of the row operand X̂^(1)ᵀ is g_i (ellA == gX): it scales Ẽ' = diag(2^g)Ẽ too, so the
   // staged value is kept for the element (the exponent functor runs right before the element functor)
   int gcur = 0;
-  for_column_x<1, true, NG, kRingE>(planes, pstride, static_cast<long long>(j) * rows, rows, rp, Lj, xc, ellA, TMA, tsm,
+  for_column_x<1, true, NG, kRingE, RPTE>(planes, pstride, static_cast<long long>(j) * rows, rows, rp, Lj, xc, ellA, TMA, tsm,
                             [&](int, int gi) { gcur = gi; return gi + eb; }, [&](int i, const dd& wv, const double* xv) {
     double e;
     w2 = __fma_rn(wv.hi, wv.hi, w2);
@@ -1145,6 +1145,9 @@ void init_attrs() {
   cudaFuncSetAttribute(K<12, 0>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     OZR_ATTR(k_recombine_V, kRingV, 1);
     OZR_ATTR(k_recombine_E, kRingE, 1);
+    cudaFuncSetAttribute(k_recombine_E<8, 1, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         tma_smem(ring_for(kRingE, 8, 1, 4)));
+    cudaFuncSetAttribute(k_recombine_E<8, 1, 4>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     OZR_ATTR(k_final, kRingF, 2);
     OZR_ATTR(k_recombine_dd, kRingD, 0);
 #undef OZR_ATTR
@@ -1217,13 +1220,19 @@ void launch_recombine_E(const int32_t* planes, long long pstride, int rows, int 
   }
   const int tma = allow_tma && !(no_tma_mask() & 2) && tma_ok(rp, planes, pstride, rows, lam, 0, nullptr, 0) &&
                   (reinterpret_cast<uintptr_t>(ellA) & 15) == 0;
-#define OZR_RE(NG_, TMA_)                                                                                            \
-  k_recombine_E<NG_, TMA_><<<cols, BS, TMA_ ? tma_smem(ring_for(kRingE, NG_, 1)) : 0, s>>>(planes, pstride, rows, rp, ellA, ellB, scale8, r_hi, lam, gX, \
+#define OZR_RE(NG_, TMA_, R_)                                                                                            \
+  k_recombine_E<NG_, TMA_, R_><<<cols, BS, TMA_ ? tma_smem(ring_for(kRingE, NG_, 1, R_)) : 0, s>>>(planes, pstride, rows, rp, ellA, ellB, scale8, r_hi, lam, gX, \
                                                           col0, Ep, lde, nrm2, eE_max, eE_col, err, eo, tma, nW2)
-  if (tma && rp.ngroups <= 4) OZR_RE(4, 1);
-  else if (tma && rp.ngroups <= 8) OZR_RE(8, 1);
-  else if (tma) OZR_RE(12, 1);
-  else OZR_RE(12, 0);
+  static int erpt = -1;  // OZR_E_RPT=4 (A/B only): four rows per thread per stage
+  if (erpt < 0) {
+    const char* e = getenv("OZR_E_RPT");
+    erpt = (e && atoi(e) == 4) ? 4 : 2;
+  }
+  if (tma && rp.ngroups <= 8 && erpt == 4) OZR_RE(8, 1, 4);
+  else if (tma && rp.ngroups <= 4) OZR_RE(4, 1, RPT);
+  else if (tma && rp.ngroups <= 8) OZR_RE(8, 1, RPT);
+  else if (tma) OZR_RE(12, 1, RPT);
+  else OZR_RE(12, 0, RPT);
 #undef OZR_RE
 }
 void launch_final(const int32_t* planes, long long pstride, int rows, int cols, const RecombPlan& rp,
