@@ -293,9 +293,14 @@ def run_c5(ctx, comm, dist_mode, ws, rank, dev, W, ozr, torch, dist, steps=2, wa
     del A, X0, X, lam0, lam
     torch.cuda.empty_cache()
     r = reps[-1]
+    # the slice GEMM's rate in these sweeps against the SUSTAINED peak (the c5 products run long enough for the
+    # power limiter to settle: DESIGN.md §6)
+    peaks, _ = _peaks()
+    gemm_tops = sum(x["int8_ops"] for x in reps) / (sum(x["ms_gemm"] for x in reps) / 1e3) / 1e12
     return {"workload": "c5: " + _describe(cfg, n), "n": n, "n_gpus": ws, "steps": steps, "warmup": warmup,
             "ms_per_sweep": ms, "value": 6.0 * n ** 3 / (ms / 1e3) / 1e12, "unit": "TFLOP/s",
             "scaling": "strong", "pair_gemms": r["pairs_V"] + r["pairs_W"] + r["pairs_U"],
+            "gemm_tops": gemm_tops, "gemm_frac_of_sustained_peak": gemm_tops / (2.0 * peaks["bf16_tflops_sustained"]),
             "note": "one refinement sweep of the whole n = 16384 problem, block columns over the ranks "
                     "(NCCL all-gather of the X^(1) digit planes per sweep); device time, max over ranks"}
 
@@ -573,8 +578,13 @@ def main():
             st4, h4 = ozr.ozr_refine_to_tol(ctx, A4, Xw, lw, p4)
             t1.record()
             torch.cuda.synchronize()
+        steady = [h for h in h4 if h["max_cluster"] == 0]
         ttt_c4 = {"ms": t0.elapsed_time(t1), "sweeps": len(h4), "status": int(st4), "delta": cfg4["delta"],
                   "largest_group": max(h["max_cluster"] for h in h4),
+                  "ms_per_sweep": [h["ms_total"] for h in h4],
+                  # the sweeps without unresolved groups (the truncated iteration proper): effective FP64 rate
+                  "steady_state_value": (6.0 * cfg4["n"] ** 3 / (np.mean([h["ms_total"] for h in steady]) / 1e3) / 1e12
+                                         if steady else None), "unit": "TFLOP/s",
                   "workload": "c4: " + _describe(cfg4, cfg4["n"]),
                   "note": "FP32 start: the first sweep's 6628-column group takes the dense sub-solve (hand-written eigensolver, syev.cu)"}
         del A4, X4, l4, Xw, lw

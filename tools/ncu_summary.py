@@ -126,7 +126,15 @@ def algorithmic_table(rep, sw, n, hbm_peak):
 
 if __name__ == "__main__":
     d = sys.argv[1] if len(sys.argv) > 1 else "gpurun_out"
-    peak = float(sys.argv[sys.argv.index("--hbm-peak") + 1]) if "--hbm-peak" in sys.argv else 6533.8
+    peak = 6533.8  # fallback: the round-1 measured copy peak
+    try:
+        import json
+        import os
+        peak = json.load(open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "MEASURED_PEAKS.json")))["hbm_gbs"]
+    except Exception:
+        pass
+    if "--hbm-peak" in sys.argv:
+        peak = float(sys.argv[sys.argv.index("--hbm-peak") + 1])
     t, _ = launch_table(f"{d}/launches.csv")
     print("## Launch list\n\n" + t + "\n")
     if "--bench" in sys.argv:  # algorithmic bytes from the bench line's sweep plan (n x n launches, 1 GPU)
