@@ -526,17 +526,19 @@ def main():
                 "gemm_share_of_step": gemm_ms / ms,
                 "library_sweep_ms": sum(r["ms_total"] for r in reps) / len(reps)}
 
-    # time to target: ozr_refine_to_tol from X̂0 (self-certified stop rule)
-    X.copy_(X0)
-    lam.copy_(lam0)
-    torch.cuda.synchronize()
+    # time to target: ozr_refine_to_tol from X̂0 (self-certified stop rule); the second of two calls is timed (the
+    # first grows the context's certificate workspace — cudaMalloc of its bf16 operands is not part of a sweep)
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
-    t0.record()
-    st, hist = ozr.ozr_refine_to_tol_dist(ctx, comm, A, X, lam,
-                                          ozr.default_params(delta=delta, max_sweeps=6, truncate=args.truncate))
-    t1.record()
-    torch.cuda.synchronize()
+    for _ in range(2):
+        X.copy_(X0)
+        lam.copy_(lam0)
+        torch.cuda.synchronize()
+        t0.record()
+        st, hist = ozr.ozr_refine_to_tol_dist(ctx, comm, A, X, lam,
+                                              ozr.default_params(delta=delta, max_sweeps=6, truncate=args.truncate))
+        t1.record()
+        torch.cuda.synchronize()
     ttt = {"ms": t0.elapsed_time(t1), "sweeps": len(hist), "status": int(st), "delta": delta,
            "certificate_per_sweep": [h["cert"] for h in hist],
            "pair_gemms": sum(h["pairs_V"] + h["pairs_W"] + h["pairs_U"] for h in hist),

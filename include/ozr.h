@@ -223,7 +223,7 @@ ozr_status ozr_last_clusters(ozr_ctx ctx, int* members, int max_members, int* of
 /* Repeat sweeps until the returned X̂ is certified (R12; the paper iterates a fixed number of times,
  * PAPER.md:536-540): after every sweep without unresolved groups, the a-posteriori estimate report.cert of
  * ‖X − X̂‖₂ (the 2-norm of PAPER.md:121) is formed from the sweep's own Ẽ — the second-order defect of Alg. 1's
- * correction, one bf16 tensor-core product Q = ẼᵀC and a power iteration — and the call returns OZR_OK with
+ * correction, two bf16 tensor-core products (Q = ẼᵀC, Ẽ²) and Golub–Kahan–Lanczos — and the call returns OZR_OK with
  * that X̂ once cert·1.15 ≤ δ. An estimate that stalls above δ (the truncated iteration's floor, quadratic in
  * 2^-β) escalates θ ← θ·4^m up to max_escalations times, then OZR_ERR_NOT_CONVERGED, as does
  * reaching max_sweeps — X / lambda then hold the last completed sweep. Sweeps with unresolved groups (cluster
