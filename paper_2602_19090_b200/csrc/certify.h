@@ -1,6 +1,7 @@
 // certify.h — launchers of the a-posteriori forward-error certificate (certify.cu, R12). Internal.
 #pragma once
 #include <cstdint>
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
 namespace ozr {
@@ -18,11 +19,11 @@ void launch_cert_rowT(const void* Eb, long long ldb, int rows, int cols, const i
 // − 2^{rE_i + sE_j}·P_ij, D_jj = −2^{rE_j + sE_j}·P_jj − ½esq_j (Q = ẼᵀC, P = Ẽ·Ẽ_{:,J}, ld = ldq);
 // dsq[j] = Σ_i D_ij²; *flag |= 1 when two estimates are equal (no certificate).
 void launch_cert_delta(const float* Q, const float* P, long long ldq, int rows, int cols, const int32_t* sE,
-                       const int32_t* sC, const int32_t* rE, const double* esq, const double* lam, int col0, float* D,
+                       const int32_t* sC, const int32_t* rE, const double* esq, const double* lam, int col0, __nv_bfloat16* D,
                        double* dsq, int* flag, cudaStream_t s);
 // y = D·z (part: cert_pi_chunks()·rows doubles of scratch); v = Dᵀ·y
-void launch_pi_dz(const float* D, int rows, int cols, const double* z, double* part, double* y, cudaStream_t s);
-void launch_pi_dty(const float* D, int rows, int cols, const double* y, double* v, cudaStream_t s);
+void launch_pi_dz(const __nv_bfloat16* D, int rows, int cols, const double* z, double* part, double* y, cudaStream_t s);
+void launch_pi_dty(const __nv_bfloat16* D, int rows, int cols, const double* y, double* v, cudaStream_t s);
 int cert_pi_chunks();
 // x = y − sqrt(c2[0])·x
 void launch_lz_axpy(double* x, const double* y, int n, const double* c2, cudaStream_t s);

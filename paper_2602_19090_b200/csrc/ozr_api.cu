@@ -1533,8 +1533,9 @@ ozr_status certify(ozr_ctx ctx, Exchange* ex, int64_t n, double delta, ozr_step_
   double* dsq = ctx->ws<double>(S_CDSQ, n);
   int* flag = ctx->ws<int>(S_CFLG, 4);
   float* Q = reinterpret_cast<float*>(ctx->ws<int32_t>(S_PLANES, nnl));  // the slice planes are dead by now
-  float* D = reinterpret_cast<float*>(ctx->ws<double>(S_VH, nnl));      // so is V (2·nnl floats: D, then P)
-  float* Pm = D + nnl;
+  float* Dw = reinterpret_cast<float*>(ctx->ws<double>(S_VH, nnl));     // so is V (2·nnl floats: D (bf16), then P)
+  __nv_bfloat16* D = reinterpret_cast<__nv_bfloat16*>(Dw);
+  float* Pm = Dw + nnl;
   int* cnt = ctx->ws<int>(S_GCNT, 4);
   double* z = ctx->ws<double>(S_PI_Z, nl);
   double* v = ctx->ws<double>(S_PI_V, nl);
@@ -1542,7 +1543,7 @@ ozr_status certify(ozr_ctx ctx, Exchange* ex, int64_t n, double delta, ozr_step_
   double* part = ctx->ws<double>(S_PI_P, static_cast<size_t>(cert_pi_chunks()) * n);
   double* sc = ctx->ws<double>(S_PI_S, 2);
   OZR_ALLOC(Eb); OZR_ALLOC(EbT); OZR_ALLOC(Cb); OZR_ALLOC(sE); OZR_ALLOC(sC); OZR_ALLOC(rE); OZR_ALLOC(esq);
-  OZR_ALLOC(dsq); OZR_ALLOC(flag); OZR_ALLOC(Q); OZR_ALLOC(D); OZR_ALLOC(cnt); OZR_ALLOC(z); OZR_ALLOC(v); OZR_ALLOC(y);
+  OZR_ALLOC(dsq); OZR_ALLOC(flag); OZR_ALLOC(Q); OZR_ALLOC(Dw); OZR_ALLOC(cnt); OZR_ALLOC(z); OZR_ALLOC(v); OZR_ALLOC(y);
   OZR_ALLOC(part); OZR_ALLOC(sc);
   auto gather = [&](void* base, size_t bytes) -> ozr_status {
     if (ex && !ex->allgather(base, bytes, s)) return fail(ctx, OZR_ERR_COMM, "all-gather: %s", ex->err.c_str());
