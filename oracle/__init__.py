@@ -17,6 +17,8 @@ Modules
   products  same-definition slice products (exact integer planes) and their exact recombination
   refine    Algorithm 1 (§2.4) with the one-sided product (§3.3), the driver, reference
             eigenvectors and forward error
+  hermitian the Hermitian extension of Algorithm 1 (R18): complex products as their
+            definition in double-double, the truncation on both parts, forward error with phase alignment
   _clib     ctypes loader for ddmm.c (double-double GEMM, __float128 Jacobi)
 
 Parity status: every function is pinned by a ``-m "not gpu"`` test in tests/test_oracle_*.py (closed forms,
