@@ -872,7 +872,8 @@ __global__ void __launch_bounds__(BS, 3)
                   const int32_t* __restrict__ ellA, const int32_t* __restrict__ ellB, int scale8,
                   const double* __restrict__ X1, long long ldx1, const double* __restrict__ s_hi,
                   const double* __restrict__ s_lo, double* __restrict__ Vh, double* __restrict__ Vl, long long ldv,
-                  double* __restrict__ lam_out, int32_t* __restrict__ eR, int* __restrict__ eR_max, int use_tma) {
+                  double* __restrict__ lam_out, int32_t* __restrict__ eR, int* __restrict__ eR_max, int use_tma,
+                  const double* __restrict__ lam0) {
   extern __shared__ __align__(128) unsigned char tsm[];
   __shared__ double sh[2 * BS / 32];
   const int j = blockIdx.x;
@@ -880,7 +881,11 @@ __global__ void __launch_bounds__(BS, 3)
   const int eb = ellB[j] + scale8;
   const double* x1 = X1 + j * ldx1;
   dd t{0.0, 0.0};
-  // pass 1: V (Alg. 1 line 1) and x̂_jᵀ v_j (line 3)
+  // pass 1: V (Alg. 1 line 1) and x̂_jᵀ v_j (line 3). Beside them, the residual against the PREVIOUS estimate
+  // λ0 (lam0, the sweep's input λ̂): m0 = max_i |RN(v_i − x̂_i λ0)|, with max |x̂_i| and max |v_i| — enough to
+  // enclose the exact column max of |Res| for the new λ̂ (below) without reading the column a second time
+  const double l0 = lam0 ? lam0[j] : 0.0;
+  double m0 = 0.0, xm = 0.0, vm = 0.0;
   const double* xc[1] = {x1};
   for_column_x<1, false, NG, kRingV>(planes, pstride, static_cast<long long>(j) * rows, rows, rp, Lj, xc, ellA, TMA, tsm,
                   [&](int, int ea) { return ea + eb; },
@@ -888,10 +893,34 @@ __global__ void __launch_bounds__(BS, 3)
                     Vh[j * ldv + i] = v.hi;
                     Vl[j * ldv + i] = v.lo;
                     t = dd_add(t, dd_mul_d(v, xv[0]));
+                    m0 = fmax(m0, fabs(__fma_rn(-xv[0], l0, v.hi) + v.lo));
+                    xm = fmax(xm, fabs(xv[0]));
+                    vm = fmax(vm, fabs(v.hi));
                   });
   t = block_sum_dd(t, sh);
   const dd lam = dd_div(t, dd{s_hi[j], s_lo[j]});  // λ̂_j = x̂_jᵀv̂_j / (1 − r_j)
   const double l = lam.hi;
+  // The split (k_split_res, R6) needs e = ⌈log2 m⌉, m = max_i |hi(dd_add(v_i, −TwoProd(x̂_i, λ̂)))|. Each such
+  // hi is within 2^-52|ρ_i| + 2^-104(|v_i| + |x̂_i λ̂|) of the exact ρ_i(λ̂) = v_i − x̂_i λ̂; pass 1's value
+  // RN(RN(v_hi − x̂λ0) + v_lo) is within 2^-51|ρ_i(λ0)| + 2^-105|v_i| of ρ_i(λ0); and
+  // |ρ_i(λ̂) − ρ_i(λ0)| ≤ |x̂_i||λ̂ − λ0|. So m ∈ [lo, hi] below (constants rounded generously outward);
+  // when ⌈log2⌉ agrees at both ends e is decided exactly, else (and without λ0) pass 2 computes m itself.
+  m0 = block_max(m0, sh);
+  xm = block_max(xm, sh);
+  vm = block_max(vm, sh);
+  const double dlt = xm * fabs(l - l0) * (1.0 + 0x1p-48);
+  const double sl = 0x1p-96 * (vm + xm * (fabs(l) + fabs(l0)));
+  const double mlo = (m0 * (1.0 - 0x1p-48) - dlt) * (1.0 - 0x1p-48) - sl;
+  const double mhi = (m0 * (1.0 + 0x1p-48) + dlt) * (1.0 + 0x1p-48) + sl;
+  if (lam0 && mlo > 0.0 && ceil_log2_d(mlo) == ceil_log2_d(mhi)) {
+    if (threadIdx.x == 0) {
+      lam_out[j] = l;
+      const int e = ceil_log2_d(mhi);
+      eR[j] = e;
+      atomicMax(eR_max, e);
+    }
+    return;
+  }
   // pass 2: column max of |Res|, Res = V − X̂ D̂ (line 4, inner part) in double-double — Res itself is
   // formed again, identically, by the digit split (k_split_res), so it is never written here
   double m = 0.0;
@@ -1194,12 +1223,16 @@ void launch_transpose_f64(const double* src, long long lds, double* dst, long lo
 void launch_recombine_V(const int32_t* planes, long long pstride, int rows, int cols, const RecombPlan& rp,
                         const int32_t* ellA, const int32_t* ellB, int scale8, const double* X1, long long ldx1,
                         const double* s_hi, const double* s_lo, double* Vh, double* Vl, long long ldv,
-                        double* lam_out, int32_t* eR, int* eR_max, cudaStream_t s, int allow_tma) {
+                        double* lam_out, int32_t* eR, int* eR_max, cudaStream_t s, int allow_tma,
+                        const double* lam0) {
   init_attrs();
   const int tma = allow_tma && !(no_tma_mask() & 1) && tma_ok(rp, planes, pstride, rows, X1, ldx1, X1, ldx1) && (reinterpret_cast<uintptr_t>(ellA) & 15) == 0;
+  // OZR_RES_2PASS=1 (A/B and the bit-identity test): always re-read the column for the Res exponent
+  if (const char* e2 = getenv("OZR_RES_2PASS"))
+    if (e2[0] == '1') lam0 = nullptr;
 #define OZR_RV(NG_, TMA_)                                                                                          \
   k_recombine_V<NG_, TMA_><<<cols, BS, TMA_ ? tma_smem(ring_for(kRingV, NG_, 1)) : 0, s>>>(planes, pstride, rows, rp, ellA, ellB, scale8, X1, ldx1, s_hi, \
-                                                          s_lo, Vh, Vl, ldv, lam_out, eR, eR_max, tma)
+                                                          s_lo, Vh, Vl, ldv, lam_out, eR, eR_max, tma, lam0)
   if (tma && rp.ngroups <= 4) OZR_RV(4, 1);
   else if (tma && rp.ngroups <= 8) OZR_RV(8, 1);
   else if (tma) OZR_RV(12, 1);

@@ -44,7 +44,8 @@ void launch_transpose_f64(const double* src, long long lds, double* dst, long lo
 void launch_recombine_V(const int32_t* planes, long long pstride, int rows, int cols, const RecombPlan& rp,
                         const int32_t* ellA, const int32_t* ellB, int scale8, const double* X1, long long ldx1,
                         const double* s_hi, const double* s_lo, double* Vh, double* Vl, long long ldv,
-                        double* lam_out, int32_t* eR, int* eR_max, cudaStream_t s, int allow_tma = 1);
+                        double* lam_out, int32_t* eR, int* eR_max, cudaStream_t s, int allow_tma = 1,
+                        const double* lam0 = nullptr);
 // Unresolved pairs of k_recombine_E (cluster branch, R13): every pair (i, j), i ≠ j, with
 // λ̂_i = λ̂_j or |ẽ_ij| > κ is united in the device union-find `parent` (O(n) memory, any number of
 // pairs; the resulting partition is independent of the order of the unions), and *any is set.

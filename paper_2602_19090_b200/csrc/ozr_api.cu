@@ -1019,7 +1019,7 @@ ozr_status sweep(ozr_ctx ctx, Exchange* ex, const double* A, int64_t n, int64_t 
       [&](int64_t c0, int64_t c1, int t0, int tma, cudaStream_t q) {
         launch_recombine_V(planes + c0 * n, nnl, N, static_cast<int>(c1 - c0), shift_plan(rp, t0), aell,
                            g + col0 + c0, scaleV, X1 + c0 * n, n, sh + c0, sl + c0, Vh + c0 * n, Vl + c0 * n, n,
-                           lam + col0 + c0, eR + c0, demax, q, tma);
+                           lam + col0 + c0, eR + c0, demax, q, tma, lambda + col0 + c0);
       },
       [&](cudaStream_t q) {
         // the digit transpose (A operand of X̂Ẽ) needs every column's digits: after the exchange on P ranks

@@ -179,3 +179,23 @@ def test_tensor_core_gram_bit_identical(ctx, cfg, n, start, dense, monkeypatch):
     assert out[0][2]["max_cluster"] >= dense
     assert np.array_equal(out[0][0], out[1][0]) and np.array_equal(out[0][1], out[1][1])
     assert out[0][2]["launches"] > out[1][2]["launches"]
+
+
+@pytest.mark.parametrize("cfg,n,start", [("c4p", 1024, "fp64"), ("c3", 1024, "fp64"), ("c2", 512, "fp32"),
+                                         ("c1", 100, "fp64")])
+def test_res_exponent_single_pass_bit_identical(ctx, cfg, n, start, monkeypatch):
+    """k_recombine_V decides the Res column exponent e = ⌈log2 max|Res|⌉ (R6) from an enclosure built in its
+    first pass (the residual against the previous λ̂ plus |x̂|·|λ̂ − λ0|) and re-reads the column only when the
+    enclosure straddles a power of two: the sweep is bit-identical to the always-two-pass form
+    (OZR_RES_2PASS=1) over two consecutive sweeps."""
+    import paper_2602_19090_b200 as ozr
+    A, lam0, X0 = _case(cfg, n, start)
+    p = ozr.default_params(delta=1e-12)
+    out = []
+    for flag in ("0", "1"):
+        monkeypatch.setenv("OZR_RES_2PASS", flag)
+        Xd, ld, Ad = to_dev(X0), vec_dev(lam0), to_dev(A)
+        for _ in range(2):
+            ozr.ozr_refine_step(ctx, Ad, Xd, ld, p)
+        out.append((to_np(Xd), to_np(ld)))
+    assert np.array_equal(out[0][0], out[1][0]) and np.array_equal(out[0][1], out[1][1])
