@@ -391,7 +391,7 @@ def main():
     ap.add_argument("--ref-cols", type=int, default=16)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-c4", action="store_true", help="skip the BASELINE c4 time-to-target line")
-    ap.add_argument("--e2e-steps", type=int, default=16)
+    ap.add_argument("--e2e-steps", type=int, default=32)
     ap.add_argument("--truncate", type=int, default=1,
                     help="1: the paper's X̂ → X̂^(1) truncation (default); 0: keep all of X̂ — the untruncated "
                          "two-sided analogue of the prior work the paper compares against (PAPER.md:432-443)")

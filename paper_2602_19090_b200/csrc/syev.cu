@@ -17,6 +17,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -903,6 +904,250 @@ __global__ void k_sub_strided(double* __restrict__ Y, int ldy, const double* __r
     Y[r + static_cast<long long>(j) * ldy] -= P[r + static_cast<long long>(j) * ldp];
 }
 
+// ---------------------------------------------------------------- (1b) the trailing matrix in one thread-block cluster
+// Once the trailing matrix A(k0:m, k0:m) fits in the distributed shared memory of one cluster of CS CTAs, the rest
+// of the tridiagonalisation runs unblocked (LAPACK dsytd2 order: reflector of column c, y = τ·A₂₂v,
+// y' = y − ½τ(yᵀv)v, A₂₂ −= v y'ᵀ + y' vᵀ) with every matrix element in shared memory: CTA k holds the columns
+// q ≡ k (mod CS) of the trailing matrix in full (both triangles, so y_q = τ·A(:, q)ᵀv needs no cross-CTA
+// reduction) and updates them itself. Per column: the owner of column c forms the reflector from its own copy of
+// the column (no grid reduction), one cluster barrier, every CTA pulls v from the owner over DSMEM and forms y
+// for its columns, a second cluster barrier, every CTA pulls the other CTAs' y and the partial sums of yᵀv (fixed
+// order) and applies the rank-2 update to its columns. Two cluster barriers and no global-memory round trip per
+// column, against two grid-wide barriers and the tile partials of the panel kernel (which stays in charge while the
+// trailing matrix is larger). Same reflector convention as k_trd_panel (β = −sign(α)·sqrt(α² + σ), τ = (β − α)/β,
+// v_{c+1} = 1, v_r = x_r/(α − β)); every sum in a fixed order (deterministic).
+constexpr int CT = 512;  // threads per cluster CTA
+__device__ __forceinline__ double ld_dsmem(const double* p, uint32_t rank) {
+  uint32_t a;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;"
+               : "=r"(a)
+               : "r"(static_cast<uint32_t>(__cvta_generic_to_shared(p))), "r"(rank));
+  double v;
+  asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_dsmem(double* p, uint32_t rank, double v) {
+  uint32_t a;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;"
+               : "=r"(a)
+               : "r"(static_cast<uint32_t>(__cvta_generic_to_shared(p))), "r"(rank));
+  asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(a), "d"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t cl_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cl_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__host__ __device__ constexpr size_t trd_cluster_smem(int mp, int cs) {
+  return sizeof(double) * (static_cast<size_t>((mp + cs - 1) / cs) * mp + 2 * static_cast<size_t>(mp) +
+                           (mp + cs - 1) / cs + 4 + CT / 32 + 16);
+}
+__device__ __forceinline__ double block_sum_ct(double v, double* red) {
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int w = threadIdx.x >> 5;
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) red[w] = v;
+  __syncthreads();
+  double a = 0.0;
+  for (int k = 0; k < CT / 32; ++k) a += red[k];
+  return a;
+}
+
+template <int CS>
+__global__ void __launch_bounds__(CT, 1) k_trd_cluster(double* __restrict__ A, int m, int k0, double* __restrict__ d,
+                                                       double* __restrict__ e, double* __restrict__ tau,
+                                                       unsigned long long* __restrict__ dbg) {
+  extern __shared__ __align__(16) double csm[];
+  const int mp = m - k0, NS = (mp + CS - 1) / CS;
+  const int rank = static_cast<int>(cl_rank());
+  // OZR_SYEV_PROBE: accumulated ns per phase as seen by CTA 1 (an owner one column in CS)
+  unsigned long long tl = gtimer();
+#define CPROBE(k)                                           \
+  if (dbg && rank == 1 && threadIdx.x == 0) {              \
+    const unsigned long long tn_ = gtimer();               \
+    dbg[8 + (k)] += tn_ - tl;                              \
+    tl = tn_;                                              \
+  }
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  double* cols = csm;                         // NS x mp: slot s = column q = s·CS + rank, rows 0..mp−1
+  double* vbuf = cols + static_cast<size_t>(NS) * mp;  // v (rows c+1..)
+  double* ybuf = vbuf + mp;                   // y, then y' (rows c+1..); y_q pushed by q's owner
+  double* misc = ybuf + mp + NS;              // [2 + parity] τ of the pivot column (pushed by its owner)
+  double* red = misc + 4;                     // CT/32 block partials, then CS cluster partials
+  double* redc = red + CT / 32;               // CS partial sums Σ y_q v_q (pushed, slot = CTA rank)
+  const long long ld = m;
+  // the trailing matrix, both triangles from the stored lower one (row r, column q relative to k0)
+  for (int s = 0; s < NS; ++s) {
+    const int q = s * CS + rank;
+    if (q >= mp) break;
+    for (int r = tid; r < mp; r += CT) {
+      const int hi = r >= q ? r : q, lo = r >= q ? q : r;
+      cols[static_cast<size_t>(s) * mp + r] = A[(k0 + hi) + (k0 + lo) * ld];
+    }
+  }
+  __syncthreads();
+  cl_sync();  // every CTA's shared memory is live before any remote access
+  for (int c = 0; c + 1 < mp; ++c) {
+    const int own = c % CS, par = c & 1;
+    if (rank == own) {
+      double* col = cols + static_cast<size_t>(c / CS) * mp;
+      double ss = 0.0;
+      for (int r = c + 2 + tid; r < mp; r += CT) ss = fma(col[r], col[r], ss);
+      const double sigma = block_sum_ct(ss, red);
+      const double alpha = col[c + 1];
+      double beta = alpha, tc = 0.0, scale = 0.0;
+      if (sigma != 0.0) {
+        beta = -copysign(sqrt(fma(alpha, alpha, sigma)), alpha);
+        tc = (beta - alpha) / beta;
+        scale = 1.0 / (alpha - beta);
+      }
+      for (int r = c + 2 + tid; r < mp; r += CT) col[r] *= scale;  // v_r (also the stored reflector)
+      if (tid == 0) {
+        d[k0 + c] = col[c];
+        e[k0 + c] = beta;
+        tau[k0 + c] = tc;
+      }
+      if (tid < CS) st_dsmem(misc + 2 + par, tid, tc);  // τ pushed into every CTA (parity slot)
+      __syncthreads();
+    }
+    CPROBE(0);
+    cl_sync();  // B1: the pivot column's reflector is final, τ is in every CTA
+    CPROBE(1);
+    const double tc = misc[2 + par];
+    if (tc == 0.0) continue;  // H = I (uniform over the cluster)
+    {
+      const double* ocol = cols + static_cast<size_t>(c / CS) * mp;
+      for (int r = c + 1 + tid; r < mp; r += CT) vbuf[r] = (r == c + 1) ? 1.0 : ld_dsmem(ocol + r, own);
+    }
+    __syncthreads();
+    CPROBE(2);
+    // y_q = τ·A(c+1:, q)ᵀ v for this CTA's columns q > c: one warp per column, lanes over rows, butterfly sum
+    const int s0 = (c + 1 - rank + CS - 1) / CS > 0 ? (c + 1 - rank + CS - 1) / CS : 0;
+    double part = 0.0;
+    for (int s = s0 + wid; s < NS; s += CT / 32) {
+      const int q = s * CS + rank;
+      if (q >= mp) break;
+      const double* col = cols + static_cast<size_t>(s) * mp;
+      double a = 0.0;
+      for (int r = c + 1 + lane; r < mp; r += 32) a = fma(col[r], vbuf[r], a);
+      for (int o = 16; o; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+      const double y = tc * a;
+      if (lane < CS) st_dsmem(ybuf + q, lane, y);  // y_q pushed into every CTA's y (same value in every lane)
+      part = fma(y, vbuf[q], part);                 // lane 0's counts
+    }
+    if (lane != 0) part = 0.0;
+    {
+      const double sp = block_sum_ct(part, red);
+      if (tid < CS) st_dsmem(redc + rank, tid, sp);  // this CTA's Σ y_q v_q into slot `rank` of every CTA
+    }
+    CPROBE(3);
+    cl_sync();  // B2: every y_q and every CTA's Σ y_q v_q have landed (release/acquire of the cluster barrier)
+    CPROBE(4);
+    double yv = 0.0;
+    for (int k = 0; k < CS; ++k) yv += redc[k];  // fixed order
+    const double a2 = -0.5 * tc * yv;
+    for (int q = c + 1 + tid; q < mp; q += CT) ybuf[q] = fma(a2, vbuf[q], ybuf[q]);
+    __syncthreads();
+    CPROBE(5);
+    // A₂₂ −= v y'ᵀ + y' vᵀ on this CTA's columns (threads over rows, every own column)
+    for (int r = c + 1 + tid; r < mp; r += CT) {
+      const double vr = vbuf[r], yr = ybuf[r];
+      for (int s = s0; s < NS; ++s) {
+        const int q = s * CS + rank;
+        if (q >= mp) break;
+        double* x = cols + static_cast<size_t>(s) * mp + r;
+        *x = fma(-vr, ybuf[q], fma(-yr, vbuf[q], *x));
+      }
+    }
+    __syncthreads();
+    CPROBE(6);
+  }
+  // the last diagonal element, and the reflectors back to global memory (rows r ≥ c + 2 of column c)
+  if (rank == (mp - 1) % CS && tid == 0) d[k0 + mp - 1] = cols[static_cast<size_t>((mp - 1) / CS) * mp + mp - 1];
+  for (int s = 0; s < NS; ++s) {
+    const int q = s * CS + rank;
+    if (q + 2 >= mp) break;
+    for (int r = q + 2 + tid; r < mp; r += CT) A[(k0 + r) + (k0 + q) * ld] = cols[static_cast<size_t>(s) * mp + r];
+  }
+  cl_sync();  // no CTA leaves while another may still read its shared memory
+#undef CPROBE
+}
+
+
+// The largest trailing size k_trd_cluster takes (0: unavailable on this device), and its cluster size. CS = 16
+// (non-portable) where the device can co-schedule it, else 8. OZR_TRD_CLUSTER=0 disables it (A/B).
+struct TrdCluster {
+  int cs = 0, maxmp = 0;
+};
+TrdCluster trd_cluster_caps() {
+  static int dev_seen[64];
+  static TrdCluster cap[64];
+  static std::mutex mu;
+  if (const char* f = getenv("OZR_TRD_CLUSTER"))
+    if (f[0] == '0') return {};
+  std::lock_guard<std::mutex> g(mu);
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return {};
+  if (dev_seen[dev]) return cap[dev];
+  dev_seen[dev] = 1;
+  int smax = 0;
+  cudaDeviceGetAttribute(&smax, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  auto largest = [&](int cs) {
+    int mp = 0;
+    while (trd_cluster_smem(mp + 1, cs) <= static_cast<size_t>(smax)) ++mp;
+    return mp;
+  };
+  for (int cs : {16, 8}) {
+    const void* fn = cs == 16 ? reinterpret_cast<const void*>(k_trd_cluster<16>) : reinterpret_cast<const void*>(k_trd_cluster<8>);
+    if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smax) != cudaSuccess) {
+      cudaGetLastError();
+      continue;
+    }
+    if (cs == 16 && cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
+      cudaGetLastError();
+      continue;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = cs;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3(cs);
+    cfg.blockDim = dim3(CT);
+    cfg.dynamicSmemBytes = smax;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int ncl = 0;
+    if (cudaOccupancyMaxActiveClusters(&ncl, fn, &cfg) != cudaSuccess || ncl < 1) {
+      cudaGetLastError();
+      continue;
+    }
+    cap[dev] = {cs, largest(cs)};
+    break;
+  }
+  return cap[dev];
+}
+cudaError_t launch_trd_cluster(const TrdCluster& tc, double* A, int m, int k0, double* d, double* e, double* tau,
+                               cudaStream_t s, unsigned long long* dbg) {
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = tc.cs;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.gridDim = dim3(tc.cs);
+  cfg.blockDim = dim3(CT);
+  cfg.dynamicSmemBytes = trd_cluster_smem(m - k0, tc.cs);
+  cfg.stream = s;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  if (tc.cs == 16) return cudaLaunchKernelEx(&cfg, k_trd_cluster<16>, A, m, k0, d, e, tau, dbg);
+  return cudaLaunchKernelEx(&cfg, k_trd_cluster<8>, A, m, k0, d, e, tau, dbg);
+}
 }  // namespace
 
 size_t syev_trd_partials(int m, int G) {
@@ -936,8 +1181,8 @@ cudaError_t syev_tridiag(double* A, int m, double* d, double* e, double* tau, do
                          int G, cudaStream_t s) {
   unsigned long long* dbg = nullptr;
   if (getenv("OZR_SYEV_PROBE")) {
-    cudaMalloc(&dbg, 8 * sizeof(unsigned long long));
-    cudaMemsetAsync(dbg, 0, 8 * sizeof(unsigned long long), s);
+    cudaMalloc(&dbg, 16 * sizeof(unsigned long long));
+    cudaMemsetAsync(dbg, 0, 16 * sizeof(unsigned long long), s);
   }
   const int mt = (m + TB - 1) / TB;
   if (G < mt) return cudaErrorInvalidConfiguration;  // every row block needs its owner CTA (m ≤ ~28000)
@@ -949,7 +1194,13 @@ cudaError_t syev_tridiag(double* A, int m, double* d, double* e, double* tau, do
     const char* f = getenv("OZR_SYEV_GDIV");  // A/B: G_panel = m'/GDIV (0: the fixed G)
     gfac = f ? atoi(f) : 0;
   }
+  const TrdCluster tcl = trd_cluster_caps();
   for (int k0 = 0; k0 < m; k0 += NB) {
+    if (m - k0 <= tcl.maxmp && m - k0 >= 2) {  // the rest inside one cluster's shared memory
+      cudaError_t err = launch_trd_cluster(tcl, A, m, k0, d, e, tau, s, dbg);
+      if (err != cudaSuccess) return err;
+      break;
+    }
     const int nb = std::min(NB, m - k0);
     const int Gk = gfac > 0 ? std::max(mt, std::min(G, (m - k0) / gfac)) : G;
     PanelArgs P{A, m, k0, nb, V, W, d, e, tau, part, yp, part + syev_trd_partials(m, G), dbg};
@@ -966,11 +1217,13 @@ cudaError_t syev_tridiag(double* A, int m, double* d, double* e, double* tau, do
     }
   }
   if (dbg) {
-    unsigned long long h[8];
+    unsigned long long h[16];
     cudaMemcpyAsync(h, dbg, sizeof h, cudaMemcpyDeviceToHost, s);
     cudaStreamSynchronize(s);
     fprintf(stderr, "[ozr syev probe] m=%d G=%d ms: A %.2f sync1 %.2f B-head %.2f tiles %.2f dots %.2f sync2 %.2f C %.2f\n", m, G,
             h[6] * 1e-6, h[0] * 1e-6, h[1] * 1e-6, h[2] * 1e-6, h[3] * 1e-6, h[4] * 1e-6, h[5] * 1e-6);
+    fprintf(stderr, "[ozr syev probe] cluster tail (CTA 1) ms: owner %.2f B1 %.2f pull-v %.2f y %.2f B2 %.2f y' %.2f update %.2f\n",
+            h[8] * 1e-6, h[9] * 1e-6, h[10] * 1e-6, h[11] * 1e-6, h[12] * 1e-6, h[13] * 1e-6, h[14] * 1e-6);
     cudaFree(dbg);
   }
   return cudaGetLastError();

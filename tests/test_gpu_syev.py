@@ -108,22 +108,40 @@ def test_syev_repeated_and_diagonal(ctx, m):
     _check_props(D, th, Y)
 
 
-@pytest.mark.parametrize("m", [3, 33, 64, 100, 257])
-def test_stage_tridiagonalisation(ctx, m):
+@pytest.mark.parametrize("m,cl", [(3, "1"), (33, "1"), (64, "1"), (100, "1"), (257, "1"), (257, "0"), (640, "1"),
+                                  (700, "1"), (700, "0"), (1000, "1")])
+def test_stage_tridiagonalisation(ctx, m, cl, monkeypatch):
     """Stage (1) alone: the reflectors H_c = I − τ_c v_c v_cᵀ it returns satisfy Q_Hᵀ K Q_H = tridiag(d, e) with
-    Q_H = H_0⋯H_{m−2} (LAPACK dsytrd's lower convention), to c·u·‖K‖."""
+    Q_H = H_0⋯H_{m−2} (LAPACK dsytrd's lower convention), to c·u·‖K‖. cl = "1": trailing matrices of up to ~640
+    columns run in one thread-block cluster (k_trd_cluster; m = 700 and 1000 hand over from the panel kernel,
+    m ≤ 640 runs there entirely); "0": the panel kernel throughout (OZR_TRD_CLUSTER=0)."""
+    monkeypatch.setenv("OZR_TRD_CLUSTER", cl)
     K = _random_sym(m, 11 + m)
     Kd = ozr.colmajor(torch.from_numpy(np.asfortranarray(K)).cuda())
     d, e, tau, R = (t.cpu().numpy() for t in ozr.ozr_syev_tridiag(ctx, Kd))
-    Q = np.eye(m)
-    for c in range(m - 1):
+    T = K.copy()
+    for c in range(m - 1):  # T ← H_c T H_c, in order (O(m²) per reflector)
         v = np.zeros(m)
         v[c + 1] = 1.0
         v[c + 2:] = R[c + 2:, c]
-        Q = Q @ (np.eye(m) - tau[c] * np.outer(v, v))
-    T = Q.T @ K @ Q
+        T -= tau[c] * np.outer(v, v @ T)
+        T -= tau[c] * np.outer(T @ v, v)
     Tref = np.diag(d) + np.diag(e[:m - 1], -1) + np.diag(e[:m - 1], 1)
     assert np.max(np.abs(T - Tref)) <= 64 * U * np.linalg.norm(K) * np.sqrt(m), np.max(np.abs(T - Tref))
+
+
+@pytest.mark.parametrize("m", [300, 640, 739])
+def test_syev_cluster_tridiagonalisation_properties(ctx, m, monkeypatch):
+    """The whole eigensolver with and without the cluster-resident tail of the tridiagonalisation: both meet the
+    backward-stability bounds, and the eigenvalues agree to c·u·‖K‖."""
+    K = _random_sym(m, 5 + m)
+    out = []
+    for cl in ("1", "0"):
+        monkeypatch.setenv("OZR_TRD_CLUSTER", cl)
+        th, Y = _run(ctx, K)
+        _check_props(K, th, Y)
+        out.append(th)
+    assert np.max(np.abs(out[0] - out[1])) <= 64 * U * np.linalg.norm(K)
 
 
 @pytest.mark.parametrize("m", [33, 64, 100, 700])
