@@ -909,23 +909,18 @@ __global__ void k_sub_strided(double* __restrict__ Y, int ldy, const double* __r
 // of the tridiagonalisation runs unblocked (LAPACK dsytd2 order: reflector of column c, y = τ·A₂₂v,
 // y' = y − ½τ(yᵀv)v, A₂₂ −= v y'ᵀ + y' vᵀ) with every matrix element in shared memory: CTA k holds the columns
 // q ≡ k (mod CS) of the trailing matrix in full (both triangles, so y_q = τ·A(:, q)ᵀv needs no cross-CTA
-// reduction) and updates them itself. Per column: the owner of column c forms the reflector from its own copy of
-// the column (no grid reduction), one cluster barrier, every CTA pulls v from the owner over DSMEM and forms y
-// for its columns, a second cluster barrier, every CTA pulls the other CTAs' y and the partial sums of yᵀv (fixed
-// order) and applies the rank-2 update to its columns. Two cluster barriers and no global-memory round trip per
-// column, against two grid-wide barriers and the tile partials of the panel kernel (which stays in charge while the
-// trailing matrix is larger). Same reflector convention as k_trd_panel (β = −sign(α)·sqrt(α² + σ), τ = (β − α)/β,
-// v_{c+1} = 1, v_r = x_r/(α − β)); every sum in a fixed order (deterministic).
+// reduction) and updates them itself. Per column c: (B1) the reflector of column c is in every CTA — its owner
+// computed it from its own copy of the column (no grid reduction) and pushed v and τ into every CTA over DSMEM;
+// every CTA forms y_q for its columns (one warp per column) and pushes y_q and its partial Σ y_q v_q into every
+// CTA; (B2) y' = y − ½τ(yᵀv)v locally (the partials summed in a fixed order), then the rank-2 update of the CTA's
+// columns. Look-ahead: the owner of column c + 1 updates that column first, forms and pushes its reflector and
+// arrives at B1(c + 1) before updating its other columns (split arrive / wait), so the reflector and the v
+// transfer overlap the other CTAs' updates. v, y, the partials and τ are double-buffered by column parity. Two
+// cluster barriers and no global-memory round trip per column, against two grid-wide barriers and the tile
+// partials of the panel kernel (which stays in charge while the trailing matrix is larger). Same reflector
+// convention as k_trd_panel (β = −sign(α)·sqrt(α² + σ), τ = (β − α)/β, v_{c+1} = 1, v_r = x_r/(α − β)); every sum
+// in a fixed order (deterministic).
 constexpr int CT = 512;  // threads per cluster CTA
-__device__ __forceinline__ double ld_dsmem(const double* p, uint32_t rank) {
-  uint32_t a;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;"
-               : "=r"(a)
-               : "r"(static_cast<uint32_t>(__cvta_generic_to_shared(p))), "r"(rank));
-  double v;
-  asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(a) : "memory");
-  return v;
-}
 __device__ __forceinline__ void st_dsmem(double* p, uint32_t rank, double v) {
   uint32_t a;
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;"
@@ -942,8 +937,8 @@ __device__ __forceinline__ void cl_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 __host__ __device__ constexpr size_t trd_cluster_smem(int mp, int cs) {
-  return sizeof(double) * (static_cast<size_t>((mp + cs - 1) / cs) * mp + 2 * static_cast<size_t>(mp) +
-                           (mp + cs - 1) / cs + 4 + CT / 32 + 16);
+  return sizeof(double) * (static_cast<size_t>((mp + cs - 1) / cs) * mp + 4 * static_cast<size_t>(mp) + 4 +
+                           CT / 32 + 2 * cs + 8);
 }
 __device__ __forceinline__ double block_sum_ct(double v, double* red) {
   for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -972,12 +967,12 @@ __global__ void __launch_bounds__(CT, 1) k_trd_cluster(double* __restrict__ A, i
     tl = tn_;                                              \
   }
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  double* cols = csm;                         // NS x mp: slot s = column q = s·CS + rank, rows 0..mp−1
-  double* vbuf = cols + static_cast<size_t>(NS) * mp;  // v (rows c+1..)
-  double* ybuf = vbuf + mp;                   // y, then y' (rows c+1..); y_q pushed by q's owner
-  double* misc = ybuf + mp + NS;              // [2 + parity] τ of the pivot column (pushed by its owner)
-  double* red = misc + 4;                     // CT/32 block partials, then CS cluster partials
-  double* redc = red + CT / 32;               // CS partial sums Σ y_q v_q (pushed, slot = CTA rank)
+  double* cols = csm;                                   // NS x mp: slot s = column q = s·CS + rank, rows 0..mp−1
+  double* vbuf = cols + static_cast<size_t>(NS) * mp;   // [2][mp] v of the pivot column (pushed by its owner)
+  double* ybuf = vbuf + 2 * static_cast<size_t>(mp);    // [2][mp] y, then y' (y_q pushed by q's owner)
+  double* misc = ybuf + 2 * static_cast<size_t>(mp);    // [parity] τ of the pivot column (pushed by its owner)
+  double* red = misc + 4;                               // CT/32 block partials
+  double* redc = red + CT / 32;                         // [2][CS] Σ y_q v_q per CTA (pushed, slot = CTA rank)
   const long long ld = m;
   // the trailing matrix, both triangles from the stored lower one (row r, column q relative to k0)
   for (int s = 0; s < NS; ++s) {
@@ -990,79 +985,123 @@ __global__ void __launch_bounds__(CT, 1) k_trd_cluster(double* __restrict__ A, i
   }
   __syncthreads();
   cl_sync();  // every CTA's shared memory is live before any remote access
-  for (int c = 0; c + 1 < mp; ++c) {
-    const int own = c % CS, par = c & 1;
-    if (rank == own) {
-      double* col = cols + static_cast<size_t>(c / CS) * mp;
-      double ss = 0.0;
-      for (int r = c + 2 + tid; r < mp; r += CT) ss = fma(col[r], col[r], ss);
-      const double sigma = block_sum_ct(ss, red);
-      const double alpha = col[c + 1];
-      double beta = alpha, tc = 0.0, scale = 0.0;
-      if (sigma != 0.0) {
-        beta = -copysign(sqrt(fma(alpha, alpha, sigma)), alpha);
-        tc = (beta - alpha) / beta;
-        scale = 1.0 / (alpha - beta);
-      }
-      for (int r = c + 2 + tid; r < mp; r += CT) col[r] *= scale;  // v_r (also the stored reflector)
-      if (tid == 0) {
-        d[k0 + c] = col[c];
-        e[k0 + c] = beta;
-        tau[k0 + c] = tc;
-      }
-      if (tid < CS) st_dsmem(misc + 2 + par, tid, tc);  // τ pushed into every CTA (parity slot)
-      __syncthreads();
+  // Reflector of column c (its owner, the column already updated): β, τ, v into the column (the stored reflector)
+  // and into vbuf[c & 1] of every CTA; τ into misc[c & 1] of every CTA; d, e, τ out.
+  auto reflector = [&](int c) {
+    double* col = cols + static_cast<size_t>(c / CS) * mp;
+    const int par = c & 1;
+    double ss = 0.0;
+    for (int r = c + 2 + tid; r < mp; r += CT) ss = fma(col[r], col[r], ss);
+    const double sigma = block_sum_ct(ss, red);
+    const double alpha = col[c + 1];
+    double beta = alpha, tc = 0.0, scale = 0.0;
+    if (sigma != 0.0) {
+      beta = -copysign(sqrt(fma(alpha, alpha, sigma)), alpha);
+      tc = (beta - alpha) / beta;
+      scale = 1.0 / (alpha - beta);
     }
-    CPROBE(0);
-    cl_sync();  // B1: the pivot column's reflector is final, τ is in every CTA
-    CPROBE(1);
-    const double tc = misc[2 + par];
-    if (tc == 0.0) continue;  // H = I (uniform over the cluster)
-    {
-      const double* ocol = cols + static_cast<size_t>(c / CS) * mp;
-      for (int r = c + 1 + tid; r < mp; r += CT) vbuf[r] = (r == c + 1) ? 1.0 : ld_dsmem(ocol + r, own);
+    double* vb = vbuf + par * static_cast<size_t>(mp);
+    for (int r = c + 1 + tid; r < mp; r += CT) {
+      double v = 1.0;
+      if (r > c + 1) {
+        v = col[r] * scale;
+        col[r] = v;
+      }
+#pragma unroll 4
+      for (int k = 0; k < CS; ++k) st_dsmem(vb + r, k, v);
+    }
+    if (tid == 0) {
+      d[k0 + c] = col[c];
+      e[k0 + c] = beta;
+      tau[k0 + c] = tc;
+    }
+    if (tid < CS) st_dsmem(misc + par, tid, tc);
+    __syncthreads();
+  };
+  auto arrive = [] { asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory"); };
+  auto wait = [] { asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory"); };
+  // A₂₂ −= v y'ᵀ + y' vᵀ on this CTA's columns in [qa, qb) (threads over rows r > c, every such column)
+  auto update = [&](int c, int sa, int sb) {
+    const int par = c & 1;
+    const double* vb = vbuf + par * static_cast<size_t>(mp);
+    const double* yb = ybuf + par * static_cast<size_t>(mp);
+    for (int r = c + 1 + tid; r < mp; r += CT) {
+      const double vr = vb[r], yr = yb[r];
+      for (int s = sa; s < sb; ++s) {
+        const int q = s * CS + rank;
+        double* x = cols + static_cast<size_t>(s) * mp + r;
+        *x = fma(-vr, yb[q], fma(-yr, vb[q], *x));
+      }
     }
     __syncthreads();
-    CPROBE(2);
-    // y_q = τ·A(c+1:, q)ᵀ v for this CTA's columns q > c: one warp per column, lanes over rows, butterfly sum
-    const int s0 = (c + 1 - rank + CS - 1) / CS > 0 ? (c + 1 - rank + CS - 1) / CS : 0;
-    double part = 0.0;
-    for (int s = s0 + wid; s < NS; s += CT / 32) {
-      const int q = s * CS + rank;
-      if (q >= mp) break;
-      const double* col = cols + static_cast<size_t>(s) * mp;
-      double a = 0.0;
-      for (int r = c + 1 + lane; r < mp; r += 32) a = fma(col[r], vbuf[r], a);
-      for (int o = 16; o; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
-      const double y = tc * a;
-      if (lane < CS) st_dsmem(ybuf + q, lane, y);  // y_q pushed into every CTA's y (same value in every lane)
-      part = fma(y, vbuf[q], part);                 // lane 0's counts
-    }
-    if (lane != 0) part = 0.0;
-    {
+  };
+  if (rank == 0 && mp >= 2) reflector(0);
+  if (mp >= 2) arrive();  // B1(0)
+  for (int c = 0; c + 1 < mp; ++c) {
+    const int par = c & 1;
+    wait();  // B1(c): the reflector of column c is in every CTA, and every CTA has finished column c − 1
+    CPROBE(1);
+    const double tc = misc[par];
+    double* vb = vbuf + par * static_cast<size_t>(mp);
+    double* yb = ybuf + par * static_cast<size_t>(mp);
+    const int s0 = (c + 1 - rank + CS - 1) / CS;  // first slot with column q > c
+    const int s1 = (mp - rank + CS - 1) / CS;     // slots of real columns
+    if (tc != 0.0) {
+      // y_q = τ·A(c+1:, q)ᵀ v for this CTA's columns q > c: one warp per column, lanes over rows (four chains)
+      double part = 0.0;
+      for (int s = s0 + wid; s < s1; s += CT / 32) {
+        const int q = s * CS + rank;
+        const double* col = cols + static_cast<size_t>(s) * mp;
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+        int r = c + 1 + lane;
+        for (; r + 96 < mp; r += 128) {
+          a0 = fma(col[r], vb[r], a0);
+          a1 = fma(col[r + 32], vb[r + 32], a1);
+          a2 = fma(col[r + 64], vb[r + 64], a2);
+          a3 = fma(col[r + 96], vb[r + 96], a3);
+        }
+        for (; r < mp; r += 32) a0 = fma(col[r], vb[r], a0);
+        double a = (a0 + a1) + (a2 + a3);
+        for (int o = 16; o; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+        const double y = tc * a;
+        if (lane < CS) st_dsmem(yb + q, lane, y);  // y_q into every CTA (same value in every lane)
+        part = fma(y, vb[q], part);                 // lane 0's counts
+      }
+      if (lane != 0) part = 0.0;
       const double sp = block_sum_ct(part, red);
-      if (tid < CS) st_dsmem(redc + rank, tid, sp);  // this CTA's Σ y_q v_q into slot `rank` of every CTA
+      if (tid < CS) st_dsmem(redc + par * CS + rank, tid, sp);
     }
     CPROBE(3);
-    cl_sync();  // B2: every y_q and every CTA's Σ y_q v_q have landed (release/acquire of the cluster barrier)
+    // B2(c): every y_q and every CTA's Σ y_q v_q have landed. Also when τ = 0: the owner of column c arrived at
+    // B1(c) before its deferred update of column c − 1, which reads vbuf[(c − 1) & 1] — the buffer the reflector
+    // of column c + 1 is about to fill
+    cl_sync();
     CPROBE(4);
-    double yv = 0.0;
-    for (int k = 0; k < CS; ++k) yv += redc[k];  // fixed order
-    const double a2 = -0.5 * tc * yv;
-    for (int q = c + 1 + tid; q < mp; q += CT) ybuf[q] = fma(a2, vbuf[q], ybuf[q]);
-    __syncthreads();
-    CPROBE(5);
-    // A₂₂ −= v y'ᵀ + y' vᵀ on this CTA's columns (threads over rows, every own column)
-    for (int r = c + 1 + tid; r < mp; r += CT) {
-      const double vr = vbuf[r], yr = ybuf[r];
-      for (int s = s0; s < NS; ++s) {
-        const int q = s * CS + rank;
-        if (q >= mp) break;
-        double* x = cols + static_cast<size_t>(s) * mp + r;
-        *x = fma(-vr, ybuf[q], fma(-yr, vbuf[q], *x));
-      }
+    if (tc != 0.0) {
+      double yv = 0.0;
+      for (int k = 0; k < CS; ++k) yv += redc[par * CS + k];  // fixed order
+      const double a2 = -0.5 * tc * yv;
+      for (int q = c + 1 + tid; q < mp; q += CT) yb[q] = fma(a2, vb[q], yb[q]);
+      __syncthreads();
+      CPROBE(5);
     }
-    __syncthreads();
+    const int c1 = c + 1;
+    if (c1 + 1 < mp) {
+      if (rank == c1 % CS) {
+        // look-ahead: column c + 1 first, its reflector published, the barrier arrived at, then the rest
+        const int sp1 = c1 / CS;
+        if (tc != 0.0) update(c, sp1, sp1 + 1);
+        reflector(c1);
+        CPROBE(0);
+        arrive();  // B1(c + 1)
+        if (tc != 0.0) update(c, sp1 + 1, s1);
+      } else {
+        if (tc != 0.0) update(c, s0, s1);
+        arrive();  // B1(c + 1)
+      }
+    } else if (tc != 0.0) {
+      update(c, s0, s1);
+    }
     CPROBE(6);
   }
   // the last diagonal element, and the reflectors back to global memory (rows r ≥ c + 2 of column c)
@@ -1222,7 +1261,7 @@ cudaError_t syev_tridiag(double* A, int m, double* d, double* e, double* tau, do
     cudaStreamSynchronize(s);
     fprintf(stderr, "[ozr syev probe] m=%d G=%d ms: A %.2f sync1 %.2f B-head %.2f tiles %.2f dots %.2f sync2 %.2f C %.2f\n", m, G,
             h[6] * 1e-6, h[0] * 1e-6, h[1] * 1e-6, h[2] * 1e-6, h[3] * 1e-6, h[4] * 1e-6, h[5] * 1e-6);
-    fprintf(stderr, "[ozr syev probe] cluster tail (CTA 1) ms: owner %.2f B1 %.2f pull-v %.2f y %.2f B2 %.2f y' %.2f update %.2f\n",
+    fprintf(stderr, "[ozr syev probe] cluster tail (CTA 1) ms: own-reflector %.2f B1-wait %.2f - %.2f y %.2f B2 %.2f y' %.2f update %.2f\n",
             h[8] * 1e-6, h[9] * 1e-6, h[10] * 1e-6, h[11] * 1e-6, h[12] * 1e-6, h[13] * 1e-6, h[14] * 1e-6);
     cudaFree(dbg);
   }
