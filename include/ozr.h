@@ -133,7 +133,7 @@ typedef struct {
                         eigensolver (ozr_syev: Householder tridiagonalisation, divide and conquer, back-
                         transformation, all in libozr's kernels) instead of the parallel Jacobi; same K,
                         same conventions (R13).
-                        Default 192 (smaller groups: one Jacobi CTA each, all groups in one launch) */
+                        Default 64 (smaller groups: one Jacobi CTA each, all groups in one launch) */
   int row_nnz;       /* k = maximum number of nonzeros in a row of A (beta_mode 2; also the contraction
                         length of the V-product's dropped-pair bound, R8). 0 → n (dense)            */
   int max_escalations; /* ozr_refine_to_tol: when the certified error stalls above δ at the truncated iteration's

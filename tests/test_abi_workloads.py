@@ -57,7 +57,7 @@ def test_params_default(libozr):
     assert p.kA_split == 15 and p.truncate == 1 and p.beta_mode == 0 and abs(p.theta_V - 1 / 16) < 1e-18
     # the ctypes mirror of ozr_params matches the C layout up to its last field
     assert p.theta == 4.0 and p.cluster_mode == 1 and p.max_cluster == 16384 and p.form_R == 0
-    assert p.dense_cluster == 192 and p.row_nnz == 0 and p.max_escalations == 2
+    assert p.dense_cluster == 64 and p.row_nnz == 0 and p.max_escalations == 2
 
 def test_ctypes_structs_match_header(tmp_path):
     """The binding's ctypes mirrors of ozr_params / ozr_step_report have the C header's size and field
