@@ -138,3 +138,24 @@ def test_bench_reference_arm_cpu():
     line = json.loads(out.decode().strip().splitlines()[-1])
     assert line["impl"] == "reference" and line["value"] > 0 and line["e2e"]["h2d_bytes_per_step"] == 0
     assert line["cpu_baseline"]["kind"] == "oracle"
+
+
+@pytest.mark.parametrize("kind", ["geometric", "clustered"])
+def test_hadamard_exact_eigensystem_in_integers(kind):
+    """W.hadamard_exact: A Q = Q Λ and QᵀQ = I hold EXACTLY — checked in Python integers on the numerators
+    (n·Q, n²·2^b·A, 2^b·λ are integers), not in floating point."""
+    m = 6
+    n, b = 2 ** m, 53 - 2 * m - 1
+    A, lam, X = W.hadamard_exact(m, kind, seed=11)
+    NQ = (X * n).astype(object)
+    NA = (A * float(n) ** 2 * 2.0 ** b)
+    NL = lam * 2.0 ** b
+    assert np.all(NQ == np.rint(X * n)) and np.all(NA == np.rint(NA)) and np.all(NL == np.rint(NL))
+    NA = np.vectorize(int, otypes=[object])(NA)
+    NL = np.vectorize(int, otypes=[object])(NL)
+    NQ = np.vectorize(int, otypes=[object])(X * n)
+    assert np.all(NQ.T.dot(NQ) == n * n * np.eye(n, dtype=object).astype(object))
+    assert np.all(NA.dot(NQ) == n * n * (NQ * NL[None, :]))      # (n² 2^b A)(n Q) = n² (n Q)(2^b Λ)
+    assert np.all(np.diff(lam) > 0) and np.all(NA == NA.T)
+    if kind == "clustered":
+        assert np.sum(np.diff(NL) == 1) == 7 * max(n // 64, 1)    # the designed clusters: gaps of one unit

@@ -366,3 +366,23 @@ def test_accmul_fixed_k_vs_rationals():
         assert e <= 2.0 ** (-(8 * (k - 1) + 6) + 2) * (k + 2)  # both splits' rounding + the dropped diagonal
     for a, b in zip(errs, errs[1:]):
         assert b <= a / 2 ** 7
+
+
+@pytest.mark.parametrize("kind,start,delta", [("geometric", "fp64", 1e-13), ("clustered", "fp64", 1e-12),
+                                              ("clustered", "fp32", 1e-12)])
+def test_driver_reaches_target_on_exactly_known_eigenvectors(kind, start, delta):
+    """W.hadamard_exact (A exactly representable, eigenvectors EXACTLY the columns of Q = H S H/n, integer-pinned in
+    tests/test_abi_workloads.py): the oracle driver from an LAPACK start returns "converged" with
+    ‖X − X̂‖₂ ≤ δ against the exact X (no computed reference involved), its certificate within a factor 2 of
+    that forward error + 2u, and λ̂ within 4u‖A‖ of the exact integers."""
+    A, lam, X = W.hadamard_exact(7, kind, seed=21)  # n = 128; "clustered": 2 clusters of 8, relative gap 2^-38
+    lam0, X0 = W.initial_eig(A, start)
+    Xr, lr, hist = orf.refine_to_tol(A, X0, lam0, delta)
+    assert hist[-1].get("stop") == "converged", hist
+    p = np.argsort(lr, kind="stable")
+    Xr, lr = Xr[:, p], lr[p]
+    sg = np.sign(np.sum(Xr * X, axis=0))
+    fe = float(np.linalg.norm(Xr * sg[None, :] - X, 2))
+    assert fe <= delta, (fe, hist)
+    assert hist[-1]["cert"] >= 0.5 * fe - 2.0 ** -52 and hist[-1]["cert"] <= 2 * fe + 2.0 ** -51, (fe, hist[-1])
+    assert np.max(np.abs(lr - lam)) <= 4 * 2.0 ** -53 * np.max(np.abs(lam))

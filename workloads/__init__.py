@@ -277,3 +277,63 @@ def householder_exact_herm(m, lam_bits=12, seed=0):
     X = H[:, order]
     return np.ascontiguousarray(A.real), np.ascontiguousarray(A.imag), lam, np.ascontiguousarray(X.real), \
         np.ascontiguousarray(X.imag)
+
+
+# ---------------------------------------------------------------- exactly known eigenvectors at full size
+def _fwht_rows(M):
+    """In-place-style fast Walsh–Hadamard transform along axis 0 (Sylvester ordering), integer arithmetic."""
+    n = M.shape[0]
+    h = 1
+    while h < n:
+        M = M.reshape(n // (2 * h), 2, h, -1)
+        M = np.concatenate((M[:, 0:1] + M[:, 1:2], M[:, 0:1] - M[:, 1:2]), axis=1).reshape(n, -1)
+        h *= 2
+    return M
+
+
+def hadamard_exact(m, kind="geometric", cnd=1e4, seed=0, lam_bits=None):
+    """Full-size family with EXACTLY known eigenpairs (no reference computation needed): n = 2^m, H the Sylvester
+    Hadamard matrix, s ∈ {±1}^n seeded, Q = H diag(s) H / n (symmetric, exactly orthogonal: Q Qᵀ = H S (H H/n) S H/n
+    = I; its entries are integers / n, q_ij = ŝ(i ⊕ j)/n with ŝ the Walsh transform of s), λ distinct INTEGERS
+    below 2^lam_bits (default 53 − 2m − 1, so every numerator below stays under 2^53). Then
+    A = Q diag(λ) Q = (H S H Λ H S H) / n² has integer numerators |n² a_ij| ≤ n² max|λ| < 2^53: A is formed in
+    int64 (four Walsh transforms, no rounding anywhere) and is exactly representable in fp64, its eigenvalues are
+    exactly λ and its eigenvectors exactly the columns of Q. Column k of Q is reordered so that λ is ascending;
+    A and λ are returned scaled by 2^-lam_bits (exact), so ‖A‖₂ ≤ 1.
+    kind = "geometric": λ_i = round(2^lam_bits · cnd^{-(i-1)/(n-1)}) (cnd small enough that they stay distinct);
+    kind = "clustered": n/64 clusters of 8 integers separated by 1 (relative separation 2^-lam_bits of ‖A‖₂) among
+    otherwise 16-separated integers of both signs (the BASELINE c3 structure with the tightest separation that
+    keeps A exact). Returns (A, λ ascending, X exact (sign-fixed))."""
+    n = 2 ** m
+    if lam_bits is None:
+        lam_bits = 53 - 2 * m - 1
+    rng = np.random.default_rng(seed)
+    s = rng.choice(np.array([-1, 1], dtype=np.int64), size=n)
+    if kind == "geometric":
+        lam = np.rint(2.0 ** lam_bits * cnd ** (-np.arange(n) / max(n - 1, 1))).astype(np.int64)
+    elif kind == "clustered":
+        ncl = max(n // 64, 1)
+        slots = 2 ** (lam_bits - 3)  # centres are multiples of 16 in (−2^lam_bits, 2^lam_bits)
+        nc = n - 7 * ncl
+        centres = (rng.choice(slots - 2, size=nc, replace=False).astype(np.int64) - (slots - 2) // 2) * 16
+        lam = np.concatenate([centres[ncl:]] + [centres[c] + np.arange(8, dtype=np.int64) for c in range(ncl)])
+    else:
+        raise ValueError(kind)
+    lam = np.sort(lam)
+    assert lam.shape == (n,) and np.all(np.diff(lam) > 0) and np.max(np.abs(lam)) <= 2 ** lam_bits, "λ not distinct"
+    # numerators of Q: N = H S H (|N_ij| ≤ n); column order of λ: column perm[k] of Q carries λ_k
+    N = _fwht_rows(_fwht_rows(np.eye(n, dtype=np.int64)) * s[:, None])
+    perm = rng.permutation(n)
+    lam_cols = np.empty(n, dtype=np.int64)
+    lam_cols[perm] = lam
+    # n² A = N Λ Nᵀ = H S (H Λ_cols H) S H, every intermediate an exact int64 (bounded by n^1.5 max|λ| in 2-norm)
+    T = _fwht_rows(np.diag(lam_cols))            # H Λ
+    T = _fwht_rows(np.ascontiguousarray(T.T))    # H Λ H (symmetric)
+    T = T * s[:, None] * s[None, :]              # S H Λ H S
+    T = _fwht_rows(T)
+    T = _fwht_rows(np.ascontiguousarray(T.T))    # H S H Λ H S H
+    assert np.max(np.abs(T)) < 2 ** 53
+    sc = 2.0 ** -lam_bits                        # power-of-two scaling to ‖A‖₂ ≤ 1 (exact)
+    A = T.astype(np.float64) / float(n) ** 2 * sc  # exact: |numerator| < 2^53, n² a power of two
+    X = N[:, perm].astype(np.float64) / float(n)
+    return A, lam.astype(np.float64) * sc, sign_fix(X)
