@@ -20,8 +20,10 @@ U = 2.0 ** -53
 
 # m (n = 2^m), spectrum, start, δ — c3's structure and size (clusters of 8, relative separation 2^-28 — the tightest
 # that keeps A exact), an FP32 start whose lower spectrum is unresolved (large groups → the dense sub-solve), and the
-# headline size n = 8192
-CASES = [(12, "clustered", "fp64", 1e-12), (11, "geometric", "fp32", 1e-12), (13, "geometric", "fp64", 1e-12)]
+# headline size n = 8192 from an FP64 start (c4') and from an FP32 start at c4's δ = 1e-10 (c4's structure: the lower
+# spectrum is unresolved in FP32, thousands of columns in one group)
+CASES = [(12, "clustered", "fp64", 1e-12), (11, "geometric", "fp32", 1e-12), (13, "geometric", "fp64", 1e-12),
+         (13, "geometric", "fp32", 1e-10)]
 
 
 def _start(A, start):
