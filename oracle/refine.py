@@ -257,19 +257,28 @@ def certificate(E, lam, n_power=None, delta=None):
     average over the columns). The sweep returns X̂_new = X̂^(1)(I + Ẽ) while the exact eigenvectors are
     X = X̂^(1)(I + E), so X − X̂_new = X̂^(1)(E − Ẽ): Ẽ's second-order defect
     (second_order_defect()) in the 2-norm of PAPER.md:121, plus X̂_new's rounding to fp64 (a noise-like matrix
-    of entries ≤ u|x_ij|: 2-norm ≈ 2u) and an allowance ‖Ẽ‖_F·‖D‖_F for the third-order terms. Returns
-        est = sqrt(‖D‖₂² + (2u)²) + ‖Ẽ‖_F‖D‖_F
-    and the parts. ‖·‖₂ exactly (LAPACK) for n ≤ 2048, else `n_power` (default 60) power iterations. With δ
+    of entries ≤ u|x_ij|: 2-norm ≈ 2u), an allowance ‖Ẽ‖_F·‖D‖_F for the third-order terms, and the defect from
+    the fp64 rounding of the λ̂ in Ẽ's denominators, ≤ 2u·‖(λ̂_i ẽ_ij/(λ̂_j − λ̂_i))_{i≠j}‖_F (pinned by the
+    exactly-known clustered family, where it is the whole error). Returns
+        est = sqrt(‖D‖₂² + (2u)²) + ‖Ẽ‖_F‖D‖_F + 2u‖(λ̂_i ẽ_ij/(λ̂_j − λ̂_i))‖_F
+    and the parts (quad = the last two terms). ‖·‖₂ exactly (LAPACK) for n ≤ 2048, else `n_power` (default 60) power iterations. With δ
     given, the library's shortcut is mirrored: when even the lower bound max_j ‖D_{:,j}‖ + quad exceeds
     16δ (no decision of the driver can then tell the value from its Frobenius upper bound), or the Frobenius
     upper bound already certifies, ‖D‖_F stands in for ‖D‖₂."""
     E = np.asarray(E, dtype=np.float64)
+    lam = np.asarray(lam, dtype=np.float64)
     D = second_order_defect(E, lam)
     if D is None:
         return dict(est=np.inf, est_q=np.inf, quad=np.inf, frob=np.inf)
     n = E.shape[0]
     frob = float(np.linalg.norm(D))
-    quad = float(np.sqrt(np.sum(E * E))) * frob
+    # the λ̂ the sweep divided by are Rayleigh quotients ROUNDED to fp64: with ε_i = λ̂_i − λ_i, |ε_i| ≤ u|λ̂_i|, the
+    # first-order part of w_ij is −(λ̂_j − λ̂_i)η_ij − ε_i η_ij − ε_j η_ji, which leaves the defect
+    # (ε_i ẽ_ij + ε_j ẽ_ji)/(λ̂_j − λ̂_i) in Ẽ — first order in Ẽ, and u|λ̂|/gap is not small in a tight cluster
+    off = ~np.eye(n, dtype=bool)
+    dl = np.where(off, lam[None, :] - lam[:, None], 1.0)
+    rlam = 2 * U * float(np.sqrt(np.sum(np.where(off, lam[:, None] * E / dl, 0.0) ** 2)))
+    quad = float(np.sqrt(np.sum(E * E))) * frob + rlam
     if delta is not None:
         upper = float(np.sqrt(frob * frob + (2 * U) ** 2)) + quad
         lower = float(np.max(np.sqrt(np.sum(D * D, axis=0)))) + quad

@@ -7,12 +7,20 @@
 // r_jj = −2η_jj − ‖η_j‖², which leaves (oracle/refine.second_order_defect, pinned against exact corrections)
 //     D := −(E − Ẽ):  D_ij = Q_ij/(λ̂_j − λ̂_i) − (Ẽ²)_ij  (i ≠ j),   D_jj = −(Ẽ²)_jj − ½‖ẽ_j‖²,
 //     Q = ẼᵀC,   c_kj = (λ̂_k − λ̂_j)·ẽ_kj.
+// The identity holds for the λ̂ the sweep actually divided by: the Rayleigh quotients ROUNDED to fp64. With
+// ε_i = λ̂_i − λ_i the first-order part of w_ij is −(λ̂_j − λ̂_i)η_ij − ε_i η_ij − ε_j η_ji, so Ẽ carries the extra
+// defect (ε_i ẽ_ij + ε_j ẽ_ji)/(λ̂_j − λ̂_i): second order in Ẽ for the Rayleigh quotient's own O(η²) part (inside
+// the third-order allowance), but FIRST order in Ẽ for the rounding |ε_i| ≤ u|λ̂_i| — u|λ̂|/gap is not small inside a
+// tight cluster (found on the exactly-known family of tests/test_gpu_exact.py: gap 1.7e-12, ẽ 3.7e-7 → 1.4e-11).
+// Its Frobenius norm is at most 2u·sqrt(Σ_{i≠j} (λ̂_i ẽ_ij/(λ̂_j − λ̂_i))²) (the two terms are transposes of one
+// another), column-local in Ẽ: est = sqrt(‖D‖₂² + (2u)²) + ‖Ẽ‖_F‖D‖_F + 2u·sqrt(Σ_j rsq_j).
 // Q and Ẽ² only have to be accurate to a few per cent, so each is ONE bf16 tensor-core GEMM (the slice-GEMM
 // kernel with kind::f16, f32 accumulator): the operands are stored scaled by powers of two (exact) per column
 // (Ẽ, C as B operands / Ẽ's columns as Q's A operand) or per row (Ẽ's rows as the A operand of Ẽ²), which keeps
 // every entry's relative precision (2^-8) whatever its magnitude inside the line.
 //
-//   k_cert_prep    Ẽ = diag(2^−g)·Ẽ' (the stored Ẽ' = diag(2^g)Ẽ is exact), its column maxima, bf16 Ẽ and C
+//   k_cert_prep    Ẽ = diag(2^−g)·Ẽ' (the stored Ẽ' = diag(2^g)Ẽ is exact), its column maxima, bf16 Ẽ and C, and
+//                  the eigenvalue-rounding term Σ_i (λ̂_i ẽ_ij/(λ̂_j − λ̂_i))² (below)
 //   k_cert_rowmax  row exponents rE_i of the (all-gathered) Ẽ
 //   k_cert_rowT    Ẽ's rows, scaled by 2^−rE_i, K-major (the A operand of Ẽ²)
 //   (GEMMs)        Q = ẼᵀC,  P = Ẽ·Ẽ_{:,J}  (launch_gemm_i8 kind 1)
@@ -73,21 +81,28 @@ __device__ __forceinline__ int ceil_log2_dev(double v) {
 __global__ void __launch_bounds__(CB)
     k_cert_prep(const double* __restrict__ Ep, long long lde, int rows, const int32_t* __restrict__ g,
                 const double* __restrict__ lam, int col0, __nv_bfloat16* __restrict__ Eb, __nv_bfloat16* __restrict__ Cb,
-                long long ldb, int32_t* __restrict__ sE, int32_t* __restrict__ sC, double* __restrict__ esq) {
+                long long ldb, int32_t* __restrict__ sE, int32_t* __restrict__ sC, double* __restrict__ esq,
+                double* __restrict__ rsq) {
   __shared__ double sh[CB / 32];
   const int j = blockIdx.x, gj = col0 + j;
   const double* col = Ep + static_cast<long long>(j) * lde;
   const double lj = lam[gj];
-  double me = 0.0, mc = 0.0, ss = 0.0;
+  double me = 0.0, mc = 0.0, ss = 0.0, rs = 0.0;
   for (int i = threadIdx.x; i < rows; i += CB) {
     const double e = ldexp(col[i], -g[i]);  // ẽ_ij = 2^{−g_i} ẽ'_ij, exact
+    const double dl = lam[i] - lj;
     me = fmax(me, fabs(e));
-    mc = fmax(mc, fabs((lam[i] - lj) * e));
+    mc = fmax(mc, fabs(dl * e));
     ss = fma(e, e, ss);
+    if (i != gj && dl != 0.0) {  // the fp64 rounding of λ̂_i seen through ẽ_ij's denominator: λ̂_i ẽ_ij/(λ̂_j − λ̂_i)
+      const double t = lam[i] * e / dl;
+      rs = fma(t, t, rs);
+    }
   }
   me = cb_max(me, sh);
   mc = cb_max(mc, sh);
   ss = cb_sum(ss, sh);
+  rs = cb_sum(rs, sh);
   const int se = ceil_log2_dev(me), sc = ceil_log2_dev(mc);
   __nv_bfloat16* eb = Eb + static_cast<long long>(gj) * ldb;  // Ẽ: all columns (the GEMM's A operand)
   __nv_bfloat16* cb = Cb + static_cast<long long>(j) * ldb;   // C: this rank's columns
@@ -100,6 +115,7 @@ __global__ void __launch_bounds__(CB)
     sE[gj] = se;
     sC[j] = sc;
     esq[j] = ss;
+    rsq[j] = rs;
   }
 }
 
@@ -252,9 +268,10 @@ void launch_lz_axpy(double* x, const double* y, int n, const double* c2, cudaStr
 }
 
 void launch_cert_prep(const double* Ep, long long lde, int rows, int cols, const int32_t* g, const double* lam, int col0,
-                      void* Eb, void* Cb, long long ldb, int32_t* sE, int32_t* sC, double* esq, cudaStream_t s) {
+                      void* Eb, void* Cb, long long ldb, int32_t* sE, int32_t* sC, double* esq, double* rsq,
+                      cudaStream_t s) {
   k_cert_prep<<<cols, CB, 0, s>>>(Ep, lde, rows, g, lam, col0, static_cast<__nv_bfloat16*>(Eb),
-                                  static_cast<__nv_bfloat16*>(Cb), ldb, sE, sC, esq);
+                                  static_cast<__nv_bfloat16*>(Cb), ldb, sE, sC, esq, rsq);
 }
 void launch_cert_rowT(const void* Eb, long long ldb, int rows, int cols, const int32_t* sE, int32_t* rE, void* EbT,
                       cudaStream_t s) {

@@ -7,10 +7,12 @@
 namespace ozr {
 
 // Ẽ = diag(2^−g)·Ẽ' from the stored Ẽ' (rows x cols, local columns [col0, col0 + cols)); per column j:
-// sE[col0 + j] = ⌈log2 max_i |ẽ_ij|⌉, sC[j] = ⌈log2 max_i |(λ̂_i − λ̂_j) ẽ_ij|⌉, esq[j] = Σ_i ẽ_ij²;
+// sE[col0 + j] = ⌈log2 max_i |ẽ_ij|⌉, sC[j] = ⌈log2 max_i |(λ̂_i − λ̂_j) ẽ_ij|⌉, esq[j] = Σ_i ẽ_ij²,
+// rsq[j] = Σ_{i≠j} (λ̂_i ẽ_ij/(λ̂_j − λ̂_i))² (the eigenvalue-rounding term of the certificate);
 // Eb (bf16, column col0 + j at Eb + (col0 + j)·ldb) = ẽ·2^−sE, Cb (bf16, local column j) = (λ̂_i − λ̂_j)ẽ_ij·2^−sC.
 void launch_cert_prep(const double* Ep, long long lde, int rows, int cols, const int32_t* g, const double* lam, int col0,
-                      void* Eb, void* Cb, long long ldb, int32_t* sE, int32_t* sC, double* esq, cudaStream_t s);
+                      void* Eb, void* Cb, long long ldb, int32_t* sE, int32_t* sC, double* esq, double* rsq,
+                      cudaStream_t s);
 // Ẽ's rows as a GEMM A operand: rE[i] = row exponent of the all-gathered Eb (rows x cols, column k scaled by
 // 2^−sE_k), EbT[i·ldb + k] = ẽ_ik·2^−rE_i in bf16.
 void launch_cert_rowT(const void* Eb, long long ldb, int rows, int cols, const int32_t* sE, int32_t* rE, void* EbT,

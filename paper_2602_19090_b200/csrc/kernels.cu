@@ -811,38 +811,54 @@ __global__ void k_transpose_i8(const int8_t* __restrict__ src, long long lds, lo
   }
 }
 
-// The same transpose with 16-byte global loads and stores (64 x 64-byte tiles, one 16-byte load and one 16-byte
-// store per thread): for 16-byte aligned planes with lds, ldt, sps, tps multiples of 16 and rows, cols ≥ 1 (the
-// 16-byte groups that straddle `rows` / `cols` stay inside each line's padding, as in k_transpose_i8).
+// The same transpose with 16-byte global loads and stores on 128 x 128-byte tiles: every global access of a warp
+// covers whole 128-byte lines of the source columns / destination rows (the 64-byte tiles of the first form touched
+// half lines: 56 % of the copy peak). For 16-byte aligned planes with lds, ldt, sps, tps multiples of 16 and rows,
+// cols ≥ 1 (the 16-byte groups that straddle `rows` / `cols` stay inside each line's padding, as in
+// k_transpose_i8). Shared memory: t[j][w ^ (j >> 4)] (32 words per column, pitch 33) — conflict-free for the
+// column-wise stores (a warp: 4 columns x 8 quads) and the row-wise gathers (a warp: 4 rows x 8 column groups).
 __global__ void __launch_bounds__(256) k_transpose_i8_v(const int8_t* __restrict__ src, long long lds, long long sps,
                                                         int8_t* __restrict__ dst, long long ldt, long long tps,
                                                         int rows, int cols) {
-  __shared__ uint32_t t[64][17];  // t[j][i/4]: column j's 64 bytes as 16 words (+1 word: conflict-free columns)
+  __shared__ uint32_t t[128][33];
   const int p = blockIdx.z;
-  const int i0 = blockIdx.x * 64, j0 = blockIdx.y * 64;
+  const int i0 = blockIdx.x * 128, j0 = blockIdx.y * 128;
   const int tid = threadIdx.x;
-  {
-    const int jj = tid >> 2, q = tid & 3;  // column j0 + jj, bytes [16q, 16q + 16) of the tile's rows
+  uint4 v[4];
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {  // all four loads in flight before the first shared-memory store
+    const int idx = tid + 256 * r;
+    const int jj = idx >> 3, q = idx & 7;  // column j0 + jj, bytes [16q, 16q + 16) of the tile's rows
     const int i = i0 + 16 * q, j = j0 + jj;
-    uint4 v = make_uint4(0u, 0u, 0u, 0u);
-    if (i < rows && j < cols) v = *reinterpret_cast<const uint4*>(src + p * sps + j * lds + i);
-    t[jj][4 * q + 0] = v.x;
-    t[jj][4 * q + 1] = v.y;
-    t[jj][4 * q + 2] = v.z;
-    t[jj][4 * q + 3] = v.w;
+    v[r] = make_uint4(0u, 0u, 0u, 0u);
+    if (i < rows && j < cols) v[r] = __ldcs(reinterpret_cast<const uint4*>(src + p * sps + j * lds + i));
+  }
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const int idx = tid + 256 * r;
+    const int jj = idx >> 3, q = idx & 7, sw = jj >> 4;
+    t[jj][(4 * q + 0) ^ sw] = v[r].x;
+    t[jj][(4 * q + 1) ^ sw] = v[r].y;
+    t[jj][(4 * q + 2) ^ sw] = v[r].z;
+    t[jj][(4 * q + 3) ^ sw] = v[r].w;
   }
   __syncthreads();
-  {
-    const int ii = tid >> 2, q = tid & 3;  // output row i0 + ii, bytes [16q, 16q + 16) = columns j0 + 16q + ..
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const int idx = tid + 256 * r;
+    const int ii = idx >> 3, q = idx & 7;  // output row i0 + ii, bytes [16q, 16q + 16) = columns j0 + 16q + ..
     const int i = i0 + ii, j = j0 + 16 * q;
     if (i < rows && j < cols) {
-      const int w = ii >> 2, sh = 8 * (ii & 3);
+      const int w = (ii >> 2) ^ q;  // columns 16q .. 16q + 15 share the swizzle (jb >> 4 = q)
+      const uint32_t b = ii & 3;
+      const uint32_t s01 = b | ((4u + b) << 4);  // byte b of the first word, byte b of the second
       uint32_t o[4];
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         const int jb = 16 * q + 4 * k;
-        o[k] = ((t[jb][w] >> sh) & 0xFFu) | (((t[jb + 1][w] >> sh) & 0xFFu) << 8) |
-               (((t[jb + 2][w] >> sh) & 0xFFu) << 16) | (((t[jb + 3][w] >> sh) & 0xFFu) << 24);
+        const uint32_t lo = __byte_perm(t[jb][w], t[jb + 1][w], s01);
+        const uint32_t hi = __byte_perm(t[jb + 2][w], t[jb + 3][w], s01);
+        o[k] = __byte_perm(lo, hi, 0x5410);
       }
       *reinterpret_cast<uint4*>(dst + p * tps + static_cast<long long>(i) * ldt + j) = make_uint4(o[0], o[1], o[2], o[3]);
     }
@@ -1210,10 +1226,12 @@ void launch_transpose_i8(const int8_t* src, long long lds, long long sps, int8_t
   dim3 grid((rows + 63) / 64, (cols + 63) / 64, planes);
   const bool al = ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0 &&
                   (lds | sps | ldt | tps) % 16 == 0;
-  if (al)
-    k_transpose_i8_v<<<grid, 256, 0, s>>>(src, lds, sps, dst, ldt, tps, rows, cols);
-  else
+  if (al) {
+    dim3 gridv((rows + 127) / 128, (cols + 127) / 128, planes);
+    k_transpose_i8_v<<<gridv, 256, 0, s>>>(src, lds, sps, dst, ldt, tps, rows, cols);
+  } else {
     k_transpose_i8<<<grid, 256, 0, s>>>(src, lds, sps, dst, ldt, tps, rows, cols);
+  }
 }
 void launch_transpose_f64(const double* src, long long lds, double* dst, long long ldt, int rows, int cols,
                           cudaStream_t s) {

@@ -1529,7 +1529,8 @@ ozr_status certify(ozr_ctx ctx, Exchange* ex, int64_t n, double delta, ozr_step_
   int32_t* sE = ctx->ws<int32_t>(S_CSE, n);
   int32_t* sC = ctx->ws<int32_t>(S_CSC, nl);
   int32_t* rE = ctx->ws<int32_t>(S_CRE, n);
-  double* esq = ctx->ws<double>(S_CESQ, n);
+  double* esq = ctx->ws<double>(S_CESQ, 2 * n);  // Σ_i ẽ_ij² per column, then the eigenvalue-rounding sums
+  double* rsq = esq + n;
   double* dsq = ctx->ws<double>(S_CDSQ, n);
   int* flag = ctx->ws<int>(S_CFLG, 4);
   float* Q = reinterpret_cast<float*>(ctx->ws<int32_t>(S_PLANES, nnl));  // the slice planes are dead by now
@@ -1555,10 +1556,11 @@ ozr_status certify(ozr_ctx ctx, Exchange* ex, int64_t n, double delta, ozr_step_
   };
   ozr_status e;
   OZR_CK(cudaMemsetAsync(flag, 0, sizeof(int), s), "memset");
-  launch_cert_prep(Ep, n, N, NL, g, lam, static_cast<int>(col0), Eb, Cb, ldb, sE, sC, esq + col0, s);
+  launch_cert_prep(Ep, n, N, NL, g, lam, static_cast<int>(col0), Eb, Cb, ldb, sE, sC, esq + col0, rsq + col0, s);
   if ((e = gather(Eb, static_cast<size_t>(nl) * ldb * 2)) != OZR_OK) return e;  // all columns: the A operand
   if ((e = gather(sE, nl * sizeof(int32_t))) != OZR_OK) return e;
   if ((e = gather(esq, nl * sizeof(double))) != OZR_OK) return e;
+  if ((e = gather(rsq, nl * sizeof(double))) != OZR_OK) return e;
   launch_cert_rowT(Eb, ldb, N, N, sE, rE, EbT, s);
   PairTable pt;
   memset(&pt, 0, sizeof pt);
@@ -1576,11 +1578,11 @@ ozr_status certify(ozr_ctx ctx, Exchange* ex, int64_t n, double delta, ozr_step_
   launch_cert_delta(Q, Pm, n, N, NL, sE, sC, rE, esq, lam, static_cast<int>(col0), D, dsq + col0, flag, s);
   OZR_CK(cudaGetLastError(), "certificate");
   if ((e = gather(dsq, nl * sizeof(double))) != OZR_OK) return e;
-  std::vector<double> hesq(n), hdsq(n);
+  std::vector<double> hesq(2 * n), hdsq(n);
   int hflag = 0;
   ctx->pend.clear();
   ctx->hst_off = 0;
-  OZR_D2H(hesq.data(), esq, n * sizeof(double));
+  OZR_D2H(hesq.data(), esq, 2 * n * sizeof(double));
   OZR_D2H(hdsq.data(), dsq, n * sizeof(double));
   OZR_D2H(&hflag, flag, sizeof(int));
   OZR_CK(cudaStreamSynchronize(s), "sync");
@@ -1590,13 +1592,16 @@ ozr_status certify(ozr_ctx ctx, Exchange* ex, int64_t n, double delta, ozr_step_
     rep.cert = rep.cert_q = rep.cert_frob = INFINITY;
     return OZR_OK;
   }
-  double e2 = 0.0, d2 = 0.0, dmax = 0.0;
+  double e2 = 0.0, d2 = 0.0, dmax = 0.0, r2 = 0.0;
   for (int64_t j = 0; j < n; ++j) {
     e2 += hesq[j];
+    r2 += hesq[n + j];
     d2 += hdsq[j];
     dmax = std::max(dmax, hdsq[j]);
   }
-  const double frob = std::sqrt(d2), quad = std::sqrt(e2) * frob, rnd = 2.0 * kU;
+  // quad: the third-order allowance ‖Ẽ‖_F‖D‖_F plus the defect Ẽ carries from the fp64 rounding of the λ̂ it
+  // divided by, ≤ 2u·sqrt(Σ_{i≠j} (λ̂_i ẽ_ij/(λ̂_j − λ̂_i))²) (certify.cu header)
+  const double frob = std::sqrt(d2), quad = std::sqrt(e2) * frob + 2.0 * kU * std::sqrt(r2), rnd = 2.0 * kU;
   rep.cert_frob = frob;
   const double upper = std::sqrt(frob * frob + rnd * rnd) + quad;
   if (upper * kCertSafety <= delta || std::sqrt(dmax) + quad > 16.0 * delta) {

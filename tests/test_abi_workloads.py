@@ -142,15 +142,14 @@ def test_bench_reference_arm_cpu():
 
 @pytest.mark.parametrize("kind", ["geometric", "clustered"])
 def test_hadamard_exact_eigensystem_in_integers(kind):
-    """W.hadamard_exact: A Q = Q Λ and QᵀQ = I hold EXACTLY — checked in Python integers on the numerators
-    (n·Q, n²·2^b·A, 2^b·λ are integers), not in floating point."""
+    """W.hadamard_exact(pairs=False): A Q = Q Λ and QᵀQ = I hold EXACTLY — checked in Python integers on the
+    numerators (n·Q, n²·2^b·A, 2^b·λ are integers), not in floating point."""
     m = 6
-    n, b = 2 ** m, 53 - 2 * m - 1
-    A, lam, X = W.hadamard_exact(m, kind, seed=11)
-    NQ = (X * n).astype(object)
+    n, b = 2 ** m, 53 - 2 * m - 2
+    A, lam, X = W.hadamard_exact(m, kind, seed=11, pairs=False)
     NA = (A * float(n) ** 2 * 2.0 ** b)
     NL = lam * 2.0 ** b
-    assert np.all(NQ == np.rint(X * n)) and np.all(NA == np.rint(NA)) and np.all(NL == np.rint(NL))
+    assert np.all(X * n == np.rint(X * n)) and np.all(NA == np.rint(NA)) and np.all(NL == np.rint(NL))
     NA = np.vectorize(int, otypes=[object])(NA)
     NL = np.vectorize(int, otypes=[object])(NL)
     NQ = np.vectorize(int, otypes=[object])(X * n)
@@ -159,3 +158,27 @@ def test_hadamard_exact_eigensystem_in_integers(kind):
     assert np.all(np.diff(lam) > 0) and np.all(NA == NA.T)
     if kind == "clustered":
         assert np.sum(np.diff(NL) == 1) == 7 * max(n // 64, 1)    # the designed clusters: gaps of one unit
+
+
+@pytest.mark.parametrize("kind", ["geometric", "clustered"])
+def test_hadamard_exact_pairs_closed_form_in_rationals(kind):
+    """W.hadamard_exact (pairs: 2 x 2 integer blocks, irrational eigenvectors in closed form): A is the SAME kind of
+    exact integer matrix (n²·2^b·A integer), and the returned fp64 (λ, X) satisfy A x − λ x and XᵀX − I to a few u
+    when evaluated EXACTLY in rationals (so the bound is on the closed form's single rounding, not on the check's
+    arithmetic). A wrong sign or a swapped (cos φ, sin φ) leaves a residual of the size of the coupling b."""
+    from fractions import Fraction as Fr
+    m = 5
+    n, b = 2 ** m, 53 - 2 * m - 2
+    A, lam, X = W.hadamard_exact(m, kind, seed=12)
+    NA = A * float(n) ** 2 * 2.0 ** b
+    assert np.all(NA == np.rint(NA)) and np.array_equal(A, A.T) and np.all(np.diff(lam) > 0)
+    fr = np.vectorize(Fr, otypes=[object])
+    Af, Xf, lf = fr(A), fr(X), fr(lam)
+    R = Af.dot(Xf) - Xf * lf[None, :]
+    G = Xf.T.dot(Xf) - np.eye(n, dtype=object)
+    u = Fr(1, 2 ** 53)
+    nrmA = max(abs(v) for v in lf)
+    assert max(abs(v) for v in R.ravel()) <= 8 * u * nrmA
+    assert max(abs(v) for v in G.ravel()) <= 8 * u
+    # not the trivial family: the eigenvectors are not the dyadic columns of Q
+    assert np.any(X * n != np.rint(X * n))

@@ -371,11 +371,11 @@ def test_accmul_fixed_k_vs_rationals():
 @pytest.mark.parametrize("kind,start,delta", [("geometric", "fp64", 1e-13), ("clustered", "fp64", 1e-12),
                                               ("clustered", "fp32", 1e-12)])
 def test_driver_reaches_target_on_exactly_known_eigenvectors(kind, start, delta):
-    """W.hadamard_exact (A exactly representable, eigenvectors EXACTLY the columns of Q = H S H/n, integer-pinned in
-    tests/test_abi_workloads.py): the oracle driver from an LAPACK start returns "converged" with
-    ‖X − X̂‖₂ ≤ δ against the exact X (no computed reference involved), its certificate within a factor 2 of
-    that forward error + 2u, and λ̂ within 4u‖A‖ of the exact integers."""
-    A, lam, X = W.hadamard_exact(7, kind, seed=21)  # n = 128; "clustered": 2 clusters of 8, relative gap 2^-38
+    """W.hadamard_exact (A = Q B Q exactly representable, B integer 2 x 2 blocks: eigenpairs in closed form, pinned
+    in integers / rationals by tests/test_abi_workloads.py): the oracle driver from an LAPACK start returns
+    "converged" with ‖X − X̂‖₂ ≤ δ against the closed-form X (no computed reference involved; the closed form is
+    good to ≈ 2u), its certificate within a factor 2 of that forward error + 4u, and λ̂ within 4u‖A‖."""
+    A, lam, X = W.hadamard_exact(7, kind, seed=21)  # n = 128; "clustered": 2 clusters of 8, relative gaps ≥ 0.24·2^-37
     lam0, X0 = W.initial_eig(A, start)
     Xr, lr, hist = orf.refine_to_tol(A, X0, lam0, delta)
     assert hist[-1].get("stop") == "converged", hist
@@ -384,5 +384,6 @@ def test_driver_reaches_target_on_exactly_known_eigenvectors(kind, start, delta)
     sg = np.sign(np.sum(Xr * X, axis=0))
     fe = float(np.linalg.norm(Xr * sg[None, :] - X, 2))
     assert fe <= delta, (fe, hist)
-    assert hist[-1]["cert"] >= 0.5 * fe - 2.0 ** -52 and hist[-1]["cert"] <= 2 * fe + 2.0 ** -51, (fe, hist[-1])
+    # the certificate: not below the exact forward error (up to the closed form's own ≈ 2u), within 3x + 8u of it
+    assert hist[-1]["cert"] >= fe / 1.15 - 2.0 ** -51 and hist[-1]["cert"] <= 3 * fe + 2.0 ** -50, (fe, hist[-1])
     assert np.max(np.abs(lr - lam)) <= 4 * 2.0 ** -53 * np.max(np.abs(lam))

@@ -291,22 +291,29 @@ def _fwht_rows(M):
     return M
 
 
-def hadamard_exact(m, kind="geometric", cnd=1e4, seed=0, lam_bits=None):
-    """Full-size family with EXACTLY known eigenpairs (no reference computation needed): n = 2^m, H the Sylvester
-    Hadamard matrix, s ∈ {±1}^n seeded, Q = H diag(s) H / n (symmetric, exactly orthogonal: Q Qᵀ = H S (H H/n) S H/n
-    = I; its entries are integers / n, q_ij = ŝ(i ⊕ j)/n with ŝ the Walsh transform of s), λ distinct INTEGERS
-    below 2^lam_bits (default 53 − 2m − 1, so every numerator below stays under 2^53). Then
-    A = Q diag(λ) Q = (H S H Λ H S H) / n² has integer numerators |n² a_ij| ≤ n² max|λ| < 2^53: A is formed in
-    int64 (four Walsh transforms, no rounding anywhere) and is exactly representable in fp64, its eigenvalues are
-    exactly λ and its eigenvectors exactly the columns of Q. Column k of Q is reordered so that λ is ascending;
-    A and λ are returned scaled by 2^-lam_bits (exact), so ‖A‖₂ ≤ 1.
-    kind = "geometric": λ_i = round(2^lam_bits · cnd^{-(i-1)/(n-1)}) (cnd small enough that they stay distinct);
-    kind = "clustered": n/64 clusters of 8 integers separated by 1 (relative separation 2^-lam_bits of ‖A‖₂) among
-    otherwise 16-separated integers of both signs (the BASELINE c3 structure with the tightest separation that
-    keeps A exact). Returns (A, λ ascending, X exact (sign-fixed))."""
+def hadamard_exact(m, kind="geometric", cnd=1e4, seed=0, lam_bits=None, pairs=True):
+    """Full-size family with eigenpairs known in CLOSED FORM (no reference computation needed): n = 2^m, H the
+    Sylvester Hadamard matrix, s ∈ {±1}^n seeded, Q = H diag(s) H / n (symmetric, exactly orthogonal: Q Qᵀ =
+    H S (H H/n) S H/n = I; its entries are integers / n, q_ij = ŝ(i ⊕ j)/n with ŝ the Walsh transform of s), μ
+    distinct INTEGERS below 2^lam_bits (default 53 − 2m − 2, so every numerator below stays under 2^53).
+    pairs = False: A = Q diag(μ) Q — eigenvalues exactly μ, eigenvectors exactly the columns of Q (dyadic entries
+    of a few bits: a refinement in fp64 lands ON them, forward error exactly 0).
+    pairs = True (default): A = Q B Q with B the direct sum of n/2 integer blocks [[a, b], [b, c]] on seeded column
+    pairs of Q, (a, c) consecutive designed μ and b = ±max(1, (c − a)//2): eigenvalues (a + c)/2 ± h,
+    h = sqrt(((c − a)/2)² + b²), eigenvectors cos φ·q_1 + sin φ·q_2 and −sin φ·q_1 + cos φ·q_2 with
+    (cos φ, sin φ) ∝ (b, (c − a)/2 + h)·sign — irrational, evaluated in closed form in extended precision and
+    rounded once to fp64 (error ≤ u per entry and per eigenvalue: the reference is good to ≈ 2u in the 2-norm).
+    Either way n² A = N B Nᵀ (N = n Q) has integer entries below 2^53: A is formed in int64 (four Walsh transforms,
+    no rounding anywhere) and is exactly representable in fp64; A and λ are returned scaled by 2^-lam_bits (exact),
+    so ‖A‖₂ ≤ 1.
+    kind = "geometric": μ_i = round(2^lam_bits · cnd^{-(i-1)/(n-1)}) (cnd small enough that they stay distinct);
+    kind = "clustered": n/64 clusters of 8 integers separated by 1 (relative separation 2^-lam_bits of ‖A‖₂; with
+    pairs the cluster's eigenvalues are a + ½ ± √5/2: separations of 0.24 and 2 units) among otherwise
+    16-separated integers of both signs (the BASELINE c3 structure with the tightest separation that keeps A
+    exact). Returns (A, λ ascending, X (sign-fixed, columns in λ order))."""
     n = 2 ** m
     if lam_bits is None:
-        lam_bits = 53 - 2 * m - 1
+        lam_bits = 53 - 2 * m - 2
     rng = np.random.default_rng(seed)
     s = rng.choice(np.array([-1, 1], dtype=np.int64), size=n)
     if kind == "geometric":
@@ -320,20 +327,43 @@ def hadamard_exact(m, kind="geometric", cnd=1e4, seed=0, lam_bits=None):
     else:
         raise ValueError(kind)
     lam = np.sort(lam)
-    assert lam.shape == (n,) and np.all(np.diff(lam) > 0) and np.max(np.abs(lam)) <= 2 ** lam_bits, "λ not distinct"
-    # numerators of Q: N = H S H (|N_ij| ≤ n); column order of λ: column perm[k] of Q carries λ_k
+    assert lam.shape == (n,) and np.all(np.diff(lam) > 0) and np.max(np.abs(lam)) <= 2 ** lam_bits, "μ not distinct"
+    # numerators of Q: N = H S H (|N_ij| ≤ n); column perm[k] of Q carries the k-th designed value
     N = _fwht_rows(_fwht_rows(np.eye(n, dtype=np.int64)) * s[:, None])
     perm = rng.permutation(n)
-    lam_cols = np.empty(n, dtype=np.int64)
-    lam_cols[perm] = lam
-    # n² A = N Λ Nᵀ = H S (H Λ_cols H) S H, every intermediate an exact int64 (bounded by n^1.5 max|λ| in 2-norm)
-    T = _fwht_rows(np.diag(lam_cols))            # H Λ
-    T = _fwht_rows(np.ascontiguousarray(T.T))    # H Λ H (symmetric)
-    T = T * s[:, None] * s[None, :]              # S H Λ H S
+    B = np.zeros((n, n), dtype=np.int64)
+    B[perm, perm] = lam
+    if pairs:
+        a, c = lam[0::2], lam[1::2]
+        b = np.maximum(1, (c - a) // 2) * rng.choice(np.array([-1, 1], dtype=np.int64), size=n // 2)
+        B[perm[0::2], perm[1::2]] = b
+        B[perm[1::2], perm[0::2]] = b
+    # n² A = N B Nᵀ = H S (H B H) S H, every intermediate an exact int64 (bounded by n^1.5 ‖B‖₂ entrywise)
+    T = _fwht_rows(B)                            # H B
+    T = _fwht_rows(np.ascontiguousarray(T.T))    # H B H (symmetric)
+    T = T * s[:, None] * s[None, :]              # S H B H S
     T = _fwht_rows(T)
-    T = _fwht_rows(np.ascontiguousarray(T.T))    # H S H Λ H S H
+    T = _fwht_rows(np.ascontiguousarray(T.T))    # H S H B H S H
     assert np.max(np.abs(T)) < 2 ** 53
     sc = 2.0 ** -lam_bits                        # power-of-two scaling to ‖A‖₂ ≤ 1 (exact)
     A = T.astype(np.float64) / float(n) ** 2 * sc  # exact: |numerator| < 2^53, n² a power of two
-    X = N[:, perm].astype(np.float64) / float(n)
-    return A, lam.astype(np.float64) * sc, sign_fix(X)
+    Q = N[:, perm].astype(np.float64) / float(n)
+    if not pairs:
+        return A, lam.astype(np.float64) * sc, sign_fix(Q)
+    LD = np.longdouble
+    d = (c - a).astype(LD) / 2
+    bb = b.astype(LD)
+    h = np.sqrt(d * d + bb * bb)
+    mid = (a + c).astype(LD) / 2
+    nrm = np.sqrt(bb * bb + (d + h) * (d + h))
+    cphi, sphi = bb / nrm, (d + h) / nrm         # (cos φ, sin φ): eigenvector of the block for mid + h; d + h > 0
+    Q1, Q2 = Q[:, 0::2].astype(LD), Q[:, 1::2].astype(LD)
+    X = np.empty((n, n))
+    ev = np.empty(n, dtype=LD)
+    X[:, 1::2] = (Q1 * cphi[None, :] + Q2 * sphi[None, :]).astype(np.float64)   # mid + h
+    X[:, 0::2] = (Q1 * sphi[None, :] - Q2 * cphi[None, :]).astype(np.float64)   # mid − h
+    ev[1::2], ev[0::2] = mid + h, mid - h
+    o = np.argsort(ev, kind="stable")
+    ev = ev[o]
+    assert np.all(np.diff(ev) > LD(0.1)), "eigenvalues of the pair blocks not separated"
+    return A, (ev * LD(sc)).astype(np.float64), sign_fix(X[:, o])
