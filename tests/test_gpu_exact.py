@@ -75,3 +75,32 @@ def test_refine_to_tol_forward_error_against_exact_eigenvectors(ctx, m, kind, st
     assert float(torch.max(torch.abs(G - torch.eye(n, device=G.device, dtype=G.dtype)))) <= max(4 * delta, 1e-13)
     print(f"exact-eigenvector check n={n} {kind} {start}: start fe {fe0:.2e} -> {fe:.2e} (delta {delta:g}, "
           f"cert {hist[-1]['cert']:.2e}, {len(hist)} sweeps, max|dlam| {dl:.1e})")
+
+
+def test_refine_to_tol_soundness_scan_exact_family(ctx):
+    """OZR_OK ⇒ ‖X − X̂‖₂ ≤ δ (+ the closed form's own ≈ 4u) over a grid of the exactly-known family at n = 256
+    (geometric / clustered spectra, FP64 / FP32 starts, δ from 1e-8 to 1e-14, two seeds), every case converging; the
+    stopping certificate never below the exact forward error by more than its safety factor."""
+    import torch
+
+    import paper_2602_19090_b200 as ozr
+    import workloads as W
+    worst = 0.0
+    for kind in ("geometric", "clustered"):
+        for start in ("fp64", "fp32"):
+            for delta in (1e-8, 1e-12, 1e-14):
+                for seed in (41, 42):
+                    A, lam, X = W.hadamard_exact(8, kind, seed=seed)
+                    Ad, l0, X0 = _start(A, start)
+                    Xe = torch.from_numpy(X).cuda()
+                    Xd, ld = ozr.colmajor(X0.clone()), l0.clone()
+                    st, hist = ozr.ozr_refine_to_tol(ctx, ozr.colmajor(Ad), Xd, ld, ozr.default_params(delta=delta))
+                    assert st == 0, (kind, start, delta, seed, hist)
+                    p = torch.argsort(ld, stable=True)
+                    Xr = Xd[:, p]
+                    sg = torch.sign(torch.sum(Xr * Xe, dim=0))
+                    fe = float(torch.linalg.matrix_norm(Xr * sg[None, :] - Xe, ord=2))
+                    assert fe <= delta + 4 * U, (kind, start, delta, seed, fe, hist[-1])
+                    assert hist[-1]["cert"] * 1.15 >= fe - 4 * U, (kind, start, delta, seed, fe, hist[-1])
+                    worst = max(worst, fe / delta)
+    print(f"exact-family scan: worst forward error / delta = {worst:.3f}")

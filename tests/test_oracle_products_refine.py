@@ -387,3 +387,21 @@ def test_driver_reaches_target_on_exactly_known_eigenvectors(kind, start, delta)
     # the certificate: not below the exact forward error (up to the closed form's own ≈ 2u), within 3x + 8u of it
     assert hist[-1]["cert"] >= fe / 1.15 - 2.0 ** -51 and hist[-1]["cert"] <= 3 * fe + 2.0 ** -50, (fe, hist[-1])
     assert np.max(np.abs(lr - lam)) <= 4 * 2.0 ** -53 * np.max(np.abs(lam))
+
+
+def test_driver_soundness_scan_exact_family():
+    """"converged" ⇒ ‖X − X̂‖₂ ≤ δ (+ the closed form's own ≈ 4u) over a grid of the exactly-known family (n = 64:
+    geometric / clustered spectra, FP64 / FP32 starts, δ from 1e-8 to 1e-15, several seeds); every case must also
+    converge within the driver's sweep limit."""
+    for kind in ("geometric", "clustered"):
+        for start in ("fp64", "fp32"):
+            for delta in (1e-8, 1e-12, 1e-15):
+                for seed in (31, 32):
+                    A, lam, X = W.hadamard_exact(6, kind, seed=seed)
+                    lam0, X0 = W.initial_eig(A, start)
+                    Xr, lr, hist = orf.refine_to_tol(A, X0, lam0, delta)
+                    assert hist[-1].get("stop") == "converged", (kind, start, delta, seed, hist)
+                    p = np.argsort(lr, kind="stable")
+                    sg = np.sign(np.sum(Xr[:, p] * X, axis=0))
+                    fe = float(np.linalg.norm(Xr[:, p] * sg[None, :] - X, 2))
+                    assert fe <= delta + 4 * 2.0 ** -53, (kind, start, delta, seed, fe, hist[-1])
