@@ -304,8 +304,8 @@ def refine_to_tol(A, X0, lam0, delta, theta=THETA_DEFAULT, max_sweeps=6, beta_mo
     without unresolved groups the sweep's own Ẽ certifies the returned X̂ (certificate(): the second-order
     defect of Ẽ, in the 2-norm of PAPER.md:121): stop with "converged" when est·CERT_SAFETY ≤ δ. An uncertified
     sweep whose estimate did not fall below CONTRACT × the previous one — or fell so fast that the next sweep's
-    quadratic part, est³/est_prev² at the observed rate, is below δ/8 while est ≤ 16δ — sits at the truncation
-    floor (the
+    quadratic part, est³/est_prev² at the observed rate, is below δ/8 while est ≤ 16δ (est_prev: the previous
+    estimate, or ν = ‖X_k − X_{k−1}‖_F when the previous sweep had none) — sits at the truncation floor (the
     quadratic error of the deliberately truncated X̂^(1)): θ grows by the power of 4 that
     brings the floor (∝ 1/θ: β falls by ½ log2 θ, the error is quadratic in 2^-β) below δ/2 — at most
     `max_escalations` times, then "stagnation". Sweeps with unresolved groups (a Rayleigh–Ritz rotation, R13) are never certified or
@@ -342,8 +342,13 @@ def refine_to_tol(A, X0, lam0, delta, theta=THETA_DEFAULT, max_sweeps=6, beta_mo
         # at the floor: not contracting, or contracting so fast that the next sweep's quadratic part
         # (est³/est_prev² from the observed rate) is below δ/8, i.e. what remains is the truncation floor
         # (floors are O(δ) by the choice of β, so only an estimate within 16δ is read that way)
-        floor = est_prev is not None and (cert["est"] > CONTRACT * est_prev or
-                                          (cert["est"] <= 16 * delta and cert["est"] ** 3 / est_prev ** 2 <= delta / 8))
+        # the first certified sweep after a start, a cluster sweep or an escalation has no previous estimate: there
+        # ν = ‖X_k − X_{k−1}‖_F, the size of the error this sweep removed, stands in for it in the second test
+        # (only while θ can still grow: without an escalation to spend, a floor read off ν would stop a run that
+        # the next sweep may well finish)
+        prev = est_prev if est_prev is not None else (nu if nu > 0 and truncate and max_escalations > 0 else None)
+        floor = (est_prev is not None and cert["est"] > CONTRACT * est_prev) or \
+                (prev is not None and cert["est"] <= 16 * delta and cert["est"] ** 3 / prev ** 2 <= delta / 8)
         if floor:
             if truncate and max_escalations > 0:
                 max_escalations -= 1

@@ -2276,7 +2276,8 @@ ozr_status ozr_refine_step_dist(ozr_ctx ctx, ozr_comm comm, const double* A, int
 // The driver (R12; the paper iterates a fixed number of times): after every sweep without
 // unresolved groups its own Ẽ certifies the returned X̂ (certify()); OK when est·kCertSafety ≤ δ. An uncertified
 // estimate that did not fall below kContract × the previous one — or fell so fast that the next sweep's quadratic
-// part est³/est_prev² is below δ/8 while est ≤ 16δ — sits at the truncation floor (quadratic in 2^-β,
+// part est³/est_prev² is below δ/8 while est ≤ 16δ (est_prev: the previous estimate, or ν = ‖X_k − X_{k−1}‖_F when
+// the previous sweep had none) — sits at the truncation floor (quadratic in 2^-β,
 // PAPER.md:341-373): θ grows by the power of 4 that brings it below δ/2, at most max_escalations times, then
 // OZR_ERR_NOT_CONVERGED. Sweeps with unresolved groups (a Rayleigh–Ritz rotation, R13) are neither certified nor
 // compared. Mirrors oracle/refine.refine_to_tol.
@@ -2317,8 +2318,14 @@ ozr_status ozr_refine_to_tol_dist(ozr_ctx ctx, ozr_comm comm, const double* A, i
       result = OZR_OK;
       break;
     }
-    const bool floor = est_prev > 0.0 && (est > kContract * est_prev ||
-                                          (est <= 16.0 * delta && est * est * est / (est_prev * est_prev) <= delta / 8));
+    // the first certified sweep after a start, a cluster sweep or an escalation has no previous estimate: there
+    // ν = ‖X_k − X_{k−1}‖_F, the size of the error this sweep removed, stands in for it in the second test
+    // (only while θ can still grow: without an escalation to spend, a floor read off ν would stop a run that the
+    // next sweep may well finish — the untruncated and fixed-slice modes, or the escalations used up)
+    const bool can_escalate = P.truncate && escalations < params->max_escalations;
+    const double prev = est_prev > 0.0 ? est_prev : (can_escalate ? rep.net_update : -1.0);
+    const bool floor = (est_prev > 0.0 && est > kContract * est_prev) ||
+                       (prev > 0.0 && est <= 16.0 * delta && est * est * est / (prev * prev) <= delta / 8);
     if (floor) {
       if (P.truncate && escalations < params->max_escalations) {
         ++escalations;

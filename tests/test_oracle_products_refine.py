@@ -235,9 +235,13 @@ def test_driver_stop_rules(monkeypatch):
     n = 8
     script = []
 
+    last = [1.0]
+
     def fake_sweep(A, X, lam, delta, theta, **kw):
         clusters, est = script.pop(0)
-        info = dict(beta=20, alpha=40, normE_fro=0.0, clusters=clusters, net_update=1.0, E=est)
+        # ν = ‖X_k − X_{k−1}‖_F is the size of the error the sweep removed: the previous sweep's error
+        info = dict(beta=20, alpha=40, normE_fro=0.0, clusters=clusters, net_update=last[0], E=est)
+        last[0] = est if est > 0 else 1.0
         return X, lam, info
 
     monkeypatch.setattr(orf, "sweep", fake_sweep)
@@ -263,6 +267,26 @@ def test_driver_stop_rules(monkeypatch):
     script[:] = [([], 1e-3), ([], 1e-6), ([], 2.9 * d), ([], 2.8 * d), ([], 2.7 * d)]
     _, _, h = orf.refine_to_tol(A, X0, lam0, d, max_escalations=1)
     assert [r["theta"] for r in h] == [4.0, 4.0, 4.0, 64.0, 64.0] and h[-1]["stop"] == "stagnation"
+    # the first certified sweep has no previous estimate: ν (the error it removed, here 1e-6) stands in — 5δ with a
+    # quadratic part (5δ)³/1e-6² ≪ δ/8 is the floor, θ × 4^⌈log4(2·5·1.15)⌉ = ×16 at once, no sweep wasted on it
+    last[0] = 1e-6
+    script[:] = [([], 5 * d), ([], 0.3 * d)]
+    _, _, h = orf.refine_to_tol(A, X0, lam0, d)
+    assert [r["theta"] for r in h] == [4.0, 64.0] and h[-1]["stop"] == "converged"
+    # ... but not when the sweep removed so little that its own quadratic part may still matter: (5δ)³/(20δ)² > δ/8
+    last[0] = 20 * d
+    script[:] = [([], 5 * d), ([], 0.3 * d)]
+    _, _, h = orf.refine_to_tol(A, X0, lam0, d)
+    assert [r["theta"] for r in h] == [4.0, 4.0] and h[-1]["stop"] == "converged"
+    # ... nor when θ cannot grow (untruncated mode, or no escalation left): the next sweep decides
+    last[0] = 1e-6
+    script[:] = [([], 5 * d), ([], 0.3 * d)]
+    _, _, h = orf.refine_to_tol(A, X0, lam0, d, truncate=False)
+    assert [r["theta"] for r in h] == [4.0, 4.0] and h[-1]["stop"] == "converged"
+    last[0] = 1e-6
+    script[:] = [([], 5 * d), ([], 0.3 * d)]
+    _, _, h = orf.refine_to_tol(A, X0, lam0, d, max_escalations=0)
+    assert [r["theta"] for r in h] == [4.0, 4.0] and h[-1]["stop"] == "converged"
     # cluster sweeps are neither certified nor compared: a tiny estimate during them does not stop
     script[:] = [([[0, 1]], 0.0), ([[0, 1]], 0.0), ([], 1e-3), ([], 1e-7), ([], 0.1 * d)]
     _, _, h = orf.refine_to_tol(A, X0, lam0, d)
