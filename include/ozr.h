@@ -175,7 +175,9 @@ typedef struct {
                                        OA-2018 cluster threshold 2(‖S − D̃‖ + ‖A‖‖R‖) (diagnostic, R13) */
   double theta;                     /* the θ this sweep used (params.theta, × 16 per escalation)       */
   double cert;                      /* a-posteriori estimate of ‖X − X̂_new‖₂ (R12): sqrt(‖D‖₂² + (2u)²)
-                                       + ‖Ẽ‖_F‖D‖_F with Ẽ's second-order defect D = −(E − Ẽ):
+                                       + ‖Ẽ‖_F‖D‖_F + 2u‖(λ̂_i ẽ_ij/(λ̂_j − λ̂_i))_{i≠j}‖_F (the last term: the
+                                       fp64 rounding of the λ̂ in Ẽ's denominators) with Ẽ's second-order
+                                       defect D = −(E − Ẽ):
                                        D_ij = q_ij/(λ̂_j − λ̂_i) − (Ẽ²)_ij (i ≠ j), D_jj = −(Ẽ²)_jj − ½‖ẽ_j‖²,
                                        Q = ẼᵀC, c_kj = (λ̂_k − λ̂_j)ẽ_kj; −1 when not evaluated
                                        (params.certify, or unresolved groups)                           */
@@ -225,7 +227,9 @@ ozr_status ozr_last_clusters(ozr_ctx ctx, int* members, int max_members, int* of
  * ‖X − X̂‖₂ (the 2-norm of PAPER.md:121) is formed from the sweep's own Ẽ — the second-order defect of Alg. 1's
  * correction, two bf16 tensor-core products (Q = ẼᵀC, Ẽ²) and Golub–Kahan–Lanczos — and the call returns OZR_OK with
  * that X̂ once cert·1.15 ≤ δ. An estimate that stalls above δ (the truncated iteration's floor, quadratic in
- * 2^-β) escalates θ ← θ·4^m up to max_escalations times, then OZR_ERR_NOT_CONVERGED, as does
+ * 2^-β: it fell by less than 8x, or the next sweep's quadratic part cert³/prev² is below δ/8 while
+ * cert ≤ 16δ — prev the previous estimate, or net_update when the previous sweep had none and an escalation is
+ * left) escalates θ ← θ·4^m up to max_escalations times, then OZR_ERR_NOT_CONVERGED, as does
  * reaching max_sweeps — X / lambda then hold the last completed sweep. Sweeps with unresolved groups (cluster
  * sub-solves rotate columns) are neither certified nor compared. history (host, nullable) receives up to
  * max_hist reports; sweeps_done (host, nullable). */

@@ -1507,10 +1507,10 @@ constexpr double kCertSafety = 1.15;  // power-iteration / bf16-GEMM slack of th
 constexpr double kContract = 1.0 / 8;  // an estimate that fell by less than this sits at the truncation floor
 
 // a10 (R12): the a-posteriori forward-error estimate of the sweep just completed, from its own Ẽ (certify.cu):
-//   est = sqrt(‖D‖₂² + (2u)²) + ‖Ẽ‖_F‖D‖_F,   D = −(E − Ẽ) to second order:
+//   est = sqrt(‖D‖₂² + (2u)²) + ‖Ẽ‖_F‖D‖_F + 2u‖(λ̂_i ẽ_ij/(λ̂_j − λ̂_i))_{i≠j}‖_F,   D = −(E − Ẽ) to second order:
 //   D_ij = q_ij/(λ̂_j − λ̂_i) − (Ẽ²)_ij (i ≠ j), D_jj = −(Ẽ²)_jj − ½‖ẽ_j‖², Q = ẼᵀC, c_kj = (λ̂_k − λ̂_j)ẽ_kj
-// (oracle/refine.second_order_defect), plus the fp64 rounding of X̂_new and an allowance for the third-order
-// terms. ‖D‖₂ comes from its Frobenius norm when that already certifies, from the power iteration otherwise —
+// (oracle/refine.second_order_defect), plus the fp64 rounding of X̂_new, an allowance for the third-order
+// terms and the defect from the fp64 rounding of the λ̂ in Ẽ's denominators (certify.cu header). ‖D‖₂ comes from its Frobenius norm when that already certifies, from the power iteration otherwise —
 // except when even the lower bound max_j ‖D_{:,j}‖ exceeds 16δ: then the upper bound (Frobenius) is reported,
 // which no decision of the driver can tell from the exact value.
 // Reads the sweep's Ẽ' (S_EP), g (S_G) and λ̂ (S_LAM); writes rep.cert, cert_q, cert_frob, cert_iters.
