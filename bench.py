@@ -547,7 +547,10 @@ def main():
     if name == "c4p" and not args.n:
         ttt["oracle_check"] = ("profiles/r01_ttt_verified_n8192.json: on this c4p n = 8192 problem the forward error "
                                "against the oracle's dd reference is 6.5e-13 = 0.65 delta after 2 sweeps (the "
-                               "certificate: 6.49e-13); other BASELINE recipes: profiles/r02/verify_*.json")
+                               "certificate: 6.49e-13); other BASELINE recipes: profiles/r02/verify_*.json; "
+                               "against EXACTLY known eigenvectors (workloads.hadamard_exact, tests/test_gpu_exact.py, "
+                               "profiles/r02c/SUMMARY.md): n = 8192 FP64 start 0.28 delta, FP32 start 0.69 delta, "
+                               "n = 16384 at delta = 1e-15 0.12 delta")
     # §8(f) rank 1: the prior work's two-sided fixed-slice plan (ozr_params.fixed_k)
     # against the proposed method on the same problem: device time to the stop rule, sweeps, pair-GEMMs
     fixed_k_cmp = None
