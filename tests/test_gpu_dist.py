@@ -145,3 +145,29 @@ def test_partitioned_certificate(ctx):
             if h1["cert"] > 0:
                 assert abs(hp["cert"] / h1["cert"] - 1) < 1e-6
     assert np.array_equal(_assemble(out, 2048, 2), to_np(Xd))
+
+
+@pytest.mark.parametrize("kind,start,P", [("clustered", "fp64", 4), ("geometric", "fp32", 2), ("clustered", "fp32", 8)])
+def test_partitioned_refine_to_tol_against_exact_eigenvectors(ctx, kind, start, P):
+    """The column-partitioned driver against an INDEPENDENT truth (not the one-GPU library): on the exactly-known
+    family (workloads.hadamard_exact, n = 1024; the clustered FP32 start goes through the cluster branch) P ranks
+    return OZR_OK with ‖X − X̂‖₂ ≤ δ against the closed-form eigenvectors, every rank holds the same
+    λ̂, and the stopping certificate is not below the exact error."""
+    import paper_2602_19090_b200 as ozr
+    n, delta = 1024, 1e-12
+    A, lam, X = W.hadamard_exact(10, kind, seed=77)
+    lam0, X0 = W.initial_eig(A, start)
+    out = _run_ranks(P, A, X0, lam0, ozr.default_params(delta=delta, max_sweeps=10), to_tol=True)
+    assert all(o[0] == 0 for o in out), [o[3][-1] for o in out]
+    Xr, lr = _assemble(out, n, P), out[0][2]
+    for o in out:
+        assert np.array_equal(o[2], lr)
+    p = np.argsort(lr, kind="stable")
+    Xr, lr = Xr[:, p], lr[p]
+    sg = np.sign(np.sum(Xr * X, axis=0))
+    fe = float(np.linalg.norm(Xr * sg[None, :] - X, 2))
+    assert fe <= delta, (fe, out[0][3][-1])
+    assert out[0][3][-1]["cert"] * 1.15 >= fe - 4 * 2.0 ** -53
+    assert np.max(np.abs(lr - lam)) <= 1e-13 * np.max(np.abs(lam))
+    if start == "fp32" and kind == "clustered":
+        assert max(h["max_cluster"] for h in out[0][3]) >= 2
